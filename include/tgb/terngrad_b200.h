@@ -1,0 +1,189 @@
+/*
+ * terngrad_b200 — C-ABI of the B200-native TernGrad gradient-synchronisation path.
+ *
+ * This is the drop-in boundary. The reference (arxiv 1705.07878 CPU library,
+ * /root/reference/proj/include/terngrad/) exposes the path as header-only C++
+ * free functions in namespace `terngrad` with value semantics and exceptions;
+ * it has no FFI of its own. Each entry point below names the reference
+ * function it replaces (file:line, relative to proj/include/terngrad/).
+ * The C++ value-semantics mirror lives in include/tgb/terngrad.hpp, the Python
+ * mirror in paper_1705_07878_b200/ (ctypes); both sit on this header only.
+ *
+ * Conventions
+ *  - All data pointers named d_* are DEVICE pointers (CUDA global memory).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is stream-ordered and asynchronous unless stated otherwise;
+ *    nothing allocates on the per-step path.
+ *  - Errors that the reference raises as exceptions are reported through a
+ *    device error word (tgb_error), read with tgb_check()/tgb_layer_check()
+ *    which synchronise. The flags map 1:1 to the reference's CodecError
+ *    sites; the C++/Python wrappers rethrow with the reference's messages.
+ *  - No CPU fallback: if no sm_100 device is present every compute entry
+ *    point returns TGB_ERR_CUDA.
+ */
+#ifndef TGB_TERNGRAD_B200_H
+#define TGB_TERNGRAD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGB_ABI_VERSION 1
+
+typedef enum tgb_status {
+    TGB_OK = 0,
+    TGB_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument, codec.hpp:90-95 */
+    TGB_ERR_CODEC = 2,            /* CodecError, codec.hpp:25-27 (detail: tgb_error) */
+    TGB_ERR_CUDA = 3,
+    TGB_ERR_NCCL = 4,
+    TGB_ERR_UNSUPPORTED = 5
+} tgb_status;
+
+/* device error word: flags are sticky until read by tgb_check */
+#define TGB_E_NONFINITE 0x1u        /* "encode_step: non-finite gradient <name>" codec.hpp:205 */
+#define TGB_E_SCALER_BELOW_MAX 0x2u /* "ternarize: scaler <s> below max |g| in <name>" :163-165 */
+#define TGB_E_S0_NONZERO 0x4u       /* "ternarize: s=0 but gradient has nonzero element" :155-158 */
+#define TGB_E_CORRUPT_CODE 0x8u     /* "corrupt ternary code 11 in block <name> at element <k>" :42-44 */
+
+typedef struct tgb_error {
+    uint32_t flags;
+    int32_t layer;  /* first offending layer (plan) or -1 */
+    uint64_t index; /* first offending element within that layer (when known) */
+} tgb_error;
+
+/* one gradient tensor of the canonical parameter order (tensor.hpp:14-43) */
+#define TGB_LAYER_PASSTHROUGH 0x1u /* name in CodecConfig::passthrough (codec.hpp:87) */
+typedef struct tgb_layer_desc {
+    uint64_t n;         /* element count (GradTensor::element_count) */
+    uint64_t name_hash; /* fnv1a64(name) (rng.hpp:37-44); see tgb_fnv1a64 */
+    uint32_t flags;
+    uint32_t reserved;
+} tgb_layer_desc;
+
+/* CodecConfig (codec.hpp:78-96) + the sharing mode of this build */
+#define TGB_BUCKET_PER_TENSOR 0 /* Bucketing::PerTensor */
+#define TGB_BUCKET_GLOBAL 1     /* Bucketing::Global */
+#define TGB_BUCKET_FIXED 2      /* Bucketing::FixedSize (not yet supported by plans) */
+#define TGB_SHARE_REF 0         /* reference semantics: ternarize with the LOCAL scaler,
+                                   decode with max over workers (cluster.hpp:195-196) */
+#define TGB_SHARE_PRESHARED 1   /* paper Eq.4: max-allreduce BEFORE ternarize */
+typedef struct tgb_codec_params {
+    float clip_factor;        /* c = 2.5 */
+    int32_t clipping_enabled; /* 1 */
+    int32_t bucketing;        /* TGB_BUCKET_* */
+    int32_t scaler_sharing;   /* 1: shared-max integer-sum decode; 0: fp64 per-worker scalers */
+    uint64_t bucket_size;     /* FixedSize only */
+    uint64_t seed;            /* Worker sets codec.seed = cluster seed (cluster.hpp:272-273) */
+    int32_t share_mode;       /* TGB_SHARE_REF | TGB_SHARE_PRESHARED */
+    int32_t reserved;
+} tgb_codec_params;
+
+typedef struct tgb_plan_info {
+    uint64_t total_elements; /* sum of n over layers */
+    uint64_t push_bytes;     /* one rank's push buffer: scaler slots + packed codes (+pad) */
+    uint64_t code_bytes;     /* sum of ceil(n/4) over ternary layers (algorithmic) */
+    uint64_t scaler_offset;  /* byte offset of the scaler slots in the push buffer (0) */
+    uint64_t codes_offset;   /* byte offset of the code region in the push buffer */
+    int32_t n_layers;
+    int32_t n_slots;      /* scaler slots (one per block) */
+    int32_t n_chunks;     /* work items per streaming kernel */
+    int32_t n_workers;
+    uint32_t chunk_elems; /* elements per chunk */
+    uint32_t reserved;
+} tgb_plan_info;
+
+typedef struct tgb_plan tgb_plan;
+typedef struct tgb_comm tgb_comm;
+
+const char* tgb_version(void);
+const char* tgb_status_string(tgb_status s);
+/* rng.hpp:37-44 (host-side; the device never hashes strings) */
+uint64_t tgb_fnv1a64(const char* s, size_t len);
+/* number of CUDA devices visible (0 on a CPU-only host) */
+int32_t tgb_device_count(void);
+
+/* ---- plan: the per-worker encode_step / sync / decode_pull pipeline ----
+ * Replaces: encode_step (codec.hpp:194-239), average (:245-311),
+ * ParameterServer::aggregate (cluster.hpp:167-221), decode_pull (wire.hpp:206-228)
+ * and the Worker::run sync segment (cluster.hpp:283-297).
+ * The plan owns its device workspace (push buffer, gather buffer, partials). */
+tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
+                           const tgb_codec_params* params, uint16_t worker, int32_t n_workers,
+                           tgb_plan** out);
+void tgb_plan_destroy(tgb_plan* plan);
+tgb_status tgb_plan_get_info(const tgb_plan* plan, tgb_plan_info* out);
+/* byte offset of layer l's packed codes inside one push buffer; its scaler slot */
+tgb_status tgb_plan_layer_layout(const tgb_plan* plan, int32_t layer, uint64_t* code_offset,
+                                 int32_t* slot);
+/* host arrays of device pointers, n_layers each: the worker's gradients (read)
+ * and the averaged-gradient outputs (written by decode). Pointers must stay
+ * valid until the next bind. 16-byte aligned pointers take the vector path. */
+tgb_status tgb_plan_bind(tgb_plan* plan, const float* const* d_grads, float* const* d_out);
+/* device buffers owned by the plan */
+tgb_status tgb_plan_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_gathered,
+                            float** d_bounds);
+
+/* K1: per-layer clip bound + local scaler -> push scaler slots, d_bounds.
+ * clip (codec.hpp:117-124) + scaler (:128-134) + Global max (:212-216). */
+tgb_status tgb_stats(tgb_plan* plan, void* stream);
+/* K2: stochastic ternarize + 2-bit pack of every layer into the push code
+ * region, using the scalers currently in the push slots (codec.hpp:148-175). */
+tgb_status tgb_ternarize_pack(tgb_plan* plan, uint64_t t, void* stream);
+/* K1 + K2 (REF mode; PRESHARED needs tgb_step or an explicit
+ * tgb_share_scalers between the two) */
+tgb_status tgb_encode(tgb_plan* plan, uint64_t t, void* stream);
+/* PRESHARED: NCCL max-allreduce of the push scaler slots (share_scalers, codec.hpp:136-141) */
+tgb_status tgb_share_scalers(tgb_plan* plan, tgb_comm* comm, void* stream);
+/* exchange: NCCL allgather of every rank's push buffer into the gather buffer
+ * (replaces push -> ParameterServer::step recv loop, cluster.hpp:137-151) */
+tgb_status tgb_sync(tgb_plan* plan, tgb_comm* comm, void* stream);
+/* K3: unpack-sum-average of N push buffers laid out back to back at
+ * d_src (stride = push_bytes) into the bound outputs. Shared: s = max_w s_w,
+ * out = (s*float(sum))*(1.0f/N); unshared: float(sum_w double(s_w)*code / N).
+ * average (codec.hpp:281-307) == decode_pull(aggregate) (wire.hpp:206-228). */
+tgb_status tgb_decode_average(tgb_plan* plan, const uint8_t* d_src, int32_t n_workers,
+                              void* stream);
+/* the whole worker step: K1 -> [allreduce] -> K2 -> allgather -> K3.
+ * comm may be NULL when n_workers == 1. */
+tgb_status tgb_step(tgb_plan* plan, tgb_comm* comm, uint64_t t, void* stream);
+/* synchronises the plan's last stream, reads and clears the error word */
+tgb_status tgb_check(tgb_plan* plan, tgb_error* out);
+
+/* ---- communicator (NCCL over NVLink/NVSwitch) ---- */
+#define TGB_UNIQUE_ID_BYTES 128
+tgb_status tgb_comm_unique_id(uint8_t out[TGB_UNIQUE_ID_BYTES]);
+tgb_status tgb_comm_init(const uint8_t id[TGB_UNIQUE_ID_BYTES], int32_t nranks, int32_t rank,
+                         tgb_comm** out);
+void tgb_comm_destroy(tgb_comm* comm);
+
+/* ---- per-layer entry points (the reference's per-layer functions) ---- */
+/* scaler (codec.hpp:128-134): *d_s = max |g| */
+tgb_status tgb_layer_scaler(const float* d_g, uint64_t n, float* d_s, void* stream);
+/* clip (codec.hpp:117-124): d_out = clipped copy; *d_bound = float(c*sigma) (inf if n<2) */
+tgb_status tgb_layer_clip(const float* d_g, uint64_t n, float c, float* d_out, float* d_bound,
+                          void* stream);
+/* ternarize (codec.hpp:148-175) with RngStream(seed, t, name, worker) (rng.hpp:50-57);
+ * d_codes receives ceil(n/4) bytes */
+tgb_status tgb_layer_ternarize(const float* d_g, uint64_t n, float s, uint64_t seed, uint64_t t,
+                               uint64_t name_hash, uint64_t worker, uint64_t rng_base,
+                               uint8_t* d_codes, void* stream);
+/* decode (codec.hpp:177-182) */
+tgb_status tgb_layer_decode(const uint8_t* d_codes, uint64_t n, float s, float* d_out,
+                            void* stream);
+/* one block of average (codec.hpp:281-307); d_codes is a HOST array of N device
+ * pointers, d_s a device array of N scalers */
+tgb_status tgb_layer_average(int32_t n_workers, const uint8_t* const* d_codes, const float* d_s,
+                             uint64_t n, int32_t sharing, float* d_out, void* stream);
+/* RngStream::bits (rng.hpp:59-66) for indices k0..k0+n-1 (KAT helper) */
+tgb_status tgb_rng_bits(uint64_t seed, uint64_t t, uint64_t name_hash, uint64_t worker,
+                        uint64_t k0, uint64_t n, uint32_t* d_out, void* stream);
+/* synchronises `stream`, reads and clears the per-layer error word of the current device */
+tgb_status tgb_layer_check(void* stream, tgb_error* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGB_TERNGRAD_B200_H */

@@ -1,0 +1,150 @@
+"""ctypes binding of libtgb.so (the C-ABI in include/tgb/terngrad_b200.h).
+
+There is deliberately no fallback: if the shared library is missing or no
+CUDA device is visible, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import build as _build
+
+_lock = threading.Lock()
+_lib = None
+
+TGB_OK = 0
+TGB_ERR_INVALID_ARGUMENT = 1
+TGB_ERR_CODEC = 2
+TGB_ERR_CUDA = 3
+TGB_ERR_NCCL = 4
+TGB_ERR_UNSUPPORTED = 5
+
+TGB_E_NONFINITE = 0x1
+TGB_E_SCALER_BELOW_MAX = 0x2
+TGB_E_S0_NONZERO = 0x4
+TGB_E_CORRUPT_CODE = 0x8
+
+TGB_LAYER_PASSTHROUGH = 0x1
+TGB_BUCKET_PER_TENSOR, TGB_BUCKET_GLOBAL, TGB_BUCKET_FIXED = 0, 1, 2
+TGB_SHARE_REF, TGB_SHARE_PRESHARED = 0, 1
+UNIQUE_ID_BYTES = 128
+
+# every symbol the header declares (checked by tests/test_capi.py)
+EXPORTS = [
+    "tgb_version", "tgb_status_string", "tgb_fnv1a64", "tgb_device_count",
+    "tgb_plan_create", "tgb_plan_destroy", "tgb_plan_get_info", "tgb_plan_layer_layout",
+    "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
+    "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_check",
+    "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
+    "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
+    "tgb_layer_average", "tgb_rng_bits", "tgb_layer_check",
+]
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("name_hash", C.c_uint64), ("flags", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class CodecParams(C.Structure):
+    _fields_ = [("clip_factor", C.c_float), ("clipping_enabled", C.c_int32),
+                ("bucketing", C.c_int32), ("scaler_sharing", C.c_int32),
+                ("bucket_size", C.c_uint64), ("seed", C.c_uint64),
+                ("share_mode", C.c_int32), ("reserved", C.c_int32)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("total_elements", C.c_uint64), ("push_bytes", C.c_uint64),
+                ("code_bytes", C.c_uint64), ("scaler_offset", C.c_uint64),
+                ("codes_offset", C.c_uint64), ("n_layers", C.c_int32), ("n_slots", C.c_int32),
+                ("n_chunks", C.c_int32), ("n_workers", C.c_int32), ("chunk_elems", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class Error(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("layer", C.c_int32), ("index", C.c_uint64)]
+
+
+_vp = C.c_void_p
+_u64 = C.c_uint64
+_i32 = C.c_int32
+
+
+def _declare(L):
+    S = C.c_int  # tgb_status
+    sig = {
+        "tgb_version": (C.c_char_p, []),
+        "tgb_status_string": (C.c_char_p, [S]),
+        "tgb_fnv1a64": (_u64, [C.c_char_p, C.c_size_t]),
+        "tgb_device_count": (_i32, []),
+        "tgb_plan_create": (S, [C.POINTER(LayerDesc), _i32, C.POINTER(CodecParams), C.c_uint16,
+                                _i32, C.POINTER(_vp)]),
+        "tgb_plan_destroy": (None, [_vp]),
+        "tgb_plan_get_info": (S, [_vp, C.POINTER(PlanInfo)]),
+        "tgb_plan_layer_layout": (S, [_vp, _i32, C.POINTER(_u64), C.POINTER(_i32)]),
+        "tgb_plan_bind": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
+        "tgb_plan_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+        "tgb_stats": (S, [_vp, _vp]),
+        "tgb_ternarize_pack": (S, [_vp, _u64, _vp]),
+        "tgb_encode": (S, [_vp, _u64, _vp]),
+        "tgb_share_scalers": (S, [_vp, _vp, _vp]),
+        "tgb_sync": (S, [_vp, _vp, _vp]),
+        "tgb_decode_average": (S, [_vp, _vp, _i32, _vp]),
+        "tgb_step": (S, [_vp, _vp, _u64, _vp]),
+        "tgb_check": (S, [_vp, C.POINTER(Error)]),
+        "tgb_comm_unique_id": (S, [C.c_char_p]),
+        "tgb_comm_init": (S, [C.c_char_p, _i32, _i32, C.POINTER(_vp)]),
+        "tgb_comm_destroy": (None, [_vp]),
+        "tgb_layer_scaler": (S, [_vp, _u64, _vp, _vp]),
+        "tgb_layer_clip": (S, [_vp, _u64, C.c_float, _vp, _vp, _vp]),
+        "tgb_layer_ternarize": (S, [_vp, _u64, C.c_float, _u64, _u64, _u64, _u64, _u64, _vp,
+                                    _vp]),
+        "tgb_layer_decode": (S, [_vp, _u64, C.c_float, _vp, _vp]),
+        "tgb_layer_average": (S, [_i32, C.POINTER(_vp), _vp, _u64, _i32, _vp, _vp]),
+        "tgb_rng_bits": (S, [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp]),
+        "tgb_layer_check": (S, [_vp, C.POINTER(Error)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libtgb.so (building it first when the CUDA toolchain is present)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = _build.LIB
+        if build_if_missing and (not os.path.exists(path) or _build.needs_build()):
+            if os.path.exists(_build.NVCC):
+                _build.build()
+        if not os.path.exists(path):
+            raise RuntimeError(f"libtgb.so not built ({path}); run __graft_entry__.build()")
+        L = C.CDLL(path)
+        _declare(L)
+        _lib = L
+        return L
+
+
+class TgbError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {load().tgb_status_string(status).decode()} ({status})")
+
+
+def check(status: int, what: str) -> None:
+    if status != TGB_OK:
+        raise TgbError(status, what)
+
+
+def require_device() -> None:
+    if load().tgb_device_count() < 1:
+        raise RuntimeError("terngrad_b200 needs a CUDA (sm_100a) device; there is no CPU path")

@@ -1,0 +1,570 @@
+// C-ABI implementation (include/tgb/terngrad_b200.h): plans, NCCL sync,
+// per-layer entry points. Host code only; kernels live in kernels.cu.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "tgb_internal.h"
+
+using namespace tgb;
+
+namespace {
+
+constexpr uint64_t kAlignCodes = 16;   // per-layer code region alignment (bytes)
+constexpr uint64_t kAlignPush = 256;   // push buffer / code region base alignment
+
+inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+#define TGB_CUDA(expr)                                  \
+    do {                                                \
+        const cudaError_t e_ = (expr);                  \
+        if (e_ != cudaSuccess) return TGB_ERR_CUDA;     \
+    } while (0)
+
+#define TGB_NCCL(expr)                                  \
+    do {                                                \
+        const ncclResult_t r_ = (expr);                 \
+        if (r_ != ncclSuccess) return TGB_ERR_NCCL;     \
+    } while (0)
+
+// rng.hpp:50-54
+inline void philox_key(uint64_t seed, uint64_t name_hash, uint64_t worker, uint32_t& k0,
+                       uint32_t& k1) {
+    k0 = static_cast<uint32_t>(seed ^ name_hash);
+    k1 = static_cast<uint32_t>((seed >> 32) ^ (name_hash >> 32) ^
+                               (worker * 0x9E3779B97F4A7C15ull));
+}
+
+// per-device scratch for the per-layer API (error word, K1 partials)
+struct DeviceScratch {
+    ErrWord* err = nullptr;
+    uint32_t* counters = nullptr;  // [0] layer_done, [1] global_done
+    float* tmp = nullptr;          // [0] slot, [1] bound
+    bool ready = false;
+};
+DeviceScratch g_scratch[64];
+
+tgb_status scratch(DeviceScratch** out) {
+    int dev = 0;
+    TGB_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return TGB_ERR_CUDA;
+    DeviceScratch& s = g_scratch[dev];
+    if (!s.ready) {
+        TGB_CUDA(cudaMalloc(&s.err, sizeof(ErrWord)));
+        TGB_CUDA(cudaMemset(s.err, 0, sizeof(ErrWord)));
+        TGB_CUDA(cudaMalloc(&s.counters, 2 * sizeof(uint32_t)));
+        TGB_CUDA(cudaMemset(s.counters, 0, 2 * sizeof(uint32_t)));
+        TGB_CUDA(cudaMalloc(&s.tmp, 2 * sizeof(float)));
+        s.ready = true;
+    }
+    *out = &s;
+    return TGB_OK;
+}
+
+inline uint32_t layer_vec_flags(const void* g, const void* out) {
+    uint32_t f = 0;
+    if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) f |= kLayerVecIn;
+    if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) f |= kLayerVecOut;
+    return f;
+}
+
+}  // namespace
+
+struct tgb_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 0, rank = 0;
+};
+
+struct tgb_plan {
+    int device = 0;
+    tgb_codec_params p{};
+    uint16_t worker = 0;
+    int32_t n_workers = 1;
+    std::vector<tgb_layer_desc> desc;
+    std::vector<LayerDev> h_layers;
+    std::vector<ChunkDev> h_chunks;
+    LayerDev* d_layers = nullptr;
+    ChunkDev* d_chunks = nullptr;
+    Partial* d_partials = nullptr;
+    uint32_t* d_counters = nullptr;  // n_layers layer_done + 1 global_done
+    float* d_bounds = nullptr;
+    uint8_t* d_push = nullptr;
+    uint8_t* d_gathered = nullptr;
+    ErrWord* d_err = nullptr;
+    uint64_t push_bytes = 0, codes_offset = 0, code_bytes = 0, total = 0;
+    int32_t n_slots = 0, n_active = 0;
+    bool bound = false;
+    cudaStream_t last = nullptr;
+};
+
+extern "C" {
+
+const char* tgb_version(void) { return "terngrad_b200 1 (sm_100a)"; }
+
+const char* tgb_status_string(tgb_status s) {
+    switch (s) {
+        case TGB_OK: return "ok";
+        case TGB_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case TGB_ERR_CODEC: return "codec error";
+        case TGB_ERR_CUDA: return "CUDA error";
+        case TGB_ERR_NCCL: return "NCCL error";
+        case TGB_ERR_UNSUPPORTED: return "unsupported configuration";
+    }
+    return "unknown";
+}
+
+uint64_t tgb_fnv1a64(const char* s, size_t len) {  // rng.hpp:37-44
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (size_t i = 0; i < len; ++i) {
+        h ^= static_cast<unsigned char>(s[i]);
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+int32_t tgb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------ plans
+tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
+                           const tgb_codec_params* params, uint16_t worker, int32_t n_workers,
+                           tgb_plan** out) {
+    if (!out || !params || n_layers < 0 || (n_layers > 0 && !layers)) return TGB_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (!(params->clip_factor > 0.0f)) return TGB_ERR_INVALID_ARGUMENT;  // codec.hpp:91-92
+    if (params->bucketing == TGB_BUCKET_FIXED) {
+        if (params->bucket_size < 1) return TGB_ERR_INVALID_ARGUMENT;  // codec.hpp:93-94
+        return TGB_ERR_UNSUPPORTED;
+    }
+    if (params->bucketing != TGB_BUCKET_PER_TENSOR && params->bucketing != TGB_BUCKET_GLOBAL)
+        return TGB_ERR_INVALID_ARGUMENT;
+    if (n_workers < 1 || n_workers > kMaxWorkers || worker >= n_workers)
+        return TGB_ERR_INVALID_ARGUMENT;
+    for (int32_t l = 0; l < n_layers; ++l) {
+        if (layers[l].flags & TGB_LAYER_PASSTHROUGH) return TGB_ERR_UNSUPPORTED;
+        if (layers[l].n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;  // TernaryBlock::n is u32
+    }
+    auto* P = new (std::nothrow) tgb_plan;
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    P->p = *params;
+    P->worker = worker;
+    P->n_workers = n_workers;
+    P->desc.assign(layers, layers + n_layers);
+    if (cudaGetDevice(&P->device) != cudaSuccess) {
+        delete P;
+        return TGB_ERR_CUDA;
+    }
+
+    // layout: [slots (one per layer)][pad to 256][codes, layer l at 16B-aligned offset][pad 256]
+    P->n_slots = n_layers;
+    P->codes_offset = round_up(static_cast<uint64_t>(n_layers) * sizeof(float), kAlignPush);
+    uint64_t off = P->codes_offset;
+    P->h_layers.resize(n_layers);
+    for (int32_t l = 0; l < n_layers; ++l) {
+        LayerDev& L = P->h_layers[l];
+        std::memset(&L, 0, sizeof(L));
+        L.n = layers[l].n;
+        L.code_off = off;
+        L.slot = l;
+        philox_key(params->seed, layers[l].name_hash, worker, L.key0, L.key1);
+        L.flags = params->clipping_enabled ? kLayerClip : 0u;
+        L.first_chunk = static_cast<uint32_t>(P->h_chunks.size());
+        for (uint64_t b = 0; b < L.n; b += kChunk) {
+            ChunkDev c;
+            c.layer = static_cast<uint32_t>(l);
+            c.begin = b;
+            c.count = static_cast<uint32_t>(std::min<uint64_t>(kChunk, L.n - b));
+            P->h_chunks.push_back(c);
+        }
+        L.n_chunks = static_cast<uint32_t>(P->h_chunks.size()) - L.first_chunk;
+        const uint64_t nb = (L.n + 3) / 4;
+        P->code_bytes += nb;
+        P->total += L.n;
+        if (L.n > 0) ++P->n_active;
+        off += round_up(nb, kAlignCodes);
+    }
+    P->push_bytes = round_up(off, kAlignPush);
+
+    const size_t nl = std::max<size_t>(1, n_layers), nc = std::max<size_t>(1, P->h_chunks.size());
+    bool ok = cudaMalloc(&P->d_layers, nl * sizeof(LayerDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_chunks, nc * sizeof(ChunkDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_partials, nc * sizeof(Partial)) == cudaSuccess &&
+              cudaMalloc(&P->d_counters, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&P->d_bounds, nl * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&P->d_push, P->push_bytes) == cudaSuccess &&
+              cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess;
+    if (ok && n_workers > 1)
+        ok = cudaMalloc(&P->d_gathered, P->push_bytes * static_cast<uint64_t>(n_workers)) ==
+             cudaSuccess;
+    ok = ok && cudaMemset(P->d_counters, 0, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
+         cudaMemset(P->d_push, 0, P->push_bytes) == cudaSuccess &&
+         cudaMemset(P->d_err, 0, sizeof(ErrWord)) == cudaSuccess &&
+         cudaMemset(P->d_bounds, 0, nl * sizeof(float)) == cudaSuccess;
+    if (ok && !P->h_chunks.empty())
+        ok = cudaMemcpy(P->d_chunks, P->h_chunks.data(), P->h_chunks.size() * sizeof(ChunkDev),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok && n_layers > 0)
+        ok = cudaMemcpy(P->d_layers, P->h_layers.data(), n_layers * sizeof(LayerDev),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+        tgb_plan_destroy(P);
+        return TGB_ERR_CUDA;
+    }
+    *out = P;
+    return TGB_OK;
+}
+
+void tgb_plan_destroy(tgb_plan* P) {
+    if (!P) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(P->device);
+    cudaFree(P->d_layers);
+    cudaFree(P->d_chunks);
+    cudaFree(P->d_partials);
+    cudaFree(P->d_counters);
+    cudaFree(P->d_bounds);
+    cudaFree(P->d_push);
+    cudaFree(P->d_gathered);
+    cudaFree(P->d_err);
+    cudaSetDevice(prev);
+    delete P;
+}
+
+tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
+    if (!P || !o) return TGB_ERR_INVALID_ARGUMENT;
+    std::memset(o, 0, sizeof(*o));
+    o->total_elements = P->total;
+    o->push_bytes = P->push_bytes;
+    o->code_bytes = P->code_bytes;
+    o->scaler_offset = 0;
+    o->codes_offset = P->codes_offset;
+    o->n_layers = static_cast<int32_t>(P->desc.size());
+    o->n_slots = P->n_slots;
+    o->n_chunks = static_cast<int32_t>(P->h_chunks.size());
+    o->n_workers = P->n_workers;
+    o->chunk_elems = kChunk;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_layer_layout(const tgb_plan* P, int32_t layer, uint64_t* code_offset,
+                                 int32_t* slot) {
+    if (!P || layer < 0 || layer >= static_cast<int32_t>(P->desc.size()))
+        return TGB_ERR_INVALID_ARGUMENT;
+    if (code_offset) *code_offset = P->h_layers[layer].code_off;
+    if (slot) *slot = P->h_layers[layer].slot;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_bind(tgb_plan* P, const float* const* d_grads, float* const* d_out) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    const size_t nl = P->desc.size();
+    if (nl > 0 && (!d_grads || !d_out)) return TGB_ERR_INVALID_ARGUMENT;
+    for (size_t l = 0; l < nl; ++l) {
+        LayerDev& L = P->h_layers[l];
+        if (L.n > 0 && (!d_grads[l] || !d_out[l])) return TGB_ERR_INVALID_ARGUMENT;
+        L.g = d_grads[l];
+        L.out = d_out[l];
+        L.flags = (L.flags & ~(kLayerVecIn | kLayerVecOut)) | layer_vec_flags(L.g, L.out);
+    }
+    if (nl > 0)
+        TGB_CUDA(cudaMemcpy(P->d_layers, P->h_layers.data(), nl * sizeof(LayerDev),
+                            cudaMemcpyHostToDevice));
+    P->bound = true;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_buffers(tgb_plan* P, uint8_t** d_push, uint8_t** d_gathered, float** d_bounds) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    if (d_push) *d_push = P->d_push;
+    if (d_gathered) *d_gathered = P->d_gathered;
+    if (d_bounds) *d_bounds = P->d_bounds;
+    return TGB_OK;
+}
+
+tgb_status tgb_stats(tgb_plan* P, void* stream) {
+    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    const int32_t nl = static_cast<int32_t>(P->desc.size());
+    K1Launch k{P->d_partials, P->d_counters, P->d_counters + nl, P->d_bounds,
+               reinterpret_cast<float*>(P->d_push), P->d_err, P->p.clip_factor,
+               P->p.bucketing == TGB_BUCKET_GLOBAL, nl, P->n_active};
+    TGB_CUDA(launch_k1_table(P->d_layers, P->d_chunks, static_cast<uint32_t>(P->h_chunks.size()), k,
+                             st));
+    return TGB_OK;
+}
+
+tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
+    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    K2Launch k{P->d_push, reinterpret_cast<const float*>(P->d_push), P->d_bounds, P->d_err, t, 1};
+    TGB_CUDA(launch_k2_table(P->d_layers, P->d_chunks, static_cast<uint32_t>(P->h_chunks.size()), k,
+                             st));
+    return TGB_OK;
+}
+
+tgb_status tgb_encode(tgb_plan* P, uint64_t t, void* stream) {
+    tgb_status s = tgb_stats(P, stream);
+    if (s != TGB_OK) return s;
+    return tgb_ternarize_pack(P, t, stream);
+}
+
+tgb_status tgb_share_scalers(tgb_plan* P, tgb_comm* C, void* stream) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    if (P->n_workers == 1) return TGB_OK;
+    if (!C || C->nranks != P->n_workers || C->rank != P->worker) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    float* slots = reinterpret_cast<float*>(P->d_push);
+    TGB_NCCL(ncclAllReduce(slots, slots, static_cast<size_t>(P->n_slots), ncclFloat, ncclMax,
+                           C->comm, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    if (P->n_workers == 1) return TGB_OK;
+    if (!C || C->nranks != P->n_workers || C->rank != P->worker) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    TGB_NCCL(ncclAllGather(P->d_push, P->d_gathered, P->push_bytes, ncclUint8, C->comm, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_workers, void* stream) {
+    if (!P || !P->bound || !d_src || n_workers < 1 || n_workers > kMaxWorkers)
+        return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    K3Launch k{d_src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
+               1.0f / static_cast<float>(n_workers), P->d_err};
+    TGB_CUDA(launch_k3_table(P->d_layers, P->d_chunks, static_cast<uint32_t>(P->h_chunks.size()), k,
+                             st));
+    return TGB_OK;
+}
+
+tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    tgb_status s = tgb_stats(P, stream);
+    if (s != TGB_OK) return s;
+    if (P->p.share_mode == TGB_SHARE_PRESHARED && P->n_workers > 1) {
+        s = tgb_share_scalers(P, C, stream);
+        if (s != TGB_OK) return s;
+    }
+    s = tgb_ternarize_pack(P, t, stream);
+    if (s != TGB_OK) return s;
+    if (P->n_workers > 1) {
+        s = tgb_sync(P, C, stream);
+        if (s != TGB_OK) return s;
+        return tgb_decode_average(P, P->d_gathered, P->n_workers, stream);
+    }
+    return tgb_decode_average(P, P->d_push, 1, stream);
+}
+
+tgb_status tgb_check(tgb_plan* P, tgb_error* out) {
+    if (!P || !out) return TGB_ERR_INVALID_ARGUMENT;
+    TGB_CUDA(cudaStreamSynchronize(P->last));
+    ErrWord e;
+    TGB_CUDA(cudaMemcpy(&e, P->d_err, sizeof(e), cudaMemcpyDeviceToHost));
+    out->flags = e.flags;
+    out->layer = e.flags ? e.layer : -1;
+    out->index = e.flags ? e.index : 0;
+    if (e.flags) TGB_CUDA(cudaMemset(P->d_err, 0, sizeof(ErrWord)));
+    return e.flags ? TGB_ERR_CODEC : TGB_OK;
+}
+
+// ------------------------------------------------------------------- comm
+tgb_status tgb_comm_unique_id(uint8_t out[TGB_UNIQUE_ID_BYTES]) {
+    static_assert(sizeof(ncclUniqueId) == TGB_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    TGB_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+    return TGB_OK;
+}
+
+tgb_status tgb_comm_init(const uint8_t id[TGB_UNIQUE_ID_BYTES], int32_t nranks, int32_t rank,
+                         tgb_comm** out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return TGB_ERR_INVALID_ARGUMENT;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    auto* C = new (std::nothrow) tgb_comm;
+    if (!C) return TGB_ERR_INVALID_ARGUMENT;
+    const ncclResult_t r = ncclCommInitRank(&C->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        delete C;
+        return TGB_ERR_NCCL;
+    }
+    C->nranks = nranks;
+    C->rank = rank;
+    *out = C;
+    return TGB_OK;
+}
+
+void tgb_comm_destroy(tgb_comm* C) {
+    if (!C) return;
+    if (C->comm) ncclCommDestroy(C->comm);
+    delete C;
+}
+
+// -------------------------------------------------------------- per layer
+tgb_status tgb_layer_scaler(const float* d_g, uint64_t n, float* d_s, void* stream) {
+    if ((n > 0 && !d_g) || !d_s) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        TGB_CUDA(cudaMemsetAsync(d_s, 0, sizeof(float), st));
+        return TGB_OK;
+    }
+    DeviceScratch* S;
+    tgb_status s = scratch(&S);
+    if (s != TGB_OK) return s;
+    const uint32_t nc = static_cast<uint32_t>((n + kChunk - 1) / kChunk);
+    Partial* parts = nullptr;
+    TGB_CUDA(cudaMallocAsync(&parts, nc * sizeof(Partial), st));
+    LayerDev L{};
+    L.g = d_g;
+    L.n = n;
+    L.slot = 0;
+    L.flags = layer_vec_flags(d_g, nullptr) & kLayerVecIn;  // clipping off => scaler = max|g|
+    K1Launch k{parts, S->counters, S->counters + 1, S->tmp + 1, d_s, S->err, 2.5f, 0, 1, 1};
+    const cudaError_t e = launch_k1_single(L, k, st);
+    cudaFreeAsync(parts, st);
+    TGB_CUDA(e);
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_clip(const float* d_g, uint64_t n, float c, float* d_out, float* d_bound,
+                          void* stream) {
+    if ((n > 0 && (!d_g || !d_out)) || !d_bound) return TGB_ERR_INVALID_ARGUMENT;
+    if (!(c > 0.0f)) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (n < 2) {  // codec.hpp:118: small tensors pass through unchanged
+        const float inf = INFINITY;
+        TGB_CUDA(cudaMemcpyAsync(d_bound, &inf, sizeof(float), cudaMemcpyHostToDevice, st));
+        if (n == 1) TGB_CUDA(cudaMemcpyAsync(d_out, d_g, sizeof(float), cudaMemcpyDeviceToDevice, st));
+        return TGB_OK;
+    }
+    DeviceScratch* S;
+    tgb_status s = scratch(&S);
+    if (s != TGB_OK) return s;
+    const uint32_t nc = static_cast<uint32_t>((n + kChunk - 1) / kChunk);
+    Partial* parts = nullptr;
+    TGB_CUDA(cudaMallocAsync(&parts, nc * sizeof(Partial), st));
+    LayerDev L{};
+    L.g = d_g;
+    L.n = n;
+    L.slot = 0;
+    L.flags = kLayerClip | (layer_vec_flags(d_g, nullptr) & kLayerVecIn);
+    K1Launch k{parts, S->counters, S->counters + 1, d_bound, S->tmp, S->err, c, 0, 1, 1};
+    cudaError_t e = launch_k1_single(L, k, st);
+    cudaFreeAsync(parts, st);
+    TGB_CUDA(e);
+    TGB_CUDA(launch_clip_apply(d_g, n, d_bound, d_out, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_ternarize(const float* d_g, uint64_t n, float s, uint64_t seed, uint64_t t,
+                               uint64_t name_hash, uint64_t worker, uint64_t rng_base,
+                               uint8_t* d_codes, void* stream) {
+    if (n > 0 && (!d_g || !d_codes)) return TGB_ERR_INVALID_ARGUMENT;
+    if (n == 0) return TGB_OK;
+    auto st = static_cast<cudaStream_t>(stream);
+    DeviceScratch* S;
+    tgb_status r = scratch(&S);
+    if (r != TGB_OK) return r;
+    uint32_t k0, k1;
+    philox_key(seed, name_hash, worker, k0, k1);
+    if ((rng_base & 3u) != 0) {  // stream lanes straddle code bytes
+        TGB_CUDA(launch_k2_offset(d_g, n, s, k0, k1, t, rng_base, d_codes, S->err, st));
+        return TGB_OK;
+    }
+    LayerDev L{};
+    L.g = d_g;
+    L.n = n;
+    L.code_off = 0;
+    L.key0 = k0;
+    L.key1 = k1;
+    L.slot = 0;
+    L.flags = layer_vec_flags(d_g, nullptr) & kLayerVecIn;
+    K2Launch k{d_codes, nullptr, nullptr, S->err, t, 0, s, rng_base >> 2};
+    TGB_CUDA(launch_k2_single(L, k, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_decode(const uint8_t* d_codes, uint64_t n, float s, float* d_out,
+                            void* stream) {
+    if (n > 0 && (!d_codes || !d_out)) return TGB_ERR_INVALID_ARGUMENT;
+    if (n == 0) return TGB_OK;
+    auto st = static_cast<cudaStream_t>(stream);
+    DeviceScratch* S;
+    tgb_status r = scratch(&S);
+    if (r != TGB_OK) return r;
+    LayerDev L{};
+    L.n = n;
+    L.out = d_out;
+    L.flags = layer_vec_flags(nullptr, d_out) & kLayerVecOut;
+    const uint8_t* codes[1] = {d_codes};
+    // decode(blk) == s * float(code) == average over N=1 with sharing (invN = 1)
+    K3Launch k{nullptr, 0, 1, 1, 1.0f, S->err, s};
+    TGB_CUDA(launch_k3_single(L, codes, nullptr, k, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_average(int32_t n_workers, const uint8_t* const* d_codes, const float* d_s,
+                             uint64_t n, int32_t sharing, float* d_out, void* stream) {
+    if (n_workers < 1 || n_workers > kMaxWorkers || !d_codes || !d_s)
+        return TGB_ERR_INVALID_ARGUMENT;
+    if (n == 0) return TGB_OK;
+    if (!d_out) return TGB_ERR_INVALID_ARGUMENT;
+    for (int w = 0; w < n_workers; ++w)
+        if (!d_codes[w]) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    DeviceScratch* S;
+    tgb_status r = scratch(&S);
+    if (r != TGB_OK) return r;
+    LayerDev L{};
+    L.n = n;
+    L.out = d_out;
+    L.flags = layer_vec_flags(nullptr, d_out) & kLayerVecOut;
+    K3Launch k{nullptr, 0, n_workers, sharing ? 1 : 0, 1.0f / static_cast<float>(n_workers),
+               S->err};
+    TGB_CUDA(launch_k3_single(L, d_codes, d_s, k, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_rng_bits(uint64_t seed, uint64_t t, uint64_t name_hash, uint64_t worker, uint64_t k0,
+                        uint64_t n, uint32_t* d_out, void* stream) {
+    if (n > 0 && !d_out) return TGB_ERR_INVALID_ARGUMENT;
+    uint32_t a, b;
+    philox_key(seed, name_hash, worker, a, b);
+    TGB_CUDA(launch_rng_bits(a, b, t, k0, n, d_out, static_cast<cudaStream_t>(stream)));
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_check(void* stream, tgb_error* out) {
+    if (!out) return TGB_ERR_INVALID_ARGUMENT;
+    DeviceScratch* S;
+    tgb_status r = scratch(&S);
+    if (r != TGB_OK) return r;
+    TGB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    ErrWord e;
+    TGB_CUDA(cudaMemcpy(&e, S->err, sizeof(e), cudaMemcpyDeviceToHost));
+    out->flags = e.flags;
+    out->layer = e.flags ? e.layer : -1;
+    out->index = e.flags ? e.index : 0;
+    if (e.flags) TGB_CUDA(cudaMemset(S->err, 0, sizeof(ErrWord)));
+    return e.flags ? TGB_ERR_CODEC : TGB_OK;
+}
+
+}  // extern "C"

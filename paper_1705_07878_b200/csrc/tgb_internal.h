@@ -1,0 +1,63 @@
+// Host-side launch interface between capi.cu and kernels.cu (not exported).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tgb/terngrad_b200.h"
+#include "tgb_device.cuh"
+
+namespace tgb {
+
+struct K1Launch {
+    Partial* partials;
+    uint32_t* layer_done;
+    uint32_t* global_done;
+    float* bounds;
+    float* slots;
+    ErrWord* err;
+    float clip_factor;
+    int32_t global_bucketing;
+    int32_t n_layers;
+    int32_t n_active_layers;
+};
+
+struct K2Launch {
+    uint8_t* push;
+    const float* slots;
+    const float* bounds;
+    ErrWord* err;
+    uint64_t t;
+    int32_t reverse;
+    float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
+    uint64_t rng_q0 = 0;   // single-layer: rng_base / 4
+};
+
+struct K3Launch {
+    const uint8_t* src;
+    uint64_t stride;
+    int32_t n_workers;
+    int32_t sharing;
+    float inv_n;
+    ErrWord* err;
+    float s_imm = 0.0f;    // single-layer: scaler by value when scalers == nullptr
+};
+
+cudaError_t launch_k1_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+                            const K1Launch& p, cudaStream_t st);
+cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
+cudaError_t launch_k2_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+                            const K2Launch& p, cudaStream_t st);
+cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st);
+cudaError_t launch_k2_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t key1,
+                             uint64_t t, uint64_t rng_base, uint8_t* codes, ErrWord* err,
+                             cudaStream_t st);
+cudaError_t launch_k3_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+                            const K3Launch& p, cudaStream_t st);
+cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, const float* scalers,
+                             const K3Launch& p, cudaStream_t st);
+cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
+                              cudaStream_t st);
+cudaError_t launch_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k0, uint64_t n,
+                            uint32_t* out, cudaStream_t st);
+
+}  // namespace tgb

@@ -1,0 +1,244 @@
+"""Plan / communicator / worker-sync wrappers over the C-ABI.
+
+``SyncWorker`` is the device replacement for the reference worker's sync
+segment (cluster.hpp:283-297): encode_step -> push -> ParameterServer::step
+-> pull -> decode_pull becomes K1 -> K2 -> NCCL allgather -> K3 on every rank.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, load
+from .codec import CodecConfig, CodecError, ShareMode, fnv1a64, _dev
+
+
+class _CudaBuf:
+    """Zero-copy torch view of plan-owned device memory."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False), "version": 3,
+        }
+
+
+def _view(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
+    if nbytes == 0 or ptr == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
+
+
+def aligned_flat(ns: Sequence[int], device, align_elems: int = 4, dtype=torch.float32):
+    """One flat HBM buffer holding every tensor at a 16-byte aligned offset.
+
+    Returns (flat, views). This is the gradient-bucket layout the kernels
+    stream with 128-bit accesses."""
+    offs, pos = [], 0
+    for n in ns:
+        offs.append(pos)
+        pos += (int(n) + align_elems - 1) // align_elems * align_elems
+    flat = torch.zeros(max(pos, 1), dtype=dtype, device=device)
+    views = [flat[o:o + int(n)] for o, n in zip(offs, ns)]
+    return flat, views
+
+
+class Comm:
+    """NCCL communicator created through the C-ABI (tgb_comm_init)."""
+
+    def __init__(self, rank: int, world_size: int, unique_id: Optional[bytes] = None,
+                 group=None):
+        L = load()
+        self.rank, self.world_size = rank, world_size
+        if unique_id is None:
+            import torch.distributed as dist
+
+            buf = [None]
+            if rank == 0:
+                raw = C.create_string_buffer(_lib.UNIQUE_ID_BYTES)
+                check(L.tgb_comm_unique_id(raw), "tgb_comm_unique_id")
+                buf[0] = bytes(raw.raw)
+            dist.broadcast_object_list(buf, src=0, group=group)
+            unique_id = buf[0]
+        h = C.c_void_p()
+        check(L.tgb_comm_init(unique_id, world_size, rank, C.byref(h)), "tgb_comm_init")
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        raw = C.create_string_buffer(_lib.UNIQUE_ID_BYTES)
+        check(load().tgb_comm_unique_id(raw), "tgb_comm_unique_id")
+        return bytes(raw.raw)
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            load().tgb_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plan:
+    """tgb_plan: one worker's layer table, push/gather buffers and workspace."""
+
+    def __init__(self, names: Sequence[str], ns: Sequence[int], cfg: CodecConfig, worker: int = 0,
+                 n_workers: int = 1, device=None, passthrough: Optional[Sequence[bool]] = None):
+        cfg.validate()
+        self.device = _dev(device)
+        self.names = list(names)
+        self.ns = [int(n) for n in ns]
+        self.cfg = cfg
+        self.worker, self.n_workers = int(worker), int(n_workers)
+        L = load()
+        nl = len(self.names)
+        descs = (_lib.LayerDesc * max(nl, 1))()
+        for l, (name, n) in enumerate(zip(self.names, self.ns)):
+            flags = _lib.TGB_LAYER_PASSTHROUGH if passthrough is not None and passthrough[l] else 0
+            descs[l] = _lib.LayerDesc(n, fnv1a64(name), flags, 0)
+        params = cfg.params()
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            check(L.tgb_plan_create(descs, nl, C.byref(params), self.worker, self.n_workers,
+                                    C.byref(h)), "tgb_plan_create")
+        self.h = h
+        info = _lib.PlanInfo()
+        check(L.tgb_plan_get_info(h, C.byref(info)), "tgb_plan_get_info")
+        self.info = info
+        self.code_offsets, self.slots = [], []
+        for l in range(nl):
+            off, slot = C.c_uint64(), C.c_int32()
+            check(L.tgb_plan_layer_layout(h, l, C.byref(off), C.byref(slot)), "layout")
+            self.code_offsets.append(off.value)
+            self.slots.append(slot.value)
+        push, gathered, bounds = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(L.tgb_plan_buffers(h, C.byref(push), C.byref(gathered), C.byref(bounds)), "buffers")
+        self.push = _view(push.value or 0, info.push_bytes, self.device)
+        self.gathered = _view(gathered.value or 0, info.push_bytes * self.n_workers
+                              if self.n_workers > 1 else 0, self.device)
+        self.bounds = _view(bounds.value or 0, 4 * nl, self.device).view(torch.float32) \
+            if nl else torch.empty(0, device=self.device)
+        self._grads = self._outs = None
+
+    # -- binding -------------------------------------------------------------
+    def bind(self, grads: Sequence[torch.Tensor], outs: Optional[Sequence[torch.Tensor]]):
+        """Bind per-layer device gradients (input) and averaged outputs."""
+        if outs is None:
+            outs = [torch.empty(0, device=self.device)] * len(grads)
+        for g, n in zip(grads, self.ns):
+            if g.numel() != n or g.dtype != torch.float32 or not g.is_contiguous():
+                raise ValueError("bind: gradient must be contiguous float32 of the planned size")
+            if n and g.device != self.device:
+                raise ValueError("bind: gradient on the wrong device")
+        nl = len(self.ns)
+        gp = (C.c_void_p * max(nl, 1))(*[g.data_ptr() if g.numel() else 0 for g in grads])
+        op = (C.c_void_p * max(nl, 1))(*[o.data_ptr() if o.numel() else 0 for o in outs])
+        # decode outputs are optional for encode-only use: point at the gradient
+        for l in range(nl):
+            if not op[l]:
+                op[l] = gp[l]
+        check(load().tgb_plan_bind(self.h, gp, op), "tgb_plan_bind")
+        self._grads, self._outs = list(grads), list(outs)
+
+    def _st(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return C.c_void_p(s.cuda_stream)
+
+    # -- pipeline stages -----------------------------------------------------
+    def stats(self, stream=None):
+        check(load().tgb_stats(self.h, self._st(stream)), "tgb_stats")
+
+    def ternarize_pack(self, t: int, stream=None):
+        check(load().tgb_ternarize_pack(self.h, int(t), self._st(stream)), "tgb_ternarize_pack")
+
+    def encode(self, t: int, stream=None):
+        check(load().tgb_encode(self.h, int(t), self._st(stream)), "tgb_encode")
+
+    def share_scalers(self, comm: Comm, stream=None):
+        check(load().tgb_share_scalers(self.h, comm.h, self._st(stream)), "tgb_share_scalers")
+
+    def sync(self, comm: Comm, stream=None):
+        check(load().tgb_sync(self.h, comm.h, self._st(stream)), "tgb_sync")
+
+    def decode_average(self, src: torch.Tensor, n_workers: int, stream=None):
+        check(load().tgb_decode_average(self.h, C.c_void_p(src.data_ptr()), int(n_workers),
+                                        self._st(stream)), "tgb_decode_average")
+
+    def step(self, t: int, comm: Optional[Comm] = None, stream=None):
+        check(load().tgb_step(self.h, comm.h if comm is not None else None, int(t),
+                              self._st(stream)), "tgb_step")
+
+    def error(self) -> _lib.Error:
+        e = _lib.Error()
+        st = load().tgb_check(self.h, C.byref(e))
+        if st not in (_lib.TGB_OK, _lib.TGB_ERR_CODEC):
+            check(st, "tgb_check")
+        return e
+
+    def raise_errors(self):
+        e = self.error()
+        if e.flags:
+            name = self.names[e.layer] if 0 <= e.layer < len(self.names) else "?"
+            if e.flags & _lib.TGB_E_NONFINITE:
+                raise CodecError("encode_step: non-finite gradient " + name)
+            if e.flags & _lib.TGB_E_CORRUPT_CODE:
+                raise CodecError(f"corrupt ternary code 11 in block {name} at element {e.index}")
+            raise CodecError(f"codec error flags {e.flags:#x} in {name}")
+
+    def scalers(self) -> torch.Tensor:
+        return self.push[:4 * len(self.ns)].view(torch.float32)
+
+    def layer_codes(self, l: int, worker: Optional[int] = None) -> torch.Tensor:
+        nb = (self.ns[l] + 3) // 4
+        if worker is None:
+            return self.push[self.code_offsets[l]:self.code_offsets[l] + nb]
+        base = worker * self.info.push_bytes + self.code_offsets[l]
+        return self.gathered[base:base + nb]
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            load().tgb_plan_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SyncWorker:
+    """One data-parallel worker's gradient synchronisation on one B200.
+
+    Mirrors Worker::run's sync segment (cluster.hpp:283-297): ``step(t)``
+    encodes this rank's gradients, exchanges scalers+codes with every rank
+    and decodes the identical averaged gradient into ``out``.
+    """
+
+    def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
+                 rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None):
+        self.device = _dev(device)
+        self.names = list(names)
+        self.shapes = [list(s) for s in shapes]
+        self.ns = [int(torch.Size(s).numel()) if len(s) else 0 for s in self.shapes]
+        self.rank, self.world_size = rank, world_size
+        if world_size > 1 and comm is None:
+            raise ValueError("SyncWorker: world_size > 1 needs a Comm")
+        self.comm = comm
+        self.plan = Plan(self.names, self.ns, cfg, worker=rank, n_workers=world_size,
+                         device=self.device)
+        self.grad_flat, self.grads = aligned_flat(self.ns, self.device)
+        self.out_flat, self.outs = aligned_flat(self.ns, self.device)
+        self.plan.bind(self.grads, self.outs)
+
+    def step(self, t: int, stream=None) -> List[torch.Tensor]:
+        self.plan.step(t, self.comm, stream)
+        return self.outs
+
+    def check(self):
+        self.plan.raise_errors()
