@@ -263,13 +263,27 @@ def run_b200(args):
 
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
-    barrier()
-    torch.cuda.synchronize(dev)
+
+    def soak(seconds, t0):
+        # untimed steps around the timed region so nvidia-smi (100 ms period)
+        # samples the clocks under this exact load
+        end = time.time() + seconds
+        t = t0
+        while time.time() < end:
+            for _ in range(20):
+                one_step(t)
+                t += 1
+            torch.cuda.synchronize(dev)
+
     with ClockSampler(local) as clk:
+        soak(0.6, 10_000)
+        barrier()
+        torch.cuda.synchronize(dev)
         for k in range(K):
             one_step(args.warmup + k, evs[k])
         torch.cuda.synchronize(dev)
-    barrier()
+        barrier()
+        soak(0.6, 20_000)
     plan.raise_errors()
     total_ms = evs[0][0].elapsed_time(evs[-1][4])
     stage = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(4)]

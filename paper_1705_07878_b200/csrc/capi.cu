@@ -4,11 +4,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
 
 #include "tgb_internal.h"
+#include "tgb_ring.cuh"
 
 using namespace tgb;
 
@@ -86,9 +88,15 @@ struct tgb_plan {
     int32_t n_workers = 1;
     std::vector<tgb_layer_desc> desc;
     std::vector<LayerDev> h_layers;
-    std::vector<ChunkDev> h_chunks;
+    std::vector<ChunkDev> h_chunks;  // K3 work items (16K elements)
+    std::vector<ChunkDev> h_tiles;   // K1/K2 persistent tiles (4K elements)
+    std::vector<SegDev> h_segs;
+    std::vector<CtaDev> h_ctas;
     LayerDev* d_layers = nullptr;
     ChunkDev* d_chunks = nullptr;
+    ChunkDev* d_tiles = nullptr;
+    SegDev* d_segs = nullptr;
+    CtaDev* d_ctas = nullptr;
     Partial* d_partials = nullptr;
     uint32_t* d_counters = nullptr;  // n_layers layer_done + 1 global_done
     float* d_bounds = nullptr;
@@ -98,6 +106,10 @@ struct tgb_plan {
     uint64_t push_bytes = 0, codes_offset = 0, code_bytes = 0, total = 0;
     int32_t n_slots = 0, n_active = 0;
     bool bound = false;
+    bool chunk_k1 = true;  // grid-per-chunk K1 (default) vs persistent TMA ring
+    bool chunk_k2 = true;
+    int32_t k2_variant = 0;  // TGB_K2V
+    int32_t k1_variant = 0;  // TGB_K1V
     cudaStream_t last = nullptr;
 };
 
@@ -148,8 +160,8 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     }
     if (params->bucketing != TGB_BUCKET_PER_TENSOR && params->bucketing != TGB_BUCKET_GLOBAL)
         return TGB_ERR_INVALID_ARGUMENT;
-    if (n_workers < 1 || n_workers > kMaxWorkers || worker >= n_workers)
-        return TGB_ERR_INVALID_ARGUMENT;
+    // worker keys the RNG (rng.hpp:54) and need not be < n_workers for encode-only plans
+    if (n_workers < 1 || n_workers > kMaxWorkers) return TGB_ERR_INVALID_ARGUMENT;
     for (int32_t l = 0; l < n_layers; ++l) {
         if (layers[l].flags & TGB_LAYER_PASSTHROUGH) return TGB_ERR_UNSUPPORTED;
         if (layers[l].n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;  // TernaryBlock::n is u32
@@ -157,6 +169,14 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     auto* P = new (std::nothrow) tgb_plan;
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     P->p = *params;
+    // default: grid-per-chunk K1/K2 (measured faster on B200, tools/ab_bench.py);
+    // TGB_K12 / TGB_K1 / TGB_K2 = persistent selects the TMA-ring kernels
+    P->chunk_k1 = P->chunk_k2 = true;
+    if (const char* m = std::getenv("TGB_K12")) P->chunk_k1 = P->chunk_k2 = std::strcmp(m, "persistent") != 0;
+    if (const char* m = std::getenv("TGB_K1")) P->chunk_k1 = std::strcmp(m, "persistent") != 0;
+    if (const char* m = std::getenv("TGB_K2")) P->chunk_k2 = std::strcmp(m, "persistent") != 0;
+    if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
+    if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
     P->worker = worker;
     P->n_workers = n_workers;
     P->desc.assign(layers, layers + n_layers);
@@ -187,6 +207,13 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
             P->h_chunks.push_back(c);
         }
         L.n_chunks = static_cast<uint32_t>(P->h_chunks.size()) - L.first_chunk;
+        for (uint64_t b = 0; b < L.n; b += kTileElems) {
+            ChunkDev c;
+            c.layer = static_cast<uint32_t>(l);
+            c.begin = b;
+            c.count = static_cast<uint32_t>(std::min<uint64_t>(kTileElems, L.n - b));
+            P->h_tiles.push_back(c);
+        }
         const uint64_t nb = (L.n + 3) / 4;
         P->code_bytes += nb;
         P->total += L.n;
@@ -195,10 +222,45 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     }
     P->push_bytes = round_up(off, kAlignPush);
 
+    // persistent K1/K2 partition: CTA c owns tiles [c*T/G, (c+1)*T/G); a segment is
+    // the part of a CTA's run inside one layer (K1 emits one partial per segment)
+    uint32_t G = 0;
+    if (persistent_grid(&G) != cudaSuccess) {
+        delete P;
+        return TGB_ERR_CUDA;
+    }
+    const uint64_t T = P->h_tiles.size();
+    if (G > T) G = static_cast<uint32_t>(T);
+    std::vector<uint32_t> segs_of_layer(n_layers, 0);
+    for (uint32_t c = 0; c < G; ++c) {
+        const uint32_t a = static_cast<uint32_t>(T * c / G), b = static_cast<uint32_t>(T * (c + 1) / G);
+        CtaDev cd;
+        cd.seg_begin = static_cast<uint32_t>(P->h_segs.size());
+        for (uint32_t t = a; t < b;) {
+            SegDev sg;
+            sg.layer = P->h_tiles[t].layer;
+            sg.tile_begin = t;
+            while (t < b && P->h_tiles[t].layer == sg.layer) ++t;
+            sg.tile_end = t;
+            sg.pad = 0;
+            if (segs_of_layer[sg.layer]++ == 0)
+                P->h_layers[sg.layer].first_seg = static_cast<uint32_t>(P->h_segs.size());
+            P->h_segs.push_back(sg);
+        }
+        cd.seg_end = static_cast<uint32_t>(P->h_segs.size());
+        P->h_ctas.push_back(cd);
+    }
+    for (int32_t l = 0; l < n_layers; ++l) P->h_layers[l].n_segs = segs_of_layer[l];
+
     const size_t nl = std::max<size_t>(1, n_layers), nc = std::max<size_t>(1, P->h_chunks.size());
+    const size_t ntl = std::max<size_t>(1, P->h_tiles.size()), nsg = std::max<size_t>(1, P->h_segs.size());
+    const size_t nct = std::max<size_t>(1, P->h_ctas.size());
     bool ok = cudaMalloc(&P->d_layers, nl * sizeof(LayerDev)) == cudaSuccess &&
               cudaMalloc(&P->d_chunks, nc * sizeof(ChunkDev)) == cudaSuccess &&
-              cudaMalloc(&P->d_partials, nc * sizeof(Partial)) == cudaSuccess &&
+              cudaMalloc(&P->d_tiles, ntl * sizeof(ChunkDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_segs, nsg * sizeof(SegDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_ctas, nct * sizeof(CtaDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_partials, std::max(nsg, nc) * sizeof(Partial)) == cudaSuccess &&
               cudaMalloc(&P->d_counters, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&P->d_bounds, nl * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&P->d_push, P->push_bytes) == cudaSuccess &&
@@ -206,10 +268,19 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     if (ok && n_workers > 1)
         ok = cudaMalloc(&P->d_gathered, P->push_bytes * static_cast<uint64_t>(n_workers)) ==
              cudaSuccess;
+    const std::vector<float> inf_bounds(nl, INFINITY);  // empty layers: no clip (codec.hpp:118)
     ok = ok && cudaMemset(P->d_counters, 0, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
          cudaMemset(P->d_push, 0, P->push_bytes) == cudaSuccess &&
          cudaMemset(P->d_err, 0, sizeof(ErrWord)) == cudaSuccess &&
-         cudaMemset(P->d_bounds, 0, nl * sizeof(float)) == cudaSuccess;
+         cudaMemcpy(P->d_bounds, inf_bounds.data(), nl * sizeof(float), cudaMemcpyHostToDevice) ==
+             cudaSuccess;
+    if (ok && !P->h_tiles.empty())
+        ok = cudaMemcpy(P->d_tiles, P->h_tiles.data(), P->h_tiles.size() * sizeof(ChunkDev),
+                        cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(P->d_segs, P->h_segs.data(), P->h_segs.size() * sizeof(SegDev),
+                        cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(P->d_ctas, P->h_ctas.data(), P->h_ctas.size() * sizeof(CtaDev),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok && !P->h_chunks.empty())
         ok = cudaMemcpy(P->d_chunks, P->h_chunks.data(), P->h_chunks.size() * sizeof(ChunkDev),
                         cudaMemcpyHostToDevice) == cudaSuccess;
@@ -231,6 +302,9 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaSetDevice(P->device);
     cudaFree(P->d_layers);
     cudaFree(P->d_chunks);
+    cudaFree(P->d_tiles);
+    cudaFree(P->d_segs);
+    cudaFree(P->d_ctas);
     cudaFree(P->d_partials);
     cudaFree(P->d_counters);
     cudaFree(P->d_bounds);
@@ -300,8 +374,14 @@ tgb_status tgb_stats(tgb_plan* P, void* stream) {
     K1Launch k{P->d_partials, P->d_counters, P->d_counters + nl, P->d_bounds,
                reinterpret_cast<float*>(P->d_push), P->d_err, P->p.clip_factor,
                P->p.bucketing == TGB_BUCKET_GLOBAL, nl, P->n_active};
-    TGB_CUDA(launch_k1_table(P->d_layers, P->d_chunks, static_cast<uint32_t>(P->h_chunks.size()), k,
-                             st));
+    const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
+                           static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
+    k.variant = P->k1_variant;
+    if (P->chunk_k1)
+        TGB_CUDA(launch_k1_table(P->d_layers, P->d_chunks,
+                                 static_cast<uint32_t>(P->h_chunks.size()), k, st));
+    else
+        TGB_CUDA(launch_k1_persistent(pl, k, st));
     return TGB_OK;
 }
 
@@ -310,8 +390,13 @@ tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     K2Launch k{P->d_push, reinterpret_cast<const float*>(P->d_push), P->d_bounds, P->d_err, t, 1};
-    TGB_CUDA(launch_k2_table(P->d_layers, P->d_chunks, static_cast<uint32_t>(P->h_chunks.size()), k,
-                             st));
+    const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
+                           static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
+    if (P->chunk_k2)
+        TGB_CUDA(launch_k2_table(P->d_layers, P->d_chunks,
+                                 static_cast<uint32_t>(P->h_chunks.size()), k, st));
+    else
+        TGB_CUDA(launch_k2_persistent(pl, k, st));
     return TGB_OK;
 }
 
@@ -324,7 +409,7 @@ tgb_status tgb_encode(tgb_plan* P, uint64_t t, void* stream) {
 tgb_status tgb_share_scalers(tgb_plan* P, tgb_comm* C, void* stream) {
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     if (P->n_workers == 1) return TGB_OK;
-    if (!C || C->nranks != P->n_workers || C->rank != P->worker) return TGB_ERR_INVALID_ARGUMENT;
+    if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     float* slots = reinterpret_cast<float*>(P->d_push);
@@ -336,7 +421,7 @@ tgb_status tgb_share_scalers(tgb_plan* P, tgb_comm* C, void* stream) {
 tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     if (P->n_workers == 1) return TGB_OK;
-    if (!C || C->nranks != P->n_workers || C->rank != P->worker) return TGB_ERR_INVALID_ARGUMENT;
+    if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     TGB_NCCL(ncclAllGather(P->d_push, P->d_gathered, P->push_bytes, ncclUint8, C->comm, st));

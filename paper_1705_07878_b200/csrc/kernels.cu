@@ -11,6 +11,7 @@
 // fp32 streams, one CTA (256 threads) per 16K-element work item.
 #include "tgb_device.cuh"
 #include "tgb_internal.h"
+#include "tgb_stats.cuh"
 
 #include <cfloat>
 #include <cmath>
@@ -41,33 +42,9 @@ struct SingleSource {
 };
 
 // ====================================================================== K1
-struct K1Out {
-    Partial* partials;     // one per chunk (indexed by blockIdx.x)
-    uint32_t* layer_done;  // per layer arrival counters (self-resetting)
-    uint32_t* global_done; // arrival counter over layers (Global bucketing)
-    float* bounds;         // per layer clip bound
-    float* slots;          // scaler slots
-    ErrWord* err;
-    float clip_factor;
-    int32_t global_bucketing;
-    int32_t n_layers;
-    int32_t n_active_layers;  // layers with n > 0
-    const LayerDev* layers;   // for the Global fix-up (table source only)
-};
-
-__device__ __forceinline__ void acc4(const float4 v, const double x0, double& S, double& Q,
-                                     float& mx) {
-    const double d0 = static_cast<double>(v.x) - x0, d1 = static_cast<double>(v.y) - x0;
-    const double d2 = static_cast<double>(v.z) - x0, d3 = static_cast<double>(v.w) - x0;
-    S += (d0 + d1) + (d2 + d3);
-    Q = fma(d0, d0, Q);
-    Q = fma(d1, d1, Q);
-    Q = fma(d2, d2, Q);
-    Q = fma(d3, d3, Q);
-    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-}
-
-template <class Src>
+// Per-layer API version (one CTA per 16K-element chunk). The plan path uses the
+// persistent TMA-ring kernel in persistent.cu; both share tgb_stats.cuh.
+template <class Src, int U = 8, int A = 1>
 __global__ void __launch_bounds__(kThreads) k1_stats(Src src, K1Out o) {
     ChunkDev ch;
     LayerDev L;
@@ -75,122 +52,35 @@ __global__ void __launch_bounds__(kThreads) k1_stats(Src src, K1Out o) {
     const float* g = L.g + ch.begin;
     const uint32_t count = ch.count;
     const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
-    double S = 0.0, Q = 0.0;
+    double S[A], Q[A];  // A independent fp64 chains; combined in fixed order
     float mx = 0.0f;
+#pragma unroll
+    for (int k = 0; k < A; ++k) S[k] = Q[k] = 0.0;
     const uint32_t tid = threadIdx.x;
     uint32_t done = 0;
     if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         const uint32_t n4 = count >> 2;
         uint32_t i = tid;
-        for (; i + 3 * kThreads < n4; i += 4 * kThreads) {
-            float4 v[4];
+        for (; i + (U - 1) * kThreads < n4; i += U * kThreads) {  // U x 16 B in flight per thread
+            float4 v[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldcs(g4 + i + u * kThreads);
+            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + i + u * kThreads);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc4(v[u], x0, S, Q, mx);
+            for (int u = 0; u < U; ++u) acc4(v[u], x0, S[u % A], Q[u % A], mx);
         }
-        for (; i < n4; i += kThreads) acc4(__ldcs(g4 + i), x0, S, Q, mx);
+        for (; i < n4; i += kThreads) acc4(__ldcs(g4 + i), x0, S[0], Q[0], mx);
         done = n4 << 2;
     }
-    for (uint32_t i = done + tid; i < count; i += kThreads) {
-        const float x = __ldcs(g + i);
-        const double d = static_cast<double>(x) - x0;
-        S += d;
-        Q = fma(d, d, Q);
-        mx = fmaxf(mx, fabsf(x));
+    for (uint32_t i = done + tid; i < count; i += kThreads) acc1(__ldcs(g + i), x0, S[0], Q[0], mx);
+    double s_all = S[0], q_all = Q[0];
+#pragma unroll
+    for (int k = 1; k < A; ++k) {
+        s_all += S[k];
+        q_all += Q[k];
     }
-    block_reduce_sq<kThreads / 32>(S, Q, mx);
-
-    __shared__ bool is_last;
-    if (tid == 0) {
-        const double cn = static_cast<double>(count);
-        Partial p;
-        p.n = cn;
-        p.mean = x0 + S / cn;
-        p.m2 = Q - S * (S / cn);
-        p.mx = mx;
-        p.pad = 0;
-        o.partials[blockIdx.x] = p;
-        __threadfence();
-        const uint32_t ticket = atomicAdd(&o.layer_done[ch.layer], 1u);
-        is_last = (ticket == L.n_chunks - 1);
-    }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-
-    // ---- last CTA of this layer: deterministic Chan merge of its partials
-    __shared__ double sn[kThreads], smean[kThreads], sm2[kThreads];
-    __shared__ float smx[kThreads];
-    const uint32_t nc = L.n_chunks;
-    const uint32_t per = (nc + kThreads - 1) / kThreads;
-    double n = 0.0, mean = 0.0, m2 = 0.0;
-    float m = 0.0f;
-    const uint32_t lo = tid * per, hi = min(nc, lo + per);
-    for (uint32_t c = lo; c < hi; ++c) {
-        const Partial* pp = o.partials + L.first_chunk + c;
-        const double pn = __ldcg(&pp->n), pmean = __ldcg(&pp->mean), pm2 = __ldcg(&pp->m2);
-        const float pmx = __ldcg(&pp->mx);
-        chan_merge(n, mean, m2, pn, pmean, pm2);
-        m = fmaxf(m, pmx);
-    }
-    sn[tid] = n;
-    smean[tid] = mean;
-    sm2[tid] = m2;
-    smx[tid] = m;
-    __syncthreads();
-    for (uint32_t s = 1; s < kThreads; s <<= 1) {
-        if ((tid & (2 * s - 1)) == 0) {
-            double a_n = sn[tid], a_mean = smean[tid], a_m2 = sm2[tid];
-            chan_merge(a_n, a_mean, a_m2, sn[tid + s], smean[tid + s], sm2[tid + s]);
-            sn[tid] = a_n;
-            smean[tid] = a_mean;
-            sm2[tid] = a_m2;
-            smx[tid] = fmaxf(smx[tid], smx[tid + s]);
-        }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        const double fm = smean[0];
-        double fm2 = sm2[0];
-        const float fmx = smx[0];
-        float bound = INFINITY, s = 0.0f;
-        if (!isfinite(fm) || !isfinite(fm2) || !isfinite(fmx)) {
-            raise_error(o.err, TGB_E_NONFINITE, static_cast<int32_t>(ch.layer), 0);
-            bound = 0.0f;
-            s = 0.0f;
-        } else {
-            if ((L.flags & kLayerClip) && L.n >= 2) {
-                if (fm2 < 0.0) fm2 = 0.0;
-                const double sigma = sqrt(fm2 / static_cast<double>(L.n));  // codec.hpp:111
-                bound = static_cast<float>(static_cast<double>(o.clip_factor) * sigma);  // :119
-            }
-            s = fminf(fmx, bound);  // == scaler(clip(g)) (codec.hpp:121-122, :130)
-        }
-        o.bounds[ch.layer] = bound;
-        o.slots[L.slot] = s;
-        o.layer_done[ch.layer] = 0u;  // self-reset for the next launch
-        if (o.global_bucketing) {
-            __threadfence();
-            const uint32_t t = atomicAdd(o.global_done, 1u);
-            if (t == static_cast<uint32_t>(o.n_active_layers) - 1) {
-                __threadfence();
-                float gs = 0.0f;  // codec.hpp:212-216
-                for (int l = 0; l < o.n_layers; ++l) {
-                    const LayerDev& Ll = o.layers[l];
-                    if (Ll.n == 0 || (Ll.flags & kLayerPassthrough)) continue;
-                    gs = fmaxf(gs, __ldcg(o.slots + Ll.slot));
-                }
-                for (int l = 0; l < o.n_layers; ++l) {
-                    const LayerDev& Ll = o.layers[l];
-                    if (Ll.n == 0 || (Ll.flags & kLayerPassthrough)) continue;
-                    o.slots[Ll.slot] = gs;
-                }
-                *o.global_done = 0u;
-            }
-        }
-    }
+    k1_emit_and_finalize(o, L, ch.layer, blockIdx.x, L.first_chunk, L.n_chunks, count, x0, s_all,
+                         q_all, mx);
 }
 
 // ====================================================================== K2
@@ -207,7 +97,7 @@ struct K2Args {
 };
 
 template <class Src>
-__global__ void __launch_bounds__(kThreads) k2_ternarize(Src src, K2Args a) {
+__global__ void __launch_bounds__(kThreads, 3) k2_ternarize(Src src, K2Args a) {
     const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
     ChunkDev ch;
     LayerDev L;
@@ -232,46 +122,55 @@ __global__ void __launch_bounds__(kThreads) k2_ternarize(Src src, K2Args a) {
     }
     Decider dec;
     dec.init(bound, s);
-    PhiloxStream ph;
     const uint64_t qg = q0 + a.rng_q0;  // Philox counter of this chunk's first byte
+    Philox4<> ph;
     ph.init(L.key0, L.key1, static_cast<uint32_t>(qg >> 32), a.t);
     const uint32_t qbase = static_cast<uint32_t>(qg);
 
     const uint32_t nfull = count >> 2;  // bytes whose 4 elements all exist
     uint32_t q = tid;
+    float bad_mag = 0.0f;  // max clipped |x| seen (per-layer API check: mag > s)
     if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
-        for (; q + 3 * kThreads < nfull; q += 4 * kThreads) {
-            float4 v[4];
+        constexpr int U = 4;
+        for (; q + (U - 1) * kThreads < nfull; q += U * kThreads) {
+            float4 v[U];
+            uint32_t ctr[U];
+            uint4 r[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldcs(g4 + q + u * kThreads);
+            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + q + u * kThreads);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t qq = q + u * kThreads;
-                const uint4 r = ph(qbase + qq);
-                codes[qq] = static_cast<uint8_t>(dec.byte(v[u], r));
+            for (int u = 0; u < U; ++u) ctr[u] = qbase + q + u * kThreads;
+            ph(ctr, r);
+            uint32_t byte[U];
+            float amb = -1.0f;
+            uint32_t zmin = 0xFFFFFFFFu;  // == 0 iff some lane's bits == 0 (u == 0 corner)  // == 0 if any lane's bits == 0 (u == 0 corner)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                byte[u] = dec.byte_fast(v[u], r[u], amb);
+                zmin = min(zmin, min(min(r[u].x, r[u].y), min(r[u].z, r[u].w)));
             }
-            if (a.check) {
+            if (amb >= 0.0f || zmin == 0u || dec.exact_all) {  // rare: redo these bytes exactly
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float mm = fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
-                                           fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
-                    if (fminf(mm, bound) > s)
-                        raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(ch.layer),
-                                    ch.begin + 4ull * (q + u * kThreads));
-                }
+                for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                codes[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
+                if (a.check)
+                    bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
+                                                   fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
             }
         }
         for (; q < nfull; q += kThreads) {
             const float4 v = __ldcs(g4 + q);
-            const uint4 r = ph(qbase + q);
-            codes[q] = static_cast<uint8_t>(dec.byte(v, r));
-            if (a.check) {
-                const float mm = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-                if (fminf(mm, bound) > s)
-                    raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(ch.layer),
-                                ch.begin + 4ull * q);
-            }
+            uint32_t ctr[1] = {qbase + q};
+            uint4 r[1];
+            ph(ctr, r);
+            codes[q] = static_cast<uint8_t>(dec.byte(v, r[0]));
+            if (a.check)
+                bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)),
+                                               fmaxf(fabsf(v.z), fabsf(v.w))));
         }
     }
     // scalar path: unaligned input and the partial last byte (pad bits stay 00)
@@ -282,15 +181,16 @@ __global__ void __launch_bounds__(kThreads) k2_ternarize(Src src, K2Args a) {
             const uint32_t i = 4 * q + e;
             x[e] = i < count ? g[i] : 0.0f;
         }
-        const uint4 r = ph(qbase + q);
-        codes[q] = static_cast<uint8_t>(dec.byte(make_float4(x[0], x[1], x[2], x[3]), r));
-        if (a.check) {
-            for (int e = 0; e < 4; ++e)
-                if (fminf(fabsf(x[e]), bound) > s)
-                    raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(ch.layer),
-                                ch.begin + 4ull * q + e);
-        }
+        uint32_t ctr[1] = {qbase + q};
+        uint4 r[1];
+        ph(ctr, r);
+        codes[q] = static_cast<uint8_t>(dec.byte(make_float4(x[0], x[1], x[2], x[3]), r[0]));
+        if (a.check)
+            bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])),
+                                           fmaxf(fabsf(x[2]), fabsf(x[3]))));
     }
+    if (a.check && fminf(bad_mag, bound) > s)  // codec.hpp:163-165
+        raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(ch.layer), ch.begin);
 }
 
 // General-offset ternarize for the per-layer API when rng_base % 4 != 0:
@@ -325,7 +225,7 @@ k2_ternarize_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t
         const uint32_t bits = lane == 0 ? r.x : lane == 1 ? r.y : lane == 2 ? r.z : r.w;
         const float x = g[i];
         if (fabsf(x) > s) raise_error(err, TGB_E_SCALER_BELOW_MAX, 0, i);
-        byte |= dec.code(x, bits) << (2 * e);
+        byte |= dec.code_exact(x, bits) << (2 * e);
     }
     codes[q] = static_cast<uint8_t>(byte);
 }
@@ -360,7 +260,7 @@ struct K3Ptrs {  // per-layer API: explicit pointers (passed by value)
     const uint8_t* codes[kMaxWorkers];
 };
 
-template <class Src, bool kTable>
+template <class Src, bool kTable, bool kShared>
 __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs ptrs) {
     ChunkDev ch;
     LayerDev L;
@@ -389,49 +289,85 @@ __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs 
     const uint64_t q0 = ch.begin >> 2;
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
-    for (uint32_t q = tid; q < nbytes; q += kThreads) {
-        uint32_t acc = 0, bad = 0;
-        float4 o;
-        if (a.sharing) {
-            for (int w = 0; w < N; ++w) {
-                const uint32_t bw = kTable ? __ldcs(a.src + a.stride * w + L.code_off + q0 + q)
-                                           : __ldcs(ptrs.codes[w] + q0 + q);
-                acc += tab[bw];
-                bad |= bw & (bw >> 1) & 0x55u;
-            }
-            o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu], lut[(acc >> 16) & 0xffu],
-                            lut[acc >> 24]);
-        } else {  // codec.hpp:299-306: fp64 worker-order sum, then /N
-            double sm[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int w = 0; w < N; ++w) {
-                const uint32_t bw = kTable ? __ldcs(a.src + a.stride * w + L.code_off + q0 + q)
-                                           : __ldcs(ptrs.codes[w] + q0 + q);
-                bad |= bw & (bw >> 1) & 0x55u;
-                const double sd = static_cast<double>(sw[w]);
+    // U code bytes per thread per iteration, every worker's loads issued before
+    // any use: the gathered codes usually come from HBM (allgather landing
+    // buffer), so memory-level parallelism decides this kernel's speed.
+    constexpr int U = 4;
+    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
+        uint32_t acc[U], bad = 0;
+        double sm[kShared ? 1 : U][4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t c = (bw >> (2 * e)) & 3u;
-                    const double v = c == 1u ? 1.0 : (c == 2u ? -1.0 : 0.0);
-                    sm[e] = __dadd_rn(sm[e], __dmul_rn(sd, v));
+        for (int u = 0; u < U; ++u) {
+            acc[u] = 0;
+            if (!kShared) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) sm[kShared ? 0 : u][e] = 0.0;
+            }
+        }
+        for (int w = 0; w < N; ++w) {
+            const uint8_t* base = kTable ? a.src + a.stride * w + L.code_off + q0 : ptrs.codes[w] + q0;
+            uint32_t bw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = qb + tid + u * kThreads;
+                bw[u] = q < nbytes ? __ldcs(base + q) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                bad |= bw[u] & (bw[u] >> 1) & 0x55u;
+                if (kShared) {
+                    acc[u] += tab[bw[u]];
+                } else {  // codec.hpp:299-306: fp64 worker-order sum, then /N
+                    const double sd = static_cast<double>(sw[w]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t c = (bw[u] >> (2 * e)) & 3u;
+                        const double v = c == 1u ? 1.0 : (c == 2u ? -1.0 : 0.0);
+                        sm[kShared ? 0 : u][e] = __dadd_rn(sm[kShared ? 0 : u][e], __dmul_rn(sd, v));
+                    }
                 }
             }
-            const double dn = static_cast<double>(N);
-            o = make_float4(static_cast<float>(sm[0] / dn), static_cast<float>(sm[1] / dn),
-                            static_cast<float>(sm[2] / dn), static_cast<float>(sm[3] / dn));
         }
-        const uint32_t base = 4 * q;
-        if (vec_out && base + 4 <= count) {
-            __stcs(reinterpret_cast<float4*>(out + base), o);
-        } else {
-            const float ov[4] = {o.x, o.y, o.z, o.w};
-            for (int e = 0; e < 4; ++e)
-                if (base + e < count) out[base + e] = ov[e];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = qb + tid + u * kThreads;
+            if (q >= nbytes) continue;
+            float4 o;
+            if (kShared) {
+                o = make_float4(lut[acc[u] & 0xffu], lut[(acc[u] >> 8) & 0xffu],
+                                lut[(acc[u] >> 16) & 0xffu], lut[acc[u] >> 24]);
+            } else {
+                const double dn = static_cast<double>(N);
+                const int v = kShared ? 0 : u;
+                o = make_float4(static_cast<float>(sm[v][0] / dn), static_cast<float>(sm[v][1] / dn),
+                                static_cast<float>(sm[v][2] / dn), static_cast<float>(sm[v][3] / dn));
+            }
+            const uint32_t b4 = 4 * q;
+            if (vec_out && b4 + 4 <= count) {
+                __stcs(reinterpret_cast<float4*>(out + b4), o);
+            } else {
+                if (b4 + 0 < count) out[b4 + 0] = o.x;
+                if (b4 + 1 < count) out[b4 + 1] = o.y;
+                if (b4 + 2 < count) out[b4 + 2] = o.z;
+                if (b4 + 3 < count) out[b4 + 3] = o.w;
+            }
         }
         if (bad) {
-            // only real elements count (pad bits are 00 by construction)
-            const uint32_t e = (__ffs(bad) - 1) >> 1;
-            raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(ch.layer),
-                        ch.begin + base + e);
+            // locate the first corrupt element of this thread (pad bits are 00 by construction)
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = qb + tid + u * kThreads;
+                if (q >= nbytes) break;
+                for (int w = 0; w < N; ++w) {
+                    const uint8_t* base =
+                        kTable ? a.src + a.stride * w + L.code_off + q0 : ptrs.codes[w] + q0;
+                    const uint32_t b = base[q] & (base[q] >> 1) & 0x55u;
+                    if (b) {
+                        raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(ch.layer),
+                                    ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
+                        break;
+                    }
+                }
+            }
         }
     }
 }
@@ -467,7 +403,13 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkDev* chunks, uint
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
             p.global_bucketing, p.n_layers, p.n_active_layers, layers};
-    k1_stats<TableSource><<<n_chunks, kThreads, 0, st>>>(TableSource{layers, chunks}, o);
+    const TableSource src{layers, chunks};
+    switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
+        case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 2: k1_stats<TableSource, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 3: k1_stats<TableSource, 8, 2><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        default: k1_stats<TableSource, 8, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+    }
     return launch_status();
 }
 
@@ -514,8 +456,12 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkDev* chunks, uint
     if (n_chunks == 0) return cudaSuccess;
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
-    k3_decode<TableSource, true><<<n_chunks, kThreads, 0, st>>>(TableSource{layers, chunks}, a,
-                                                                  ptrs);
+    if (p.sharing)
+        k3_decode<TableSource, true, true><<<n_chunks, kThreads, 0, st>>>(
+            TableSource{layers, chunks}, a, ptrs);
+    else
+        k3_decode<TableSource, true, false><<<n_chunks, kThreads, 0, st>>>(
+            TableSource{layers, chunks}, a, ptrs);
     return launch_status();
 }
 
@@ -526,7 +472,10 @@ cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, con
     K3Args a{nullptr, 0, nullptr, scalers, p.s_imm, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
     for (int w = 0; w < p.n_workers; ++w) ptrs.codes[w] = codes[w];
-    k3_decode<SingleSource, false><<<nc, kThreads, 0, st>>>(SingleSource{L}, a, ptrs);
+    if (p.sharing)
+        k3_decode<SingleSource, false, true><<<nc, kThreads, 0, st>>>(SingleSource{L}, a, ptrs);
+    else
+        k3_decode<SingleSource, false, false><<<nc, kThreads, 0, st>>>(SingleSource{L}, a, ptrs);
     return launch_status();
 }
 

@@ -31,13 +31,26 @@ struct LayerDev {
     uint32_t key0, key1; // Philox key of RngStream(seed, *, name, worker)
     int32_t slot;        // scaler slot
     uint32_t flags;
-    uint32_t first_chunk, n_chunks;
+    uint32_t first_chunk, n_chunks;  // chunk-mode K1 partial units of this layer
+    uint32_t first_seg, n_segs;      // persistent-mode K1 partial units (segments)
 };
 
 struct ChunkDev {
     uint32_t layer;
     uint32_t count;  // elements in this chunk
     uint64_t begin;  // first element (multiple of 4, and of kChunk inside a layer)
+};
+
+// persistent kernels: a CTA owns a contiguous run of tiles (ChunkDev with
+// count <= kTileElems); a segment is the part of that run inside one layer.
+struct SegDev {
+    uint32_t layer;
+    uint32_t tile_begin, tile_end;  // [begin, end) in the plan's tile table
+    uint32_t pad;
+};
+
+struct CtaDev {
+    uint32_t seg_begin, seg_end;  // [begin, end) in the plan's segment table
 };
 
 // per-chunk clip statistics (Chan et al. mergeable moments)
@@ -79,82 +92,155 @@ __device__ __forceinline__ uint4 philox10(uint4 c, uint32_t k0, uint32_t k1) {
     return c;
 }
 
-// Philox with the counter words 1..3 fixed for a whole work item
-// (ctr1 = hi32 of the byte index, ctr2/3 = iteration). Round 1's c.z product
-// is invariant, so it is hoisted: per byte only 19 wide multiplies remain.
-struct PhiloxStream {
-    uint32_t k0, k1;   // key
-    uint32_t r1x, r1y; // round-1 outputs that do not depend on ctr0
-    uint32_t r1wk;     // ctr3 ^ k1 (round-1 z input)
-
-    __device__ __forceinline__ void init(uint32_t key0, uint32_t key1, uint32_t ctr1,
-                                         uint64_t t) {
-        k0 = key0;
-        k1 = key1;
-        const uint32_t t_lo = static_cast<uint32_t>(t), t_hi = static_cast<uint32_t>(t >> 32);
-        r1x = __umulhi(kMul1, t_lo) ^ ctr1 ^ key0;
-        r1y = kMul1 * t_lo;
-        r1wk = t_hi ^ key1;
-    }
-
-    __device__ __forceinline__ uint4 operator()(uint32_t ctr0) const {
-        uint4 c = make_uint4(r1x, r1y, __umulhi(kMul0, ctr0) ^ r1wk, kMul0 * ctr0);
-        uint32_t a = k0 + kWeyl0, b = k1 + kWeyl1;
-#pragma unroll
-        for (int r = 1; r < 10; ++r) {
-            const uint32_t hi0 = __umulhi(kMul0, c.x), lo0 = kMul0 * c.x;
-            const uint32_t hi1 = __umulhi(kMul1, c.z), lo1 = kMul1 * c.z;
-            c = make_uint4(hi1 ^ c.y ^ a, lo1, hi0 ^ c.w ^ b, lo0);
-            a += kWeyl0;
-            b += kWeyl1;
-        }
-        return c;
-    }
-};
-
 // ------------------------------------------------------ ternary decision
 // Reference (codec.hpp:161-169 after clip :121-122):
-//   mag = |clip(x)| = min(|x|, bound); p = mag / s (IEEE fp32 divide);
-//   take iff float(bits)*2^-32 < p; code = clip(x) > 0 ? 01 : 10.
-// Device: the divide is replaced by two products with a per-layer reciprocal
-// carrying a +-2^-20 relative margin (provably decisive outside it, see
-// DESIGN.md §K2); inside the margin, or for bits == 0, the exact IEEE divide
-// decides. Bit-exact with the reference for every input.
+//   mag = |clip(x)| = min(|x|, bound); p = RN(mag / s) (IEEE fp32 divide);
+//   take iff u = RN(float(bits))*2^-32 < p; code = clip(x) > 0 ? 01 : 10.
+//
+// exact_take() decides u < RN(m/s) without dividing: RN(q) > u  <=>  q > mid
+// (mid = midpoint of u and its successor), or q == mid and the successor's
+// significand is even (ties-to-even). m, s*mid are exact in fp64 (s has 24
+// significant bits, mid 25), so the test is exact for every finite input,
+// including u == 0 and subnormal quotients.
+__device__ __forceinline__ bool exact_take(float m, float s, float uf) {
+    const float u = __fmul_rn(uf, 0x1p-32f);
+    const float succ = __uint_as_float(__float_as_uint(u) + 1u);
+    const double mid = (static_cast<double>(u) + static_cast<double>(succ)) * 0.5;
+    const double t = static_cast<double>(s) * mid;
+    const double dm = static_cast<double>(m);
+    return dm > t || (dm == t && (__float_as_uint(succ) & 1u) == 0u);
+}
+
+// Fast form. Let c = bound (or s when there is no clip bound), R = RN(1/s)*2^32,
+// rl = RN(c*R*(1-2^-20)), rh = RN(c*R*(1+2^-20)), m' = sat(|x| * RN(1/c)) ~ m/c.
+//   d = uf - m'*rl  (one FFMA rounding: sign exact) :  d < 0  =>  u < p  (take)
+//   e = m'*rh - uf                                   :  e < 0  =>  u >= p (no take)
+// Every approximation above is a few 2^-24 relative roundings, well inside the
+// 2^-20 margin, so only uf in the ~2^-19-wide band (d >= 0 && e >= 0, i.e.
+// d*e >= 0) or bits == 0 needs exact_take. Valid for 2^-90 <= s <= 2^120
+// (else exact_all). The whole fast path is FP32 (FMUL.SAT/FFMA on the FMA-lite
+// pipe), leaving the integer multiplier (IMAD.WIDE, fma-heavy) to Philox.
 struct Decider {
     float bound, s;
-    float r_lo, r_hi;  // RN(1/s)*2^32*(1 -+ 2^-20)
-    bool exact_all;    // s too small for the reciprocal form
+    float ib, rl, rh;  // RN(1/c), c*R*(1 -+ 2^-20)
+    bool exact_all;
 
     __device__ __forceinline__ void init(float bound_, float s_) {
         bound = bound_;
         s = s_;
-        exact_all = !(s_ >= 0x1p-90f) || s_ > 0x1p+120f;  // keep RN(1/s)*2^32 normal and finite
+        exact_all = !(s_ >= 0x1p-90f) || s_ > 0x1p+120f;
+        const float c = bound_ < INFINITY ? bound_ : s_;
         const float r = __fmul_rn(__frcp_rn(s_), 4294967296.0f);
-        r_lo = __fmul_rn(r, 1.0f - 0x1p-20f);
-        r_hi = __fmul_rn(r, 1.0f + 0x1p-20f);
+        ib = __frcp_rn(c);
+        rl = __fmul_rn(__fmul_rn(r, c), 1.0f - 0x1p-20f);
+        rh = __fmul_rn(__fmul_rn(r, c), 1.0f + 0x1p-20f);
     }
 
-    // returns the 2-bit code of one element
-    __device__ __forceinline__ uint32_t code(float x, uint32_t bits) const {
-        const float m = fminf(fabsf(x), bound);
+    // 2-bit code for a taken element: 1 + sign (01 positive, 10 negative)
+    __device__ __forceinline__ static uint32_t sign_code(float x) {
+        return (__float_as_uint(x) >> 31) + 1u;
+    }
+
+    // fast decision, FP form: returns the 2-bit code as a float in {0, 1, 2}
+    __device__ __forceinline__ float code_fast(float x, uint32_t bits, float& amb) const {
+        const float mp = __saturatef(__fmul_rn(fabsf(x), ib));
         const float uf = __uint2float_rn(bits);
-        bool take;
-        if (!exact_all) {
-            const float a = __fmul_rn(m, r_lo);
-            const float b = __fmul_rn(m, r_hi);
-            take = uf < a;
-            const bool amb = (!take && !(uf > b)) || bits == 0u;
-            if (amb) take = __fmul_rn(uf, 0x1p-32f) < __fdiv_rn(m, s);
-        } else {
-            take = __fmul_rn(uf, 0x1p-32f) < __fdiv_rn(m, s);
-        }
-        const uint32_t sign = __float_as_uint(x) >> 31;  // taken => x != 0
-        return take ? (1u + sign) : 0u;
+        const float d = __fmaf_rn(-mp, rl, uf);
+        const float e = __fmaf_rn(mp, rh, -uf);
+        amb = fmaxf(amb, __fmul_rn(d, e));
+        // d < 0 => |d| >= 2^-47 (uf >= 1 integer, m'*rl a product of floats > 1),
+        // and a taken x has |x| >= 2^-122: both saturate to exactly 1.0
+        const float t = __saturatef(__fmul_rn(d, -0x1p126f));
+        const float sg = __saturatef(__fmul_rn(x, -0x1p126f));
+        return __fmaf_rn(t, sg, t);  // t * (1 + sign)
     }
 
+    __device__ __forceinline__ uint32_t code_exact(float x, uint32_t bits) const {
+        const float m = fminf(fabsf(x), bound);
+        return exact_take(m, s, __uint2float_rn(bits)) ? sign_code(x) : 0u;
+    }
+
+    __device__ __forceinline__ uint32_t byte_exact(float4 v, uint4 r) const {
+        return code_exact(v.x, r.x) | (code_exact(v.y, r.y) << 2) | (code_exact(v.z, r.z) << 4) |
+               (code_exact(v.w, r.w) << 6);
+    }
+
+    // fast byte as float value in [0, 255] (exact); amb >= 0 flags an
+    // ambiguous element. Lanes with bits == 0 (u == 0 corner) are caught by
+    // the caller's min(bits) == 0 test.
+    __device__ __forceinline__ float byte_fast_f(float4 v, uint4 r, float& amb) const {
+        const float c0 = code_fast(v.x, r.x, amb), c1 = code_fast(v.y, r.y, amb);
+        const float c2 = code_fast(v.z, r.z, amb), c3 = code_fast(v.w, r.w, amb);
+        return __fmaf_rn(__fmaf_rn(__fmaf_rn(c3, 4.0f, c2), 4.0f, c1), 4.0f, c0);
+    }
+
+    // float byte value -> integer (low 8 bits of the bit pattern of 2^23 + v)
+    __device__ __forceinline__ static uint32_t to_u8(float bf) {
+        return __float_as_uint(__fadd_rn(bf, 8388608.0f)) & 0xFFu;
+    }
+
+    __device__ __forceinline__ uint32_t byte_fast(float4 v, uint4 r, float& amb) const {
+        return to_u8(byte_fast_f(v, r, amb));
+    }
+
+    // one code byte (4 elements, one Philox block)
     __device__ __forceinline__ uint32_t byte(float4 v, uint4 r) const {
-        return code(v.x, r.x) | (code(v.y, r.y) << 2) | (code(v.z, r.z) << 4) |
-               (code(v.w, r.w) << 6);
+        if (!exact_all) {
+            float amb = -1.0f;
+            const uint32_t c = byte_fast(v, r, amb);
+            if (!(amb >= 0.0f) && min(min(r.x, r.y), min(r.z, r.w)) != 0u) return c;
+        }
+        return byte_exact(v, r);
+    }
+};
+
+// Four independent Philox4x32-10 blocks, round-interleaved for ILP. Round 0's
+// ctr2 product is hoisted. kRolling: derive round keys with one add per round
+// (shared by the U lanes) instead of holding 18 key registers.
+template <bool kRolling = false>
+struct Philox4 {
+    uint32_t r1x, r1y, r1wk;
+    uint32_t ka[10], kb[10];
+
+    __device__ __forceinline__ void init(uint32_t key0, uint32_t key1, uint32_t ctr1, uint64_t t) {
+        const uint32_t t_lo = static_cast<uint32_t>(t), t_hi = static_cast<uint32_t>(t >> 32);
+        r1x = __umulhi(kMul1, t_lo) ^ ctr1 ^ key0;
+        r1y = kMul1 * t_lo;
+        r1wk = t_hi ^ key1;
+        if (kRolling) {
+            ka[0] = key0;
+            kb[0] = key1;
+        } else {
+#pragma unroll
+            for (int r = 0; r < 10; ++r) {
+                ka[r] = key0 + static_cast<uint32_t>(r) * kWeyl0;
+                kb[r] = key1 + static_cast<uint32_t>(r) * kWeyl1;
+            }
+        }
+    }
+
+    template <int U>
+    __device__ __forceinline__ void operator()(const uint32_t (&ctr0)[U], uint4 (&c)[U]) const {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            c[u] = make_uint4(r1x, r1y, __umulhi(kMul0, ctr0[u]) ^ r1wk, kMul0 * ctr0[u]);
+        uint32_t a = ka[0], b = kb[0];
+#pragma unroll
+        for (int r = 1; r < 10; ++r) {
+            if (kRolling) {
+                a += kWeyl0;
+                b += kWeyl1;
+            } else {
+                a = ka[r];
+                b = kb[r];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t hi0 = __umulhi(kMul0, c[u].x), lo0 = kMul0 * c[u].x;
+                const uint32_t hi1 = __umulhi(kMul1, c[u].z), lo1 = kMul1 * c[u].z;
+                c[u] = make_uint4(hi1 ^ c[u].y ^ a, lo1, hi0 ^ c[u].w ^ b, lo0);
+            }
+        }
     }
 };
 
@@ -176,8 +262,20 @@ __device__ __forceinline__ void chan_merge(double& n, double& mean, double& m2, 
     n = nn;
 }
 
+// Barriers for block-wide phases: the whole CTA, or only the 256 consumer
+// threads of a warp-specialized CTA (named barrier 1; the producer warp never
+// joins, so __syncthreads would deadlock there).
+struct BlockBar {
+    __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+struct ConsumerBar {
+    __device__ __forceinline__ static void sync() {
+        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    }
+};
+
 // deterministic CTA reduction of (S, Q, mx) — fixed shuffle tree + fixed warp order
-template <int kWarps>
+template <int kWarps, class Bar = BlockBar>
 __device__ __forceinline__ void block_reduce_sq(double& S, double& Q, float& mx) {
     __shared__ double sh_s[kWarps], sh_q[kWarps];
     __shared__ float sh_m[kWarps];
@@ -193,7 +291,7 @@ __device__ __forceinline__ void block_reduce_sq(double& S, double& Q, float& mx)
         sh_q[warp] = Q;
         sh_m[warp] = mx;
     }
-    __syncthreads();
+    Bar::sync();
     if (threadIdx.x == 0) {
         S = sh_s[0];
         Q = sh_q[0];

@@ -19,6 +19,7 @@ struct K1Launch {
     int32_t global_bucketing;
     int32_t n_layers;
     int32_t n_active_layers;
+    int32_t variant = 0;  // chunk K1 kernel variant (TGB_K1V, A/B only)
 };
 
 struct K2Launch {
@@ -42,11 +43,24 @@ struct K3Launch {
     float s_imm = 0.0f;    // single-layer: scaler by value when scalers == nullptr
 };
 
+struct PersistLaunch {
+    const LayerDev* layers;
+    const ChunkDev* tiles;
+    const SegDev* segs;
+    const CtaDev* ctas;
+    uint32_t n_ctas;
+    int32_t variant;  // K2: 0 hoisted Philox keys, 1 rolling keys (TGB_K2V)
+};
+
+// resident CTAs for the persistent kernels (SMs x min occupancy of K1p/K2p)
+cudaError_t persistent_grid(uint32_t* ctas);
+cudaError_t launch_k1_persistent(const PersistLaunch& P, const K1Launch& p, cudaStream_t st);
+cudaError_t launch_k2_persistent(const PersistLaunch& P, const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k1_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
                             const K1Launch& p, cudaStream_t st);
-cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st);
+cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k2_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t key1,
                              uint64_t t, uint64_t rng_base, uint8_t* codes, ErrWord* err,

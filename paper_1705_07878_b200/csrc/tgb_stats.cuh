@@ -1,0 +1,152 @@
+// K1 building blocks: fp64 moment accumulation, partial emission and the
+// deterministic per-layer merge + clip/scaler epilogue.
+//
+// Reference: stddev (codec.hpp:101-112, sequential fp64 two-pass), clip bound
+// float(c*sigma) (:119), scaler = max |clip(g)| (:128-134) = min(max|g|, bound),
+// Global bucketing max over tensors (:212-216). See DESIGN.md §K1 for why the
+// parallel fp64 Chan merge reproduces the reference's float bound.
+#pragma once
+
+#include "tgb_device.cuh"
+#include "tgb/terngrad_b200.h"
+
+namespace tgb {
+
+struct K1Out {
+    Partial* partials;      // one per work unit (chunk or segment)
+    uint32_t* layer_done;   // per layer arrival counters (self-resetting)
+    uint32_t* global_done;  // arrival counter over layers (Global bucketing)
+    float* bounds;          // per layer clip bound
+    float* slots;           // scaler slots
+    ErrWord* err;
+    float clip_factor;
+    int32_t global_bucketing;
+    int32_t n_layers;
+    int32_t n_active_layers;  // layers with n > 0
+    const LayerDev* layers;   // for the Global fix-up (plan only)
+};
+
+// x - x0 in fp64 (exact for any two floats within 2^29 of each other's exponent)
+__device__ __forceinline__ void acc4(const float4 v, const double x0, double& S, double& Q,
+                                     float& mx) {
+    const double d0 = static_cast<double>(v.x) - x0, d1 = static_cast<double>(v.y) - x0;
+    const double d2 = static_cast<double>(v.z) - x0, d3 = static_cast<double>(v.w) - x0;
+    S += (d0 + d1) + (d2 + d3);
+    Q = fma(d0, d0, Q);
+    Q = fma(d1, d1, Q);
+    Q = fma(d2, d2, Q);
+    Q = fma(d3, d3, Q);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+}
+
+__device__ __forceinline__ void acc1(const float x, const double x0, double& S, double& Q,
+                                     float& mx) {
+    const double d = static_cast<double>(x) - x0;
+    S += d;
+    Q = fma(d, d, Q);
+    mx = fmaxf(mx, fabsf(x));
+}
+
+// Block-wide: reduce (S, Q, mx) of `count` elements shifted by x0, write the
+// unit's partial, count the layer's arrivals; the last arriving unit merges
+// the layer's partials [first, first + n_units) in a fixed order and writes
+// bound + scaler. Must be called by every thread of the block.
+template <class Bar = BlockBar>
+__device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const LayerDev& L,
+                                                     uint32_t layer, uint32_t unit,
+                                                     uint32_t first_unit, uint32_t n_units,
+                                                     uint64_t count, double x0, double S, double Q,
+                                                     float mx) {
+    block_reduce_sq<kThreads / 32, Bar>(S, Q, mx);
+    const uint32_t tid = threadIdx.x;
+    __shared__ bool is_last;
+    if (tid == 0) {
+        const double cn = static_cast<double>(count);
+        Partial p;
+        p.n = cn;
+        p.mean = x0 + S / cn;
+        p.m2 = Q - S * (S / cn);
+        p.mx = mx;
+        p.pad = 0;
+        o.partials[unit] = p;
+        __threadfence();
+        const uint32_t ticket = atomicAdd(&o.layer_done[layer], 1u);
+        is_last = (ticket == n_units - 1);
+    }
+    Bar::sync();
+    if (!is_last) return;
+    __threadfence();
+
+    __shared__ double sn[kThreads], smean[kThreads], sm2[kThreads];
+    __shared__ float smx[kThreads];
+    const uint32_t nc = n_units;
+    const uint32_t per = (nc + kThreads - 1) / kThreads;
+    double n = 0.0, mean = 0.0, m2 = 0.0;
+    float m = 0.0f;
+    const uint32_t lo = tid * per, hi = min(nc, lo + per);
+    for (uint32_t c = lo; c < hi; ++c) {
+        const Partial* pp = o.partials + first_unit + c;
+        const double pn = __ldcg(&pp->n), pmean = __ldcg(&pp->mean), pm2 = __ldcg(&pp->m2);
+        const float pmx = __ldcg(&pp->mx);
+        chan_merge(n, mean, m2, pn, pmean, pm2);
+        m = fmaxf(m, pmx);
+    }
+    sn[tid] = n;
+    smean[tid] = mean;
+    sm2[tid] = m2;
+    smx[tid] = m;
+    Bar::sync();
+    for (uint32_t s = 1; s < kThreads; s <<= 1) {
+        if ((tid & (2 * s - 1)) == 0) {
+            double a_n = sn[tid], a_mean = smean[tid], a_m2 = sm2[tid];
+            chan_merge(a_n, a_mean, a_m2, sn[tid + s], smean[tid + s], sm2[tid + s]);
+            sn[tid] = a_n;
+            smean[tid] = a_mean;
+            sm2[tid] = a_m2;
+            smx[tid] = fmaxf(smx[tid], smx[tid + s]);
+        }
+        Bar::sync();
+    }
+    if (tid == 0) {
+        const double fm = smean[0];
+        double fm2 = sm2[0];
+        const float fmx = smx[0];
+        float bound = INFINITY, s = 0.0f;
+        if (!isfinite(fm) || !isfinite(fm2) || !isfinite(fmx)) {
+            raise_error(o.err, TGB_E_NONFINITE, static_cast<int32_t>(layer), 0);
+            bound = 0.0f;
+            s = 0.0f;
+        } else {
+            if ((L.flags & kLayerClip) && L.n >= 2) {
+                if (fm2 < 0.0) fm2 = 0.0;
+                const double sigma = sqrt(fm2 / static_cast<double>(L.n));  // codec.hpp:111
+                bound = static_cast<float>(static_cast<double>(o.clip_factor) * sigma);  // :119
+            }
+            s = fminf(fmx, bound);  // == scaler(clip(g)) (codec.hpp:121-122, :130)
+        }
+        o.bounds[layer] = bound;
+        o.slots[L.slot] = s;
+        o.layer_done[layer] = 0u;  // self-reset for the next launch
+        if (o.global_bucketing) {
+            __threadfence();
+            const uint32_t t = atomicAdd(o.global_done, 1u);
+            if (t == static_cast<uint32_t>(o.n_active_layers) - 1) {
+                __threadfence();
+                float gs = 0.0f;  // codec.hpp:212-216
+                for (int l = 0; l < o.n_layers; ++l) {
+                    const LayerDev& Ll = o.layers[l];
+                    if (Ll.n == 0 || (Ll.flags & kLayerPassthrough)) continue;
+                    gs = fmaxf(gs, __ldcg(o.slots + Ll.slot));
+                }
+                for (int l = 0; l < o.n_layers; ++l) {
+                    const LayerDev& Ll = o.layers[l];
+                    if (Ll.n == 0 || (Ll.flags & kLayerPassthrough)) continue;
+                    o.slots[Ll.slot] = gs;
+                }
+                *o.global_done = 0u;
+            }
+        }
+    }
+}
+
+}  // namespace tgb

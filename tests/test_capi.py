@@ -87,7 +87,8 @@ def test_plan_argument_validation():
     assert L.tgb_plan_create(d, 1, C.byref(fixed), 0, 1, C.byref(h)) == \
         _lib.TGB_ERR_INVALID_ARGUMENT
     ok = _lib.CodecParams(2.5, 1, 0, 1, 0, 42, 0, 0)
-    assert L.tgb_plan_create(d, 1, C.byref(ok), 3, 2, C.byref(h)) == _lib.TGB_ERR_INVALID_ARGUMENT
+    assert L.tgb_plan_create(d, 1, C.byref(ok), 0, 0, C.byref(h)) == _lib.TGB_ERR_INVALID_ARGUMENT
+    assert L.tgb_plan_create(d, 1, C.byref(ok), 0, 65, C.byref(h)) == _lib.TGB_ERR_INVALID_ARGUMENT
 
 
 def test_push_layout():
