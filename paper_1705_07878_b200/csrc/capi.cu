@@ -88,12 +88,14 @@ struct tgb_plan {
     int32_t n_workers = 1;
     std::vector<tgb_layer_desc> desc;
     std::vector<LayerDev> h_layers;
-    std::vector<ChunkDev> h_chunks;  // K3 work items (16K elements)
+    std::vector<ChunkDev> h_chunks;   // K1/K2 work items (kChunk12 elements)
+    std::vector<ChunkDev> h_chunks3;  // K3 work items (kChunk3 elements)
     std::vector<ChunkDev> h_tiles;   // K1/K2 persistent tiles (4K elements)
     std::vector<SegDev> h_segs;
     std::vector<CtaDev> h_ctas;
     LayerDev* d_layers = nullptr;
-    ChunkDev* d_chunks = nullptr;
+    ChunkFat* d_fat = nullptr;   // K1/K2: chunk + layer copy (rebuilt on bind)
+    ChunkFat* d_fat3 = nullptr;  // K3
     ChunkDev* d_tiles = nullptr;
     SegDev* d_segs = nullptr;
     CtaDev* d_ctas = nullptr;
@@ -105,6 +107,7 @@ struct tgb_plan {
     ErrWord* d_err = nullptr;
     uint64_t push_bytes = 0, codes_offset = 0, code_bytes = 0, total = 0;
     int32_t n_slots = 0, n_active = 0;
+    uint32_t chunk12 = kChunk12;
     bool bound = false;
     bool chunk_k1 = true;  // grid-per-chunk K1 (default) vs persistent TMA ring
     bool chunk_k2 = true;
@@ -188,6 +191,18 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     // layout: [slots (one per layer)][pad to 256][codes, layer l at 16B-aligned offset][pad 256]
     P->n_slots = n_layers;
     P->codes_offset = round_up(static_cast<uint64_t>(n_layers) * sizeof(float), kAlignPush);
+    // elements per grid-per-chunk work item: K1/K2 amortise a heavier per-CTA
+    // setup over 32K elements, K3 (store-bound) prefers 16K (tools/ab_bench.py)
+    uint64_t chunk = kChunk12, chunk3 = kChunk3;
+    if (const char* m = std::getenv("TGB_CHUNK")) {  // A/B only
+        const uint64_t v = std::strtoull(m, nullptr, 10);
+        if (v >= 1024 && v % 1024 == 0) chunk = v;
+    }
+    P->chunk12 = static_cast<uint32_t>(chunk);
+    if (const char* m = std::getenv("TGB_CHUNK3")) {
+        const uint64_t v = std::strtoull(m, nullptr, 10);
+        if (v >= 1024 && v % 1024 == 0) chunk3 = v;
+    }
     uint64_t off = P->codes_offset;
     P->h_layers.resize(n_layers);
     for (int32_t l = 0; l < n_layers; ++l) {
@@ -199,14 +214,21 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
         philox_key(params->seed, layers[l].name_hash, worker, L.key0, L.key1);
         L.flags = params->clipping_enabled ? kLayerClip : 0u;
         L.first_chunk = static_cast<uint32_t>(P->h_chunks.size());
-        for (uint64_t b = 0; b < L.n; b += kChunk) {
+        for (uint64_t b = 0; b < L.n; b += chunk) {
             ChunkDev c;
             c.layer = static_cast<uint32_t>(l);
             c.begin = b;
-            c.count = static_cast<uint32_t>(std::min<uint64_t>(kChunk, L.n - b));
+            c.count = static_cast<uint32_t>(std::min<uint64_t>(chunk, L.n - b));
             P->h_chunks.push_back(c);
         }
         L.n_chunks = static_cast<uint32_t>(P->h_chunks.size()) - L.first_chunk;
+        for (uint64_t b = 0; b < L.n; b += chunk3) {
+            ChunkDev c;
+            c.layer = static_cast<uint32_t>(l);
+            c.begin = b;
+            c.count = static_cast<uint32_t>(std::min<uint64_t>(chunk3, L.n - b));
+            P->h_chunks3.push_back(c);
+        }
         for (uint64_t b = 0; b < L.n; b += kTileElems) {
             ChunkDev c;
             c.layer = static_cast<uint32_t>(l);
@@ -256,7 +278,9 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     const size_t ntl = std::max<size_t>(1, P->h_tiles.size()), nsg = std::max<size_t>(1, P->h_segs.size());
     const size_t nct = std::max<size_t>(1, P->h_ctas.size());
     bool ok = cudaMalloc(&P->d_layers, nl * sizeof(LayerDev)) == cudaSuccess &&
-              cudaMalloc(&P->d_chunks, nc * sizeof(ChunkDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_fat, nc * sizeof(ChunkFat)) == cudaSuccess &&
+              cudaMalloc(&P->d_fat3, std::max<size_t>(1, P->h_chunks3.size()) * sizeof(ChunkFat)) ==
+                  cudaSuccess &&
               cudaMalloc(&P->d_tiles, ntl * sizeof(ChunkDev)) == cudaSuccess &&
               cudaMalloc(&P->d_segs, nsg * sizeof(SegDev)) == cudaSuccess &&
               cudaMalloc(&P->d_ctas, nct * sizeof(CtaDev)) == cudaSuccess &&
@@ -281,9 +305,6 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                         cudaMemcpyHostToDevice) == cudaSuccess &&
              cudaMemcpy(P->d_ctas, P->h_ctas.data(), P->h_ctas.size() * sizeof(CtaDev),
                         cudaMemcpyHostToDevice) == cudaSuccess;
-    if (ok && !P->h_chunks.empty())
-        ok = cudaMemcpy(P->d_chunks, P->h_chunks.data(), P->h_chunks.size() * sizeof(ChunkDev),
-                        cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok && n_layers > 0)
         ok = cudaMemcpy(P->d_layers, P->h_layers.data(), n_layers * sizeof(LayerDev),
                         cudaMemcpyHostToDevice) == cudaSuccess;
@@ -301,7 +322,8 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaGetDevice(&prev);
     cudaSetDevice(P->device);
     cudaFree(P->d_layers);
-    cudaFree(P->d_chunks);
+    cudaFree(P->d_fat);
+    cudaFree(P->d_fat3);
     cudaFree(P->d_tiles);
     cudaFree(P->d_segs);
     cudaFree(P->d_ctas);
@@ -327,7 +349,7 @@ tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
     o->n_slots = P->n_slots;
     o->n_chunks = static_cast<int32_t>(P->h_chunks.size());
     o->n_workers = P->n_workers;
-    o->chunk_elems = kChunk;
+    o->chunk_elems = P->chunk12;
     return TGB_OK;
 }
 
@@ -354,6 +376,17 @@ tgb_status tgb_plan_bind(tgb_plan* P, const float* const* d_grads, float* const*
     if (nl > 0)
         TGB_CUDA(cudaMemcpy(P->d_layers, P->h_layers.data(), nl * sizeof(LayerDev),
                             cudaMemcpyHostToDevice));
+    for (int which = 0; which < 2; ++which) {
+        const std::vector<ChunkDev>& chs = which == 0 ? P->h_chunks : P->h_chunks3;
+        if (chs.empty()) continue;
+        std::vector<ChunkFat> fat(chs.size());
+        for (size_t c = 0; c < fat.size(); ++c) {
+            fat[c].ch = chs[c];
+            fat[c].L = P->h_layers[chs[c].layer];
+        }
+        TGB_CUDA(cudaMemcpy(which == 0 ? P->d_fat : P->d_fat3, fat.data(),
+                            fat.size() * sizeof(ChunkFat), cudaMemcpyHostToDevice));
+    }
     P->bound = true;
     return TGB_OK;
 }
@@ -378,7 +411,7 @@ tgb_status tgb_stats(tgb_plan* P, void* stream) {
                            static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
     k.variant = P->k1_variant;
     if (P->chunk_k1)
-        TGB_CUDA(launch_k1_table(P->d_layers, P->d_chunks,
+        TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat,
                                  static_cast<uint32_t>(P->h_chunks.size()), k, st));
     else
         TGB_CUDA(launch_k1_persistent(pl, k, st));
@@ -390,10 +423,11 @@ tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     K2Launch k{P->d_push, reinterpret_cast<const float*>(P->d_push), P->d_bounds, P->d_err, t, 1};
+    k.variant = P->k2_variant;
     const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
                            static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
     if (P->chunk_k2)
-        TGB_CUDA(launch_k2_table(P->d_layers, P->d_chunks,
+        TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat,
                                  static_cast<uint32_t>(P->h_chunks.size()), k, st));
     else
         TGB_CUDA(launch_k2_persistent(pl, k, st));
@@ -435,7 +469,7 @@ tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_worke
     P->last = st;
     K3Launch k{d_src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
                1.0f / static_cast<float>(n_workers), P->d_err};
-    TGB_CUDA(launch_k3_table(P->d_layers, P->d_chunks, static_cast<uint32_t>(P->h_chunks.size()), k,
+    TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3, static_cast<uint32_t>(P->h_chunks3.size()), k,
                              st));
     return TGB_OK;
 }
@@ -582,7 +616,7 @@ tgb_status tgb_layer_ternarize(const float* d_g, uint64_t n, float s, uint64_t s
     L.key1 = k1;
     L.slot = 0;
     L.flags = layer_vec_flags(d_g, nullptr) & kLayerVecIn;
-    K2Launch k{d_codes, nullptr, nullptr, S->err, t, 0, s, rng_base >> 2};
+    K2Launch k{d_codes, nullptr, nullptr, S->err, t, 0, 0, s, rng_base >> 2};
     TGB_CUDA(launch_k2_single(L, k, st));
     return TGB_OK;
 }

@@ -22,11 +22,11 @@ namespace tgb {
 // A "source" maps blockIdx.x to (chunk, layer). Table: plan tables in HBM.
 // Single: one layer passed by value (per-layer API), chunks computed.
 struct TableSource {
-    const LayerDev* layers;
-    const ChunkDev* chunks;
+    const ChunkFat* fat;
     __device__ __forceinline__ void get(uint32_t b, ChunkDev& ch, LayerDev& L) const {
-        ch = chunks[b];
-        L = layers[ch.layer];
+        const ChunkFat* f = fat + b;
+        ch = f->ch;
+        L = f->L;
     }
 };
 
@@ -96,8 +96,8 @@ struct K2Args {
     uint64_t rng_q0;     // per-layer API: rng_base / 4 added to the Philox counter
 };
 
-template <class Src>
-__global__ void __launch_bounds__(kThreads, 3) k2_ternarize(Src src, K2Args a) {
+template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kPipe = false>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
     ChunkDev ch;
     LayerDev L;
@@ -123,16 +123,59 @@ __global__ void __launch_bounds__(kThreads, 3) k2_ternarize(Src src, K2Args a) {
     Decider dec;
     dec.init(bound, s);
     const uint64_t qg = q0 + a.rng_q0;  // Philox counter of this chunk's first byte
-    Philox4<> ph;
+    Philox4<kRolling> ph;
     ph.init(L.key0, L.key1, static_cast<uint32_t>(qg >> 32), a.t);
     const uint32_t qbase = static_cast<uint32_t>(qg);
 
     const uint32_t nfull = count >> 2;  // bytes whose 4 elements all exist
     uint32_t q = tid;
     float bad_mag = 0.0f;  // max clipped |x| seen (per-layer API check: mag > s)
+    if (kPipe && (L.flags & kLayerVecIn) && q + (U - 1) * kThreads < nfull) {
+        // software-pipelined: loads + Philox of iteration i+1 are issued in the
+        // same basic block as the decisions of iteration i, so the integer
+        // multiplier (Philox) and the FP32 pipes (decisions) overlap per warp
+        const float4* g4 = reinterpret_cast<const float4*>(g);
+        float4 v[U];
+        uint4 r[U];
+        uint32_t ctr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + q + u * kThreads);
+#pragma unroll
+        for (int u = 0; u < U; ++u) ctr[u] = qbase + q + u * kThreads;
+        ph(ctr, r);
+        for (;;) {
+            const uint32_t qn = q + U * kThreads;
+            const bool more = qn + (U - 1) * kThreads < nfull;
+            float4 vn[U];
+            uint4 rn[U];
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) vn[u] = __ldcs(g4 + qn + u * kThreads);
+#pragma unroll
+                for (int u = 0; u < U; ++u) ctr[u] = qbase + qn + u * kThreads;
+                ph(ctr, rn);
+            }
+            uint32_t byte[U];
+            float amb = -1.0f;
+#pragma unroll
+            for (int u = 0; u < U; ++u) byte[u] = dec.byte_fast(v[u], r[u], amb);
+            if (amb >= 0.0f || dec.exact_all) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) codes[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
+            q = qn;
+            if (!more) break;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = vn[u];
+                r[u] = rn[u];
+            }
+        }
+    }
     if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
-        constexpr int U = 4;
         for (; q + (U - 1) * kThreads < nfull; q += U * kThreads) {
             float4 v[U];
             uint32_t ctr[U];
@@ -144,13 +187,11 @@ __global__ void __launch_bounds__(kThreads, 3) k2_ternarize(Src src, K2Args a) {
             ph(ctr, r);
             uint32_t byte[U];
             float amb = -1.0f;
-            uint32_t zmin = 0xFFFFFFFFu;  // == 0 iff some lane's bits == 0 (u == 0 corner)  // == 0 if any lane's bits == 0 (u == 0 corner)
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 byte[u] = dec.byte_fast(v[u], r[u], amb);
-                zmin = min(zmin, min(min(r[u].x, r[u].y), min(r[u].z, r[u].w)));
             }
-            if (amb >= 0.0f || zmin == 0u || dec.exact_all) {  // rare: redo these bytes exactly
+            if (amb >= 0.0f || dec.exact_all) {  // rare: redo these bytes exactly
 #pragma unroll
                 for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
             }
@@ -398,12 +439,12 @@ k_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k0, uint64_t n, ui
 // ============================================================ launchers
 static inline cudaError_t launch_status() { return cudaGetLastError(); }
 
-cudaError_t launch_k1_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K1Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
             p.global_bucketing, p.n_layers, p.n_active_layers, layers};
-    const TableSource src{layers, chunks};
+    const TableSource src{chunks};
     switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
         case 2: k1_stats<TableSource, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
@@ -425,11 +466,22 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
     return launch_status();
 }
 
-cudaError_t launch_k2_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0};
-    k2_ternarize<TableSource><<<n_chunks, kThreads, 0, st>>>(TableSource{layers, chunks}, a);
+    const TableSource src{chunks};
+    switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x unroll x occupancy
+        case 1: k2_ternarize<TableSource, true, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 2: k2_ternarize<TableSource, true, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 3: k2_ternarize<TableSource, false, 2, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 4: k2_ternarize<TableSource, true, 8, 2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 5: k2_ternarize<TableSource, true, 2, 5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 6: k2_ternarize<TableSource, false, 2, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 7: k2_ternarize<TableSource, false, 4, 2, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 8: k2_ternarize<TableSource, true, 2, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        default: k2_ternarize<TableSource, false, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+    }
     return launch_status();
 }
 
@@ -451,17 +503,17 @@ cudaError_t launch_k2_offset(const float* g, uint64_t n, float s, uint32_t key0,
     return launch_status();
 }
 
-cudaError_t launch_k3_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K3Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
     if (p.sharing)
         k3_decode<TableSource, true, true><<<n_chunks, kThreads, 0, st>>>(
-            TableSource{layers, chunks}, a, ptrs);
+            TableSource{chunks}, a, ptrs);
     else
         k3_decode<TableSource, true, false><<<n_chunks, kThreads, 0, st>>>(
-            TableSource{layers, chunks}, a, ptrs);
+            TableSource{chunks}, a, ptrs);
     return launch_status();
 }
 

@@ -222,13 +222,11 @@ __global__ void __launch_bounds__(kBlock, 3) k2_persistent(PersistTables T, K2PA
             R.release(i);
             uint32_t byte[U];
             float amb = -1.0f;
-            uint32_t zmin = 0xFFFFFFFFu;  // == 0 iff some lane's bits == 0 (u == 0 corner)
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 byte[u] = dec.byte_fast(v[u], r[u], amb);
-                zmin = min(zmin, min(min(r[u].x, r[u].y), min(r[u].z, r[u].w)));
             }
-            if (amb >= 0.0f || zmin == 0u || dec.exact_all) {
+            if (amb >= 0.0f || dec.exact_all) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
             }

@@ -14,7 +14,9 @@
 namespace tgb {
 
 constexpr int kThreads = 256;       // CTA size of every streaming kernel
-constexpr uint32_t kChunk = 16384;  // elements per work item (multiple of 16)
+constexpr uint32_t kChunk = 16384;    // per-layer API work item (elements, multiple of 16)
+constexpr uint32_t kChunk12 = 32768;  // plan K1/K2 work item
+constexpr uint32_t kChunk3 = 16384;   // plan K3 work item
 constexpr int kMaxWorkers = 64;     // decode LUT capacity (2N+1 entries)
 
 // layer flags (device)
@@ -39,6 +41,14 @@ struct ChunkDev {
     uint32_t layer;
     uint32_t count;  // elements in this chunk
     uint64_t begin;  // first element (multiple of 4, and of kChunk inside a layer)
+};
+
+// self-contained work item of the grid-per-chunk kernels: the chunk plus a
+// copy of its layer descriptor, fetched in one round trip (5 x LDG.128)
+// instead of the chunk -> layer dependent chain
+struct ChunkFat {
+    LayerDev L;
+    ChunkDev ch;
 };
 
 // persistent kernels: a CTA owns a contiguous run of tiles (ChunkDev with
@@ -112,17 +122,18 @@ __device__ __forceinline__ bool exact_take(float m, float s, float uf) {
 }
 
 // Fast form. Let c = bound (or s when there is no clip bound), R = RN(1/s)*2^32,
-// rl = RN(c*R*(1-2^-20)), rh = RN(c*R*(1+2^-20)), m' = sat(|x| * RN(1/c)) ~ m/c.
+// rl = RN(c*R*(1-2^-20)), dr = RN(c*R*2^-19), m' = sat(|x| * RN(1/c)) ~ m/c.
 //   d = uf - m'*rl  (one FFMA rounding: sign exact) :  d < 0  =>  u < p  (take)
-//   e = m'*rh - uf                                   :  e < 0  =>  u >= p (no take)
-// Every approximation above is a few 2^-24 relative roundings, well inside the
-// 2^-20 margin, so only uf in the ~2^-19-wide band (d >= 0 && e >= 0, i.e.
-// d*e >= 0) or bits == 0 needs exact_take. Valid for 2^-90 <= s <= 2^120
-// (else exact_all). The whole fast path is FP32 (FMUL.SAT/FFMA on the FMA-lite
-// pipe), leaving the integer multiplier (IMAD.WIDE, fma-heavy) to Philox.
+// and d >= 0 decides "no take" unless uf lies in the margin band, which is
+// contained in |d| <= m'*dr (z = m'*dr - |d| >= 0). Every approximation is a
+// few 2^-24 relative roundings, well inside the 2^-20 margin, so only z >= 0
+// (probability ~2^-18) or bits == 0 (uf == 0, flagged through -uf) needs
+// exact_take. Valid for 2^-90 <= s <= 2^120 (else exact_all). The fast path is
+// pure FP32 (FMUL.SAT/FFMA/FMNMX3), leaving the integer multiplier (IMAD.WIDE,
+// fma-heavy) to Philox.
 struct Decider {
     float bound, s;
-    float ib, rl, rh;  // RN(1/c), c*R*(1 -+ 2^-20)
+    float ib, rl, dr;  // RN(1/c), c*R*(1-2^-20), c*R*2^-19
     bool exact_all;
 
     __device__ __forceinline__ void init(float bound_, float s_) {
@@ -130,10 +141,10 @@ struct Decider {
         s = s_;
         exact_all = !(s_ >= 0x1p-90f) || s_ > 0x1p+120f;
         const float c = bound_ < INFINITY ? bound_ : s_;
-        const float r = __fmul_rn(__frcp_rn(s_), 4294967296.0f);
+        const float rc = __fmul_rn(__fmul_rn(__frcp_rn(s_), 4294967296.0f), c);
         ib = __frcp_rn(c);
-        rl = __fmul_rn(__fmul_rn(r, c), 1.0f - 0x1p-20f);
-        rh = __fmul_rn(__fmul_rn(r, c), 1.0f + 0x1p-20f);
+        rl = __fmul_rn(rc, 1.0f - 0x1p-20f);
+        dr = __fmul_rn(rc, 0x1p-19f);
     }
 
     // 2-bit code for a taken element: 1 + sign (01 positive, 10 negative)
@@ -141,13 +152,14 @@ struct Decider {
         return (__float_as_uint(x) >> 31) + 1u;
     }
 
-    // fast decision, FP form: returns the 2-bit code as a float in {0, 1, 2}
+    // fast decision, FP form: returns the 2-bit code as a float in {0, 1, 2};
+    // amb = max(amb, z, -uf) >= 0 flags "needs the exact test"
     __device__ __forceinline__ float code_fast(float x, uint32_t bits, float& amb) const {
         const float mp = __saturatef(__fmul_rn(fabsf(x), ib));
         const float uf = __uint2float_rn(bits);
         const float d = __fmaf_rn(-mp, rl, uf);
-        const float e = __fmaf_rn(mp, rh, -uf);
-        amb = fmaxf(amb, __fmul_rn(d, e));
+        const float z = __fmaf_rn(mp, dr, -fabsf(d));
+        amb = fmaxf(amb, fmaxf(z, -uf));
         // d < 0 => |d| >= 2^-47 (uf >= 1 integer, m'*rl a product of floats > 1),
         // and a taken x has |x| >= 2^-122: both saturate to exactly 1.0
         const float t = __saturatef(__fmul_rn(d, -0x1p126f));
@@ -165,9 +177,8 @@ struct Decider {
                (code_exact(v.w, r.w) << 6);
     }
 
-    // fast byte as float value in [0, 255] (exact); amb >= 0 flags an
-    // ambiguous element. Lanes with bits == 0 (u == 0 corner) are caught by
-    // the caller's min(bits) == 0 test.
+    // fast byte as float value in [0, 255] (exact); amb >= 0 flags an element
+    // that needs the exact test (margin band, or bits == 0).
     __device__ __forceinline__ float byte_fast_f(float4 v, uint4 r, float& amb) const {
         const float c0 = code_fast(v.x, r.x, amb), c1 = code_fast(v.y, r.y, amb);
         const float c2 = code_fast(v.z, r.z, amb), c3 = code_fast(v.w, r.w, amb);
@@ -188,7 +199,7 @@ struct Decider {
         if (!exact_all) {
             float amb = -1.0f;
             const uint32_t c = byte_fast(v, r, amb);
-            if (!(amb >= 0.0f) && min(min(r.x, r.y), min(r.z, r.w)) != 0u) return c;
+            if (!(amb >= 0.0f)) return c;
         }
         return byte_exact(v, r);
     }

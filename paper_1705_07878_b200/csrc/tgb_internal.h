@@ -29,6 +29,7 @@ struct K2Launch {
     ErrWord* err;
     uint64_t t;
     int32_t reverse;
+    int32_t variant = 0;   // chunk K2 kernel variant (TGB_K2V, A/B only)
     float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
     uint64_t rng_q0 = 0;   // single-layer: rng_base / 4
 };
@@ -56,16 +57,16 @@ struct PersistLaunch {
 cudaError_t persistent_grid(uint32_t* ctas);
 cudaError_t launch_k1_persistent(const PersistLaunch& P, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_persistent(const PersistLaunch& P, const K2Launch& p, cudaStream_t st);
-cudaError_t launch_k1_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K1Launch& p, cudaStream_t st);
-cudaError_t launch_k2_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k2_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t key1,
                              uint64_t t, uint64_t rng_base, uint8_t* codes, ErrWord* err,
                              cudaStream_t st);
-cudaError_t launch_k3_table(const LayerDev* layers, const ChunkDev* chunks, uint32_t n_chunks,
+cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K3Launch& p, cudaStream_t st);
 cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, const float* scalers,
                              const K3Launch& p, cudaStream_t st);

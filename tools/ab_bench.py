@@ -28,6 +28,8 @@ for m in modes:
     os.environ["TGB_K1"], os.environ["TGB_K2"] = k1m, k2m
     os.environ["TGB_K2V"] = parts[2] if len(parts) > 2 else "0"
     os.environ["TGB_K1V"] = parts[3] if len(parts) > 3 else "0"
+    os.environ["TGB_CHUNK"] = parts[4] if len(parts) > 4 else "32768"
+    os.environ["TGB_CHUNK3"] = parts[5] if len(parts) > 5 else "16384"
     w = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
                       device=dev)
     g = torch.Generator(device=dev).manual_seed(1)
