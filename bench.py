@@ -225,7 +225,9 @@ def run_b200(args):
     names = [n for n, _ in layers]
     shapes = [s for _, s in layers]
     cfg = tg.CodecConfig(seed=42)
-    sw = tg.SyncWorker(names, shapes, cfg, rank=rank, world_size=ws, comm=comm, device=dev)
+    fused = os.environ.get("TGB_EXCHANGE", "fused") != "nccl"
+    sw = tg.SyncWorker(names, shapes, cfg, rank=rank, world_size=ws, comm=comm, device=dev,
+                       fused=fused)
     ns = sw.ns
     n = sum(ns)
     plan = sw.plan
@@ -249,10 +251,10 @@ def run_b200(args):
         if ev is not None:
             ev[2].record(stream)
         if N > 1:
-            plan.sync(comm)
+            plan.sync(comm)  # fused path: device barrier (codes already pushed by K2)
         if ev is not None:
             ev[3].record(stream)
-        plan.decode_average(plan.gathered if N > 1 else plan.push, N)
+        plan.decode_average(None, N)
         if ev is not None:
             ev[4].record(stream)
 
@@ -381,15 +383,20 @@ def run_b200(args):
                           "K3_decode": k3_ms},
             "kernels": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
-            "gpu_launches": 3 * K,
-            "gpu_launches_note": "K1+K2+K3 per step (own kernels); NCCL allgather adds "
-                                 "1 library kernel per step when N > 1",
+            "gpu_launches": (3 if N == 1 else 4) * K,
+            "gpu_launches_note": "own kernels per step: K1 + K2 + K3, plus the peer-flag barrier "
+                                 "when N > 1 (codes move inside K2 as NVLink peer stores); with "
+                                 "TGB_EXCHANGE=nccl the barrier is an NCCL allgather instead",
+            "exchange": ("fused NVLink peer stores in K2 + device barrier" if N > 1 and fused
+                         else ("NCCL allgather" if N > 1 else "none (N=1)")),
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    barrier()  # fused exchange: no rank frees a gather buffer a peer may still write
     sw.plan.close()
+    barrier()
     if comm is not None:
         comm.close()
     if ws > 1:

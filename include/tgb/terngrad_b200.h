@@ -47,6 +47,7 @@ typedef enum tgb_status {
 #define TGB_E_SCALER_BELOW_MAX 0x2u /* "ternarize: scaler <s> below max |g| in <name>" :163-165 */
 #define TGB_E_S0_NONZERO 0x4u       /* "ternarize: s=0 but gradient has nonzero element" :155-158 */
 #define TGB_E_CORRUPT_CODE 0x8u     /* "corrupt ternary code 11 in block <name> at element <k>" :42-44 */
+#define TGB_E_PEER_TIMEOUT 0x10u    /* fused exchange: a peer never reached the barrier (index = peer) */
 
 typedef struct tgb_error {
     uint32_t flags;
@@ -146,7 +147,17 @@ tgb_status tgb_sync(tgb_plan* plan, tgb_comm* comm, void* stream);
  * average (codec.hpp:281-307) == decode_pull(aggregate) (wire.hpp:206-228). */
 tgb_status tgb_decode_average(tgb_plan* plan, const uint8_t* d_src, int32_t n_workers,
                               void* stream);
-/* the whole worker step: K1 -> [allreduce] -> K2 -> allgather -> K3.
+/* Fused exchange (replaces tgb_sync inside tgb_step): map every rank's gather
+ * buffers into this process (CUDA IPC over NVLink/NVSwitch; handles exchanged
+ * with one NCCL allgather). Afterwards K1/K2 store this rank's scalers and
+ * packed codes directly into every peer's gather buffer, a device flag barrier
+ * orders the step, and K3 decodes from local HBM: no allgather launch and the
+ * NVLink traffic overlaps K2. Collective: every rank calls it once. */
+tgb_status tgb_plan_attach_peers(tgb_plan* plan, tgb_comm* comm);
+/* device pointers of the push area written by the last step (own scaler slots
+ * + codes) and of the gather buffer (n_workers push areas) the last K3 read */
+tgb_status tgb_plan_last_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_gathered);
+/* the whole worker step: K1 -> [allreduce] -> K2 -> exchange -> K3.
  * comm may be NULL when n_workers == 1. */
 tgb_status tgb_step(tgb_plan* plan, tgb_comm* comm, uint64_t t, void* stream);
 /* synchronises the plan's last stream, reads and clears the error word */

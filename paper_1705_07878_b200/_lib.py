@@ -25,6 +25,7 @@ TGB_E_NONFINITE = 0x1
 TGB_E_SCALER_BELOW_MAX = 0x2
 TGB_E_S0_NONZERO = 0x4
 TGB_E_CORRUPT_CODE = 0x8
+TGB_E_PEER_TIMEOUT = 0x10
 
 TGB_LAYER_PASSTHROUGH = 0x1
 TGB_BUCKET_PER_TENSOR, TGB_BUCKET_GLOBAL, TGB_BUCKET_FIXED = 0, 1, 2
@@ -37,6 +38,7 @@ EXPORTS = [
     "tgb_plan_create", "tgb_plan_destroy", "tgb_plan_get_info", "tgb_plan_layer_layout",
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_check",
+    "tgb_plan_attach_peers", "tgb_plan_last_buffers",
     "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
     "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
     "tgb_layer_average", "tgb_rng_bits", "tgb_layer_check",
@@ -94,6 +96,8 @@ def _declare(L):
         "tgb_decode_average": (S, [_vp, _vp, _i32, _vp]),
         "tgb_step": (S, [_vp, _vp, _u64, _vp]),
         "tgb_check": (S, [_vp, C.POINTER(Error)]),
+        "tgb_plan_attach_peers": (S, [_vp, _vp]),
+        "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_comm_unique_id": (S, [C.c_char_p]),
         "tgb_comm_init": (S, [C.c_char_p, _i32, _i32, C.POINTER(_vp)]),
         "tgb_comm_destroy": (None, [_vp]),

@@ -103,7 +103,14 @@ struct tgb_plan {
     uint32_t* d_counters = nullptr;  // n_layers layer_done + 1 global_done
     float* d_bounds = nullptr;
     uint8_t* d_push = nullptr;
-    uint8_t* d_gathered = nullptr;
+    uint8_t* d_gathered = nullptr;  // N > 1: parity-0 gather buffer inside d_ipc
+    // N > 1: one IPC-shareable allocation [gather parity 0][gather parity 1][flags]
+    uint8_t* d_ipc = nullptr;
+    uint64_t flags_off = 0;
+    uint8_t* peer_ipc[kMaxPeers] = {};  // every rank's d_ipc mapped here (self = d_ipc)
+    bool attached = false;
+    int32_t rank = 0;
+    uint64_t epoch = 0;  // attached: steps begun (barrier value); parity = epoch & 1
     ErrWord* d_err = nullptr;
     uint64_t push_bytes = 0, codes_offset = 0, code_bytes = 0, total = 0;
     int32_t n_slots = 0, n_active = 0;
@@ -289,9 +296,14 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
               cudaMalloc(&P->d_bounds, nl * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&P->d_push, P->push_bytes) == cudaSuccess &&
               cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess;
-    if (ok && n_workers > 1)
-        ok = cudaMalloc(&P->d_gathered, P->push_bytes * static_cast<uint64_t>(n_workers)) ==
-             cudaSuccess;
+    if (ok && n_workers > 1) {
+        const uint64_t g = P->push_bytes * static_cast<uint64_t>(n_workers);
+        P->flags_off = 2 * g;
+        const uint64_t bytes = P->flags_off + round_up(kMaxPeers * sizeof(uint64_t), kAlignPush);
+        ok = cudaMalloc(&P->d_ipc, bytes) == cudaSuccess &&
+             cudaMemset(P->d_ipc, 0, bytes) == cudaSuccess;
+        P->d_gathered = P->d_ipc;
+    }
     const std::vector<float> inf_bounds(nl, INFINITY);  // empty layers: no clip (codec.hpp:118)
     ok = ok && cudaMemset(P->d_counters, 0, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
          cudaMemset(P->d_push, 0, P->push_bytes) == cudaSuccess &&
@@ -331,7 +343,10 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaFree(P->d_counters);
     cudaFree(P->d_bounds);
     cudaFree(P->d_push);
-    cudaFree(P->d_gathered);
+    if (P->attached)
+        for (int p = 0; p < P->n_workers; ++p)
+            if (p != P->rank && P->peer_ipc[p]) cudaIpcCloseMemHandle(P->peer_ipc[p]);
+    cudaFree(P->d_ipc);
     cudaFree(P->d_err);
     cudaSetDevice(prev);
     delete P;
@@ -399,18 +414,40 @@ tgb_status tgb_plan_buffers(tgb_plan* P, uint8_t** d_push, uint8_t** d_gathered,
     return TGB_OK;
 }
 
+// attached plans: this rank's push area in rank p's gather buffer of the
+// current parity
+static inline uint8_t* push_area(const tgb_plan* P, int p) {
+    const uint64_t g = P->push_bytes * static_cast<uint64_t>(P->n_workers);
+    return P->peer_ipc[p] + (P->epoch & 1u) * g + static_cast<uint64_t>(P->rank) * P->push_bytes;
+}
+static inline uint8_t* own_push(const tgb_plan* P) {
+    return P->attached ? push_area(P, P->rank) : P->d_push;
+}
+static inline uint8_t* cur_gathered(const tgb_plan* P) {
+    if (P->attached)
+        return P->d_ipc + (P->epoch & 1u) * P->push_bytes * static_cast<uint64_t>(P->n_workers);
+    return P->n_workers > 1 ? P->d_gathered : P->d_push;
+}
+
 tgb_status tgb_stats(tgb_plan* P, void* stream) {
     if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
+    if (P->attached) ++P->epoch;  // a step begins: flip the gather-buffer parity
     const int32_t nl = static_cast<int32_t>(P->desc.size());
     K1Launch k{P->d_partials, P->d_counters, P->d_counters + nl, P->d_bounds,
-               reinterpret_cast<float*>(P->d_push), P->d_err, P->p.clip_factor,
+               reinterpret_cast<float*>(own_push(P)), P->d_err, P->p.clip_factor,
                P->p.bucketing == TGB_BUCKET_GLOBAL, nl, P->n_active};
+    if (P->attached) {  // scalers also land in every peer's gather buffer
+        k.push.n = 0;
+        for (int p = 0; p < P->n_workers; ++p)
+            if (p != P->rank) k.push.base[k.push.n++] = push_area(P, p);
+        k.push.remote = 1;
+    }
     const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
                            static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
     k.variant = P->k1_variant;
-    if (P->chunk_k1)
+    if (P->chunk_k1 || P->attached)
         TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat,
                                  static_cast<uint32_t>(P->h_chunks.size()), k, st));
     else
@@ -422,11 +459,18 @@ tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
     if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
-    K2Launch k{P->d_push, reinterpret_cast<const float*>(P->d_push), P->d_bounds, P->d_err, t, 1};
+    uint8_t* own = own_push(P);
+    K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.variant = P->k2_variant;
+    if (const char* m = std::getenv("TGB_STREAM")) k.stream_blocks = std::atoi(m);
+    if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
+        for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
+        k.dst.n = P->n_workers;
+        k.dst.remote = 1;
+    }
     const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
                            static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
-    if (P->chunk_k2)
+    if (P->chunk_k2 || P->attached)
         TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat,
                                  static_cast<uint32_t>(P->h_chunks.size()), k, st));
     else
@@ -446,7 +490,7 @@ tgb_status tgb_share_scalers(tgb_plan* P, tgb_comm* C, void* stream) {
     if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
-    float* slots = reinterpret_cast<float*>(P->d_push);
+    float* slots = reinterpret_cast<float*>(own_push(P));
     TGB_NCCL(ncclAllReduce(slots, slots, static_cast<size_t>(P->n_slots), ncclFloat, ncclMax,
                            C->comm, st));
     return TGB_OK;
@@ -455,16 +499,26 @@ tgb_status tgb_share_scalers(tgb_plan* P, tgb_comm* C, void* stream) {
 tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     if (P->n_workers == 1) return TGB_OK;
-    if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
+    if (P->attached) {  // data already moved by K1/K2: only order the step
+        PeerFlags f{};
+        for (int p = 0; p < P->n_workers; ++p)
+            f.remote[p] = reinterpret_cast<uint64_t*>(P->peer_ipc[p] + P->flags_off) + P->rank;
+        f.local = reinterpret_cast<uint64_t*>(P->d_ipc + P->flags_off);
+        f.n = P->n_workers;
+        TGB_CUDA(launch_peer_barrier(f, P->epoch, P->d_err, st));
+        return TGB_OK;
+    }
+    if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
     TGB_NCCL(ncclAllGather(P->d_push, P->d_gathered, P->push_bytes, ncclUint8, C->comm, st));
     return TGB_OK;
 }
 
 tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_workers, void* stream) {
-    if (!P || !P->bound || !d_src || n_workers < 1 || n_workers > kMaxWorkers)
+    if (!P || !P->bound || n_workers < 1 || n_workers > kMaxWorkers)
         return TGB_ERR_INVALID_ARGUMENT;
+    if (!d_src) d_src = cur_gathered(P);  // NULL: this step's gather buffer
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     K3Launch k{d_src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
@@ -487,9 +541,50 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
     if (P->n_workers > 1) {
         s = tgb_sync(P, C, stream);
         if (s != TGB_OK) return s;
-        return tgb_decode_average(P, P->d_gathered, P->n_workers, stream);
     }
-    return tgb_decode_average(P, P->d_push, 1, stream);
+    return tgb_decode_average(P, nullptr, P->n_workers, stream);
+}
+
+tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {
+    if (!P || !C) return TGB_ERR_INVALID_ARGUMENT;
+    if (P->n_workers == 1) return TGB_OK;
+    if (C->nranks != P->n_workers || C->rank != P->worker || P->n_workers > kMaxPeers)
+        return TGB_ERR_INVALID_ARGUMENT;
+    if (P->attached) return TGB_OK;
+    cudaIpcMemHandle_t h;
+    TGB_CUDA(cudaIpcGetMemHandle(&h, P->d_ipc));
+    const int N = P->n_workers;
+    std::vector<cudaIpcMemHandle_t> all(N);
+    uint8_t* d_tmp = nullptr;
+    TGB_CUDA(cudaMalloc(&d_tmp, sizeof(cudaIpcMemHandle_t) * (N + 1)));
+    TGB_CUDA(cudaMemcpy(d_tmp, &h, sizeof(h), cudaMemcpyHostToDevice));
+    const ncclResult_t r = ncclAllGather(d_tmp, d_tmp + sizeof(h), sizeof(h), ncclUint8, C->comm,
+                                         nullptr);
+    cudaError_t e = cudaStreamSynchronize(nullptr);
+    if (r == ncclSuccess && e == cudaSuccess)
+        e = cudaMemcpy(all.data(), d_tmp + sizeof(h), sizeof(h) * N, cudaMemcpyDeviceToHost);
+    cudaFree(d_tmp);
+    if (r != ncclSuccess) return TGB_ERR_NCCL;
+    TGB_CUDA(e);
+    P->rank = C->rank;
+    for (int p = 0; p < N; ++p) {
+        if (p == P->rank) {
+            P->peer_ipc[p] = P->d_ipc;
+            continue;
+        }
+        void* ptr = nullptr;
+        TGB_CUDA(cudaIpcOpenMemHandle(&ptr, all[p], cudaIpcMemLazyEnablePeerAccess));
+        P->peer_ipc[p] = static_cast<uint8_t*>(ptr);
+    }
+    P->attached = true;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_last_buffers(tgb_plan* P, uint8_t** d_push, uint8_t** d_gathered) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    if (d_push) *d_push = own_push(P);
+    if (d_gathered) *d_gathered = cur_gathered(P);
+    return TGB_OK;
 }
 
 tgb_status tgb_check(tgb_plan* P, tgb_error* out) {

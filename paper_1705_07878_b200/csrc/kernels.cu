@@ -94,10 +94,32 @@ struct K2Args {
     int32_t check;       // per-layer API: raise mag > s / s == 0 errors
     float s_imm;         // per-layer API: scaler by value (slots == nullptr)
     uint64_t rng_q0;     // per-layer API: rng_base / 4 added to the Philox counter
+    PeerPush dst;        // plan: code destinations (n == 0: just `push`)
+    int32_t stream_blocks = 0;  // remote dst: write each 1 KB block as soon as it is coded (A/B: slower)
 };
 
-template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kPipe = false>
+// Chunk codes are staged in shared memory, then written with 16-byte stores to
+// every destination: the rank's own push area and, with peers attached, the
+// same offset of every peer's gathered buffer over NVLink (the allgather is
+// fused into K2 and overlaps its Philox-bound compute).
+constexpr uint32_t kStageBytes = kChunk12 / 4;
+
+__device__ __forceinline__ void copy_out(const uint8_t* stage, uint8_t* dst, uint32_t nbytes) {
+    const uint32_t tid = threadIdx.x;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        const uint32_t n16 = nbytes >> 4;
+        const uint4* s4 = reinterpret_cast<const uint4*>(stage);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (uint32_t i = tid; i < n16; i += kThreads) d4[i] = s4[i];
+        for (uint32_t i = (n16 << 4) + tid; i < nbytes; i += kThreads) dst[i] = stage[i];
+    } else {
+        for (uint32_t i = tid; i < nbytes; i += kThreads) dst[i] = stage[i];
+    }
+}
+
+template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
+    __shared__ __align__(16) uint8_t stage[kStageBytes];
     const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
     ChunkDev ch;
     LayerDev L;
@@ -107,19 +129,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
     const uint64_t q0 = ch.begin >> 2;  // byte index of this chunk inside the layer
-    uint8_t* codes = a.push + L.code_off + q0;
     const float* g = L.g + ch.begin;
     const uint32_t tid = threadIdx.x;
 
-    if (s == 0.0f) {  // codec.hpp:155-159
-        for (uint32_t q = tid; q < nbytes; q += kThreads) codes[q] = 0;
-        if (a.check)
-            for (uint32_t i = tid; i < count; i += kThreads)
-                if (g[i] != 0.0f)
-                    raise_error(a.err, TGB_E_S0_NONZERO, static_cast<int32_t>(ch.layer),
-                                ch.begin + i);
-        return;
-    }
     Decider dec;
     dec.init(bound, s);
     const uint64_t qg = q0 + a.rng_q0;  // Philox counter of this chunk's first byte
@@ -129,54 +141,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
 
     const uint32_t nfull = count >> 2;  // bytes whose 4 elements all exist
     uint32_t q = tid;
+    uint32_t streamed = 0;  // leading code bytes already written to every destination
     float bad_mag = 0.0f;  // max clipped |x| seen (per-layer API check: mag > s)
-    if (kPipe && (L.flags & kLayerVecIn) && q + (U - 1) * kThreads < nfull) {
-        // software-pipelined: loads + Philox of iteration i+1 are issued in the
-        // same basic block as the decisions of iteration i, so the integer
-        // multiplier (Philox) and the FP32 pipes (decisions) overlap per warp
+    if (s == 0.0f) {  // codec.hpp:155-159: all codes 0
+        for (; q < nbytes; q += kThreads) stage[q] = 0;
+        if (a.check)
+            for (uint32_t i = tid; i < count; i += kThreads)
+                if (g[i] != 0.0f)
+                    raise_error(a.err, TGB_E_S0_NONZERO, static_cast<int32_t>(ch.layer),
+                                ch.begin + i);
+    } else if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
-        float4 v[U];
-        uint4 r[U];
-        uint32_t ctr[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + q + u * kThreads);
-#pragma unroll
-        for (int u = 0; u < U; ++u) ctr[u] = qbase + q + u * kThreads;
-        ph(ctr, r);
-        for (;;) {
-            const uint32_t qn = q + U * kThreads;
-            const bool more = qn + (U - 1) * kThreads < nfull;
-            float4 vn[U];
-            uint4 rn[U];
-            if (more) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) vn[u] = __ldcs(g4 + qn + u * kThreads);
-#pragma unroll
-                for (int u = 0; u < U; ++u) ctr[u] = qbase + qn + u * kThreads;
-                ph(ctr, rn);
-            }
-            uint32_t byte[U];
-            float amb = -1.0f;
-#pragma unroll
-            for (int u = 0; u < U; ++u) byte[u] = dec.byte_fast(v[u], r[u], amb);
-            if (amb >= 0.0f || dec.exact_all) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) codes[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
-            q = qn;
-            if (!more) break;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = vn[u];
-                r[u] = rn[u];
-            }
-        }
-    }
-    if (L.flags & kLayerVecIn) {
-        const float4* g4 = reinterpret_cast<const float4*>(g);
-        for (; q + (U - 1) * kThreads < nfull; q += U * kThreads) {
+        // uniform trip count (every thread runs every block: __syncthreads below)
+        uint32_t blk = 0;
+        const uint64_t off = L.code_off + q0;
+        for (; blk + U * kThreads <= nfull; blk += U * kThreads, q += U * kThreads) {
             float4 v[U];
             uint32_t ctr[U];
             uint4 r[U];
@@ -188,50 +167,71 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
             uint32_t byte[U];
             float amb = -1.0f;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                byte[u] = dec.byte_fast(v[u], r[u], amb);
-            }
+            for (int u = 0; u < U; ++u) byte[u] = dec.byte_fast(v[u], r[u], amb);
             if (amb >= 0.0f || dec.exact_all) {  // rare: redo these bytes exactly
 #pragma unroll
                 for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                codes[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
+                stage[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
                 if (a.check)
                     bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
                                                    fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
             }
+            if (a.dst.remote && a.stream_blocks) {
+                // stream this block's codes to every destination now, so the NVLink
+                // stores drain while the CTA keeps computing (cheap final fence)
+                static_assert(U * kThreads == 4 * kThreads, "one u32 per thread per block");
+                __syncthreads();
+                const uint32_t w = reinterpret_cast<const uint32_t*>(stage + blk)[tid];
+                for (int p = 0; p < a.dst.n; ++p)
+                    reinterpret_cast<uint32_t*>(a.dst.base[p] + off + blk)[tid] = w;
+            }
         }
+        if (a.dst.remote && a.stream_blocks) streamed = blk;
         for (; q < nfull; q += kThreads) {
             const float4 v = __ldcs(g4 + q);
             uint32_t ctr[1] = {qbase + q};
             uint4 r[1];
             ph(ctr, r);
-            codes[q] = static_cast<uint8_t>(dec.byte(v, r[0]));
+            stage[q] = static_cast<uint8_t>(dec.byte(v, r[0]));
             if (a.check)
                 bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)),
                                                fmaxf(fabsf(v.z), fabsf(v.w))));
         }
     }
     // scalar path: unaligned input and the partial last byte (pad bits stay 00)
-    for (; q < nbytes; q += kThreads) {
-        float x[4];
+    if (s != 0.0f) {
+        for (; q < nbytes; q += kThreads) {
+            float x[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t i = 4 * q + e;
-            x[e] = i < count ? g[i] : 0.0f;
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t i = 4 * q + e;
+                x[e] = i < count ? g[i] : 0.0f;
+            }
+            uint32_t ctr[1] = {qbase + q};
+            uint4 r[1];
+            ph(ctr, r);
+            stage[q] = static_cast<uint8_t>(dec.byte(make_float4(x[0], x[1], x[2], x[3]), r[0]));
+            if (a.check)
+                bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])),
+                                               fmaxf(fabsf(x[2]), fabsf(x[3]))));
         }
-        uint32_t ctr[1] = {qbase + q};
-        uint4 r[1];
-        ph(ctr, r);
-        codes[q] = static_cast<uint8_t>(dec.byte(make_float4(x[0], x[1], x[2], x[3]), r[0]));
-        if (a.check)
-            bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])),
-                                           fmaxf(fabsf(x[2]), fabsf(x[3]))));
     }
     if (a.check && fminf(bad_mag, bound) > s)  // codec.hpp:163-165
         raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(ch.layer), ch.begin);
+    __syncthreads();
+    const uint64_t off = L.code_off + q0;
+    if (a.dst.n == 0) {
+        copy_out(stage, a.push + off, nbytes);
+    } else {
+        for (int p = 0; p < a.dst.n; ++p)
+            copy_out(stage + streamed, a.dst.base[p] + off + streamed, nbytes - streamed);
+        // No fence: the step barrier kernel runs after this grid completes in
+        // stream order, and grid completion implies its (peer) stores are
+        // performed -- the same guarantee event-based multi-GPU sync relies on.
+    }
 }
 
 // General-offset ternarize for the per-layer API when rng_base % 4 != 0:
@@ -443,7 +443,7 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
                             const K1Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
-            p.global_bucketing, p.n_layers, p.n_active_layers, layers};
+            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push};
     const TableSource src{chunks};
     switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
@@ -469,17 +469,12 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
-    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0};
+    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0, p.dst,
+             p.stream_blocks};
     const TableSource src{chunks};
-    switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x unroll x occupancy
+    switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
         case 1: k2_ternarize<TableSource, true, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
         case 2: k2_ternarize<TableSource, true, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 3: k2_ternarize<TableSource, false, 2, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 4: k2_ternarize<TableSource, true, 8, 2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 5: k2_ternarize<TableSource, true, 2, 5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 6: k2_ternarize<TableSource, false, 2, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 7: k2_ternarize<TableSource, false, 4, 2, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 8: k2_ternarize<TableSource, true, 2, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
         default: k2_ternarize<TableSource, false, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
     }
     return launch_status();
@@ -488,7 +483,7 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st) {
     const uint32_t nc = static_cast<uint32_t>((L.n + kChunk - 1) / kChunk);
     if (nc == 0) return cudaSuccess;
-    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, 0, 1, p.s_imm, p.rng_q0};
+    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, 0, 1, p.s_imm, p.rng_q0, PeerPush{}};
     k2_ternarize<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{L}, a);
     return launch_status();
 }
@@ -545,6 +540,36 @@ cudaError_t launch_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k
     if (n == 0) return cudaSuccess;
     const uint32_t blocks = static_cast<uint32_t>((n + kThreads - 1) / kThreads);
     k_rng_bits<<<blocks, kThreads, 0, st>>>(key0, key1, t, k0, n, out);
+    return launch_status();
+}
+
+
+// ===================================================== peer flag barrier
+// Cross-GPU barrier for the fused exchange: thread p stores this rank's epoch
+// into peer p's flag array (release, system scope) and then waits until every
+// peer has stored the same epoch into ours (acquire). One GPU per rank, so the
+// waiting kernels run on different devices. A bounded spin turns a dead peer
+// into TGB_E_PEER_TIMEOUT instead of a hang.
+__global__ void k_peer_barrier(PeerFlags f, uint64_t epoch, ErrWord* err) {
+    const int p = threadIdx.x;
+    if (p >= f.n) return;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f.remote[p]), "l"(epoch) : "memory");
+    uint64_t v = 0;
+    long long spins = 0;
+    const long long t0 = clock64();
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.local + p) : "memory");
+        if (v >= epoch) break;
+        if ((++spins & 1023) == 0 && clock64() - t0 > 20000000000ll) {  // ~10 s
+            raise_error(err, TGB_E_PEER_TIMEOUT, -1, static_cast<uint64_t>(p));
+            break;
+        }
+    }
+}
+
+cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,
+                                cudaStream_t st) {
+    k_peer_barrier<<<1, 32, 0, st>>>(f, epoch, err);
     return launch_status();
 }
 

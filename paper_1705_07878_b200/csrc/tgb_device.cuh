@@ -70,6 +70,16 @@ struct Partial {
     uint32_t pad;
 };
 
+// Destinations of this rank's push area (scaler slots + packed codes): its own
+// buffer plus, with peers attached, the same offset inside every other rank's
+// gathered buffer, written directly over NVLink (IPC-mapped peer memory).
+constexpr int kMaxPeers = 8;  // one NVSwitch box
+struct PeerPush {
+    uint8_t* base[kMaxPeers];
+    int32_t n;       // number of destinations (>= 1)
+    int32_t remote;  // destinations include peer memory (ordered by the step barrier)
+};
+
 struct ErrWord {
     uint32_t flags;
     int32_t layer;

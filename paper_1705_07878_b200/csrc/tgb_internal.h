@@ -8,6 +8,13 @@
 
 namespace tgb {
 
+// flag arrays of the cross-GPU barrier (inside each rank's IPC allocation)
+struct PeerFlags {
+    uint64_t* remote[kMaxPeers];  // address of THIS rank's slot in peer p's flag array
+    uint64_t* local;              // this rank's flag array (one slot per peer)
+    int32_t n;
+};
+
 struct K1Launch {
     Partial* partials;
     uint32_t* layer_done;
@@ -20,6 +27,7 @@ struct K1Launch {
     int32_t n_layers;
     int32_t n_active_layers;
     int32_t variant = 0;  // chunk K1 kernel variant (TGB_K1V, A/B only)
+    PeerPush push{};      // scaler slot destinations
 };
 
 struct K2Launch {
@@ -32,6 +40,8 @@ struct K2Launch {
     int32_t variant = 0;   // chunk K2 kernel variant (TGB_K2V, A/B only)
     float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
     uint64_t rng_q0 = 0;   // single-layer: rng_base / 4
+    PeerPush dst{};        // plan: code destinations (n == 0: push only)
+    int32_t stream_blocks = 0;  // TGB_STREAM (A/B): per-block remote streaming in K2
 };
 
 struct K3Launch {
@@ -72,6 +82,8 @@ cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, con
                              const K3Launch& p, cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
+cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,
+                                cudaStream_t st);
 cudaError_t launch_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k0, uint64_t n,
                             uint32_t* out, cudaStream_t st);
 

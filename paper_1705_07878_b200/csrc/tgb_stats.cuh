@@ -24,7 +24,13 @@ struct K1Out {
     int32_t n_layers;
     int32_t n_active_layers;  // layers with n > 0
     const LayerDev* layers;   // for the Global fix-up (plan only)
+    PeerPush push;            // scaler slot destinations (n == 0: slots only)
 };
+
+__device__ __forceinline__ void put_slot(const K1Out& o, int32_t slot, float v) {
+    o.slots[slot] = v;
+    for (int p = 0; p < o.push.n; ++p) reinterpret_cast<float*>(o.push.base[p])[slot] = v;
+}
 
 // x - x0 in fp64 (exact for any two floats within 2^29 of each other's exponent)
 __device__ __forceinline__ void acc4(const float4 v, const double x0, double& S, double& Q,
@@ -125,7 +131,7 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
             s = fminf(fmx, bound);  // == scaler(clip(g)) (codec.hpp:121-122, :130)
         }
         o.bounds[layer] = bound;
-        o.slots[L.slot] = s;
+        put_slot(o, L.slot, s);
         o.layer_done[layer] = 0u;  // self-reset for the next launch
         if (o.global_bucketing) {
             __threadfence();
@@ -141,7 +147,7 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
                 for (int l = 0; l < o.n_layers; ++l) {
                     const LayerDev& Ll = o.layers[l];
                     if (Ll.n == 0 || (Ll.flags & kLayerPassthrough)) continue;
-                    o.slots[Ll.slot] = gs;
+                    put_slot(o, Ll.slot, gs);
                 }
                 *o.global_done = 0u;
             }

@@ -124,6 +124,7 @@ class Plan:
         self.bounds = _view(bounds.value or 0, 4 * nl, self.device).view(torch.float32) \
             if nl else torch.empty(0, device=self.device)
         self._grads = self._outs = None
+        self.attached = False
 
     # -- binding -------------------------------------------------------------
     def bind(self, grads: Sequence[torch.Tensor], outs: Optional[Sequence[torch.Tensor]]):
@@ -162,12 +163,31 @@ class Plan:
     def share_scalers(self, comm: Comm, stream=None):
         check(load().tgb_share_scalers(self.h, comm.h, self._st(stream)), "tgb_share_scalers")
 
-    def sync(self, comm: Comm, stream=None):
-        check(load().tgb_sync(self.h, comm.h, self._st(stream)), "tgb_sync")
+    def sync(self, comm: Optional[Comm], stream=None):
+        """NCCL allgather of push buffers, or (peers attached) the step barrier."""
+        check(load().tgb_sync(self.h, comm.h if comm is not None else None, self._st(stream)),
+              "tgb_sync")
 
-    def decode_average(self, src: torch.Tensor, n_workers: int, stream=None):
-        check(load().tgb_decode_average(self.h, C.c_void_p(src.data_ptr()), int(n_workers),
-                                        self._st(stream)), "tgb_decode_average")
+    def decode_average(self, src: Optional[torch.Tensor], n_workers: int, stream=None):
+        """K3 over `src` (N push buffers back to back); None = this step's gather buffer."""
+        ptr = C.c_void_p(src.data_ptr()) if src is not None else None
+        check(load().tgb_decode_average(self.h, ptr, int(n_workers), self._st(stream)),
+              "tgb_decode_average")
+
+    def attach_peers(self, comm: Comm):
+        """Fused exchange over NVLink (CUDA IPC); collective over all ranks."""
+        with torch.cuda.device(self.device):
+            check(load().tgb_plan_attach_peers(self.h, comm.h), "tgb_plan_attach_peers")
+        self.attached = True
+
+    def last_buffers(self):
+        """(own push area, gather buffer) of the last step, as uint8 views."""
+        push, gathered = C.c_void_p(), C.c_void_p()
+        check(load().tgb_plan_last_buffers(self.h, C.byref(push), C.byref(gathered)),
+              "tgb_plan_last_buffers")
+        P = self.info.push_bytes
+        return (_view(push.value or 0, P, self.device),
+                _view(gathered.value or 0, P * self.n_workers, self.device))
 
     def step(self, t: int, comm: Optional[Comm] = None, stream=None):
         check(load().tgb_step(self.h, comm.h if comm is not None else None, int(t),
@@ -191,14 +211,16 @@ class Plan:
             raise CodecError(f"codec error flags {e.flags:#x} in {name}")
 
     def scalers(self) -> torch.Tensor:
-        return self.push[:4 * len(self.ns)].view(torch.float32)
+        push, _ = self.last_buffers()
+        return push[:4 * len(self.ns)].view(torch.float32)
 
     def layer_codes(self, l: int, worker: Optional[int] = None) -> torch.Tensor:
         nb = (self.ns[l] + 3) // 4
+        push, gathered = self.last_buffers()
         if worker is None:
-            return self.push[self.code_offsets[l]:self.code_offsets[l] + nb]
+            return push[self.code_offsets[l]:self.code_offsets[l] + nb]
         base = worker * self.info.push_bytes + self.code_offsets[l]
-        return self.gathered[base:base + nb]
+        return gathered[base:base + nb]
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:
@@ -221,7 +243,8 @@ class SyncWorker:
     """
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
-                 rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None):
+                 rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None,
+                 fused: bool = True):
         self.device = _dev(device)
         self.names = list(names)
         self.shapes = [list(s) for s in shapes]
@@ -235,6 +258,8 @@ class SyncWorker:
         self.grad_flat, self.grads = aligned_flat(self.ns, self.device)
         self.out_flat, self.outs = aligned_flat(self.ns, self.device)
         self.plan.bind(self.grads, self.outs)
+        if world_size > 1 and fused:  # K2 stores codes straight into every peer (NVLink)
+            self.plan.attach_peers(comm)
 
     def step(self, t: int, stream=None) -> List[torch.Tensor]:
         self.plan.step(t, self.comm, stream)

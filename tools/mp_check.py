@@ -1,0 +1,154 @@
+"""Multi-GPU parity + timing check (one process per GPU, torchrun).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 tools/mp_check.py
+
+Every rank encodes its own gradients (worker id = rank), the plan's NCCL
+allgather exchanges scalers+codes, K3 decodes on every rank. Checks:
+  * all ranks hold bit-identical averaged gradients (the reference's
+    "every worker decodes the same pull", cluster.hpp:153-161);
+  * on the small tensor set, the result is bit-identical to the reference's
+    average over the same N workers (oracle/_ref, cluster_test.cpp:157-195),
+    for shared and unshared scalers and the PRESHARED mode's own oracle.
+Prints one JSON line from rank 0.
+"""
+import hashlib
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_1705_07878_b200 as tg  # noqa: E402
+
+FUSED = os.environ.get("TGB_EXCHANGE", "fused") != "nccl"
+
+
+def main():
+    ws = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    comm = tg.Comm(rank, ws)
+    from oracle.oracle import Config, Reference, Restated
+
+    R = Restated()
+    names = ["conv1.weight", "conv1.bias", "empty", "fc.weight", "fc.bias"]
+    sizes = [1728, 64, 0, 40003, 10]
+    report = {"world_size": ws, "exchange": "fused" if FUSED else "nccl", "checks": {}}
+    for sharing, mode in [(True, tg.ShareMode.REF), (False, tg.ShareMode.REF),
+                          (True, tg.ShareMode.PRESHARED)]:
+        cfg = tg.CodecConfig(seed=42, scaler_sharing=sharing, share_mode=mode)
+        sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws, comm=comm,
+                           device=dev, fused=FUSED)
+        grads = [R.normal(100 + rank, 0, "mp/" + n, k, 1e-2) for n, k in zip(names, sizes)]
+        for v, g in zip(sw.grads, grads):
+            if g.size:
+                v.copy_(torch.from_numpy(g).to(dev))
+        for t in (5, 6):  # exercise both gather-buffer parities before the checked step
+            sw.step(t)
+        out = sw.step(7)
+        sw.check()
+        torch.cuda.synchronize()
+        flat = torch.cat([o.cpu() for o in out]).numpy()
+        h = hashlib.sha256(flat.tobytes()).hexdigest()
+        hs = [None] * ws
+        dist.all_gather_object(hs, h)
+        allg = [None] * ws
+        dist.all_gather_object(allg, grads)
+        key = f"sharing={sharing},mode={mode.name}"
+        ok_same = len(set(hs)) == 1
+        ok_ref = None
+        if rank == 0:
+            if mode == tg.ShareMode.REF:
+                (st, msg), ref = Reference().average_encoded(
+                    names, allg, Config(seed=42, scaler_sharing=sharing), 7)
+                ok_ref = st == 0 and np.array_equal(ref.view(np.uint32), flat.view(np.uint32))
+            else:  # PRESHARED: every worker ternarizes with s = max_w s_w (paper Eq. 4)
+                ok_ref = preshared_oracle(R, names, allg, flat, ws)
+        report["checks"][key] = {"ranks_identical": ok_same, "matches_oracle": ok_ref}
+        dist.barrier()
+        sw.plan.close()
+
+    # timing: full VGG-16 step at this world size
+    layers = tg.layersets.get("vgg16")
+    sw = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
+                       rank=rank, world_size=ws, comm=comm, device=dev, fused=FUSED)
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    sw.grad_flat.normal_(0.0, 1e-3, generator=gen)
+    st = torch.cuda.current_stream(dev)
+    p = sw.plan
+    for t in range(5):
+        sw.step(t)
+    torch.cuda.synchronize()
+    K = 20
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    dist.barrier()
+    for k in range(K):
+        ev[k][0].record(st)
+        p.stats()
+        ev[k][1].record(st)
+        p.ternarize_pack(k)
+        ev[k][2].record(st)
+        p.sync(comm)
+        ev[k][3].record(st)
+        p.decode_average(None, ws)
+        ev[k][4].record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    sw.check()
+    stage = [sorted(e[i].elapsed_time(e[i + 1]) for e in ev)[K // 2] for i in range(4)]
+    tot = ev[0][0].elapsed_time(ev[-1][4]) / K
+    t_all = torch.tensor([tot] + stage, dtype=torch.float64)
+    dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        n = sum(sw.ns)
+        report["vgg16_ms_per_step_max_over_ranks"] = float(t_all[0])
+        report["stage_ms_median_max_over_ranks"] = {
+            k: float(v) for k, v in zip(["K1", "K2", "allgather", "K3"], t_all[1:])}
+        report["aggregate_Gelem_s"] = ws * n / (float(t_all[0]) * 1e-3) / 1e9
+        report["allgather_GBps_per_rank_in"] = (ws - 1) * p.info.push_bytes / (
+            float(t_all[3]) * 1e-3) / 1e9
+        print(json.dumps(report), flush=True)
+    dist.barrier()  # no rank frees memory a peer may still write
+    sw.plan.close()
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+    ok = all(v["ranks_identical"] and (v["matches_oracle"] in (True, None))
+             for v in report["checks"].values())
+    sys.exit(0 if ok else 1)
+
+
+def preshared_oracle(R, names, allg, flat, ws):
+    """Oracle for PRESHARED: clip per worker, s = max over workers of the local
+    scalers, ternarize every worker with that s (ternarize(name, g, s, rng, 0),
+    codec.hpp:148), then the shared-sum average."""
+    outs = []
+    for li, name in enumerate(names):
+        n = allg[0][li].size
+        clipped, local = [], []
+        for w in range(ws):
+            c, _ = R.clip(allg[w][li], 2.5) if n >= 2 else (allg[w][li], 0)
+            clipped.append(c)
+            local.append(R.scaler(c))
+        s = max(local) if local else 0.0
+        codes = []
+        for w in range(ws):
+            st, cw = R.ternarize(clipped[w], s, 42, 7, name, w)
+            if st:
+                return False
+            codes.append(cw)
+        st, avg = R.average_block([s] * ws, codes, n, True)
+        outs.append(avg)
+    ref = np.concatenate(outs)
+    return bool(np.array_equal(ref.view(np.uint32), flat.view(np.uint32)))
+
+
+if __name__ == "__main__":
+    main()
