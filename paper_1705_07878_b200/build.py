@@ -68,5 +68,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_cpp_tests(verbose: bool = False) -> str:
+    """The C++ host-API test binary (tests/cpp/test_api.cpp -> build/tgb_cpp_api_test)."""
+    out_dir = os.path.join(ROOT, "build")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "tgb_cpp_api_test")
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+           "-I/usr/local/cuda/include", os.path.join(ROOT, "tests", "cpp", "test_api.cpp"),
+           "-o", out, "-L" + LIBDIR, "-ltgb", "-L/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,$ORIGIN/../paper_1705_07878_b200/lib"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    build_cpp_tests(verbose=True)

@@ -283,3 +283,15 @@ def test_vgg16_step_properties():
     for l, o in enumerate(a):
         vals = torch.unique(o.cpu())
         assert all(v in (-sc[l], 0.0, sc[l]) for v in vals.tolist())
+
+
+def test_plan_layout_matches_host_restatement():
+    from paper_1705_07878_b200.layout import push_layout
+
+    ns = [5, 0, 16, 1000003, 4096, 7]
+    plan = tg.Plan([f"l{i}" for i in range(len(ns))], ns, tg.CodecConfig(), device=DEV)
+    lay = push_layout(ns)
+    assert plan.code_offsets == lay.code_offsets
+    assert plan.info.push_bytes == lay.push_bytes
+    assert plan.info.code_bytes == lay.code_bytes
+    plan.close()
