@@ -93,7 +93,7 @@ typedef struct tgb_plan_info {
     int32_t n_chunks;     /* work items per streaming kernel */
     int32_t n_workers;
     uint32_t chunk_elems; /* elements per chunk */
-    uint32_t reserved;
+    uint32_t n_groups;    /* tgb_step schedule: 1 sequential, 2 = dominant layer || rest */
 } tgb_plan_info;
 
 typedef struct tgb_plan tgb_plan;

@@ -62,7 +62,7 @@ class PlanInfo(C.Structure):
                 ("code_bytes", C.c_uint64), ("scaler_offset", C.c_uint64),
                 ("codes_offset", C.c_uint64), ("n_layers", C.c_int32), ("n_slots", C.c_int32),
                 ("n_chunks", C.c_int32), ("n_workers", C.c_int32), ("chunk_elems", C.c_uint32),
-                ("reserved", C.c_uint32)]
+                ("n_groups", C.c_uint32)]
 
 
 class Error(C.Structure):

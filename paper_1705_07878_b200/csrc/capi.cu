@@ -111,6 +111,15 @@ struct tgb_plan {
     bool attached = false;
     int32_t rank = 0;
     uint64_t epoch = 0;  // attached: steps begun (barrier value); parity = epoch & 1
+    // Two-group schedule (tgb_step): group 1 = the dominant layer, group 0 = the
+    // rest. Each group runs K1 -> K2 -> [barrier] -> K3 on its own stream, so a
+    // memory-bound kernel of one group overlaps a compute-bound kernel of the
+    // other (K1(big) || K2(rest), K2(big) || K3(rest)). Chunk tables are ordered
+    // group 0 first; cb/cc and cb3/cc3 are the groups' chunk ranges.
+    bool grouped = false;
+    uint32_t cb[2] = {0, 0}, cc[2] = {0, 0}, cb3[2] = {0, 0}, cc3[2] = {0, 0};
+    cudaStream_t gs[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     ErrWord* d_err = nullptr;
     uint64_t push_bytes = 0, codes_offset = 0, code_bytes = 0, total = 0;
     int32_t n_slots = 0, n_active = 0;
@@ -158,6 +167,18 @@ int32_t tgb_device_count(void) {
 }
 
 // ------------------------------------------------------------------ plans
+// two-group stream priorities: the dominant layer's chain is the critical path
+// (K1 -> K2 -> K3 of the big layer), so it runs at high priority and the rest
+// fills the gaps (TGB_GPRIO=0 flips it, A/B only)
+static int gprio0(int lo, int hi) {
+    const char* m = std::getenv("TGB_GPRIO");
+    return (m && std::atoi(m) == 0) ? hi : lo;
+}
+static int gprio1(int lo, int hi) {
+    const char* m = std::getenv("TGB_GPRIO");
+    return (m && std::atoi(m) == 0) ? lo : hi;
+}
+
 tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                            const tgb_codec_params* params, uint16_t worker, int32_t n_workers,
                            tgb_plan** out) {
@@ -251,6 +272,51 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     }
     P->push_bytes = round_up(off, kAlignPush);
 
+    // two-group schedule: the dominant layer vs the rest (PerTensor + REF only:
+    // Global and PRESHARED need every layer's K1 before any K2)
+    {
+        int32_t big = -1;
+        for (int32_t l = 0; l < n_layers; ++l)
+            if (big < 0 || layers[l].n > layers[big].n) big = l;
+        bool want = big >= 0 && n_layers > 1 && params->bucketing == TGB_BUCKET_PER_TENSOR &&
+                    params->share_mode == TGB_SHARE_REF &&
+                    layers[big].n * 100 >= P->total * 35 && layers[big].n * 100 <= P->total * 95;
+        if (const char* m = std::getenv("TGB_GROUPS")) want = want && std::atoi(m) != 0;
+        if (want) {
+            auto part = [&](std::vector<ChunkDev>& v, uint32_t* cbeg, uint32_t* ccnt) {
+                std::stable_partition(v.begin(), v.end(),
+                                      [&](const ChunkDev& c) { return c.layer != static_cast<uint32_t>(big); });
+                uint32_t n0 = 0;
+                while (n0 < v.size() && v[n0].layer != static_cast<uint32_t>(big)) ++n0;
+                cbeg[0] = 0;
+                ccnt[0] = n0;
+                cbeg[1] = n0;
+                ccnt[1] = static_cast<uint32_t>(v.size()) - n0;
+            };
+            part(P->h_chunks, P->cb, P->cc);
+            part(P->h_chunks3, P->cb3, P->cc3);
+            // K1 partial units of a layer, relative to its group's first chunk
+            for (int32_t l = 0; l < n_layers; ++l) P->h_layers[l].n_chunks = 0;
+            for (uint32_t c = 0; c < P->h_chunks.size(); ++c) {
+                LayerDev& L = P->h_layers[P->h_chunks[c].layer];
+                const uint32_t base = P->h_chunks[c].layer == static_cast<uint32_t>(big) ? P->cb[1] : 0;
+                if (L.n_chunks++ == 0) L.first_chunk = c - base;
+            }
+            P->grouped = true;
+            int lo = 0, hi = 0;
+            bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess &&
+                      cudaStreamCreateWithPriority(&P->gs[0], cudaStreamNonBlocking, gprio0(lo, hi)) == cudaSuccess &&
+                      cudaStreamCreateWithPriority(&P->gs[1], cudaStreamNonBlocking, gprio1(lo, hi)) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&P->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming) == cudaSuccess;
+            if (!ok) {
+                tgb_plan_destroy(P);
+                return TGB_ERR_CUDA;
+            }
+        }
+    }
+
     // persistent K1/K2 partition: CTA c owns tiles [c*T/G, (c+1)*T/G); a segment is
     // the part of a CTA's run inside one layer (K1 emits one partial per segment)
     uint32_t G = 0;
@@ -299,7 +365,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     if (ok && n_workers > 1) {
         const uint64_t g = P->push_bytes * static_cast<uint64_t>(n_workers);
         P->flags_off = 2 * g;
-        const uint64_t bytes = P->flags_off + round_up(kMaxPeers * sizeof(uint64_t), kAlignPush);
+        const uint64_t bytes = P->flags_off + round_up(2 * kMaxPeers * sizeof(uint64_t), kAlignPush);
         ok = cudaMalloc(&P->d_ipc, bytes) == cudaSuccess &&
              cudaMemset(P->d_ipc, 0, bytes) == cudaSuccess;
         P->d_gathered = P->d_ipc;
@@ -348,6 +414,11 @@ void tgb_plan_destroy(tgb_plan* P) {
             if (p != P->rank && P->peer_ipc[p]) cudaIpcCloseMemHandle(P->peer_ipc[p]);
     cudaFree(P->d_ipc);
     cudaFree(P->d_err);
+    for (int g = 0; g < 2; ++g) {
+        if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
+        if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
+    }
+    if (P->ev_fork) cudaEventDestroy(P->ev_fork);
     cudaSetDevice(prev);
     delete P;
 }
@@ -365,6 +436,7 @@ tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
     o->n_chunks = static_cast<int32_t>(P->h_chunks.size());
     o->n_workers = P->n_workers;
     o->chunk_elems = P->chunk12;
+    o->n_groups = P->grouped ? 2u : 1u;
     return TGB_OK;
 }
 
@@ -429,13 +501,22 @@ static inline uint8_t* cur_gathered(const tgb_plan* P) {
     return P->n_workers > 1 ? P->d_gathered : P->d_push;
 }
 
-tgb_status tgb_stats(tgb_plan* P, void* stream) {
-    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
-    auto st = static_cast<cudaStream_t>(stream);
-    P->last = st;
-    if (P->attached) ++P->epoch;  // a step begins: flip the gather-buffer parity
+// ---- per-group launches (group g = chunk ranges cb/cc, cb3/cc3; an ungrouped
+// plan is the single group 0 spanning every chunk)
+static inline int n_groups(const tgb_plan* P) { return P->grouped ? 2 : 1; }
+static inline uint32_t g_begin(const tgb_plan* P, int g) { return P->grouped ? P->cb[g] : 0; }
+static inline uint32_t g_count(const tgb_plan* P, int g) {
+    return P->grouped ? P->cc[g] : static_cast<uint32_t>(P->h_chunks.size());
+}
+static inline uint32_t g_begin3(const tgb_plan* P, int g) { return P->grouped ? P->cb3[g] : 0; }
+static inline uint32_t g_count3(const tgb_plan* P, int g) {
+    return P->grouped ? P->cc3[g] : static_cast<uint32_t>(P->h_chunks3.size());
+}
+
+static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     const int32_t nl = static_cast<int32_t>(P->desc.size());
-    K1Launch k{P->d_partials, P->d_counters, P->d_counters + nl, P->d_bounds,
+    const uint32_t b = g_begin(P, g);
+    K1Launch k{P->d_partials + b, P->d_counters, P->d_counters + nl, P->d_bounds,
                reinterpret_cast<float*>(own_push(P)), P->d_err, P->p.clip_factor,
                P->p.bucketing == TGB_BUCKET_GLOBAL, nl, P->n_active};
     if (P->attached) {  // scalers also land in every peer's gather buffer
@@ -444,23 +525,22 @@ tgb_status tgb_stats(tgb_plan* P, void* stream) {
             if (p != P->rank) k.push.base[k.push.n++] = push_area(P, p);
         k.push.remote = 1;
     }
-    const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
-                           static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
     k.variant = P->k1_variant;
-    if (P->chunk_k1 || P->attached)
-        TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat,
-                                 static_cast<uint32_t>(P->h_chunks.size()), k, st));
-    else
+    if (P->chunk_k1 || P->attached || P->grouped) {
+        TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, g_count(P, g), k, st));
+    } else {
+        const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
+                               static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
         TGB_CUDA(launch_k1_persistent(pl, k, st));
+    }
     return TGB_OK;
 }
 
-tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
-    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
-    auto st = static_cast<cudaStream_t>(stream);
-    P->last = st;
+static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
+                              bool fuse_decode = false) {
     uint8_t* own = own_push(P);
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
+    k.fuse_decode = fuse_decode ? 1 : 0;
     k.variant = P->k2_variant;
     if (const char* m = std::getenv("TGB_STREAM")) k.stream_blocks = std::atoi(m);
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
@@ -468,19 +548,61 @@ tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
         k.dst.n = P->n_workers;
         k.dst.remote = 1;
     }
-    const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
-                           static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
-    if (P->chunk_k2 || P->attached)
-        TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat,
-                                 static_cast<uint32_t>(P->h_chunks.size()), k, st));
-    else
+    if (P->chunk_k2 || P->attached || P->grouped) {
+        const uint32_t b = g_begin(P, g);
+        TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + b, g_count(P, g), k, st));
+    } else {
+        const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
+                               static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
         TGB_CUDA(launch_k2_persistent(pl, k, st));
+    }
+    return TGB_OK;
+}
+
+static tgb_status launch_barrier(tgb_plan* P, int g, cudaStream_t st) {
+    PeerFlags f{};
+    for (int p = 0; p < P->n_workers; ++p)
+        f.remote[p] = reinterpret_cast<uint64_t*>(P->peer_ipc[p] + P->flags_off) +
+                      g * kMaxPeers + P->rank;
+    f.local = reinterpret_cast<uint64_t*>(P->d_ipc + P->flags_off) + g * kMaxPeers;
+    f.n = P->n_workers;
+    TGB_CUDA(launch_peer_barrier(f, P->epoch, P->d_err, st));
+    return TGB_OK;
+}
+
+static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t n_workers,
+                                cudaStream_t st) {
+    K3Launch k{src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
+               1.0f / static_cast<float>(n_workers), P->d_err};
+    TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + g_begin3(P, g), g_count3(P, g), k, st));
+    return TGB_OK;
+}
+
+#define TGB_TRY(expr)                        \
+    do {                                     \
+        const tgb_status s_ = (expr);        \
+        if (s_ != TGB_OK) return s_;         \
+    } while (0)
+
+tgb_status tgb_stats(tgb_plan* P, void* stream) {
+    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    if (P->attached) ++P->epoch;  // a step begins: flip the gather-buffer parity
+    for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_stats(P, g, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
+    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    P->last = st;
+    for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_tern(P, g, t, st));
     return TGB_OK;
 }
 
 tgb_status tgb_encode(tgb_plan* P, uint64_t t, void* stream) {
-    tgb_status s = tgb_stats(P, stream);
-    if (s != TGB_OK) return s;
+    TGB_TRY(tgb_stats(P, stream));
     return tgb_ternarize_pack(P, t, stream);
 }
 
@@ -502,12 +624,7 @@ tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     if (P->attached) {  // data already moved by K1/K2: only order the step
-        PeerFlags f{};
-        for (int p = 0; p < P->n_workers; ++p)
-            f.remote[p] = reinterpret_cast<uint64_t*>(P->peer_ipc[p] + P->flags_off) + P->rank;
-        f.local = reinterpret_cast<uint64_t*>(P->d_ipc + P->flags_off);
-        f.n = P->n_workers;
-        TGB_CUDA(launch_peer_barrier(f, P->epoch, P->d_err, st));
+        for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_barrier(P, g, st));
         return TGB_OK;
     }
     if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
@@ -521,28 +638,64 @@ tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_worke
     if (!d_src) d_src = cur_gathered(P);  // NULL: this step's gather buffer
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
-    K3Launch k{d_src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
-               1.0f / static_cast<float>(n_workers), P->d_err};
-    TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3, static_cast<uint32_t>(P->h_chunks3.size()), k,
-                             st));
+    for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_decode(P, g, d_src, n_workers, st));
     return TGB_OK;
 }
 
 tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
-    if (!P) return TGB_ERR_INVALID_ARGUMENT;
-    tgb_status s = tgb_stats(P, stream);
-    if (s != TGB_OK) return s;
-    if (P->p.share_mode == TGB_SHARE_PRESHARED && P->n_workers > 1) {
-        s = tgb_share_scalers(P, C, stream);
-        if (s != TGB_OK) return s;
+    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    const bool nccl_exchange = P->n_workers > 1 && !P->attached;
+    // N == 1: decode is this worker's own s*code; K2 writes it directly
+    bool fuse = P->n_workers == 1 && P->chunk_k2;
+    if (const char* m = std::getenv("TGB_FUSE1")) fuse = fuse && std::atoi(m) != 0;
+    if (fuse) {
+        P->last = st;
+        if (!P->grouped) {
+            TGB_TRY(tgb_stats(P, stream));
+            return launch_tern(P, 0, t, st, true);
+        }
+        TGB_CUDA(cudaEventRecord(P->ev_fork, st));
+        for (int gi = 0; gi < 2; ++gi) {
+            const int g = 1 - gi;
+            cudaStream_t gs = P->gs[g];
+            TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_fork, 0));
+            TGB_TRY(launch_stats(P, g, gs));
+            TGB_TRY(launch_tern(P, g, t, gs, true));
+            TGB_CUDA(cudaEventRecord(P->ev_join[g], gs));
+        }
+        TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[0], 0));
+        TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[1], 0));
+        return TGB_OK;
     }
-    s = tgb_ternarize_pack(P, t, stream);
-    if (s != TGB_OK) return s;
-    if (P->n_workers > 1) {
-        s = tgb_sync(P, C, stream);
-        if (s != TGB_OK) return s;
+    if (!P->grouped || nccl_exchange) {
+        TGB_TRY(tgb_stats(P, stream));
+        if (P->p.share_mode == TGB_SHARE_PRESHARED && P->n_workers > 1)
+            TGB_TRY(tgb_share_scalers(P, C, stream));
+        TGB_TRY(tgb_ternarize_pack(P, t, stream));
+        if (P->n_workers > 1) TGB_TRY(tgb_sync(P, C, stream));
+        return tgb_decode_average(P, nullptr, P->n_workers, stream);
     }
-    return tgb_decode_average(P, nullptr, P->n_workers, stream);
+    // overlapped two-group schedule: fork the step onto the plan's two streams
+    // (group 0 = small layers at high priority, group 1 = the dominant layer),
+    // join back into the caller's stream.
+    P->last = st;
+    if (P->attached) ++P->epoch;
+    TGB_CUDA(cudaEventRecord(P->ev_fork, st));
+    const uint8_t* src = cur_gathered(P);
+    for (int gi = 0; gi < 2; ++gi) {
+        const int g = 1 - gi;  // launch the critical (dominant-layer) chain first
+        cudaStream_t gs = P->gs[g];
+        TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_fork, 0));
+        TGB_TRY(launch_stats(P, g, gs));
+        TGB_TRY(launch_tern(P, g, t, gs));
+        if (P->attached) TGB_TRY(launch_barrier(P, g, gs));
+        TGB_TRY(launch_decode(P, g, src, P->n_workers, gs));
+        TGB_CUDA(cudaEventRecord(P->ev_join[g], gs));
+    }
+    TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[0], 0));
+    TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[1], 0));
+    return TGB_OK;
 }
 
 tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {

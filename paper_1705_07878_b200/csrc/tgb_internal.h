@@ -42,6 +42,7 @@ struct K2Launch {
     uint64_t rng_q0 = 0;   // single-layer: rng_base / 4
     PeerPush dst{};        // plan: code destinations (n == 0: push only)
     int32_t stream_blocks = 0;  // TGB_STREAM (A/B): per-block remote streaming in K2
+    int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
 };
 
 struct K3Launch {

@@ -125,6 +125,7 @@ class Plan:
             if nl else torch.empty(0, device=self.device)
         self._grads = self._outs = None
         self.attached = False
+        self.grouped = info.n_groups == 2  # tgb_step overlaps the dominant layer with the rest
 
     # -- binding -------------------------------------------------------------
     def bind(self, grads: Sequence[torch.Tensor], outs: Optional[Sequence[torch.Tensor]]):
