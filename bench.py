@@ -298,7 +298,37 @@ def run_b200(args):
     plan.raise_errors()
     total_ms = e_start.elapsed_time(e_stop)
 
-    # per-kernel breakdown (same kernels, launched sequentially with events between)
+    # per-kernel breakdown (same kernels, launched sequentially with events between).
+    # N = 1: on a second, ungrouped plan over the same gradients, so every kernel
+    # covers the whole set in one launch; N > 1: the stage API of this plan.
+    if N == 1:
+        os.environ["TGB_GROUPS"] = "0"
+        sw_b = tg.SyncWorker(names, shapes, cfg, device=dev)
+        os.environ.pop("TGB_GROUPS")
+        sw_b.grad_flat.copy_(sw.grad_flat)
+        plan_b = sw_b.plan
+    else:
+        plan_b = plan
+
+    def staged_step(t, ev=None):  # noqa: F811
+        if ev is not None:
+            ev[0].record(stream)
+        plan_b.stats()
+        if ev is not None:
+            ev[1].record(stream)
+        plan_b.ternarize_pack(t)
+        if ev is not None:
+            ev[2].record(stream)
+        if N > 1:
+            plan_b.sync(comm)
+        if ev is not None:
+            ev[3].record(stream)
+        plan_b.decode_average(None, N)
+        if ev is not None:
+            ev[4].record(stream)
+
+    for t in range(3):
+        staged_step(40_000 + t)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
     barrier()
     torch.cuda.synchronize(dev)
