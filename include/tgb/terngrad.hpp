@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <variant>
 #include <vector>
 
 #include "tgb/terngrad_b200.h"
@@ -203,10 +204,18 @@ struct TernaryBlock {
     }
 };
 
+// codec.hpp:63-76
+struct PassthroughBlock {
+    std::string name;
+    std::vector<float> values;
+};
+
+using GradBlock = std::variant<TernaryBlock, PassthroughBlock>;
+
 struct EncodedGradient {
     uint64_t iteration = 0;
     uint16_t worker = 0;
-    std::vector<TernaryBlock> blocks;
+    std::vector<GradBlock> blocks;
 };
 
 struct EncodeResult {
@@ -288,20 +297,53 @@ struct PlanHolder {
     tgb_plan* p = nullptr;
     ~PlanHolder() { tgb_plan_destroy(p); }
 };
+
+inline bool is_passthrough(const CodecConfig& cfg, const std::string& name) {
+    return cfg.float_mode || cfg.passthrough.count(name) != 0;  // cluster.hpp:274-275
+}
+
+// plan error -> the reference's CodecError text; corrupt-code indices are
+// reported by the device per tensor and converted to the bucket's element
+[[noreturn]] inline void throw_plan_error(const tgb_plan* p, const tgb_error& e,
+                                          const std::vector<std::string>& names) {
+    const std::string nm =
+        e.layer >= 0 && e.layer < static_cast<int32_t>(names.size()) ? names[e.layer] : "?";
+    if (e.flags & TGB_E_NONFINITE) throw CodecError("encode_step: non-finite gradient " + nm);
+    if (e.flags & TGB_E_CORRUPT_CODE) {
+        uint64_t k = e.index;
+        tgb_plan_info info{};
+        if (tgb_plan_get_info(p, &info) == TGB_OK)
+            for (int32_t b = 0; b < info.n_blocks; ++b) {
+                tgb_block_info bi{};
+                if (tgb_plan_block_info(p, b, &bi) == TGB_OK && bi.layer == e.layer &&
+                    bi.offset <= e.index && e.index < bi.offset + bi.n)
+                    k = e.index - bi.offset;
+            }
+        throw CodecError("corrupt ternary code 11 in block " + nm + " at element " +
+                         std::to_string(k));
+    }
+    if (e.flags & TGB_E_PEER_TIMEOUT)
+        throw CodecError("fused exchange: peer " + std::to_string(e.index) +
+                         " never reached the step barrier");
+    throw CodecError("codec error in " + nm);
+}
 }  // namespace detail
 
-// codec.hpp:194-239 (PerTensor / Global bucketing)
+// codec.hpp:194-239: clip -> bucket scalers -> ternarize; passthrough tensors verbatim
 inline EncodeResult encode_step(const std::vector<GradTensor>& grads, const CodecConfig& cfg,
                                 uint64_t t, uint16_t worker) {
     cfg.validate();
-    if (!cfg.passthrough.empty() || cfg.float_mode || cfg.bucketing == Bucketing::FixedSize)
-        throw std::invalid_argument("encode_step: passthrough/FixedSize not in this build");
     const int nl = static_cast<int>(grads.size());
     std::vector<tgb_layer_desc> d(nl);
     std::vector<size_t> offs(nl);
+    std::vector<std::string> names(nl);
     size_t total = 0;
     for (int l = 0; l < nl; ++l) {
-        d[l] = tgb_layer_desc{grads[l].size(), fnv1a64(grads[l].name), 0u, 0u};
+        names[l] = grads[l].name;
+        d[l] = tgb_layer_desc{grads[l].size(), fnv1a64(grads[l].name),
+                              detail::is_passthrough(cfg, grads[l].name) ? TGB_LAYER_PASSTHROUGH
+                                                                          : 0u,
+                              0u};
         offs[l] = total;
         total += (grads[l].size() + 3) / 4 * 4;  // 16-byte aligned tensors
     }
@@ -323,11 +365,7 @@ inline EncodeResult encode_step(const std::vector<GradTensor>& grads, const Code
     detail::check(tgb_encode(P.p, t, nullptr), "tgb_encode");
     tgb_error e{};
     const tgb_status st = tgb_check(P.p, &e);
-    if (st == TGB_ERR_CODEC) {
-        const std::string nm = e.layer >= 0 ? grads[e.layer].name : "?";
-        if (e.flags & TGB_E_NONFINITE) throw CodecError("encode_step: non-finite gradient " + nm);
-        throw CodecError("codec error in " + nm);
-    }
+    if (st == TGB_ERR_CODEC) detail::throw_plan_error(P.p, e, names);
     detail::check(st, "tgb_check");
     uint8_t *push = nullptr, *gath = nullptr;
     detail::check(tgb_plan_last_buffers(P.p, &push, &gath), "tgb_plan_last_buffers");
@@ -338,24 +376,31 @@ inline EncodeResult encode_step(const std::vector<GradTensor>& grads, const Code
     EncodeResult r;
     r.encoded.iteration = t;
     r.encoded.worker = worker;
-    for (int l = 0; l < nl; ++l) {
-        uint64_t code_off = 0;
-        int32_t slot = 0;
-        detail::check(tgb_plan_layer_layout(P.p, l, &code_off, &slot), "layout");
-        float s = 0.0f;
-        std::memcpy(&s, host.data() + 4 * slot, 4);
-        TernaryBlock b;
-        b.name = grads[l].name;
-        b.n = static_cast<uint32_t>(grads[l].size());
-        b.s = s;
-        b.codes.assign(host.begin() + code_off, host.begin() + code_off + (b.n + 3) / 4);
-        r.local_scalers.push_back(s);
-        r.encoded.blocks.push_back(std::move(b));
+    r.local_scalers.resize(info.n_slots);
+    std::memcpy(r.local_scalers.data(), host.data(), 4ull * info.n_slots);
+    for (int32_t b = 0; b < info.n_blocks; ++b) {
+        tgb_block_info bi{};
+        detail::check(tgb_plan_block_info(P.p, b, &bi), "tgb_plan_block_info");
+        const uint8_t* reg = host.data() + bi.region_offset;
+        if (bi.flags & TGB_LAYER_PASSTHROUGH) {
+            PassthroughBlock pb;
+            pb.name = grads[bi.layer].name;
+            pb.values.resize(bi.n);
+            std::memcpy(pb.values.data(), reg, 4 * bi.n);
+            r.encoded.blocks.push_back(std::move(pb));
+            continue;
+        }
+        TernaryBlock tb;
+        tb.name = grads[bi.layer].name;
+        tb.n = static_cast<uint32_t>(bi.n);
+        tb.s = r.local_scalers[bi.slot];
+        tb.codes.assign(reg, reg + (bi.n + 3) / 4);
+        r.encoded.blocks.push_back(std::move(tb));
     }
     return r;
 }
 
-// codec.hpp:245-311 (ternary blocks)
+// codec.hpp:245-311
 inline std::vector<GradTensor> average(const std::vector<EncodedGradient>& encoded, std::size_t N,
                                        bool scaler_sharing) {
     if (encoded.size() != N || N == 0)
@@ -367,21 +412,57 @@ inline std::vector<GradTensor> average(const std::vector<EncodedGradient>& encod
         if (e.blocks.size() != nblocks) throw CodecError("average: mismatched block structure");
     }
     std::vector<GradTensor> out;
+    auto append = [&](const std::string& name, std::vector<float>&& avg) {
+        if (!out.empty() && out.back().name == name) {  // merge bucket runs by name
+            out.back().values.insert(out.back().values.end(), avg.begin(), avg.end());
+            out.back().shape = {out.back().values.size()};
+        } else {
+            const std::size_t n = avg.size();
+            out.emplace_back(name, std::vector<std::size_t>{n}, std::move(avg));
+        }
+    };
     for (std::size_t b = 0; b < nblocks; ++b) {
-        const TernaryBlock& first = encoded[0].blocks[b];
-        for (const auto& e : encoded)
-            if (e.blocks[b].name != first.name || e.blocks[b].n != first.n)
+        if (const auto* pf = std::get_if<PassthroughBlock>(&encoded[0].blocks[b])) {
+            const std::size_t n = pf->values.size();
+            std::vector<detail::DevBuf<float>> vals;
+            std::vector<const float*> ptrs;
+            for (const auto& e : encoded) {
+                const auto* pb = std::get_if<PassthroughBlock>(&e.blocks[b]);
+                if (!pb || pb->name != pf->name || pb->values.size() != n)
+                    throw CodecError("average: block structure mismatch at " + pf->name);
+                vals.emplace_back(n);
+                vals.back().upload(pb->values.data(), n);
+                ptrs.push_back(vals.back().p);
+            }
+            std::vector<float> avg(n);
+            if (n) {
+                detail::DevBuf<float> o(n);
+                detail::check(tgb_layer_average_raw(static_cast<int32_t>(N), ptrs.data(), n, o.p,
+                                                    nullptr),
+                              "tgb_layer_average_raw");
+                detail::layer_check(pf->name);
+                o.download(avg.data(), n);
+            }
+            append(pf->name, std::move(avg));
+            continue;
+        }
+        const TernaryBlock& first = std::get<TernaryBlock>(encoded[0].blocks[b]);
+        for (const auto& e : encoded) {
+            const auto* tb = std::get_if<TernaryBlock>(&e.blocks[b]);
+            if (!tb || tb->name != first.name || tb->n != first.n)
                 throw CodecError("average: block structure mismatch at " + first.name);
+        }
         std::vector<float> avg(first.n);
         if (first.n) {
             std::vector<detail::DevBuf<uint8_t>> codes;
             std::vector<const uint8_t*> ptrs;
             std::vector<float> s;
             for (const auto& e : encoded) {
-                codes.emplace_back(e.blocks[b].codes.size());
-                codes.back().upload(e.blocks[b].codes.data(), e.blocks[b].codes.size());
+                const TernaryBlock& tb = std::get<TernaryBlock>(e.blocks[b]);
+                codes.emplace_back(tb.codes.size());
+                codes.back().upload(tb.codes.data(), tb.codes.size());
                 ptrs.push_back(codes.back().p);
-                s.push_back(e.blocks[b].s);
+                s.push_back(tb.s);
             }
             detail::DevBuf<float> ds(N), o(first.n);
             ds.upload(s.data(), N);
@@ -391,12 +472,7 @@ inline std::vector<GradTensor> average(const std::vector<EncodedGradient>& encod
             detail::layer_check(first.name);
             o.download(avg.data(), first.n);
         }
-        if (!out.empty() && out.back().name == first.name) {  // merge bucket runs by name
-            out.back().values.insert(out.back().values.end(), avg.begin(), avg.end());
-            out.back().shape = {out.back().values.size()};
-        } else {
-            out.emplace_back(first.name, std::vector<std::size_t>{avg.size()}, std::move(avg));
-        }
+        append(first.name, std::move(avg));
     }
     return out;
 }
@@ -436,7 +512,10 @@ public:
         offs_.resize(nl);
         std::size_t total = 0;
         for (int l = 0; l < nl; ++l) {
-            d[l] = tgb_layer_desc{sizes_[l], fnv1a64(names_[l]), 0u, 0u};
+            d[l] = tgb_layer_desc{sizes_[l], fnv1a64(names_[l]),
+                                  detail::is_passthrough(cfg, names_[l]) ? TGB_LAYER_PASSTHROUGH
+                                                                         : 0u,
+                                  0u};
             offs_[l] = total;
             total += (sizes_[l] + 3) / 4 * 4;
         }
@@ -471,14 +550,7 @@ public:
     void check() {
         tgb_error e{};
         const tgb_status st = tgb_check(plan_, &e);
-        if (st == TGB_ERR_CODEC) {
-            const std::string nm = e.layer >= 0 ? names_[e.layer] : "?";
-            if (e.flags & TGB_E_NONFINITE) throw CodecError("encode_step: non-finite gradient " + nm);
-            if (e.flags & TGB_E_CORRUPT_CODE)
-                throw CodecError("corrupt ternary code 11 in block " + nm + " at element " +
-                                 std::to_string(e.index));
-            throw CodecError("codec error in " + nm);
-        }
+        if (st == TGB_ERR_CODEC) detail::throw_plan_error(plan_, e, names_);
         detail::check(st, "tgb_check");
     }
     tgb_plan* plan() const { return plan_; }

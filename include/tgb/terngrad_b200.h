@@ -51,8 +51,8 @@ typedef enum tgb_status {
 
 typedef struct tgb_error {
     uint32_t flags;
-    int32_t layer;  /* first offending layer (plan) or -1 */
-    uint64_t index; /* first offending element within that layer (when known) */
+    int32_t layer;  /* first offending tensor (plan layer index) or -1 */
+    uint64_t index; /* first offending element within that tensor (when known) */
 } tgb_error;
 
 /* one gradient tensor of the canonical parameter order (tensor.hpp:14-43) */
@@ -67,7 +67,7 @@ typedef struct tgb_layer_desc {
 /* CodecConfig (codec.hpp:78-96) + the sharing mode of this build */
 #define TGB_BUCKET_PER_TENSOR 0 /* Bucketing::PerTensor */
 #define TGB_BUCKET_GLOBAL 1     /* Bucketing::Global */
-#define TGB_BUCKET_FIXED 2      /* Bucketing::FixedSize (not yet supported by plans) */
+#define TGB_BUCKET_FIXED 2      /* Bucketing::FixedSize: buckets of bucket_size elements */
 #define TGB_SHARE_REF 0         /* reference semantics: ternarize with the LOCAL scaler,
                                    decode with max over workers (cluster.hpp:195-196) */
 #define TGB_SHARE_PRESHARED 1   /* paper Eq.4: max-allreduce BEFORE ternarize */
@@ -94,7 +94,23 @@ typedef struct tgb_plan_info {
     int32_t n_workers;
     uint32_t chunk_elems; /* elements per chunk */
     uint32_t n_groups;    /* tgb_step schedule: 1 sequential, 2 = dominant layer || rest */
+    int32_t n_blocks;     /* blocks: buckets of ternary layers + one per passthrough layer */
+    int32_t reserved;
 } tgb_plan_info;
+
+/* One block of the encoded gradient (EncodedGradient::blocks, codec.hpp:70-76):
+ * a bucket of a ternary layer (TernaryBlock, the whole layer unless FixedSize)
+ * or a passthrough layer (PassthroughBlock, raw fp32). Blocks follow the
+ * canonical layer order; a multi-bucket layer is a contiguous run. */
+typedef struct tgb_block_info {
+    int32_t layer;          /* owning layer */
+    int32_t slot;           /* scaler slot (index into the push scaler array); -1 passthrough */
+    uint64_t offset;        /* first element inside the layer (ternarize rng_base, :229) */
+    uint64_t n;             /* elements */
+    uint64_t region_offset; /* byte offset in a push buffer: ceil(n/4) code bytes, or 4n raw bytes */
+    uint32_t flags;         /* TGB_LAYER_PASSTHROUGH */
+    uint32_t reserved;
+} tgb_block_info;
 
 typedef struct tgb_plan tgb_plan;
 typedef struct tgb_comm tgb_comm;
@@ -116,9 +132,12 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                            tgb_plan** out);
 void tgb_plan_destroy(tgb_plan* plan);
 tgb_status tgb_plan_get_info(const tgb_plan* plan, tgb_plan_info* out);
-/* byte offset of layer l's packed codes inside one push buffer; its scaler slot */
+/* layer l's first block: byte offset of its region inside one push buffer, its
+ * scaler slot (-1 for a passthrough layer) */
 tgb_status tgb_plan_layer_layout(const tgb_plan* plan, int32_t layer, uint64_t* code_offset,
                                  int32_t* slot);
+/* block b's layout (0 <= b < n_blocks) */
+tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_info* out);
 /* host arrays of device pointers, n_layers each: the worker's gradients (read)
  * and the averaged-gradient outputs (written by decode). Pointers must stay
  * valid until the next bind. 16-byte aligned pointers take the vector path. */
@@ -127,7 +146,7 @@ tgb_status tgb_plan_bind(tgb_plan* plan, const float* const* d_grads, float* con
 tgb_status tgb_plan_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_gathered,
                             float** d_bounds);
 
-/* K1: per-layer clip bound + local scaler -> push scaler slots, d_bounds.
+/* K1: per-layer clip bound + per-block local scaler -> push scaler slots, d_bounds (per block).
  * clip (codec.hpp:117-124) + scaler (:128-134) + Global max (:212-216). */
 tgb_status tgb_stats(tgb_plan* plan, void* stream);
 /* K2: stochastic ternarize + 2-bit pack of every layer into the push code
@@ -188,6 +207,10 @@ tgb_status tgb_layer_decode(const uint8_t* d_codes, uint64_t n, float s, float* 
  * pointers, d_s a device array of N scalers */
 tgb_status tgb_layer_average(int32_t n_workers, const uint8_t* const* d_codes, const float* d_s,
                              uint64_t n, int32_t sharing, float* d_out, void* stream);
+/* one PassthroughBlock position of average (codec.hpp:269-279): d_vals is a HOST
+ * array of N device pointers; out = float(sum_w double(v_w) / N), worker order */
+tgb_status tgb_layer_average_raw(int32_t n_workers, const float* const* d_vals, uint64_t n,
+                                 float* d_out, void* stream);
 /* RngStream::bits (rng.hpp:59-66) for indices k0..k0+n-1 (KAT helper) */
 tgb_status tgb_rng_bits(uint64_t seed, uint64_t t, uint64_t name_hash, uint64_t worker,
                         uint64_t k0, uint64_t n, uint32_t* d_out, void* stream);

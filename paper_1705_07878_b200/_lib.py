@@ -36,12 +36,13 @@ UNIQUE_ID_BYTES = 128
 EXPORTS = [
     "tgb_version", "tgb_status_string", "tgb_fnv1a64", "tgb_device_count",
     "tgb_plan_create", "tgb_plan_destroy", "tgb_plan_get_info", "tgb_plan_layer_layout",
+    "tgb_plan_block_info",
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_check",
     "tgb_plan_attach_peers", "tgb_plan_last_buffers",
     "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
     "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
-    "tgb_layer_average", "tgb_rng_bits", "tgb_layer_check",
+    "tgb_layer_average", "tgb_layer_average_raw", "tgb_rng_bits", "tgb_layer_check",
 ]
 
 
@@ -62,7 +63,13 @@ class PlanInfo(C.Structure):
                 ("code_bytes", C.c_uint64), ("scaler_offset", C.c_uint64),
                 ("codes_offset", C.c_uint64), ("n_layers", C.c_int32), ("n_slots", C.c_int32),
                 ("n_chunks", C.c_int32), ("n_workers", C.c_int32), ("chunk_elems", C.c_uint32),
-                ("n_groups", C.c_uint32)]
+                ("n_groups", C.c_uint32), ("n_blocks", C.c_int32), ("reserved", C.c_int32)]
+
+
+class BlockInfo(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("slot", C.c_int32), ("offset", C.c_uint64),
+                ("n", C.c_uint64), ("region_offset", C.c_uint64), ("flags", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 class Error(C.Structure):
@@ -86,6 +93,7 @@ def _declare(L):
         "tgb_plan_destroy": (None, [_vp]),
         "tgb_plan_get_info": (S, [_vp, C.POINTER(PlanInfo)]),
         "tgb_plan_layer_layout": (S, [_vp, _i32, C.POINTER(_u64), C.POINTER(_i32)]),
+        "tgb_plan_block_info": (S, [_vp, _i32, C.POINTER(BlockInfo)]),
         "tgb_plan_bind": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_plan_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_stats": (S, [_vp, _vp]),
@@ -107,6 +115,7 @@ def _declare(L):
                                     _vp]),
         "tgb_layer_decode": (S, [_vp, _u64, C.c_float, _vp, _vp]),
         "tgb_layer_average": (S, [_i32, C.POINTER(_vp), _vp, _u64, _i32, _vp, _vp]),
+        "tgb_layer_average_raw": (S, [_i32, C.POINTER(_vp), _u64, _vp, _vp]),
         "tgb_rng_bits": (S, [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp]),
         "tgb_layer_check": (S, [_vp, C.POINTER(Error)]),
     }

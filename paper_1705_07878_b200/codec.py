@@ -311,30 +311,36 @@ _plans = _PlanCache()
 
 
 def encode_step(grads: Sequence[GradTensor], cfg: CodecConfig, t: int, worker: int) -> EncodeResult:
-    """codec.hpp:194-239 through one B200 plan (K1 stats + K2 ternarize)."""
+    """codec.hpp:194-239 through one B200 plan (K1 stats + K2 ternarize/copy).
+
+    Blocks come back in canonical order: one TernaryBlock per bucket (FixedSize)
+    or tensor, one PassthroughBlock per tensor named in cfg.passthrough; the
+    codes/values are views of one copy of the plan's push area."""
     from .plan import Plan  # local import: plan.py builds on this module
 
     cfg.validate()
-    if cfg.passthrough or cfg.float_mode:
-        raise NotImplementedError("passthrough blocks are not in this round's device path")
-    if cfg.bucketing == Bucketing.FixedSize:
-        raise NotImplementedError("FixedSize bucketing is not in this round's device path")
     dev = grads[0].values.device if grads else _dev()
     names = [g.name for g in grads]
     ns = [g.size() for g in grads]
-    key = ("enc", tuple(names), tuple(ns), cfg.clip_factor, cfg.clipping_enabled,
-           int(cfg.bucketing), cfg.scaler_sharing, cfg.seed, int(cfg.share_mode), worker, str(dev))
-    plan = _plans.get(key, lambda: Plan(names, ns, cfg, worker=worker, n_workers=1, device=dev))
+    passthrough = tuple(name in cfg.passthrough for name in names)
+    key = ("enc", tuple(names), tuple(ns), passthrough, cfg.clip_factor, cfg.clipping_enabled,
+           int(cfg.bucketing), cfg.bucket_size, cfg.scaler_sharing, cfg.seed,
+           int(cfg.share_mode), worker, str(dev))
+    plan = _plans.get(key, lambda: Plan(names, ns, cfg, worker=worker, n_workers=1, device=dev,
+                                        passthrough=list(passthrough)))
     plan.bind([g.values for g in grads], None)
     plan.encode(t)
     plan.raise_errors()
     push = plan.push.clone()
-    scal = push[:4 * len(grads)].view(torch.float32).cpu().tolist() if grads else []
+    scal = push[:4 * plan.info.n_slots].view(torch.float32).cpu().tolist()
     blocks: List[GradBlock] = []
-    for l, g in enumerate(grads):
-        off = plan.code_offsets[l]
-        nb = (g.size() + 3) // 4
-        blocks.append(TernaryBlock(g.name, g.size(), scal[l], push[off:off + nb]))
+    for bi in plan.blocks:
+        name = names[bi.layer]
+        o = bi.region_offset
+        if bi.flags & _lib.TGB_LAYER_PASSTHROUGH:
+            blocks.append(PassthroughBlock(name, push[o:o + 4 * bi.n].view(torch.float32)))
+        else:
+            blocks.append(TernaryBlock(name, bi.n, scal[bi.slot], push[o:o + (bi.n + 3) // 4]))
     return EncodeResult(EncodedGradient(t, worker, blocks), scal)
 
 
@@ -352,8 +358,22 @@ def average(encoded: Sequence[EncodedGradient], N: int, scaler_sharing: bool) ->
     lib = load()
     for b in range(nblocks):
         first = encoded[0].blocks[b]
-        if isinstance(first, PassthroughBlock):
-            raise NotImplementedError("passthrough blocks are not in this round's device path")
+        if isinstance(first, PassthroughBlock):  # codec.hpp:269-279
+            dev = first.values.device if first.values.numel() else _dev()
+            avg = torch.empty(first.values.numel(), dtype=torch.float32, device=dev)
+            for e in encoded:
+                blk = e.blocks[b]
+                if not isinstance(blk, PassthroughBlock) or blk.name != first.name or \
+                        blk.values.numel() != first.values.numel():
+                    raise CodecError("average: block structure mismatch at " + first.name)
+            if avg.numel():
+                vals = [e.blocks[b].values.contiguous() for e in encoded]
+                ptrs = (C.c_void_p * N)(*[v.data_ptr() for v in vals])
+                check(lib.tgb_layer_average_raw(N, ptrs, avg.numel(), _ptr(avg), _stream(dev)),
+                      "tgb_layer_average_raw")
+                _layer_check(dev, first.name)
+            _append(out, first.name, avg)
+            continue
         for e in encoded:
             blk = e.blocks[b]
             if not isinstance(blk, TernaryBlock) or blk.name != first.name or blk.n != first.n:
@@ -366,9 +386,14 @@ def average(encoded: Sequence[EncodedGradient], N: int, scaler_sharing: bool) ->
             check(lib.tgb_layer_average(N, ptrs, _ptr(s), first.n, int(scaler_sharing), _ptr(avg),
                                         _stream(dev)), "tgb_layer_average")
             _layer_check(dev, first.name)
-        if out and out[-1].name == first.name:  # merge bucket runs by name
-            merged = torch.cat([out[-1].values, avg])
-            out[-1] = GradTensor(first.name, [merged.numel()], merged)
-        else:
-            out.append(GradTensor(first.name, [first.n], avg))
+        _append(out, first.name, avg)
     return out
+
+
+def _append(out: List[GradTensor], name: str, avg: torch.Tensor) -> None:
+    """merge bucket runs by name (codec.hpp:259-265)"""
+    if out and out[-1].name == name:
+        merged = torch.cat([out[-1].values, avg])
+        out[-1] = GradTensor(name, [merged.numel()], merged)
+    else:
+        out.append(GradTensor(name, [avg.numel()], avg))

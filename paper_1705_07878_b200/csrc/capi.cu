@@ -10,7 +10,6 @@
 #include <vector>
 
 #include "tgb_internal.h"
-#include "tgb_ring.cuh"
 
 using namespace tgb;
 
@@ -86,22 +85,21 @@ struct tgb_plan {
     tgb_codec_params p{};
     uint16_t worker = 0;
     int32_t n_workers = 1;
-    std::vector<tgb_layer_desc> desc;
-    std::vector<LayerDev> h_layers;
-    std::vector<ChunkDev> h_chunks;   // K1/K2 work items (kChunk12 elements)
-    std::vector<ChunkDev> h_chunks3;  // K3 work items (kChunk3 elements)
-    std::vector<ChunkDev> h_tiles;   // K1/K2 persistent tiles (4K elements)
-    std::vector<SegDev> h_segs;
-    std::vector<CtaDev> h_ctas;
+    std::vector<tgb_layer_desc> desc;   // tensors (layers) in canonical order
+    std::vector<TensorDev> h_tensors;
+    std::vector<LayerDev> h_layers;     // BLOCKS (buckets / passthrough tensors)
+    std::vector<uint64_t> block_off;    // block's first element inside its tensor
+    std::vector<uint2> h_units;         // per block: K1 work items {first (group-relative), count}
+    std::vector<ChunkDev> h_chunks;     // K1/K2 work items (chunk12 elements, never straddle blocks)
+    std::vector<ChunkDev> h_chunks3;    // K3 work items (kChunk3 elements)
     LayerDev* d_layers = nullptr;
-    ChunkFat* d_fat = nullptr;   // K1/K2: chunk + layer copy (rebuilt on bind)
+    TensorDev* d_tensors = nullptr;
+    uint2* d_units = nullptr;
+    ChunkFat* d_fat = nullptr;   // K1/K2: chunk + block copy (rebuilt on bind)
     ChunkFat* d_fat3 = nullptr;  // K3
-    ChunkDev* d_tiles = nullptr;
-    SegDev* d_segs = nullptr;
-    CtaDev* d_ctas = nullptr;
     Partial* d_partials = nullptr;
     uint32_t* d_counters = nullptr;  // n_layers layer_done + 1 global_done
-    float* d_bounds = nullptr;
+    float* d_bounds = nullptr;       // per block
     uint8_t* d_push = nullptr;
     uint8_t* d_gathered = nullptr;  // N > 1: parity-0 gather buffer inside d_ipc
     // N > 1: one IPC-shareable allocation [gather parity 0][gather parity 1][flags]
@@ -111,13 +109,14 @@ struct tgb_plan {
     bool attached = false;
     int32_t rank = 0;
     uint64_t epoch = 0;  // attached: steps begun (barrier value); parity = epoch & 1
-    // Two-group schedule (tgb_step): group 1 = the dominant layer, group 0 = the
-    // rest. Each group runs K1 -> K2 -> [barrier] -> K3 on its own stream, so a
-    // memory-bound kernel of one group overlaps a compute-bound kernel of the
-    // other (K1(big) || K2(rest), K2(big) || K3(rest)). Chunk tables are ordered
-    // group 0 first; cb/cc and cb3/cc3 are the groups' chunk ranges.
+    // Chunk tables are ordered by group, and inside a group ternary chunks come
+    // before passthrough chunks (K1 launches only the ternary prefix). An
+    // ungrouped plan is the single group 0. Two-group schedule (tgb_step):
+    // group 1 = the dominant tensor, group 0 = the rest; each group runs
+    // K1 -> K2 -> [barrier] -> K3 on its own stream, so a memory-bound kernel of
+    // one group overlaps a compute-bound kernel of the other.
     bool grouped = false;
-    uint32_t cb[2] = {0, 0}, cc[2] = {0, 0}, cb3[2] = {0, 0}, cc3[2] = {0, 0};
+    uint32_t cb[2] = {0, 0}, cc[2] = {0, 0}, ck1[2] = {0, 0}, cb3[2] = {0, 0}, cc3[2] = {0, 0};
     cudaStream_t gs[2] = {nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     ErrWord* d_err = nullptr;
@@ -125,8 +124,6 @@ struct tgb_plan {
     int32_t n_slots = 0, n_active = 0;
     uint32_t chunk12 = kChunk12;
     bool bound = false;
-    bool chunk_k1 = true;  // grid-per-chunk K1 (default) vs persistent TMA ring
-    bool chunk_k2 = true;
     int32_t k2_variant = 0;  // TGB_K2V
     int32_t k1_variant = 0;  // TGB_K1V
     cudaStream_t last = nullptr;
@@ -179,33 +176,40 @@ static int gprio1(int lo, int hi) {
     return (m && std::atoi(m) == 0) ? lo : hi;
 }
 
+// Block model (EncodedGradient::blocks, codec.hpp:70-76, built by encode_step
+// :218-236): a ternary tensor is one block (PerTensor / Global) or
+// ceil(n/k) buckets (FixedSize, an empty tensor still one empty block); a
+// passthrough tensor is one raw block. Push layout:
+//   [scaler slot per ternary block, f32][pad 256][block regions, 16-B aligned:
+//    ceil(n/4) code bytes or 4n raw bytes][pad 256]
+constexpr uint64_t kMaxBlocks = 1ull << 24;  // plan tables stay < 1.5 GB
+
 tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                            const tgb_codec_params* params, uint16_t worker, int32_t n_workers,
                            tgb_plan** out) {
     if (!out || !params || n_layers < 0 || (n_layers > 0 && !layers)) return TGB_ERR_INVALID_ARGUMENT;
     *out = nullptr;
     if (!(params->clip_factor > 0.0f)) return TGB_ERR_INVALID_ARGUMENT;  // codec.hpp:91-92
-    if (params->bucketing == TGB_BUCKET_FIXED) {
-        if (params->bucket_size < 1) return TGB_ERR_INVALID_ARGUMENT;  // codec.hpp:93-94
-        return TGB_ERR_UNSUPPORTED;
-    }
-    if (params->bucketing != TGB_BUCKET_PER_TENSOR && params->bucketing != TGB_BUCKET_GLOBAL)
+    if (params->bucketing == TGB_BUCKET_FIXED && params->bucket_size < 1)
+        return TGB_ERR_INVALID_ARGUMENT;  // codec.hpp:93-94
+    if (params->bucketing != TGB_BUCKET_PER_TENSOR && params->bucketing != TGB_BUCKET_GLOBAL &&
+        params->bucketing != TGB_BUCKET_FIXED)
         return TGB_ERR_INVALID_ARGUMENT;
     // worker keys the RNG (rng.hpp:54) and need not be < n_workers for encode-only plans
     if (n_workers < 1 || n_workers > kMaxWorkers) return TGB_ERR_INVALID_ARGUMENT;
+    uint64_t n_blocks = 0;
     for (int32_t l = 0; l < n_layers; ++l) {
-        if (layers[l].flags & TGB_LAYER_PASSTHROUGH) return TGB_ERR_UNSUPPORTED;
         if (layers[l].n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;  // TernaryBlock::n is u32
+        const bool pass = (layers[l].flags & TGB_LAYER_PASSTHROUGH) != 0;
+        if (pass || params->bucketing != TGB_BUCKET_FIXED || layers[l].n == 0)
+            n_blocks += 1;
+        else
+            n_blocks += (layers[l].n + params->bucket_size - 1) / params->bucket_size;
     }
+    if (n_blocks > kMaxBlocks) return TGB_ERR_UNSUPPORTED;
     auto* P = new (std::nothrow) tgb_plan;
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     P->p = *params;
-    // default: grid-per-chunk K1/K2 (measured faster on B200, tools/ab_bench.py);
-    // TGB_K12 / TGB_K1 / TGB_K2 = persistent selects the TMA-ring kernels
-    P->chunk_k1 = P->chunk_k2 = true;
-    if (const char* m = std::getenv("TGB_K12")) P->chunk_k1 = P->chunk_k2 = std::strcmp(m, "persistent") != 0;
-    if (const char* m = std::getenv("TGB_K1")) P->chunk_k1 = std::strcmp(m, "persistent") != 0;
-    if (const char* m = std::getenv("TGB_K2")) P->chunk_k2 = std::strcmp(m, "persistent") != 0;
     if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
     P->worker = worker;
@@ -215,151 +219,147 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
         delete P;
         return TGB_ERR_CUDA;
     }
-
-    // layout: [slots (one per layer)][pad to 256][codes, layer l at 16B-aligned offset][pad 256]
-    P->n_slots = n_layers;
-    P->codes_offset = round_up(static_cast<uint64_t>(n_layers) * sizeof(float), kAlignPush);
     // elements per grid-per-chunk work item: K1/K2 amortise a heavier per-CTA
     // setup over 32K elements, K3 (store-bound) prefers 16K (tools/ab_bench.py)
     uint64_t chunk = kChunk12, chunk3 = kChunk3;
     if (const char* m = std::getenv("TGB_CHUNK")) {  // A/B only
         const uint64_t v = std::strtoull(m, nullptr, 10);
-        if (v >= 1024 && v % 1024 == 0) chunk = v;
+        if (v >= 1024 && v % 1024 == 0 && v <= kChunk12) chunk = v;
     }
     P->chunk12 = static_cast<uint32_t>(chunk);
     if (const char* m = std::getenv("TGB_CHUNK3")) {
         const uint64_t v = std::strtoull(m, nullptr, 10);
         if (v >= 1024 && v % 1024 == 0) chunk3 = v;
     }
-    uint64_t off = P->codes_offset;
-    P->h_layers.resize(n_layers);
+
+    // ---- tensors -> blocks, scaler slots
+    P->h_tensors.resize(n_layers);
+    P->h_layers.reserve(n_blocks);
+    P->block_off.reserve(n_blocks);
+    int32_t slot = 0;
     for (int32_t l = 0; l < n_layers; ++l) {
-        LayerDev& L = P->h_layers[l];
-        std::memset(&L, 0, sizeof(L));
-        L.n = layers[l].n;
+        const uint64_t n = layers[l].n;
+        const bool pass = (layers[l].flags & TGB_LAYER_PASSTHROUGH) != 0;
+        TensorDev& T = P->h_tensors[l];
+        std::memset(&T, 0, sizeof(T));
+        T.n = n;
+        T.first_block = static_cast<uint32_t>(P->h_layers.size());
+        T.flags = (params->clipping_enabled && !pass) ? kLayerClip : 0u;  // codec.hpp:206-209
+        uint32_t k0 = 0, k1 = 0;
+        philox_key(params->seed, layers[l].name_hash, worker, k0, k1);
+        const uint64_t k = (!pass && params->bucketing == TGB_BUCKET_FIXED) ? params->bucket_size
+                                                                            : std::max<uint64_t>(n, 1);
+        for (uint64_t off = 0; off < std::max<uint64_t>(n, 1); off += k) {
+            LayerDev L;
+            std::memset(&L, 0, sizeof(L));
+            L.n = static_cast<uint32_t>(std::min<uint64_t>(k, n - std::min(n, off)));
+            L.tensor = static_cast<uint32_t>(l);
+            L.key0 = k0;
+            L.key1 = k1;
+            L.slot = pass ? -1 : slot++;
+            L.flags = (pass ? kLayerPassthrough : 0u) | T.flags;
+            L.rng_q = static_cast<uint32_t>(off >> 2);
+            L.rng_shift = static_cast<uint32_t>(off & 3u);
+            P->h_layers.push_back(L);
+            P->block_off.push_back(off);
+            P->total += L.n;
+            if (!pass) P->code_bytes += (L.n + 3) / 4;
+        }
+        T.n_blocks = static_cast<uint32_t>(P->h_layers.size()) - T.first_block;
+        if (n > 0 && !pass) ++P->n_active;
+    }
+    P->n_slots = slot;
+    P->codes_offset = round_up(static_cast<uint64_t>(slot) * sizeof(float), kAlignPush);
+    uint64_t off = P->codes_offset;
+    for (LayerDev& L : P->h_layers) {
         L.code_off = off;
-        L.slot = l;
-        philox_key(params->seed, layers[l].name_hash, worker, L.key0, L.key1);
-        L.flags = params->clipping_enabled ? kLayerClip : 0u;
-        L.first_chunk = static_cast<uint32_t>(P->h_chunks.size());
-        for (uint64_t b = 0; b < L.n; b += chunk) {
-            ChunkDev c;
-            c.layer = static_cast<uint32_t>(l);
-            c.begin = b;
-            c.count = static_cast<uint32_t>(std::min<uint64_t>(chunk, L.n - b));
-            P->h_chunks.push_back(c);
-        }
-        L.n_chunks = static_cast<uint32_t>(P->h_chunks.size()) - L.first_chunk;
-        for (uint64_t b = 0; b < L.n; b += chunk3) {
-            ChunkDev c;
-            c.layer = static_cast<uint32_t>(l);
-            c.begin = b;
-            c.count = static_cast<uint32_t>(std::min<uint64_t>(chunk3, L.n - b));
-            P->h_chunks3.push_back(c);
-        }
-        for (uint64_t b = 0; b < L.n; b += kTileElems) {
-            ChunkDev c;
-            c.layer = static_cast<uint32_t>(l);
-            c.begin = b;
-            c.count = static_cast<uint32_t>(std::min<uint64_t>(kTileElems, L.n - b));
-            P->h_tiles.push_back(c);
-        }
-        const uint64_t nb = (L.n + 3) / 4;
-        P->code_bytes += nb;
-        P->total += L.n;
-        if (L.n > 0) ++P->n_active;
-        off += round_up(nb, kAlignCodes);
+        const uint64_t bytes = (L.flags & kLayerPassthrough) ? 4ull * L.n : (L.n + 3ull) / 4;
+        off += round_up(bytes, kAlignCodes);
     }
     P->push_bytes = round_up(off, kAlignPush);
 
-    // two-group schedule: the dominant layer vs the rest (PerTensor + REF only:
-    // Global and PRESHARED need every layer's K1 before any K2)
-    {
-        int32_t big = -1;
-        for (int32_t l = 0; l < n_layers; ++l)
-            if (big < 0 || layers[l].n > layers[big].n) big = l;
-        bool want = big >= 0 && n_layers > 1 && params->bucketing == TGB_BUCKET_PER_TENSOR &&
-                    params->share_mode == TGB_SHARE_REF &&
-                    layers[big].n * 100 >= P->total * 35 && layers[big].n * 100 <= P->total * 95;
-        if (const char* m = std::getenv("TGB_GROUPS")) want = want && std::atoi(m) != 0;
-        if (want) {
-            auto part = [&](std::vector<ChunkDev>& v, uint32_t* cbeg, uint32_t* ccnt) {
-                std::stable_partition(v.begin(), v.end(),
-                                      [&](const ChunkDev& c) { return c.layer != static_cast<uint32_t>(big); });
-                uint32_t n0 = 0;
-                while (n0 < v.size() && v[n0].layer != static_cast<uint32_t>(big)) ++n0;
-                cbeg[0] = 0;
-                ccnt[0] = n0;
-                cbeg[1] = n0;
-                ccnt[1] = static_cast<uint32_t>(v.size()) - n0;
-            };
-            part(P->h_chunks, P->cb, P->cc);
-            part(P->h_chunks3, P->cb3, P->cc3);
-            // K1 partial units of a layer, relative to its group's first chunk
-            for (int32_t l = 0; l < n_layers; ++l) P->h_layers[l].n_chunks = 0;
-            for (uint32_t c = 0; c < P->h_chunks.size(); ++c) {
-                LayerDev& L = P->h_layers[P->h_chunks[c].layer];
-                const uint32_t base = P->h_chunks[c].layer == static_cast<uint32_t>(big) ? P->cb[1] : 0;
-                if (L.n_chunks++ == 0) L.first_chunk = c - base;
-            }
-            P->grouped = true;
-            int lo = 0, hi = 0;
-            bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess &&
-                      cudaStreamCreateWithPriority(&P->gs[0], cudaStreamNonBlocking, gprio0(lo, hi)) == cudaSuccess &&
-                      cudaStreamCreateWithPriority(&P->gs[1], cudaStreamNonBlocking, gprio1(lo, hi)) == cudaSuccess &&
-                      cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-                      cudaEventCreateWithFlags(&P->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
-                      cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming) == cudaSuccess;
-            if (!ok) {
-                tgb_plan_destroy(P);
-                return TGB_ERR_CUDA;
-            }
+    // ---- work items (chunks never straddle blocks)
+    const uint32_t nb = static_cast<uint32_t>(P->h_layers.size());
+    for (uint32_t b = 0; b < nb; ++b) {
+        const uint64_t n = P->h_layers[b].n;
+        for (uint64_t e = 0; e < n; e += chunk)
+            P->h_chunks.push_back({b, static_cast<uint32_t>(std::min<uint64_t>(chunk, n - e)), e});
+        for (uint64_t e = 0; e < n; e += chunk3)
+            P->h_chunks3.push_back({b, static_cast<uint32_t>(std::min<uint64_t>(chunk3, n - e)), e});
+    }
+
+    // ---- two-group schedule: the dominant tensor vs the rest (PerTensor + REF
+    // only: Global and PRESHARED need every tensor's K1 before any K2)
+    int32_t big = -1;
+    for (int32_t l = 0; l < n_layers; ++l)
+        if (!(layers[l].flags & TGB_LAYER_PASSTHROUGH) && (big < 0 || layers[l].n > layers[big].n))
+            big = l;
+    bool want = big >= 0 && n_layers > 1 && params->bucketing == TGB_BUCKET_PER_TENSOR &&
+                params->share_mode == TGB_SHARE_REF && layers[big].n * 100 >= P->total * 35 &&
+                layers[big].n * 100 <= P->total * 95;
+    if (const char* m = std::getenv("TGB_GROUPS")) want = want && std::atoi(m) != 0;
+    P->grouped = want;
+    auto group_of = [&](const ChunkDev& c) {
+        return (P->grouped && P->h_layers[c.layer].tensor == static_cast<uint32_t>(big)) ? 1u : 0u;
+    };
+    auto is_pass = [&](const ChunkDev& c) {
+        return (P->h_layers[c.layer].flags & kLayerPassthrough) ? 1u : 0u;
+    };
+    std::stable_sort(P->h_chunks.begin(), P->h_chunks.end(), [&](const ChunkDev& x, const ChunkDev& y) {
+        return 2 * group_of(x) + is_pass(x) < 2 * group_of(y) + is_pass(y);
+    });
+    std::stable_sort(P->h_chunks3.begin(), P->h_chunks3.end(), [&](const ChunkDev& x, const ChunkDev& y) {
+        return group_of(x) < group_of(y);
+    });
+    for (const ChunkDev& c : P->h_chunks) {
+        const uint32_t g = group_of(c);
+        ++P->cc[g];
+        if (!is_pass(c)) ++P->ck1[g];
+    }
+    P->cb[1] = P->cc[0];
+    for (const ChunkDev& c : P->h_chunks3) ++P->cc3[group_of(c)];
+    P->cb3[1] = P->cc3[0];
+    // K1 units (group-relative chunk indices) per block and per tensor
+    P->h_units.assign(nb, make_uint2(0, 0));
+    std::vector<uint2> tunits(n_layers, make_uint2(0, 0));
+    for (uint32_t c = 0; c < P->h_chunks.size(); ++c) {
+        const ChunkDev& ch = P->h_chunks[c];
+        if (is_pass(ch)) continue;
+        const uint32_t rel = c - P->cb[group_of(ch)];
+        uint2& u = P->h_units[ch.layer];
+        if (u.y++ == 0) u.x = rel;
+        uint2& tu = tunits[P->h_layers[ch.layer].tensor];
+        if (tu.y++ == 0) tu.x = rel;
+    }
+    for (LayerDev& L : P->h_layers) {
+        L.first_chunk = tunits[L.tensor].x;
+        L.n_chunks = tunits[L.tensor].y;
+    }
+    if (P->grouped) {
+        int lo = 0, hi = 0;
+        bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess &&
+                  cudaStreamCreateWithPriority(&P->gs[0], cudaStreamNonBlocking, gprio0(lo, hi)) == cudaSuccess &&
+                  cudaStreamCreateWithPriority(&P->gs[1], cudaStreamNonBlocking, gprio1(lo, hi)) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&P->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            tgb_plan_destroy(P);
+            return TGB_ERR_CUDA;
         }
     }
 
-    // persistent K1/K2 partition: CTA c owns tiles [c*T/G, (c+1)*T/G); a segment is
-    // the part of a CTA's run inside one layer (K1 emits one partial per segment)
-    uint32_t G = 0;
-    if (persistent_grid(&G) != cudaSuccess) {
-        delete P;
-        return TGB_ERR_CUDA;
-    }
-    const uint64_t T = P->h_tiles.size();
-    if (G > T) G = static_cast<uint32_t>(T);
-    std::vector<uint32_t> segs_of_layer(n_layers, 0);
-    for (uint32_t c = 0; c < G; ++c) {
-        const uint32_t a = static_cast<uint32_t>(T * c / G), b = static_cast<uint32_t>(T * (c + 1) / G);
-        CtaDev cd;
-        cd.seg_begin = static_cast<uint32_t>(P->h_segs.size());
-        for (uint32_t t = a; t < b;) {
-            SegDev sg;
-            sg.layer = P->h_tiles[t].layer;
-            sg.tile_begin = t;
-            while (t < b && P->h_tiles[t].layer == sg.layer) ++t;
-            sg.tile_end = t;
-            sg.pad = 0;
-            if (segs_of_layer[sg.layer]++ == 0)
-                P->h_layers[sg.layer].first_seg = static_cast<uint32_t>(P->h_segs.size());
-            P->h_segs.push_back(sg);
-        }
-        cd.seg_end = static_cast<uint32_t>(P->h_segs.size());
-        P->h_ctas.push_back(cd);
-    }
-    for (int32_t l = 0; l < n_layers; ++l) P->h_layers[l].n_segs = segs_of_layer[l];
-
-    const size_t nl = std::max<size_t>(1, n_layers), nc = std::max<size_t>(1, P->h_chunks.size());
-    const size_t ntl = std::max<size_t>(1, P->h_tiles.size()), nsg = std::max<size_t>(1, P->h_segs.size());
-    const size_t nct = std::max<size_t>(1, P->h_ctas.size());
-    bool ok = cudaMalloc(&P->d_layers, nl * sizeof(LayerDev)) == cudaSuccess &&
+    const size_t nl = std::max<size_t>(1, n_layers), nbl = std::max<size_t>(1, nb);
+    const size_t nc = std::max<size_t>(1, P->h_chunks.size());
+    bool ok = cudaMalloc(&P->d_layers, nbl * sizeof(LayerDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_tensors, nl * sizeof(TensorDev)) == cudaSuccess &&
+              cudaMalloc(&P->d_units, nbl * sizeof(uint2)) == cudaSuccess &&
               cudaMalloc(&P->d_fat, nc * sizeof(ChunkFat)) == cudaSuccess &&
               cudaMalloc(&P->d_fat3, std::max<size_t>(1, P->h_chunks3.size()) * sizeof(ChunkFat)) ==
                   cudaSuccess &&
-              cudaMalloc(&P->d_tiles, ntl * sizeof(ChunkDev)) == cudaSuccess &&
-              cudaMalloc(&P->d_segs, nsg * sizeof(SegDev)) == cudaSuccess &&
-              cudaMalloc(&P->d_ctas, nct * sizeof(CtaDev)) == cudaSuccess &&
-              cudaMalloc(&P->d_partials, std::max(nsg, nc) * sizeof(Partial)) == cudaSuccess &&
+              cudaMalloc(&P->d_partials, nc * sizeof(Partial)) == cudaSuccess &&
               cudaMalloc(&P->d_counters, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
-              cudaMalloc(&P->d_bounds, nl * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&P->d_bounds, nbl * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&P->d_push, P->push_bytes) == cudaSuccess &&
               cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess;
     if (ok && n_workers > 1) {
@@ -370,21 +370,19 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
              cudaMemset(P->d_ipc, 0, bytes) == cudaSuccess;
         P->d_gathered = P->d_ipc;
     }
-    const std::vector<float> inf_bounds(nl, INFINITY);  // empty layers: no clip (codec.hpp:118)
+    const std::vector<float> inf_bounds(nbl, INFINITY);  // empty / unclipped: no clip (codec.hpp:118)
     ok = ok && cudaMemset(P->d_counters, 0, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
          cudaMemset(P->d_push, 0, P->push_bytes) == cudaSuccess &&
          cudaMemset(P->d_err, 0, sizeof(ErrWord)) == cudaSuccess &&
-         cudaMemcpy(P->d_bounds, inf_bounds.data(), nl * sizeof(float), cudaMemcpyHostToDevice) ==
+         cudaMemcpy(P->d_bounds, inf_bounds.data(), nbl * sizeof(float), cudaMemcpyHostToDevice) ==
              cudaSuccess;
-    if (ok && !P->h_tiles.empty())
-        ok = cudaMemcpy(P->d_tiles, P->h_tiles.data(), P->h_tiles.size() * sizeof(ChunkDev),
+    if (ok && nb > 0)
+        ok = cudaMemcpy(P->d_layers, P->h_layers.data(), nb * sizeof(LayerDev),
                         cudaMemcpyHostToDevice) == cudaSuccess &&
-             cudaMemcpy(P->d_segs, P->h_segs.data(), P->h_segs.size() * sizeof(SegDev),
-                        cudaMemcpyHostToDevice) == cudaSuccess &&
-             cudaMemcpy(P->d_ctas, P->h_ctas.data(), P->h_ctas.size() * sizeof(CtaDev),
-                        cudaMemcpyHostToDevice) == cudaSuccess;
+             cudaMemcpy(P->d_units, P->h_units.data(), nb * sizeof(uint2), cudaMemcpyHostToDevice) ==
+                 cudaSuccess;
     if (ok && n_layers > 0)
-        ok = cudaMemcpy(P->d_layers, P->h_layers.data(), n_layers * sizeof(LayerDev),
+        ok = cudaMemcpy(P->d_tensors, P->h_tensors.data(), n_layers * sizeof(TensorDev),
                         cudaMemcpyHostToDevice) == cudaSuccess;
     if (!ok) {
         tgb_plan_destroy(P);
@@ -400,11 +398,10 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaGetDevice(&prev);
     cudaSetDevice(P->device);
     cudaFree(P->d_layers);
+    cudaFree(P->d_tensors);
+    cudaFree(P->d_units);
     cudaFree(P->d_fat);
     cudaFree(P->d_fat3);
-    cudaFree(P->d_tiles);
-    cudaFree(P->d_segs);
-    cudaFree(P->d_ctas);
     cudaFree(P->d_partials);
     cudaFree(P->d_counters);
     cudaFree(P->d_bounds);
@@ -437,6 +434,7 @@ tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
     o->n_workers = P->n_workers;
     o->chunk_elems = P->chunk12;
     o->n_groups = P->grouped ? 2u : 1u;
+    o->n_blocks = static_cast<int32_t>(P->h_layers.size());
     return TGB_OK;
 }
 
@@ -444,8 +442,23 @@ tgb_status tgb_plan_layer_layout(const tgb_plan* P, int32_t layer, uint64_t* cod
                                  int32_t* slot) {
     if (!P || layer < 0 || layer >= static_cast<int32_t>(P->desc.size()))
         return TGB_ERR_INVALID_ARGUMENT;
-    if (code_offset) *code_offset = P->h_layers[layer].code_off;
-    if (slot) *slot = P->h_layers[layer].slot;
+    const LayerDev& L = P->h_layers[P->h_tensors[layer].first_block];
+    if (code_offset) *code_offset = L.code_off;
+    if (slot) *slot = L.slot;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_block_info(const tgb_plan* P, int32_t block, tgb_block_info* o) {
+    if (!P || !o || block < 0 || block >= static_cast<int32_t>(P->h_layers.size()))
+        return TGB_ERR_INVALID_ARGUMENT;
+    const LayerDev& L = P->h_layers[block];
+    std::memset(o, 0, sizeof(*o));
+    o->layer = static_cast<int32_t>(L.tensor);
+    o->slot = L.slot;
+    o->offset = P->block_off[block];
+    o->n = L.n;
+    o->region_offset = L.code_off;
+    o->flags = (L.flags & kLayerPassthrough) ? TGB_LAYER_PASSTHROUGH : 0u;
     return TGB_OK;
 }
 
@@ -453,15 +466,17 @@ tgb_status tgb_plan_bind(tgb_plan* P, const float* const* d_grads, float* const*
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     const size_t nl = P->desc.size();
     if (nl > 0 && (!d_grads || !d_out)) return TGB_ERR_INVALID_ARGUMENT;
-    for (size_t l = 0; l < nl; ++l) {
-        LayerDev& L = P->h_layers[l];
-        if (L.n > 0 && (!d_grads[l] || !d_out[l])) return TGB_ERR_INVALID_ARGUMENT;
-        L.g = d_grads[l];
-        L.out = d_out[l];
+    for (size_t l = 0; l < nl; ++l)
+        if (P->desc[l].n > 0 && (!d_grads[l] || !d_out[l])) return TGB_ERR_INVALID_ARGUMENT;
+    for (size_t b = 0; b < P->h_layers.size(); ++b) {
+        LayerDev& L = P->h_layers[b];
+        const uint64_t off = P->block_off[b];
+        L.g = d_grads[L.tensor] ? d_grads[L.tensor] + off : nullptr;
+        L.out = d_out[L.tensor] ? d_out[L.tensor] + off : nullptr;
         L.flags = (L.flags & ~(kLayerVecIn | kLayerVecOut)) | layer_vec_flags(L.g, L.out);
     }
-    if (nl > 0)
-        TGB_CUDA(cudaMemcpy(P->d_layers, P->h_layers.data(), nl * sizeof(LayerDev),
+    if (!P->h_layers.empty())
+        TGB_CUDA(cudaMemcpy(P->d_layers, P->h_layers.data(), P->h_layers.size() * sizeof(LayerDev),
                             cudaMemcpyHostToDevice));
     for (int which = 0; which < 2; ++which) {
         const std::vector<ChunkDev>& chs = which == 0 ? P->h_chunks : P->h_chunks3;
@@ -504,21 +519,14 @@ static inline uint8_t* cur_gathered(const tgb_plan* P) {
 // ---- per-group launches (group g = chunk ranges cb/cc, cb3/cc3; an ungrouped
 // plan is the single group 0 spanning every chunk)
 static inline int n_groups(const tgb_plan* P) { return P->grouped ? 2 : 1; }
-static inline uint32_t g_begin(const tgb_plan* P, int g) { return P->grouped ? P->cb[g] : 0; }
-static inline uint32_t g_count(const tgb_plan* P, int g) {
-    return P->grouped ? P->cc[g] : static_cast<uint32_t>(P->h_chunks.size());
-}
-static inline uint32_t g_begin3(const tgb_plan* P, int g) { return P->grouped ? P->cb3[g] : 0; }
-static inline uint32_t g_count3(const tgb_plan* P, int g) {
-    return P->grouped ? P->cc3[g] : static_cast<uint32_t>(P->h_chunks3.size());
-}
 
 static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
-    const int32_t nl = static_cast<int32_t>(P->desc.size());
-    const uint32_t b = g_begin(P, g);
-    K1Launch k{P->d_partials + b, P->d_counters, P->d_counters + nl, P->d_bounds,
+    const uint32_t b = P->cb[g];
+    K1Launch k{P->d_partials + b, P->d_counters,
+               P->d_counters + P->desc.size(), P->d_bounds,
                reinterpret_cast<float*>(own_push(P)), P->d_err, P->p.clip_factor,
-               P->p.bucketing == TGB_BUCKET_GLOBAL, nl, P->n_active};
+               P->p.bucketing == TGB_BUCKET_GLOBAL, static_cast<int32_t>(P->h_layers.size()),
+               P->n_active};
     if (P->attached) {  // scalers also land in every peer's gather buffer
         k.push.n = 0;
         for (int p = 0; p < P->n_workers; ++p)
@@ -526,13 +534,9 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
         k.push.remote = 1;
     }
     k.variant = P->k1_variant;
-    if (P->chunk_k1 || P->attached || P->grouped) {
-        TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, g_count(P, g), k, st));
-    } else {
-        const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
-                               static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
-        TGB_CUDA(launch_k1_persistent(pl, k, st));
-    }
+    k.tensors = P->d_tensors;
+    k.block_units = P->d_units;
+    TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, P->ck1[g], k, st));
     return TGB_OK;
 }
 
@@ -548,14 +552,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
         k.dst.n = P->n_workers;
         k.dst.remote = 1;
     }
-    if (P->chunk_k2 || P->attached || P->grouped) {
-        const uint32_t b = g_begin(P, g);
-        TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + b, g_count(P, g), k, st));
-    } else {
-        const PersistLaunch pl{P->d_layers, P->d_tiles, P->d_segs, P->d_ctas,
-                               static_cast<uint32_t>(P->h_ctas.size()), P->k2_variant};
-        TGB_CUDA(launch_k2_persistent(pl, k, st));
-    }
+    TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + P->cb[g], P->cc[g], k, st));
     return TGB_OK;
 }
 
@@ -574,7 +571,7 @@ static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t 
                                 cudaStream_t st) {
     K3Launch k{src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
                1.0f / static_cast<float>(n_workers), P->d_err};
-    TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + g_begin3(P, g), g_count3(P, g), k, st));
+    TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + P->cb3[g], P->cc3[g], k, st));
     return TGB_OK;
 }
 
@@ -647,7 +644,7 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     const bool nccl_exchange = P->n_workers > 1 && !P->attached;
     // N == 1: decode is this worker's own s*code; K2 writes it directly
-    bool fuse = P->n_workers == 1 && P->chunk_k2;
+    bool fuse = P->n_workers == 1;
     if (const char* m = std::getenv("TGB_FUSE1")) fuse = fuse && std::atoi(m) != 0;
     if (fuse) {
         P->last = st;
@@ -746,8 +743,8 @@ tgb_status tgb_check(tgb_plan* P, tgb_error* out) {
     ErrWord e;
     TGB_CUDA(cudaMemcpy(&e, P->d_err, sizeof(e), cudaMemcpyDeviceToHost));
     out->flags = e.flags;
-    out->layer = e.flags ? e.layer : -1;
-    out->index = e.flags ? e.index : 0;
+    out->layer = e.flags ? e.layer() : -1;
+    out->index = e.flags ? e.index() : 0;
     if (e.flags) TGB_CUDA(cudaMemset(P->d_err, 0, sizeof(ErrWord)));
     return e.flags ? TGB_ERR_CODEC : TGB_OK;
 }
@@ -787,6 +784,7 @@ void tgb_comm_destroy(tgb_comm* C) {
 
 // -------------------------------------------------------------- per layer
 tgb_status tgb_layer_scaler(const float* d_g, uint64_t n, float* d_s, void* stream) {
+    if (n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;  // TernaryBlock::n is u32
     if ((n > 0 && !d_g) || !d_s) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     if (n == 0) {
@@ -801,7 +799,7 @@ tgb_status tgb_layer_scaler(const float* d_g, uint64_t n, float* d_s, void* stre
     TGB_CUDA(cudaMallocAsync(&parts, nc * sizeof(Partial), st));
     LayerDev L{};
     L.g = d_g;
-    L.n = n;
+    L.n = static_cast<uint32_t>(n);
     L.slot = 0;
     L.flags = layer_vec_flags(d_g, nullptr) & kLayerVecIn;  // clipping off => scaler = max|g|
     K1Launch k{parts, S->counters, S->counters + 1, S->tmp + 1, d_s, S->err, 2.5f, 0, 1, 1};
@@ -813,7 +811,7 @@ tgb_status tgb_layer_scaler(const float* d_g, uint64_t n, float* d_s, void* stre
 
 tgb_status tgb_layer_clip(const float* d_g, uint64_t n, float c, float* d_out, float* d_bound,
                           void* stream) {
-    if ((n > 0 && (!d_g || !d_out)) || !d_bound) return TGB_ERR_INVALID_ARGUMENT;
+    if ((n > 0 && (!d_g || !d_out)) || !d_bound || n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;
     if (!(c > 0.0f)) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
     if (n < 2) {  // codec.hpp:118: small tensors pass through unchanged
@@ -830,7 +828,7 @@ tgb_status tgb_layer_clip(const float* d_g, uint64_t n, float c, float* d_out, f
     TGB_CUDA(cudaMallocAsync(&parts, nc * sizeof(Partial), st));
     LayerDev L{};
     L.g = d_g;
-    L.n = n;
+    L.n = static_cast<uint32_t>(n);
     L.slot = 0;
     L.flags = kLayerClip | (layer_vec_flags(d_g, nullptr) & kLayerVecIn);
     K1Launch k{parts, S->counters, S->counters + 1, d_bound, S->tmp, S->err, c, 0, 1, 1};
@@ -844,7 +842,7 @@ tgb_status tgb_layer_clip(const float* d_g, uint64_t n, float c, float* d_out, f
 tgb_status tgb_layer_ternarize(const float* d_g, uint64_t n, float s, uint64_t seed, uint64_t t,
                                uint64_t name_hash, uint64_t worker, uint64_t rng_base,
                                uint8_t* d_codes, void* stream) {
-    if (n > 0 && (!d_g || !d_codes)) return TGB_ERR_INVALID_ARGUMENT;
+    if ((n > 0 && (!d_g || !d_codes)) || n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;
     if (n == 0) return TGB_OK;
     auto st = static_cast<cudaStream_t>(stream);
     DeviceScratch* S;
@@ -852,25 +850,23 @@ tgb_status tgb_layer_ternarize(const float* d_g, uint64_t n, float s, uint64_t s
     if (r != TGB_OK) return r;
     uint32_t k0, k1;
     philox_key(seed, name_hash, worker, k0, k1);
-    if ((rng_base & 3u) != 0) {  // stream lanes straddle code bytes
-        TGB_CUDA(launch_k2_offset(d_g, n, s, k0, k1, t, rng_base, d_codes, S->err, st));
-        return TGB_OK;
-    }
     LayerDev L{};
     L.g = d_g;
-    L.n = n;
+    L.n = static_cast<uint32_t>(n);
     L.code_off = 0;
     L.key0 = k0;
     L.key1 = k1;
     L.slot = 0;
     L.flags = layer_vec_flags(d_g, nullptr) & kLayerVecIn;
-    K2Launch k{d_codes, nullptr, nullptr, S->err, t, 0, 0, s, rng_base >> 2};
+    K2Launch k{d_codes, nullptr, nullptr, S->err, t, 0, 0, s};
+    k.rng_base = rng_base;  // unaligned bases take K2's lane-straddling path
     TGB_CUDA(launch_k2_single(L, k, st));
     return TGB_OK;
 }
 
 tgb_status tgb_layer_decode(const uint8_t* d_codes, uint64_t n, float s, float* d_out,
                             void* stream) {
+    if (n > 0xFFFFFFFFull) return TGB_ERR_INVALID_ARGUMENT;  // TernaryBlock::n is u32
     if (n > 0 && (!d_codes || !d_out)) return TGB_ERR_INVALID_ARGUMENT;
     if (n == 0) return TGB_OK;
     auto st = static_cast<cudaStream_t>(stream);
@@ -878,7 +874,7 @@ tgb_status tgb_layer_decode(const uint8_t* d_codes, uint64_t n, float s, float* 
     tgb_status r = scratch(&S);
     if (r != TGB_OK) return r;
     LayerDev L{};
-    L.n = n;
+    L.n = static_cast<uint32_t>(n);
     L.out = d_out;
     L.flags = layer_vec_flags(nullptr, d_out) & kLayerVecOut;
     const uint8_t* codes[1] = {d_codes};
@@ -890,7 +886,7 @@ tgb_status tgb_layer_decode(const uint8_t* d_codes, uint64_t n, float s, float* 
 
 tgb_status tgb_layer_average(int32_t n_workers, const uint8_t* const* d_codes, const float* d_s,
                              uint64_t n, int32_t sharing, float* d_out, void* stream) {
-    if (n_workers < 1 || n_workers > kMaxWorkers || !d_codes || !d_s)
+    if (n_workers < 1 || n_workers > kMaxWorkers || !d_codes || !d_s || n > 0xFFFFFFFFull)
         return TGB_ERR_INVALID_ARGUMENT;
     if (n == 0) return TGB_OK;
     if (!d_out) return TGB_ERR_INVALID_ARGUMENT;
@@ -901,12 +897,23 @@ tgb_status tgb_layer_average(int32_t n_workers, const uint8_t* const* d_codes, c
     tgb_status r = scratch(&S);
     if (r != TGB_OK) return r;
     LayerDev L{};
-    L.n = n;
+    L.n = static_cast<uint32_t>(n);
     L.out = d_out;
     L.flags = layer_vec_flags(nullptr, d_out) & kLayerVecOut;
     K3Launch k{nullptr, 0, n_workers, sharing ? 1 : 0, 1.0f / static_cast<float>(n_workers),
                S->err};
     TGB_CUDA(launch_k3_single(L, d_codes, d_s, k, st));
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_average_raw(int32_t n_workers, const float* const* d_vals, uint64_t n,
+                                 float* d_out, void* stream) {
+    if (n_workers < 1 || n_workers > kMaxWorkers || !d_vals) return TGB_ERR_INVALID_ARGUMENT;
+    if (n == 0) return TGB_OK;
+    if (!d_out) return TGB_ERR_INVALID_ARGUMENT;
+    for (int w = 0; w < n_workers; ++w)
+        if (!d_vals[w]) return TGB_ERR_INVALID_ARGUMENT;
+    TGB_CUDA(launch_average_raw(n_workers, d_vals, n, d_out, static_cast<cudaStream_t>(stream)));
     return TGB_OK;
 }
 
@@ -928,8 +935,8 @@ tgb_status tgb_layer_check(void* stream, tgb_error* out) {
     ErrWord e;
     TGB_CUDA(cudaMemcpy(&e, S->err, sizeof(e), cudaMemcpyDeviceToHost));
     out->flags = e.flags;
-    out->layer = e.flags ? e.layer : -1;
-    out->index = e.flags ? e.index : 0;
+    out->layer = e.flags ? e.layer() : -1;
+    out->index = e.flags ? e.index() : 0;
     if (e.flags) TGB_CUDA(cudaMemset(S->err, 0, sizeof(ErrWord)));
     return e.flags ? TGB_ERR_CODEC : TGB_OK;
 }

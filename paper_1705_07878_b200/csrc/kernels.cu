@@ -8,7 +8,10 @@
 //                        codec.hpp:281-307 == cluster.hpp:189-204 + wire.hpp:206-228
 //
 // All three are HBM-streaming kernels: 128-bit coalesced loads/stores of the
-// fp32 streams, one CTA (256 threads) per 16K-element work item.
+// fp32 streams, one CTA (256 threads) per work item = a chunk of one block
+// (32K elements for K1/K2, 16K for K3). A block is one bucket of a tensor
+// (the whole tensor for PerTensor/Global, k elements for FixedSize) or a
+// passthrough tensor (raw fp32, codec.hpp:206-209).
 #include "tgb_device.cuh"
 #include "tgb_internal.h"
 #include "tgb_stats.cuh"
@@ -32,23 +35,33 @@ struct TableSource {
 
 struct SingleSource {
     LayerDev L;
+    uint32_t chunk;  // elements per work item
     __device__ __forceinline__ void get(uint32_t b, ChunkDev& ch, LayerDev& L_) const {
         ch.layer = 0;
-        ch.begin = static_cast<uint64_t>(b) * kChunk;
+        ch.begin = static_cast<uint64_t>(b) * chunk;
         const uint64_t rem = L.n - ch.begin;
-        ch.count = static_cast<uint32_t>(rem < kChunk ? rem : kChunk);
+        ch.count = static_cast<uint32_t>(rem < chunk ? rem : chunk);
         L_ = L;
     }
 };
 
+// RNG stream index of a block's first element: the bucket's element offset
+// inside its tensor (ternarize rng_base, codec.hpp:167 via :229), or the
+// per-layer API's rng_base (passed whole, it may exceed 32 bits).
+__device__ __forceinline__ uint64_t block_rng_base(const LayerDev& L) {
+    return 4ull * L.rng_q + L.rng_shift;
+}
+
 // ====================================================================== K1
-// Per-layer API version (one CTA per 16K-element chunk). The plan path uses the
-// persistent TMA-ring kernel in persistent.cu; both share tgb_stats.cuh.
+// One CTA per work item (a chunk of one block); the tensor's last arriving CTA
+// merges the tensor's partials (tgb_stats.cuh). Passthrough blocks have no
+// statistics (codec.hpp:206-209) and are never in a K1 grid.
 template <class Src, int U = 8, int A = 1>
 __global__ void __launch_bounds__(kThreads) k1_stats(Src src, K1Out o) {
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
+    if (L.flags & kLayerPassthrough) return;
     const float* g = L.g + ch.begin;
     const uint32_t count = ch.count;
     const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
@@ -93,7 +106,7 @@ struct K2Args {
     int32_t reverse;     // walk chunks last-to-first (re-read K1's L2-resident tail)
     int32_t check;       // per-layer API: raise mag > s / s == 0 errors
     float s_imm;         // per-layer API: scaler by value (slots == nullptr)
-    uint64_t rng_q0;     // per-layer API: rng_base / 4 added to the Philox counter
+    uint64_t rng_base;   // per-layer API: ternarize rng_base (codec.hpp:148); plan: 0
     PeerPush dst;        // plan: code destinations (n == 0: just `push`)
     int32_t stream_blocks = 0;  // remote dst: write each 1 KB block as soon as it is coded (A/B: slower)
 };
@@ -117,6 +130,64 @@ __device__ __forceinline__ void copy_out(const uint8_t* stage, uint8_t* dst, uin
     }
 }
 
+// Passthrough block (codec.hpp:206-209, 221-224): the raw fp32 values go to
+// the block's region of every destination; the finite check of encode_step
+// (:204) runs here since K1 never sees these blocks. N == 1 (kFuse): the
+// average is float((0.0 + x) / 1.0) (codec.hpp:271-276), i.e. x with -0 -> +0.
+template <bool kFuse>
+__device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& L,
+                                               const ChunkDev& ch) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t count = ch.count;
+    const float* g = L.g + ch.begin;
+    const uint64_t off = L.code_off + 4ull * ch.begin;  // 16-B aligned (begin % 16 == 0)
+    const int nd = a.dst.n == 0 ? 1 : a.dst.n;
+    auto dst = [&](int p) {
+        return reinterpret_cast<float*>((a.dst.n == 0 ? a.push : a.dst.base[p]) + off);
+    };
+    float* out = L.out + ch.begin;
+    uint32_t bad = 0xFFFFFFFFu;
+    uint32_t done = 0;
+    if (L.flags & kLayerVecIn) {
+        const uint32_t n4 = count >> 2;
+        const float4* g4 = reinterpret_cast<const float4*>(g);
+        for (uint32_t i = tid; i < n4; i += kThreads) {
+            const float4 v = __ldcs(g4 + i);
+            for (int p = 0; p < nd; ++p) reinterpret_cast<float4*>(dst(p))[i] = v;
+            const bool fin = isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+            if (!fin && bad == 0xFFFFFFFFu) bad = 4 * i;
+            if (kFuse) {
+                const float4 o = make_float4(__fadd_rn(v.x, 0.0f), __fadd_rn(v.y, 0.0f),
+                                             __fadd_rn(v.z, 0.0f), __fadd_rn(v.w, 0.0f));
+                if (L.flags & kLayerVecOut) {
+                    __stcs(reinterpret_cast<float4*>(out) + i, o);
+                } else {
+                    out[4 * i] = o.x;
+                    out[4 * i + 1] = o.y;
+                    out[4 * i + 2] = o.z;
+                    out[4 * i + 3] = o.w;
+                }
+            }
+        }
+        done = n4 << 2;
+    }
+    for (uint32_t i = done + tid; i < count; i += kThreads) {
+        const float v = g[i];
+        for (int p = 0; p < nd; ++p) dst(p)[i] = v;
+        if (!isfinite(v) && bad == 0xFFFFFFFFu) bad = i;
+        if (kFuse) out[i] = __fadd_rn(v, 0.0f);
+    }
+    if (bad != 0xFFFFFFFFu) {
+        for (uint32_t i = bad; i < count && i < bad + 4; ++i)  // first non-finite of the float4
+            if (!isfinite(g[i])) {
+                bad = i;
+                break;
+            }
+        raise_error(a.err, TGB_E_NONFINITE, static_cast<int32_t>(L.tensor),
+                    block_rng_base(L) + ch.begin + bad);
+    }
+}
+
 template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
@@ -124,17 +195,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     ChunkDev ch;
     LayerDev L;
     src.get(b, ch, L);
+    if (L.flags & kLayerPassthrough) {
+        k2_passthrough<kFuse>(a, L, ch);
+        return;
+    }
     const float s = a.slots ? a.slots[L.slot] : a.s_imm;
     const float bound = a.bounds ? a.bounds[ch.layer] : INFINITY;
     const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
-    const uint64_t q0 = ch.begin >> 2;  // byte index of this chunk inside the layer
+    const uint64_t q0 = ch.begin >> 2;  // byte index of this chunk inside the block
     const float* g = L.g + ch.begin;
     const uint32_t tid = threadIdx.x;
 
     Decider dec;
     dec.init(bound, s);
-    const uint64_t qg = q0 + a.rng_q0;  // Philox counter of this chunk's first byte
+    // stream index of the chunk's first element (codec.hpp:167): element j of
+    // the chunk draws lane (B + j) & 3 of Philox block (B + j) >> 2
+    const uint64_t B = a.rng_base + block_rng_base(L) + ch.begin;
+    const uint64_t qg = B >> 2;
+    // fast paths: one Philox block per code byte, 32-bit counter arithmetic
+    const bool lane_aligned = (B & 3u) == 0 && static_cast<uint32_t>(qg) <= 0xFFFFFFFFu - nbytes;
     Philox4<kRolling> ph;
     ph.init(L.key0, L.key1, static_cast<uint32_t>(qg >> 32), a.t);
     const uint32_t qbase = static_cast<uint32_t>(qg);
@@ -148,8 +228,49 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         if (a.check)
             for (uint32_t i = tid; i < count; i += kThreads)
                 if (g[i] != 0.0f)
-                    raise_error(a.err, TGB_E_S0_NONZERO, static_cast<int32_t>(ch.layer),
-                                ch.begin + i);
+                    raise_error(a.err, TGB_E_S0_NONZERO, static_cast<int32_t>(L.tensor),
+                                block_rng_base(L) + ch.begin + i);
+    } else if (!lane_aligned) {
+        // block offset not a multiple of 4 (FixedSize with k % 4 != 0) or an
+        // unaligned per-layer rng_base: byte q's elements straddle Philox blocks
+        // qg+q and qg+q+1. Each lane computes block qg+q and takes the next one
+        // from its neighbour (lane 31 computes it); full 64-bit counters.
+        const uint32_t sh = static_cast<uint32_t>(B & 3u);
+        const uint32_t lane = tid & 31u;
+        const uint32_t t_lo = static_cast<uint32_t>(a.t), t_hi = static_cast<uint32_t>(a.t >> 32);
+        for (uint32_t qw = tid - lane; qw < nbytes; qw += kThreads) {
+            const uint32_t qq = qw + lane;
+            const uint64_t c = qg + qq;
+            const uint4 r = philox10(
+                make_uint4(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32), t_lo, t_hi),
+                L.key0, L.key1);
+            uint4 rn;
+            rn.x = __shfl_down_sync(0xffffffffu, r.x, 1);
+            rn.y = __shfl_down_sync(0xffffffffu, r.y, 1);
+            rn.z = __shfl_down_sync(0xffffffffu, r.z, 1);
+            if (lane == 31u) {
+                const uint64_t c1 = c + 1;
+                rn = philox10(make_uint4(static_cast<uint32_t>(c1), static_cast<uint32_t>(c1 >> 32),
+                                         t_lo, t_hi),
+                              L.key0, L.key1);
+            }
+            if (qq < nbytes) {
+                uint32_t byte = 0;
+#pragma unroll
+                for (uint32_t e = 0; e < 4; ++e) {
+                    const uint32_t i = 4 * qq + e;
+                    if (i >= count) break;
+                    const uint32_t j = sh + e;  // <= 6
+                    const uint32_t bits = j == 0 ? r.x : j == 1 ? r.y : j == 2 ? r.z : j == 3 ? r.w
+                                        : j == 4 ? rn.x : j == 5 ? rn.y : rn.z;
+                    const float x = g[i];
+                    byte |= dec.code(x, bits) << (2 * e);
+                    if (a.check) bad_mag = fmaxf(bad_mag, fabsf(x));
+                }
+                stage[qq] = static_cast<uint8_t>(byte);
+            }
+        }
+        q = nbytes;
     } else if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         // uniform trip count (every thread runs every block: __syncthreads below)
@@ -220,7 +341,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         }
     }
     if (a.check && fminf(bad_mag, bound) > s)  // codec.hpp:163-165
-        raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(ch.layer), ch.begin);
+        raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(L.tensor),
+                    block_rng_base(L) + ch.begin);
     __syncthreads();
     const uint64_t off = L.code_off + q0;
     if (a.dst.n == 0) {
@@ -267,43 +389,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     }
 }
 
-// General-offset ternarize for the per-layer API when rng_base % 4 != 0:
-// element k uses stream index rng_base + k (codec.hpp:167), which straddles
-// Philox blocks; one thread per output byte, up to two blocks each.
-__global__ void __launch_bounds__(kThreads)
-k2_ternarize_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t key1, uint64_t t,
-                    uint64_t rng_base, uint8_t* codes, ErrWord* err) {
-    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    const uint64_t nbytes = (n + 3) >> 2;
-    if (q >= nbytes) return;
-    if (s == 0.0f) {
-        codes[q] = 0;
-        for (int e = 0; e < 4; ++e) {
-            const uint64_t i = 4 * q + e;
-            if (i < n && g[i] != 0.0f) raise_error(err, TGB_E_S0_NONZERO, 0, i);
-        }
-        return;
-    }
-    Decider dec;
-    dec.init(INFINITY, s);
-    uint32_t byte = 0;
-    for (int e = 0; e < 4; ++e) {
-        const uint64_t i = 4 * q + e;
-        if (i >= n) break;
-        const uint64_t idx = rng_base + i;
-        const uint64_t c = idx >> 2;
-        const uint4 r = philox10(make_uint4(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32),
-                                            static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32)),
-                                 key0, key1);
-        const uint32_t lane = static_cast<uint32_t>(idx & 3);
-        const uint32_t bits = lane == 0 ? r.x : lane == 1 ? r.y : lane == 2 ? r.z : r.w;
-        const float x = g[i];
-        if (fabsf(x) > s) raise_error(err, TGB_E_SCALER_BELOW_MAX, 0, i);
-        byte |= dec.code_exact(x, bits) << (2 * e);
-    }
-    codes[q] = static_cast<uint8_t>(byte);
-}
-
 // ====================================================================== K3
 // code byte -> 4 lanes of (1 + v) in {0,1,2}; summed over N workers lane e holds
 // N + sum_w v_w, the LUT index. 11 codes map to 0 and are flagged separately.
@@ -316,6 +401,35 @@ __device__ __forceinline__ uint32_t lane_biased(uint32_t b) {
         r |= v << (8 * e);
     }
     return r;
+}
+
+// Passthrough block average (codec.hpp:269-279): per element an fp64 sum
+// from 0.0 over workers in order, divided by N in fp64, rounded to fp32.
+// base(w) = worker w's raw values of this chunk.
+template <class Base>
+__device__ __forceinline__ void k3_passthrough(Base base, int N, float* out, uint32_t count,
+                                               bool vec) {
+    const uint32_t tid = threadIdx.x;
+    const double dn = static_cast<double>(N);
+    const uint32_t n4 = vec ? (count >> 2) : 0u;
+    for (uint32_t i = tid; i < n4; i += kThreads) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int w = 0; w < N; ++w) {
+            const float4 v = __ldcs(reinterpret_cast<const float4*>(base(w)) + i);
+            s0 = __dadd_rn(s0, static_cast<double>(v.x));
+            s1 = __dadd_rn(s1, static_cast<double>(v.y));
+            s2 = __dadd_rn(s2, static_cast<double>(v.z));
+            s3 = __dadd_rn(s3, static_cast<double>(v.w));
+        }
+        __stcs(reinterpret_cast<float4*>(out) + i,
+               make_float4(static_cast<float>(s0 / dn), static_cast<float>(s1 / dn),
+                           static_cast<float>(s2 / dn), static_cast<float>(s3 / dn)));
+    }
+    for (uint32_t i = 4 * n4 + tid; i < count; i += kThreads) {
+        double sum = 0.0;
+        for (int w = 0; w < N; ++w) sum = __dadd_rn(sum, static_cast<double>(base(w)[i]));
+        out[i] = static_cast<float>(sum / dn);
+    }
 }
 
 struct K3Args {
@@ -339,6 +453,12 @@ __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs 
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
+    if (kTable && (L.flags & kLayerPassthrough)) {
+        const uint64_t off = L.code_off + 4ull * ch.begin;
+        k3_passthrough([&](int w) { return reinterpret_cast<const float*>(a.src + a.stride * w + off); },
+                       a.n_workers, L.out + ch.begin, ch.count, (L.flags & kLayerVecOut) != 0);
+        return;
+    }
     const int N = a.n_workers;
     __shared__ uint32_t tab[256];
     __shared__ float lut[2 * kMaxWorkers + 1];
@@ -436,13 +556,98 @@ __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs 
                         kTable ? a.src + a.stride * w + L.code_off + q0 : ptrs.codes[w] + q0;
                     const uint32_t b = base[q] & (base[q] >> 1) & 0x55u;
                     if (b) {
-                        raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(ch.layer),
-                                    ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
+                        raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
+                                    block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
                         break;
                     }
                 }
             }
         }
+    }
+}
+
+// Plan K3, shared scalers, worker count known at compile time (N <= 8, one
+// NVSwitch box): per-worker code pointers live in registers, every worker's
+// bytes for U positions are loaded before use, no per-load address math or
+// bounds checks on full chunks. Same arithmetic as k3_decode (LUT of
+// (s*float(sum))*invN indexed by N + sum).
+template <int NW>
+__global__ void __launch_bounds__(kThreads) k3_decode_nw(TableSource src, K3Args a) {
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    if (L.flags & kLayerPassthrough) {
+        const uint64_t off = L.code_off + 4ull * ch.begin;
+        k3_passthrough([&](int w) { return reinterpret_cast<const float*>(a.src + a.stride * w + off); },
+                       NW, L.out + ch.begin, ch.count, (L.flags & kLayerVecOut) != 0);
+        return;
+    }
+    __shared__ uint32_t tab[256];
+    __shared__ float lut[2 * NW + 1];
+    __shared__ float sw[NW];
+    const uint32_t tid = threadIdx.x;
+    tab[tid] = lane_biased(tid);
+    if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
+    const uint32_t count = ch.count;
+    const uint32_t nbytes = (count + 3) >> 2;
+    const uint8_t* base[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) base[w] = a.src + a.stride * w + L.code_off + (ch.begin >> 2);
+    __syncthreads();
+    if (tid <= 2 * NW) {
+        float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s = fmaxf(s, sw[w]);
+        lut[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - NW)),
+                             a.inv_n);  // codec.hpp:296
+    }
+    __syncthreads();
+    float* out = L.out + ch.begin;
+    const bool vec_out = (L.flags & kLayerVecOut) != 0;
+    constexpr int U = 4;
+    uint32_t bad = 0;
+    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
+        const bool full = qb + U * kThreads <= nbytes;
+        uint32_t bw[NW][U];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = qb + tid + u * kThreads;
+                bw[w][u] = (full || q < nbytes) ? __ldcs(base[w] + q) : 0u;
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                acc += tab[bw[w][u]];
+                bad |= bw[w][u] & (bw[w][u] >> 1);
+            }
+            const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
+                                         lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
+            const uint32_t q = qb + tid + u * kThreads;
+            const uint32_t b4 = 4 * q;
+            if (vec_out && (full || b4 + 4 <= count)) {
+                __stcs(reinterpret_cast<float4*>(out + b4), o);
+            } else if (q < nbytes) {
+                if (b4 + 0 < count) out[b4 + 0] = o.x;
+                if (b4 + 1 < count) out[b4 + 1] = o.y;
+                if (b4 + 2 < count) out[b4 + 2] = o.z;
+                if (b4 + 3 < count) out[b4 + 3] = o.w;
+            }
+        }
+    }
+    if (bad & 0x55u) {  // rare: locate the first corrupt element of this thread
+        for (uint32_t q = tid; q < nbytes; q += kThreads)
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t b = base[w][q] & (base[w][q] >> 1) & 0x55u;
+                if (b) {
+                    raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
+                                block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
+                    return;
+                }
+            }
     }
 }
 
@@ -455,6 +660,16 @@ k_clip_apply(const float* g, uint64_t n, const float* bound, float* out) {
         const float x = g[i];
         out[i] = fabsf(x) > b ? copysignf(b, x) : x;
     }
+}
+
+// per-layer raw average (PassthroughBlock part of average, codec.hpp:269-279)
+__global__ void __launch_bounds__(kThreads) k_average_raw(K3Ptrs ptrs, int32_t n_workers,
+                                                          uint64_t n, float* out, int vec) {
+    const uint64_t begin = static_cast<uint64_t>(blockIdx.x) * kChunk;
+    const uint64_t rem = n - begin;
+    const uint32_t count = static_cast<uint32_t>(rem < kChunk ? rem : kChunk);
+    k3_passthrough([&](int w) { return reinterpret_cast<const float*>(ptrs.codes[w]) + begin; },
+                   n_workers, out + begin, count, vec != 0);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -476,7 +691,8 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
                             const K1Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
-            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push};
+            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors,
+            p.block_units};
     const TableSource src{chunks};
     switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
@@ -491,11 +707,12 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
     const uint32_t nc = static_cast<uint32_t>((L.n + kChunk - 1) / kChunk);
     if (nc == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor, 0,
-            1, 1, nullptr};
+            1, 1, nullptr, PeerPush{}, nullptr, nullptr};
     LayerDev l = L;
+    l.tensor = 0;
     l.first_chunk = 0;
     l.n_chunks = nc;
-    k1_stats<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{l}, o);
+    k1_stats<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{l, kChunk}, o);
     return launch_status();
 }
 
@@ -518,20 +735,10 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
 }
 
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st) {
-    const uint32_t nc = static_cast<uint32_t>((L.n + kChunk - 1) / kChunk);
+    const uint32_t nc = static_cast<uint32_t>((L.n + kChunk12 - 1) / kChunk12);
     if (nc == 0) return cudaSuccess;
-    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, 0, 1, p.s_imm, p.rng_q0, PeerPush{}};
-    k2_ternarize<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{L}, a);
-    return launch_status();
-}
-
-cudaError_t launch_k2_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t key1,
-                             uint64_t t, uint64_t rng_base, uint8_t* codes, ErrWord* err,
-                             cudaStream_t st) {
-    const uint64_t nbytes = (n + 3) / 4;
-    if (nbytes == 0) return cudaSuccess;
-    const uint32_t blocks = static_cast<uint32_t>((nbytes + kThreads - 1) / kThreads);
-    k2_ternarize_offset<<<blocks, kThreads, 0, st>>>(g, n, s, key0, key1, t, rng_base, codes, err);
+    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, 0, 1, p.s_imm, p.rng_base, PeerPush{}};
+    k2_ternarize<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{L, kChunk12}, a);
     return launch_status();
 }
 
@@ -540,9 +747,21 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
     if (n_chunks == 0) return cudaSuccess;
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
-    if (p.sharing)
-        k3_decode<TableSource, true, true><<<n_chunks, kThreads, 0, st>>>(
-            TableSource{chunks}, a, ptrs);
+    const TableSource src{chunks};
+    if (p.sharing) {
+        switch (p.n_workers) {
+            case 1: k3_decode_nw<1><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 2: k3_decode_nw<2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 3: k3_decode_nw<3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 4: k3_decode_nw<4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 5: k3_decode_nw<5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 6: k3_decode_nw<6><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 7: k3_decode_nw<7><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 8: k3_decode_nw<8><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            default:
+                k3_decode<TableSource, true, true><<<n_chunks, kThreads, 0, st>>>(src, a, ptrs);
+        }
+    }
     else
         k3_decode<TableSource, true, false><<<n_chunks, kThreads, 0, st>>>(
             TableSource{chunks}, a, ptrs);
@@ -556,10 +775,26 @@ cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, con
     K3Args a{nullptr, 0, nullptr, scalers, p.s_imm, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
     for (int w = 0; w < p.n_workers; ++w) ptrs.codes[w] = codes[w];
+    const SingleSource src{L, kChunk};
     if (p.sharing)
-        k3_decode<SingleSource, false, true><<<nc, kThreads, 0, st>>>(SingleSource{L}, a, ptrs);
+        k3_decode<SingleSource, false, true><<<nc, kThreads, 0, st>>>(src, a, ptrs);
     else
-        k3_decode<SingleSource, false, false><<<nc, kThreads, 0, st>>>(SingleSource{L}, a, ptrs);
+        k3_decode<SingleSource, false, false><<<nc, kThreads, 0, st>>>(src, a, ptrs);
+    return launch_status();
+}
+
+cudaError_t launch_average_raw(int32_t n_workers, const float* const* vals, uint64_t n,
+                               float* out, cudaStream_t st) {
+    const uint64_t nc = (n + kChunk - 1) / kChunk;
+    if (nc == 0) return cudaSuccess;
+    K3Ptrs ptrs{};
+    bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+    for (int w = 0; w < n_workers; ++w) {
+        ptrs.codes[w] = reinterpret_cast<const uint8_t*>(vals[w]);
+        vec = vec && (reinterpret_cast<uintptr_t>(vals[w]) & 15u) == 0;
+    }
+    k_average_raw<<<static_cast<uint32_t>(nc), kThreads, 0, st>>>(ptrs, n_workers, n, out,
+                                                                   vec ? 1 : 0);
     return launch_status();
 }
 

@@ -25,42 +25,41 @@ constexpr uint32_t kLayerClip = 2u;     // clip this layer (clipping on, not pas
 constexpr uint32_t kLayerVecIn = 4u;    // gradient pointer is 16-byte aligned
 constexpr uint32_t kLayerVecOut = 8u;   // output pointer is 16-byte aligned
 
+// A block: one bucket of one tensor (PerTensor/Global: the whole tensor;
+// FixedSize(k): [off, off+k) of it, codec.hpp:224-232) or a passthrough tensor.
 struct LayerDev {
-    const float* g;      // worker gradient (input)
-    float* out;          // averaged gradient (output of decode)
-    uint64_t n;          // elements
-    uint64_t code_off;   // byte offset of the packed codes inside a push buffer
-    uint32_t key0, key1; // Philox key of RngStream(seed, *, name, worker)
-    int32_t slot;        // scaler slot
+    const float* g;      // block's first gradient element
+    float* out;          // block's first averaged-output element
+    uint64_t code_off;   // byte offset in a push area: packed codes, or raw fp32 (passthrough)
+    uint32_t n;          // elements in the block
+    uint32_t tensor;     // owning tensor (K1 statistics are per tensor, codec.hpp:206-209)
+    uint32_t key0, key1; // Philox key of RngStream(seed, *, tensor name, worker)
+    int32_t slot;        // scaler slot (passthrough: -1)
     uint32_t flags;
-    uint32_t first_chunk, n_chunks;  // chunk-mode K1 partial units of this layer
-    uint32_t first_seg, n_segs;      // persistent-mode K1 partial units (segments)
+    uint32_t rng_q;      // block start within the tensor >> 2 (ternarize rng_base, :167)
+    uint32_t rng_shift;  // block start within the tensor & 3 (!= 0: lanes straddle bytes)
+    uint32_t first_chunk, n_chunks;  // K1 work items of the TENSOR (group-relative)
 };
 
 struct ChunkDev {
-    uint32_t layer;
+    uint32_t layer;  // block index
     uint32_t count;  // elements in this chunk
-    uint64_t begin;  // first element (multiple of 4, and of kChunk inside a layer)
+    uint64_t begin;  // first element, relative to the block (multiple of 16)
 };
 
 // self-contained work item of the grid-per-chunk kernels: the chunk plus a
-// copy of its layer descriptor, fetched in one round trip (5 x LDG.128)
-// instead of the chunk -> layer dependent chain
+// copy of its block descriptor, fetched in one round trip (5 x LDG.128)
 struct ChunkFat {
     LayerDev L;
     ChunkDev ch;
 };
 
-// persistent kernels: a CTA owns a contiguous run of tiles (ChunkDev with
-// count <= kTileElems); a segment is the part of that run inside one layer.
-struct SegDev {
-    uint32_t layer;
-    uint32_t tile_begin, tile_end;  // [begin, end) in the plan's tile table
+// K1 finalize: a tensor's blocks and, per block, its K1 work items
+struct TensorDev {
+    uint64_t n;                      // tensor elements (sigma over the whole tensor)
+    uint32_t first_block, n_blocks;  // blocks of this tensor in the block table
+    uint32_t flags;                  // kLayerClip
     uint32_t pad;
-};
-
-struct CtaDev {
-    uint32_t seg_begin, seg_end;  // [begin, end) in the plan's segment table
 };
 
 // per-chunk clip statistics (Chan et al. mergeable moments)
@@ -80,19 +79,26 @@ struct PeerPush {
     int32_t remote;  // destinations include peer memory (ordered by the step barrier)
 };
 
+// Sticky error word. The location kept is the smallest (tensor, element) over
+// all raised errors -- the first one the reference's sequential loops would
+// throw at -- stored complemented so one atomicMax keeps it and 0 means none.
 struct ErrWord {
     uint32_t flags;
-    int32_t layer;
-    unsigned long long index;
+    uint32_t pad;
+    unsigned long long inv_key;  // ~((layer + 1) << 40 | index)
+    __host__ __device__ int32_t layer() const {
+        return static_cast<int32_t>((~inv_key) >> 40) - 1;
+    }
+    __host__ __device__ uint64_t index() const { return (~inv_key) & ((1ull << 40) - 1); }
 };
 
 __device__ __forceinline__ void raise_error(ErrWord* e, uint32_t flag, int32_t layer,
                                             uint64_t index) {
-    const uint32_t prev = atomicOr(&e->flags, flag);
-    if (prev == 0u) {  // first error wins the location fields
-        e->layer = layer;
-        e->index = index;
-    }
+    atomicOr(&e->flags, flag);
+    const unsigned long long key =
+        (static_cast<unsigned long long>(static_cast<uint32_t>(layer + 1) & 0xFFFFFFu) << 40) |
+        (index & ((1ull << 40) - 1));
+    atomicMax(&e->inv_key, ~key);
 }
 
 // ---------------------------------------------------------------- Philox
@@ -180,6 +186,16 @@ struct Decider {
     __device__ __forceinline__ uint32_t code_exact(float x, uint32_t bits) const {
         const float m = fminf(fabsf(x), bound);
         return exact_take(m, s, __uint2float_rn(bits)) ? sign_code(x) : 0u;
+    }
+
+    // one element's code (fast form, exact when flagged)
+    __device__ __forceinline__ uint32_t code(float x, uint32_t bits) const {
+        if (!exact_all) {
+            float amb = -1.0f;
+            const float c = code_fast(x, bits, amb);
+            if (!(amb >= 0.0f)) return static_cast<uint32_t>(c);
+        }
+        return code_exact(x, bits);
     }
 
     __device__ __forceinline__ uint32_t byte_exact(float4 v, uint4 r) const {

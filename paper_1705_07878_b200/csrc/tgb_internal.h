@@ -28,6 +28,8 @@ struct K1Launch {
     int32_t n_active_layers;
     int32_t variant = 0;  // chunk K1 kernel variant (TGB_K1V, A/B only)
     PeerPush push{};      // scaler slot destinations
+    const TensorDev* tensors = nullptr;  // plan: tensor table (per-tensor finalize)
+    const uint2* block_units = nullptr;  // plan: per block {first K1 unit, count}, group-relative
 };
 
 struct K2Launch {
@@ -39,7 +41,7 @@ struct K2Launch {
     int32_t reverse;
     int32_t variant = 0;   // chunk K2 kernel variant (TGB_K2V, A/B only)
     float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
-    uint64_t rng_q0 = 0;   // single-layer: rng_base / 4
+    uint64_t rng_base = 0; // single-layer: ternarize rng_base (codec.hpp:148)
     PeerPush dst{};        // plan: code destinations (n == 0: push only)
     int32_t stream_blocks = 0;  // TGB_STREAM (A/B): per-block remote streaming in K2
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
@@ -55,32 +57,18 @@ struct K3Launch {
     float s_imm = 0.0f;    // single-layer: scaler by value when scalers == nullptr
 };
 
-struct PersistLaunch {
-    const LayerDev* layers;
-    const ChunkDev* tiles;
-    const SegDev* segs;
-    const CtaDev* ctas;
-    uint32_t n_ctas;
-    int32_t variant;  // K2: 0 hoisted Philox keys, 1 rolling keys (TGB_K2V)
-};
-
-// resident CTAs for the persistent kernels (SMs x min occupancy of K1p/K2p)
-cudaError_t persistent_grid(uint32_t* ctas);
-cudaError_t launch_k1_persistent(const PersistLaunch& P, const K1Launch& p, cudaStream_t st);
-cudaError_t launch_k2_persistent(const PersistLaunch& P, const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st);
-cudaError_t launch_k2_offset(const float* g, uint64_t n, float s, uint32_t key0, uint32_t key1,
-                             uint64_t t, uint64_t rng_base, uint8_t* codes, ErrWord* err,
-                             cudaStream_t st);
 cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K3Launch& p, cudaStream_t st);
 cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, const float* scalers,
                              const K3Launch& p, cudaStream_t st);
+cudaError_t launch_average_raw(int32_t n_workers, const float* const* vals, uint64_t n,
+                               float* out, cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,

@@ -13,18 +13,20 @@
 namespace tgb {
 
 struct K1Out {
-    Partial* partials;      // one per work unit (chunk or segment)
-    uint32_t* layer_done;   // per layer arrival counters (self-resetting)
-    uint32_t* global_done;  // arrival counter over layers (Global bucketing)
-    float* bounds;          // per layer clip bound
+    Partial* partials;      // one per work unit (chunk), group-relative
+    uint32_t* layer_done;   // per TENSOR arrival counters (self-resetting)
+    uint32_t* global_done;  // arrival counter over tensors (Global bucketing)
+    float* bounds;          // per block clip bound (the tensor's bound)
     float* slots;           // scaler slots
     ErrWord* err;
     float clip_factor;
     int32_t global_bucketing;
-    int32_t n_layers;
-    int32_t n_active_layers;  // layers with n > 0
-    const LayerDev* layers;   // for the Global fix-up (plan only)
+    int32_t n_layers;         // blocks (Global fix-up)
+    int32_t n_active_layers;  // tensors that finalize (non-empty, ternary)
+    const LayerDev* layers;   // block table (slots of a tensor's blocks, Global fix-up)
     PeerPush push;            // scaler slot destinations (n == 0: slots only)
+    const TensorDev* tensors; // plan only; nullptr = single-block single-layer API
+    const uint2* block_units; // per block: {first work item (group-relative), count}
 };
 
 __device__ __forceinline__ void put_slot(const K1Out& o, int32_t slot, float v) {
@@ -76,7 +78,7 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
         p.pad = 0;
         o.partials[unit] = p;
         __threadfence();
-        const uint32_t ticket = atomicAdd(&o.layer_done[layer], 1u);
+        const uint32_t ticket = atomicAdd(&o.layer_done[L.tensor], 1u);
         is_last = (ticket == n_units - 1);
     }
     Bar::sync();
@@ -113,27 +115,45 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
         }
         Bar::sync();
     }
+    __shared__ float s_bound;
+    __shared__ bool s_bad;
     if (tid == 0) {
         const double fm = smean[0];
         double fm2 = sm2[0];
         const float fmx = smx[0];
-        float bound = INFINITY, s = 0.0f;
-        if (!isfinite(fm) || !isfinite(fm2) || !isfinite(fmx)) {
-            raise_error(o.err, TGB_E_NONFINITE, static_cast<int32_t>(layer), 0);
+        const uint64_t tn = o.tensors ? o.tensors[L.tensor].n : L.n;
+        const bool clip = o.tensors ? (o.tensors[L.tensor].flags & kLayerClip) != 0
+                                    : (L.flags & kLayerClip) != 0;
+        float bound = INFINITY;
+        s_bad = !isfinite(fm) || !isfinite(fm2) || !isfinite(fmx);
+        if (s_bad) {
+            raise_error(o.err, TGB_E_NONFINITE, static_cast<int32_t>(L.tensor), 0);
             bound = 0.0f;
-            s = 0.0f;
-        } else {
-            if ((L.flags & kLayerClip) && L.n >= 2) {
-                if (fm2 < 0.0) fm2 = 0.0;
-                const double sigma = sqrt(fm2 / static_cast<double>(L.n));  // codec.hpp:111
-                bound = static_cast<float>(static_cast<double>(o.clip_factor) * sigma);  // :119
-            }
-            s = fminf(fmx, bound);  // == scaler(clip(g)) (codec.hpp:121-122, :130)
+        } else if (clip && tn >= 2) {
+            if (fm2 < 0.0) fm2 = 0.0;
+            const double sigma = sqrt(fm2 / static_cast<double>(tn));  // codec.hpp:111
+            bound = static_cast<float>(static_cast<double>(o.clip_factor) * sigma);  // :119
         }
-        o.bounds[layer] = bound;
-        put_slot(o, L.slot, s);
-        o.layer_done[layer] = 0u;  // self-reset for the next launch
-        if (o.global_bucketing) {
+        s_bound = bound;
+        if (!o.tensors) {  // single layer: one block
+            o.bounds[0] = bound;
+            put_slot(o, L.slot, s_bad ? 0.0f : fminf(fmx, bound));
+        }
+        o.layer_done[L.tensor] = 0u;  // self-reset for the next launch
+    }
+    Bar::sync();
+    if (o.tensors) {
+        // per block: s = max |clip(part)| = min(max |part|, bound) (codec.hpp:121-122, :229-230)
+        const TensorDev T = o.tensors[L.tensor];
+        for (uint32_t b = T.first_block + tid; b < T.first_block + T.n_blocks; b += kThreads) {
+            const uint2 u = o.block_units[b];
+            float bm = 0.0f;
+            for (uint32_t c = u.x; c < u.x + u.y; ++c) bm = fmaxf(bm, __ldcg(&o.partials[c].mx));
+            o.bounds[b] = s_bound;
+            put_slot(o, o.layers[b].slot, s_bad ? 0.0f : fminf(bm, s_bound));
+        }
+        Bar::sync();
+        if (tid == 0 && o.global_bucketing) {
             __threadfence();
             const uint32_t t = atomicAdd(o.global_done, 1u);
             if (t == static_cast<uint32_t>(o.n_active_layers) - 1) {

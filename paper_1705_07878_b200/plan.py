@@ -97,9 +97,12 @@ class Plan:
         self.worker, self.n_workers = int(worker), int(n_workers)
         L = load()
         nl = len(self.names)
+        if passthrough is None:  # CodecConfig::passthrough / float_mode (cluster.hpp:274-275)
+            passthrough = [cfg.float_mode or name in cfg.passthrough for name in self.names]
+        self.passthrough = [bool(x) for x in passthrough]
         descs = (_lib.LayerDesc * max(nl, 1))()
         for l, (name, n) in enumerate(zip(self.names, self.ns)):
-            flags = _lib.TGB_LAYER_PASSTHROUGH if passthrough is not None and passthrough[l] else 0
+            flags = _lib.TGB_LAYER_PASSTHROUGH if self.passthrough[l] else 0
             descs[l] = _lib.LayerDesc(n, fnv1a64(name), flags, 0)
         params = cfg.params()
         h = C.c_void_p()
@@ -116,13 +119,20 @@ class Plan:
             check(L.tgb_plan_layer_layout(h, l, C.byref(off), C.byref(slot)), "layout")
             self.code_offsets.append(off.value)
             self.slots.append(slot.value)
+        # blocks of the encoded gradient (EncodedGradient::blocks, codec.hpp:70-76)
+        self.blocks: List[_lib.BlockInfo] = []
+        for b in range(info.n_blocks):
+            bi = _lib.BlockInfo()
+            check(L.tgb_plan_block_info(h, b, C.byref(bi)), "tgb_plan_block_info")
+            self.blocks.append(bi)
         push, gathered, bounds = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(L.tgb_plan_buffers(h, C.byref(push), C.byref(gathered), C.byref(bounds)), "buffers")
         self.push = _view(push.value or 0, info.push_bytes, self.device)
         self.gathered = _view(gathered.value or 0, info.push_bytes * self.n_workers
                               if self.n_workers > 1 else 0, self.device)
-        self.bounds = _view(bounds.value or 0, 4 * nl, self.device).view(torch.float32) \
-            if nl else torch.empty(0, device=self.device)
+        nb = len(self.blocks)  # clip bound per block (its tensor's bound)
+        self.bounds = _view(bounds.value or 0, 4 * nb, self.device).view(torch.float32) \
+            if nb else torch.empty(0, device=self.device)
         self._grads = self._outs = None
         self.attached = False
         self.grouped = info.n_groups == 2  # tgb_step overlaps the dominant layer with the rest
@@ -201,27 +211,54 @@ class Plan:
             check(st, "tgb_check")
         return e
 
+    def block_of(self, layer: int, index: int) -> int:
+        """block holding element `index` of `layer` (first block if none)."""
+        first = None
+        for b, bi in enumerate(self.blocks):
+            if bi.layer == layer:
+                first = b if first is None else first
+                if bi.offset <= index < bi.offset + bi.n:
+                    return b
+        return first if first is not None else -1
+
     def raise_errors(self):
+        """Rethrow the device error word with the reference's CodecError text."""
         e = self.error()
         if e.flags:
             name = self.names[e.layer] if 0 <= e.layer < len(self.names) else "?"
+            b = self.block_of(e.layer, e.index) if 0 <= e.layer < len(self.names) else -1
+            k = e.index - self.blocks[b].offset if b >= 0 else e.index
             if e.flags & _lib.TGB_E_NONFINITE:
                 raise CodecError("encode_step: non-finite gradient " + name)
             if e.flags & _lib.TGB_E_CORRUPT_CODE:
-                raise CodecError(f"corrupt ternary code 11 in block {name} at element {e.index}")
+                raise CodecError(f"corrupt ternary code 11 in block {name} at element {k}")
+            if e.flags & _lib.TGB_E_PEER_TIMEOUT:
+                raise CodecError(f"fused exchange: peer {e.index} never reached the step barrier")
             raise CodecError(f"codec error flags {e.flags:#x} in {name}")
 
     def scalers(self) -> torch.Tensor:
+        """this worker's scaler slots (one per ternary block, canonical order)"""
         push, _ = self.last_buffers()
-        return push[:4 * len(self.ns)].view(torch.float32)
+        return push[:4 * self.info.n_slots].view(torch.float32)
 
-    def layer_codes(self, l: int, worker: Optional[int] = None) -> torch.Tensor:
-        nb = (self.ns[l] + 3) // 4
+    def block_region(self, b: int, worker: Optional[int] = None) -> torch.Tensor:
+        """block b's packed codes (uint8) or raw values (float32) in the last
+        step's own push area, or in worker `worker`'s area of the gather buffer"""
+        bi = self.blocks[b]
+        raw = bool(bi.flags & _lib.TGB_LAYER_PASSTHROUGH)
+        nbytes = 4 * bi.n if raw else (bi.n + 3) // 4
         push, gathered = self.last_buffers()
         if worker is None:
-            return push[self.code_offsets[l]:self.code_offsets[l] + nb]
-        base = worker * self.info.push_bytes + self.code_offsets[l]
-        return gathered[base:base + nb]
+            r = push[bi.region_offset:bi.region_offset + nbytes]
+        else:
+            base = worker * self.info.push_bytes + bi.region_offset
+            r = gathered[base:base + nbytes]
+        return r.view(torch.float32) if raw else r
+
+    def layer_codes(self, l: int, worker: Optional[int] = None) -> torch.Tensor:
+        """codes of layer l's first block (the whole layer unless FixedSize)"""
+        return self.block_region(next(b for b, bi in enumerate(self.blocks) if bi.layer == l),
+                                 worker)
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:

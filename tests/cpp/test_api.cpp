@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <fstream>
 #include <string>
+#include <variant>
 #include <vector>
 
 #include "tgb/terngrad.hpp"
@@ -42,7 +43,10 @@ int main(int argc, char** argv) {
     for (int w = 0; w < 2; ++w) {
         auto r = tgb::encode_step(grads[w], cfg, 3, static_cast<uint16_t>(w));
         put(f, r.local_scalers.data(), r.local_scalers.size() * 4);
-        for (auto& b : r.encoded.blocks) put(f, b.codes.data(), b.codes.size());
+        for (auto& b : r.encoded.blocks) {
+            const auto& tb = std::get<tgb::TernaryBlock>(b);
+            put(f, tb.codes.data(), tb.codes.size());
+        }
         enc.push_back(std::move(r.encoded));
     }
     // 2. average over the two workers (codec.hpp:245-311), shared and unshared
@@ -82,6 +86,32 @@ int main(int argc, char** argv) {
         msg = e.what();
     }
     put(f, msg.data(), msg.size());
+    // 5. FixedSize(k = 1000) buckets + a passthrough tensor (codec.hpp:206-236, 269-279)
+    tgb::CodecConfig fx = cfg;
+    fx.bucketing = tgb::Bucketing::FixedSize;
+    fx.bucket_size = 1000;
+    fx.passthrough = {"conv.bias"};
+    std::vector<tgb::EncodedGradient> enc2;
+    for (int w = 0; w < 2; ++w) {
+        auto r = tgb::encode_step(grads[w], fx, 5, static_cast<uint16_t>(w));
+        put(f, r.local_scalers.data(), r.local_scalers.size() * 4);
+        std::vector<uint8_t> cat;
+        for (auto& b : r.encoded.blocks) {
+            if (const auto* tb = std::get_if<tgb::TernaryBlock>(&b))
+                cat.insert(cat.end(), tb->codes.begin(), tb->codes.end());
+            else  // passthrough values come back verbatim
+                put(f, std::get<tgb::PassthroughBlock>(b).values.data(),
+                    std::get<tgb::PassthroughBlock>(b).values.size() * 4);
+        }
+        put(f, cat.data(), cat.size());
+        enc2.push_back(std::move(r.encoded));
+    }
+    for (bool sharing : {true, false}) {
+        auto avg = tgb::average(enc2, 2, sharing);
+        std::vector<float> flat;
+        for (auto& a : avg) flat.insert(flat.end(), a.values.begin(), a.values.end());
+        put(f, flat.data(), flat.size() * 4);
+    }
     std::printf("cpp api ok: %s\n", msg.c_str());
     return 0;
 }

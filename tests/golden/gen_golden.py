@@ -34,13 +34,13 @@ def f32hex(a) -> str:
     return np.ascontiguousarray(a, dtype=np.float32).tobytes().hex()
 
 
-def enc_case(name, tensors, cfg, t, worker, store_inputs=True):
+def enc_case(name, tensors, cfg, t, worker, store_inputs=True, passthrough=None):
     names = [n for n, _ in tensors]
     grads = [make_input(r) for _, r in tensors]
-    (st, msg), blocks, scal = ref.encode_step(names, grads, cfg, t, worker)
-    bounds = []
-    for g in grads:
-        if cfg.clipping_enabled and g.size >= 2:
+    (st, msg), blocks, scal = ref.encode_step(names, grads, cfg, t, worker, passthrough)
+    bounds = []  # clip bound per tensor; passthrough tensors are never clipped (codec.hpp:206)
+    for i, g in enumerate(grads):
+        if cfg.clipping_enabled and g.size >= 2 and not (passthrough and passthrough[i]):
             _, b = ref.clip(g, cfg.clip_factor)
         else:
             b = float("inf")
@@ -53,19 +53,25 @@ def enc_case(name, tensors, cfg, t, worker, store_inputs=True):
         "tensors": [{"name": n, "recipe": r, "n": int(g.size), "input_sha256": sha(g),
                      **({"input_hex": f32hex(g)} if store_inputs else {})}
                     for (n, r), g in zip(tensors, grads)],
+        **({"passthrough": [int(x) for x in passthrough]} if passthrough else {}),
         "status": st, "error": msg,
-        "scalers_hex": f32hex(scal),
         "bounds_hex": f32hex(np.array(bounds, dtype=np.float32)),
-        "codes": [bytes(b).hex() if store_inputs else None for b in blocks],
-        "codes_sha256": [sha(b) for b in blocks],
+        "n_blocks": len(blocks),
     }
+    if len(blocks) <= 64:
+        case.update({"scalers_hex": f32hex(scal),
+                     "codes": [bytes(b).hex() if store_inputs else None for b in blocks],
+                     "codes_sha256": [sha(b) for b in blocks]})
+    else:  # many buckets: digests of the concatenations keep the fixture small
+        case.update({"scalers_sha256": sha(np.asarray(scal, np.float32)),
+                     "codes_concat_sha256": sha(np.concatenate(blocks))})
     return case
 
 
-def avg_case(name, tensors, cfg, t, N, store=True):
+def avg_case(name, tensors, cfg, t, N, store=True, passthrough=None):
     names = [n for n, _ in tensors]
     gw = [[make_input(dict(r, worker=w)) for _, r in tensors] for w in range(N)]
-    (st, msg), out = ref.average_encoded(names, gw, cfg, t)
+    (st, msg), out = ref.average_encoded(names, gw, cfg, t, passthrough)
     return {
         "name": name, "t": t, "N": N,
         "cfg": {"clip_factor": cfg.clip_factor, "clipping_enabled": cfg.clipping_enabled,
@@ -73,6 +79,7 @@ def avg_case(name, tensors, cfg, t, N, store=True):
                 "scaler_sharing": cfg.scaler_sharing, "seed": cfg.seed},
         "tensors": [{"name": n, "recipe": r, "n": int(gw[0][i].size)}
                     for i, (n, r) in enumerate(tensors)],
+        **({"passthrough": [int(x) for x in passthrough]} if passthrough else {}),
         "status": st, "error": msg,
         "out_sha256": sha(out),
         **({"out_hex": f32hex(out)} if store else {}),
@@ -151,6 +158,25 @@ def main():
     enc.append(enc_case("multi_global_noclip", multi, Config(seed=42, bucketing=1,
                                                              clipping_enabled=False), 2, 0,
                         store_inputs=False))
+    # FixedSize(k) buckets (codec.hpp:226-236): k % 4 != 0 shifts the RNG lanes
+    # against the code bytes; k = 1 is the clip-equals-bucket case (codec_test 241-254)
+    for k in (1, 3, 4, 5, 7, 64, 1000, 16385, 40000):
+        enc.append(enc_case(f"fixed_k{k}", multi, Config(seed=42, bucketing=2, bucket_size=k),
+                            6, 1, store_inputs=False))
+    enc.append(enc_case("fixed_k13_noclip", multi, Config(seed=42, bucketing=2, bucket_size=13,
+                                                          clipping_enabled=False), 1, 2,
+                        store_inputs=False))
+    # passthrough tensors (codec.hpp:206-209, 221-224), alone and with buckets / Global
+    pt = [0, 1, 0, 0, 1]
+    enc.append(enc_case("passthrough_per_tensor", multi, Config(seed=42), 2, 1,
+                        store_inputs=False, passthrough=pt))
+    enc.append(enc_case("passthrough_global", multi, Config(seed=42, bucketing=1), 2, 1,
+                        store_inputs=False, passthrough=pt))
+    enc.append(enc_case("passthrough_fixed_k6", multi, Config(seed=42, bucketing=2,
+                                                              bucket_size=6), 2, 1,
+                        store_inputs=False, passthrough=[1, 0, 0, 0, 0]))
+    enc.append(enc_case("float_mode", multi, Config(seed=42), 2, 1, store_inputs=False,
+                        passthrough=[1] * len(multi)))
     g["encode"] = enc
 
     # --- average across workers (inputs per worker from recipe + worker) ---
@@ -166,6 +192,23 @@ def main():
             avg.append(avg_case(f"avg_tiny_N{N}_{'shared' if sharing else 'unshared'}", tiny,
                                 Config(seed=42, scaler_sharing=sharing, clipping_enabled=False),
                                 0, N, store=True))
+    for N in (2, 3):
+        for sharing in (True, False):
+            sh = "shared" if sharing else "unshared"
+            avg.append(avg_case(f"avg_fixed_k5_N{N}_{sh}", multi,
+                                Config(seed=42, scaler_sharing=sharing, bucketing=2,
+                                       bucket_size=5), 3, N, store=False))
+            avg.append(avg_case(f"avg_fixed_k1000_N{N}_{sh}", multi,
+                                Config(seed=42, scaler_sharing=sharing, bucketing=2,
+                                       bucket_size=1000), 3, N, store=False))
+            avg.append(avg_case(f"avg_passthrough_N{N}_{sh}", multi,
+                                Config(seed=42, scaler_sharing=sharing), 3, N, store=False,
+                                passthrough=[0, 1, 0, 0, 1]))
+    avg.append(avg_case("avg_float_mode_N3", multi, Config(seed=42), 3, 3, store=False,
+                        passthrough=[1] * len(multi)))
+    avg.append(avg_case("avg_passthrough_fixed_k7_N2", multi,
+                        Config(seed=42, bucketing=2, bucket_size=7), 3, 2, store=False,
+                        passthrough=[0, 0, 0, 1, 0]))
     g["average"] = avg
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:

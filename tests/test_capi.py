@@ -98,3 +98,15 @@ def test_push_layout():
     assert lay.code_bytes == 2 + 0 + 4 + 250001
     assert lay.push_bytes % 256 == 0 and lay.push_bytes >= 288 + 250001
     assert all(o % 16 == 0 for o in lay.code_offsets)
+
+
+def test_push_layout_blocks():
+    # FixedSize k = 6 over [13, 0, 3] with layer 2 passthrough:
+    # blocks (0,0,6) (0,6,6) (0,12,1) (1,0,0) | raw (2,0,3)
+    lay = push_layout([13, 0, 3], [False, False, True], bucketing=2, bucket_size=6)
+    assert [(b.layer, b.offset, b.n, b.slot) for b in lay.blocks] == \
+        [(0, 0, 6, 0), (0, 6, 6, 1), (0, 12, 1, 2), (1, 0, 0, 3), (2, 0, 3, -1)]
+    assert lay.n_slots == 4 and lay.codes_offset == 256
+    assert [b.region_offset for b in lay.blocks] == [256, 272, 288, 304, 304]
+    assert lay.blocks[-1].nbytes == 12 and lay.code_bytes == 2 + 2 + 1 + 0
+    assert lay.push_bytes == 512

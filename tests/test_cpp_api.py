@@ -15,6 +15,7 @@ import pytest
 import torch
 
 from oracle.oracle import Config
+from tests.golden.check import restated_average
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "build", "tgb_cpp_api_test")
@@ -93,3 +94,18 @@ def test_cpp_api_matches_oracle(restated):
     assert sec[i] == dec.tobytes(); i += 1
     msg = sec[i].decode()
     assert msg.startswith("ternarize: scaler 0.000000 below max |g| in fc.weight"), msg
+    i += 1
+    # FixedSize(1000) + passthrough conv.bias
+    fx = Config(seed=42, bucketing=2, bucket_size=1000)
+    pt = [0, 1, 0]
+    for w in range(2):
+        st, blocks, sc, _, _ = restated.encode_step(NAMES, grads[w], fx, 5, w, pt)
+        assert st == 0
+        assert sec[i] == sc.tobytes(); i += 1
+        assert sec[i] == grads[w][1].tobytes(); i += 1
+        assert sec[i] == b"".join(bytes(b) for b in blocks); i += 1
+    for sharing in (True, False):
+        fx.scaler_sharing = sharing
+        flat = restated_average(restated, NAMES, grads, fx, 5, pt)
+        assert sec[i] == flat.tobytes(), sharing; i += 1
+    assert i == len(sec)

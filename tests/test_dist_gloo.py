@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, ws, port, sharing, q):
+def _worker(rank, ws, port, sharing, bucket, pt, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -49,27 +49,35 @@ def _worker(rank, ws, port, sharing, q):
 
         # 2. encode (oracle stands in for K1/K2), pack, allgather, unpack, decode
         R = Restated()
-        cfg = Config(seed=42, scaler_sharing=sharing)
+        cfg = Config(seed=42, scaler_sharing=sharing, bucketing=2 if bucket else 0,
+                     bucket_size=bucket)
         grads = [R.normal(100 + rank, 0, "mp/" + n, k, 1e-2) for n, k in zip(NAMES, SIZES)]
-        st, blocks, scal, _, _ = R.encode_step(NAMES, grads, cfg, 7, rank)
+        st, blocks, scal, _, _ = R.encode_step(NAMES, grads, cfg, 7, rank, pt)
         assert st == 0
-        lay = push_layout(SIZES)
-        mine = torch.frombuffer(bytearray(pack_push(lay, scal, blocks)), dtype=torch.uint8)
+        lay = push_layout(SIZES, pt, cfg.bucketing, bucket)
+        tern = iter(blocks)
+        regions = [grads[b.layer].tobytes() if b.passthrough else bytes(next(tern))
+                   for b in lay.blocks]
+        mine = torch.frombuffer(bytearray(pack_push(lay, scal, regions)), dtype=torch.uint8)
         gathered = torch.empty(ws * lay.push_bytes, dtype=torch.uint8)
         dist.all_gather_into_tensor(gathered, mine)
-        sc, cs = unpack_gathered(lay, bytes(gathered.numpy()), ws)
+        sc, rs = unpack_gathered(lay, bytes(gathered.numpy()), ws)
         out = []
-        for l, n in enumerate(SIZES):
-            st, avg = R.average_block([sc[w][l] for w in range(ws)],
-                                      [np.frombuffer(cs[w][l], np.uint8) for w in range(ws)],
-                                      n, sharing)
+        for i, b in enumerate(lay.blocks):  # K3 per block (codec.hpp:268-307)
+            if b.passthrough:
+                out.append(R.average_passthrough([np.frombuffer(rs[w][i], np.float32)
+                                                  for w in range(ws)]))
+                continue
+            st, avg = R.average_block([sc[w][b.slot] for w in range(ws)],
+                                      [np.frombuffer(rs[w][i], np.uint8) for w in range(ws)],
+                                      b.n, sharing)
             assert st == 0
             out.append(avg)
         flat = np.concatenate(out)
         allg = [None] * ws
         dist.all_gather_object(allg, grads)
         if rank == 0 and os.path.exists(REF_SO):
-            (st, msg), ref = Reference().average_encoded(NAMES, allg, cfg, 7)
+            (st, msg), ref = Reference().average_encoded(NAMES, allg, cfg, 7, pt)
             assert st == 0, msg
             assert np.array_equal(ref.view(np.uint32), flat.view(np.uint32))
         hs = [None] * ws
@@ -81,12 +89,18 @@ def _worker(rank, ws, port, sharing, q):
         q.put((rank, repr(e)))
 
 
-@pytest.mark.parametrize("sharing", [True, False])
-def test_two_rank_exchange_layout_gloo(sharing):
+@pytest.mark.parametrize("sharing,bucket,pt", [
+    (True, 0, None), (False, 0, None),
+    (True, 1000, [0, 1, 0, 0, 0]),   # FixedSize buckets + a passthrough tensor
+    (False, 7, [0, 0, 0, 0, 1]),     # k % 4 != 0
+])
+def test_two_rank_exchange_layout_gloo(sharing, bucket, pt):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, sharing, q)) for r in range(2)]
+    pt = pt or [0] * len(NAMES)
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, sharing, bucket, pt, q))
+          for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=240) for _ in ps)

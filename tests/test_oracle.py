@@ -13,7 +13,8 @@ import math
 import numpy as np
 import pytest
 
-from oracle.oracle import Config, RefCluster
+from oracle.oracle import Config, RefCluster, block_layout
+from tests.golden.check import check_codes, check_scalers, passthrough_of, restated_average
 from tests.golden.recipes import make_input
 
 
@@ -85,10 +86,10 @@ def test_restated_matches_golden_encode(restated, golden):
         for t, g in zip(case["tensors"], grads):
             assert sha(g) == t["input_sha256"], (case["name"], t["name"])
         st, blocks, sc, bounds, _ = restated.encode_step(names, grads, cfg, case["t"],
-                                                         case["worker"])
+                                                         case["worker"], passthrough_of(case))
         assert st == case["status"], case["name"]
-        assert sc.tobytes().hex() == case["scalers_hex"], case["name"]
-        assert [sha(b) for b in blocks] == case["codes_sha256"], case["name"]
+        check_scalers(case, sc)
+        check_codes(case, blocks)
         assert bounds.tobytes().hex() == case["bounds_hex"], case["name"]
 
 
@@ -96,21 +97,9 @@ def test_restated_matches_golden_average(restated, golden):
     for case in golden["average"]:
         cfg = cfg_of(case["cfg"])
         names = [t["name"] for t in case["tensors"]]
-        N = case["N"]
-        enc = []
-        for w in range(N):
-            grads = [make_input(dict(t["recipe"], worker=w)) for t in case["tensors"]]
-            st, blocks, sc, _, _ = restated.encode_step(names, grads, cfg, case["t"], w)
-            assert st == 0
-            enc.append((blocks, sc))
-        out = []
-        for b in range(len(names)):
-            n = case["tensors"][b]["n"]
-            st, o = restated.average_block([e[1][b] for e in enc], [e[0][b] for e in enc], n,
-                                           cfg.scaler_sharing)
-            assert st == 0
-            out.append(o)
-        flat = np.concatenate(out) if out else np.zeros(0, np.float32)
+        gw = [[make_input(dict(t["recipe"], worker=w)) for t in case["tensors"]]
+              for w in range(case["N"])]
+        flat = restated_average(restated, names, gw, cfg, case["t"], passthrough_of(case))
         assert sha(flat) == case["out_sha256"], case["name"]
         if "out_hex" in case:
             assert flat.tobytes().hex() == case["out_hex"]

@@ -14,6 +14,7 @@ import torch
 
 import paper_1705_07878_b200 as tg
 from oracle.oracle import Config
+from tests.golden.check import check_codes, check_scalers, passthrough_of
 from tests.golden.recipes import make_input
 
 pytestmark = pytest.mark.gpu
@@ -35,9 +36,10 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(DEV)
 
 
-def plan_encode(names, grads, cfg, t, worker, n_workers=1):
+def plan_encode(names, grads, cfg, t, worker, n_workers=1, passthrough=None):
     ns = [int(g.size) for g in grads]
-    plan = tg.Plan(names, ns, cfg, worker=worker, n_workers=n_workers, device=DEV)
+    plan = tg.Plan(names, ns, cfg, worker=worker, n_workers=n_workers, device=DEV,
+                   passthrough=passthrough)
     gflat, gviews = tg.aligned_flat(ns, DEV)
     oflat, oviews = tg.aligned_flat(ns, DEV)
     for v, g in zip(gviews, grads):
@@ -47,9 +49,19 @@ def plan_encode(names, grads, cfg, t, worker, n_workers=1):
     plan.raise_errors()
     torch.cuda.synchronize()
     scal = plan.scalers().cpu().numpy().copy()
-    codes = [plan.layer_codes(l).cpu().numpy().copy() for l in range(len(ns))]
+    codes = [plan.block_region(b).cpu().numpy().copy() for b, bi in enumerate(plan.blocks)
+             if not bi.flags & 1]
     bounds = plan.bounds.cpu().numpy().copy()
     return plan, scal, codes, bounds, (gflat, gviews, oflat, oviews)
+
+
+def tensor_bounds(plan, bounds):
+    """per-tensor clip bound from the per-block array (inf for passthrough)"""
+    out = np.full(len(plan.ns), np.inf, np.float32)
+    for b, bi in enumerate(plan.blocks):
+        if not bi.flags & 1 and bi.offset == 0:
+            out[bi.layer] = bounds[b]
+    return out
 
 
 # ----------------------------------------------------------------- rng
@@ -68,15 +80,24 @@ def test_encode_step_golden(golden):
         cfg = cfg_of(case["cfg"])
         names = [t["name"] for t in case["tensors"]]
         grads = [make_input(t["recipe"]) for t in case["tensors"]]
-        plan, scal, codes, bounds, _ = plan_encode(names, grads, cfg, case["t"], case["worker"])
-        assert scal.tobytes().hex() == case["scalers_hex"], case["name"]
-        assert [sha(c) for c in codes] == case["codes_sha256"], case["name"]
-        assert bounds.tobytes().hex() == case["bounds_hex"], case["name"]
-        # the reference-shaped API returns the same blocks
+        pt = passthrough_of(case)
+        plan, scal, codes, bounds, _ = plan_encode(names, grads, cfg, case["t"], case["worker"],
+                                                   passthrough=pt)
+        check_scalers(case, scal)
+        check_codes(case, codes)
+        assert tensor_bounds(plan, bounds).tobytes().hex() == case["bounds_hex"], case["name"]
+        # the reference-shaped API returns the same blocks; passthrough blocks verbatim
+        cfg.passthrough = {n for n, p in zip(names, pt) if p}
         res = tg.encode_step([tg.GradTensor(n, [g.size], to_dev(g)) for n, g in zip(names, grads)],
                              cfg, case["t"], case["worker"])
-        assert [sha(b.codes.cpu().numpy()) for b in res.encoded.blocks] == case["codes_sha256"]
-        assert np.array(res.local_scalers, np.float32).tobytes().hex() == case["scalers_hex"]
+        tern = [b for b in res.encoded.blocks if isinstance(b, tg.TernaryBlock)]
+        check_codes(case, [b.codes.cpu().numpy() for b in tern])
+        check_scalers(case, res.local_scalers)
+        raw = [b for b in res.encoded.blocks if isinstance(b, tg.PassthroughBlock)]
+        want = [g for g, p in zip(grads, pt) if p]
+        assert len(raw) == len(want)
+        for b, g in zip(raw, want):
+            assert b.values.cpu().numpy().tobytes() == np.asarray(g, np.float32).tobytes()
         plan.close()
 
 
@@ -181,6 +202,8 @@ def test_average_golden(golden):
     for case in golden["average"]:
         cfg = cfg_of(case["cfg"])
         names = [t["name"] for t in case["tensors"]]
+        pt = passthrough_of(case)
+        cfg.passthrough = {n for n, p in zip(names, pt) if p}
         N = case["N"]
         encs, pushes, plans = [], [], []
         for w in range(N):
@@ -188,7 +211,8 @@ def test_average_golden(golden):
             res = tg.encode_step([tg.GradTensor(n, [g.size], to_dev(g))
                                   for n, g in zip(names, grads)], cfg, case["t"], w)
             encs.append(res.encoded)
-            plan, _, _, _, bufs = plan_encode(names, grads, cfg, case["t"], w, n_workers=N)
+            plan, _, _, _, bufs = plan_encode(names, grads, cfg, case["t"], w, n_workers=N,
+                                              passthrough=pt)
             pushes.append(plan.push.clone())
             plans.append((plan, bufs))
         # reference-shaped average (codec.hpp:245-311)
@@ -204,6 +228,12 @@ def test_average_golden(golden):
         plan.raise_errors()
         out = torch.cat([v for v in oviews]).cpu().numpy()
         assert sha(out) == case["out_sha256"], case["name"] + " (plan)"
+        # the whole step at N = 1 (K2 writes the decoded output) equals average([enc])
+        if N == 1:
+            plan.step(case["t"])
+            plan.raise_errors()
+            out = torch.cat([v for v in oviews]).cpu().numpy()
+            assert sha(out) == case["out_sha256"], case["name"] + " (step)"
         for p, _ in plans:
             p.close()
 
@@ -285,13 +315,55 @@ def test_vgg16_step_properties():
         assert all(v in (-sc[l], 0.0, sc[l]) for v in vals.tolist())
 
 
-def test_plan_layout_matches_host_restatement():
+@pytest.mark.parametrize("bucketing,k,pt", [(0, 0, None), (2, 6, [0, 0, 1, 0, 0, 1]),
+                                             (2, 4096, None), (1, 0, [1, 0, 0, 0, 0, 0])])
+def test_plan_layout_matches_host_restatement(bucketing, k, pt):
     from paper_1705_07878_b200.layout import push_layout
 
     ns = [5, 0, 16, 1000003, 4096, 7]
-    plan = tg.Plan([f"l{i}" for i in range(len(ns))], ns, tg.CodecConfig(), device=DEV)
-    lay = push_layout(ns)
+    cfg = tg.CodecConfig(bucketing=tg.Bucketing(bucketing), bucket_size=k)
+    plan = tg.Plan([f"l{i}" for i in range(len(ns))], ns, cfg, device=DEV, passthrough=pt)
+    lay = push_layout(ns, pt, bucketing, k)
     assert plan.code_offsets == lay.code_offsets
     assert plan.info.push_bytes == lay.push_bytes
     assert plan.info.code_bytes == lay.code_bytes
+    assert plan.info.n_slots == lay.n_slots
+    assert [(b.layer, b.offset, b.n, b.slot, b.region_offset) for b in plan.blocks] == \
+        [(b.layer, b.offset, b.n, b.slot, b.region_offset) for b in lay.blocks]
     plan.close()
+
+
+# ------------------------------------------- FixedSize / passthrough at size
+@pytest.mark.parametrize("k", [1000, 4097, (1 << 20) + 3, 3 << 20])
+def test_fixed_size_large_vs_oracle(restated, k):
+    names = ["fc.weight", "fc.bias", "conv.weight"]
+    grads = [restated.normal(21, 0, "fx/" + n, m, 1e-3) for n, m in
+             zip(names, [(1 << 22) + 5, 1001, 300000])]
+    cfg = Config(seed=42, bucketing=2, bucket_size=k)
+    st, blocks, sc, _, _ = restated.encode_step(names, grads, cfg, 11, 3)
+    assert st == 0
+    plan, scal, codes, _, _ = plan_encode(names, grads, cfg_of(cfg.__dict__), 11, 3)
+    assert scal.tobytes() == np.asarray(sc, np.float32).tobytes()
+    assert len(codes) == len(blocks)
+    assert np.concatenate(codes).tobytes() == np.concatenate(blocks).tobytes()
+    plan.close()
+
+
+def test_passthrough_and_bucket_errors():
+    nan = np.array([1.0, 2.0, np.nan, 4.0, 5.0], np.float32)
+    ok = np.array([0.5, -0.25, 0.125], np.float32)
+    cfg = tg.CodecConfig(passthrough={"p"})
+    with pytest.raises(tg.CodecError, match="encode_step: non-finite gradient p"):
+        tg.encode_step([tg.GradTensor("w", [3], to_dev(ok)), tg.GradTensor("p", [5], to_dev(nan))],
+                       cfg, 0, 0)
+    cfg = tg.CodecConfig(bucketing=tg.Bucketing.FixedSize, bucket_size=2)
+    with pytest.raises(tg.CodecError, match="encode_step: non-finite gradient q"):
+        tg.encode_step([tg.GradTensor("w", [3], to_dev(ok)), tg.GradTensor("q", [5], to_dev(nan))],
+                       cfg, 0, 0)
+    # a corrupt code in the 2nd bucket reports the element inside that bucket
+    res = tg.encode_step([tg.GradTensor("w", [9], to_dev(np.arange(9, dtype=np.float32)))],
+                         tg.CodecConfig(bucketing=tg.Bucketing.FixedSize, bucket_size=5), 0, 0)
+    blk = res.encoded.blocks[1]
+    blk.codes[0] = 0b00110000  # element 2 of the bucket
+    with pytest.raises(tg.CodecError, match="corrupt ternary code 11 in block w at element 2"):
+        tg.average([res.encoded], 1, True)

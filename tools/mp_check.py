@@ -41,9 +41,18 @@ def main():
     names = ["conv1.weight", "conv1.bias", "empty", "fc.weight", "fc.bias"]
     sizes = [1728, 64, 0, 40003, 10]
     report = {"world_size": ws, "exchange": "fused" if FUSED else "nccl", "checks": {}}
-    for sharing, mode in [(True, tg.ShareMode.REF), (False, tg.ShareMode.REF),
-                          (True, tg.ShareMode.PRESHARED)]:
-        cfg = tg.CodecConfig(seed=42, scaler_sharing=sharing, share_mode=mode)
+    P, G, F = tg.Bucketing.PerTensor, tg.Bucketing.Global, tg.Bucketing.FixedSize
+    configs = [  # (sharing, mode, bucketing, k, passthrough names)
+        (True, tg.ShareMode.REF, P, 0, ()), (False, tg.ShareMode.REF, P, 0, ()),
+        (True, tg.ShareMode.PRESHARED, P, 0, ()), (True, tg.ShareMode.REF, G, 0, ()),
+        (True, tg.ShareMode.REF, F, 1000, ("conv1.bias",)),
+        (False, tg.ShareMode.REF, F, 7, ("fc.bias",)),
+        (True, tg.ShareMode.PRESHARED, F, 1000, ("conv1.bias",)),
+    ]
+    for sharing, mode, bucketing, k, pt_names in configs:
+        cfg = tg.CodecConfig(seed=42, scaler_sharing=sharing, share_mode=mode,
+                             bucketing=bucketing, bucket_size=k, passthrough=set(pt_names))
+        pt = [int(n in pt_names) for n in names]
         sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws, comm=comm,
                            device=dev, fused=FUSED)
         grads = [R.normal(100 + rank, 0, "mp/" + n, k, 1e-2) for n, k in zip(names, sizes)]
@@ -61,16 +70,17 @@ def main():
         dist.all_gather_object(hs, h)
         allg = [None] * ws
         dist.all_gather_object(allg, grads)
-        key = f"sharing={sharing},mode={mode.name}"
+        key = f"sharing={sharing},mode={mode.name},bucketing={bucketing.name}{k or ''}," \
+              f"passthrough={'+'.join(pt_names) or '-'}"
         ok_same = len(set(hs)) == 1
         ok_ref = None
         if rank == 0:
+            ocfg = Config(seed=42, scaler_sharing=sharing, bucketing=int(bucketing), bucket_size=k)
             if mode == tg.ShareMode.REF:
-                (st, msg), ref = Reference().average_encoded(
-                    names, allg, Config(seed=42, scaler_sharing=sharing), 7)
+                (st, msg), ref = Reference().average_encoded(names, allg, ocfg, 7, pt)
                 ok_ref = st == 0 and np.array_equal(ref.view(np.uint32), flat.view(np.uint32))
             else:  # PRESHARED: every worker ternarizes with s = max_w s_w (paper Eq. 4)
-                ok_ref = preshared_oracle(R, names, allg, flat, ws)
+                ok_ref = preshared_oracle(R, names, allg, flat, ws, ocfg, pt)
         report["checks"][key] = {"ranks_identical": ok_same, "matches_oracle": ok_ref}
         dist.barrier()
         sw.plan.close()
@@ -125,27 +135,40 @@ def main():
     sys.exit(0 if ok else 1)
 
 
-def preshared_oracle(R, names, allg, flat, ws):
-    """Oracle for PRESHARED: clip per worker, s = max over workers of the local
-    scalers, ternarize every worker with that s (ternarize(name, g, s, rng, 0),
-    codec.hpp:148), then the shared-sum average."""
-    outs = []
+def preshared_oracle(R, names, allg, flat, ws, cfg, pt):
+    """Oracle for PRESHARED: per block, s = max over workers of the local
+    scalers; every worker ternarizes its clipped bucket with that s
+    (ternarize(name, part, s, rng, off), codec.hpp:148, :229), then the
+    shared-sum average; passthrough tensors take the fp64 mean."""
+    from oracle.oracle import block_layout
+
+    ns = [g.size for g in allg[0]]
+    local = []
+    for w in range(ws):
+        st, _, sc, _, _ = R.encode_step(names, allg[w], cfg, 7, w, pt)
+        if st:
+            return False
+        local.append(sc)
+    lay = block_layout(ns, cfg, pt)
+    outs, b = [], 0
     for li, name in enumerate(names):
-        n = allg[0][li].size
-        clipped, local = [], []
-        for w in range(ws):
-            c, _ = R.clip(allg[w][li], 2.5) if n >= 2 else (allg[w][li], 0)
-            clipped.append(c)
-            local.append(R.scaler(c))
-        s = max(local) if local else 0.0
-        codes = []
-        for w in range(ws):
-            st, cw = R.ternarize(clipped[w], s, 42, 7, name, w)
-            if st:
-                return False
-            codes.append(cw)
-        st, avg = R.average_block([s] * ws, codes, n, True)
-        outs.append(avg)
+        if pt[li]:
+            outs.append(R.average_passthrough([allg[w][li] for w in range(ws)]))
+            continue
+        clipped = [R.clip(allg[w][li], cfg.clip_factor)[0] if ns[li] >= 2 else allg[w][li]
+                   for w in range(ws)]
+        while b < len(lay) and lay[b][0] == li:
+            _, off, ln = lay[b]
+            s = max(float(local[w][b]) for w in range(ws))
+            codes = []
+            for w in range(ws):
+                st, cw = R.ternarize(clipped[w][off:off + ln], s, 42, 7, name, w, off)
+                if st:
+                    return False
+                codes.append(cw)
+            st, avg = R.average_block([s] * ws, codes, ln, True)
+            outs.append(avg)
+            b += 1
     ref = np.concatenate(outs)
     return bool(np.array_equal(ref.view(np.uint32), flat.view(np.uint32)))
 
