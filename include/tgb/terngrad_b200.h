@@ -95,8 +95,14 @@ typedef struct tgb_plan_info {
     uint32_t chunk_elems; /* elements per chunk */
     uint32_t n_groups;    /* tgb_step schedule: 1 sequential, 2 = dominant layer || rest */
     int32_t n_blocks;     /* blocks: buckets of ternary layers + one per passthrough layer */
-    int32_t reserved;
+    int32_t exchange;     /* TGB_EXCHANGE_*: how tgb_step moves data between ranks */
 } tgb_plan_info;
+
+#define TGB_EXCHANGE_NONE 0    /* n_workers == 1 */
+#define TGB_EXCHANGE_NCCL 1    /* ncclAllGather of push buffers, K3 on every rank */
+#define TGB_EXCHANGE_FUSED 2   /* K1/K2 store scalers + codes into every peer (NVLink) */
+#define TGB_EXCHANGE_SHARDED 3 /* codes to the chunk's owner, owner sums N workers and
+                                  stores packed sums into every peer, K3 decodes sums */
 
 /* One block of the encoded gradient (EncodedGradient::blocks, codec.hpp:70-76):
  * a bucket of a ternary layer (TernaryBlock, the whole layer unless FixedSize)

@@ -31,6 +31,7 @@ TGB_LAYER_PASSTHROUGH = 0x1
 TGB_BUCKET_PER_TENSOR, TGB_BUCKET_GLOBAL, TGB_BUCKET_FIXED = 0, 1, 2
 TGB_SHARE_REF, TGB_SHARE_PRESHARED = 0, 1
 UNIQUE_ID_BYTES = 128
+TGB_EXCHANGE_NONE, TGB_EXCHANGE_NCCL, TGB_EXCHANGE_FUSED, TGB_EXCHANGE_SHARDED = 0, 1, 2, 3
 
 # every symbol the header declares (checked by tests/test_capi.py)
 EXPORTS = [
@@ -63,7 +64,7 @@ class PlanInfo(C.Structure):
                 ("code_bytes", C.c_uint64), ("scaler_offset", C.c_uint64),
                 ("codes_offset", C.c_uint64), ("n_layers", C.c_int32), ("n_slots", C.c_int32),
                 ("n_chunks", C.c_int32), ("n_workers", C.c_int32), ("chunk_elems", C.c_uint32),
-                ("n_groups", C.c_uint32), ("n_blocks", C.c_int32), ("reserved", C.c_int32)]
+                ("n_groups", C.c_uint32), ("n_blocks", C.c_int32), ("exchange", C.c_int32)]
 
 
 class BlockInfo(C.Structure):

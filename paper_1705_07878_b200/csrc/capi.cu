@@ -89,12 +89,10 @@ struct tgb_plan {
     std::vector<TensorDev> h_tensors;
     std::vector<LayerDev> h_layers;     // BLOCKS (buckets / passthrough tensors)
     std::vector<uint64_t> block_off;    // block's first element inside its tensor
-    std::vector<uint2> h_units;         // per block: K1 work items {first (group-relative), count}
     std::vector<ChunkDev> h_chunks;     // K1/K2 work items (chunk12 elements, never straddle blocks)
     std::vector<ChunkDev> h_chunks3;    // K3 work items (kChunk3 elements)
     LayerDev* d_layers = nullptr;
     TensorDev* d_tensors = nullptr;
-    uint2* d_units = nullptr;
     ChunkFat* d_fat = nullptr;   // K1/K2: chunk + block copy (rebuilt on bind)
     ChunkFat* d_fat3 = nullptr;  // K3
     Partial* d_partials = nullptr;
@@ -126,6 +124,15 @@ struct tgb_plan {
     bool bound = false;
     int32_t k2_variant = 0;  // TGB_K2V
     int32_t k1_variant = 0;  // TGB_K1V
+    int32_t k3_variant = 1;  // TGB_K3V: 1 smem-staged (default, tools/k3_probe.py), 0 byte loads
+    // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
+    // K2 chunks [cs[r], cs[r+1]) and reduces them to packed sums for every rank.
+    // d_ipc = [gather parity 0][gather parity 1][sums parity 0][sums parity 1][flags]
+    bool shard_capable = false, shard = false;
+    int32_t nib = 1;  // 4-bit sums (N <= 7), else 8-bit
+    uint64_t sums_bytes = 0, sums_off = 0;
+    uint32_t cs[kMaxPeers + 1] = {};
+    uint32_t chunk3 = kChunk3;
     cudaStream_t last = nullptr;
 };
 
@@ -212,6 +219,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     P->p = *params;
     if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
+    if (const char* m = std::getenv("TGB_K3V")) P->k3_variant = std::atoi(m);
     P->worker = worker;
     P->n_workers = n_workers;
     P->desc.assign(layers, layers + n_layers);
@@ -231,6 +239,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
         const uint64_t v = std::strtoull(m, nullptr, 10);
         if (v >= 1024 && v % 1024 == 0) chunk3 = v;
     }
+    P->chunk3 = static_cast<uint32_t>(chunk3);
 
     // ---- tensors -> blocks, scaler slots
     P->h_tensors.resize(n_layers);
@@ -257,9 +266,9 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
             L.key0 = k0;
             L.key1 = k1;
             L.slot = pass ? -1 : slot++;
-            L.flags = (pass ? kLayerPassthrough : 0u) | T.flags;
+            L.flags = (pass ? kLayerPassthrough : 0u) | T.flags |
+                      (static_cast<uint32_t>(off & 3u) << kLayerShiftBit);
             L.rng_q = static_cast<uint32_t>(off >> 2);
-            L.rng_shift = static_cast<uint32_t>(off & 3u);
             P->h_layers.push_back(L);
             P->block_off.push_back(off);
             P->total += L.n;
@@ -294,7 +303,13 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     for (int32_t l = 0; l < n_layers; ++l)
         if (!(layers[l].flags & TGB_LAYER_PASSTHROUGH) && (big < 0 || layers[l].n > layers[big].n))
             big = l;
-    bool want = big >= 0 && n_layers > 1 && params->bucketing == TGB_BUCKET_PER_TENSOR &&
+    int shard_min = 3;  // measured: the allgather design wins at N = 2
+    if (const char* m = std::getenv("TGB_SHARD_MIN")) shard_min = std::max(2, std::atoi(m));
+    P->shard_capable = n_workers >= shard_min && n_workers <= kMaxPeers && params->scaler_sharing;
+    if (const char* m = std::getenv("TGB_SHARD")) P->shard_capable = P->shard_capable && std::atoi(m) != 0;
+    P->nib = n_workers <= 7 ? 1 : 0;
+    bool want = !P->shard_capable && big >= 0 && n_layers > 1 &&
+                params->bucketing == TGB_BUCKET_PER_TENSOR &&
                 params->share_mode == TGB_SHARE_REF && layers[big].n * 100 >= P->total * 35 &&
                 layers[big].n * 100 <= P->total * 95;
     if (const char* m = std::getenv("TGB_GROUPS")) want = want && std::atoi(m) != 0;
@@ -319,21 +334,41 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     P->cb[1] = P->cc[0];
     for (const ChunkDev& c : P->h_chunks3) ++P->cc3[group_of(c)];
     P->cb3[1] = P->cc3[0];
-    // K1 units (group-relative chunk indices) per block and per tensor
-    P->h_units.assign(nb, make_uint2(0, 0));
+    // K1 units (group-relative chunk indices) per tensor
     std::vector<uint2> tunits(n_layers, make_uint2(0, 0));
     for (uint32_t c = 0; c < P->h_chunks.size(); ++c) {
         const ChunkDev& ch = P->h_chunks[c];
         if (is_pass(ch)) continue;
         const uint32_t rel = c - P->cb[group_of(ch)];
-        uint2& u = P->h_units[ch.layer];
-        if (u.y++ == 0) u.x = rel;
         uint2& tu = tunits[P->h_layers[ch.layer].tensor];
         if (tu.y++ == 0) tu.x = rel;
     }
     for (LayerDev& L : P->h_layers) {
         L.first_chunk = tunits[L.tensor].x;
         L.n_chunks = tunits[L.tensor].y;
+    }
+    if (P->shard_capable) {
+        // sums regions: 2 (4-bit) or 4 (8-bit) bytes per code byte, raw fp32 means
+        uint64_t so = 0;
+        for (LayerDev& L : P->h_layers) {
+            L.sum_off16 = static_cast<uint32_t>(so / 16);
+            const uint64_t bytes = (L.flags & kLayerPassthrough) ? 4ull * L.n
+                                   : (P->nib ? 2ull : 4ull) * ((L.n + 3ull) / 4);
+            so += round_up(bytes, kAlignCodes);
+        }
+        P->sums_bytes = round_up(std::max<uint64_t>(so, 1), kAlignPush);
+        // owners: contiguous K2-chunk ranges balanced by K3a bytes (raw fp32 = 16x codes)
+        std::vector<uint64_t> cum(P->h_chunks.size() + 1, 0);
+        for (size_t c = 0; c < P->h_chunks.size(); ++c)
+            cum[c + 1] = cum[c] + P->h_chunks[c].count * (is_pass(P->h_chunks[c]) ? 16ull : 1ull);
+        const uint64_t W = cum.back();
+        for (int r = 0; r <= n_workers; ++r) {
+            const uint64_t target = W * static_cast<uint64_t>(r) / static_cast<uint64_t>(n_workers);
+            P->cs[r] = static_cast<uint32_t>(std::lower_bound(cum.begin(), cum.end(), target) -
+                                             cum.begin());
+        }
+        P->cs[n_workers] = static_cast<uint32_t>(P->h_chunks.size());
+        for (int r = n_workers + 1; r <= kMaxPeers; ++r) P->cs[r] = P->cs[n_workers];
     }
     if (P->grouped) {
         int lo = 0, hi = 0;
@@ -353,7 +388,6 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     const size_t nc = std::max<size_t>(1, P->h_chunks.size());
     bool ok = cudaMalloc(&P->d_layers, nbl * sizeof(LayerDev)) == cudaSuccess &&
               cudaMalloc(&P->d_tensors, nl * sizeof(TensorDev)) == cudaSuccess &&
-              cudaMalloc(&P->d_units, nbl * sizeof(uint2)) == cudaSuccess &&
               cudaMalloc(&P->d_fat, nc * sizeof(ChunkFat)) == cudaSuccess &&
               cudaMalloc(&P->d_fat3, std::max<size_t>(1, P->h_chunks3.size()) * sizeof(ChunkFat)) ==
                   cudaSuccess &&
@@ -364,7 +398,8 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
               cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess;
     if (ok && n_workers > 1) {
         const uint64_t g = P->push_bytes * static_cast<uint64_t>(n_workers);
-        P->flags_off = 2 * g;
+        P->sums_off = 2 * g;
+        P->flags_off = P->sums_off + 2 * P->sums_bytes;
         const uint64_t bytes = P->flags_off + round_up(2 * kMaxPeers * sizeof(uint64_t), kAlignPush);
         ok = cudaMalloc(&P->d_ipc, bytes) == cudaSuccess &&
              cudaMemset(P->d_ipc, 0, bytes) == cudaSuccess;
@@ -378,9 +413,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
              cudaSuccess;
     if (ok && nb > 0)
         ok = cudaMemcpy(P->d_layers, P->h_layers.data(), nb * sizeof(LayerDev),
-                        cudaMemcpyHostToDevice) == cudaSuccess &&
-             cudaMemcpy(P->d_units, P->h_units.data(), nb * sizeof(uint2), cudaMemcpyHostToDevice) ==
-                 cudaSuccess;
+                        cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok && n_layers > 0)
         ok = cudaMemcpy(P->d_tensors, P->h_tensors.data(), n_layers * sizeof(TensorDev),
                         cudaMemcpyHostToDevice) == cudaSuccess;
@@ -399,7 +432,6 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaSetDevice(P->device);
     cudaFree(P->d_layers);
     cudaFree(P->d_tensors);
-    cudaFree(P->d_units);
     cudaFree(P->d_fat);
     cudaFree(P->d_fat3);
     cudaFree(P->d_partials);
@@ -435,6 +467,10 @@ tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
     o->chunk_elems = P->chunk12;
     o->n_groups = P->grouped ? 2u : 1u;
     o->n_blocks = static_cast<int32_t>(P->h_layers.size());
+    o->exchange = P->n_workers == 1 ? TGB_EXCHANGE_NONE
+                  : !P->attached    ? TGB_EXCHANGE_NCCL
+                  : P->shard        ? TGB_EXCHANGE_SHARDED
+                                    : TGB_EXCHANGE_FUSED;
     return TGB_OK;
 }
 
@@ -535,7 +571,6 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     }
     k.variant = P->k1_variant;
     k.tensors = P->d_tensors;
-    k.block_units = P->d_units;
     TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, P->ck1[g], k, st));
     return TGB_OK;
 }
@@ -546,11 +581,14 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
     k.variant = P->k2_variant;
-    if (const char* m = std::getenv("TGB_STREAM")) k.stream_blocks = std::atoi(m);
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
         k.dst.n = P->n_workers;
         k.dst.remote = 1;
+        if (P->shard) {
+            k.shard_n = P->n_workers;
+            for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->cs[r];
+        }
     }
     TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + P->cb[g], P->cc[g], k, st));
     return TGB_OK;
@@ -571,7 +609,42 @@ static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t 
                                 cudaStream_t st) {
     K3Launch k{src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
                1.0f / static_cast<float>(n_workers), P->d_err};
+    k.variant = P->k3_variant;
+    k.chunk3 = P->chunk3;
     TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + P->cb3[g], P->cc3[g], k, st));
+    return TGB_OK;
+}
+
+#define TGB_TRY_INNER(expr)                  \
+    do {                                     \
+        const tgb_status s_ = (expr);        \
+        if (s_ != TGB_OK) return s_;         \
+    } while (0)
+
+static inline uint8_t* sums_area(const tgb_plan* P, int p) {
+    return P->peer_ipc[p] + P->sums_off + (P->epoch & 1u) * P->sums_bytes;
+}
+
+static ShardLaunch shard_launch(const tgb_plan* P) {
+    ShardLaunch k{};
+    k.src = P->d_ipc + (P->epoch & 1u) * P->push_bytes * static_cast<uint64_t>(P->n_workers);
+    k.stride = P->push_bytes;
+    for (int p = 0; p < P->n_workers; ++p) k.sums[p] = sums_area(P, p);
+    k.own_sums = sums_area(P, P->rank);
+    k.n_workers = P->n_workers;
+    k.nib = P->nib;
+    k.inv_n = 1.0f / static_cast<float>(P->n_workers);
+    k.err = P->d_err;
+    return k;
+}
+
+// sharded exchange after K2: [codes landed at their owner] barrier 0 -> K3a
+// (owned chunks -> packed sums to every rank) -> barrier 1
+static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
+    TGB_TRY_INNER(launch_barrier(P, 0, st));
+    const uint32_t r = static_cast<uint32_t>(P->rank);
+    TGB_CUDA(launch_k3_reduce(P->d_fat + P->cs[r], P->cs[r + 1] - P->cs[r], shard_launch(P), st));
+    TGB_TRY_INNER(launch_barrier(P, 1, st));
     return TGB_OK;
 }
 
@@ -621,6 +694,7 @@ tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     if (P->attached) {  // data already moved by K1/K2: only order the step
+        if (P->shard) return launch_shard_reduce(P, st);
         for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_barrier(P, g, st));
         return TGB_OK;
     }
@@ -632,9 +706,15 @@ tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
 tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_workers, void* stream) {
     if (!P || !P->bound || n_workers < 1 || n_workers > kMaxWorkers)
         return TGB_ERR_INVALID_ARGUMENT;
-    if (!d_src) d_src = cur_gathered(P);  // NULL: this step's gather buffer
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
+    if (!d_src && P->shard) {  // sharded exchange: decode this step's packed sums
+        if (n_workers != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
+        TGB_CUDA(launch_k3_expand(P->d_fat3, static_cast<uint32_t>(P->h_chunks3.size()),
+                                  shard_launch(P), st));
+        return TGB_OK;
+    }
+    if (!d_src) d_src = cur_gathered(P);  // NULL: this step's gather buffer
     for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_decode(P, g, d_src, n_workers, st));
     return TGB_OK;
 }
@@ -727,6 +807,7 @@ tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {
         P->peer_ipc[p] = static_cast<uint8_t*>(ptr);
     }
     P->attached = true;
+    P->shard = P->shard_capable;
     return TGB_OK;
 }
 

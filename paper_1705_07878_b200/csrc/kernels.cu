@@ -49,7 +49,7 @@ struct SingleSource {
 // inside its tensor (ternarize rng_base, codec.hpp:167 via :229), or the
 // per-layer API's rng_base (passed whole, it may exceed 32 bits).
 __device__ __forceinline__ uint64_t block_rng_base(const LayerDev& L) {
-    return 4ull * L.rng_q + L.rng_shift;
+    return 4ull * L.rng_q + ((L.flags >> kLayerShiftBit) & 3u);
 }
 
 // ====================================================================== K1
@@ -108,8 +108,15 @@ struct K2Args {
     float s_imm;         // per-layer API: scaler by value (slots == nullptr)
     uint64_t rng_base;   // per-layer API: ternarize rng_base (codec.hpp:148); plan: 0
     PeerPush dst;        // plan: code destinations (n == 0: just `push`)
-    int32_t stream_blocks = 0;  // remote dst: write each 1 KB block as soon as it is coded (A/B: slower)
+    int32_t shard_n = 0;        // sharded exchange: ranks; chunk b belongs to rank r with
+    uint32_t shard_bounds[kMaxPeers + 1];  // shard_bounds[r] <= b < shard_bounds[r + 1]
 };
+
+__device__ __forceinline__ int shard_owner(const K2Args& a, uint32_t b) {
+    int r = 0;
+    while (r + 1 < a.shard_n && b >= a.shard_bounds[r + 1]) ++r;
+    return r;
+}
 
 // Chunk codes are staged in shared memory, then written with 16-byte stores to
 // every destination: the rank's own push area and, with peers attached, the
@@ -136,14 +143,18 @@ __device__ __forceinline__ void copy_out(const uint8_t* stage, uint8_t* dst, uin
 // average is float((0.0 + x) / 1.0) (codec.hpp:271-276), i.e. x with -0 -> +0.
 template <bool kFuse>
 __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& L,
-                                               const ChunkDev& ch) {
+                                               const ChunkDev& ch, uint32_t b) {
     const uint32_t tid = threadIdx.x;
     const uint32_t count = ch.count;
     const float* g = L.g + ch.begin;
     const uint64_t off = L.code_off + 4ull * ch.begin;  // 16-B aligned (begin % 16 == 0)
-    const int nd = a.dst.n == 0 ? 1 : a.dst.n;
+    int p0 = 0, nd = a.dst.n == 0 ? 1 : a.dst.n;  // sharded exchange: the chunk's owner only
+    if (a.shard_n) {
+        p0 = shard_owner(a, b);
+        nd = 1;
+    }
     auto dst = [&](int p) {
-        return reinterpret_cast<float*>((a.dst.n == 0 ? a.push : a.dst.base[p]) + off);
+        return reinterpret_cast<float*>((a.dst.n == 0 ? a.push : a.dst.base[p0 + p]) + off);
     };
     float* out = L.out + ch.begin;
     uint32_t bad = 0xFFFFFFFFu;
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     LayerDev L;
     src.get(b, ch, L);
     if (L.flags & kLayerPassthrough) {
-        k2_passthrough<kFuse>(a, L, ch);
+        k2_passthrough<kFuse>(a, L, ch, b);
         return;
     }
     const float s = a.slots ? a.slots[L.slot] : a.s_imm;
@@ -221,7 +232,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
 
     const uint32_t nfull = count >> 2;  // bytes whose 4 elements all exist
     uint32_t q = tid;
-    uint32_t streamed = 0;  // leading code bytes already written to every destination
     float bad_mag = 0.0f;  // max clipped |x| seen (per-layer API check: mag > s)
     if (s == 0.0f) {  // codec.hpp:155-159: all codes 0
         for (; q < nbytes; q += kThreads) stage[q] = 0;
@@ -274,9 +284,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     } else if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         // uniform trip count (every thread runs every block: __syncthreads below)
-        uint32_t blk = 0;
-        const uint64_t off = L.code_off + q0;
-        for (; blk + U * kThreads <= nfull; blk += U * kThreads, q += U * kThreads) {
+        for (uint32_t blk = 0; blk + U * kThreads <= nfull; blk += U * kThreads, q += U * kThreads) {
             float4 v[U];
             uint32_t ctr[U];
             uint4 r[U];
@@ -300,17 +308,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
                     bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
                                                    fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
             }
-            if (a.dst.remote && a.stream_blocks) {
-                // stream this block's codes to every destination now, so the NVLink
-                // stores drain while the CTA keeps computing (cheap final fence)
-                static_assert(U * kThreads == 4 * kThreads, "one u32 per thread per block");
-                __syncthreads();
-                const uint32_t w = reinterpret_cast<const uint32_t*>(stage + blk)[tid];
-                for (int p = 0; p < a.dst.n; ++p)
-                    reinterpret_cast<uint32_t*>(a.dst.base[p] + off + blk)[tid] = w;
-            }
         }
-        if (a.dst.remote && a.stream_blocks) streamed = blk;
         for (; q < nfull; q += kThreads) {
             const float4 v = __ldcs(g4 + q);
             uint32_t ctr[1] = {qbase + q};
@@ -348,8 +346,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     if (a.dst.n == 0) {
         copy_out(stage, a.push + off, nbytes);
     } else {
-        for (int p = 0; p < a.dst.n; ++p)
-            copy_out(stage + streamed, a.dst.base[p] + off + streamed, nbytes - streamed);
+        int p0 = 0, p1 = a.dst.n;  // sharded exchange: the chunk's owner only
+        if (a.shard_n) p1 = (p0 = shard_owner(a, b)) + 1;
+        for (int p = p0; p < p1; ++p) copy_out(stage, a.dst.base[p] + off, nbytes);
         // No fence: the step barrier kernel runs after this grid completes in
         // stream order, and grid completion implies its (peer) stores are
         // performed -- the same guarantee event-based multi-GPU sync relies on.
@@ -651,6 +650,273 @@ __global__ void __launch_bounds__(kThreads) k3_decode_nw(TableSource src, K3Args
     }
 }
 
+// K3 variant (TGB_K3V=1, A/B): the chunk's code bytes of all NW workers are
+// first staged in shared memory with 16-byte loads (NW independent uint4 per
+// thread in flight, 16x fewer load instructions than byte loads), then decoded
+// from shared memory with the same byte -> LUT arithmetic as k3_decode_nw.
+template <int NW>
+__global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3Args a) {
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    if (L.flags & kLayerPassthrough) {
+        const uint64_t off = L.code_off + 4ull * ch.begin;
+        k3_passthrough([&](int w) { return reinterpret_cast<const float*>(a.src + a.stride * w + off); },
+                       NW, L.out + ch.begin, ch.count, (L.flags & kLayerVecOut) != 0);
+        return;
+    }
+    constexpr uint32_t kStage = kChunk3 / 4;  // code bytes per worker
+    __shared__ __align__(16) uint8_t codes[NW][kStage];
+    __shared__ uint32_t tab[256];
+    __shared__ float lut[2 * NW + 1];
+    __shared__ float sw[NW];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t count = ch.count;
+    const uint32_t nbytes = (count + 3) >> 2;
+    const uint32_t n16 = nbytes >> 4;
+    {
+        uint4 v[NW][kStage / 16 / kThreads > 0 ? kStage / 16 / kThreads : 1];
+        constexpr int R = kStage / 16 / kThreads > 0 ? kStage / 16 / kThreads : 1;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint4* b4 = reinterpret_cast<const uint4*>(a.src + a.stride * w + L.code_off +
+                                                             (ch.begin >> 2));
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = tid + r * kThreads;
+                v[w][r] = i < n16 ? __ldcs(b4 + i) : make_uint4(0, 0, 0, 0);
+            }
+        }
+        tab[tid] = lane_biased(tid);
+        if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = tid + r * kThreads;
+                if (i < n16) reinterpret_cast<uint4*>(codes[w])[i] = v[w][r];
+            }
+        for (uint32_t i = (n16 << 4) + tid; i < nbytes; i += kThreads)
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                codes[w][i] = a.src[a.stride * w + L.code_off + (ch.begin >> 2) + i];
+    }
+    __syncthreads();
+    if (tid <= 2 * NW) {
+        float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s = fmaxf(s, sw[w]);
+        lut[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - NW)),
+                             a.inv_n);  // codec.hpp:296
+    }
+    __syncthreads();
+    float* out = L.out + ch.begin;
+    const bool vec_out = (L.flags & kLayerVecOut) != 0;
+    uint32_t bad = 0;
+    for (uint32_t q = tid; q < nbytes; q += kThreads) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t b = codes[w][q];
+            acc += tab[b];
+            bad |= b & (b >> 1);
+        }
+        const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
+                                     lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
+        const uint32_t b4 = 4 * q;
+        if (vec_out && b4 + 4 <= count) {
+            __stcs(reinterpret_cast<float4*>(out + b4), o);
+        } else {
+            if (b4 + 0 < count) out[b4 + 0] = o.x;
+            if (b4 + 1 < count) out[b4 + 1] = o.y;
+            if (b4 + 2 < count) out[b4 + 2] = o.z;
+            if (b4 + 3 < count) out[b4 + 3] = o.w;
+        }
+    }
+    if (bad & 0x55u) {  // rare: locate the first corrupt element of this thread
+        for (uint32_t q = tid; q < nbytes; q += kThreads)
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t b = codes[w][q] & (codes[w][q] >> 1) & 0x55u;
+                if (b) {
+                    raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
+                                block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
+                    return;
+                }
+            }
+    }
+}
+
+// ====================================================== sharded exchange
+// N >= 3 with shared scalers (TGB_SHARD): instead of every rank receiving and
+// decoding all N code streams, rank r owns a contiguous range of K2 chunks
+// (a parameter-server shard, cluster.hpp:167-221 partitioned over the ranks).
+// K2 stores each chunk's codes into its owner's gather buffer only; K3a (here)
+// sums the N workers' codes of the owned chunks into biased integer sums
+// N + sum_w code_w in [0, 2N] -- the reference's SharedSumBlock sums
+// (wire.hpp:79-97) -- packed 4 bits (N <= 7) or 8 bits per element, and stores
+// them into every rank's sums buffer; K3b decodes the sums on every rank with
+// the same LUT (s*float(sum))*invN. Passthrough chunks: K3a writes the final
+// fp64 worker-order mean (codec.hpp:269-279) and K3b copies it.
+struct ShardArgs {
+    const uint8_t* src;            // own gather buffer (N push areas, stride apart)
+    uint64_t stride;
+    uint8_t* sums[kMaxPeers];      // every rank's sums buffer (this step's parity)
+    const uint8_t* own_sums;
+    int32_t n_workers;
+    int32_t nib;                   // 4-bit sums (N <= 7), else 8-bit
+    float inv_n;
+    ErrWord* err;
+};
+
+__device__ __forceinline__ uint32_t pack_nib(uint32_t acc) {  // 4 byte lanes -> 4 nibbles
+    return (acc & 0xFu) | ((acc >> 4) & 0xF0u) | ((acc >> 8) & 0xF00u) | ((acc >> 12) & 0xF000u);
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs a) {
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    const uint32_t tid = threadIdx.x;
+    const uint64_t soff = 16ull * L.sum_off16;
+    if (L.flags & kLayerPassthrough) {
+        const uint64_t off = L.code_off + 4ull * ch.begin;
+        const double dn = static_cast<double>(NW);
+        const uint32_t count = ch.count;
+        for (uint32_t i = tid; i < count; i += kThreads) {
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                sum = __dadd_rn(sum, static_cast<double>(
+                                         reinterpret_cast<const float*>(a.src + a.stride * w + off)[i]));
+            const float v = static_cast<float>(sum / dn);
+#pragma unroll
+            for (int p = 0; p < NW; ++p)
+                (reinterpret_cast<float*>(a.sums[p] + soff) + ch.begin)[i] = v;
+        }
+        return;
+    }
+    __shared__ uint32_t tab[256];
+    tab[tid] = lane_biased(tid);
+    __syncthreads();
+    const uint32_t count = ch.count;
+    const uint32_t nbytes = (count + 3) >> 2;
+    const uint8_t* base[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) base[w] = a.src + a.stride * w + L.code_off + (ch.begin >> 2);
+    constexpr int U = 4;
+    uint32_t bad = 0;
+    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
+        uint32_t bw[NW][U];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = qb + tid + u * kThreads;
+                bw[w][u] = q < nbytes ? __ldcs(base[w] + q) : 0u;
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = qb + tid + u * kThreads;
+            if (q >= nbytes) break;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                acc += tab[bw[w][u]];
+                bad |= bw[w][u] & (bw[w][u] >> 1);
+            }
+            if (a.nib) {
+                const uint16_t v = static_cast<uint16_t>(pack_nib(acc));
+#pragma unroll
+                for (int p = 0; p < NW; ++p)
+                    reinterpret_cast<uint16_t*>(a.sums[p] + soff + (ch.begin >> 1))[q] = v;
+            } else {
+#pragma unroll
+                for (int p = 0; p < NW; ++p)
+                    reinterpret_cast<uint32_t*>(a.sums[p] + soff + ch.begin)[q] = acc;
+            }
+        }
+    }
+    if (bad & 0x55u) {  // rare: locate the first corrupt element of this thread
+        for (uint32_t q = tid; q < nbytes; q += kThreads)
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t b = base[w][q] & (base[w][q] >> 1) & 0x55u;
+                if (b) {
+                    raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
+                                block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
+                    return;
+                }
+            }
+    }
+}
+
+template <bool kNib>
+__global__ void __launch_bounds__(kThreads) k3_expand(TableSource src, ShardArgs a) {
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    const uint32_t tid = threadIdx.x;
+    const uint64_t soff = 16ull * L.sum_off16;
+    float* out = L.out + ch.begin;
+    const bool vec_out = (L.flags & kLayerVecOut) != 0;
+    const uint32_t count = ch.count;
+    if (L.flags & kLayerPassthrough) {
+        const float* v = reinterpret_cast<const float*>(a.own_sums + soff) + ch.begin;
+        const uint32_t n4 = vec_out ? (count >> 2) : 0u;
+        for (uint32_t i = tid; i < n4; i += kThreads)
+            __stcs(reinterpret_cast<float4*>(out) + i, __ldcs(reinterpret_cast<const float4*>(v) + i));
+        for (uint32_t i = 4 * n4 + tid; i < count; i += kThreads) out[i] = v[i];
+        return;
+    }
+    const int N = a.n_workers;
+    __shared__ float lut[2 * kMaxPeers + 1];
+    __shared__ float sw[kMaxPeers];
+    if (tid < static_cast<uint32_t>(N))
+        sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
+    __syncthreads();
+    if (tid <= static_cast<uint32_t>(2 * N)) {
+        float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
+        for (int w = 0; w < N; ++w) s = fmaxf(s, sw[w]);
+        lut[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - N)),
+                             a.inv_n);  // codec.hpp:296
+    }
+    __syncthreads();
+    const uint32_t nbytes = (count + 3) >> 2;  // one packed word per 4 elements
+    constexpr int U = 4;
+    constexpr uint32_t kBits = kNib ? 4u : 8u, kMask = kNib ? 0xFu : 0xFFu;
+    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
+        uint32_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = qb + tid + u * kThreads;
+            if (kNib)
+                v[u] = q < nbytes ? __ldcs(reinterpret_cast<const uint16_t*>(a.own_sums + soff +
+                                                                              (ch.begin >> 1)) + q)
+                                  : 0u;
+            else
+                v[u] = q < nbytes ? __ldcs(reinterpret_cast<const uint32_t*>(a.own_sums + soff +
+                                                                              ch.begin) + q)
+                                  : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = qb + tid + u * kThreads;
+            const float4 o = make_float4(lut[v[u] & kMask], lut[(v[u] >> kBits) & kMask],
+                                         lut[(v[u] >> (2 * kBits)) & kMask],
+                                         lut[(v[u] >> (3 * kBits)) & kMask]);
+            const uint32_t b4 = 4 * q;
+            if (vec_out && b4 + 4 <= count) {
+                __stcs(reinterpret_cast<float4*>(out + b4), o);
+            } else if (q < nbytes) {
+                if (b4 + 0 < count) out[b4 + 0] = o.x;
+                if (b4 + 1 < count) out[b4 + 1] = o.y;
+                if (b4 + 2 < count) out[b4 + 2] = o.z;
+                if (b4 + 3 < count) out[b4 + 3] = o.w;
+            }
+        }
+    }
+}
+
 // clip apply for the per-layer clip API (codec.hpp:121-122)
 __global__ void __launch_bounds__(kThreads)
 k_clip_apply(const float* g, uint64_t n, const float* bound, float* out) {
@@ -691,8 +957,7 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
                             const K1Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
-            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors,
-            p.block_units};
+            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors};
     const TableSource src{chunks};
     switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
@@ -707,7 +972,7 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
     const uint32_t nc = static_cast<uint32_t>((L.n + kChunk - 1) / kChunk);
     if (nc == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor, 0,
-            1, 1, nullptr, PeerPush{}, nullptr, nullptr};
+            1, 1, nullptr, PeerPush{}, nullptr};
     LayerDev l = L;
     l.tensor = 0;
     l.first_chunk = 0;
@@ -719,8 +984,9 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
-    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0, p.dst,
-             p.stream_blocks};
+    K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0, p.dst};
+    a.shard_n = p.shard_n;
+    for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
     if (p.fuse_decode) {
         k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
@@ -738,6 +1004,7 @@ cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t 
     const uint32_t nc = static_cast<uint32_t>((L.n + kChunk12 - 1) / kChunk12);
     if (nc == 0) return cudaSuccess;
     K2Args a{p.push, p.slots, p.bounds, p.err, p.t, 0, 1, p.s_imm, p.rng_base, PeerPush{}};
+    a.shard_n = 0;
     k2_ternarize<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{L, kChunk12}, a);
     return launch_status();
 }
@@ -748,6 +1015,16 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
     const TableSource src{chunks};
+    if (p.sharing && p.variant == 1 && p.chunk3 == kChunk3) {
+        switch (p.n_workers) {
+            case 1: k3_decode_staged<1><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 2: k3_decode_staged<2><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 3: k3_decode_staged<3><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 4: k3_decode_staged<4><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 8: k3_decode_staged<8><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            default: break;
+        }
+    }
     if (p.sharing) {
         switch (p.n_workers) {
             case 1: k3_decode_nw<1><<<n_chunks, kThreads, 0, st>>>(src, a); break;
@@ -795,6 +1072,37 @@ cudaError_t launch_average_raw(int32_t n_workers, const float* const* vals, uint
     }
     k_average_raw<<<static_cast<uint32_t>(nc), kThreads, 0, st>>>(ptrs, n_workers, n, out,
                                                                    vec ? 1 : 0);
+    return launch_status();
+}
+
+cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
+                             cudaStream_t st) {
+    if (n_chunks == 0) return cudaSuccess;
+    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err};
+    for (int r = 0; r < p.n_workers; ++r) a.sums[r] = p.sums[r];
+    const TableSource src{chunks};
+    switch (p.n_workers) {
+        case 2: k3_reduce<2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 3: k3_reduce<3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 4: k3_reduce<4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 5: k3_reduce<5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 6: k3_reduce<6><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 7: k3_reduce<7><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 8: k3_reduce<8><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return launch_status();
+}
+
+cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
+                             cudaStream_t st) {
+    if (n_chunks == 0) return cudaSuccess;
+    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err};
+    const TableSource src{chunks};
+    if (p.nib)
+        k3_expand<true><<<n_chunks, kThreads, 0, st>>>(src, a);
+    else
+        k3_expand<false><<<n_chunks, kThreads, 0, st>>>(src, a);
     return launch_status();
 }
 

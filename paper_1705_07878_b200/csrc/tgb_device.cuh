@@ -24,6 +24,7 @@ constexpr uint32_t kLayerPassthrough = 1u;
 constexpr uint32_t kLayerClip = 2u;     // clip this layer (clipping on, not passthrough)
 constexpr uint32_t kLayerVecIn = 4u;    // gradient pointer is 16-byte aligned
 constexpr uint32_t kLayerVecOut = 8u;   // output pointer is 16-byte aligned
+constexpr uint32_t kLayerShiftBit = 16; // bits 16-17: block start within the tensor & 3
 
 // A block: one bucket of one tensor (PerTensor/Global: the whole tensor;
 // FixedSize(k): [off, off+k) of it, codec.hpp:224-232) or a passthrough tensor.
@@ -37,7 +38,7 @@ struct LayerDev {
     int32_t slot;        // scaler slot (passthrough: -1)
     uint32_t flags;
     uint32_t rng_q;      // block start within the tensor >> 2 (ternarize rng_base, :167)
-    uint32_t rng_shift;  // block start within the tensor & 3 (!= 0: lanes straddle bytes)
+    uint32_t sum_off16;  // sharded exchange: block's region in the sums buffer, 16-B units
     uint32_t first_chunk, n_chunks;  // K1 work items of the TENSOR (group-relative)
 };
 
@@ -66,7 +67,7 @@ struct TensorDev {
 struct Partial {
     double n, mean, m2;
     float mx;
-    uint32_t pad;
+    uint32_t block;  // block (bucket) the work item belongs to
 };
 
 // Destinations of this rank's push area (scaler slots + packed codes): its own

@@ -29,7 +29,6 @@ struct K1Launch {
     int32_t variant = 0;  // chunk K1 kernel variant (TGB_K1V, A/B only)
     PeerPush push{};      // scaler slot destinations
     const TensorDev* tensors = nullptr;  // plan: tensor table (per-tensor finalize)
-    const uint2* block_units = nullptr;  // plan: per block {first K1 unit, count}, group-relative
 };
 
 struct K2Launch {
@@ -43,7 +42,8 @@ struct K2Launch {
     float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
     uint64_t rng_base = 0; // single-layer: ternarize rng_base (codec.hpp:148)
     PeerPush dst{};        // plan: code destinations (n == 0: push only)
-    int32_t stream_blocks = 0;  // TGB_STREAM (A/B): per-block remote streaming in K2
+    int32_t shard_n = 0;        // sharded exchange: codes go to the chunk's owner only
+    uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
 };
 
@@ -55,6 +55,19 @@ struct K3Launch {
     float inv_n;
     ErrWord* err;
     float s_imm = 0.0f;    // single-layer: scaler by value when scalers == nullptr
+    int32_t variant = 0;   // TGB_K3V (A/B): 1 = smem-staged 16-B code loads
+    uint32_t chunk3 = 0;   // plan K3 chunk elements (the staged variant needs kChunk3)
+};
+
+struct ShardLaunch {
+    const uint8_t* src;        // own gather buffer
+    uint64_t stride;           // push_bytes
+    uint8_t* sums[kMaxPeers];  // every rank's sums buffer (this step's parity)
+    const uint8_t* own_sums;
+    int32_t n_workers;
+    int32_t nib;
+    float inv_n;
+    ErrWord* err;
 };
 
 cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
@@ -69,6 +82,10 @@ cudaError_t launch_k3_single(const LayerDev& L, const uint8_t* const* codes, con
                              const K3Launch& p, cudaStream_t st);
 cudaError_t launch_average_raw(int32_t n_workers, const float* const* vals, uint64_t n,
                                float* out, cudaStream_t st);
+cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
+                             cudaStream_t st);
+cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
+                             cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,

@@ -26,7 +26,6 @@ struct K1Out {
     const LayerDev* layers;   // block table (slots of a tensor's blocks, Global fix-up)
     PeerPush push;            // scaler slot destinations (n == 0: slots only)
     const TensorDev* tensors; // plan only; nullptr = single-block single-layer API
-    const uint2* block_units; // per block: {first work item (group-relative), count}
 };
 
 __device__ __forceinline__ void put_slot(const K1Out& o, int32_t slot, float v) {
@@ -75,7 +74,7 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
         p.mean = x0 + S / cn;
         p.m2 = Q - S * (S / cn);
         p.mx = mx;
-        p.pad = 0;
+        p.block = layer;
         o.partials[unit] = p;
         __threadfence();
         const uint32_t ticket = atomicAdd(&o.layer_done[L.tensor], 1u);
@@ -145,12 +144,34 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
     if (o.tensors) {
         // per block: s = max |clip(part)| = min(max |part|, bound) (codec.hpp:121-122, :229-230)
         const TensorDev T = o.tensors[L.tensor];
-        for (uint32_t b = T.first_block + tid; b < T.first_block + T.n_blocks; b += kThreads) {
-            const uint2 u = o.block_units[b];
-            float bm = 0.0f;
-            for (uint32_t c = u.x; c < u.x + u.y; ++c) bm = fmaxf(bm, __ldcg(&o.partials[c].mx));
-            o.bounds[b] = s_bound;
-            put_slot(o, o.layers[b].slot, s_bad ? 0.0f : fminf(bm, s_bound));
+        if (T.n_blocks == 1) {  // PerTensor / Global: the tree's max is the block's
+            if (tid == 0) {
+                o.bounds[T.first_block] = s_bound;
+                put_slot(o, o.layers[T.first_block].slot, s_bad ? 0.0f : fminf(smx[0], s_bound));
+            }
+        } else {
+            // FixedSize buckets: scatter each unit's max into its block (partial.block),
+            // kWin blocks per pass; |x| >= 0 so float order == int order
+            constexpr uint32_t kWin = 2048;
+            __shared__ int wmax[kWin];
+            for (uint32_t w0 = 0; w0 < T.n_blocks; w0 += kWin) {
+                const uint32_t nw = min(kWin, T.n_blocks - w0);
+                for (uint32_t i = tid; i < nw; i += kThreads) wmax[i] = 0;
+                Bar::sync();
+                for (uint32_t c = tid; c < nc; c += kThreads) {
+                    const Partial* pp = o.partials + first_unit + c;
+                    const uint32_t b = __ldcg(&pp->block) - T.first_block - w0;
+                    if (b < nw) atomicMax(&wmax[b], __float_as_int(__ldcg(&pp->mx)));
+                }
+                Bar::sync();
+                for (uint32_t i = tid; i < nw; i += kThreads) {
+                    const uint32_t b = T.first_block + w0 + i;
+                    o.bounds[b] = s_bound;
+                    put_slot(o, o.layers[b].slot,
+                             s_bad ? 0.0f : fminf(__int_as_float(wmax[i]), s_bound));
+                }
+                Bar::sync();
+            }
         }
         Bar::sync();
         if (tid == 0 && o.global_bucketing) {

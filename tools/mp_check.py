@@ -81,7 +81,10 @@ def main():
                 ok_ref = st == 0 and np.array_equal(ref.view(np.uint32), flat.view(np.uint32))
             else:  # PRESHARED: every worker ternarizes with s = max_w s_w (paper Eq. 4)
                 ok_ref = preshared_oracle(R, names, allg, flat, ws, ocfg, pt)
-        report["checks"][key] = {"ranks_identical": ok_same, "matches_oracle": ok_ref}
+        info = tg._lib.PlanInfo()
+        tg._lib.check(tg._lib.load().tgb_plan_get_info(sw.plan.h, tg.codec.C.byref(info)), "info")
+        report["checks"][key] = {"ranks_identical": ok_same, "matches_oracle": ok_ref,
+                                 "exchange": ["none", "nccl", "fused", "sharded"][info.exchange]}
         dist.barrier()
         sw.plan.close()
 
@@ -118,9 +121,12 @@ def main():
     dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
     if rank == 0:
         n = sum(sw.ns)
+        info = tg._lib.PlanInfo()
+        tg._lib.check(tg._lib.load().tgb_plan_get_info(p.h, tg.codec.C.byref(info)), "info")
+        report["vgg16_exchange"] = ["none", "nccl", "fused", "sharded"][info.exchange]
         report["vgg16_ms_per_step_max_over_ranks"] = float(t_all[0])
         report["stage_ms_median_max_over_ranks"] = {
-            k: float(v) for k, v in zip(["K1", "K2", "allgather", "K3"], t_all[1:])}
+            k: float(v) for k, v in zip(["K1", "K2", "sync", "K3"], t_all[1:])}
         report["aggregate_Gelem_s"] = ws * n / (float(t_all[0]) * 1e-3) / 1e9
         report["allgather_GBps_per_rank_in"] = (ws - 1) * p.info.push_bytes / (
             float(t_all[3]) * 1e-3) / 1e9
