@@ -231,6 +231,14 @@ def run_b200(args):
     ns = sw.ns
     n = sum(ns)
     plan = sw.plan
+    info = tg._lib.PlanInfo()
+    tg._lib.check(tg._lib.load().tgb_plan_get_info(plan.h, tg.codec.C.byref(info)), "info")
+    mode = ["none", "nccl", "fused", "sharded"][info.exchange]
+    # algorithmic HBM bytes per element per GPU:
+    #   allgather designs: B(N) = 12 + 0.5 N;
+    #   sharded: 4 (K1) + 4.25 (K2) + 0.25 (K3a codes) + 2 x sums (land + K3b read) + 4 = 12.5 + 2 w
+    sum_w = (0.5 if N <= 7 else 1.0) if mode == "sharded" else 0.0
+    B_elem = 12.5 + 2 * sum_w if mode == "sharded" else 12.0 + 0.5 * N
     host, _ = synth_host(ns, rank)
     sw.grad_flat[:host.numel()].copy_(host.to(dev, non_blocking=True))
     stream = torch.cuda.current_stream(dev)
@@ -352,7 +360,7 @@ def run_b200(args):
     sync_ms = sum(stage[2]) / K
     k3_ms = sum(stage[3]) / K
     kb = {"K1_stats": (4.0 * n, k1_ms), "K2_ternarize_pack": (4.0 * n + n / 4.0, k2_ms),
-          "K3_decode": (N * n / 4.0 + 4.0 * n, k3_ms)}
+          "K3_decode": ((sum_w if mode == "sharded" else N / 4.0) * n + 4.0 * n, k3_ms)}
     dom = max(kb, key=lambda k: kb[k][1])
     dom_bytes, dom_ms = kb[dom]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
@@ -363,7 +371,7 @@ def run_b200(args):
             traffic = json.load(open(tpath)).get(args.workload, {}).get(dom)
         except Exception:
             traffic = None
-    step_bytes = n * (12.0 + 0.5 * N)  # B(N) = 12 + 0.5 N bytes/element/GPU
+    step_bytes = n * B_elem
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (pinned)
@@ -409,7 +417,9 @@ def run_b200(args):
                    "sample": f"unavailable: {ex}"}
 
     groups = 2 if plan.grouped else 1
-    launches_per_step = groups * (2 if N == 1 else 4)
+    # own kernels per tgb_step: N=1: K1 + K2(decode fused); fused: K1 + K2 + barrier + K3;
+    # sharded: K1 + K2 + barrier + K3a + barrier + K3b; nccl: K1 + K2 + K3 (+ NCCL's own)
+    launches_per_step = groups * {"none": 2, "fused": 4, "sharded": 6, "nccl": 3}[mode]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K,
@@ -430,7 +440,7 @@ def run_b200(args):
             "roofline_step": {"bytes_per_step": step_bytes,
                               "achieved": step_bytes / (ms_step * 1e-3) / 1e9,
                               "frac": step_bytes / (ms_step * 1e-3) / 1e9 / hbm,
-                              "B_per_elem": 12.0 + 0.5 * N},
+                              "B_per_elem": B_elem},
             "stages_ms": {"K1_stats": k1_ms, "K2_ternarize_pack": k2_ms, "exchange": sync_ms,
                           "K3_decode": k3_ms, "sequential_step": staged_total / K,
                           "note": "per-kernel breakdown from a sequential pass; the headline "
@@ -438,11 +448,15 @@ def run_b200(args):
             "kernels": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
             "gpu_launches": launches_per_step * K,
-            "gpu_launches_note": "own kernels per tgb_step: per layer group K1 + K2 (N=1: K2 "
-                                 "also decodes) or K1 + K2 + peer barrier + K3 (N>1, codes move "
-                                 "inside K2 as NVLink peer stores)",
-            "exchange": ("fused NVLink peer stores in K2 + device barrier" if N > 1 and fused
-                         else ("NCCL allgather" if N > 1 else "none (N=1)")),
+            "gpu_launches_note": "own kernels per tgb_step and layer group: N=1 K1 + K2 (K2 "
+                                 "also decodes); fused K1 + K2 + peer barrier + K3; sharded K1 + "
+                                 "K2 + barrier + K3a (owner sums) + barrier + K3b; nccl K1 + K2 + "
+                                 "K3",
+            "exchange": {"fused": "fused NVLink peer stores in K2 + device barrier",
+                         "sharded": "sharded: K2 stores codes at the chunk owner, owner sums N "
+                                    "workers into packed sums stored at every rank (NVLink), "
+                                    "2 device barriers",
+                         "nccl": "NCCL allgather", "none": "none (N=1)"}[mode],
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

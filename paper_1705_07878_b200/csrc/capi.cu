@@ -124,6 +124,7 @@ struct tgb_plan {
     bool bound = false;
     int32_t k2_variant = 0;  // TGB_K2V
     int32_t k1_variant = 0;  // TGB_K1V
+    int32_t fuse_mode = 2;   // TGB_FUSEV: N == 1 decode inside K2, 1 post pass, 2 in-loop
     int32_t k3_variant = 1;  // TGB_K3V: 1 smem-staged (default, tools/k3_probe.py), 0 byte loads
     // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
     // K2 chunks [cs[r], cs[r+1]) and reduces them to packed sums for every rank.
@@ -220,6 +221,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K3V")) P->k3_variant = std::atoi(m);
+    if (const char* m = std::getenv("TGB_FUSEV")) P->fuse_mode = std::atoi(m) == 1 ? 1 : 2;
     P->worker = worker;
     P->n_workers = n_workers;
     P->desc.assign(layers, layers + n_layers);
@@ -579,7 +581,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
                               bool fuse_decode = false) {
     uint8_t* own = own_push(P);
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
-    k.fuse_decode = fuse_decode ? 1 : 0;
+    k.fuse_decode = fuse_decode ? P->fuse_mode : 0;
     k.variant = P->k2_variant;
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);

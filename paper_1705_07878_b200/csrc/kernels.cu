@@ -56,8 +56,8 @@ __device__ __forceinline__ uint64_t block_rng_base(const LayerDev& L) {
 // One CTA per work item (a chunk of one block); the tensor's last arriving CTA
 // merges the tensor's partials (tgb_stats.cuh). Passthrough blocks have no
 // statistics (codec.hpp:206-209) and are never in a K1 grid.
-template <class Src, int U = 8, int A = 1>
-__global__ void __launch_bounds__(kThreads) k1_stats(Src src, K1Out o) {
+template <class Src, int U = 8, int A = 1, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out o) {
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
@@ -199,7 +199,11 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
     }
 }
 
-template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false>
+// kFuse (N == 1: the average is this worker's own decode, K3 folded into K2):
+// 1 = decode pass over the staged codes after the loop, 2 = each thread writes
+// the decoded float4 of every code byte as soon as it is computed, so the
+// output stream overlaps the Philox compute.
+template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, int kFuse = 0>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     LayerDev L;
     src.get(b, ch, L);
     if (L.flags & kLayerPassthrough) {
-        k2_passthrough<kFuse>(a, L, ch, b);
+        k2_passthrough<kFuse != 0>(a, L, ch, b);
         return;
     }
     const float s = a.slots ? a.slots[L.slot] : a.s_imm;
@@ -231,10 +235,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     const uint32_t qbase = static_cast<uint32_t>(qg);
 
     const uint32_t nfull = count >> 2;  // bytes whose 4 elements all exist
+    // kFuse: byte -> float4 table of (s*float(sum))*invN with invN = 1, sum in
+    // {0, +1, -1} (codec.hpp:296, wire.hpp:220): +0, s, -s
+    __shared__ float4 lutv[kFuse ? 256 : 1];
+    if (kFuse) {
+        const float v0 = __fmul_rn(__fmul_rn(s, 0.0f), 1.0f), v1 = __fmul_rn(__fmul_rn(s, 1.0f), 1.0f),
+                    v2 = __fmul_rn(__fmul_rn(s, -1.0f), 1.0f);
+        auto val = [&](uint32_t c) { return c == 1u ? v1 : (c == 2u ? v2 : v0); };
+        lutv[tid] = make_float4(val(tid & 3u), val((tid >> 2) & 3u), val((tid >> 4) & 3u),
+                                val((tid >> 6) & 3u));
+        if (kFuse == 2) __syncthreads();
+    }
+    float* out = L.out + ch.begin;
+    const bool vec_out = (L.flags & kLayerVecOut) != 0;
+    auto emit = [&](uint32_t qq, uint32_t byte) {  // kFuse == 2: decoded float4 of byte qq
+        if (kFuse != 2) return;
+        const float4 o = lutv[byte];
+        if (vec_out && 4 * qq + 4 <= count) {
+            __stcs(reinterpret_cast<float4*>(out) + qq, o);
+        } else {
+            const uint32_t e = 4 * qq;
+            if (e < count) out[e] = o.x;
+            if (e + 1 < count) out[e + 1] = o.y;
+            if (e + 2 < count) out[e + 2] = o.z;
+            if (e + 3 < count) out[e + 3] = o.w;
+        }
+    };
     uint32_t q = tid;
     float bad_mag = 0.0f;  // max clipped |x| seen (per-layer API check: mag > s)
     if (s == 0.0f) {  // codec.hpp:155-159: all codes 0
-        for (; q < nbytes; q += kThreads) stage[q] = 0;
+        for (; q < nbytes; q += kThreads) {
+            stage[q] = 0;
+            emit(q, 0);
+        }
         if (a.check)
             for (uint32_t i = tid; i < count; i += kThreads)
                 if (g[i] != 0.0f)
@@ -278,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
                     if (a.check) bad_mag = fmaxf(bad_mag, fabsf(x));
                 }
                 stage[qq] = static_cast<uint8_t>(byte);
+                emit(qq, byte);
             }
         }
         q = nbytes;
@@ -304,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 stage[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
+                emit(q + u * kThreads, byte[u]);
                 if (a.check)
                     bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
                                                    fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
@@ -314,7 +349,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
             uint32_t ctr[1] = {qbase + q};
             uint4 r[1];
             ph(ctr, r);
-            stage[q] = static_cast<uint8_t>(dec.byte(v, r[0]));
+            const uint32_t byte = dec.byte(v, r[0]);
+            stage[q] = static_cast<uint8_t>(byte);
+            emit(q, byte);
             if (a.check)
                 bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)),
                                                fmaxf(fabsf(v.z), fabsf(v.w))));
@@ -332,7 +369,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
             uint32_t ctr[1] = {qbase + q};
             uint4 r[1];
             ph(ctr, r);
-            stage[q] = static_cast<uint8_t>(dec.byte(make_float4(x[0], x[1], x[2], x[3]), r[0]));
+            const uint32_t byte = dec.byte(make_float4(x[0], x[1], x[2], x[3]), r[0]);
+            stage[q] = static_cast<uint8_t>(byte);
+            emit(q, byte);
             if (a.check)
                 bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])),
                                                fmaxf(fabsf(x[2]), fabsf(x[3]))));
@@ -353,20 +392,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         // stream order, and grid completion implies its (peer) stores are
         // performed -- the same guarantee event-based multi-GPU sync relies on.
     }
-    if (kFuse) {
-        // N == 1: the averaged gradient is this worker's own decode, so K3 runs
-        // here from the codes still in shared memory (no code re-read, no extra
-        // launch). Byte -> float4 table of (s*float(sum))*invN with invN = 1,
-        // sum in {0, +1, -1} (codec.hpp:296, wire.hpp:220): +0, s, -s.
-        __shared__ float4 lutv[256];
-        const float v0 = __fmul_rn(__fmul_rn(s, 0.0f), 1.0f), v1 = __fmul_rn(__fmul_rn(s, 1.0f), 1.0f),
-                    v2 = __fmul_rn(__fmul_rn(s, -1.0f), 1.0f);
-        auto val = [&](uint32_t c) { return c == 1u ? v1 : (c == 2u ? v2 : v0); };
-        lutv[tid] = make_float4(val(tid & 3u), val((tid >> 2) & 3u), val((tid >> 4) & 3u),
-                                val((tid >> 6) & 3u));
-        __syncthreads();
-        float* out = L.out + ch.begin;
-        if (L.flags & kLayerVecOut) {
+    if (kFuse == 1) {
+        // decode pass from the codes still in shared memory (no code re-read,
+        // no extra launch); lutv was filled before the loop
+        if (vec_out) {
             float4* o4 = reinterpret_cast<float4*>(out);
             for (uint32_t qq = tid; qq < nfull; qq += kThreads) __stcs(o4 + qq, lutv[stage[qq]]);
         } else {
@@ -772,6 +801,11 @@ __device__ __forceinline__ uint32_t pack_nib(uint32_t acc) {  // 4 byte lanes ->
     return (acc & 0xFu) | ((acc >> 4) & 0xF0u) | ((acc >> 8) & 0xF00u) | ((acc >> 12) & 0xF000u);
 }
 
+// K3a: one CTA per owned K2 chunk (<= kChunk12 elements). Each thread takes
+// 16-byte groups of code bytes (one uint4 per worker, all NW in flight),
+// builds the 16 packed sums in registers, stages them in shared memory, and
+// the CTA then writes the chunk's sums to every rank with 16-byte stores
+// (NVLink stores stay full-width).
 template <int NW>
 __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs a) {
     ChunkDev ch;
@@ -779,11 +813,28 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
     src.get(blockIdx.x, ch, L);
     const uint32_t tid = threadIdx.x;
     const uint64_t soff = 16ull * L.sum_off16;
-    if (L.flags & kLayerPassthrough) {
+    const uint32_t count = ch.count;
+    if (L.flags & kLayerPassthrough) {  // fp64 worker-order mean (codec.hpp:269-279)
         const uint64_t off = L.code_off + 4ull * ch.begin;
         const double dn = static_cast<double>(NW);
-        const uint32_t count = ch.count;
-        for (uint32_t i = tid; i < count; i += kThreads) {
+        const uint32_t n4 = count >> 2;
+        for (uint32_t i = tid; i < n4; i += kThreads) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(a.src + a.stride * w + off) + i);
+                s0 = __dadd_rn(s0, static_cast<double>(v.x));
+                s1 = __dadd_rn(s1, static_cast<double>(v.y));
+                s2 = __dadd_rn(s2, static_cast<double>(v.z));
+                s3 = __dadd_rn(s3, static_cast<double>(v.w));
+            }
+            const float4 o = make_float4(static_cast<float>(s0 / dn), static_cast<float>(s1 / dn),
+                                         static_cast<float>(s2 / dn), static_cast<float>(s3 / dn));
+#pragma unroll
+            for (int p = 0; p < NW; ++p)
+                reinterpret_cast<float4*>(a.sums[p] + soff + 4ull * ch.begin)[i] = o;
+        }
+        for (uint32_t i = 4 * n4 + tid; i < count; i += kThreads) {
             double sum = 0.0;
 #pragma unroll
             for (int w = 0; w < NW; ++w)
@@ -792,61 +843,86 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
             const float v = static_cast<float>(sum / dn);
 #pragma unroll
             for (int p = 0; p < NW; ++p)
-                (reinterpret_cast<float*>(a.sums[p] + soff) + ch.begin)[i] = v;
+                reinterpret_cast<float*>(a.sums[p] + soff + 4ull * ch.begin)[i] = v;
         }
         return;
     }
+    constexpr uint32_t kMaxBytes = kChunk12 / 4;  // code bytes per chunk
+    __shared__ __align__(16) uint32_t stage[kMaxBytes];  // 4 B of sums per code byte (max)
     __shared__ uint32_t tab[256];
     tab[tid] = lane_biased(tid);
     __syncthreads();
-    const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
+    const uint32_t n16 = nbytes >> 4;
     const uint8_t* base[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) base[w] = a.src + a.stride * w + L.code_off + (ch.begin >> 2);
-    constexpr int U = 4;
     uint32_t bad = 0;
-    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
-        uint32_t bw[NW][U];
+    uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
+    for (uint32_t i = tid; i < n16; i += kThreads) {
+        uint4 v[NW];
 #pragma unroll
-        for (int w = 0; w < NW; ++w)
+        for (int w = 0; w < NW; ++w) v[w] = __ldcs(reinterpret_cast<const uint4*>(base[w]) + i);
+        uint32_t acc[16];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t q = qb + tid + u * kThreads;
-                bw[w][u] = q < nbytes ? __ldcs(base[w] + q) : 0u;
-            }
+        for (int j = 0; j < 16; ++j) acc[j] = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t q = qb + tid + u * kThreads;
-            if (q >= nbytes) break;
-            uint32_t acc = 0;
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t wd[4] = {v[w].x, v[w].y, v[w].z, v[w].w};
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                acc += tab[bw[w][u]];
-                bad |= bw[w][u] & (bw[w][u] >> 1);
-            }
-            if (a.nib) {
-                const uint16_t v = static_cast<uint16_t>(pack_nib(acc));
+            for (int j = 0; j < 16; ++j) acc[j] += tab[(wd[j >> 2] >> (8 * (j & 3))) & 0xFFu];
+            bad |= (wd[0] & (wd[0] >> 1)) | (wd[1] & (wd[1] >> 1)) | (wd[2] & (wd[2] >> 1)) |
+                   (wd[3] & (wd[3] >> 1));
+        }
+        if (a.nib) {
+            uint4 o0, o1;
+            o0.x = pack_nib(acc[0]) | (pack_nib(acc[1]) << 16);
+            o0.y = pack_nib(acc[2]) | (pack_nib(acc[3]) << 16);
+            o0.z = pack_nib(acc[4]) | (pack_nib(acc[5]) << 16);
+            o0.w = pack_nib(acc[6]) | (pack_nib(acc[7]) << 16);
+            o1.x = pack_nib(acc[8]) | (pack_nib(acc[9]) << 16);
+            o1.y = pack_nib(acc[10]) | (pack_nib(acc[11]) << 16);
+            o1.z = pack_nib(acc[12]) | (pack_nib(acc[13]) << 16);
+            o1.w = pack_nib(acc[14]) | (pack_nib(acc[15]) << 16);
+            reinterpret_cast<uint4*>(stage)[2 * i] = o0;
+            reinterpret_cast<uint4*>(stage)[2 * i + 1] = o1;
+        } else {
 #pragma unroll
-                for (int p = 0; p < NW; ++p)
-                    reinterpret_cast<uint16_t*>(a.sums[p] + soff + (ch.begin >> 1))[q] = v;
-            } else {
-#pragma unroll
-                for (int p = 0; p < NW; ++p)
-                    reinterpret_cast<uint32_t*>(a.sums[p] + soff + ch.begin)[q] = acc;
-            }
+            for (int k = 0; k < 4; ++k)
+                reinterpret_cast<uint4*>(stage)[4 * i + k] =
+                    make_uint4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
         }
     }
-    if (bad & 0x55u) {  // rare: locate the first corrupt element of this thread
-        for (uint32_t q = tid; q < nbytes; q += kThreads)
+    for (uint32_t q = (n16 << 4) + tid; q < nbytes; q += kThreads) {  // tail code bytes
+        uint32_t acc = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t bw = base[w][q];
+            acc += tab[bw];
+            bad |= bw & (bw >> 1);
+        }
+        if (a.nib)
+            st16[q] = static_cast<uint16_t>(pack_nib(acc));
+        else
+            stage[q] = acc;
+    }
+    __syncthreads();
+    const uint32_t sbytes = nbytes * (a.nib ? 2u : 4u);
+    const uint64_t doff = soff + (a.nib ? (ch.begin >> 1) : ch.begin);
+#pragma unroll
+    for (int p = 0; p < NW; ++p)
+        copy_out(reinterpret_cast<const uint8_t*>(stage), a.sums[p] + doff, sbytes);
+    if (bad & 0x55555555u) {  // rare: locate the chunk's first corrupt element
+        for (uint32_t q = 0; q < nbytes; ++q) {
             for (int w = 0; w < NW; ++w) {
-                const uint32_t b = base[w][q] & (base[w][q] >> 1) & 0x55u;
-                if (b) {
+                const uint32_t bb = base[w][q] & (base[w][q] >> 1) & 0x55u;
+                if (bb) {
                     raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
-                                block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
+                                block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(bb) - 1) >> 1));
                     return;
                 }
             }
+        }
     }
 }
 
@@ -963,7 +1039,13 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
         case 2: k1_stats<TableSource, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
         case 3: k1_stats<TableSource, 8, 2><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        default: k1_stats<TableSource, 8, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 4: k1_stats<TableSource, 8, 1, 6><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 5: k1_stats<TableSource, 4, 1, 8><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 6: k1_stats<TableSource, 6, 1, 6><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 8: k1_stats<TableSource, 4, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 9: k1_stats<TableSource, 8, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        default:  // 8 float4 in flight per thread, <= 64 registers: 4 CTAs/SM (tools/k1_probe.py)
+            k1_stats<TableSource, 8, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
     }
     return launch_status();
 }
@@ -977,7 +1059,7 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
     l.tensor = 0;
     l.first_chunk = 0;
     l.n_chunks = nc;
-    k1_stats<SingleSource><<<nc, kThreads, 0, st>>>(SingleSource{l, kChunk}, o);
+    k1_stats<SingleSource, 8, 1, 4><<<nc, kThreads, 0, st>>>(SingleSource{l, kChunk}, o);
     return launch_status();
 }
 
@@ -989,7 +1071,10 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
     if (p.fuse_decode) {
-        k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+        if (p.fuse_decode == 2)
+            k2_ternarize<TableSource, false, 4, 3, 2><<<n_chunks, kThreads, 0, st>>>(src, a);
+        else
+            k2_ternarize<TableSource, false, 4, 3, 1><<<n_chunks, kThreads, 0, st>>>(src, a);
         return launch_status();
     }
     switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
