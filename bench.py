@@ -233,7 +233,7 @@ def run_b200(args):
     plan = sw.plan
     info = tg._lib.PlanInfo()
     tg._lib.check(tg._lib.load().tgb_plan_get_info(plan.h, tg.codec.C.byref(info)), "info")
-    mode = ["none", "nccl", "fused", "sharded"][info.exchange]
+    mode = tg._lib.EXCHANGE_NAMES[info.exchange]
     # algorithmic HBM bytes per element per GPU:
     #   allgather designs: B(N) = 12 + 0.5 N;
     #   sharded: 4 (K1) + 4.25 (K2) + 0.25 (K3a codes) + 2 x sums (land + K3b read) + 4 = 12.5 + 2 w
@@ -419,7 +419,8 @@ def run_b200(args):
     groups = 2 if plan.grouped else 1
     # own kernels per tgb_step: N=1: K1 + K2(decode fused); fused: K1 + K2 + barrier + K3;
     # sharded: K1 + K2 + barrier + K3a + barrier + K3b; nccl: K1 + K2 + K3 (+ NCCL's own)
-    launches_per_step = groups * {"none": 2, "fused": 4, "sharded": 6, "nccl": 3}[mode]
+    launches_per_step = groups * {"none": 2, "fused": 4, "sharded": 6, "nccl": 3,
+                                  "pipelined": 2}[mode]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K,
@@ -449,13 +450,16 @@ def run_b200(args):
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
             "gpu_launches": launches_per_step * K,
             "gpu_launches_note": "own kernels per tgb_step and layer group: N=1 K1 + K2 (K2 "
-                                 "also decodes); fused K1 + K2 + peer barrier + K3; sharded K1 + "
-                                 "K2 + barrier + K3a (owner sums) + barrier + K3b; nccl K1 + K2 + "
-                                 "K3",
+                                 "also decodes); pipelined K1 + K23; fused K1 + K2 + peer barrier "
+                                 "+ K3; sharded K1 + K2 + barrier + K3a (owner sums) + barrier + "
+                                 "K3b; nccl K1 + K2 + K3",
             "exchange": {"fused": "fused NVLink peer stores in K2 + device barrier",
                          "sharded": "sharded: K2 stores codes at the chunk owner, owner sums N "
                                     "workers into packed sums stored at every rank (NVLink), "
                                     "2 device barriers",
+                         "pipelined": "pipelined: one persistent K2+K3 kernel, codes stored "
+                                      "into every rank item by item (NVLink), per-item epoch "
+                                      "flags, decode overlapped with ternarize",
                          "nccl": "NCCL allgather", "none": "none (N=1)"}[mode],
             "clocks": clocks,
             "e2e": e2e,

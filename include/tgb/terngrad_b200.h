@@ -103,6 +103,9 @@ typedef struct tgb_plan_info {
 #define TGB_EXCHANGE_FUSED 2   /* K1/K2 store scalers + codes into every peer (NVLink) */
 #define TGB_EXCHANGE_SHARDED 3 /* codes to the chunk's owner, owner sums N workers and
                                   stores packed sums into every peer, K3 decodes sums */
+#define TGB_EXCHANGE_PIPELINED 4 /* one persistent kernel per step: codes stored into every
+                                    peer item by item, per-item epoch flags, each item
+                                    decoded as soon as all ranks published it */
 
 /* One block of the encoded gradient (EncodedGradient::blocks, codec.hpp:70-76):
  * a bucket of a ternary layer (TernaryBlock, the whole layer unless FixedSize)

@@ -32,6 +32,8 @@ TGB_BUCKET_PER_TENSOR, TGB_BUCKET_GLOBAL, TGB_BUCKET_FIXED = 0, 1, 2
 TGB_SHARE_REF, TGB_SHARE_PRESHARED = 0, 1
 UNIQUE_ID_BYTES = 128
 TGB_EXCHANGE_NONE, TGB_EXCHANGE_NCCL, TGB_EXCHANGE_FUSED, TGB_EXCHANGE_SHARDED = 0, 1, 2, 3
+TGB_EXCHANGE_PIPELINED = 4
+EXCHANGE_NAMES = ["none", "nccl", "fused", "sharded", "pipelined"]
 
 # every symbol the header declares (checked by tests/test_capi.py)
 EXPORTS = [

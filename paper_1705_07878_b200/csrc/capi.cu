@@ -124,12 +124,16 @@ struct tgb_plan {
     bool bound = false;
     int32_t k2_variant = 0;  // TGB_K2V
     int32_t k1_variant = 0;  // TGB_K1V
-    int32_t fuse_mode = 2;   // TGB_FUSEV: N == 1 decode inside K2, 1 post pass, 2 in-loop
     int32_t k3_variant = 1;  // TGB_K3V: 1 smem-staged (default, tools/k3_probe.py), 0 byte loads
     // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
     // K2 chunks [cs[r], cs[r+1]) and reduces them to packed sums for every rank.
     // d_ipc = [gather parity 0][gather parity 1][sums parity 0][sums parity 1][flags]
     bool shard_capable = false, shard = false;
+    // pipelined fused exchange (attached, shared scalers, not sharded): one
+    // persistent K2+K3 kernel per step with per-item epoch flags
+    // (d_ipc + pflags_off: [item][kMaxPeers] u32) instead of the step barrier
+    bool pipe_capable = false, pipe = false;
+    uint64_t pflags_off = 0;
     int32_t nib = 1;  // 4-bit sums (N <= 7), else 8-bit
     uint64_t sums_bytes = 0, sums_off = 0;
     uint32_t cs[kMaxPeers + 1] = {};
@@ -221,7 +225,6 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K3V")) P->k3_variant = std::atoi(m);
-    if (const char* m = std::getenv("TGB_FUSEV")) P->fuse_mode = std::atoi(m) == 1 ? 1 : 2;
     P->worker = worker;
     P->n_workers = n_workers;
     P->desc.assign(layers, layers + n_layers);
@@ -310,7 +313,10 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     P->shard_capable = n_workers >= shard_min && n_workers <= kMaxPeers && params->scaler_sharing;
     if (const char* m = std::getenv("TGB_SHARD")) P->shard_capable = P->shard_capable && std::atoi(m) != 0;
     P->nib = n_workers <= 7 ? 1 : 0;
-    bool want = !P->shard_capable && big >= 0 && n_layers > 1 &&
+    P->pipe_capable = n_workers >= 2 && n_workers <= kMaxPeers && params->scaler_sharing &&
+                      !P->shard_capable;
+    if (const char* m = std::getenv("TGB_PIPE")) P->pipe_capable = P->pipe_capable && std::atoi(m) != 0;
+    bool want = !P->shard_capable && !P->pipe_capable && big >= 0 && n_layers > 1 &&
                 params->bucketing == TGB_BUCKET_PER_TENSOR &&
                 params->share_mode == TGB_SHARE_REF && layers[big].n * 100 >= P->total * 35 &&
                 layers[big].n * 100 <= P->total * 95;
@@ -402,7 +408,9 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
         const uint64_t g = P->push_bytes * static_cast<uint64_t>(n_workers);
         P->sums_off = 2 * g;
         P->flags_off = P->sums_off + 2 * P->sums_bytes;
-        const uint64_t bytes = P->flags_off + round_up(2 * kMaxPeers * sizeof(uint64_t), kAlignPush);
+        P->pflags_off = P->flags_off + round_up(2 * kMaxPeers * sizeof(uint64_t), kAlignPush);
+        const uint64_t pflags = P->pipe_capable ? P->h_chunks.size() * kMaxPeers * sizeof(uint32_t) : 0;
+        const uint64_t bytes = P->pflags_off + round_up(std::max<uint64_t>(pflags, 1), kAlignPush);
         ok = cudaMalloc(&P->d_ipc, bytes) == cudaSuccess &&
              cudaMemset(P->d_ipc, 0, bytes) == cudaSuccess;
         P->d_gathered = P->d_ipc;
@@ -472,6 +480,7 @@ tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
     o->exchange = P->n_workers == 1 ? TGB_EXCHANGE_NONE
                   : !P->attached    ? TGB_EXCHANGE_NCCL
                   : P->shard        ? TGB_EXCHANGE_SHARDED
+                  : P->pipe         ? TGB_EXCHANGE_PIPELINED
                                     : TGB_EXCHANGE_FUSED;
     return TGB_OK;
 }
@@ -581,7 +590,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
                               bool fuse_decode = false) {
     uint8_t* own = own_push(P);
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
-    k.fuse_decode = fuse_decode ? P->fuse_mode : 0;
+    k.fuse_decode = fuse_decode ? 1 : 0;
     k.variant = P->k2_variant;
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
@@ -647,6 +656,27 @@ static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
     const uint32_t r = static_cast<uint32_t>(P->rank);
     TGB_CUDA(launch_k3_reduce(P->d_fat + P->cs[r], P->cs[r + 1] - P->cs[r], shard_launch(P), st));
     TGB_TRY_INNER(launch_barrier(P, 1, st));
+    return TGB_OK;
+}
+
+// pipelined K2+K3 (one persistent kernel; codes to every rank, per-item flags)
+static tgb_status launch_pipelined(tgb_plan* P, uint64_t t, cudaStream_t st) {
+    uint8_t* own = own_push(P);
+    K2Launch k2{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 0};
+    for (int p = 0; p < P->n_workers; ++p) k2.dst.base[p] = push_area(P, p);
+    k2.dst.n = P->n_workers;
+    k2.dst.remote = 1;
+    K3Launch k3{cur_gathered(P), P->push_bytes, P->n_workers, 1,
+                1.0f / static_cast<float>(P->n_workers), P->d_err};
+    PipeLaunch pl{};
+    pl.flags = reinterpret_cast<uint32_t*>(P->d_ipc + P->pflags_off);
+    for (int p = 0; p < P->n_workers; ++p)
+        pl.peer_flags[p] = reinterpret_cast<uint32_t*>(P->peer_ipc[p] + P->pflags_off);
+    pl.epoch = static_cast<uint32_t>(P->epoch);
+    pl.rank = P->rank;
+    pl.n_items = static_cast<uint32_t>(P->h_chunks.size());
+    P->last = st;
+    TGB_CUDA(launch_k23_pipelined(P->d_fat, pl.n_items, k2, k3, pl, st));
     return TGB_OK;
 }
 
@@ -747,6 +777,11 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
         TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[1], 0));
         return TGB_OK;
     }
+    if (P->attached && P->pipe) {
+        TGB_TRY(tgb_stats(P, stream));  // K1 (scalers to every rank); epoch++
+        if (P->p.share_mode == TGB_SHARE_PRESHARED) TGB_TRY(tgb_share_scalers(P, C, stream));
+        return launch_pipelined(P, t, st);
+    }
     if (!P->grouped || nccl_exchange) {
         TGB_TRY(tgb_stats(P, stream));
         if (P->p.share_mode == TGB_SHARE_PRESHARED && P->n_workers > 1)
@@ -810,6 +845,7 @@ tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {
     }
     P->attached = true;
     P->shard = P->shard_capable;
+    P->pipe = P->pipe_capable;
     return TGB_OK;
 }
 

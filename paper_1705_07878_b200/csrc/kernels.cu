@@ -199,26 +199,24 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
     }
 }
 
-// kFuse (N == 1: the average is this worker's own decode, K3 folded into K2):
-// 1 = decode pass over the staged codes after the loop, 2 = each thread writes
-// the decoded float4 of every code byte as soon as it is computed, so the
-// output stream overlaps the Philox compute.
-template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, int kFuse = 0>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
-    __shared__ __align__(16) uint8_t stage[kStageBytes];
-    const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
-    ChunkDev ch;
-    LayerDev L;
-    src.get(b, ch, L);
+// Codes of one chunk (work item b) into `stage`; returns the number of staged
+// code bytes (passthrough chunks are copied to their destinations here and
+// return 0). kFuse (N == 1: the average is this worker's own decode, K3 folded
+// into K2): every thread writes the decoded float4 of each code byte as soon as
+// it is computed, so the output stream overlaps the Philox compute. Ends with
+// a CTA barrier (stage complete).
+template <bool kRolling, int U, bool kFuse>
+__device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDev& L,
+                                                  const ChunkDev& ch, uint32_t b,
+                                                  uint8_t* __restrict__ stage, float4* lutv) {
     if (L.flags & kLayerPassthrough) {
-        k2_passthrough<kFuse != 0>(a, L, ch, b);
-        return;
+        k2_passthrough<kFuse>(a, L, ch, b);
+        return 0;
     }
     const float s = a.slots ? a.slots[L.slot] : a.s_imm;
     const float bound = a.bounds ? a.bounds[ch.layer] : INFINITY;
     const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
-    const uint64_t q0 = ch.begin >> 2;  // byte index of this chunk inside the block
     const float* g = L.g + ch.begin;
     const uint32_t tid = threadIdx.x;
 
@@ -237,19 +235,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     const uint32_t nfull = count >> 2;  // bytes whose 4 elements all exist
     // kFuse: byte -> float4 table of (s*float(sum))*invN with invN = 1, sum in
     // {0, +1, -1} (codec.hpp:296, wire.hpp:220): +0, s, -s
-    __shared__ float4 lutv[kFuse ? 256 : 1];
     if (kFuse) {
         const float v0 = __fmul_rn(__fmul_rn(s, 0.0f), 1.0f), v1 = __fmul_rn(__fmul_rn(s, 1.0f), 1.0f),
                     v2 = __fmul_rn(__fmul_rn(s, -1.0f), 1.0f);
         auto val = [&](uint32_t c) { return c == 1u ? v1 : (c == 2u ? v2 : v0); };
         lutv[tid] = make_float4(val(tid & 3u), val((tid >> 2) & 3u), val((tid >> 4) & 3u),
                                 val((tid >> 6) & 3u));
-        if (kFuse == 2) __syncthreads();
+        __syncthreads();
     }
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
-    auto emit = [&](uint32_t qq, uint32_t byte) {  // kFuse == 2: decoded float4 of byte qq
-        if (kFuse != 2) return;
+    auto emit = [&](uint32_t qq, uint32_t byte) {  // kFuse: decoded float4 of byte qq
+        if (!kFuse) return;
         const float4 o = lutv[byte];
         if (vec_out && 4 * qq + 4 <= count) {
             __stcs(reinterpret_cast<float4*>(out) + qq, o);
@@ -381,40 +378,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(L.tensor),
                     block_rng_base(L) + ch.begin);
     __syncthreads();
-    const uint64_t off = L.code_off + q0;
+    return nbytes;
+}
+
+// The staged codes of chunk b to every destination: the rank's own push area
+// and, with peers attached, the same offset of every peer's gather buffer over
+// NVLink (the allgather is fused into K2 and overlaps its Philox-bound compute).
+__device__ __forceinline__ void k2_store_chunk(const K2Args& a, const LayerDev& L,
+                                               const ChunkDev& ch, uint32_t b,
+                                               const uint8_t* stage, uint32_t nbytes) {
+    const uint64_t off = L.code_off + (ch.begin >> 2);
     if (a.dst.n == 0) {
         copy_out(stage, a.push + off, nbytes);
     } else {
         int p0 = 0, p1 = a.dst.n;  // sharded exchange: the chunk's owner only
         if (a.shard_n) p1 = (p0 = shard_owner(a, b)) + 1;
         for (int p = p0; p < p1; ++p) copy_out(stage, a.dst.base[p] + off, nbytes);
-        // No fence: the step barrier kernel runs after this grid completes in
-        // stream order, and grid completion implies its (peer) stores are
-        // performed -- the same guarantee event-based multi-GPU sync relies on.
     }
-    if (kFuse == 1) {
-        // decode pass from the codes still in shared memory (no code re-read,
-        // no extra launch); lutv was filled before the loop
-        if (vec_out) {
-            float4* o4 = reinterpret_cast<float4*>(out);
-            for (uint32_t qq = tid; qq < nfull; qq += kThreads) __stcs(o4 + qq, lutv[stage[qq]]);
-        } else {
-            for (uint32_t qq = tid; qq < nfull; qq += kThreads) {
-                const float4 o = lutv[stage[qq]];
-                out[4 * qq] = o.x;
-                out[4 * qq + 1] = o.y;
-                out[4 * qq + 2] = o.z;
-                out[4 * qq + 3] = o.w;
-            }
-        }
-        if (tid == 0 && nfull < nbytes) {  // partial last byte (pad codes are 00)
-            const float4 o = lutv[stage[nfull]];
-            const uint32_t rem = count - 4 * nfull;
-            out[4 * nfull] = o.x;
-            if (rem > 1) out[4 * nfull + 1] = o.y;
-            if (rem > 2) out[4 * nfull + 2] = o.z;
-        }
-    }
+}
+
+template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
+    __shared__ __align__(16) uint8_t stage[kStageBytes];
+    __shared__ float4 lutv[kFuse ? 256 : 1];
+    const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
+    ChunkDev ch;
+    LayerDev L;
+    src.get(b, ch, L);
+    const uint32_t nbytes = k2_code_chunk<kRolling, U, kFuse>(a, L, ch, b, stage, lutv);
+    // No fence after the peer stores: the step barrier kernel runs after this
+    // grid completes in stream order, and grid completion implies its (peer)
+    // stores are performed -- the guarantee event-based multi-GPU sync relies on.
+    if (nbytes) k2_store_chunk(a, L, ch, b, stage, nbytes);
 }
 
 // ====================================================================== K3
@@ -599,22 +594,18 @@ __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs 
 // bytes for U positions are loaded before use, no per-load address math or
 // bounds checks on full chunks. Same arithmetic as k3_decode (LUT of
 // (s*float(sum))*invN indexed by N + sum).
+// One chunk; tab[] must hold lane_biased (written before the first barrier
+// here); lut/sw are per-chunk scratch, safe to reuse across calls.
 template <int NW>
-__global__ void __launch_bounds__(kThreads) k3_decode_nw(TableSource src, K3Args a) {
-    ChunkDev ch;
-    LayerDev L;
-    src.get(blockIdx.x, ch, L);
+__device__ __forceinline__ void k3_chunk_nw(const K3Args& a, const LayerDev& L, const ChunkDev& ch,
+                                            const uint32_t* tab, float* lut, float* sw) {
     if (L.flags & kLayerPassthrough) {
         const uint64_t off = L.code_off + 4ull * ch.begin;
         k3_passthrough([&](int w) { return reinterpret_cast<const float*>(a.src + a.stride * w + off); },
                        NW, L.out + ch.begin, ch.count, (L.flags & kLayerVecOut) != 0);
         return;
     }
-    __shared__ uint32_t tab[256];
-    __shared__ float lut[2 * NW + 1];
-    __shared__ float sw[NW];
     const uint32_t tid = threadIdx.x;
-    tab[tid] = lane_biased(tid);
     if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
     const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
@@ -676,6 +667,112 @@ __global__ void __launch_bounds__(kThreads) k3_decode_nw(TableSource src, K3Args
                     return;
                 }
             }
+    }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kThreads) k3_decode_nw(TableSource src, K3Args a) {
+    __shared__ uint32_t tab[256];
+    __shared__ float lut[2 * NW + 1];
+    __shared__ float sw[NW];
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    tab[threadIdx.x] = lane_biased(threadIdx.x);
+    k3_chunk_nw<NW>(a, L, ch, tab, lut, sw);
+}
+
+// ================================================ pipelined fused exchange
+// N >= 2, peers attached (TGB_PIPE, default): ONE persistent kernel per step
+// runs K2 and K3. CTA j takes work items j, j+G, j+2G, ... (G = resident CTAs).
+// Per item: ternarize into smem; publish the PREVIOUS item (fence.sys, then
+// epoch flag -> every rank: its stores were issued one item ago, so the fence
+// is cheap); store this item's codes into every rank's gather buffer; decode
+// the item from two iterations back once every rank's flag for it reached the
+// epoch. Decoding (HBM-bound) thus overlaps Philox (issue-bound) and the
+// NVLink stores, and there is no step barrier: decoding item c at epoch e
+// needs every rank's flag e for c, i.e. every rank finished step e-1, so the
+// parity-(e+1) buffers this rank writes next step are free (double buffering).
+// Deadlock freedom: item j+kG waits only on items j+(k-2)G of the same CTA
+// index on every rank; all G CTAs are resident (grid sized by occupancy).
+struct PipeArgs {
+    K2Args k2;
+    K3Args k3;
+    uint32_t* flags;                 // this rank's flags: [item][rank]
+    uint32_t* peer_flags[kMaxPeers]; // every rank's flags array (self included)
+    uint32_t epoch;
+    int32_t rank;
+    uint32_t n_items;
+};
+
+__device__ __forceinline__ void pipe_publish(const PipeArgs& a, uint32_t c, int n) {
+    __syncthreads();  // the CTA's stores of item c happen-before thread 0's fence
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < n; ++p) {
+            uint32_t* f = a.peer_flags[p] + c * kMaxPeers + a.rank;
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(a.epoch) : "memory");
+        }
+    }
+}
+
+__device__ __forceinline__ void pipe_wait(const PipeArgs& a, uint32_t c, int n) {
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        for (int w = 0; w < n; ++w) {
+            const uint32_t* f = a.flags + c * kMaxPeers + w;
+            uint32_t v;
+            for (uint32_t spin = 0;; ++spin) {
+                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if (static_cast<int32_t>(v - a.epoch) >= 0) break;
+                if (spin > 64) __nanosleep(256);
+                if ((spin & 255) == 255 && clock64() - t0 > 20000000000ll) {  // ~10 s
+                    raise_error(a.k3.err, TGB_E_PEER_TIMEOUT, -1, static_cast<uint64_t>(w));
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kThreads, 3) k23_pipelined(TableSource src, PipeArgs a) {
+    __shared__ __align__(16) uint8_t stage[kStageBytes];
+    __shared__ uint32_t tab[256];
+    __shared__ float lut[2 * NW + 1];
+    __shared__ float sw[NW];
+    tab[threadIdx.x] = lane_biased(threadIdx.x);
+    const uint32_t G = gridDim.x, n = a.n_items;
+    // items walk last-to-first (re-read K1's L2-resident tail first)
+    auto item = [&](uint32_t k) { return n - 1 - (blockIdx.x + k * G); };
+    uint32_t k = 0;
+    for (; blockIdx.x + k * G < n; ++k) {
+        const uint32_t c = item(k);
+        ChunkDev ch;
+        LayerDev L;
+        src.get(c, ch, L);
+        __syncthreads();  // stage is free (previous item's stores were issued)
+        const uint32_t nb = k2_code_chunk<false, 4, false>(a.k2, L, ch, c, stage, nullptr);
+        if (k >= 1) pipe_publish(a, item(k - 1), NW);
+        if (nb) k2_store_chunk(a.k2, L, ch, c, stage, nb);
+        if (k >= 2) {
+            const uint32_t d = item(k - 2);
+            pipe_wait(a, d, NW);
+            ChunkDev dch;
+            LayerDev dL;
+            src.get(d, dch, dL);
+            k3_chunk_nw<NW>(a.k3, dL, dch, tab, lut, sw);
+        }
+    }
+    if (k >= 1) pipe_publish(a, item(k - 1), NW);
+    for (uint32_t j = k >= 2 ? k - 2 : 0; j < k; ++j) {
+        const uint32_t d = item(j);
+        pipe_wait(a, d, NW);
+        ChunkDev dch;
+        LayerDev dL;
+        src.get(d, dch, dL);
+        k3_chunk_nw<NW>(a.k3, dL, dch, tab, lut, sw);
     }
 }
 
@@ -1071,10 +1168,7 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
     if (p.fuse_decode) {
-        if (p.fuse_decode == 2)
-            k2_ternarize<TableSource, false, 4, 3, 2><<<n_chunks, kThreads, 0, st>>>(src, a);
-        else
-            k2_ternarize<TableSource, false, 4, 3, 1><<<n_chunks, kThreads, 0, st>>>(src, a);
+        k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
         return launch_status();
     }
     switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
@@ -1188,6 +1282,59 @@ cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const Sh
         k3_expand<true><<<n_chunks, kThreads, 0, st>>>(src, a);
     else
         k3_expand<false><<<n_chunks, kThreads, 0, st>>>(src, a);
+    return launch_status();
+}
+
+static PipeArgs pipe_args(const K2Launch& k2, const K3Launch& k3, const PipeLaunch& p) {
+    PipeArgs a{};
+    a.k2 = K2Args{k2.push, k2.slots, k2.bounds, k2.err, k2.t, 0, 0, 0.0f, 0, k2.dst};
+    a.k2.shard_n = 0;
+    a.k3 = K3Args{k3.src, k3.stride, nullptr, nullptr, 0.0f, k3.n_workers, k3.sharing, k3.inv_n,
+                  k3.err};
+    a.flags = p.flags;
+    for (int r = 0; r < kMaxPeers; ++r) a.peer_flags[r] = p.peer_flags[r];
+    a.epoch = p.epoch;
+    a.rank = p.rank;
+    a.n_items = p.n_items;
+    return a;
+}
+
+template <int NW>
+static cudaError_t pipe_grid(uint32_t* grid) {
+    int dev = 0, sms = 0, per = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k23_pipelined<NW>, kThreads, 0);
+    *grid = static_cast<uint32_t>(sms * per);
+    return e;
+}
+
+cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const K2Launch& k2,
+                                 const K3Launch& k3, const PipeLaunch& p, cudaStream_t st) {
+    if (n_items == 0) return cudaSuccess;
+    const PipeArgs a = pipe_args(k2, k3, p);
+    const TableSource src{chunks};
+    uint32_t g = 0;
+    cudaError_t e = cudaSuccess;
+#define TGB_PIPE_CASE(NW)                                                             \
+    case NW:                                                                          \
+        e = pipe_grid<NW>(&g);                                                        \
+        if (e != cudaSuccess) return e;                                               \
+        g = g < n_items ? g : n_items;                                                \
+        k23_pipelined<NW><<<g, kThreads, 0, st>>>(src, a);                            \
+        break;
+    switch (k3.n_workers) {
+        TGB_PIPE_CASE(2)
+        TGB_PIPE_CASE(3)
+        TGB_PIPE_CASE(4)
+        TGB_PIPE_CASE(5)
+        TGB_PIPE_CASE(6)
+        TGB_PIPE_CASE(7)
+        TGB_PIPE_CASE(8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TGB_PIPE_CASE
     return launch_status();
 }
 

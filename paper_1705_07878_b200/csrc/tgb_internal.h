@@ -70,6 +70,14 @@ struct ShardLaunch {
     ErrWord* err;
 };
 
+struct PipeLaunch {
+    uint32_t* flags;                  // this rank's item flags [item][kMaxPeers]
+    uint32_t* peer_flags[kMaxPeers];  // every rank's flags array
+    uint32_t epoch;
+    int32_t rank;
+    uint32_t n_items;
+};
+
 cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
@@ -86,6 +94,8 @@ cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const Sh
                              cudaStream_t st);
 cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
                              cudaStream_t st);
+cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const K2Launch& k2,
+                                 const K3Launch& k3, const PipeLaunch& p, cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,

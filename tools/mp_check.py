@@ -84,7 +84,7 @@ def main():
         info = tg._lib.PlanInfo()
         tg._lib.check(tg._lib.load().tgb_plan_get_info(sw.plan.h, tg.codec.C.byref(info)), "info")
         report["checks"][key] = {"ranks_identical": ok_same, "matches_oracle": ok_ref,
-                                 "exchange": ["none", "nccl", "fused", "sharded"][info.exchange]}
+                                 "exchange": tg._lib.EXCHANGE_NAMES[info.exchange]}
         dist.barrier()
         sw.plan.close()
 
@@ -123,7 +123,7 @@ def main():
         n = sum(sw.ns)
         info = tg._lib.PlanInfo()
         tg._lib.check(tg._lib.load().tgb_plan_get_info(p.h, tg.codec.C.byref(info)), "info")
-        report["vgg16_exchange"] = ["none", "nccl", "fused", "sharded"][info.exchange]
+        report["vgg16_exchange"] = tg._lib.EXCHANGE_NAMES[info.exchange]
         report["vgg16_ms_per_step_max_over_ranks"] = float(t_all[0])
         report["stage_ms_median_max_over_ranks"] = {
             k: float(v) for k, v in zip(["K1", "K2", "sync", "K3"], t_all[1:])}
