@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -134,6 +135,9 @@ struct tgb_plan {
     // (d_ipc + pflags_off: [item][kMaxPeers] u32) instead of the step barrier
     bool pipe_capable = false, pipe = false;
     uint64_t pflags_off = 0;
+    uint32_t* d_done = nullptr;             // pipelined: local per-item done flags
+    unsigned long long* d_pprof = nullptr;  // TGB_PIPE_PROF (A/B instrumentation)
+    uint64_t pipe_steps = 0;
     int32_t nib = 1;  // 4-bit sums (N <= 7), else 8-bit
     uint64_t sums_bytes = 0, sums_off = 0;
     uint32_t cs[kMaxPeers + 1] = {};
@@ -308,14 +312,22 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     for (int32_t l = 0; l < n_layers; ++l)
         if (!(layers[l].flags & TGB_LAYER_PASSTHROUGH) && (big < 0 || layers[l].n > layers[big].n))
             big = l;
-    int shard_min = 3;  // measured: the allgather design wins at N = 2
+    // sharded exchange from N >= 5 (TGB_SHARD_MIN): measured at N = 4 the fused
+    // two-group schedule wins (0.425 vs 0.447 ms, VGG-16); the sharded design moves
+    // 0.25(N-1)/N + w(N-1)/N bytes/element over NVLink instead of 0.25(N-1), which
+    // is the dominant cost at N = 8
+    int shard_min = 5;
     if (const char* m = std::getenv("TGB_SHARD_MIN")) shard_min = std::max(2, std::atoi(m));
     P->shard_capable = n_workers >= shard_min && n_workers <= kMaxPeers && params->scaler_sharing;
     if (const char* m = std::getenv("TGB_SHARD")) P->shard_capable = P->shard_capable && std::atoi(m) != 0;
     P->nib = n_workers <= 7 ? 1 : 0;
-    P->pipe_capable = n_workers >= 2 && n_workers <= kMaxPeers && params->scaler_sharing &&
-                      !P->shard_capable;
-    if (const char* m = std::getenv("TGB_PIPE")) P->pipe_capable = P->pipe_capable && std::atoi(m) != 0;
+    // pipelined K2+K3 kernel: opt-in (TGB_PIPE=1). Bit-exact, but measured slower
+    // than the two-group schedule (N=2 0.443 vs 0.326 ms, N=4 0.486 vs 0.425 ms):
+    // items wait on peers' per-item flags
+    P->pipe_capable = false;
+    if (const char* m = std::getenv("TGB_PIPE"))
+        P->pipe_capable = std::atoi(m) != 0 && n_workers >= 2 && n_workers <= kMaxPeers &&
+                          params->scaler_sharing && !P->shard_capable;
     bool want = !P->shard_capable && !P->pipe_capable && big >= 0 && n_layers > 1 &&
                 params->bucketing == TGB_BUCKET_PER_TENSOR &&
                 params->share_mode == TGB_SHARE_REF && layers[big].n * 100 >= P->total * 35 &&
@@ -413,6 +425,10 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
         const uint64_t bytes = P->pflags_off + round_up(std::max<uint64_t>(pflags, 1), kAlignPush);
         ok = cudaMalloc(&P->d_ipc, bytes) == cudaSuccess &&
              cudaMemset(P->d_ipc, 0, bytes) == cudaSuccess;
+        if (ok && P->pipe_capable) {
+            const size_t nd = std::max<size_t>(1, P->h_chunks.size()) * sizeof(uint32_t);
+            ok = cudaMalloc(&P->d_done, nd) == cudaSuccess && cudaMemset(P->d_done, 0, nd) == cudaSuccess;
+        }
         P->d_gathered = P->d_ipc;
     }
     const std::vector<float> inf_bounds(nbl, INFINITY);  // empty / unclipped: no clip (codec.hpp:118)
@@ -440,6 +456,18 @@ void tgb_plan_destroy(tgb_plan* P) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(P->device);
+    if (P->d_pprof) {  // A/B instrumentation: mean cycles per step per phase (all CTAs summed)
+        unsigned long long h[8] = {};
+        if (cudaMemcpy(h, P->d_pprof, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess && P->pipe_steps)
+            std::fprintf(stderr,
+                         "[tgb pipe prof rank %d] cycles/step summed over CTAs: wait %.3g prepare %.3g "
+                         "code %.3g finish %.3g publish %.3g store %.3g tailwait %.3g taildecode %.3g\n",
+                         P->rank, h[0] / double(P->pipe_steps), h[1] / double(P->pipe_steps),
+                         h[2] / double(P->pipe_steps), h[3] / double(P->pipe_steps),
+                         h[4] / double(P->pipe_steps), h[5] / double(P->pipe_steps),
+                         h[6] / double(P->pipe_steps), h[7] / double(P->pipe_steps));
+        cudaFree(P->d_pprof);
+    }
     cudaFree(P->d_layers);
     cudaFree(P->d_tensors);
     cudaFree(P->d_fat);
@@ -452,6 +480,7 @@ void tgb_plan_destroy(tgb_plan* P) {
         for (int p = 0; p < P->n_workers; ++p)
             if (p != P->rank && P->peer_ipc[p]) cudaIpcCloseMemHandle(P->peer_ipc[p]);
     cudaFree(P->d_ipc);
+    cudaFree(P->d_done);
     cudaFree(P->d_err);
     for (int g = 0; g < 2; ++g) {
         if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
@@ -675,6 +704,16 @@ static tgb_status launch_pipelined(tgb_plan* P, uint64_t t, cudaStream_t st) {
     pl.epoch = static_cast<uint32_t>(P->epoch);
     pl.rank = P->rank;
     pl.n_items = static_cast<uint32_t>(P->h_chunks.size());
+    pl.done = P->d_done;
+    if (const char* m = std::getenv("TGB_PIPEV")) pl.variant = std::atoi(m);
+    if (std::getenv("TGB_PIPE_PROF")) {
+        if (!P->d_pprof) {
+            TGB_CUDA(cudaMalloc(&P->d_pprof, 8 * sizeof(unsigned long long)));
+            TGB_CUDA(cudaMemset(P->d_pprof, 0, 8 * sizeof(unsigned long long)));
+        }
+        pl.prof = P->d_pprof;
+        ++P->pipe_steps;
+    }
     P->last = st;
     TGB_CUDA(launch_k23_pipelined(P->d_fat, pl.n_items, k2, k3, pl, st));
     return TGB_OK;

@@ -205,10 +205,18 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
 // into K2): every thread writes the decoded float4 of each code byte as soon as
 // it is computed, so the output stream overlaps the Philox compute. Ends with
 // a CTA barrier (stage complete).
-template <bool kRolling, int U, bool kFuse>
+struct NoHook {
+    __device__ __forceinline__ void operator()(uint32_t) const {}
+};
+
+// hook(i) runs once per iteration i of the vectorised main loop (the pipelined
+// kernel decodes a slice of an older item there, interleaving HBM streaming
+// with the Philox compute).
+template <bool kRolling, int U, bool kFuse, class Hook = NoHook>
 __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDev& L,
                                                   const ChunkDev& ch, uint32_t b,
-                                                  uint8_t* __restrict__ stage, float4* lutv) {
+                                                  uint8_t* __restrict__ stage, float4* lutv,
+                                                  const Hook& hook = Hook()) {
     if (L.flags & kLayerPassthrough) {
         k2_passthrough<kFuse>(a, L, ch, b);
         return 0;
@@ -315,7 +323,10 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
     } else if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         // uniform trip count (every thread runs every block: __syncthreads below)
-        for (uint32_t blk = 0; blk + U * kThreads <= nfull; blk += U * kThreads, q += U * kThreads) {
+        uint32_t it = 0;
+        for (uint32_t blk = 0; blk + U * kThreads <= nfull;
+             blk += U * kThreads, q += U * kThreads, ++it) {
+            hook(it);
             float4 v[U];
             uint32_t ctr[U];
             uint4 r[U];
@@ -703,15 +714,105 @@ struct PipeArgs {
     uint32_t epoch;
     int32_t rank;
     uint32_t n_items;
+    uint32_t* done;                  // this rank's per-item "stores issued" flags (local)
+    unsigned long long* prof;        // optional phase cycle counters (TGB_PIPE_PROF)
 };
 
-__device__ __forceinline__ void pipe_publish(const PipeArgs& a, uint32_t c, int n) {
-    __syncthreads();  // the CTA's stores of item c happen-before thread 0's fence
+// Item c's stores are issued by the whole CTA: a GPU-scope release of a local
+// done flag (MEMBAR.GPU: cheap). The sys-scope fence that makes them visible to
+// peers is paid once per batch by the publisher CTA (pipe_publisher): a
+// MEMBAR.SYS costs microseconds regardless of what is outstanding
+// (tools/nvl_probe.cu), so one per item would serialise the pipeline.
+__device__ __forceinline__ void pipe_done(const PipeArgs& a, uint32_t c) {
+    __syncthreads();  // every thread's stores of item c happen-before thread 0's release
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        for (int p = 0; p < n; ++p) {
-            uint32_t* f = a.peer_flags[p] + c * kMaxPeers + a.rank;
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(a.epoch) : "memory");
+        asm volatile("fence.release.gpu;" ::: "memory");
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.done + c), "r"(a.epoch) : "memory");
+    }
+}
+
+// Publisher (CTA 0, warp 0): scans the local done flags of a window of items
+// ahead of the published prefix (completion order = item n-1-pos, iteration
+// major), acquires the newly completed ones, then ONE fence.release.sys covers
+// them all (cumulativity: the producers' stores happen-before their release,
+// which synchronises with this acquire) and their epoch flags go to every rank.
+// Items are published as soon as they complete, not in prefix order.
+constexpr uint32_t kPubWindow = 2048;  // items tracked ahead of the prefix (smem bitmap)
+__device__ __forceinline__ void pipe_publisher(const PipeArgs& a, int n_ranks) {
+    __shared__ uint32_t pub[kPubWindow / 32];  // published bits of [base, base + window)
+    __shared__ uint32_t fresh[kPubWindow / 32];
+    if (threadIdx.x >= 32) return;
+    const uint32_t lane = threadIdx.x, n = a.n_items;
+    for (uint32_t i = lane; i < kPubWindow / 32; i += 32) pub[i] = 0;
+    __syncwarp();
+    const long long t0 = clock64();
+    uint32_t base = 0, idle = 0;  // completion positions [0, base) are published
+    while (base < n) {
+        const uint32_t win = min(kPubWindow, n - base);
+        const uint32_t nwords = (win + 31) / 32;
+        uint32_t any = 0;
+        // relaxed loads, 8 words in flight per lane; the acquire is one fence below
+        for (uint32_t w0 = 0; w0 < nwords; w0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t pos = base + (w0 + u) * 32 + lane;
+                v[u] = a.epoch - 1u;
+                if (w0 + u < nwords && pos < n && !((pub[w0 + u] >> lane) & 1u))
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v[u]) : "l"(a.done + (n - 1 - pos)) : "memory");
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t bits =
+                    __ballot_sync(0xffffffffu, static_cast<int32_t>(v[u] - a.epoch) >= 0);
+                if (lane == 0 && w0 + u < nwords) fresh[w0 + u] = bits;
+                any |= w0 + u < nwords ? bits : 0u;
+            }
+        }
+        __syncwarp();
+        if (any) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the observed flags
+        if (!any) {
+            if (++idle > 64) __nanosleep(200);
+            if ((idle & 1023) == 1023 && clock64() - t0 > 20000000000ll) {  // ~10 s
+                if (lane == 0) raise_error(a.k3.err, TGB_E_PEER_TIMEOUT, -1, ~0ull);
+                return;
+            }
+            continue;
+        }
+        idle = 0;
+        if (lane == 0) asm volatile("fence.release.sys;" ::: "memory");
+        __syncwarp();
+        for (uint32_t w = 0; w < nwords; ++w) {
+            uint32_t bits = fresh[w];
+            while (bits) {
+                const uint32_t b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const uint32_t c = n - 1 - (base + w * 32 + b);
+                if (lane < static_cast<uint32_t>(n_ranks)) {
+                    uint32_t* f = a.peer_flags[lane] + c * kMaxPeers + a.rank;
+                    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(a.epoch) : "memory");
+                }
+            }
+            if (lane == 0) pub[w] |= fresh[w];
+        }
+        __syncwarp();
+        // slide the window past the fully published words
+        uint32_t adv = 0;
+        while (adv * 32 < win) {
+            const uint32_t rem = n - base - adv * 32;  // > 0 while adv * 32 < win
+            const uint32_t valid = rem >= 32 ? 0xffffffffu : (1u << rem) - 1u;
+            if ((pub[adv] & valid) != valid) break;
+            ++adv;
+        }
+        if (adv) {
+            const uint32_t nw = kPubWindow / 32;
+            for (uint32_t i = lane; i < nw; i += 32) {
+                const uint32_t v = i + adv < nw ? pub[i + adv] : 0u;
+                __syncwarp();
+                pub[i] = v;
+            }
+            __syncwarp();
+            base += adv * 32;
         }
     }
 }
@@ -736,43 +837,176 @@ __device__ __forceinline__ void pipe_wait(const PipeArgs& a, uint32_t c, int n) 
     __syncthreads();
 }
 
+// Decode of one item in slices of kThreads * 4 code bytes (4K elements), run
+// from inside the ternarize loop of a newer item. prepare() must be called by
+// the whole CTA (two barriers); slice(i) and finish() touch no shared state
+// except the read-only tab/lut.
 template <int NW>
-__global__ void __launch_bounds__(kThreads, 3) k23_pipelined(TableSource src, PipeArgs a) {
+struct SliceDecoder {
+    const K3Args* a;
+    const uint32_t* tab;
+    const float* lut;
+    const uint8_t* base0;  // worker 0's codes of the item; worker w at + w * stride
+    float* out;
+    uint32_t count, nbytes, n_slices, done;
+    bool vec_out, active;
+    uint32_t bad;
+
+    __device__ __forceinline__ void prepare(const K3Args& args, const LayerDev& L,
+                                            const ChunkDev& ch, const uint32_t* tab_, float* lut_,
+                                            float* sw) {
+        a = &args;
+        tab = tab_;
+        lut = lut_;
+        active = (L.flags & kLayerPassthrough) == 0;
+        done = 0;
+        bad = 0;
+        count = ch.count;
+        nbytes = (count + 3) >> 2;
+        n_slices = active ? (nbytes + 4 * kThreads - 1) / (4 * kThreads) : 0;
+        base0 = args.src + L.code_off + (ch.begin >> 2);
+        out = L.out + ch.begin;
+        vec_out = (L.flags & kLayerVecOut) != 0;
+        if (!active) {  // passthrough item: fp64 mean now (rare, small)
+            const uint64_t off = L.code_off + 4ull * ch.begin;
+            k3_passthrough([&](int w) { return reinterpret_cast<const float*>(args.src + args.stride * w + off); },
+                           NW, out, count, vec_out);
+            return;
+        }
+        const uint32_t tid = threadIdx.x;
+        if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(args.src + args.stride * tid) + L.slot);
+        __syncthreads();
+        if (tid <= 2 * NW) {
+            float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s = fmaxf(s, sw[w]);
+            lut_[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - NW)),
+                                  args.inv_n);  // codec.hpp:296
+        }
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void slice(uint32_t i) {
+        if (i >= n_slices) return;
+        const uint32_t tid = threadIdx.x;
+        const uint32_t qb = i * 4 * kThreads;
+        uint32_t bw[NW][4];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t q = qb + tid + u * kThreads;
+                bw[w][u] = q < nbytes ? __ldcs(base0 + a->stride * w + q) : 0u;
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                acc += tab[bw[w][u]];
+                bad |= bw[w][u] & (bw[w][u] >> 1);
+            }
+            const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
+                                         lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
+            const uint32_t q = qb + tid + u * kThreads;
+            const uint32_t b4 = 4 * q;
+            if (vec_out && b4 + 4 <= count) {
+                __stcs(reinterpret_cast<float4*>(out + b4), o);
+            } else if (q < nbytes) {
+                if (b4 + 0 < count) out[b4 + 0] = o.x;
+                if (b4 + 1 < count) out[b4 + 1] = o.y;
+                if (b4 + 2 < count) out[b4 + 2] = o.z;
+                if (b4 + 3 < count) out[b4 + 3] = o.w;
+            }
+        }
+        done = i + 1;
+    }
+
+    // remaining slices, then corrupt-code reporting
+    __device__ __forceinline__ void finish(const LayerDev& L, const ChunkDev& ch) {
+        for (uint32_t i = done; i < n_slices; ++i) slice(i);
+        if (active && (bad & 0x55u)) {
+            for (uint32_t q = 0; q < nbytes; ++q)
+                for (int w = 0; w < NW; ++w) {
+                    const uint8_t by = base0[a->stride * w + q];
+                    const uint32_t bb = by & (by >> 1) & 0x55u;
+                    if (bb) {
+                        raise_error(a->err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
+                                    block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(bb) - 1) >> 1));
+                        return;
+                    }
+                }
+        }
+        active = false;
+    }
+};
+
+template <int NW, int kMinBlocks = 3, int U = 4>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k23_pipelined(TableSource src, PipeArgs a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     __shared__ uint32_t tab[256];
     __shared__ float lut[2 * NW + 1];
     __shared__ float sw[NW];
+    // CTA 0 (dispatched first, so resident whenever any producer is): publisher
+    const uint32_t G = gridDim.x - 1, n = a.n_items;
+    if (blockIdx.x == 0) {
+        pipe_publisher(a, NW);
+        return;
+    }
+    const uint32_t j0 = blockIdx.x - 1;
     tab[threadIdx.x] = lane_biased(threadIdx.x);
-    const uint32_t G = gridDim.x, n = a.n_items;
     // items walk last-to-first (re-read K1's L2-resident tail first)
-    auto item = [&](uint32_t k) { return n - 1 - (blockIdx.x + k * G); };
+    auto item = [&](uint32_t k) { return n - 1 - (j0 + k * G); };
+    SliceDecoder<NW> dec;
+    dec.n_slices = 0;
     uint32_t k = 0;
-    for (; blockIdx.x + k * G < n; ++k) {
+    // optional phase profile (TGB_PIPE_PROF): clock64 cycles per phase, thread 0
+    long long tp = a.prof ? clock64() : 0;
+    auto mark = [&](int ph) {
+        if (a.prof && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(a.prof + ph, static_cast<unsigned long long>(t - tp));
+            tp = t;
+        }
+    };
+    for (; j0 + k * G < n; ++k) {
         const uint32_t c = item(k);
         ChunkDev ch;
         LayerDev L;
         src.get(c, ch, L);
-        __syncthreads();  // stage is free (previous item's stores were issued)
-        const uint32_t nb = k2_code_chunk<false, 4, false>(a.k2, L, ch, c, stage, nullptr);
-        if (k >= 1) pipe_publish(a, item(k - 1), NW);
-        if (nb) k2_store_chunk(a.k2, L, ch, c, stage, nb);
-        if (k >= 2) {
-            const uint32_t d = item(k - 2);
-            pipe_wait(a, d, NW);
-            ChunkDev dch;
-            LayerDev dL;
-            src.get(d, dch, dL);
-            k3_chunk_nw<NW>(a.k3, dL, dch, tab, lut, sw);
-        }
-    }
-    if (k >= 1) pipe_publish(a, item(k - 1), NW);
-    for (uint32_t j = k >= 2 ? k - 2 : 0; j < k; ++j) {
-        const uint32_t d = item(j);
-        pipe_wait(a, d, NW);
         ChunkDev dch;
         LayerDev dL;
-        src.get(d, dch, dL);
-        k3_chunk_nw<NW>(a.k3, dL, dch, tab, lut, sw);
+        if (k >= 2) {  // decode item k-2 in slices during this item's ternarize loop
+            src.get(item(k - 2), dch, dL);
+            pipe_wait(a, item(k - 2), NW);
+            mark(0);
+            dec.prepare(a.k3, dL, dch, tab, lut, sw);
+        } else {
+            __syncthreads();  // stage is free (previous item's stores were issued)
+        }
+        mark(1);
+        // U = 4: one decode slice per loop iteration; U = 2: every other iteration
+        const uint32_t nb = k2_code_chunk<false, U, false>(
+            a.k2, L, ch, c, stage, nullptr, [&](uint32_t i) {
+                if (k >= 2 && (U == 4 || (i & 1) == 0)) dec.slice(U == 4 ? i : i >> 1);
+            });
+        mark(2);
+        if (k >= 2) dec.finish(dL, dch);
+        mark(3);
+        mark(4);
+        if (nb) k2_store_chunk(a.k2, L, ch, c, stage, nb);
+        pipe_done(a, c);
+        mark(5);
+    }
+    for (uint32_t j = k >= 2 ? k - 2 : 0; j < k; ++j) {
+        ChunkDev dch;
+        LayerDev dL;
+        src.get(item(j), dch, dL);
+        pipe_wait(a, item(j), NW);
+        mark(6);
+        dec.prepare(a.k3, dL, dch, tab, lut, sw);
+        dec.finish(dL, dch);
+        mark(7);
     }
 }
 
@@ -1296,18 +1530,33 @@ static PipeArgs pipe_args(const K2Launch& k2, const K3Launch& k3, const PipeLaun
     a.epoch = p.epoch;
     a.rank = p.rank;
     a.n_items = p.n_items;
+    a.done = p.done;
+    a.prof = p.prof;
     return a;
 }
 
-template <int NW>
-static cudaError_t pipe_grid(uint32_t* grid) {
+template <class K>
+static cudaError_t pipe_launch(K kernel, uint32_t n_items, const TableSource& src,
+                               const PipeArgs& a, cudaStream_t st) {
     int dev = 0, sms = 0, per = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k23_pipelined<NW>, kThreads, 0);
-    *grid = static_cast<uint32_t>(sms * per);
-    return e;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    uint32_t g = static_cast<uint32_t>(sms * per) - 1;  // every CTA resident (deadlock freedom)
+    g = g < n_items ? g : n_items;
+    kernel<<<g + 1, kThreads, 0, st>>>(src, a);  // + the publisher CTA
+    return cudaGetLastError();
+}
+
+template <int NW>
+static cudaError_t pipe_variant(int v, uint32_t n_items, const TableSource& src, const PipeArgs& a,
+                                cudaStream_t st) {
+    switch (v) {  // TGB_PIPEV (A/B)
+        case 1: return pipe_launch(k23_pipelined<NW, 2, 4>, n_items, src, a, st);
+        case 2: return pipe_launch(k23_pipelined<NW, 3, 2>, n_items, src, a, st);
+        default: return pipe_launch(k23_pipelined<NW, 3, 4>, n_items, src, a, st);
+    }
 }
 
 cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const K2Launch& k2,
@@ -1315,27 +1564,16 @@ cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const
     if (n_items == 0) return cudaSuccess;
     const PipeArgs a = pipe_args(k2, k3, p);
     const TableSource src{chunks};
-    uint32_t g = 0;
-    cudaError_t e = cudaSuccess;
-#define TGB_PIPE_CASE(NW)                                                             \
-    case NW:                                                                          \
-        e = pipe_grid<NW>(&g);                                                        \
-        if (e != cudaSuccess) return e;                                               \
-        g = g < n_items ? g : n_items;                                                \
-        k23_pipelined<NW><<<g, kThreads, 0, st>>>(src, a);                            \
-        break;
     switch (k3.n_workers) {
-        TGB_PIPE_CASE(2)
-        TGB_PIPE_CASE(3)
-        TGB_PIPE_CASE(4)
-        TGB_PIPE_CASE(5)
-        TGB_PIPE_CASE(6)
-        TGB_PIPE_CASE(7)
-        TGB_PIPE_CASE(8)
+        case 2: return pipe_variant<2>(p.variant, n_items, src, a, st);
+        case 3: return pipe_variant<3>(p.variant, n_items, src, a, st);
+        case 4: return pipe_variant<4>(p.variant, n_items, src, a, st);
+        case 5: return pipe_variant<5>(p.variant, n_items, src, a, st);
+        case 6: return pipe_variant<6>(p.variant, n_items, src, a, st);
+        case 7: return pipe_variant<7>(p.variant, n_items, src, a, st);
+        case 8: return pipe_variant<8>(p.variant, n_items, src, a, st);
         default: return cudaErrorInvalidValue;
     }
-#undef TGB_PIPE_CASE
-    return launch_status();
 }
 
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,

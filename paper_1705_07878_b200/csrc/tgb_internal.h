@@ -76,6 +76,9 @@ struct PipeLaunch {
     uint32_t epoch;
     int32_t rank;
     uint32_t n_items;
+    int32_t variant = 0;  // TGB_PIPEV (A/B)
+    uint32_t* done = nullptr;  // local per-item done flags (n_items)
+    unsigned long long* prof = nullptr;  // TGB_PIPE_PROF: 8 phase cycle counters
 };
 
 cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
