@@ -188,6 +188,12 @@ tgb_status tgb_plan_last_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_g
 /* the whole worker step: K1 -> [allreduce] -> K2 -> exchange -> K3.
  * comm may be NULL when n_workers == 1. */
 tgb_status tgb_step(tgb_plan* plan, tgb_comm* comm, uint64_t t, void* stream);
+/* tgb_step with HOST buffers (n_layers pointers each, pinned recommended): H2D of
+ * the gradients into the bound device buffers, the step, D2H of the averaged
+ * gradients, all stream-ordered after `stream` and completing before it; the
+ * next call's H2D overlaps this call's D2H (separate copy streams). */
+tgb_status tgb_step_host(tgb_plan* plan, tgb_comm* comm, uint64_t t, const float* const* h_grads,
+                         float* const* h_out, void* stream);
 /* synchronises the plan's last stream, reads and clears the error word */
 tgb_status tgb_check(tgb_plan* plan, tgb_error* out);
 

@@ -41,7 +41,7 @@ EXPORTS = [
     "tgb_plan_create", "tgb_plan_destroy", "tgb_plan_get_info", "tgb_plan_layer_layout",
     "tgb_plan_block_info",
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
-    "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_check",
+    "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_step_host", "tgb_check",
     "tgb_plan_attach_peers", "tgb_plan_last_buffers",
     "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
     "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
@@ -106,6 +106,7 @@ def _declare(L):
         "tgb_sync": (S, [_vp, _vp, _vp]),
         "tgb_decode_average": (S, [_vp, _vp, _i32, _vp]),
         "tgb_step": (S, [_vp, _vp, _u64, _vp]),
+        "tgb_step_host": (S, [_vp, _vp, _u64, C.POINTER(_vp), C.POINTER(_vp), _vp]),
         "tgb_check": (S, [_vp, C.POINTER(Error)]),
         "tgb_plan_attach_peers": (S, [_vp, _vp]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),

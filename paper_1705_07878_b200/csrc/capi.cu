@@ -143,6 +143,12 @@ struct tgb_plan {
     uint32_t cs[kMaxPeers + 1] = {};
     uint32_t chunk3 = kChunk3;
     cudaStream_t last = nullptr;
+    // host-buffer steps (tgb_step_host): per-tensor bound pointers, copy streams
+    std::vector<const float*> bound_g;
+    std::vector<float*> bound_out;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_d2h = nullptr;
+    bool host_io = false;
 };
 
 extern "C" {
@@ -487,6 +493,11 @@ void tgb_plan_destroy(tgb_plan* P) {
         if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
     }
     if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+    if (P->s_h2d) cudaStreamDestroy(P->s_h2d);
+    if (P->s_d2h) cudaStreamDestroy(P->s_d2h);
+    if (P->ev_h2d) cudaEventDestroy(P->ev_h2d);
+    if (P->ev_comp) cudaEventDestroy(P->ev_comp);
+    if (P->ev_d2h) cudaEventDestroy(P->ev_d2h);
     cudaSetDevice(prev);
     delete P;
 }
@@ -551,6 +562,8 @@ tgb_status tgb_plan_bind(tgb_plan* P, const float* const* d_grads, float* const*
         L.out = d_out[L.tensor] ? d_out[L.tensor] + off : nullptr;
         L.flags = (L.flags & ~(kLayerVecIn | kLayerVecOut)) | layer_vec_flags(L.g, L.out);
     }
+    P->bound_g.assign(d_grads, d_grads + nl);
+    P->bound_out.assign(d_out, d_out + nl);
     if (!P->h_layers.empty())
         TGB_CUDA(cudaMemcpy(P->d_layers, P->h_layers.data(), P->h_layers.size() * sizeof(LayerDev),
                             cudaMemcpyHostToDevice));
@@ -848,6 +861,52 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
     }
     TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[0], 0));
     TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[1], 0));
+    return TGB_OK;
+}
+
+// Host-buffer step: H2D of every tensor on a copy stream, tgb_step on `stream`,
+// D2H of every averaged tensor on a second copy stream; `stream` finally waits
+// for the D2H, so synchronising it means the outputs are in host memory. The
+// next call's H2D only waits for this call's compute (the gradient buffers are
+// free once K2 has read them), so it overlaps this call's D2H: PCIe runs full
+// duplex across consecutive steps. Host buffers should be pinned.
+tgb_status tgb_step_host(tgb_plan* P, tgb_comm* C, uint64_t t, const float* const* h_grads,
+                         float* const* h_out, void* stream) {
+    if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    const size_t nl = P->desc.size();
+    if (nl > 0 && (!h_grads || !h_out)) return TGB_ERR_INVALID_ARGUMENT;
+    for (size_t l = 0; l < nl; ++l)
+        if (P->desc[l].n > 0 && (!h_grads[l] || !h_out[l])) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (!P->host_io) {
+        TGB_CUDA(cudaStreamCreateWithFlags(&P->s_h2d, cudaStreamNonBlocking));
+        TGB_CUDA(cudaStreamCreateWithFlags(&P->s_d2h, cudaStreamNonBlocking));
+        TGB_CUDA(cudaEventCreateWithFlags(&P->ev_h2d, cudaEventDisableTiming));
+        TGB_CUDA(cudaEventCreateWithFlags(&P->ev_comp, cudaEventDisableTiming));
+        TGB_CUDA(cudaEventCreateWithFlags(&P->ev_d2h, cudaEventDisableTiming));
+        TGB_CUDA(cudaEventRecord(P->ev_comp, st));  // nothing computed yet
+        TGB_CUDA(cudaEventRecord(P->ev_d2h, st));
+        P->host_io = true;
+    }
+    TGB_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_comp, 0));  // previous K2 read the gradients
+    for (size_t l = 0; l < nl; ++l)
+        if (P->desc[l].n)
+            TGB_CUDA(cudaMemcpyAsync(const_cast<float*>(P->bound_g[l]), h_grads[l],
+                                     P->desc[l].n * sizeof(float), cudaMemcpyHostToDevice,
+                                     P->s_h2d));
+    TGB_CUDA(cudaEventRecord(P->ev_h2d, P->s_h2d));
+    TGB_CUDA(cudaStreamWaitEvent(st, P->ev_h2d, 0));
+    TGB_CUDA(cudaStreamWaitEvent(st, P->ev_d2h, 0));  // previous outputs copied out
+    TGB_TRY(tgb_step(P, C, t, stream));
+    TGB_CUDA(cudaEventRecord(P->ev_comp, st));
+    TGB_CUDA(cudaStreamWaitEvent(P->s_d2h, P->ev_comp, 0));
+    for (size_t l = 0; l < nl; ++l)
+        if (P->desc[l].n)
+            TGB_CUDA(cudaMemcpyAsync(h_out[l], P->bound_out[l], P->desc[l].n * sizeof(float),
+                                     cudaMemcpyDeviceToHost, P->s_d2h));
+    TGB_CUDA(cudaEventRecord(P->ev_d2h, P->s_d2h));
+    TGB_CUDA(cudaStreamWaitEvent(st, P->ev_d2h, 0));
+    P->last = st;
     return TGB_OK;
 }
 

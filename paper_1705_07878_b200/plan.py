@@ -31,16 +31,17 @@ def _view(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
     return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
 
 
-def aligned_flat(ns: Sequence[int], device, align_elems: int = 4, dtype=torch.float32):
-    """One flat HBM buffer holding every tensor at a 16-byte aligned offset.
+def aligned_flat(ns: Sequence[int], device, align_elems: int = 4, dtype=torch.float32,
+                 pin_memory: bool = False):
+    """One flat buffer holding every tensor at a 16-byte aligned offset.
 
     Returns (flat, views). This is the gradient-bucket layout the kernels
-    stream with 128-bit accesses."""
+    stream with 128-bit accesses (pin_memory: page-locked host buffer)."""
     offs, pos = [], 0
     for n in ns:
         offs.append(pos)
         pos += (int(n) + align_elems - 1) // align_elems * align_elems
-    flat = torch.zeros(max(pos, 1), dtype=dtype, device=device)
+    flat = torch.zeros(max(pos, 1), dtype=dtype, device=device, pin_memory=pin_memory)
     views = [flat[o:o + int(n)] for o, n in zip(offs, ns)]
     return flat, views
 
@@ -204,6 +205,21 @@ class Plan:
         check(load().tgb_step(self.h, comm.h if comm is not None else None, int(t),
                               self._st(stream)), "tgb_step")
 
+    def step_host(self, t: int, host_grads: Sequence[torch.Tensor],
+                  host_outs: Sequence[torch.Tensor], comm: Optional[Comm] = None, stream=None):
+        """tgb_step_host: per-layer host (pinned) gradients in, averaged gradients out;
+        completes in `stream` order, the next call's H2D overlaps this call's D2H."""
+        nl = len(self.ns)
+        for h, n in zip(list(host_grads) + list(host_outs), self.ns + self.ns):
+            if h.device.type != "cpu" or h.numel() != n or h.dtype != torch.float32 or \
+                    not h.is_contiguous():
+                raise ValueError("step_host: host tensors must be contiguous float32 of the "
+                                 "planned sizes")
+        gp = (C.c_void_p * max(nl, 1))(*[h.data_ptr() if h.numel() else 0 for h in host_grads])
+        op = (C.c_void_p * max(nl, 1))(*[h.data_ptr() if h.numel() else 0 for h in host_outs])
+        check(load().tgb_step_host(self.h, comm.h if comm is not None else None, int(t), gp, op,
+                                   self._st(stream)), "tgb_step_host")
+
     def error(self) -> _lib.Error:
         e = _lib.Error()
         st = load().tgb_check(self.h, C.byref(e))
@@ -302,6 +318,17 @@ class SyncWorker:
     def step(self, t: int, stream=None) -> List[torch.Tensor]:
         self.plan.step(t, self.comm, stream)
         return self.outs
+
+    def host_buffers(self, pinned: bool = True):
+        """pinned host buffers for step_host: (in_flat, in_views, out_flat, out_views)"""
+        gi, gv = aligned_flat(self.ns, torch.device("cpu"), pin_memory=pinned)
+        go, ov = aligned_flat(self.ns, torch.device("cpu"), pin_memory=pinned)
+        return gi, gv, go, ov
+
+    def step_host(self, t: int, host_grads: Sequence[torch.Tensor],
+                  host_outs: Sequence[torch.Tensor], stream=None):
+        """Worker::run sync segment with host buffers: gradients in, averaged out."""
+        self.plan.step_host(t, host_grads, host_outs, self.comm, stream)
 
     def check(self):
         self.plan.raise_errors()

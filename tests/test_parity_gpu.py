@@ -367,3 +367,27 @@ def test_passthrough_and_bucket_errors():
     blk.codes[0] = 0b00110000  # element 2 of the bucket
     with pytest.raises(tg.CodecError, match="corrupt ternary code 11 in block w at element 2"):
         tg.average([res.encoded], 1, True)
+
+
+def test_step_host_matches_device_step(restated):
+    # tgb_step_host (host buffers in/out, copy streams) == tgb_step on device buffers
+    names = ["conv.weight", "conv.bias", "fc.weight"]
+    ns = [1728, 64, 40003]
+    cfg = tg.CodecConfig(seed=42)
+    w = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    hin, hin_v, hout, hout_v = w.host_buffers()
+    ref = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    for t in range(3):
+        grads = [restated.normal(7 + t, 0, "host/" + nm, n, 1e-3) for nm, n in zip(names, ns)]
+        for v, g in zip(hin_v, grads):
+            v.copy_(torch.from_numpy(g))
+        w.step_host(t, hin_v, hout_v)
+        for v, g in zip(ref.grads, grads):
+            v.copy_(to_dev(g))
+        outs = ref.step(t)
+        torch.cuda.synchronize()
+        w.check()
+        for o, h in zip(outs, hout_v):
+            assert o.cpu().numpy().tobytes() == h.numpy().tobytes()
+    with pytest.raises(ValueError):
+        w.step_host(9, [h[:1] for h in hin_v], hout_v)
