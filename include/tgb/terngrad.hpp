@@ -291,6 +291,32 @@ inline GradTensor decode(const TernaryBlock& blk) {
     return out;
 }
 
+// codec.hpp:485-517 (device histogram; edges/counts identical to the reference's)
+struct HistogramBin {
+    double edge;
+    std::size_t count;
+};
+
+inline std::vector<HistogramBin> histogram(std::span<const float> v, std::size_t bins) {
+    if (bins < 1) throw std::invalid_argument("histogram: bins must be >= 1");
+    detail::DevBuf<float> d(v.size());
+    d.upload(v.data(), v.size());
+    detail::DevBuf<uint64_t> c(bins);
+    detail::DevBuf<double> e(bins);
+    detail::check(tgb_layer_histogram(d.p, v.size(), static_cast<uint32_t>(bins), c.p, e.p, nullptr),
+                  "tgb_layer_histogram");
+    std::vector<uint64_t> hc(bins);
+    std::vector<double> he(bins);
+    c.download(hc.data(), bins);
+    e.download(he.data(), bins);
+    std::vector<HistogramBin> out(bins);
+    for (std::size_t b = 0; b < bins; ++b) out[b] = {he[b], static_cast<std::size_t>(hc[b])};
+    return out;
+}
+inline std::vector<HistogramBin> histogram(const GradTensor& g, std::size_t bins) {
+    return histogram(std::span<const float>(g.values), bins);
+}
+
 namespace detail {
 // one plan per call (value semantics); the hot path keeps plans alive in SyncWorker
 struct PlanHolder {
@@ -552,6 +578,19 @@ public:
         const tgb_status st = tgb_check(plan_, &e);
         if (st == TGB_ERR_CODEC) detail::throw_plan_error(plan_, e, names_);
         detail::check(st, "tgb_check");
+    }
+    // host buffers in/out (pinned recommended): tgb_step_host
+    void step_host(uint64_t t, const std::vector<const float*>& h_grads,
+                   const std::vector<float*>& h_out, cudaStream_t stream = nullptr) {
+        detail::check(tgb_step_host(plan_, comm_ ? comm_->get() : nullptr, t, h_grads.data(),
+                                    h_out.data(), stream),
+                      "tgb_step_host");
+    }
+    // Worker::zero_fraction of the last step's encode (cluster.hpp:336-346)
+    double zero_fraction() {
+        uint64_t nz = 0, tot = 0;
+        detail::check(tgb_plan_code_stats(plan_, &nz, &tot), "tgb_plan_code_stats");
+        return tot ? static_cast<double>(tot - nz) / static_cast<double>(tot) : 0.0;
     }
     tgb_plan* plan() const { return plan_; }
 

@@ -194,6 +194,10 @@ tgb_status tgb_step(tgb_plan* plan, tgb_comm* comm, uint64_t t, void* stream);
  * next call's H2D overlaps this call's D2H (separate copy streams). */
 tgb_status tgb_step_host(tgb_plan* plan, tgb_comm* comm, uint64_t t, const float* const* h_grads,
                          float* const* h_out, void* stream);
+/* telemetry of the last encode: nonzero ternary codes and ternary elements over all
+ * blocks; zero fraction = 1 - nonzero/total (Worker::zero_fraction, cluster.hpp:336-346).
+ * Counted inside K2 (no extra pass). Synchronises the plan's last stream. */
+tgb_status tgb_plan_code_stats(tgb_plan* plan, uint64_t* nonzero, uint64_t* total);
 /* synchronises the plan's last stream, reads and clears the error word */
 tgb_status tgb_check(tgb_plan* plan, tgb_error* out);
 
@@ -226,6 +230,10 @@ tgb_status tgb_layer_average(int32_t n_workers, const uint8_t* const* d_codes, c
  * array of N device pointers; out = float(sum_w double(v_w) / N), worker order */
 tgb_status tgb_layer_average_raw(int32_t n_workers, const float* const* d_vals, uint64_t n,
                                  float* d_out, void* stream);
+/* histogram (codec.hpp:491-517): equal-width bins over [min, max]; d_counts and
+ * d_edges (left edges, double) are device arrays of `bins` entries. Synchronises. */
+tgb_status tgb_layer_histogram(const float* d_v, uint64_t n, uint32_t bins, uint64_t* d_counts,
+                               double* d_edges, void* stream);
 /* RngStream::bits (rng.hpp:59-66) for indices k0..k0+n-1 (KAT helper) */
 tgb_status tgb_rng_bits(uint64_t seed, uint64_t t, uint64_t name_hash, uint64_t worker,
                         uint64_t k0, uint64_t n, uint32_t* d_out, void* stream);

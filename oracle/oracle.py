@@ -225,6 +225,31 @@ class Restated:
         st = self.L.tgo_average_block(N, _ptr(s, _f32p), cp, n, int(sharing), _ptr(out, _f32p))
         return st, out
 
+    def histogram(self, v, bins):
+        """codec.hpp:491-517 restated: lo/hi by the reference's sequential std::min/max
+        chain from v[0], width = (hi - lo) / bins in double, b = size_t((x - lo) / width)
+        clamped to bins - 1 (NaN -> last bin, like the x86-64 conversion)."""
+        v = _f32(v)
+        if bins < 1:
+            raise ValueError("histogram: bins must be >= 1")
+        if v.size == 0:
+            return np.zeros(bins, np.float64), np.zeros(bins, np.uint64)
+        lo = hi = float(v[0])
+        for x in v.astype(np.float64):  # small cases only (pure-Python loop)
+            lo = x if x < lo else lo
+            hi = x if hi < x else hi
+        width = (hi - lo) / float(bins)
+        edges = np.array([lo + width * float(b) for b in range(bins)], np.float64)
+        counts = np.zeros(bins, np.uint64)
+        for x in v.astype(np.float64):
+            if width > 0.0:
+                q = (x - lo) / width
+                b = int(q) if q == q and q < 2.0 ** 64 else bins - 1
+            else:
+                b = 0
+            counts[min(b, bins - 1)] += 1
+        return edges, counts
+
     def average_passthrough(self, vals):
         N = len(vals)
         vs = [_f32(v) for v in vals]
@@ -255,6 +280,8 @@ class Reference:
         L.tgref_stddev.restype = C.c_double
         L.tgref_stddev.argtypes = [_f32p, C.c_size_t]
         L.tgref_clip.argtypes = [_f32p, C.c_size_t, C.c_float, _f32p, _f32p]
+        L.tgref_histogram.argtypes = [_f32p, C.c_size_t, C.c_size_t, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_uint64)]
         L.tgref_scaler.restype = C.c_float
         L.tgref_scaler.argtypes = [_f32p, C.c_size_t]
         L.tgref_ternarize.restype = C.c_int
@@ -324,6 +351,16 @@ class Reference:
     def scaler(self, v):
         v = _f32(v)
         return self.L.tgref_scaler(_ptr(v, _f32p), v.size)
+
+    def histogram(self, v, bins):
+        """codec.hpp:491-517 -> ((status, msg), edges float64[bins], counts uint64[bins])"""
+        v = _f32(v)
+        edges = np.zeros(bins, np.float64)
+        counts = np.zeros(bins, np.uint64)
+        st = self.L.tgref_histogram(_ptr(v, _f32p), v.size, bins,
+                                    edges.ctypes.data_as(C.POINTER(C.c_double)),
+                                    counts.ctypes.data_as(C.POINTER(C.c_uint64)))
+        return (st, self.err() if st else ""), edges, counts
 
     def ternarize(self, g, s, seed, t, name, worker=0, rng_base=0):
         g = _f32(g)

@@ -287,4 +287,19 @@ void tgref_cluster_output(tgref_cluster* c, int worker, float* out) {
 
 void tgref_cluster_destroy(tgref_cluster* c) { delete c; }
 
+// codec.hpp:491-517
+int tgref_histogram(const float* v, std::size_t n, std::size_t bins, double* edges,
+                    std::uint64_t* counts) {
+    try {
+        auto h = histogram(std::span<const float>(v, n), bins);
+        for (std::size_t b = 0; b < bins; ++b) {
+            edges[b] = h[b].edge;
+            counts[b] = h[b].count;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

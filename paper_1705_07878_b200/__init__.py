@@ -5,15 +5,15 @@ Public surface mirrors the reference's namespace ``terngrad``
 All compute runs in libtgb.so (sm_100a); there is no CPU fallback.
 """
 from .codec import (Bucketing, CodecConfig, CodecError, EncodedGradient, EncodeResult,
-                    GradTensor, PassthroughBlock, RngStream, ShareMode, TernaryBlock, average,
-                    clip, clip_bound, decode, encode_step, fnv1a64, scaler, share_scalers,
-                    ternarize)
+                    GradTensor, HistogramBin, PassthroughBlock, RngStream, ShareMode,
+                    TernaryBlock, average, clip, clip_bound, decode, encode_step, fnv1a64,
+                    histogram, scaler, share_scalers, ternarize)
 from .plan import Comm, Plan, SyncWorker, aligned_flat
 from . import layersets
 
 __all__ = [
     "Bucketing", "CodecConfig", "CodecError", "EncodedGradient", "EncodeResult", "GradTensor",
-    "PassthroughBlock", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
+    "HistogramBin", "histogram", "PassthroughBlock", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
     "clip_bound", "decode", "encode_step", "fnv1a64", "scaler", "share_scalers", "ternarize",
     "Comm", "Plan", "SyncWorker", "aligned_flat", "layersets",
 ]

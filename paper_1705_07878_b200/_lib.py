@@ -42,10 +42,12 @@ EXPORTS = [
     "tgb_plan_block_info",
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_step_host", "tgb_check",
+    "tgb_plan_code_stats",
     "tgb_plan_attach_peers", "tgb_plan_last_buffers",
     "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
     "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
-    "tgb_layer_average", "tgb_layer_average_raw", "tgb_rng_bits", "tgb_layer_check",
+    "tgb_layer_average", "tgb_layer_average_raw", "tgb_layer_histogram", "tgb_rng_bits",
+    "tgb_layer_check",
 ]
 
 
@@ -108,6 +110,7 @@ def _declare(L):
         "tgb_step": (S, [_vp, _vp, _u64, _vp]),
         "tgb_step_host": (S, [_vp, _vp, _u64, C.POINTER(_vp), C.POINTER(_vp), _vp]),
         "tgb_check": (S, [_vp, C.POINTER(Error)]),
+        "tgb_plan_code_stats": (S, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
         "tgb_plan_attach_peers": (S, [_vp, _vp]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_comm_unique_id": (S, [C.c_char_p]),
@@ -120,6 +123,7 @@ def _declare(L):
         "tgb_layer_decode": (S, [_vp, _u64, C.c_float, _vp, _vp]),
         "tgb_layer_average": (S, [_i32, C.POINTER(_vp), _vp, _u64, _i32, _vp, _vp]),
         "tgb_layer_average_raw": (S, [_i32, C.POINTER(_vp), _u64, _vp, _vp]),
+        "tgb_layer_histogram": (S, [_vp, _u64, C.c_uint32, _vp, _vp, _vp]),
         "tgb_rng_bits": (S, [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp]),
         "tgb_layer_check": (S, [_vp, C.POINTER(Error)]),
     }

@@ -294,6 +294,28 @@ def decode(blk: TernaryBlock) -> GradTensor:
     return GradTensor(blk.name, [blk.n], out)
 
 
+# ------------------------------------------------------------- telemetry
+@dataclass
+class HistogramBin:
+    """codec.hpp:485-488"""
+    edge: float  # left edge
+    count: int
+
+
+def histogram(values: Union[torch.Tensor, GradTensor], bins: int) -> List[HistogramBin]:
+    """codec.hpp:491-517 on the device (equal-width bins over [min, max])."""
+    if bins < 1:
+        raise ValueError("histogram: bins must be >= 1")
+    v = values.values if isinstance(values, GradTensor) else values.reshape(-1).contiguous()
+    dev = v.device if v.numel() else _dev()
+    counts = torch.zeros(bins, dtype=torch.int64, device=dev)
+    edges = torch.zeros(bins, dtype=torch.float64, device=dev)
+    check(load().tgb_layer_histogram(_ptr(v), v.numel(), int(bins), _ptr(counts), _ptr(edges),
+                                     _stream(dev)), "tgb_layer_histogram")
+    return [HistogramBin(float(e), int(c)) for e, c in zip(edges.cpu().tolist(),
+                                                           counts.cpu().tolist())]
+
+
 # ------------------------------------------------------------- encode_step
 class _PlanCache:
     def __init__(self):

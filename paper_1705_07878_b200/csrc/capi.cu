@@ -136,6 +136,7 @@ struct tgb_plan {
     bool pipe_capable = false, pipe = false;
     uint64_t pflags_off = 0;
     uint32_t* d_done = nullptr;             // pipelined: local per-item done flags
+    unsigned long long* d_nnz = nullptr;    // telemetry: nonzero codes per group (last step)
     unsigned long long* d_pprof = nullptr;  // TGB_PIPE_PROF (A/B instrumentation)
     uint64_t pipe_steps = 0;
     int32_t nib = 1;  // 4-bit sums (N <= 7), else 8-bit
@@ -421,7 +422,9 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
               cudaMalloc(&P->d_counters, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&P->d_bounds, nbl * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&P->d_push, P->push_bytes) == cudaSuccess &&
-              cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess;
+              cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess &&
+              cudaMalloc(&P->d_nnz, 2 * sizeof(unsigned long long)) == cudaSuccess &&
+              cudaMemset(P->d_nnz, 0, 2 * sizeof(unsigned long long)) == cudaSuccess;
     if (ok && n_workers > 1) {
         const uint64_t g = P->push_bytes * static_cast<uint64_t>(n_workers);
         P->sums_off = 2 * g;
@@ -487,6 +490,7 @@ void tgb_plan_destroy(tgb_plan* P) {
             if (p != P->rank && P->peer_ipc[p]) cudaIpcCloseMemHandle(P->peer_ipc[p]);
     cudaFree(P->d_ipc);
     cudaFree(P->d_done);
+    cudaFree(P->d_nnz);
     cudaFree(P->d_err);
     for (int g = 0; g < 2; ++g) {
         if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
@@ -624,6 +628,7 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     }
     k.variant = P->k1_variant;
     k.tensors = P->d_tensors;
+    k.nnz = P->d_nnz + g;
     TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, P->ck1[g], k, st));
     return TGB_OK;
 }
@@ -633,6 +638,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
     uint8_t* own = own_push(P);
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
+    k.nnz = P->d_nnz + g;
     k.variant = P->k2_variant;
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
@@ -705,6 +711,7 @@ static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
 static tgb_status launch_pipelined(tgb_plan* P, uint64_t t, cudaStream_t st) {
     uint8_t* own = own_push(P);
     K2Launch k2{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 0};
+    k2.nnz = P->d_nnz;  // pipelined: single group (K1 group 0 reset it)
     for (int p = 0; p < P->n_workers; ++p) k2.dst.base[p] = push_area(P, p);
     k2.dst.n = P->n_workers;
     k2.dst.remote = 1;
@@ -954,6 +961,19 @@ tgb_status tgb_plan_last_buffers(tgb_plan* P, uint8_t** d_push, uint8_t** d_gath
     return TGB_OK;
 }
 
+tgb_status tgb_plan_code_stats(tgb_plan* P, uint64_t* nonzero, uint64_t* total) {
+    if (!P || !nonzero || !total) return TGB_ERR_INVALID_ARGUMENT;
+    TGB_CUDA(cudaStreamSynchronize(P->last));
+    unsigned long long h[2] = {0, 0};
+    TGB_CUDA(cudaMemcpy(h, P->d_nnz, sizeof(h), cudaMemcpyDeviceToHost));
+    *nonzero = h[0] + (P->grouped ? h[1] : 0ull);
+    uint64_t tot = 0;
+    for (const LayerDev& L : P->h_layers)
+        if (!(L.flags & kLayerPassthrough)) tot += L.n;
+    *total = tot;
+    return TGB_OK;
+}
+
 tgb_status tgb_check(tgb_plan* P, tgb_error* out) {
     if (!P || !out) return TGB_ERR_INVALID_ARGUMENT;
     TGB_CUDA(cudaStreamSynchronize(P->last));
@@ -1131,6 +1151,34 @@ tgb_status tgb_layer_average_raw(int32_t n_workers, const float* const* d_vals, 
     for (int w = 0; w < n_workers; ++w)
         if (!d_vals[w]) return TGB_ERR_INVALID_ARGUMENT;
     TGB_CUDA(launch_average_raw(n_workers, d_vals, n, d_out, static_cast<cudaStream_t>(stream)));
+    return TGB_OK;
+}
+
+tgb_status tgb_layer_histogram(const float* d_v, uint64_t n, uint32_t bins, uint64_t* d_counts,
+                               double* d_edges, void* stream) {
+    if (bins < 1 || !d_counts || !d_edges || (n > 0 && !d_v)) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    TGB_CUDA(cudaMemsetAsync(d_counts, 0, bins * sizeof(uint64_t), st));
+    if (n == 0) {  // codec.hpp:495-498: bins of {0.0, 0}
+        TGB_CUDA(cudaMemsetAsync(d_edges, 0, bins * sizeof(double), st));
+        return TGB_OK;
+    }
+    // the reference's min/max chain starts at v[0]; a NaN there poisons lo/hi
+    float first = 0.0f;
+    TGB_CUDA(cudaMemcpyAsync(&first, d_v, sizeof(float), cudaMemcpyDeviceToHost, st));
+    TGB_CUDA(cudaStreamSynchronize(st));
+    uint32_t* mm = nullptr;
+    TGB_CUDA(cudaMallocAsync(&mm, 2 * sizeof(uint32_t), st));
+    const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+    cudaError_t e = cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = launch_histogram(d_v, n, bins, mm, 0, nullptr, nullptr, st, 0);
+    if (e == cudaSuccess)
+        e = launch_histogram(d_v, n, bins, mm, std::isnan(first) ? 1 : 0,
+                             reinterpret_cast<unsigned long long*>(d_counts), d_edges, st, 1);
+    cudaFreeAsync(mm, st);
+    TGB_CUDA(e);
+    TGB_CUDA(cudaStreamSynchronize(st));  // init[] lives on this stack frame
     return TGB_OK;
 }
 

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
+    if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;  // this group's K2 counts next
     if (L.flags & kLayerPassthrough) return;
     const float* g = L.g + ch.begin;
     const uint32_t count = ch.count;
@@ -110,7 +111,30 @@ struct K2Args {
     PeerPush dst;        // plan: code destinations (n == 0: just `push`)
     int32_t shard_n = 0;        // sharded exchange: ranks; chunk b belongs to rank r with
     uint32_t shard_bounds[kMaxPeers + 1];  // shard_bounds[r] <= b < shard_bounds[r + 1]
+    unsigned long long* nnz = nullptr;     // telemetry: += nonzero codes (cluster.hpp:336-346)
 };
+
+// nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
+__device__ __forceinline__ void count_nonzero(const uint8_t* stage, uint32_t nbytes,
+                                              unsigned long long* nnz) {
+    __shared__ uint32_t cta_nnz;
+    if (threadIdx.x == 0) cta_nnz = 0;
+    __syncthreads();
+    uint32_t c = 0;
+    const uint32_t nw = nbytes >> 2;
+    for (uint32_t i = threadIdx.x; i < nw; i += kThreads) {
+        const uint32_t w = reinterpret_cast<const uint32_t*>(stage)[i];
+        c += __popc((w | (w >> 1)) & 0x55555555u);
+    }
+    for (uint32_t i = (nw << 2) + threadIdx.x; i < nbytes; i += kThreads) {
+        const uint32_t w = stage[i];
+        c += __popc((w | (w >> 1)) & 0x55u);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31u) == 0 && c) atomicAdd(&cta_nnz, c);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_nnz) atomicAdd(nnz, static_cast<unsigned long long>(cta_nnz));
+}
 
 __device__ __forceinline__ int shard_owner(const K2Args& a, uint32_t b) {
     int r = 0;
@@ -389,6 +413,7 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
         raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(L.tensor),
                     block_rng_base(L) + ch.begin);
     __syncthreads();
+    if (a.nnz) count_nonzero(stage, nbytes, a.nnz);
     return nbytes;
 }
 
@@ -1364,7 +1389,7 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
                             const K1Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
-            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors};
+            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors, p.nnz};
     const TableSource src{chunks};
     switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
@@ -1398,6 +1423,7 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
                             const K2Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0, p.dst};
+    a.nnz = p.nnz;
     a.shard_n = p.shard_n;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
@@ -1523,6 +1549,7 @@ static PipeArgs pipe_args(const K2Launch& k2, const K3Launch& k3, const PipeLaun
     PipeArgs a{};
     a.k2 = K2Args{k2.push, k2.slots, k2.bounds, k2.err, k2.t, 0, 0, 0.0f, 0, k2.dst};
     a.k2.shard_n = 0;
+    a.k2.nnz = k2.nnz;
     a.k3 = K3Args{k3.src, k3.stride, nullptr, nullptr, 0.0f, k3.n_workers, k3.sharing, k3.inv_n,
                   k3.err};
     a.flags = p.flags;
@@ -1574,6 +1601,90 @@ cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const
         case 8: return pipe_variant<8>(p.variant, n_items, src, a, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// ============================================================== telemetry
+// histogram (codec.hpp:491-517): equal-width bins over [min, max] in double,
+// b = size_t((double(x) - lo) / width) clamped to bins - 1 (width 0: bin 0).
+// Pass 1: float min/max (NaN ignored; the host handles a NaN first element,
+// which the reference's std::min/max chain would propagate). Pass 2: bins.
+__device__ __forceinline__ uint32_t float_order(float x) {  // monotone float -> uint32
+    const uint32_t u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float order_float(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__global__ void __launch_bounds__(kThreads) k_minmax(const float* v, uint64_t n, uint32_t* mm) {
+    float lo = INFINITY, hi = -INFINITY;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * kThreads) {
+        const float x = v[i];
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        atomicMin(mm, float_order(lo));
+        atomicMax(mm + 1, float_order(hi));
+    }
+}
+
+constexpr uint32_t kHistSmem = 4096;  // bins counted in shared memory per CTA
+
+__global__ void __launch_bounds__(kThreads) k_histogram(const float* v, uint64_t n, uint32_t bins,
+                                                        const uint32_t* mm, int nan_first,
+                                                        unsigned long long* counts,
+                                                        double* edges) {
+    __shared__ unsigned int sh[kHistSmem];
+    const bool use_sh = bins <= kHistSmem;
+    const double lo = nan_first ? static_cast<double>(NAN) : static_cast<double>(order_float(mm[0]));
+    const double hi = nan_first ? static_cast<double>(NAN) : static_cast<double>(order_float(mm[1]));
+    const double width = __ddiv_rn(__dsub_rn(hi, lo), static_cast<double>(bins));
+    if (use_sh)
+        for (uint32_t b = threadIdx.x; b < bins; b += kThreads) sh[b] = 0;
+    if (blockIdx.x == 0)
+        for (uint32_t b = threadIdx.x; b < bins; b += kThreads)
+            edges[b] = __dadd_rn(lo, __dmul_rn(width, static_cast<double>(b)));
+    __syncthreads();
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * kThreads) {
+        uint64_t b = 0;
+        if (width > 0.0) {
+            const double q = __ddiv_rn(__dsub_rn(static_cast<double>(v[i]), lo), width);
+            // size_t conversion; NaN (and out-of-range) lands in the last bin like x86-64
+            b = (q == q && q < 18446744073709551616.0) ? static_cast<uint64_t>(q) : ~0ull;
+        }
+        if (b >= bins) b = bins - 1;
+        if (use_sh)
+            atomicAdd(&sh[b], 1u);
+        else
+            atomicAdd(counts + b, 1ull);
+    }
+    if (use_sh) {
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < bins; b += kThreads)
+            if (sh[b]) atomicAdd(counts + b, static_cast<unsigned long long>(sh[b]));
+    }
+}
+
+cudaError_t launch_histogram(const float* v, uint64_t n, uint32_t bins, uint32_t* mm,
+                             int nan_first, unsigned long long* counts, double* edges,
+                             cudaStream_t st, int pass) {
+    uint64_t blocks = (n + kThreads - 1) / kThreads;
+    if (blocks > 148ull * 8) blocks = 148ull * 8;
+    if (blocks == 0) blocks = 1;
+    if (pass == 0)
+        k_minmax<<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(v, n, mm);
+    else
+        k_histogram<<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(v, n, bins, mm, nan_first,
+                                                                     counts, edges);
+    return launch_status();
 }
 
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,

@@ -29,6 +29,7 @@ struct K1Launch {
     int32_t variant = 0;  // chunk K1 kernel variant (TGB_K1V, A/B only)
     PeerPush push{};      // scaler slot destinations
     const TensorDev* tensors = nullptr;  // plan: tensor table (per-tensor finalize)
+    unsigned long long* nnz = nullptr;   // telemetry counter to reset (this group)
 };
 
 struct K2Launch {
@@ -42,6 +43,7 @@ struct K2Launch {
     float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
     uint64_t rng_base = 0; // single-layer: ternarize rng_base (codec.hpp:148)
     PeerPush dst{};        // plan: code destinations (n == 0: push only)
+    unsigned long long* nnz = nullptr;  // telemetry: nonzero-code counter of this group
     int32_t shard_n = 0;        // sharded exchange: codes go to the chunk's owner only
     uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
@@ -99,6 +101,9 @@ cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const Sh
                              cudaStream_t st);
 cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const K2Launch& k2,
                                  const K3Launch& k3, const PipeLaunch& p, cudaStream_t st);
+cudaError_t launch_histogram(const float* v, uint64_t n, uint32_t bins, uint32_t* mm,
+                             int nan_first, unsigned long long* counts, double* edges,
+                             cudaStream_t st, int pass);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,

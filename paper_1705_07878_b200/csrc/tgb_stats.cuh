@@ -26,6 +26,7 @@ struct K1Out {
     const LayerDev* layers;   // block table (slots of a tensor's blocks, Global fix-up)
     PeerPush push;            // scaler slot destinations (n == 0: slots only)
     const TensorDev* tensors; // plan only; nullptr = single-block single-layer API
+    unsigned long long* nnz = nullptr;  // telemetry counter of this group (reset by block 0)
 };
 
 __device__ __forceinline__ void put_slot(const K1Out& o, int32_t slot, float v) {

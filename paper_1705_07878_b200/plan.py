@@ -227,6 +227,17 @@ class Plan:
             check(st, "tgb_check")
         return e
 
+    def code_stats(self):
+        """(nonzero codes, ternary elements) of the last encode, counted inside K2"""
+        nz, tot = C.c_uint64(), C.c_uint64()
+        check(load().tgb_plan_code_stats(self.h, C.byref(nz), C.byref(tot)), "tgb_plan_code_stats")
+        return nz.value, tot.value
+
+    def zero_fraction(self) -> float:
+        """Worker::zero_fraction of the last encode (cluster.hpp:336-346)"""
+        nz, tot = self.code_stats()
+        return (tot - nz) / tot if tot else 0.0
+
     def block_of(self, layer: int, index: int) -> int:
         """block holding element `index` of `layer` (first block if none)."""
         first = None

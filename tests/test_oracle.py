@@ -185,3 +185,17 @@ def test_statistical_properties(restated):
         _, dec = restated.decode(codes, 4, s)
         acc += dec
     assert np.allclose(acc / T, small, atol=0.05)
+
+
+def test_restated_histogram_vs_reference(restated, reference):
+    rng = np.random.default_rng(5)
+    cases = [np.zeros(0, np.float32), np.full(7, 0.25, np.float32),
+             np.array([1, 2, 3, 4, 5], np.float32),
+             (rng.standard_normal(3001) * 1e-3).astype(np.float32),
+             np.array([-0.0, 0.0, 1e-30, -1e-30, 3.0], np.float32)]
+    for v in cases:
+        for bins in (1, 2, 7, 64):
+            e, c = restated.histogram(v, bins)
+            (st, _), re_, rc = reference.histogram(v, bins)
+            assert st == 0
+            assert e.tobytes() == re_.tobytes() and c.tobytes() == rc.tobytes(), (v.size, bins)

@@ -391,3 +391,46 @@ def test_step_host_matches_device_step(restated):
             assert o.cpu().numpy().tobytes() == h.numpy().tobytes()
     with pytest.raises(ValueError):
         w.step_host(9, [h[:1] for h in hin_v], hout_v)
+
+
+def test_histogram_vs_reference(restated):
+    from oracle.oracle import Reference
+
+    R = Reference()
+    rng = np.random.default_rng(6)
+    cases = [np.zeros(0, np.float32), np.full(70001, 0.25, np.float32),
+             (rng.standard_normal(1_000_003) * 1e-3).astype(np.float32),
+             np.array([-0.0, 0.0, 1e-30, -1e-30, 3.0], np.float32),
+             np.array([np.nan, 1.0, 2.0], np.float32), np.array([1.0, np.nan, 2.0], np.float32)]
+    for v in cases:
+        for bins in (1, 3, 64, 5000):
+            h = tg.histogram(to_dev(v) if v.size else torch.zeros(0, device=DEV), bins)
+            (st, _), e, c = R.histogram(v, bins)
+            assert st == 0
+            got_e = np.array([b.edge for b in h], np.float64)
+            got_c = np.array([b.count for b in h], np.uint64)
+            assert got_e.tobytes() == e.tobytes(), (v.size, bins)
+            assert got_c.tobytes() == c.tobytes(), (v.size, bins)
+
+
+def test_zero_fraction_telemetry():
+    # Worker::zero_fraction (cluster.hpp:336-346) of the last encode, counted inside K2
+    names = ["a", "b", "c", "p"]
+    ns = [1000003, 17, 0, 33]
+    rng = np.random.default_rng(8)
+    grads = [(rng.standard_normal(n) * 1e-2).astype(np.float32) for n in ns]
+    for cfg, pt in [(tg.CodecConfig(seed=1), None),
+                    (tg.CodecConfig(seed=1, bucketing=tg.Bucketing.FixedSize, bucket_size=999),
+                     [0, 0, 0, 1])]:
+        plan, scal, codes, _, _ = plan_encode(names, grads, cfg, 3, 0, passthrough=pt)
+        zeros = total = 0
+        for b, bi in enumerate(plan.blocks):
+            if bi.flags & 1:
+                continue
+            cb = np.frombuffer(bytes(plan.block_region(b).cpu().numpy()), np.uint8)
+            lanes = np.stack([(cb >> (2 * e)) & 3 for e in range(4)], 1).reshape(-1)[:bi.n]
+            zeros += int((lanes == 0).sum())
+            total += bi.n
+        assert plan.code_stats() == (total - zeros, total)
+        assert plan.zero_fraction() == zeros / total
+        plan.close()
