@@ -201,6 +201,33 @@ tgb_status tgb_plan_code_stats(tgb_plan* plan, uint64_t* nonzero, uint64_t* tota
 /* synchronises the plan's last stream, reads and clears the error word */
 tgb_status tgb_check(tgb_plan* plan, tgb_error* out);
 
+/* ---- optimizer (optimizer.hpp:60-125): applied identically on every worker to the
+ * averaged gradient; tgb_step_apply does it inside the step ---- */
+#define TGB_OPT_VANILLA 0  /* OptimizerRule::Vanilla */
+#define TGB_OPT_MOMENTUM 1 /* OptimizerRule::Momentum (v <- mu*v + g; w <- w - rate*v) */
+#define TGB_OPT_ADAM 2     /* OptimizerRule::Adam */
+typedef struct tgb_optimizer {
+    int32_t rule;
+    int32_t reserved;
+    double momentum, beta1, beta2, epsilon, weight_decay; /* OptimizerConfig defaults:
+                                                             0.9, 0.9, 0.999, 1e-8, 0 */
+} tgb_optimizer;
+/* OptimizerState::apply for n_layers tensors (device pointers): params -= update(grads);
+ * state1 = velocity (Momentum) / first moment (Adam), state2 = second moment (Adam),
+ * zero-initialised by the caller, NULL when the rule has none; `step` = the state's step
+ * count including this apply (Adam bias corrections 1 - beta^step). */
+tgb_status tgb_optimizer_apply(const tgb_optimizer* opt, uint64_t step, double rate,
+                               int32_t n_layers, const uint64_t* ns, float* const* d_params,
+                               const float* const* d_grads, float* const* d_state1,
+                               float* const* d_state2, void* stream);
+/* bind parameters + optimizer state (per layer, device) to a plan for tgb_step_apply */
+tgb_status tgb_plan_bind_optimizer(tgb_plan* plan, const tgb_optimizer* opt,
+                                   float* const* d_params, float* const* d_state1,
+                                   float* const* d_state2);
+/* tgb_step + OptimizerState::apply(params, averaged gradient, rate) (cluster.hpp:296-299);
+ * the plan counts optimizer steps itself */
+tgb_status tgb_step_apply(tgb_plan* plan, tgb_comm* comm, uint64_t t, double rate, void* stream);
+
 /* ---- communicator (NCCL over NVLink/NVSwitch) ---- */
 #define TGB_UNIQUE_ID_BYTES 128
 tgb_status tgb_comm_unique_id(uint8_t out[TGB_UNIQUE_ID_BYTES]);

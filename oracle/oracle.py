@@ -250,6 +250,35 @@ class Restated:
             counts[min(b, bins - 1)] += 1
         return edges, counts
 
+    @staticmethod
+    def optimizer_run(rule, w, grads, rates, momentum=0.9, beta1=0.9, beta2=0.999,
+                      epsilon=1e-8, weight_decay=0.0):
+        """optimizer.hpp:80-125 restated in numpy (one op per IEEE rounding, no FMA):
+        len(rates) applies of one OptimizerState to one tensor."""
+        f32, f64 = np.float32, np.float64
+        w = _f32(w).copy()
+        s1 = np.zeros_like(w)
+        s2 = np.zeros_like(w)
+        for step, (g, rate) in enumerate(zip(grads, rates), start=1):
+            g = _f32(g)
+            if rule == 2:  # Adam, double precision (optimizer.hpp:108-121)
+                bc1 = 1.0 - f64(beta1) ** f64(step)
+                bc2 = 1.0 - f64(beta2) ** f64(step)
+                eff = g.astype(f64) + f64(weight_decay) * w.astype(f64)
+                s1 = (f64(beta1) * s1.astype(f64) + (1.0 - f64(beta1)) * eff).astype(f32)
+                s2 = (f64(beta2) * s2.astype(f64) + (1.0 - f64(beta2)) * eff * eff).astype(f32)
+                mhat = s1.astype(f64) / bc1
+                vhat = s2.astype(f64) / bc2
+                w = (w - (f64(rate) * mhat / (np.sqrt(vhat) + f64(epsilon))).astype(f32)).astype(f32)
+                continue
+            eff = (g + f32(weight_decay) * w).astype(f32)
+            if rule == 1:  # Momentum (optimizer.hpp:98-105)
+                s1 = (f32(momentum) * s1 + eff).astype(f32)
+                w = (w - f32(rate) * s1).astype(f32)
+            else:  # Vanilla (optimizer.hpp:91-96)
+                w = (w - f32(rate) * eff).astype(f32)
+        return w
+
     def average_passthrough(self, vals):
         N = len(vals)
         vs = [_f32(v) for v in vals]
@@ -280,6 +309,9 @@ class Reference:
         L.tgref_stddev.restype = C.c_double
         L.tgref_stddev.argtypes = [_f32p, C.c_size_t]
         L.tgref_clip.argtypes = [_f32p, C.c_size_t, C.c_float, _f32p, _f32p]
+        L.tgref_optimizer_run.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double,
+                                          C.c_double, C.c_double, C.c_int, C.c_size_t, _f32p,
+                                          _f32p, C.POINTER(C.c_double)]
         L.tgref_histogram.argtypes = [_f32p, C.c_size_t, C.c_size_t, C.POINTER(C.c_double),
                                       C.POINTER(C.c_uint64)]
         L.tgref_scaler.restype = C.c_float
@@ -351,6 +383,17 @@ class Reference:
     def scaler(self, v):
         v = _f32(v)
         return self.L.tgref_scaler(_ptr(v, _f32p), v.size)
+
+    def optimizer_run(self, rule, w, grads, rates, momentum=0.9, beta1=0.9, beta2=0.999,
+                      epsilon=1e-8, weight_decay=0.0):
+        """OptimizerState(cfg).apply() len(rates) times on one tensor (optimizer.hpp:80-125)"""
+        w = _f32(w).copy()
+        g = np.ascontiguousarray(np.stack([_f32(x) for x in grads]), dtype=np.float32)
+        r = np.ascontiguousarray(rates, dtype=np.float64)
+        st = self.L.tgref_optimizer_run(int(rule), momentum, beta1, beta2, epsilon, weight_decay,
+                                        len(rates), w.size, _ptr(w, _f32p), _ptr(g, _f32p),
+                                        r.ctypes.data_as(C.POINTER(C.c_double)))
+        return (st, self.err() if st else ""), w
 
     def histogram(self, v, bins):
         """codec.hpp:491-517 -> ((status, msg), edges float64[bins], counts uint64[bins])"""

@@ -16,6 +16,7 @@
 
 #include "terngrad/cluster.hpp"
 #include "terngrad/codec.hpp"
+#include "terngrad/optimizer.hpp"
 #include "terngrad/rng.hpp"
 #include "terngrad/transport.hpp"
 #include "terngrad/wire.hpp"
@@ -296,6 +297,33 @@ int tgref_histogram(const float* v, std::size_t n, std::size_t bins, double* edg
             edges[b] = h[b].edge;
             counts[b] = h[b].count;
         }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// optimizer.hpp:80-125: `steps` applies of one OptimizerState to one tensor;
+// grads holds steps x n floats, rates steps doubles; w is updated in place
+int tgref_optimizer_run(int rule, double momentum, double beta1, double beta2, double epsilon,
+                        double weight_decay, int steps, std::size_t n, float* w,
+                        const float* grads, const double* rates) {
+    try {
+        OptimizerConfig cfg;
+        cfg.rule = static_cast<OptimizerRule>(rule);
+        cfg.momentum = momentum;
+        cfg.beta1 = beta1;
+        cfg.beta2 = beta2;
+        cfg.epsilon = epsilon;
+        cfg.weight_decay = weight_decay;
+        OptimizerState st(cfg);
+        std::vector<GradTensor> params{GradTensor("w", {n}, std::vector<float>(w, w + n))};
+        for (int k = 0; k < steps; ++k) {
+            std::vector<GradTensor> g{GradTensor("w", {n}, std::vector<float>(
+                                                                grads + k * n, grads + (k + 1) * n))};
+            st.apply(params, g, rates[k]);
+        }
+        std::memcpy(w, params[0].values.data(), n * sizeof(float));
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

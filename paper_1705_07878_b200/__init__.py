@@ -8,6 +8,8 @@ from .codec import (Bucketing, CodecConfig, CodecError, EncodedGradient, EncodeR
                     GradTensor, HistogramBin, PassthroughBlock, RngStream, ShareMode,
                     TernaryBlock, average, clip, clip_bound, decode, encode_step, fnv1a64,
                     histogram, scaler, share_scalers, ternarize)
+from .optimizer import (LrSchedule, OptimizerConfig, OptimizerRule, OptimizerState,
+                        ScheduleKind)
 from .plan import Comm, Plan, SyncWorker, aligned_flat
 from . import layersets
 
@@ -15,5 +17,6 @@ __all__ = [
     "Bucketing", "CodecConfig", "CodecError", "EncodedGradient", "EncodeResult", "GradTensor",
     "HistogramBin", "histogram", "PassthroughBlock", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
     "clip_bound", "decode", "encode_step", "fnv1a64", "scaler", "share_scalers", "ternarize",
-    "Comm", "Plan", "SyncWorker", "aligned_flat", "layersets",
+    "Comm", "Plan", "SyncWorker", "aligned_flat", "layersets", "LrSchedule",
+    "OptimizerConfig", "OptimizerRule", "OptimizerState", "ScheduleKind",
 ]

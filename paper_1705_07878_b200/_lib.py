@@ -44,6 +44,7 @@ EXPORTS = [
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_step_host", "tgb_check",
     "tgb_plan_code_stats",
     "tgb_plan_attach_peers", "tgb_plan_last_buffers",
+    "tgb_optimizer_apply", "tgb_plan_bind_optimizer", "tgb_step_apply",
     "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
     "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
     "tgb_layer_average", "tgb_layer_average_raw", "tgb_layer_histogram", "tgb_rng_bits",
@@ -75,6 +76,12 @@ class BlockInfo(C.Structure):
     _fields_ = [("layer", C.c_int32), ("slot", C.c_int32), ("offset", C.c_uint64),
                 ("n", C.c_uint64), ("region_offset", C.c_uint64), ("flags", C.c_uint32),
                 ("reserved", C.c_uint32)]
+
+
+class Optimizer(C.Structure):
+    _fields_ = [("rule", C.c_int32), ("reserved", C.c_int32), ("momentum", C.c_double),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("epsilon", C.c_double),
+                ("weight_decay", C.c_double)]
 
 
 class Error(C.Structure):
@@ -113,6 +120,12 @@ def _declare(L):
         "tgb_plan_code_stats": (S, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
         "tgb_plan_attach_peers": (S, [_vp, _vp]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
+        "tgb_optimizer_apply": (S, [C.POINTER(Optimizer), _u64, C.c_double, _i32,
+                                    C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp),
+                                    C.POINTER(_vp), C.POINTER(_vp), _vp]),
+        "tgb_plan_bind_optimizer": (S, [_vp, C.POINTER(Optimizer), C.POINTER(_vp),
+                                        C.POINTER(_vp), C.POINTER(_vp)]),
+        "tgb_step_apply": (S, [_vp, _vp, _u64, C.c_double, _vp]),
         "tgb_comm_unique_id": (S, [C.c_char_p]),
         "tgb_comm_init": (S, [C.c_char_p, _i32, _i32, C.POINTER(_vp)]),
         "tgb_comm_destroy": (None, [_vp]),

@@ -150,6 +150,11 @@ struct tgb_plan {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_d2h = nullptr;
     bool host_io = false;
+    // optimizer bound for tgb_step_apply
+    bool opt_bound = false;
+    tgb_optimizer opt{};
+    uint64_t opt_steps = 0;
+    std::vector<float*> opt_w, opt_s1, opt_s2;
 };
 
 extern "C" {
@@ -914,6 +919,87 @@ tgb_status tgb_step_host(tgb_plan* P, tgb_comm* C, uint64_t t, const float* cons
     TGB_CUDA(cudaEventRecord(P->ev_d2h, P->s_d2h));
     TGB_CUDA(cudaStreamWaitEvent(st, P->ev_d2h, 0));
     P->last = st;
+    return TGB_OK;
+}
+
+// ------------------------------------------------------------ optimizer
+static tgb_status make_opt(const tgb_optimizer* opt, uint64_t step, double rate, OptArgs* o) {
+    if (!opt || opt->rule < TGB_OPT_VANILLA || opt->rule > TGB_OPT_ADAM)
+        return TGB_ERR_INVALID_ARGUMENT;
+    o->rule = opt->rule;
+    o->wd_f = static_cast<float>(opt->weight_decay);  // optimizer.hpp:95,103
+    o->mu_f = static_cast<float>(opt->momentum);
+    o->rate_f = static_cast<float>(rate);
+    o->wd = opt->weight_decay;
+    o->b1 = opt->beta1;
+    o->omb1 = 1.0 - opt->beta1;
+    o->b2 = opt->beta2;
+    o->omb2 = 1.0 - opt->beta2;
+    o->eps = opt->epsilon;
+    o->rate = rate;
+    o->bc1 = 1.0 - std::pow(opt->beta1, static_cast<double>(step));  // optimizer.hpp:111-112
+    o->bc2 = 1.0 - std::pow(opt->beta2, static_cast<double>(step));
+    return TGB_OK;
+}
+
+tgb_status tgb_optimizer_apply(const tgb_optimizer* opt, uint64_t step, double rate,
+                               int32_t n_layers, const uint64_t* ns, float* const* d_params,
+                               const float* const* d_grads, float* const* d_state1,
+                               float* const* d_state2, void* stream) {
+    OptArgs o{};
+    TGB_TRY_INNER(make_opt(opt, step, rate, &o));
+    if (n_layers < 0 || (n_layers > 0 && (!ns || !d_params || !d_grads)))
+        return TGB_ERR_INVALID_ARGUMENT;
+    const bool need1 = opt->rule != TGB_OPT_VANILLA, need2 = opt->rule == TGB_OPT_ADAM;
+    for (int32_t l = 0; l < n_layers; ++l) {
+        if (ns[l] == 0) continue;
+        float* s1 = need1 ? (d_state1 ? d_state1[l] : nullptr) : nullptr;
+        float* s2 = need2 ? (d_state2 ? d_state2[l] : nullptr) : nullptr;
+        if (!d_params[l] || !d_grads[l] || (need1 && !s1) || (need2 && !s2))
+            return TGB_ERR_INVALID_ARGUMENT;
+        TGB_CUDA(launch_opt_apply(o, ns[l], d_params[l], d_grads[l], s1, s2,
+                                  static_cast<cudaStream_t>(stream)));
+    }
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_bind_optimizer(tgb_plan* P, const tgb_optimizer* opt, float* const* d_params,
+                                   float* const* d_state1, float* const* d_state2) {
+    OptArgs o{};
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    TGB_TRY_INNER(make_opt(opt, 1, 0.0, &o));
+    const size_t nl = P->desc.size();
+    const bool need1 = opt->rule != TGB_OPT_VANILLA, need2 = opt->rule == TGB_OPT_ADAM;
+    if (nl > 0 && (!d_params || (need1 && !d_state1) || (need2 && !d_state2)))
+        return TGB_ERR_INVALID_ARGUMENT;
+    P->opt_w.assign(nl, nullptr);
+    P->opt_s1.assign(nl, nullptr);
+    P->opt_s2.assign(nl, nullptr);
+    for (size_t l = 0; l < nl; ++l) {
+        if (P->desc[l].n == 0) continue;
+        P->opt_w[l] = d_params[l];
+        if (need1) P->opt_s1[l] = d_state1[l];
+        if (need2) P->opt_s2[l] = d_state2[l];
+        if (!P->opt_w[l] || (need1 && !P->opt_s1[l]) || (need2 && !P->opt_s2[l]))
+            return TGB_ERR_INVALID_ARGUMENT;
+    }
+    P->opt = *opt;
+    P->opt_steps = 0;
+    P->opt_bound = true;
+    return TGB_OK;
+}
+
+tgb_status tgb_step_apply(tgb_plan* P, tgb_comm* C, uint64_t t, double rate, void* stream) {
+    if (!P || !P->opt_bound) return TGB_ERR_INVALID_ARGUMENT;
+    TGB_TRY_INNER(tgb_step(P, C, t, stream));
+    OptArgs o{};
+    TGB_TRY_INNER(make_opt(&P->opt, P->opt_steps + 1, rate, &o));
+    ++P->opt_steps;
+    auto st = static_cast<cudaStream_t>(stream);
+    for (size_t l = 0; l < P->desc.size(); ++l)
+        if (P->desc[l].n)
+            TGB_CUDA(launch_opt_apply(o, P->desc[l].n, P->opt_w[l], P->bound_out[l], P->opt_s1[l],
+                                      P->opt_s2[l], st));
     return TGB_OK;
 }
 

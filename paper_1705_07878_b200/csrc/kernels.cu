@@ -1687,6 +1687,28 @@ cudaError_t launch_histogram(const float* v, uint64_t n, uint32_t bins, uint32_t
     return launch_status();
 }
 
+// standalone optimizer apply over one tensor (unfused path / per-layer API)
+__global__ void __launch_bounds__(kThreads) k_opt_apply(OptArgs o, uint64_t n, float* w,
+                                                        const float* g, float* s1, float* s2) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * kThreads) {
+        float wi = w[i], a = s1 ? s1[i] : 0.0f, b = s2 ? s2[i] : 0.0f;
+        opt_apply1(o, g[i], wi, a, b);
+        w[i] = wi;
+        if (s1) s1[i] = a;
+        if (s2) s2[i] = b;
+    }
+}
+
+cudaError_t launch_opt_apply(const OptArgs& o, uint64_t n, float* w, const float* g, float* s1,
+                             float* s2, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + kThreads - 1) / kThreads;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    k_opt_apply<<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(o, n, w, g, s1, s2);
+    return launch_status();
+}
+
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st) {
     if (n == 0) return cudaSuccess;

@@ -102,6 +102,41 @@ __device__ __forceinline__ void raise_error(ErrWord* e, uint32_t flag, int32_t l
     atomicMax(&e->inv_key, ~key);
 }
 
+// ------------------------------------------------------------- optimizer
+// OptimizerState::apply (optimizer.hpp:80-125), element k, in the reference's
+// operation order and precision (x86-64 SSE: no FMA contraction):
+//   Vanilla:  eff = g + f(wd)*w;            w -= f(rate)*eff
+//   Momentum: eff = g + f(wd)*w; v = f(mu)*v + eff; w -= f(rate)*v
+//   Adam (double): eff = g + wd*w; m = f(b1*m + (1-b1)*eff); v = f(b2*v + (1-b2)*eff*eff);
+//            w -= f(rate * (m/bc1) / (sqrt(v/bc2) + eps))
+struct OptArgs {
+    int32_t rule;  // TGB_OPT_*
+    float wd_f, mu_f, rate_f;
+    double wd, b1, omb1, b2, omb2, eps, rate, bc1, bc2;
+};
+
+__device__ __forceinline__ void opt_apply1(const OptArgs& o, float g, float& w, float& s1,
+                                           float& s2) {
+    if (o.rule == 2) {  // Adam
+        const double eff = __dadd_rn(static_cast<double>(g), __dmul_rn(o.wd, static_cast<double>(w)));
+        s1 = static_cast<float>(__dadd_rn(__dmul_rn(o.b1, static_cast<double>(s1)), __dmul_rn(o.omb1, eff)));
+        s2 = static_cast<float>(__dadd_rn(__dmul_rn(o.b2, static_cast<double>(s2)),
+                                          __dmul_rn(__dmul_rn(o.omb2, eff), eff)));
+        const double mhat = __ddiv_rn(static_cast<double>(s1), o.bc1);
+        const double vhat = __ddiv_rn(static_cast<double>(s2), o.bc2);
+        const double upd = __ddiv_rn(__dmul_rn(o.rate, mhat), __dadd_rn(__dsqrt_rn(vhat), o.eps));
+        w = __fsub_rn(w, static_cast<float>(upd));
+        return;
+    }
+    const float eff = __fadd_rn(g, __fmul_rn(o.wd_f, w));
+    if (o.rule == 1) {  // Momentum (gradient-accumulation form)
+        s1 = __fadd_rn(__fmul_rn(o.mu_f, s1), eff);
+        w = __fsub_rn(w, __fmul_rn(o.rate_f, s1));
+    } else {  // Vanilla
+        w = __fsub_rn(w, __fmul_rn(o.rate_f, eff));
+    }
+}
+
 // ---------------------------------------------------------------- Philox
 constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
 constexpr uint32_t kWeyl0 = 0x9E3779B9u, kWeyl1 = 0xBB67AE85u;

@@ -104,6 +104,8 @@ cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const
 cudaError_t launch_histogram(const float* v, uint64_t n, uint32_t bins, uint32_t* mm,
                              int nan_first, unsigned long long* counts, double* edges,
                              cudaStream_t st, int pass);
+cudaError_t launch_opt_apply(const OptArgs& o, uint64_t n, float* w, const float* g, float* s1,
+                             float* s2, cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,

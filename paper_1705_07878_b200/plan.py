@@ -341,5 +341,26 @@ class SyncWorker:
         """Worker::run sync segment with host buffers: gradients in, averaged out."""
         self.plan.step_host(t, host_grads, host_outs, self.comm, stream)
 
+    def bind_optimizer(self, cfg, params: Sequence[torch.Tensor]):
+        """Parameters (device, one per layer) updated by step_apply with
+        OptimizerState::apply semantics (optimizer.hpp:80-125); state zero-initialised."""
+        n = cfg.n_state()
+        self.params = list(params)
+        self.opt_state1 = [torch.zeros_like(p) for p in self.params] if n >= 1 else None
+        self.opt_state2 = [torch.zeros_like(p) for p in self.params] if n >= 2 else None
+        nl = len(self.ns)
+        P = C.c_void_p * max(nl, 1)
+        opt = cfg.c()
+        check(load().tgb_plan_bind_optimizer(
+            self.plan.h, C.byref(opt), P(*[p.data_ptr() for p in self.params]),
+            P(*[b.data_ptr() for b in self.opt_state1]) if self.opt_state1 else None,
+            P(*[b.data_ptr() for b in self.opt_state2]) if self.opt_state2 else None),
+            "tgb_plan_bind_optimizer")
+
+    def step_apply(self, t: int, rate: float, stream=None):
+        """Worker::run sync segment + opt.apply (cluster.hpp:283-299) in one call"""
+        check(load().tgb_step_apply(self.plan.h, self.comm.h if self.comm is not None else None,
+                                    int(t), float(rate), self.plan._st(stream)), "tgb_step_apply")
+
     def check(self):
         self.plan.raise_errors()

@@ -199,3 +199,16 @@ def test_restated_histogram_vs_reference(restated, reference):
             (st, _), re_, rc = reference.histogram(v, bins)
             assert st == 0
             assert e.tobytes() == re_.tobytes() and c.tobytes() == rc.tobytes(), (v.size, bins)
+
+
+@pytest.mark.parametrize("rule", [0, 1, 2])
+def test_restated_optimizer_vs_reference(restated, reference, rule):
+    rng = np.random.default_rng(10 + rule)
+    for wd in (0.0, 5e-4):
+        w = rng.standard_normal(4099).astype(np.float32)
+        gs = [(rng.standard_normal(4099) * 1e-2).astype(np.float32) for _ in range(5)]
+        rates = [0.1, 0.05, 0.3, 1e-3, 0.2]
+        (st, msg), ref = reference.optimizer_run(rule, w, gs, rates, weight_decay=wd)
+        assert st == 0, msg
+        got = restated.optimizer_run(rule, w, gs, rates, weight_decay=wd)
+        assert got.tobytes() == ref.tobytes(), (rule, wd)

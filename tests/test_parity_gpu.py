@@ -434,3 +434,50 @@ def test_zero_fraction_telemetry():
         assert plan.code_stats() == (total - zeros, total)
         assert plan.zero_fraction() == zeros / total
         plan.close()
+
+
+@pytest.mark.parametrize("rule", [0, 1, 2])
+def test_optimizer_apply_vs_reference(rule):
+    from oracle.oracle import Reference
+
+    R = Reference()
+    rng = np.random.default_rng(20 + rule)
+    for wd in (0.0, 5e-4):
+        ns = [70001, 5, 1]
+        ws = [rng.standard_normal(n).astype(np.float32) for n in ns]
+        gs = [[(rng.standard_normal(n) * 1e-2).astype(np.float32) for n in ns] for _ in range(4)]
+        rates = [0.1, 0.05, 0.3, 1e-3]
+        st = tg.OptimizerState(tg.OptimizerConfig(rule=tg.OptimizerRule(rule), weight_decay=wd))
+        params = [to_dev(w) for w in ws]
+        for k, r in enumerate(rates):
+            st.apply(params, [to_dev(g) for g in gs[k]], r)
+        for l in range(len(ns)):
+            (s, msg), ref = R.optimizer_run(rule, ws[l], [gs[k][l] for k in range(4)], rates,
+                                            weight_decay=wd)
+            assert s == 0, msg
+            assert params[l].cpu().numpy().tobytes() == ref.tobytes(), (rule, wd, l)
+
+
+def test_step_apply_matches_step_then_optimizer(restated):
+    names = ["conv.weight", "conv.bias", "fc.weight"]
+    ns = [1728, 64, 40003]
+    cfg = tg.CodecConfig(seed=42)
+    ocfg = tg.OptimizerConfig(rule=tg.OptimizerRule.Momentum, weight_decay=1e-4)
+    w = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    p0 = [(np.arange(n, dtype=np.float32) % 7) * 0.01 for n in ns]
+    params = [to_dev(p) for p in p0]
+    w.bind_optimizer(ocfg, params)
+    ref = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    ref_params = [to_dev(p) for p in p0]
+    ref_state = tg.OptimizerState(ocfg)
+    for t, rate in enumerate([0.1, 0.05, 0.2]):
+        grads = [restated.normal(30 + t, 0, "opt/" + nm, n, 1e-3) for nm, n in zip(names, ns)]
+        for v, r, g in zip(w.grads, ref.grads, grads):
+            v.copy_(to_dev(g))
+            r.copy_(to_dev(g))
+        w.step_apply(t, rate)
+        ref_state.apply(ref_params, ref.step(t), rate)
+        torch.cuda.synchronize()
+        w.check()
+        for a, b in zip(params, ref_params):
+            assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes()
