@@ -155,6 +155,8 @@ struct tgb_plan {
     tgb_optimizer opt{};
     uint64_t opt_steps = 0;
     std::vector<float*> opt_w, opt_s1, opt_s2;
+    OptDev* d_optd = nullptr;        // per-block optimizer table (fused decode -> optimizer)
+    const OptArgs* opt_active = nullptr;  // set during tgb_step_apply when fused
 };
 
 extern "C" {
@@ -496,6 +498,7 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaFree(P->d_ipc);
     cudaFree(P->d_done);
     cudaFree(P->d_nnz);
+    cudaFree(P->d_optd);
     cudaFree(P->d_err);
     for (int g = 0; g < 2; ++g) {
         if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
@@ -644,6 +647,10 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
     k.nnz = P->d_nnz + g;
+    if (fuse_decode && P->opt_active) {
+        k.optd = P->d_optd;
+        k.opt = *P->opt_active;
+    }
     k.variant = P->k2_variant;
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
@@ -675,6 +682,10 @@ static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t 
                1.0f / static_cast<float>(n_workers), P->d_err};
     k.variant = P->k3_variant;
     k.chunk3 = P->chunk3;
+    if (P->opt_active) {
+        k.optd = P->d_optd;
+        k.opt = *P->opt_active;
+    }
     TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + P->cb3[g], P->cc3[g], k, st));
     return TGB_OK;
 }
@@ -983,17 +994,50 @@ tgb_status tgb_plan_bind_optimizer(tgb_plan* P, const tgb_optimizer* opt, float*
         if (!P->opt_w[l] || (need1 && !P->opt_s1[l]) || (need2 && !P->opt_s2[l]))
             return TGB_ERR_INVALID_ARGUMENT;
     }
+    // per-block table for the fused decode -> optimizer kernels
+    std::vector<OptDev> od(std::max<size_t>(1, P->h_layers.size()));
+    for (size_t b = 0; b < P->h_layers.size(); ++b) {
+        const LayerDev& L = P->h_layers[b];
+        const uint64_t off = P->block_off[b];
+        OptDev& d = od[b];
+        d.w = P->opt_w[L.tensor] ? P->opt_w[L.tensor] + off : nullptr;
+        d.s1 = P->opt_s1[L.tensor] ? P->opt_s1[L.tensor] + off : nullptr;
+        d.s2 = P->opt_s2[L.tensor] ? P->opt_s2[L.tensor] + off : nullptr;
+        auto al = [](const float* q) { return !q || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+        d.vec = al(d.w) && al(d.s1) && al(d.s2) ? 1u : 0u;
+    }
+    if (!P->d_optd) TGB_CUDA(cudaMalloc(&P->d_optd, od.size() * sizeof(OptDev)));
+    TGB_CUDA(cudaMemcpy(P->d_optd, od.data(), od.size() * sizeof(OptDev), cudaMemcpyHostToDevice));
     P->opt = *opt;
     P->opt_steps = 0;
     P->opt_bound = true;
     return TGB_OK;
 }
 
+// the step schedules whose decode kernel applies the optimizer in place of
+// writing the averaged gradient: N = 1 (K2 fused decode) and the shared-scaler
+// K3 of the fused / NCCL exchanges for N in {2, 3, 4, 8}
+static bool opt_fusable(const tgb_plan* P) {
+    if (const char* m = std::getenv("TGB_OPT_FUSED"))
+        if (std::atoi(m) == 0) return false;
+    if (P->n_workers == 1) return true;
+    const int N = P->n_workers;
+    return P->p.scaler_sharing && !P->shard && !P->pipe && P->k3_variant == 1 &&
+           P->chunk3 == kChunk3 && (N <= 4 || N == 8);
+}
+
 tgb_status tgb_step_apply(tgb_plan* P, tgb_comm* C, uint64_t t, double rate, void* stream) {
     if (!P || !P->opt_bound) return TGB_ERR_INVALID_ARGUMENT;
-    TGB_TRY_INNER(tgb_step(P, C, t, stream));
     OptArgs o{};
     TGB_TRY_INNER(make_opt(&P->opt, P->opt_steps + 1, rate, &o));
+    if (opt_fusable(P)) {  // decode -> optimizer in one kernel; no averaged gradient written
+        P->opt_active = &o;
+        const tgb_status r = tgb_step(P, C, t, stream);
+        P->opt_active = nullptr;
+        if (r == TGB_OK) ++P->opt_steps;
+        return r;
+    }
+    TGB_TRY_INNER(tgb_step(P, C, t, stream));
     ++P->opt_steps;
     auto st = static_cast<cudaStream_t>(stream);
     for (size_t l = 0; l < P->desc.size(); ++l)

@@ -112,6 +112,8 @@ struct K2Args {
     int32_t shard_n = 0;        // sharded exchange: ranks; chunk b belongs to rank r with
     uint32_t shard_bounds[kMaxPeers + 1];  // shard_bounds[r] <= b < shard_bounds[r + 1]
     unsigned long long* nnz = nullptr;     // telemetry: += nonzero codes (cluster.hpp:336-346)
+    const OptDev* optd = nullptr;          // fused optimizer (kOpt kernels): per-block state
+    OptArgs opt{};
 };
 
 // nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
@@ -165,7 +167,7 @@ __device__ __forceinline__ void copy_out(const uint8_t* stage, uint8_t* dst, uin
 // the block's region of every destination; the finite check of encode_step
 // (:204) runs here since K1 never sees these blocks. N == 1 (kFuse): the
 // average is float((0.0 + x) / 1.0) (codec.hpp:271-276), i.e. x with -0 -> +0.
-template <bool kFuse>
+template <bool kFuse, bool kOpt = false>
 __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& L,
                                                const ChunkDev& ch, uint32_t b) {
     const uint32_t tid = threadIdx.x;
@@ -191,7 +193,14 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
             for (int p = 0; p < nd; ++p) reinterpret_cast<float4*>(dst(p))[i] = v;
             const bool fin = isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
             if (!fin && bad == 0xFFFFFFFFu) bad = 4 * i;
-            if (kFuse) {
+            if (kFuse && kOpt) {
+                const OptDev od = a.optd[ch.layer];
+                const uint64_t e = ch.begin + 4ull * i;
+                opt_apply4(a.opt, od.w + e, od.s1 ? od.s1 + e : nullptr, od.s2 ? od.s2 + e : nullptr,
+                           make_float4(__fadd_rn(v.x, 0.0f), __fadd_rn(v.y, 0.0f),
+                                       __fadd_rn(v.z, 0.0f), __fadd_rn(v.w, 0.0f)),
+                           od.vec != 0, 4);
+            } else if (kFuse) {
                 const float4 o = make_float4(__fadd_rn(v.x, 0.0f), __fadd_rn(v.y, 0.0f),
                                              __fadd_rn(v.z, 0.0f), __fadd_rn(v.w, 0.0f));
                 if (L.flags & kLayerVecOut) {
@@ -210,7 +219,14 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
         const float v = g[i];
         for (int p = 0; p < nd; ++p) dst(p)[i] = v;
         if (!isfinite(v) && bad == 0xFFFFFFFFu) bad = i;
-        if (kFuse) out[i] = __fadd_rn(v, 0.0f);
+        if (kFuse && kOpt) {
+            const OptDev od = a.optd[ch.layer];
+            const uint64_t e = ch.begin + i;
+            opt_apply4(a.opt, od.w + e, od.s1 ? od.s1 + e : nullptr, od.s2 ? od.s2 + e : nullptr,
+                       make_float4(__fadd_rn(v, 0.0f), 0.f, 0.f, 0.f), false, 1);
+        } else if (kFuse) {
+            out[i] = __fadd_rn(v, 0.0f);
+        }
     }
     if (bad != 0xFFFFFFFFu) {
         for (uint32_t i = bad; i < count && i < bad + 4; ++i)  // first non-finite of the float4
@@ -236,13 +252,13 @@ struct NoHook {
 // hook(i) runs once per iteration i of the vectorised main loop (the pipelined
 // kernel decodes a slice of an older item there, interleaving HBM streaming
 // with the Philox compute).
-template <bool kRolling, int U, bool kFuse, class Hook = NoHook>
+template <bool kRolling, int U, bool kFuse, class Hook = NoHook, bool kOpt = false>
 __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDev& L,
                                                   const ChunkDev& ch, uint32_t b,
                                                   uint8_t* __restrict__ stage, float4* lutv,
                                                   const Hook& hook = Hook()) {
     if (L.flags & kLayerPassthrough) {
-        k2_passthrough<kFuse>(a, L, ch, b);
+        k2_passthrough<kFuse, kOpt>(a, L, ch, b);
         return 0;
     }
     const float s = a.slots ? a.slots[L.slot] : a.s_imm;
@@ -277,9 +293,18 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
     }
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
+    OptDev od{};
+    if (kOpt) od = a.optd[ch.layer];
     auto emit = [&](uint32_t qq, uint32_t byte) {  // kFuse: decoded float4 of byte qq
         if (!kFuse) return;
         const float4 o = lutv[byte];
+        if (kOpt) {  // fused optimizer: the averaged gradient drives the update directly
+            const uint64_t e = ch.begin + 4ull * qq;
+            const uint32_t nv = count - 4 * qq < 4 ? count - 4 * qq : 4;
+            opt_apply4(a.opt, od.w + e, od.s1 ? od.s1 + e : nullptr, od.s2 ? od.s2 + e : nullptr, o,
+                       od.vec != 0, nv);
+            return;
+        }
         if (vec_out && 4 * qq + 4 <= count) {
             __stcs(reinterpret_cast<float4*>(out) + qq, o);
         } else {
@@ -433,7 +458,8 @@ __device__ __forceinline__ void k2_store_chunk(const K2Args& a, const LayerDev& 
     }
 }
 
-template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false>
+template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false,
+          bool kOpt = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     __shared__ float4 lutv[kFuse ? 256 : 1];
@@ -441,7 +467,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     ChunkDev ch;
     LayerDev L;
     src.get(b, ch, L);
-    const uint32_t nbytes = k2_code_chunk<kRolling, U, kFuse>(a, L, ch, b, stage, lutv);
+    const uint32_t nbytes =
+        k2_code_chunk<kRolling, U, kFuse, NoHook, kOpt>(a, L, ch, b, stage, lutv);
     // No fence after the peer stores: the step barrier kernel runs after this
     // grid completes in stream order, and grid completion implies its (peer)
     // stores are performed -- the guarantee event-based multi-GPU sync relies on.
@@ -501,6 +528,8 @@ struct K3Args {
     int32_t sharing;
     float inv_n;            // 1.0f / float(N), rounded on the host (codec.hpp:267)
     ErrWord* err;
+    const OptDev* optd = nullptr;  // fused decode -> optimizer (kOpt kernels)
+    OptArgs opt{};
 };
 
 struct K3Ptrs {  // per-layer API: explicit pointers (passed by value)
@@ -1039,13 +1068,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k23_pipelined(TableSourc
 // first staged in shared memory with 16-byte loads (NW independent uint4 per
 // thread in flight, 16x fewer load instructions than byte loads), then decoded
 // from shared memory with the same byte -> LUT arithmetic as k3_decode_nw.
-template <int NW>
+template <int NW, bool kOpt = false>
 __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3Args a) {
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
     if (L.flags & kLayerPassthrough) {
         const uint64_t off = L.code_off + 4ull * ch.begin;
+        if (kOpt) {  // fp64 worker-order mean (codec.hpp:269-279) drives the update
+            const OptDev od = a.optd[ch.layer];
+            for (uint32_t i = threadIdx.x; i < ch.count; i += kThreads) {
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    sum = __dadd_rn(sum, static_cast<double>(reinterpret_cast<const float*>(
+                                             a.src + a.stride * w + off)[i]));
+                const uint64_t e = ch.begin + i;
+                opt_apply4(a.opt, od.w + e, od.s1 ? od.s1 + e : nullptr,
+                           od.s2 ? od.s2 + e : nullptr,
+                           make_float4(static_cast<float>(sum / static_cast<double>(NW)), 0.f, 0.f,
+                                       0.f),
+                           false, 1);
+            }
+            return;
+        }
         k3_passthrough([&](int w) { return reinterpret_cast<const float*>(a.src + a.stride * w + off); },
                        NW, L.out + ch.begin, ch.count, (L.flags & kLayerVecOut) != 0);
         return;
@@ -1095,6 +1141,8 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
                              a.inv_n);  // codec.hpp:296
     }
     __syncthreads();
+    OptDev od{};
+    if (kOpt) od = a.optd[ch.layer];
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
     uint32_t bad = 0;
@@ -1109,7 +1157,11 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
         const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
                                      lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
         const uint32_t b4 = 4 * q;
-        if (vec_out && b4 + 4 <= count) {
+        if (kOpt) {  // fused optimizer: the averaged gradient is never written
+            const uint64_t e = ch.begin + b4;
+            opt_apply4(a.opt, od.w + e, od.s1 ? od.s1 + e : nullptr, od.s2 ? od.s2 + e : nullptr, o,
+                       od.vec != 0, count - b4 < 4 ? count - b4 : 4);
+        } else if (vec_out && b4 + 4 <= count) {
             __stcs(reinterpret_cast<float4*>(out + b4), o);
         } else {
             if (b4 + 0 < count) out[b4 + 0] = o.x;
@@ -1428,7 +1480,13 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
     if (p.fuse_decode) {
-        k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+        if (p.optd) {  // N == 1 fused decode -> optimizer
+            a.optd = p.optd;
+            a.opt = p.opt;
+            k2_ternarize<TableSource, false, 4, 3, true, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+        } else {
+            k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+        }
         return launch_status();
     }
     switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
@@ -1454,6 +1512,19 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
     const TableSource src{chunks};
+    if (p.optd) {  // fused decode -> optimizer (the caller checked the supported N)
+        a.optd = p.optd;
+        a.opt = p.opt;
+        switch (p.n_workers) {
+            case 1: k3_decode_staged<1, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 2: k3_decode_staged<2, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 3: k3_decode_staged<3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 4: k3_decode_staged<4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 8: k3_decode_staged<8, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return launch_status();
+    }
     if (p.sharing && p.variant == 1 && p.chunk3 == kChunk3) {
         switch (p.n_workers) {
             case 1: k3_decode_staged<1><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();

@@ -137,6 +137,42 @@ __device__ __forceinline__ void opt_apply1(const OptArgs& o, float g, float& w, 
     }
 }
 
+// Fused decode -> optimizer: per block, the parameter and state bases (element
+// 0 of the block); vec = all three 16-byte aligned.
+struct OptDev {
+    float* w;
+    float* s1;  // velocity / first moment (nullptr if the rule has none)
+    float* s2;  // second moment (Adam)
+    uint32_t vec;
+    uint32_t pad;
+};
+
+// apply to `nvalid` (<= 4) consecutive elements at w/s1/s2 with gradients g
+__device__ __forceinline__ void opt_apply4(const OptArgs& o, float* w, float* s1, float* s2,
+                                           float4 g, bool vec, uint32_t nvalid) {
+    if (vec && nvalid == 4) {
+        float4 wv = *reinterpret_cast<const float4*>(w);
+        float4 a = s1 ? *reinterpret_cast<const float4*>(s1) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 b = s2 ? *reinterpret_cast<const float4*>(s2) : make_float4(0.f, 0.f, 0.f, 0.f);
+        opt_apply1(o, g.x, wv.x, a.x, b.x);
+        opt_apply1(o, g.y, wv.y, a.y, b.y);
+        opt_apply1(o, g.z, wv.z, a.z, b.z);
+        opt_apply1(o, g.w, wv.w, a.w, b.w);
+        *reinterpret_cast<float4*>(w) = wv;
+        if (s1) *reinterpret_cast<float4*>(s1) = a;
+        if (s2) *reinterpret_cast<float4*>(s2) = b;
+        return;
+    }
+    const float gg[4] = {g.x, g.y, g.z, g.w};
+    for (uint32_t e = 0; e < nvalid; ++e) {
+        float wv = w[e], a = s1 ? s1[e] : 0.0f, b = s2 ? s2[e] : 0.0f;
+        opt_apply1(o, gg[e], wv, a, b);
+        w[e] = wv;
+        if (s1) s1[e] = a;
+        if (s2) s2[e] = b;
+    }
+}
+
 // ---------------------------------------------------------------- Philox
 constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
 constexpr uint32_t kWeyl0 = 0x9E3779B9u, kWeyl1 = 0xBB67AE85u;

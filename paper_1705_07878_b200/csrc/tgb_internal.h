@@ -44,6 +44,8 @@ struct K2Launch {
     uint64_t rng_base = 0; // single-layer: ternarize rng_base (codec.hpp:148)
     PeerPush dst{};        // plan: code destinations (n == 0: push only)
     unsigned long long* nnz = nullptr;  // telemetry: nonzero-code counter of this group
+    const OptDev* optd = nullptr;       // fused decode -> optimizer (per-block state table)
+    OptArgs opt{};
     int32_t shard_n = 0;        // sharded exchange: codes go to the chunk's owner only
     uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
@@ -59,6 +61,8 @@ struct K3Launch {
     float s_imm = 0.0f;    // single-layer: scaler by value when scalers == nullptr
     int32_t variant = 0;   // TGB_K3V (A/B): 1 = smem-staged 16-B code loads
     uint32_t chunk3 = 0;   // plan K3 chunk elements (the staged variant needs kChunk3)
+    const OptDev* optd = nullptr;  // fused decode -> optimizer (staged kernel, N in {1,2,3,4,8})
+    OptArgs opt{};
 };
 
 struct ShardLaunch {

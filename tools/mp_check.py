@@ -88,6 +88,39 @@ def main():
         dist.barrier()
         sw.plan.close()
 
+    # fused decode -> optimizer (tgb_step_apply) == step + OptimizerState::apply, every rank
+    for rule in (tg.OptimizerRule.Momentum, tg.OptimizerRule.Adam):
+        ocfg = tg.OptimizerConfig(rule=rule, weight_decay=1e-4)
+        cfg = tg.CodecConfig(seed=42)
+        sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws,
+                           comm=comm, device=dev, fused=FUSED)
+        ref = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws,
+                            comm=comm, device=dev, fused=FUSED)
+        p0 = [torch.full((n,), 0.5, device=dev) for n in sizes]
+        params = [x.clone() for x in p0]
+        ref_params = [x.clone() for x in p0]
+        sw.bind_optimizer(ocfg, params)
+        ref_state = tg.OptimizerState(ocfg)
+        for t, rate in enumerate([0.1, 0.05, 0.2]):
+            grads = [R.normal(200 + rank + t, 0, "opt/" + nm, k, 1e-2) for nm, k in zip(names, sizes)]
+            for v, r, g in zip(sw.grads, ref.grads, grads):
+                if g.size:
+                    v.copy_(torch.from_numpy(g).to(dev))
+                    r.copy_(torch.from_numpy(g).to(dev))
+            sw.step_apply(t, rate)
+            ref_state.apply(ref_params, ref.step(t), rate)
+        torch.cuda.synchronize()
+        sw.check()
+        same = all(torch.equal(a, b) for a, b in zip(params, ref_params))
+        h = hashlib.sha256(torch.cat([x.cpu() for x in params]).numpy().tobytes()).hexdigest()
+        hs = [None] * ws
+        dist.all_gather_object(hs, h)
+        report["checks"][f"step_apply,{rule.name}"] = {"ranks_identical": len(set(hs)) == 1,
+                                                      "matches_oracle": same}
+        dist.barrier()
+        sw.plan.close()
+        ref.plan.close()
+
     # timing: full VGG-16 step at this world size
     layers = tg.layersets.get("vgg16")
     sw = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
