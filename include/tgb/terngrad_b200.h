@@ -39,7 +39,8 @@ typedef enum tgb_status {
     TGB_ERR_CODEC = 2,            /* CodecError, codec.hpp:25-27 (detail: tgb_error) */
     TGB_ERR_CUDA = 3,
     TGB_ERR_NCCL = 4,
-    TGB_ERR_UNSUPPORTED = 5
+    TGB_ERR_UNSUPPORTED = 5,
+    TGB_ERR_PROTOCOL = 6 /* ProtocolError, wire.hpp:14-16 (text: tgb_last_error_message) */
 } tgb_status;
 
 /* device error word: flags are sticky until read by tgb_check */
@@ -227,6 +228,22 @@ tgb_status tgb_plan_bind_optimizer(tgb_plan* plan, const tgb_optimizer* opt,
 /* tgb_step + OptimizerState::apply(params, averaged gradient, rate) (cluster.hpp:296-299);
  * the plan counts optimizer steps itself */
 tgb_status tgb_step_apply(tgb_plan* plan, tgb_comm* comm, uint64_t t, double rate, void* stream);
+
+/* ---- reference wire format (interop with the reference's parameter server) ---- */
+/* text of the last TGB_ERR_PROTOCOL on this thread (the reference's ProtocolError what()) */
+const char* tgb_last_error_message(void);
+/* tensor names (needed by the wire format only; must hash to the plan's name_hash) */
+tgb_status tgb_plan_set_names(tgb_plan* plan, const char* const* names);
+/* bytes of one push frame: kHeaderSize + wire_size(encoded) (wire.hpp:28-36, codec.hpp:442-454) */
+tgb_status tgb_plan_push_frame_size(const tgb_plan* plan, uint64_t* bytes);
+/* frame(Message{Push, t, worker, serialize_encoded(last encode)}) into h_frame
+ * (codec.hpp:395-438, wire.hpp:41-53): packed on the device from the push area. Synchronous. */
+tgb_status tgb_plan_serialize_push(tgb_plan* plan, uint64_t t, uint8_t* h_frame, void* stream);
+/* decode_pull(deserialize_pull(unframe(h_frame).payload)) (wire.hpp:57-75, 147-228) into the
+ * bound outputs; radix-packed sums unpacked on the device. Returns the frame's iteration.
+ * Synchronous. */
+tgb_status tgb_plan_decode_pull(tgb_plan* plan, const uint8_t* h_frame, uint64_t len,
+                                uint64_t* iteration, void* stream);
 
 /* ---- communicator (NCCL over NVLink/NVSwitch) ---- */
 #define TGB_UNIQUE_ID_BYTES 128

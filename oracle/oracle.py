@@ -486,6 +486,16 @@ class RefCluster:
         # the C++ side copied the gradients; drop ours
         self._gs = None
 
+    def frame(self, worker: int, which: int) -> bytes:
+        """last step's push (which=0) or received pull (which=1) frame of `worker`"""
+        L = self.ref.L
+        L.tgref_cluster_frame.restype = C.c_size_t
+        L.tgref_cluster_frame.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]
+        n = L.tgref_cluster_frame(self.h, worker, which, None, 0)
+        buf = (C.c_uint8 * max(n, 1))()
+        L.tgref_cluster_frame(self.h, worker, which, buf, n)
+        return bytes(buf)[:n]
+
     def step(self, t: int) -> float:
         dt = self.ref.L.tgref_cluster_step(self.h, t)
         if dt < 0:

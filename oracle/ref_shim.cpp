@@ -212,6 +212,7 @@ struct tgref_cluster {
     std::unique_ptr<ParameterServer> server;
     std::vector<std::unique_ptr<InProcessWorkerTransport>> wts;
     std::vector<std::vector<GradTensor>> decoded;
+    std::vector<std::vector<std::uint8_t>> push_frames, pull_frames;  // per worker, last step
 };
 
 tgref_cluster* tgref_cluster_create(int N, int n_tensors, const char* const* names,
@@ -235,6 +236,8 @@ tgref_cluster* tgref_cluster_create(int N, int n_tensors, const char* const* nam
             c->wts.push_back(
                 std::make_unique<InProcessWorkerTransport>(*c->hub, static_cast<std::uint16_t>(w)));
         c->decoded.resize(N);
+        c->push_frames.resize(N);
+        c->pull_frames.resize(N);
         return c;
     } catch (const std::exception& e) {
         fail(e);
@@ -256,8 +259,10 @@ double tgref_cluster_step(tgref_cluster* c, std::uint64_t t) {
                 push.iteration = t;
                 push.worker = static_cast<std::uint16_t>(w);
                 push.payload = serialize_encoded(enc.encoded);
+                c->push_frames[w] = frame(push);
                 c->wts[w]->send(push);
                 const Message reply = c->wts[w]->recv();
+                c->pull_frames[w] = frame(reply);
                 c->decoded[w] = decode_pull(deserialize_pull(reply.payload));
             } catch (const std::exception& e) {
                 errs[w + 1] = e.what();
@@ -284,6 +289,16 @@ void tgref_cluster_output(tgref_cluster* c, int worker, float* out) {
         std::memcpy(out + pos, a.values.data(), a.values.size() * sizeof(float));
         pos += a.values.size();
     }
+}
+
+// the last step's wire frames of `worker` (which 0 = its push, 1 = the pull it
+// received), as the reference's socket transport would carry them; returns the
+// size, copies min(size, cap) bytes
+std::size_t tgref_cluster_frame(tgref_cluster* c, int worker, int which, std::uint8_t* out,
+                                std::size_t cap) {
+    const auto& f = which == 0 ? c->push_frames[worker] : c->pull_frames[worker];
+    if (out) std::memcpy(out, f.data(), std::min(cap, f.size()));
+    return f.size();
 }
 
 void tgref_cluster_destroy(tgref_cluster* c) { delete c; }

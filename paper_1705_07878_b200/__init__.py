@@ -6,8 +6,8 @@ All compute runs in libtgb.so (sm_100a); there is no CPU fallback.
 """
 from .codec import (Bucketing, CodecConfig, CodecError, EncodedGradient, EncodeResult,
                     GradTensor, HistogramBin, PassthroughBlock, RngStream, ShareMode,
-                    TernaryBlock, average, clip, clip_bound, decode, encode_step, fnv1a64,
-                    histogram, scaler, share_scalers, ternarize)
+                    ProtocolError, TernaryBlock, average, clip, clip_bound, decode, encode_step,
+                    fnv1a64, histogram, scaler, share_scalers, ternarize)
 from .optimizer import (LrSchedule, OptimizerConfig, OptimizerRule, OptimizerState,
                         ScheduleKind)
 from .plan import Comm, Plan, SyncWorker, aligned_flat
@@ -15,7 +15,7 @@ from . import layersets
 
 __all__ = [
     "Bucketing", "CodecConfig", "CodecError", "EncodedGradient", "EncodeResult", "GradTensor",
-    "HistogramBin", "histogram", "PassthroughBlock", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
+    "HistogramBin", "histogram", "PassthroughBlock", "ProtocolError", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
     "clip_bound", "decode", "encode_step", "fnv1a64", "scaler", "share_scalers", "ternarize",
     "Comm", "Plan", "SyncWorker", "aligned_flat", "layersets", "LrSchedule",
     "OptimizerConfig", "OptimizerRule", "OptimizerState", "ScheduleKind",

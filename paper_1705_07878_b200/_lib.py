@@ -20,6 +20,7 @@ TGB_ERR_CODEC = 2
 TGB_ERR_CUDA = 3
 TGB_ERR_NCCL = 4
 TGB_ERR_UNSUPPORTED = 5
+TGB_ERR_PROTOCOL = 6
 
 TGB_E_NONFINITE = 0x1
 TGB_E_SCALER_BELOW_MAX = 0x2
@@ -45,6 +46,8 @@ EXPORTS = [
     "tgb_plan_code_stats",
     "tgb_plan_attach_peers", "tgb_plan_last_buffers",
     "tgb_optimizer_apply", "tgb_plan_bind_optimizer", "tgb_step_apply",
+    "tgb_last_error_message", "tgb_plan_set_names", "tgb_plan_push_frame_size",
+    "tgb_plan_serialize_push", "tgb_plan_decode_pull",
     "tgb_comm_unique_id", "tgb_comm_init", "tgb_comm_destroy",
     "tgb_layer_scaler", "tgb_layer_clip", "tgb_layer_ternarize", "tgb_layer_decode",
     "tgb_layer_average", "tgb_layer_average_raw", "tgb_layer_histogram", "tgb_rng_bits",
@@ -126,6 +129,11 @@ def _declare(L):
         "tgb_plan_bind_optimizer": (S, [_vp, C.POINTER(Optimizer), C.POINTER(_vp),
                                         C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_step_apply": (S, [_vp, _vp, _u64, C.c_double, _vp]),
+        "tgb_last_error_message": (C.c_char_p, []),
+        "tgb_plan_set_names": (S, [_vp, C.POINTER(C.c_char_p)]),
+        "tgb_plan_push_frame_size": (S, [_vp, C.POINTER(_u64)]),
+        "tgb_plan_serialize_push": (S, [_vp, _u64, _vp, _vp]),
+        "tgb_plan_decode_pull": (S, [_vp, _vp, _u64, C.POINTER(_u64), _vp]),
         "tgb_comm_unique_id": (S, [C.c_char_p]),
         "tgb_comm_init": (S, [C.c_char_p, _i32, _i32, C.POINTER(_vp)]),
         "tgb_comm_destroy": (None, [_vp]),

@@ -19,6 +19,10 @@ from . import _lib
 from ._lib import check, load
 
 
+class ProtocolError(RuntimeError):
+    """wire.hpp:14-16"""
+
+
 class CodecError(RuntimeError):
     """terngrad::CodecError (codec.hpp:25-27)."""
 

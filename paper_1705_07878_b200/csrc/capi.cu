@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "tgb_internal.h"
@@ -15,6 +16,13 @@
 using namespace tgb;
 
 namespace {
+
+thread_local std::string g_last_error;  // tgb_last_error_message (PROTOCOL detail)
+
+inline tgb_status protocol_error(const std::string& msg) {
+    g_last_error = msg;
+    return TGB_ERR_PROTOCOL;
+}
 
 constexpr uint64_t kAlignCodes = 16;   // per-layer code region alignment (bytes)
 constexpr uint64_t kAlignPush = 256;   // push buffer / code region base alignment
@@ -155,6 +163,14 @@ struct tgb_plan {
     tgb_optimizer opt{};
     uint64_t opt_steps = 0;
     std::vector<float*> opt_w, opt_s1, opt_s2;
+    // reference wire format (tgb_plan_set_names / serialize_push / decode_pull)
+    std::vector<std::string> names;
+    uint64_t push_frame_bytes = 0;
+    uint8_t* d_frame = nullptr;     // push frame image (static headers written once)
+    WireSeg* d_wsegs = nullptr;     // dynamic parts: scalers, codes, raw values
+    uint32_t n_wsegs = 0;
+    uint8_t* d_pull = nullptr;      // pull payload staging
+    uint64_t pull_cap = 0;
     OptDev* d_optd = nullptr;        // per-block optimizer table (fused decode -> optimizer)
     const OptArgs* opt_active = nullptr;  // set during tgb_step_apply when fused
 };
@@ -171,6 +187,7 @@ const char* tgb_status_string(tgb_status s) {
         case TGB_ERR_CUDA: return "CUDA error";
         case TGB_ERR_NCCL: return "NCCL error";
         case TGB_ERR_UNSUPPORTED: return "unsupported configuration";
+        case TGB_ERR_PROTOCOL: return "protocol error";
     }
     return "unknown";
 }
@@ -499,6 +516,9 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaFree(P->d_done);
     cudaFree(P->d_nnz);
     cudaFree(P->d_optd);
+    cudaFree(P->d_frame);
+    cudaFree(P->d_wsegs);
+    cudaFree(P->d_pull);
     cudaFree(P->d_err);
     for (int g = 0; g < 2; ++g) {
         if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
@@ -1044,6 +1064,225 @@ tgb_status tgb_step_apply(tgb_plan* P, tgb_comm* C, uint64_t t, double rate, voi
         if (P->desc[l].n)
             TGB_CUDA(launch_opt_apply(o, P->desc[l].n, P->opt_w[l], P->bound_out[l], P->opt_s1[l],
                                       P->opt_s2[l], st));
+    return TGB_OK;
+}
+
+// ----------------------------------------------------------------- wire
+const char* tgb_last_error_message(void) { return g_last_error.c_str(); }
+
+namespace {
+void put_le(std::vector<uint8_t>& b, uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) b.push_back(static_cast<uint8_t>(v >> (8 * i)));
+}
+constexpr uint16_t kWireMagic = 0x5447;  // wire.hpp:18-19
+constexpr uint8_t kWireVersion = 1;
+constexpr uint64_t kHeaderSize = 18;  // wire.hpp:28-30
+}  // namespace
+
+// Static parts of the push frame (codec.hpp:395-438, wire.hpp:41-53) and the
+// segment list of its per-step parts; names are needed by the wire format only.
+tgb_status tgb_plan_set_names(tgb_plan* P, const char* const* names) {
+    if (!P || (!names && !P->desc.empty())) return TGB_ERR_INVALID_ARGUMENT;
+    const size_t nl = P->desc.size();
+    P->names.assign(nl, std::string());
+    for (size_t l = 0; l < nl; ++l) {
+        if (!names[l]) return TGB_ERR_INVALID_ARGUMENT;
+        P->names[l] = names[l];
+        if (P->names[l].size() > 0xFFFF) return protocol_error("tensor name too long");
+        if (tgb_fnv1a64(names[l], P->names[l].size()) != P->desc[l].name_hash)
+            return TGB_ERR_INVALID_ARGUMENT;  // names must be the plan's tensors
+    }
+    if (P->h_layers.size() > 0xFFFF) return TGB_ERR_UNSUPPORTED;  // u16 block count
+    std::vector<uint8_t> f;
+    put_le(f, kWireMagic, 2);
+    f.push_back(kWireVersion);
+    f.push_back(1);      // MsgType::Push
+    put_le(f, 0, 8);     // iteration: patched per frame
+    put_le(f, P->worker, 2);
+    put_le(f, 0, 4);     // payload length: patched below
+    put_le(f, P->h_layers.size(), 2);
+    std::vector<WireSeg> segs;
+    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
+        for (uint64_t o = 0; o < bytes; o += 65536)
+            segs.push_back({src + o, dst + o, std::min<uint64_t>(65536, bytes - o)});
+    };
+    for (const LayerDev& L : P->h_layers) {
+        const bool pass = (L.flags & kLayerPassthrough) != 0;
+        const std::string& nm = P->names[L.tensor];
+        f.push_back(pass ? 2 : 1);  // kBlockPassthrough / kBlockTernary
+        put_le(f, nm.size(), 2);
+        f.insert(f.end(), nm.begin(), nm.end());
+        put_le(f, L.n, 4);
+        if (pass) {
+            add(L.code_off, f.size(), 4ull * L.n);
+            f.resize(f.size() + 4ull * L.n);
+        } else {
+            add(4ull * static_cast<uint64_t>(L.slot), f.size(), 4);  // scaler slot
+            f.resize(f.size() + 4);
+            const uint64_t nb = (L.n + 3ull) / 4;
+            add(L.code_off, f.size(), nb);
+            f.resize(f.size() + nb);
+        }
+    }
+    const uint64_t payload = f.size() - kHeaderSize;
+    if (payload > 0xFFFFFFFFull) return TGB_ERR_UNSUPPORTED;
+    for (int i = 0; i < 4; ++i) f[14 + i] = static_cast<uint8_t>(payload >> (8 * i));
+    cudaFree(P->d_frame);
+    cudaFree(P->d_wsegs);
+    P->d_frame = nullptr;
+    P->d_wsegs = nullptr;
+    TGB_CUDA(cudaMalloc(&P->d_frame, f.size()));
+    TGB_CUDA(cudaMemcpy(P->d_frame, f.data(), f.size(), cudaMemcpyHostToDevice));
+    TGB_CUDA(cudaMalloc(&P->d_wsegs, std::max<size_t>(1, segs.size()) * sizeof(WireSeg)));
+    if (!segs.empty())
+        TGB_CUDA(cudaMemcpy(P->d_wsegs, segs.data(), segs.size() * sizeof(WireSeg),
+                            cudaMemcpyHostToDevice));
+    P->n_wsegs = static_cast<uint32_t>(segs.size());
+    P->push_frame_bytes = f.size();
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_push_frame_size(const tgb_plan* P, uint64_t* bytes) {
+    if (!P || !bytes || !P->d_frame) return TGB_ERR_INVALID_ARGUMENT;
+    *bytes = P->push_frame_bytes;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_serialize_push(tgb_plan* P, uint64_t t, uint8_t* h_frame, void* stream) {
+    if (!P || !h_frame || !P->d_frame) return TGB_ERR_INVALID_ARGUMENT;
+    auto st = static_cast<cudaStream_t>(stream);
+    TGB_CUDA(launch_wire_gather(own_push(P), P->d_wsegs, P->n_wsegs, P->d_frame, st));
+    TGB_CUDA(cudaMemcpyAsync(h_frame, P->d_frame, P->push_frame_bytes, cudaMemcpyDeviceToHost, st));
+    TGB_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < 8; ++i) h_frame[4 + i] = static_cast<uint8_t>(t >> (8 * i));
+    return TGB_OK;
+}
+
+namespace {
+struct Rd {  // detail::Reader (codec.hpp:334-381) over the host frame
+    const uint8_t* p;
+    uint64_t n, pos;
+    bool ok = true;
+    uint64_t le(int bytes) {
+        if (pos + bytes > n) {
+            ok = false;
+            return 0;
+        }
+        uint64_t v = 0;
+        for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | p[pos + i];
+        pos += bytes;
+        return v;
+    }
+};
+uint64_t radix_digits_per_word(uint64_t base) {  // wire.hpp:104-112
+    uint64_t m = 0, acc = 1;
+    while (acc <= UINT64_MAX / base) {
+        acc *= base;
+        ++m;
+    }
+    return m;
+}
+}  // namespace
+
+// unframe + deserialize_pull + decode_pull (wire.hpp:57-75, 147-228) into the
+// plan's bound outputs: headers parsed and validated on the host with the
+// reference's ProtocolError texts, sums unpacked and decoded on the device.
+tgb_status tgb_plan_decode_pull(tgb_plan* P, const uint8_t* h_frame, uint64_t len,
+                                uint64_t* iteration, void* stream) {
+    if (!P || !h_frame || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
+    if (P->names.size() != P->desc.size()) return TGB_ERR_INVALID_ARGUMENT;  // set_names first
+    Rd r{h_frame, len, 0};
+    if (len < kHeaderSize) return protocol_error("deserialize: truncated at byte 0");
+    if (r.le(2) != kWireMagic) return protocol_error("bad magic");
+    if (r.le(1) != kWireVersion) return protocol_error("bad version");
+    const uint64_t type = r.le(1);
+    if (type < 1 || type > 4) return protocol_error("bad message type " + std::to_string(type));
+    if (type != 2) return protocol_error("worker: expected Pull");  // cluster.hpp:291-292
+    const uint64_t it = r.le(8);
+    r.le(2);  // worker
+    const uint64_t plen = r.le(4);
+    if (len - kHeaderSize != plen)
+        return protocol_error("payload length mismatch: header says " + std::to_string(plen) +
+                              ", got " + std::to_string(len - kHeaderSize));
+    const uint64_t count = r.le(2);
+    if (count != P->h_layers.size())
+        return protocol_error("worker: averaged gradient tensor count mismatch");
+    std::vector<PullSeg> segs;
+    uint32_t threads = 0;
+    for (uint64_t b = 0; b < count; ++b) {
+        const LayerDev& L = P->h_layers[b];
+        const uint64_t tag = r.le(1);
+        const uint64_t nlen = r.le(2);
+        if (!r.ok || r.pos + nlen > len)
+            return protocol_error("deserialize: truncated at byte " + std::to_string(r.pos));
+        const std::string name(reinterpret_cast<const char*>(h_frame + r.pos), nlen);
+        r.pos += nlen;
+        const uint64_t n = r.le(4);
+        if (!r.ok) return protocol_error("deserialize: truncated at byte " + std::to_string(r.pos));
+        if (name != P->names[L.tensor] || n != L.n)
+            return protocol_error("worker: averaged gradient mismatch at " + P->names[L.tensor]);
+        PullSeg sg{};
+        sg.out = P->bound_out[L.tensor] + P->block_off[b];
+        sg.n = static_cast<uint32_t>(n);
+        sg.first_thread = threads;
+        if (tag == 3) {  // kPullSharedSum
+            const uint64_t workers = r.le(2);
+            if (workers == 0) return protocol_error("pull: zero worker count");
+            const uint32_t sbits = static_cast<uint32_t>(r.le(4));
+            float s;
+            std::memcpy(&s, &sbits, 4);
+            const uint64_t base = 2 * workers + 1;
+            const uint64_t m = radix_digits_per_word(base);
+            const uint64_t words = r.le(4);
+            if (!r.ok) return protocol_error("deserialize: truncated at byte " + std::to_string(r.pos));
+            if (words != (n + m - 1) / m) return protocol_error("pull: bad word count");
+            if (r.pos + 8 * words > len)
+                return protocol_error("deserialize: truncated at byte " + std::to_string(r.pos));
+            sg.kind = 3;
+            sg.src_off = r.pos;
+            sg.words = static_cast<uint32_t>(words);
+            sg.base = static_cast<uint32_t>(base);
+            sg.m = static_cast<uint32_t>(m);
+            sg.s = s;
+            sg.inv_n = 1.0f / static_cast<float>(workers);  // wire.hpp:216
+            r.pos += 8 * words;
+            threads += sg.words;
+        } else if (tag == 4) {  // kPullFloatAvg
+            if (r.pos + 4 * n > len)
+                return protocol_error("deserialize: truncated at byte " + std::to_string(r.pos));
+            sg.kind = 4;
+            sg.src_off = r.pos;
+            r.pos += 4 * n;
+            threads += sg.n;
+        } else {
+            return protocol_error("pull: unknown block tag " + std::to_string(tag));
+        }
+        if (n) segs.push_back(sg);
+    }
+    if (r.pos != len) return protocol_error("pull: trailing bytes");
+    auto st = static_cast<cudaStream_t>(stream);
+    const uint64_t plen_bytes = len;  // the whole frame (offsets are frame-relative)
+    if (P->pull_cap < plen_bytes + segs.size() * sizeof(PullSeg) + 256) {
+        cudaFree(P->d_pull);
+        P->pull_cap = plen_bytes + segs.size() * sizeof(PullSeg) + 256;
+        TGB_CUDA(cudaMalloc(&P->d_pull, P->pull_cap));
+    }
+    uint8_t* d_payload = P->d_pull;
+    const uint64_t seg_off = round_up(plen_bytes, 16);
+    PullSeg* d_segs = reinterpret_cast<PullSeg*>(P->d_pull + seg_off);
+    int* d_bad = reinterpret_cast<int*>(P->d_pull + seg_off + segs.size() * sizeof(PullSeg));
+    TGB_CUDA(cudaMemcpyAsync(d_payload, h_frame, len, cudaMemcpyHostToDevice, st));
+    if (!segs.empty())
+        TGB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(PullSeg),
+                                 cudaMemcpyHostToDevice, st));
+    TGB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    TGB_CUDA(launch_pull_decode(d_payload, d_segs, static_cast<uint32_t>(segs.size()), threads,
+                                d_bad, st));
+    int bad = 0;
+    TGB_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TGB_CUDA(cudaStreamSynchronize(st));
+    if (bad) return protocol_error("pull: nonzero radix remainder");
+    if (iteration) *iteration = it;
     return TGB_OK;
 }
 

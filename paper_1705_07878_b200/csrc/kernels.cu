@@ -1780,6 +1780,91 @@ cudaError_t launch_opt_apply(const OptArgs& o, uint64_t n, float* w, const float
     return launch_status();
 }
 
+// ================================================================== wire
+// Reference wire format (codec.hpp:383-438 push payload, wire.hpp:41-228 frame
+// and pull payload) on the device. Little-endian byte streams at arbitrary
+// offsets, so everything below is byte-granular.
+
+// push: copy the dynamic parts (scalers, codes, raw values) of this step's push
+// area into the frame image whose static headers were written once.
+
+// segments are pre-split into pieces of <= 64 KB; one CTA per piece (grid-stride)
+__global__ void __launch_bounds__(kThreads) k_wire_gather(const uint8_t* push, const WireSeg* segs,
+                                                          uint32_t n_segs, uint8_t* frame) {
+    for (uint32_t p = blockIdx.x; p < n_segs; p += gridDim.x) {
+        const WireSeg sg = segs[p];
+        for (uint64_t i = threadIdx.x; i < sg.bytes; i += kThreads)
+            frame[sg.dst_off + i] = push[sg.src_off + i];
+    }
+}
+
+cudaError_t launch_wire_gather(const uint8_t* push, const WireSeg* d_segs, uint32_t n_segs,
+                               uint8_t* frame, cudaStream_t st) {
+    if (n_segs == 0) return cudaSuccess;
+    const uint32_t g = n_segs < 148u * 8 ? n_segs : 148u * 8;
+    k_wire_gather<<<g, kThreads, 0, st>>>(push, d_segs, n_segs, frame);
+    return launch_status();
+}
+
+// pull: one thread per radix word of a SharedSumBlock (wire.hpp:147-185):
+// digits little-endian within the word, sum = digit - N,
+// out = (s * float(sum)) * (1.0f / N) (decode_pull, wire.hpp:216-220).
+
+__device__ __forceinline__ uint64_t load_u64_le(const uint8_t* p) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) k_pull_decode(const uint8_t* payload, const PullSeg* segs,
+                                                          uint32_t n_segs, uint32_t total_threads,
+                                                          int* bad) {
+    const uint32_t gt = blockIdx.x * kThreads + threadIdx.x;
+    if (gt >= total_threads) return;
+    uint32_t lo = 0, hi = n_segs;  // segment with first_thread <= gt (binary search)
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (segs[mid].first_thread <= gt) lo = mid; else hi = mid;
+    }
+    const PullSeg sg = segs[lo];
+    const uint32_t i = gt - sg.first_thread;
+    if (sg.kind == 4) {  // FloatAvgBlock: values verbatim
+        if (i >= sg.n) return;
+        const uint8_t* p = payload + sg.src_off + 4ull * i;
+        sg.out[i] = __uint_as_float(static_cast<uint32_t>(p[0]) | (static_cast<uint32_t>(p[1]) << 8) |
+                                    (static_cast<uint32_t>(p[2]) << 16) |
+                                    (static_cast<uint32_t>(p[3]) << 24));
+        return;
+    }
+    if (i >= sg.words) return;
+    uint64_t word = load_u64_le(payload + sg.src_off + 8ull * i);
+    const uint64_t base = sg.base;
+    const uint64_t magic = ~0ull / base;  // q = umulhi(word, magic) underestimates by <= 2
+    const uint32_t k0 = i * sg.m, k1 = min(k0 + sg.m, sg.n);
+    const int N = static_cast<int>((sg.base - 1) / 2);
+    for (uint32_t k = k0; k < k1; ++k) {
+        uint64_t q = __umul64hi(word, magic);
+        uint64_t r = word - q * base;
+        while (r >= base) {
+            ++q;
+            r -= base;
+        }
+        word = q;
+        const int sum = static_cast<int>(r) - N;
+        sg.out[k] = __fmul_rn(__fmul_rn(sg.s, static_cast<float>(sum)), sg.inv_n);
+    }
+    if (word != 0) atomicExch(bad, 1);  // "pull: nonzero radix remainder" (wire.hpp:180)
+}
+
+cudaError_t launch_pull_decode(const uint8_t* payload, const PullSeg* d_segs, uint32_t n_segs,
+                               uint32_t total_threads, int* bad, cudaStream_t st) {
+    if (total_threads == 0) return cudaSuccess;
+    k_pull_decode<<<(total_threads + kThreads - 1) / kThreads, kThreads, 0, st>>>(
+        payload, d_segs, n_segs, total_threads, bad);
+    return launch_status();
+}
+
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st) {
     if (n == 0) return cudaSuccess;

@@ -173,6 +173,22 @@ __device__ __forceinline__ void opt_apply4(const OptArgs& o, float* w, float* s1
     }
 }
 
+// wire format segments (kernels.cu, capi.cu)
+struct WireSeg {
+    uint64_t src_off;  // in the push area
+    uint64_t dst_off;  // in the frame
+    uint64_t bytes;
+};
+struct PullSeg {
+    uint64_t src_off;  // first word (SharedSum) or first float (FloatAvg) in the payload
+    float* out;
+    uint32_t n, words;
+    uint32_t base, m;  // 2N+1, digits per word
+    float s, inv_n;
+    uint32_t kind;     // 3 SharedSum, 4 FloatAvg (wire.hpp:99-100)
+    uint32_t first_thread;  // prefix over segments of threads used
+};
+
 // ---------------------------------------------------------------- Philox
 constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
 constexpr uint32_t kWeyl0 = 0x9E3779B9u, kWeyl1 = 0xBB67AE85u;

@@ -110,6 +110,10 @@ cudaError_t launch_histogram(const float* v, uint64_t n, uint32_t bins, uint32_t
                              cudaStream_t st, int pass);
 cudaError_t launch_opt_apply(const OptArgs& o, uint64_t n, float* w, const float* g, float* s1,
                              float* s2, cudaStream_t st);
+cudaError_t launch_wire_gather(const uint8_t* push, const WireSeg* d_segs, uint32_t n_segs,
+                               uint8_t* frame, cudaStream_t st);
+cudaError_t launch_pull_decode(const uint8_t* payload, const PullSeg* d_segs, uint32_t n_segs,
+                               uint32_t total_threads, int* bad, cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,

@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import check, load
-from .codec import CodecConfig, CodecError, ShareMode, fnv1a64, _dev
+from .codec import CodecConfig, CodecError, ProtocolError, ShareMode, fnv1a64, _dev
 
 
 class _CudaBuf:
@@ -111,6 +111,9 @@ class Plan:
             check(L.tgb_plan_create(descs, nl, C.byref(params), self.worker, self.n_workers,
                                     C.byref(h)), "tgb_plan_create")
         self.h = h
+        # the reference wire format carries tensor names (serialize_push / decode_pull)
+        cn = (C.c_char_p * max(nl, 1))(*[x.encode() for x in self.names])
+        check(L.tgb_plan_set_names(h, cn), "tgb_plan_set_names")
         info = _lib.PlanInfo()
         check(L.tgb_plan_get_info(h, C.byref(info)), "tgb_plan_get_info")
         self.info = info
@@ -226,6 +229,27 @@ class Plan:
         if st not in (_lib.TGB_OK, _lib.TGB_ERR_CODEC):
             check(st, "tgb_check")
         return e
+
+    # -- reference wire format ----------------------------------------------
+    def serialize_push(self, t: int, stream=None) -> bytes:
+        """frame(Message{Push, t, worker, serialize_encoded(last encode)}) (wire.hpp:41-53)"""
+        n = C.c_uint64()
+        check(load().tgb_plan_push_frame_size(self.h, C.byref(n)), "tgb_plan_push_frame_size")
+        buf = (C.c_uint8 * n.value)()
+        check(load().tgb_plan_serialize_push(self.h, int(t), buf, self._st(stream)),
+              "tgb_plan_serialize_push")
+        return bytes(buf)
+
+    def decode_pull(self, frame: bytes, stream=None) -> int:
+        """decode_pull(deserialize_pull(unframe(frame).payload)) into the bound outputs;
+        returns the frame's iteration (wire.hpp:57-75, 147-228)"""
+        buf = (C.c_uint8 * len(frame)).from_buffer_copy(frame) if frame else (C.c_uint8 * 1)()
+        it = C.c_uint64()
+        st = load().tgb_plan_decode_pull(self.h, buf, len(frame), C.byref(it), self._st(stream))
+        if st == _lib.TGB_ERR_PROTOCOL:
+            raise ProtocolError(load().tgb_last_error_message().decode())
+        check(st, "tgb_plan_decode_pull")
+        return it.value
 
     def code_stats(self):
         """(nonzero codes, ternary elements) of the last encode, counted inside K2"""

@@ -485,3 +485,57 @@ def test_step_apply_matches_step_then_optimizer(restated, monkeypatch, rule, fus
         w.check()
         for a, b in zip(params, ref_params):
             assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("bucketing,k,pt,sharing", [(0, 0, [0, 0, 0, 0], True),
+                                                    (2, 5, [0, 1, 0, 0], True),
+                                                    (0, 0, [0, 0, 0, 1], False)])
+def test_wire_push_and_pull_match_reference(bucketing, k, pt, sharing):
+    # interop with the reference's parameter server: our push frame is byte-identical to
+    # frame(Message{Push, ...serialize_encoded}) and decoding its radix-packed pull frame
+    # gives the workers' decode_pull bit-for-bit (cluster.hpp:283-297)
+    from oracle.oracle import Config, Reference, RefCluster
+
+    R = Reference()
+    names = ["conv.weight", "conv.bias", "empty", "fc.weight"]
+    ns = [1728, 64, 0, 40003]
+    N, t = 3, 11
+    rng = np.random.default_rng(3)
+    gw = [[(rng.standard_normal(n) * 1e-2).astype(np.float32) for n in ns] for _ in range(N)]
+    ocfg = Config(seed=42, bucketing=bucketing, bucket_size=k, scaler_sharing=sharing)
+    c = RefCluster(R, names, gw, ocfg, passthrough=pt)
+    c.step(t)
+    want = c.output(0)
+    cfg = tg.CodecConfig(seed=42, bucketing=tg.Bucketing(bucketing), bucket_size=k,
+                         scaler_sharing=sharing,
+                         passthrough={n for n, p in zip(names, pt) if p})
+    for w in range(N):
+        plan, _, _, _, (gflat, gviews, oflat, oviews) = plan_encode(names, gw[w], cfg, t, w,
+                                                                     n_workers=N)
+        assert plan.serialize_push(t) == c.frame(w, 0), w
+        assert plan.decode_pull(c.frame(w, 1)) == t
+        got = torch.cat([v for v in oviews]).cpu().numpy()
+        assert got.tobytes() == want.tobytes(), w
+        plan.close()
+
+
+def test_wire_protocol_errors():
+    from oracle.oracle import Config, Reference, RefCluster
+
+    R = Reference()
+    gw = [[np.full(9, 0.5, np.float32)] for _ in range(2)]
+    c = RefCluster(R, ["w"], gw, Config(seed=1))
+    c.step(0)
+    pull = c.frame(0, 1)
+    plan, _, _, _, _ = plan_encode(["w"], gw[0], tg.CodecConfig(seed=1), 0, 0, n_workers=2)
+    with pytest.raises(tg.ProtocolError, match="bad magic"):
+        plan.decode_pull(b"\x00" + pull[1:])
+    with pytest.raises(tg.ProtocolError, match="worker: expected Pull"):
+        plan.decode_pull(c.frame(0, 0))
+    with pytest.raises(tg.ProtocolError, match="payload length mismatch"):
+        plan.decode_pull(pull[:-1])
+    bad = bytearray(pull)
+    bad[-1] = 0xFF  # last radix word's top byte: digits beyond n are not zero
+    with pytest.raises(tg.ProtocolError, match="nonzero radix remainder"):
+        plan.decode_pull(bytes(bad))
+    plan.close()
