@@ -35,6 +35,11 @@ struct CodecError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// wire.hpp:14-16
+struct ProtocolError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
 namespace detail {
 
 inline void cuda_check(cudaError_t e, const char* what) {
@@ -559,6 +564,9 @@ public:
             op[l] = outs_.p + offs_[l];
         }
         detail::check(tgb_plan_bind(plan_, gp.data(), op.data()), "tgb_plan_bind");
+        std::vector<const char*> cn(nl);
+        for (int l = 0; l < nl; ++l) cn[l] = names_[l].c_str();
+        detail::check(tgb_plan_set_names(plan_, cn.data()), "tgb_plan_set_names");
         if (world_size > 1 && fused)
             detail::check(tgb_plan_attach_peers(plan_, comm_ ? comm_->get() : nullptr),
                           "tgb_plan_attach_peers");
@@ -585,6 +593,23 @@ public:
         detail::check(tgb_step_host(plan_, comm_ ? comm_->get() : nullptr, t, h_grads.data(),
                                     h_out.data(), stream),
                       "tgb_step_host");
+    }
+    // interop with the reference's parameter server (wire.hpp): the push frame of the
+    // last encode, byte-identical to frame(Message{Push, t, rank, serialize_encoded(...)})
+    std::vector<uint8_t> serialize_push(uint64_t t, cudaStream_t stream = nullptr) {
+        uint64_t n = 0;
+        detail::check(tgb_plan_push_frame_size(plan_, &n), "tgb_plan_push_frame_size");
+        std::vector<uint8_t> f(n);
+        detail::check(tgb_plan_serialize_push(plan_, t, f.data(), stream), "tgb_plan_serialize_push");
+        return f;
+    }
+    // decode_pull(deserialize_pull(unframe(frame).payload)) into output(l); returns the iteration
+    uint64_t decode_pull(std::span<const uint8_t> frame, cudaStream_t stream = nullptr) {
+        uint64_t it = 0;
+        const tgb_status st = tgb_plan_decode_pull(plan_, frame.data(), frame.size(), &it, stream);
+        if (st == TGB_ERR_PROTOCOL) throw ProtocolError(tgb_last_error_message());
+        detail::check(st, "tgb_plan_decode_pull");
+        return it;
     }
     // Worker::zero_fraction of the last step's encode (cluster.hpp:336-346)
     double zero_fraction() {
