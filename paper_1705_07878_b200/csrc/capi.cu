@@ -132,6 +132,7 @@ struct tgb_plan {
     uint32_t chunk12 = kChunk12;
     bool bound = false;
     int32_t k2_variant = 0;  // TGB_K2V
+    int32_t k2_direct = 0;   // TGB_K2DIRECT: K2 stores codes from registers during the loop
     int32_t k1_variant = 0;  // TGB_K1V
     int32_t k3_variant = 1;  // TGB_K3V: 1 smem-staged (default, tools/k3_probe.py), 0 byte loads
     // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
@@ -258,6 +259,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     if (!P) return TGB_ERR_INVALID_ARGUMENT;
     P->p = *params;
     if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
+    if (const char* m = std::getenv("TGB_K2DIRECT")) P->k2_direct = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K3V")) P->k3_variant = std::atoi(m);
     P->worker = worker;
@@ -666,6 +668,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
     uint8_t* own = own_push(P);
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
+    k.direct = P->k2_direct;
     k.nnz = P->d_nnz + g;
     if (fuse_decode && P->opt_active) {
         k.optd = P->d_optd;

@@ -117,18 +117,19 @@ struct K2Args {
 };
 
 // nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
-__device__ __forceinline__ void count_nonzero(const uint8_t* stage, uint32_t nbytes,
-                                              unsigned long long* nnz) {
+// stage[from, nbytes) plus `extra` already counted by this thread (from % 4 == 0)
+__device__ __forceinline__ void count_nonzero(const uint8_t* stage, uint32_t from, uint32_t nbytes,
+                                              unsigned long long* nnz, uint32_t extra) {
     __shared__ uint32_t cta_nnz;
     if (threadIdx.x == 0) cta_nnz = 0;
     __syncthreads();
-    uint32_t c = 0;
+    uint32_t c = extra;
     const uint32_t nw = nbytes >> 2;
-    for (uint32_t i = threadIdx.x; i < nw; i += kThreads) {
+    for (uint32_t i = (from >> 2) + threadIdx.x; i < nw; i += kThreads) {
         const uint32_t w = reinterpret_cast<const uint32_t*>(stage)[i];
         c += __popc((w | (w >> 1)) & 0x55555555u);
     }
-    for (uint32_t i = (nw << 2) + threadIdx.x; i < nbytes; i += kThreads) {
+    for (uint32_t i = max(nw << 2, from) + threadIdx.x; i < nbytes; i += kThreads) {
         const uint32_t w = stage[i];
         c += __popc((w | (w >> 1)) & 0x55u);
     }
@@ -252,15 +253,34 @@ struct NoHook {
 // hook(i) runs once per iteration i of the vectorised main loop (the pipelined
 // kernel decodes a slice of an older item there, interleaving HBM streaming
 // with the Philox compute).
-template <bool kRolling, int U, bool kFuse, class Hook = NoHook, bool kOpt = false>
+// destinations of chunk b's codes: [p0, p1) of a.dst (a.push when a.dst.n == 0)
+__device__ __forceinline__ void k2_dst_range(const K2Args& a, uint32_t b, int& p0, int& p1) {
+    p0 = 0;
+    p1 = a.dst.n == 0 ? 1 : a.dst.n;
+    if (a.dst.n && a.shard_n) p1 = (p0 = shard_owner(a, b)) + 1;  // sharded: owner only
+}
+__device__ __forceinline__ uint8_t* k2_dst(const K2Args& a, int p) {
+    return a.dst.n == 0 ? a.push : a.dst.base[p];
+}
+
+// kDirect (U == 4): in the vectorised loop each thread owns 4 consecutive code
+// bytes and stores them as one u32 straight to every destination while the CTA
+// keeps computing (NVLink stores overlap the Philox work); `streamed` returns
+// how many leading code bytes were written that way, the rest is staged.
+template <bool kRolling, int U, bool kFuse, class Hook = NoHook, bool kOpt = false,
+          bool kDirect = false>
 __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDev& L,
                                                   const ChunkDev& ch, uint32_t b,
                                                   uint8_t* __restrict__ stage, float4* lutv,
-                                                  const Hook& hook = Hook()) {
+                                                  const Hook& hook = Hook(),
+                                                  uint32_t* streamed_out = nullptr) {
+    static_assert(!kDirect || U == 4, "direct stores pack 4 code bytes per thread");
+    if (streamed_out) *streamed_out = 0;
     if (L.flags & kLayerPassthrough) {
         k2_passthrough<kFuse, kOpt>(a, L, ch, b);
         return 0;
     }
+    uint32_t streamed = 0, nz_direct = 0;
     const float s = a.slots ? a.slots[L.slot] : a.s_imm;
     const float bound = a.bounds ? a.bounds[ch.layer] : INFINITY;
     const uint32_t count = ch.count;
@@ -373,16 +393,21 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
         const float4* g4 = reinterpret_cast<const float4*>(g);
         // uniform trip count (every thread runs every block: __syncthreads below)
         uint32_t it = 0;
+        int dp0 = 0, dp1 = 0;
+        if (kDirect) k2_dst_range(a, b, dp0, dp1);
+        const uint64_t doff = L.code_off + (ch.begin >> 2);
         for (uint32_t blk = 0; blk + U * kThreads <= nfull;
              blk += U * kThreads, q += U * kThreads, ++it) {
             hook(it);
             float4 v[U];
             uint32_t ctr[U];
             uint4 r[U];
+            // byte of lane u: direct = blk + 4 tid + u (thread-contiguous), else q + u kThreads
+            const uint32_t qd = blk + 4 * tid;
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + q + u * kThreads);
+            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + (kDirect ? qd + u : q + u * kThreads));
 #pragma unroll
-            for (int u = 0; u < U; ++u) ctr[u] = qbase + q + u * kThreads;
+            for (int u = 0; u < U; ++u) ctr[u] = qbase + (kDirect ? qd + u : q + u * kThreads);
             ph(ctr, r);
             uint32_t byte[U];
             float amb = -1.0f;
@@ -392,10 +417,17 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
 #pragma unroll
                 for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
             }
+            if (kDirect) {
+                const uint32_t word = byte[0] | (byte[1] << 8) | (byte[2] << 16) | (byte[3] << 24);
+                for (int p = dp0; p < dp1; ++p)
+                    *reinterpret_cast<uint32_t*>(k2_dst(a, p) + doff + qd) = word;
+                if (a.nnz) nz_direct += __popc((word | (word >> 1)) & 0x55555555u);
+                streamed = blk + U * kThreads;
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                stage[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
-                emit(q + u * kThreads, byte[u]);
+                if (!kDirect) stage[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
+                emit(kDirect ? qd + u : q + u * kThreads, byte[u]);
                 if (a.check)
                     bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
                                                    fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
@@ -438,7 +470,8 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
         raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(L.tensor),
                     block_rng_base(L) + ch.begin);
     __syncthreads();
-    if (a.nnz) count_nonzero(stage, nbytes, a.nnz);
+    if (a.nnz) count_nonzero(stage, streamed, nbytes, a.nnz, nz_direct);
+    if (streamed_out) *streamed_out = streamed;
     return nbytes;
 }
 
@@ -447,19 +480,17 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
 // NVLink (the allgather is fused into K2 and overlaps its Philox-bound compute).
 __device__ __forceinline__ void k2_store_chunk(const K2Args& a, const LayerDev& L,
                                                const ChunkDev& ch, uint32_t b,
-                                               const uint8_t* stage, uint32_t nbytes) {
-    const uint64_t off = L.code_off + (ch.begin >> 2);
-    if (a.dst.n == 0) {
-        copy_out(stage, a.push + off, nbytes);
-    } else {
-        int p0 = 0, p1 = a.dst.n;  // sharded exchange: the chunk's owner only
-        if (a.shard_n) p1 = (p0 = shard_owner(a, b)) + 1;
-        for (int p = p0; p < p1; ++p) copy_out(stage, a.dst.base[p] + off, nbytes);
-    }
+                                               const uint8_t* stage, uint32_t nbytes,
+                                               uint32_t streamed = 0) {
+    if (streamed >= nbytes) return;
+    const uint64_t off = L.code_off + (ch.begin >> 2) + streamed;
+    int p0, p1;
+    k2_dst_range(a, b, p0, p1);
+    for (int p = p0; p < p1; ++p) copy_out(stage + streamed, k2_dst(a, p) + off, nbytes - streamed);
 }
 
 template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false,
-          bool kOpt = false>
+          bool kOpt = false, bool kDirect = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     __shared__ float4 lutv[kFuse ? 256 : 1];
@@ -467,12 +498,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     ChunkDev ch;
     LayerDev L;
     src.get(b, ch, L);
-    const uint32_t nbytes =
-        k2_code_chunk<kRolling, U, kFuse, NoHook, kOpt>(a, L, ch, b, stage, lutv);
+    uint32_t streamed = 0;
+    const uint32_t nbytes = k2_code_chunk<kRolling, U, kFuse, NoHook, kOpt, kDirect>(
+        a, L, ch, b, stage, lutv, NoHook(), &streamed);
     // No fence after the peer stores: the step barrier kernel runs after this
     // grid completes in stream order, and grid completion implies its (peer)
     // stores are performed -- the guarantee event-based multi-GPU sync relies on.
-    if (nbytes) k2_store_chunk(a, L, ch, b, stage, nbytes);
+    if (nbytes) k2_store_chunk(a, L, ch, b, stage, nbytes, streamed);
 }
 
 // ====================================================================== K3
@@ -1483,10 +1515,19 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
         if (p.optd) {  // N == 1 fused decode -> optimizer
             a.optd = p.optd;
             a.opt = p.opt;
-            k2_ternarize<TableSource, false, 4, 3, true, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+            if (p.direct)
+                k2_ternarize<TableSource, false, 4, 3, true, true, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+            else
+                k2_ternarize<TableSource, false, 4, 3, true, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+        } else if (p.direct) {
+            k2_ternarize<TableSource, false, 4, 3, true, false, true><<<n_chunks, kThreads, 0, st>>>(src, a);
         } else {
             k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
         }
+        return launch_status();
+    }
+    if (p.direct) {
+        k2_ternarize<TableSource, false, 4, 3, false, false, true><<<n_chunks, kThreads, 0, st>>>(src, a);
         return launch_status();
     }
     switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy

@@ -49,6 +49,7 @@ struct K2Launch {
     int32_t shard_n = 0;        // sharded exchange: codes go to the chunk's owner only
     uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
+    int32_t direct = 0;         // thread-contiguous code bytes stored straight from registers
 };
 
 struct K3Launch {
