@@ -612,6 +612,9 @@ public:
         return it;
     }
     // Worker::zero_fraction of the last step's encode (cluster.hpp:336-346)
+    void enable_code_stats(bool on = true) {
+        detail::check(tgb_plan_enable_code_stats(plan_, on ? 1 : 0), "tgb_plan_enable_code_stats");
+    }
     double zero_fraction() {
         uint64_t nz = 0, tot = 0;
         detail::check(tgb_plan_code_stats(plan_, &nz, &tot), "tgb_plan_code_stats");

@@ -195,9 +195,12 @@ tgb_status tgb_step(tgb_plan* plan, tgb_comm* comm, uint64_t t, void* stream);
  * next call's H2D overlaps this call's D2H (separate copy streams). */
 tgb_status tgb_step_host(tgb_plan* plan, tgb_comm* comm, uint64_t t, const float* const* h_grads,
                          float* const* h_out, void* stream);
+/* telemetry: count nonzero codes inside K2 from now on (off by default: it costs one
+ * shared-memory pass per chunk) */
+tgb_status tgb_plan_enable_code_stats(tgb_plan* plan, int32_t on);
 /* telemetry of the last encode: nonzero ternary codes and ternary elements over all
  * blocks; zero fraction = 1 - nonzero/total (Worker::zero_fraction, cluster.hpp:336-346).
- * Counted inside K2 (no extra pass). Synchronises the plan's last stream. */
+ * Requires tgb_plan_enable_code_stats before that step. Synchronises the plan's last stream. */
 tgb_status tgb_plan_code_stats(tgb_plan* plan, uint64_t* nonzero, uint64_t* total);
 /* synchronises the plan's last stream, reads and clears the error word */
 tgb_status tgb_check(tgb_plan* plan, tgb_error* out);
@@ -234,6 +237,8 @@ tgb_status tgb_step_apply(tgb_plan* plan, tgb_comm* comm, uint64_t t, double rat
 const char* tgb_last_error_message(void);
 /* tensor names (needed by the wire format only; must hash to the plan's name_hash) */
 tgb_status tgb_plan_set_names(tgb_plan* plan, const char* const* names);
+/* (push frames need <= 65535 blocks and a payload < 4 GB; otherwise the push functions
+ * return TGB_ERR_UNSUPPORTED) */
 /* bytes of one push frame: kHeaderSize + wire_size(encoded) (wire.hpp:28-36, codec.hpp:442-454) */
 tgb_status tgb_plan_push_frame_size(const tgb_plan* plan, uint64_t* bytes);
 /* frame(Message{Push, t, worker, serialize_encoded(last encode)}) into h_frame

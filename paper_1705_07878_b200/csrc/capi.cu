@@ -146,6 +146,7 @@ struct tgb_plan {
     uint64_t pflags_off = 0;
     uint32_t* d_done = nullptr;             // pipelined: local per-item done flags
     unsigned long long* d_nnz = nullptr;    // telemetry: nonzero codes per group (last step)
+    bool code_stats = false;                // counted only when enabled (one pass over smem)
     unsigned long long* d_pprof = nullptr;  // TGB_PIPE_PROF (A/B instrumentation)
     uint64_t pipe_steps = 0;
     int32_t nib = 1;  // 4-bit sums (N <= 7), else 8-bit
@@ -658,7 +659,7 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     }
     k.variant = P->k1_variant;
     k.tensors = P->d_tensors;
-    k.nnz = P->d_nnz + g;
+    k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
     TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, P->ck1[g], k, st));
     return TGB_OK;
 }
@@ -669,7 +670,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
     k.direct = P->k2_direct;
-    k.nnz = P->d_nnz + g;
+    k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
     if (fuse_decode && P->opt_active) {
         k.optd = P->d_optd;
         k.opt = *P->opt_active;
@@ -750,7 +751,7 @@ static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
 static tgb_status launch_pipelined(tgb_plan* P, uint64_t t, cudaStream_t st) {
     uint8_t* own = own_push(P);
     K2Launch k2{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 0};
-    k2.nnz = P->d_nnz;  // pipelined: single group (K1 group 0 reset it)
+    k2.nnz = P->code_stats ? P->d_nnz : nullptr;  // pipelined: single group (K1 group 0 reset it)
     for (int p = 0; p < P->n_workers; ++p) k2.dst.base[p] = push_area(P, p);
     k2.dst.n = P->n_workers;
     k2.dst.remote = 1;
@@ -1095,7 +1096,12 @@ tgb_status tgb_plan_set_names(tgb_plan* P, const char* const* names) {
         if (tgb_fnv1a64(names[l], P->names[l].size()) != P->desc[l].name_hash)
             return TGB_ERR_INVALID_ARGUMENT;  // names must be the plan's tensors
     }
-    if (P->h_layers.size() > 0xFFFF) return TGB_ERR_UNSUPPORTED;  // u16 block count
+    cudaFree(P->d_frame);
+    cudaFree(P->d_wsegs);
+    P->d_frame = nullptr;
+    P->d_wsegs = nullptr;
+    P->push_frame_bytes = 0;
+    if (P->h_layers.size() > 0xFFFF) return TGB_OK;  // u16 block count: no wire frames for this plan
     std::vector<uint8_t> f;
     put_le(f, kWireMagic, 2);
     f.push_back(kWireVersion);
@@ -1128,12 +1134,8 @@ tgb_status tgb_plan_set_names(tgb_plan* P, const char* const* names) {
         }
     }
     const uint64_t payload = f.size() - kHeaderSize;
-    if (payload > 0xFFFFFFFFull) return TGB_ERR_UNSUPPORTED;
+    if (payload > 0xFFFFFFFFull) return TGB_OK;  // u32 payload length: no wire frames
     for (int i = 0; i < 4; ++i) f[14 + i] = static_cast<uint8_t>(payload >> (8 * i));
-    cudaFree(P->d_frame);
-    cudaFree(P->d_wsegs);
-    P->d_frame = nullptr;
-    P->d_wsegs = nullptr;
     TGB_CUDA(cudaMalloc(&P->d_frame, f.size()));
     TGB_CUDA(cudaMemcpy(P->d_frame, f.data(), f.size(), cudaMemcpyHostToDevice));
     TGB_CUDA(cudaMalloc(&P->d_wsegs, std::max<size_t>(1, segs.size()) * sizeof(WireSeg)));
@@ -1146,13 +1148,15 @@ tgb_status tgb_plan_set_names(tgb_plan* P, const char* const* names) {
 }
 
 tgb_status tgb_plan_push_frame_size(const tgb_plan* P, uint64_t* bytes) {
-    if (!P || !bytes || !P->d_frame) return TGB_ERR_INVALID_ARGUMENT;
+    if (!P || !bytes || P->names.size() != P->desc.size()) return TGB_ERR_INVALID_ARGUMENT;
+    if (!P->d_frame) return TGB_ERR_UNSUPPORTED;  // > 65535 blocks or > 4 GB payload
     *bytes = P->push_frame_bytes;
     return TGB_OK;
 }
 
 tgb_status tgb_plan_serialize_push(tgb_plan* P, uint64_t t, uint8_t* h_frame, void* stream) {
-    if (!P || !h_frame || !P->d_frame) return TGB_ERR_INVALID_ARGUMENT;
+    if (!P || !h_frame || P->names.size() != P->desc.size()) return TGB_ERR_INVALID_ARGUMENT;
+    if (!P->d_frame) return TGB_ERR_UNSUPPORTED;
     auto st = static_cast<cudaStream_t>(stream);
     TGB_CUDA(launch_wire_gather(own_push(P), P->d_wsegs, P->n_wsegs, P->d_frame, st));
     TGB_CUDA(cudaMemcpyAsync(h_frame, P->d_frame, P->push_frame_bytes, cudaMemcpyDeviceToHost, st));
@@ -1333,8 +1337,15 @@ tgb_status tgb_plan_last_buffers(tgb_plan* P, uint8_t** d_push, uint8_t** d_gath
     return TGB_OK;
 }
 
+tgb_status tgb_plan_enable_code_stats(tgb_plan* P, int32_t on) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    P->code_stats = on != 0;
+    return TGB_OK;
+}
+
 tgb_status tgb_plan_code_stats(tgb_plan* P, uint64_t* nonzero, uint64_t* total) {
     if (!P || !nonzero || !total) return TGB_ERR_INVALID_ARGUMENT;
+    if (!P->code_stats) return TGB_ERR_INVALID_ARGUMENT;  // enable before the step
     TGB_CUDA(cudaStreamSynchronize(P->last));
     unsigned long long h[2] = {0, 0};
     TGB_CUDA(cudaMemcpy(h, P->d_nnz, sizeof(h), cudaMemcpyDeviceToHost));

@@ -251,6 +251,10 @@ class Plan:
         check(st, "tgb_plan_decode_pull")
         return it.value
 
+    def enable_code_stats(self, on: bool = True):
+        """count nonzero codes inside K2 from the next step on (telemetry, off by default)"""
+        check(load().tgb_plan_enable_code_stats(self.h, int(on)), "tgb_plan_enable_code_stats")
+
     def code_stats(self):
         """(nonzero codes, ternary elements) of the last encode, counted inside K2"""
         nz, tot = C.c_uint64(), C.c_uint64()

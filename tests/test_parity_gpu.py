@@ -423,6 +423,8 @@ def test_zero_fraction_telemetry():
                     (tg.CodecConfig(seed=1, bucketing=tg.Bucketing.FixedSize, bucket_size=999),
                      [0, 0, 0, 1])]:
         plan, scal, codes, _, _ = plan_encode(names, grads, cfg, 3, 0, passthrough=pt)
+        plan.enable_code_stats()
+        plan.encode(3)
         zeros = total = 0
         for b, bi in enumerate(plan.blocks):
             if bi.flags & 1:
