@@ -134,7 +134,7 @@ struct tgb_plan {
     int32_t k2_variant = 0;  // TGB_K2V
     int32_t k2_direct = 0;   // TGB_K2DIRECT: K2 stores codes from registers during the loop
     int32_t k1_variant = 0;  // TGB_K1V
-    int32_t k3_variant = 1;  // TGB_K3V: 1 smem-staged (default, tools/k3_probe.py), 0 byte loads
+    int32_t k3_variant = 2;  // TGB_K3V: 2 staged + SWAR sums + register LUT (default), 1 staged + tables, 0 byte loads
     // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
     // K2 chunks [cs[r], cs[r+1]) and reduces them to packed sums for every rank.
     // d_ipc = [gather parity 0][gather parity 1][sums parity 0][sums parity 1][flags]
@@ -1046,7 +1046,7 @@ static bool opt_fusable(const tgb_plan* P) {
         if (std::atoi(m) == 0) return false;
     if (P->n_workers == 1) return true;
     const int N = P->n_workers;
-    return P->p.scaler_sharing && !P->shard && !P->pipe && P->k3_variant == 1 &&
+    return P->p.scaler_sharing && !P->shard && !P->pipe && P->k3_variant >= 1 &&
            P->chunk3 == kChunk3 && (N <= 4 || N == 8);
 }
 

@@ -97,6 +97,90 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
                          q_all, mx);
 }
 
+// K1 with a TMA bulk-copy ring (TGB_K1V=10, A/B): a producer warp streams the
+// chunk through S shared-memory stages of 16 KB with cp.async.bulk (no
+// registers held by loads in flight), 8 consumer warps accumulate from shared
+// memory. Same arithmetic and finalize as k1_stats (ConsumerBar: the producer
+// warp never joins a CTA barrier after the ring is set up).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr uint32_t kK1TileBytes = 16384;  // 1024 float4 per stage
+
+template <int S>
+__global__ void __launch_bounds__(kThreads + 32) k1_stats_tma(TableSource src, K1Out o) {
+    extern __shared__ __align__(128) uint8_t k1_dsm[];
+    float4* buf = reinterpret_cast<float4*>(k1_dsm);
+    uint64_t* full = reinterpret_cast<uint64_t*>(k1_dsm + S * kK1TileBytes);
+    uint64_t* empty = full + S;
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;
+    if (L.flags & kLayerPassthrough) return;
+    const float* g = L.g + ch.begin;
+    const uint32_t count = ch.count;
+    const bool vec = (L.flags & kLayerVecIn) != 0;
+    const uint32_t n4 = vec ? (count >> 2) : 0u;
+    constexpr uint32_t kTile4 = kK1TileBytes / 16;
+    const uint32_t n_tiles = (n4 + kTile4 - 1) / kTile4;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_addr(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kThreads / 32) {  // producer
+        if (lane == 0) {
+            const float4* g4 = reinterpret_cast<const float4*>(g);
+            for (uint32_t t = 0; t < n_tiles; ++t) {
+                const uint32_t s = t % S, ph = (t / S) & 1u;
+                if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
+                const uint32_t bytes = 16u * min(kTile4, n4 - t * kTile4);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                 smem_addr(&full[s])),
+                             "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(buf + s * kTile4)),
+                    "l"(g4 + static_cast<uint64_t>(t) * kTile4), "r"(bytes), "r"(smem_addr(&full[s]))
+                    : "memory");
+            }
+        }
+        return;
+    }
+    const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
+    double Sx = 0.0, Qx = 0.0;
+    float mx = 0.0f;
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+        const uint32_t s = t % S, ph = (t / S) & 1u;
+        mbar_wait(&full[s], ph);
+        const uint32_t m = min(kTile4, n4 - t * kTile4);
+        const float4* tb = buf + s * kTile4;
+#pragma unroll 4
+        for (uint32_t j = tid; j < m; j += kThreads) acc4(tb[j], x0, Sx, Qx, mx);
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s]))
+                         : "memory");
+    }
+    for (uint32_t i = (n4 << 2) + tid; i < count; i += kThreads) acc1(__ldcs(g + i), x0, Sx, Qx, mx);
+    k1_emit_and_finalize<ConsumerBar>(o, L, ch.layer, blockIdx.x, L.first_chunk, L.n_chunks, count,
+                                      x0, Sx, Qx, mx);
+}
+
 // ====================================================================== K2
 struct K2Args {
     uint8_t* push;       // codes at push + L.code_off (table) / codes base (single)
@@ -1100,7 +1184,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k23_pipelined(TableSourc
 // first staged in shared memory with 16-byte loads (NW independent uint4 per
 // thread in flight, 16x fewer load instructions than byte loads), then decoded
 // from shared memory with the same byte -> LUT arithmetic as k3_decode_nw.
-template <int NW, bool kOpt = false>
+// SWAR form of lane_biased(b): the four 2-bit codes spread to bytes, then
+// 1 + (c & 1) - (c >> 1) per byte (8 integer ops instead of a table load)
+__device__ __forceinline__ uint32_t lane_biased_swar(uint32_t b) {
+    uint32_t x = (b | (b << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return 0x01010101u + (x & 0x01010101u) - ((x >> 1) & 0x01010101u);
+}
+
+// exact float(k) for |k| < 2^22 without I2F: 1.5*2^23 + k, then subtract
+__device__ __forceinline__ float small_int_float(int k) {
+    return __fsub_rn(__int_as_float(0x4B400000 + k), 12582912.0f);
+}
+
+template <int NW, bool kOpt = false, bool kArith = false>
 __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3Args a) {
     ChunkDev ch;
     LayerDev L;
@@ -1178,16 +1275,26 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
     uint32_t bad = 0;
+    float s_max = 0.0f;  // kArith: the LUT entries computed in registers
+    if (kArith) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
+    }
+    auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
+        return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
+    };
     for (uint32_t q = tid; q < nbytes; q += kThreads) {
         uint32_t acc = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             const uint32_t b = codes[w][q];
-            acc += tab[b];
+            acc += kArith ? lane_biased_swar(b) : tab[b];
             bad |= b & (b >> 1);
         }
-        const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
-                                     lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
+        const float4 o = kArith ? make_float4(val(acc & 0xffu), val((acc >> 8) & 0xffu),
+                                              val((acc >> 16) & 0xffu), val(acc >> 24))
+                                : make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
+                                              lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
         const uint32_t b4 = 4 * q;
         if (kOpt) {  // fused optimizer: the averaged gradient is never written
             const uint64_t e = ch.begin + b4;
@@ -1484,6 +1591,18 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
         case 6: k1_stats<TableSource, 6, 1, 6><<<n_chunks, kThreads, 0, st>>>(src, o); break;
         case 8: k1_stats<TableSource, 4, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
         case 9: k1_stats<TableSource, 8, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
+        case 10: {
+            constexpr int S = 3;
+            const size_t smem = S * kK1TileBytes + 2 * S * sizeof(uint64_t);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k1_stats_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+                attr = true;
+            }
+            k1_stats_tma<S><<<n_chunks, kThreads + 32, smem, st>>>(src, o);
+            break;
+        }
         default:  // 8 float4 in flight per thread, <= 64 registers: 4 CTAs/SM (tools/k1_probe.py)
             k1_stats<TableSource, 8, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
     }
@@ -1565,6 +1684,16 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
             default: return cudaErrorInvalidValue;
         }
         return launch_status();
+    }
+    if (p.sharing && p.variant == 2 && p.chunk3 == kChunk3) {  // SWAR sums, register LUT
+        switch (p.n_workers) {
+            case 1: k3_decode_staged<1, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 2: k3_decode_staged<2, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 3: k3_decode_staged<3, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 4: k3_decode_staged<4, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            case 8: k3_decode_staged<8, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
+            default: break;
+        }
     }
     if (p.sharing && p.variant == 1 && p.chunk3 == kChunk3) {
         switch (p.n_workers) {
