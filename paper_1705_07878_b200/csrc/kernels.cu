@@ -605,6 +605,19 @@ __device__ __forceinline__ uint32_t lane_biased(uint32_t b) {
     return r;
 }
 
+// SWAR form of lane_biased(b): the four 2-bit codes spread to bytes, then
+// 1 + (c & 1) - (c >> 1) per byte (8 integer ops instead of a table load)
+__device__ __forceinline__ uint32_t lane_biased_swar(uint32_t b) {
+    uint32_t x = (b | (b << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return 0x01010101u + (x & 0x01010101u) - ((x >> 1) & 0x01010101u);
+}
+
+// exact float(k) for |k| < 2^22 without I2F: 1.5*2^23 + k, then subtract
+__device__ __forceinline__ float small_int_float(int k) {
+    return __fsub_rn(__int_as_float(0x4B400000 + k), 12582912.0f);
+}
+
 // Passthrough block average (codec.hpp:269-279): per element an fp64 sum
 // from 0.0 over workers in order, divided by N in fp64, rounded to fp32.
 // base(w) = worker w's raw values of this chunk.
@@ -1184,19 +1197,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k23_pipelined(TableSourc
 // first staged in shared memory with 16-byte loads (NW independent uint4 per
 // thread in flight, 16x fewer load instructions than byte loads), then decoded
 // from shared memory with the same byte -> LUT arithmetic as k3_decode_nw.
-// SWAR form of lane_biased(b): the four 2-bit codes spread to bytes, then
-// 1 + (c & 1) - (c >> 1) per byte (8 integer ops instead of a table load)
-__device__ __forceinline__ uint32_t lane_biased_swar(uint32_t b) {
-    uint32_t x = (b | (b << 12)) & 0x000F000Fu;
-    x = (x | (x << 6)) & 0x03030303u;
-    return 0x01010101u + (x & 0x01010101u) - ((x >> 1) & 0x01010101u);
-}
-
-// exact float(k) for |k| < 2^22 without I2F: 1.5*2^23 + k, then subtract
-__device__ __forceinline__ float small_int_float(int k) {
-    return __fsub_rn(__int_as_float(0x4B400000 + k), 12582912.0f);
-}
-
 template <int NW, bool kOpt = false, bool kArith = false>
 __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3Args a) {
     ChunkDev ch;
@@ -1417,7 +1417,7 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
         for (int w = 0; w < NW; ++w) {
             const uint32_t wd[4] = {v[w].x, v[w].y, v[w].z, v[w].w};
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] += tab[(wd[j >> 2] >> (8 * (j & 3))) & 0xFFu];
+            for (int j = 0; j < 16; ++j) acc[j] += lane_biased_swar((wd[j >> 2] >> (8 * (j & 3))) & 0xFFu);
             bad |= (wd[0] & (wd[0] >> 1)) | (wd[1] & (wd[1] >> 1)) | (wd[2] & (wd[2] >> 1)) |
                    (wd[3] & (wd[3] >> 1));
         }
@@ -1676,11 +1676,11 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
         a.optd = p.optd;
         a.opt = p.opt;
         switch (p.n_workers) {
-            case 1: k3_decode_staged<1, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 2: k3_decode_staged<2, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 3: k3_decode_staged<3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 4: k3_decode_staged<4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 8: k3_decode_staged<8, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 1: k3_decode_staged<1, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 2: k3_decode_staged<2, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 3: k3_decode_staged<3, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 4: k3_decode_staged<4, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            case 8: k3_decode_staged<8, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
             default: return cudaErrorInvalidValue;
         }
         return launch_status();
