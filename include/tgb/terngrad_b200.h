@@ -183,6 +183,17 @@ tgb_status tgb_decode_average(tgb_plan* plan, const uint8_t* d_src, int32_t n_wo
  * orders the step, and K3 decodes from local HBM: no allgather launch and the
  * NVLink traffic overlaps K2. Collective: every rank calls it once. */
 tgb_status tgb_plan_attach_peers(tgb_plan* plan, tgb_comm* comm);
+/* Fused exchange between N plans of ONE process (workers 0..N-1, on one device or
+ * on devices with peer access): every plan maps the others' gather buffers
+ * directly (no IPC, no NCCL), then tgb_step runs the same K1/K2 peer stores,
+ * flag barriers and K3 (or the sharded reduce/expand) as with tgb_plan_attach_peers.
+ * Each plan's tgb_step must be issued on its own stream (the steps of all N plans
+ * run concurrently: a plan's barrier waits for the others' K2). Single-process
+ * counterpart of the reference's run_cluster over InProcessHub
+ * (inc/cluster.hpp:378-397, inc/transport.hpp:77-125); used to run N = 8
+ * workers' exchanges on fewer GPUs. REF sharing only (TGB_ERR_UNSUPPORTED for
+ * PRESHARED, whose max-allreduce needs a communicator). */
+tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n);
 /* device pointers of the push area written by the last step (own scaler slots
  * + codes) and of the gather buffer (n_workers push areas) the last K3 read */
 tgb_status tgb_plan_last_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_gathered);

@@ -44,7 +44,7 @@ EXPORTS = [
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_step_host", "tgb_check",
     "tgb_plan_code_stats", "tgb_plan_enable_code_stats",
-    "tgb_plan_attach_peers", "tgb_plan_last_buffers",
+    "tgb_plan_attach_peers", "tgb_plan_attach_local", "tgb_plan_last_buffers",
     "tgb_optimizer_apply", "tgb_plan_bind_optimizer", "tgb_step_apply",
     "tgb_last_error_message", "tgb_plan_set_names", "tgb_plan_push_frame_size",
     "tgb_plan_serialize_push", "tgb_plan_decode_pull",
@@ -123,6 +123,7 @@ def _declare(L):
         "tgb_plan_code_stats": (S, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
         "tgb_plan_enable_code_stats": (S, [_vp, _i32]),
         "tgb_plan_attach_peers": (S, [_vp, _vp]),
+        "tgb_plan_attach_local": (S, [C.POINTER(_vp), _i32]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_optimizer_apply": (S, [C.POINTER(Optimizer), _u64, C.c_double, _i32,
                                     C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp),

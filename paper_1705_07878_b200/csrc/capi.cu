@@ -114,6 +114,7 @@ struct tgb_plan {
     uint64_t flags_off = 0;
     uint8_t* peer_ipc[kMaxPeers] = {};  // every rank's d_ipc mapped here (self = d_ipc)
     bool attached = false;
+    bool local_peers = false;  // tgb_plan_attach_local: peers are plans of this process
     int32_t rank = 0;
     uint64_t epoch = 0;  // attached: steps begun (barrier value); parity = epoch & 1
     // Chunk tables are ordered by group, and inside a group ternary chunks come
@@ -512,7 +513,7 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaFree(P->d_counters);
     cudaFree(P->d_bounds);
     cudaFree(P->d_push);
-    if (P->attached)
+    if (P->attached && !P->local_peers)
         for (int p = 0; p < P->n_workers; ++p)
             if (p != P->rank && P->peer_ipc[p]) cudaIpcCloseMemHandle(P->peer_ipc[p]);
     cudaFree(P->d_ipc);
@@ -1327,6 +1328,45 @@ tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {
     P->attached = true;
     P->shard = P->shard_capable;
     P->pipe = P->pipe_capable;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n) {
+    if (!plans || n < 1 || n > kMaxPeers) return TGB_ERR_INVALID_ARGUMENT;
+    for (int32_t p = 0; p < n; ++p) {
+        tgb_plan* P = plans[p];
+        if (!P || P->n_workers != n || P->worker != p || P->attached) return TGB_ERR_INVALID_ARGUMENT;
+        // PRESHARED needs the max-allreduce between K1 and K2 (NCCL): ranks only
+        if (n > 1 && P->p.share_mode == TGB_SHARE_PRESHARED) return TGB_ERR_UNSUPPORTED;
+    }
+    if (n == 1) return TGB_OK;
+    int cur = 0;
+    TGB_CUDA(cudaGetDevice(&cur));
+    for (int32_t p = 0; p < n; ++p)
+        for (int32_t q = 0; q < n; ++q) {
+            const int dp = plans[p]->device, dq = plans[q]->device;
+            if (dp == dq) continue;
+            int ok = 0;
+            TGB_CUDA(cudaDeviceCanAccessPeer(&ok, dp, dq));
+            if (!ok) return TGB_ERR_UNSUPPORTED;
+            TGB_CUDA(cudaSetDevice(dp));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(dq, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+            else if (e != cudaSuccess) {
+                cudaSetDevice(cur);
+                TGB_CUDA(e);
+            }
+        }
+    TGB_CUDA(cudaSetDevice(cur));
+    for (int32_t p = 0; p < n; ++p) {
+        tgb_plan* P = plans[p];
+        P->rank = p;
+        for (int32_t q = 0; q < n; ++q) P->peer_ipc[q] = plans[q]->d_ipc;
+        P->attached = true;
+        P->local_peers = true;
+        P->shard = P->shard_capable;
+        P->pipe = P->pipe_capable;
+    }
     return TGB_OK;
 }
 

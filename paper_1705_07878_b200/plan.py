@@ -195,6 +195,16 @@ class Plan:
             check(load().tgb_plan_attach_peers(self.h, comm.h), "tgb_plan_attach_peers")
         self.attached = True
 
+    @staticmethod
+    def attach_local(plans: Sequence["Plan"]):
+        """Fused exchange between the N plans of this process (workers 0..N-1;
+        tgb_plan_attach_local). Afterwards every plan's step must be issued on its
+        own stream: a plan's barrier waits for the other plans' K2."""
+        arr = (C.c_void_p * len(plans))(*[p.h.value for p in plans])
+        check(load().tgb_plan_attach_local(arr, len(plans)), "tgb_plan_attach_local")
+        for p in plans:
+            p.attached = True
+
     def last_buffers(self):
         """(own push area, gather buffer) of the last step, as uint8 views."""
         push, gathered = C.c_void_p(), C.c_void_p()
@@ -392,3 +402,60 @@ class SyncWorker:
 
     def check(self):
         self.plan.raise_errors()
+
+
+class LocalCluster:
+    """N data-parallel workers in ONE process (the reference's run_cluster over
+    InProcessHub, cluster.hpp:378-397): one plan per worker, attached to each
+    other with tgb_plan_attach_local, each stepping on its own stream. The
+    exchange kernels are the ones the multi-process path runs (K1/K2 peer
+    stores, flag barriers, K3 or the sharded reduce/expand), so N = 8 workers
+    can run on fewer GPUs. ``devices``: one device for all, or one per worker.
+    Set CUDA_DEVICE_MAX_CONNECTIONS >= 2N + 2 before CUDA initialises so the
+    workers' streams do not share hardware queues (a shared queue serialises a
+    worker's K2 behind another worker's barrier until the barrier times out),
+    and CUDA_MODULE_LOADING=EAGER: a lazily loaded kernel's first launch waits
+    for the context to idle, which a worker spinning in its barrier never does."""
+
+    def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
+                 n_workers: int, devices=None):
+        if not isinstance(devices, (list, tuple)):
+            devices = [devices] * n_workers
+        self.devices = [_dev(d) for d in devices]
+        self.names = list(names)
+        self.ns = [int(torch.Size(s).numel()) if len(s) else 0 for s in shapes]
+        self.n_workers = int(n_workers)
+        self.plans, self.grad_flat, self.grads, self.out_flat, self.outs = [], [], [], [], []
+        for w in range(self.n_workers):
+            dev = self.devices[w]
+            p = Plan(self.names, self.ns, cfg, worker=w, n_workers=self.n_workers, device=dev)
+            gf, gv = aligned_flat(self.ns, dev)
+            of, ov = aligned_flat(self.ns, dev)
+            p.bind(gv, ov)
+            self.plans.append(p)
+            self.grad_flat.append(gf)
+            self.grads.append(gv)
+            self.out_flat.append(of)
+            self.outs.append(ov)
+        if self.n_workers > 1:
+            Plan.attach_local(self.plans)
+        self.streams = [torch.cuda.Stream(d) for d in self.devices]
+
+    def step(self, t: int) -> List[List[torch.Tensor]]:
+        """Every worker's tgb_step for iteration t, each on its own stream."""
+        for p, s in zip(self.plans, self.streams):
+            p.step(t, None, s)
+        return self.outs
+
+    def synchronize(self):
+        for s in self.streams:
+            s.synchronize()
+
+    def check(self):
+        for p in self.plans:
+            p.raise_errors()
+
+    def close(self):
+        self.synchronize()
+        for p in self.plans:
+            p.close()

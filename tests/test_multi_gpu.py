@@ -35,3 +35,19 @@ def test_mp_check(exchange):
     for k, v in rep["checks"].items():
         assert v["ranks_identical"], k
         assert v["matches_oracle"], k
+
+
+def test_local_cluster_n8_on_one_gpu():
+    """N = 2/3/5/8 workers as plans of one process on cuda:0 (tgb_plan_attach_local):
+    the fused and sharded exchange kernels (incl. N = 8's 8-bit sums) bit-identical
+    on every worker and equal to the reference's average / the allgather path."""
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "local_cluster_check.py")],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert line, r.stdout[-2000:] + r.stderr[-2000:]
+    rep = json.loads(line[0])
+    bad = {k: v for k, v in rep["checks"].items()
+           if not (v["workers_identical"] and v["matches_reference"])}
+    assert not bad and r.returncode == 0, bad
+    assert rep["checks"]["N=8,vgg16"]["exchange"] == "sharded"
