@@ -42,6 +42,8 @@ def parse():
                     help="target CPU work for the in-line cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true",
+                    help="no per-launch events inside the timed region (A/B of their cost)")
     return ap.parse_args()
 
 
@@ -292,15 +294,20 @@ def run_b200(args):
 
     e_start = torch.cuda.Event(enable_timing=True)
     e_stop = torch.cuda.Event(enable_timing=True)
+    live_timing = not args.no_kernel_timing
     with ClockSampler(local) as clk:
         soak(0.6, 10_000)
         barrier()
         torch.cuda.synchronize(dev)
+        if live_timing:  # events around every kernel launch of the timed steps
+            plan.enable_timing(64 * K)
         e_start.record(stream)
         for k in range(K):
             one_step(args.warmup + k)
         e_stop.record(stream)
         torch.cuda.synchronize(dev)
+        live = plan.read_timing() if live_timing else []
+        plan.enable_timing(0)
         barrier()
         soak(0.6, 20_000)
     plan.raise_errors()
@@ -361,14 +368,52 @@ def run_b200(args):
     k3_ms = sum(stage[3]) / K
     kb = {"K1_stats": (4.0 * n, k1_ms), "K2_ternarize_pack": (4.0 * n + n / 4.0, k2_ms),
           "K3_decode": ((sum_w if mode == "sharded" else N / 4.0) * n + 4.0 * n, k3_ms)}
-    dom = max(kb, key=lambda k: kb[k][1])
-    dom_bytes, dom_ms = kb[dom]
+    # live per-kernel timing of the timed tgb_step region (events on each kernel's
+    # own stream): aggregate per (kernel, layer group); the dominant kernel is the
+    # one with the largest total time. Max over ranks of the per-kernel totals.
+    agg = {}
+    for r in live:
+        key = f"{r['kernel']}[g{r['group']}]"
+        a = agg.setdefault(key, {"launches": 0, "ms": 0.0, "hbm_bytes": 0, "nvlink_bytes": 0,
+                                 "elements": 0})
+        a["launches"] += 1
+        a["ms"] += r["ms"]
+        a["hbm_bytes"] += r["hbm_bytes"]
+        a["nvlink_bytes"] += r["nvlink_bytes"]
+        a["elements"] += r["elements"]
+    keys = sorted(agg)
+    if ws > 1 and keys:
+        tt = torch.tensor([agg[k]["ms"] for k in keys], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        for k, v in zip(keys, tt.tolist()):
+            agg[k]["ms"] = v
+    kernels_live = {}
+    for k in keys:
+        a = agg[k]
+        if a["ms"] <= 0:
+            continue
+        kernels_live[k] = {
+            "launches_per_step": a["launches"] / K, "ms_per_launch": a["ms"] / a["launches"],
+            "share_of_step": a["ms"] / K / ms_step if ms_step > 0 else None,
+            "hbm_bytes_per_launch": a["hbm_bytes"] / a["launches"],
+            "nvlink_bytes_per_launch": a["nvlink_bytes"] / a["launches"],
+            "GB/s": a["hbm_bytes"] / (a["ms"] * 1e-3) / 1e9,
+            "frac": a["hbm_bytes"] / (a["ms"] * 1e-3) / 1e9 / hbm}
+    if kernels_live:
+        dom = max(kernels_live, key=lambda k: agg[k]["ms"])
+        dom_bytes = kernels_live[dom]["hbm_bytes_per_launch"]
+        dom_ms = kernels_live[dom]["ms_per_launch"]
+        dom_src = "live: CUDA events around each launch inside the timed tgb_step region"
+    else:  # --no-kernel-timing: the sequential breakdown
+        dom = max(kb, key=lambda k: kb[k][1])
+        dom_bytes, dom_ms = kb[dom]
+        dom_src = "sequential stage pass"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.workload, {}).get(dom)
+            traffic = json.load(open(tpath)).get(args.workload, {}).get(f"n{N}", {}).get(dom)
         except Exception:
             traffic = None
     step_bytes = n * B_elem
@@ -437,8 +482,9 @@ def run_b200(args):
                        "no flush"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                         "peak_source": hbm_src,
-                         "algorithmic_bytes_per_launch": dom_bytes},
+                         "peak_source": hbm_src, "timing": dom_src,
+                         "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms},
+            "kernels_live": kernels_live,
             "roofline_step": {"bytes_per_step": step_bytes,
                               "achieved": step_bytes / (ms_step * 1e-3) / 1e9,
                               "frac": step_bytes / (ms_step * 1e-3) / 1e9 / hbm,
@@ -447,9 +493,10 @@ def run_b200(args):
                           "K3_decode": k3_ms, "sequential_step": staged_total / K,
                           "note": "per-kernel breakdown from a sequential pass; the headline "
                                   "ms_per_step is tgb_step (two-group overlap, N=1 fused decode)"},
-            "kernels": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
+            "kernels_sequential": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
-            "gpu_launches": launches_per_step * K,
+            "gpu_launches": (sum(1 for r in live if r["kernel"] != "nccl") if live
+                             else launches_per_step * K),
             "gpu_launches_note": "own kernels per tgb_step and layer group: N=1 K1 + K2 (K2 "
                                  "also decodes); pipelined K1 + K23; fused K1 + K2 + peer barrier "
                                  "+ K3; sharded K1 + K2 + barrier + K3a (owner sums) + barrier + "

@@ -206,6 +206,33 @@ tgb_status tgb_step(tgb_plan* plan, tgb_comm* comm, uint64_t t, void* stream);
  * next call's H2D overlaps this call's D2H (separate copy streams). */
 tgb_status tgb_step_host(tgb_plan* plan, tgb_comm* comm, uint64_t t, const float* const* h_grads,
                          float* const* h_out, void* stream);
+/* ---- live kernel timing (measurement, not semantics) ----
+ * With capacity > 0, every kernel launch issued by this plan (tgb_step and the
+ * stage entry points) is bracketed by two CUDA events recorded on the stream the
+ * kernel is launched on, until `capacity` launches are recorded; capacity 0
+ * turns it off. Each call resets the record list. tgb_plan_read_timing waits
+ * for the recorded events and returns one record per launch: its kernel, layer
+ * group, elapsed ms and ALGORITHMIC bytes (local HBM reads + writes the
+ * kernel's work requires; NVLink bytes separately). */
+#define TGB_KERNEL_K1 0      /* k1_stats: clip bound + scalers */
+#define TGB_KERNEL_K2 1      /* k2_ternarize (+ fused N = 1 decode / peer stores) */
+#define TGB_KERNEL_BARRIER 2 /* k_peer_barrier */
+#define TGB_KERNEL_K3 3      /* k3 decode of the gather buffer */
+#define TGB_KERNEL_K3A 4     /* sharded: owner sums N workers' codes */
+#define TGB_KERNEL_K3B 5     /* sharded: decode of the packed sums */
+#define TGB_KERNEL_K23 6     /* pipelined K2+K3 */
+#define TGB_KERNEL_NCCL 7    /* ncclAllGather / ncclAllReduce issued by the plan */
+typedef struct tgb_kernel_time {
+    int32_t kind;          /* TGB_KERNEL_* */
+    int32_t group;         /* layer group (two-group schedule) or 0 */
+    float ms;              /* event-measured duration on the launching stream */
+    uint64_t elements;     /* gradient elements the launch covers */
+    uint64_t hbm_bytes;    /* algorithmic local HBM bytes (read + write) */
+    uint64_t nvlink_bytes; /* bytes this rank stores into peers */
+} tgb_kernel_time;
+tgb_status tgb_plan_enable_timing(tgb_plan* plan, int32_t capacity);
+tgb_status tgb_plan_read_timing(tgb_plan* plan, tgb_kernel_time* out, int32_t cap,
+                                int32_t* n_records);
 /* telemetry: count nonzero codes inside K2 from now on (off by default: it costs one
  * shared-memory pass per chunk) */
 tgb_status tgb_plan_enable_code_stats(tgb_plan* plan, int32_t on);

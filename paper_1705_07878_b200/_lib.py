@@ -43,7 +43,8 @@ EXPORTS = [
     "tgb_plan_block_info",
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_step_host", "tgb_check",
-    "tgb_plan_code_stats", "tgb_plan_enable_code_stats",
+    "tgb_plan_code_stats", "tgb_plan_enable_code_stats", "tgb_plan_enable_timing",
+    "tgb_plan_read_timing",
     "tgb_plan_attach_peers", "tgb_plan_attach_local", "tgb_plan_last_buffers",
     "tgb_optimizer_apply", "tgb_plan_bind_optimizer", "tgb_step_apply",
     "tgb_last_error_message", "tgb_plan_set_names", "tgb_plan_push_frame_size",
@@ -73,6 +74,16 @@ class PlanInfo(C.Structure):
                 ("codes_offset", C.c_uint64), ("n_layers", C.c_int32), ("n_slots", C.c_int32),
                 ("n_chunks", C.c_int32), ("n_workers", C.c_int32), ("chunk_elems", C.c_uint32),
                 ("n_groups", C.c_uint32), ("n_blocks", C.c_int32), ("exchange", C.c_int32)]
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("group", C.c_int32), ("ms", C.c_float),
+                ("elements", C.c_uint64), ("hbm_bytes", C.c_uint64),
+                ("nvlink_bytes", C.c_uint64)]
+
+
+KERNEL_NAMES = {0: "K1_stats", 1: "K2_ternarize_pack", 2: "peer_barrier", 3: "K3_decode",
+                4: "K3a_shard_reduce", 5: "K3b_shard_expand", 6: "K23_pipelined", 7: "nccl"}
 
 
 class BlockInfo(C.Structure):
@@ -122,6 +133,8 @@ def _declare(L):
         "tgb_check": (S, [_vp, C.POINTER(Error)]),
         "tgb_plan_code_stats": (S, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
         "tgb_plan_enable_code_stats": (S, [_vp, _i32]),
+        "tgb_plan_enable_timing": (S, [_vp, _i32]),
+        "tgb_plan_read_timing": (S, [_vp, C.POINTER(KernelTime), _i32, C.POINTER(_i32)]),
         "tgb_plan_attach_peers": (S, [_vp, _vp]),
         "tgb_plan_attach_local": (S, [C.POINTER(_vp), _i32]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),

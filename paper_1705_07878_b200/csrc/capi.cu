@@ -175,6 +175,12 @@ struct tgb_plan {
     uint8_t* d_pull = nullptr;      // pull payload staging
     uint64_t pull_cap = 0;
     OptDev* d_optd = nullptr;        // per-block optimizer table (fused decode -> optimizer)
+    // live kernel timing (tgb_plan_enable_timing): two events per launch
+    int32_t t_cap = 0, t_used = 0;
+    std::vector<cudaEvent_t> t_ev;
+    std::vector<tgb_kernel_time> t_rec;
+    bool t_sized = false;
+    uint64_t t_k12[2][2] = {}, t_k3[2][2] = {};  // [group][ternary, passthrough] elements
     const OptArgs* opt_active = nullptr;  // set during tgb_step_apply when fused
 };
 
@@ -529,6 +535,7 @@ void tgb_plan_destroy(tgb_plan* P) {
         if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
     }
     if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+    for (cudaEvent_t e : P->t_ev) cudaEventDestroy(e);
     if (P->s_h2d) cudaStreamDestroy(P->s_h2d);
     if (P->s_d2h) cudaStreamDestroy(P->s_d2h);
     if (P->ev_h2d) cudaEventDestroy(P->ev_h2d);
@@ -645,6 +652,37 @@ static inline uint8_t* cur_gathered(const tgb_plan* P) {
 // plan is the single group 0 spanning every chunk)
 static inline int n_groups(const tgb_plan* P) { return P->grouped ? 2 : 1; }
 
+// ---- live kernel timing: events around each launch on its own stream
+static void chunk_elems(const tgb_plan* P, const std::vector<ChunkDev>& chs, uint32_t b,
+                        uint32_t c, uint64_t out[2]) {
+    out[0] = out[1] = 0;
+    for (uint32_t i = b; i < b + c && i < chs.size(); ++i)
+        out[(P->h_layers[chs[i].layer].flags & kLayerPassthrough) ? 1 : 0] += chs[i].count;
+}
+
+static void timing_size(tgb_plan* P) {
+    if (P->t_sized) return;
+    for (int g = 0; g < n_groups(P); ++g) {
+        chunk_elems(P, P->h_chunks, P->cb[g], P->cc[g], P->t_k12[g]);
+        chunk_elems(P, P->h_chunks3, P->cb3[g], P->cc3[g], P->t_k3[g]);
+    }
+    P->t_sized = true;
+}
+
+static int t_begin(tgb_plan* P, cudaStream_t st) {
+    if (P->t_used >= P->t_cap) return -1;
+    const int slot = P->t_used++;
+    if (cudaEventRecord(P->t_ev[2 * slot], st) != cudaSuccess) return -1;
+    return slot;
+}
+
+static void t_end(tgb_plan* P, cudaStream_t st, int slot, int32_t kind, int32_t g,
+                  uint64_t elems, uint64_t hbm, uint64_t nvl) {
+    if (slot < 0) return;
+    cudaEventRecord(P->t_ev[2 * slot + 1], st);
+    P->t_rec[slot] = tgb_kernel_time{kind, g, 0.0f, elems, hbm, nvl};
+}
+
 static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     const uint32_t b = P->cb[g];
     K1Launch k{P->d_partials + b, P->d_counters,
@@ -661,7 +699,13 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     k.variant = P->k1_variant;
     k.tensors = P->d_tensors;
     k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
+    const int ts = t_begin(P, st);
     TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, P->ck1[g], k, st));
+    if (ts >= 0) {
+        timing_size(P);
+        const uint64_t n = P->t_k12[g][0];
+        t_end(P, st, ts, TGB_KERNEL_K1, g, n, 4 * n, 0);
+    }
     return TGB_OK;
 }
 
@@ -686,7 +730,22 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
             for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->cs[r];
         }
     }
+    const int ts = t_begin(P, st);
     TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + P->cb[g], P->cc[g], k, st));
+    if (ts >= 0) {
+        timing_size(P);
+        const uint64_t nt = P->t_k12[g][0], np = P->t_k12[g][1], N = P->n_workers;
+        const uint64_t msg = (nt + 3) / 4 + 4 * np;  // code bytes + raw passthrough bytes
+        uint64_t own = msg, nvl = 0;
+        if (P->attached && P->shard) {
+            own = msg / N;
+            nvl = msg - own;
+        } else if (P->attached) {
+            nvl = (N - 1) * msg;
+        }
+        const uint64_t out = fuse_decode ? 4 * (nt + np) : 0;
+        t_end(P, st, ts, TGB_KERNEL_K2, g, nt + np, 4 * (nt + np) + own + out, nvl);
+    }
     return TGB_OK;
 }
 
@@ -697,7 +756,9 @@ static tgb_status launch_barrier(tgb_plan* P, int g, cudaStream_t st) {
                       g * kMaxPeers + P->rank;
     f.local = reinterpret_cast<uint64_t*>(P->d_ipc + P->flags_off) + g * kMaxPeers;
     f.n = P->n_workers;
+    const int ts = t_begin(P, st);
     TGB_CUDA(launch_peer_barrier(f, P->epoch, P->d_err, st));
+    t_end(P, st, ts, TGB_KERNEL_BARRIER, g, 0, 0, 0);
     return TGB_OK;
 }
 
@@ -711,7 +772,13 @@ static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t 
         k.optd = P->d_optd;
         k.opt = *P->opt_active;
     }
+    const int ts = t_begin(P, st);
     TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + P->cb3[g], P->cc3[g], k, st));
+    if (ts >= 0) {
+        timing_size(P);
+        const uint64_t nt = P->t_k3[g][0], np = P->t_k3[g][1], N = n_workers;
+        t_end(P, st, ts, TGB_KERNEL_K3, g, nt + np, N * ((nt + 3) / 4 + 4 * np) + 4 * (nt + np), 0);
+    }
     return TGB_OK;
 }
 
@@ -743,7 +810,17 @@ static ShardLaunch shard_launch(const tgb_plan* P) {
 static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
     TGB_TRY_INNER(launch_barrier(P, 0, st));
     const uint32_t r = static_cast<uint32_t>(P->rank);
+    const int ts = t_begin(P, st);
     TGB_CUDA(launch_k3_reduce(P->d_fat + P->cs[r], P->cs[r + 1] - P->cs[r], shard_launch(P), st));
+    if (ts >= 0) {
+        uint64_t e[2];
+        chunk_elems(P, P->h_chunks, P->cs[r], P->cs[r + 1] - P->cs[r], e);
+        const uint64_t N = P->n_workers;
+        const uint64_t sums = P->nib ? (e[0] + 1) / 2 : e[0];  // packed biased sums
+        const uint64_t out = sums + 4 * e[1];
+        t_end(P, st, ts, TGB_KERNEL_K3A, 0, e[0] + e[1], N * ((e[0] + 3) / 4 + 4 * e[1]) + out,
+              (N - 1) * out);
+    }
     TGB_TRY_INNER(launch_barrier(P, 1, st));
     return TGB_OK;
 }
@@ -776,7 +853,15 @@ static tgb_status launch_pipelined(tgb_plan* P, uint64_t t, cudaStream_t st) {
         ++P->pipe_steps;
     }
     P->last = st;
+    const int ts = t_begin(P, st);
     TGB_CUDA(launch_k23_pipelined(P->d_fat, pl.n_items, k2, k3, pl, st));
+    if (ts >= 0) {
+        uint64_t e[2];
+        chunk_elems(P, P->h_chunks, 0, pl.n_items, e);
+        const uint64_t N = P->n_workers, msg = (e[0] + 3) / 4 + 4 * e[1];
+        t_end(P, st, ts, TGB_KERNEL_K23, 0, e[0] + e[1],
+              4 * (e[0] + e[1]) + msg + N * msg + 4 * (e[0] + e[1]), (N - 1) * msg);
+    }
     return TGB_OK;
 }
 
@@ -831,7 +916,11 @@ tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
         return TGB_OK;
     }
     if (!C || C->nranks != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
+    const int ts = t_begin(P, st);
     TGB_NCCL(ncclAllGather(P->d_push, P->d_gathered, P->push_bytes, ncclUint8, C->comm, st));
+    t_end(P, st, ts, TGB_KERNEL_NCCL, 0, P->total,
+          static_cast<uint64_t>(P->n_workers) * P->push_bytes,
+          static_cast<uint64_t>(P->n_workers - 1) * P->push_bytes);
     return TGB_OK;
 }
 
@@ -842,8 +931,15 @@ tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_worke
     P->last = st;
     if (!d_src && P->shard) {  // sharded exchange: decode this step's packed sums
         if (n_workers != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
+        const int ts = t_begin(P, st);
         TGB_CUDA(launch_k3_expand(P->d_fat3, static_cast<uint32_t>(P->h_chunks3.size()),
                                   shard_launch(P), st));
+        if (ts >= 0) {
+            uint64_t e[2];
+            chunk_elems(P, P->h_chunks3, 0, static_cast<uint32_t>(P->h_chunks3.size()), e);
+            const uint64_t sums = P->nib ? (e[0] + 1) / 2 : e[0];
+            t_end(P, st, ts, TGB_KERNEL_K3B, 0, e[0] + e[1], sums + 4 * e[1] + 4 * (e[0] + e[1]), 0);
+        }
         return TGB_OK;
     }
     if (!d_src) d_src = cur_gathered(P);  // NULL: this step's gather buffer
@@ -1328,6 +1424,34 @@ tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {
     P->attached = true;
     P->shard = P->shard_capable;
     P->pipe = P->pipe_capable;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_enable_timing(tgb_plan* P, int32_t capacity) {
+    if (!P || capacity < 0) return TGB_ERR_INVALID_ARGUMENT;
+    const size_t want = 2 * static_cast<size_t>(capacity);
+    while (P->t_ev.size() < want) {
+        cudaEvent_t e = nullptr;
+        TGB_CUDA(cudaEventCreate(&e));
+        P->t_ev.push_back(e);
+    }
+    P->t_rec.assign(static_cast<size_t>(capacity), tgb_kernel_time{});
+    P->t_cap = capacity;
+    P->t_used = 0;
+    return TGB_OK;
+}
+
+tgb_status tgb_plan_read_timing(tgb_plan* P, tgb_kernel_time* out, int32_t cap, int32_t* n) {
+    if (!P || (cap > 0 && !out) || !n) return TGB_ERR_INVALID_ARGUMENT;
+    const int32_t m = std::min(cap, P->t_used);
+    for (int32_t i = 0; i < m; ++i) {
+        TGB_CUDA(cudaEventSynchronize(P->t_ev[2 * i + 1]));
+        float ms = 0.0f;
+        TGB_CUDA(cudaEventElapsedTime(&ms, P->t_ev[2 * i], P->t_ev[2 * i + 1]));
+        out[i] = P->t_rec[i];
+        out[i].ms = ms;
+    }
+    *n = P->t_used;
     return TGB_OK;
 }
 

@@ -261,6 +261,23 @@ class Plan:
         check(st, "tgb_plan_decode_pull")
         return it.value
 
+    def enable_timing(self, capacity: int):
+        """Bracket the next `capacity` kernel launches of this plan with CUDA events on
+        their own streams (0 = off); resets the records (tgb_plan_enable_timing)."""
+        check(load().tgb_plan_enable_timing(self.h, int(capacity)), "tgb_plan_enable_timing")
+        self._t_cap = int(capacity)
+
+    def read_timing(self) -> List[dict]:
+        """One record per timed launch: kernel, group, ms, elements, algorithmic HBM and
+        NVLink bytes (waits for the recorded events)."""
+        cap = getattr(self, "_t_cap", 0)
+        arr = (_lib.KernelTime * max(cap, 1))()
+        n = C.c_int32()
+        check(load().tgb_plan_read_timing(self.h, arr, cap, C.byref(n)), "tgb_plan_read_timing")
+        return [{"kernel": _lib.KERNEL_NAMES.get(r.kind, str(r.kind)), "group": r.group,
+                 "ms": r.ms, "elements": r.elements, "hbm_bytes": r.hbm_bytes,
+                 "nvlink_bytes": r.nvlink_bytes} for r in arr[:min(n.value, cap)]]
+
     def enable_code_stats(self, on: bool = True):
         """count nonzero codes inside K2 from the next step on (telemetry, off by default)"""
         check(load().tgb_plan_enable_code_stats(self.h, int(on)), "tgb_plan_enable_code_stats")
