@@ -299,15 +299,11 @@ def run_b200(args):
         soak(0.6, 10_000)
         barrier()
         torch.cuda.synchronize(dev)
-        if live_timing:  # events around every kernel launch of the timed steps
-            plan.enable_timing(64 * K)
         e_start.record(stream)
         for k in range(K):
             one_step(args.warmup + k)
         e_stop.record(stream)
         torch.cuda.synchronize(dev)
-        live = plan.read_timing() if live_timing else []
-        plan.enable_timing(0)
         barrier()
         soak(0.6, 20_000)
     plan.raise_errors()
@@ -347,9 +343,22 @@ def run_b200(args):
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
     barrier()
     torch.cuda.synchronize(dev)
+    # attribution pass: the step's own kernels, one after another on one stream,
+    # each bracketed by CUDA events on that stream (tgb_plan_enable_timing).
+    # N = 1: tgb_step on the ungrouped plan (K1 + K2 with the fused decode);
+    # N > 1: the stage API = the same K1 / K2 (peer stores) / barrier / K3 kernels.
+    if live_timing:
+        plan_b.enable_timing(64 * K)
     for k in range(K):
         staged_step(30_000 + k, evs[k])
     torch.cuda.synchronize(dev)
+    if N == 1 and live_timing:
+        plan_b.enable_timing(64 * K)
+        for k in range(K):
+            plan_b.step(50_000 + k)
+        torch.cuda.synchronize(dev)
+    live = plan_b.read_timing() if live_timing else []
+    plan_b.enable_timing(0)
     barrier()
     plan.raise_errors()
     stage = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(4)]
@@ -368,12 +377,12 @@ def run_b200(args):
     k3_ms = sum(stage[3]) / K
     kb = {"K1_stats": (4.0 * n, k1_ms), "K2_ternarize_pack": (4.0 * n + n / 4.0, k2_ms),
           "K3_decode": ((sum_w if mode == "sharded" else N / 4.0) * n + 4.0 * n, k3_ms)}
-    # live per-kernel timing of the timed tgb_step region (events on each kernel's
-    # own stream): aggregate per (kernel, layer group); the dominant kernel is the
-    # one with the largest total time. Max over ranks of the per-kernel totals.
+    # live per-kernel timing of the attribution pass (events on each kernel's own
+    # stream): aggregate per kernel over its launches (one per layer group); the
+    # dominant kernel has the largest total time. Max over ranks of the totals.
     agg = {}
     for r in live:
-        key = f"{r['kernel']}[g{r['group']}]"
+        key = r["kernel"] + ("+decode" if N == 1 and r["kernel"].startswith("K2") else "")
         a = agg.setdefault(key, {"launches": 0, "ms": 0.0, "hbm_bytes": 0, "nvlink_bytes": 0,
                                  "elements": 0})
         a["launches"] += 1
@@ -394,7 +403,7 @@ def run_b200(args):
             continue
         kernels_live[k] = {
             "launches_per_step": a["launches"] / K, "ms_per_launch": a["ms"] / a["launches"],
-            "share_of_step": a["ms"] / K / ms_step if ms_step > 0 else None,
+            "ms_per_step": a["ms"] / K,
             "hbm_bytes_per_launch": a["hbm_bytes"] / a["launches"],
             "nvlink_bytes_per_launch": a["nvlink_bytes"] / a["launches"],
             "GB/s": a["hbm_bytes"] / (a["ms"] * 1e-3) / 1e9,
@@ -403,7 +412,8 @@ def run_b200(args):
         dom = max(kernels_live, key=lambda k: agg[k]["ms"])
         dom_bytes = kernels_live[dom]["hbm_bytes_per_launch"]
         dom_ms = kernels_live[dom]["ms_per_launch"]
-        dom_src = "live: CUDA events around each launch inside the timed tgb_step region"
+        dom_src = ("live: CUDA events around each launch on its stream, attribution pass "
+                   "(the step's kernels run sequentially: N=1 tgb_step ungrouped, N>1 stage API)")
     else:  # --no-kernel-timing: the sequential breakdown
         dom = max(kb, key=lambda k: kb[k][1])
         dom_bytes, dom_ms = kb[dom]
