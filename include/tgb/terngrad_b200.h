@@ -226,6 +226,7 @@ typedef struct tgb_kernel_time {
     int32_t kind;          /* TGB_KERNEL_* */
     int32_t group;         /* layer group (two-group schedule) or 0 */
     float ms;              /* event-measured duration on the launching stream */
+    float start_ms;        /* launch start relative to the first recorded launch */
     uint64_t elements;     /* gradient elements the launch covers */
     uint64_t hbm_bytes;    /* algorithmic local HBM bytes (read + write) */
     uint64_t nvlink_bytes; /* bytes this rank stores into peers */

@@ -78,7 +78,7 @@ class PlanInfo(C.Structure):
 
 class KernelTime(C.Structure):
     _fields_ = [("kind", C.c_int32), ("group", C.c_int32), ("ms", C.c_float),
-                ("elements", C.c_uint64), ("hbm_bytes", C.c_uint64),
+                ("start_ms", C.c_float), ("elements", C.c_uint64), ("hbm_bytes", C.c_uint64),
                 ("nvlink_bytes", C.c_uint64)]
 
 

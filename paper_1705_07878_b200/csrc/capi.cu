@@ -136,8 +136,23 @@ struct tgb_plan {
     uint32_t pc_b[kMaxPieces] = {}, pc_c[kMaxPieces] = {}, pc_b3[kMaxPieces] = {},
              pc_c3[kMaxPieces] = {};
     cudaStream_t gs3 = nullptr;
-    cudaEvent_t ev_piece[kMaxPieces] = {};
+    cudaEvent_t ev_piece[kMaxPieces] = {}, ev_pbar[kMaxPieces] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    // two-group start order (TGB_STAGGER, A/B): 1 = group 0's K1 first, group 1
+    // (the dominant layer) starts when it is done, so K1 of the dominant layer
+    // (HBM-bound) overlaps K2 of the rest (Philox / NVLink-bound); 2 = the other
+    // way round; 0 = both at once (default). Measured (VGG-16, profiles/
+    // r01_schedule_ab.json): 0 is best at N = 1/2/4 (N=4 0.409 ms vs 0.423 / 0.431):
+    // the groups already overlap, and the step is bound by the total HBM traffic
+    // plus K2's NVLink stores, which no reordering shrinks.
+    int32_t stagger = 0;
+    cudaEvent_t ev_stag = nullptr;
+    // attached two-group steps: each group's barrier kernel runs on its own stream
+    // at the greatest priority (TGB_BSTREAM), so a group's barrier (which releases
+    // the peers waiting on this rank) is not queued behind the other group's CTAs
+    int32_t bstream = 0;  // A/B: 0.411 vs 0.409 ms at N = 4 (no gain)
+    cudaStream_t gsb[2] = {nullptr, nullptr};
+    cudaEvent_t ev_b0[2] = {nullptr, nullptr}, ev_b1[2] = {nullptr, nullptr};
     ErrWord* d_err = nullptr;
     uint64_t push_bytes = 0, codes_offset = 0, code_bytes = 0, total = 0;
     int32_t n_slots = 0, n_active = 0;
@@ -483,12 +498,21 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                   cudaStreamCreateWithPriority(&P->gs[1], cudaStreamNonBlocking, gprio1(lo, hi)) == cudaSuccess &&
                   cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
                   cudaEventCreateWithFlags(&P->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming) == cudaSuccess;
+                  cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&P->ev_stag, cudaEventDisableTiming) == cudaSuccess;
+        if (const char* m = std::getenv("TGB_STAGGER")) P->stagger = std::atoi(m);
+        if (const char* m = std::getenv("TGB_BSTREAM")) P->bstream = std::atoi(m);
+        for (int g = 0; ok && g < 2; ++g)
+            ok = cudaStreamCreateWithPriority(&P->gsb[g], cudaStreamNonBlocking, hi) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&P->ev_b0[g], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&P->ev_b1[g], cudaEventDisableTiming) == cudaSuccess;
         if (ok && P->pieces > 1) {
-            ok = cudaStreamCreateWithPriority(&P->gs3, cudaStreamNonBlocking, gprio1(lo, hi)) ==
-                 cudaSuccess;
+            int p3 = gprio1(lo, hi);
+            if (const char* m = std::getenv("TGB_P3PRIO")) p3 = std::atoi(m) ? hi : lo;
+            ok = cudaStreamCreateWithPriority(&P->gs3, cudaStreamNonBlocking, p3) == cudaSuccess;
             for (int pc = 0; ok && pc < P->pieces; ++pc)
-                ok = cudaEventCreateWithFlags(&P->ev_piece[pc], cudaEventDisableTiming) == cudaSuccess;
+                ok = cudaEventCreateWithFlags(&P->ev_piece[pc], cudaEventDisableTiming) == cudaSuccess &&
+                     cudaEventCreateWithFlags(&P->ev_pbar[pc], cudaEventDisableTiming) == cudaSuccess;
         }
         if (!ok) {
             tgb_plan_destroy(P);
@@ -586,9 +610,17 @@ void tgb_plan_destroy(tgb_plan* P) {
         if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
     }
     if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+    if (P->ev_stag) cudaEventDestroy(P->ev_stag);
+    for (int g = 0; g < 2; ++g) {
+        if (P->gsb[g]) cudaStreamDestroy(P->gsb[g]);
+        if (P->ev_b0[g]) cudaEventDestroy(P->ev_b0[g]);
+        if (P->ev_b1[g]) cudaEventDestroy(P->ev_b1[g]);
+    }
     if (P->gs3) cudaStreamDestroy(P->gs3);
-    for (int pc = 0; pc < kMaxPieces; ++pc)
+    for (int pc = 0; pc < kMaxPieces; ++pc) {
         if (P->ev_piece[pc]) cudaEventDestroy(P->ev_piece[pc]);
+        if (P->ev_pbar[pc]) cudaEventDestroy(P->ev_pbar[pc]);
+    }
     for (cudaEvent_t e : P->t_ev) cudaEventDestroy(e);
     if (P->s_h2d) cudaStreamDestroy(P->s_h2d);
     if (P->s_d2h) cudaStreamDestroy(P->s_d2h);
@@ -734,7 +766,7 @@ static void t_end(tgb_plan* P, cudaStream_t st, int slot, int32_t kind, int32_t 
                   uint64_t elems, uint64_t hbm, uint64_t nvl) {
     if (slot < 0) return;
     cudaEventRecord(P->t_ev[2 * slot + 1], st);
-    P->t_rec[slot] = tgb_kernel_time{kind, g, 0.0f, elems, hbm, nvl};
+    P->t_rec[slot] = tgb_kernel_time{kind, g, 0.0f, 0.0f, elems, hbm, nvl};
 }
 
 static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
@@ -1014,6 +1046,20 @@ tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_worke
     return TGB_OK;
 }
 
+// two-group schedule: the gi-th group to launch, and the event its chain waits for
+static inline int stag_group(const tgb_plan* P, int gi) {
+    if (P->stagger == 0) return 1 - gi;  // both at once, dominant chain launched first
+    const int first = P->stagger == 2 ? 1 : 0;
+    return gi == 0 ? first : 1 - first;
+}
+static inline cudaEvent_t stag_wait(const tgb_plan* P, int gi) {
+    return (gi == 0 || P->stagger == 0) ? P->ev_fork : P->ev_stag;
+}
+static inline tgb_status stag_mark(tgb_plan* P, int gi, cudaStream_t gs) {
+    if (gi == 0 && P->stagger != 0) TGB_CUDA(cudaEventRecord(P->ev_stag, gs));
+    return TGB_OK;
+}
+
 tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
     if (!P || !P->bound) return TGB_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
@@ -1029,10 +1075,11 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
         }
         TGB_CUDA(cudaEventRecord(P->ev_fork, st));
         for (int gi = 0; gi < 2; ++gi) {
-            const int g = 1 - gi;
+            const int g = stag_group(P, gi);
             cudaStream_t gs = P->gs[g];
-            TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_fork, 0));
+            TGB_CUDA(cudaStreamWaitEvent(gs, stag_wait(P, gi), 0));
             TGB_TRY(launch_stats(P, g, gs));
+            TGB_TRY(stag_mark(P, gi, gs));
             TGB_TRY(launch_tern(P, g, t, gs, true));
             TGB_CUDA(cudaEventRecord(P->ev_join[g], gs));
         }
@@ -1061,18 +1108,26 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
     TGB_CUDA(cudaEventRecord(P->ev_fork, st));
     const uint8_t* src = cur_gathered(P);
     for (int gi = 0; gi < 2; ++gi) {
-        const int g = 1 - gi;  // launch the critical (dominant-layer) chain first
+        const int g = stag_group(P, gi);
         cudaStream_t gs = P->gs[g];
-        TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_fork, 0));
+        TGB_CUDA(cudaStreamWaitEvent(gs, stag_wait(P, gi), 0));
         TGB_TRY(launch_stats(P, g, gs));
+        TGB_TRY(stag_mark(P, gi, gs));
         if (g == 1 && P->attached && P->pieces > 1) {
             // dominant layer in pieces: K2 piece p on gs, then on gs3 the barrier of
             // piece p (every rank's K2 piece p done) and its K3, overlapping K2 p+1
             for (int pc = 0; pc < P->pieces; ++pc) {
                 TGB_TRY(launch_tern_rng(P, 1, P->pc_b[pc], P->pc_c[pc], t, gs, false));
                 TGB_CUDA(cudaEventRecord(P->ev_piece[pc], gs));
-                TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_piece[pc], 0));
-                TGB_TRY(launch_barrier(P, 2 + pc, P->gs3));
+                if (P->bstream) {  // barrier at the greatest priority, K3 piece on gs3
+                    TGB_CUDA(cudaStreamWaitEvent(P->gsb[1], P->ev_piece[pc], 0));
+                    TGB_TRY(launch_barrier(P, 2 + pc, P->gsb[1]));
+                    TGB_CUDA(cudaEventRecord(P->ev_pbar[pc], P->gsb[1]));
+                    TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_pbar[pc], 0));
+                } else {
+                    TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_piece[pc], 0));
+                    TGB_TRY(launch_barrier(P, 2 + pc, P->gs3));
+                }
                 TGB_TRY(launch_decode_rng(P, 1, P->pc_b3[pc], P->pc_c3[pc], src, P->n_workers,
                                           P->gs3));
             }
@@ -1080,7 +1135,15 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
             continue;
         }
         TGB_TRY(launch_tern(P, g, t, gs));
-        if (P->attached) TGB_TRY(launch_barrier(P, g, gs));
+        if (P->attached && P->bstream) {
+            TGB_CUDA(cudaEventRecord(P->ev_b0[g], gs));
+            TGB_CUDA(cudaStreamWaitEvent(P->gsb[g], P->ev_b0[g], 0));
+            TGB_TRY(launch_barrier(P, g, P->gsb[g]));
+            TGB_CUDA(cudaEventRecord(P->ev_b1[g], P->gsb[g]));
+            TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_b1[g], 0));
+        } else if (P->attached) {
+            TGB_TRY(launch_barrier(P, g, gs));
+        }
         TGB_TRY(launch_decode(P, g, src, P->n_workers, gs));
         TGB_CUDA(cudaEventRecord(P->ev_join[g], gs));
     }
@@ -1549,10 +1612,12 @@ tgb_status tgb_plan_read_timing(tgb_plan* P, tgb_kernel_time* out, int32_t cap, 
     const int32_t m = std::min(cap, P->t_used);
     for (int32_t i = 0; i < m; ++i) {
         TGB_CUDA(cudaEventSynchronize(P->t_ev[2 * i + 1]));
-        float ms = 0.0f;
+        float ms = 0.0f, t0 = 0.0f;
         TGB_CUDA(cudaEventElapsedTime(&ms, P->t_ev[2 * i], P->t_ev[2 * i + 1]));
+        TGB_CUDA(cudaEventElapsedTime(&t0, P->t_ev[0], P->t_ev[2 * i]));
         out[i] = P->t_rec[i];
         out[i].ms = ms;
+        out[i].start_ms = t0;
     }
     *n = P->t_used;
     return TGB_OK;

@@ -275,7 +275,7 @@ class Plan:
         n = C.c_int32()
         check(load().tgb_plan_read_timing(self.h, arr, cap, C.byref(n)), "tgb_plan_read_timing")
         return [{"kernel": _lib.KERNEL_NAMES.get(r.kind, str(r.kind)), "group": r.group,
-                 "ms": r.ms, "elements": r.elements, "hbm_bytes": r.hbm_bytes,
+                 "ms": r.ms, "start_ms": r.start_ms, "elements": r.elements, "hbm_bytes": r.hbm_bytes,
                  "nvlink_bytes": r.nvlink_bytes} for r in arr[:min(n.value, cap)]]
 
     def enable_code_stats(self, on: bool = True):
