@@ -135,10 +135,16 @@ def synth_host(ns, rank, pinned=True):
 
 
 # ------------------------------------------------------------------ CPU arm
-def cpu_reference_sample(layers, n_workers, budget_s, max_steps=None, warmup=1):
+def cpu_reference_sample(layers, n_workers, budget_s, max_steps=None, warmup=1, replicas=1):
     """Time the reference as shipped (oracle/_ref: encode_step x N worker threads
     -> ParameterServer::step -> decode_pull) on a bounded sample of the
-    workload: every tensor truncated to its first CAP elements."""
+    workload: every tensor truncated to its first CAP elements. `replicas`
+    independent clusters (each N worker threads + 1 server thread, its own
+    gradients) run concurrently from Python threads (ctypes releases the GIL), so
+    the sample uses replicas x (N + 1) host threads; throughput = all replicas'
+    elements / wall time."""
+    import threading as _th
+
     import numpy as np
 
     from oracle.oracle import Config, RefCluster, Reference
@@ -147,25 +153,52 @@ def cpu_reference_sample(layers, n_workers, budget_s, max_steps=None, warmup=1):
     names = [n for n, _ in layers]
     ns = [min(CAP, _numel(s)) for _, s in layers]
     ref = Reference()
-    rng = np.random.default_rng(0)
-    grads = [[(rng.standard_normal(n).astype(np.float32) * np.float32(1e-3)) for n in ns]
-             for _ in range(n_workers)]
-    cl = RefCluster(ref, names, grads, Config(seed=42))
-    for t in range(warmup):
-        cl.step(t)
-    times, t = [], warmup
-    while True:
-        times.append(cl.step(t))
-        t += 1
-        if max_steps is not None and len(times) >= max_steps:
-            break
-        if max_steps is None and sum(times) >= budget_s:
-            break
-    cl.close()
-    elems = n_workers * sum(ns)
+    clusters = []
+    for r in range(replicas):
+        rng = np.random.default_rng(r)
+        grads = [[(rng.standard_normal(n).astype(np.float32) * np.float32(1e-3)) for n in ns]
+                 for _ in range(n_workers)]
+        clusters.append(RefCluster(ref, names, grads, Config(seed=42)))
+    for cl in clusters:
+        for t in range(warmup):
+            cl.step(t)
+    steps = [0] * replicas
+    stop = [False]
+
+    def run(i):
+        t = warmup
+        while not stop[0]:
+            clusters[i].step(t)
+            t += 1
+            steps[i] += 1
+            if max_steps is not None and steps[i] >= max_steps:
+                break
+
+    threads = [_th.Thread(target=run, args=(i,)) for i in range(replicas)]
+    t0 = time.perf_counter()
+    for th in threads:
+        th.start()
+    if max_steps is None:
+        while time.perf_counter() - t0 < budget_s and any(th.is_alive() for th in threads):
+            time.sleep(0.05)
+        stop[0] = True
+    for th in threads:
+        th.join()
+    wall = time.perf_counter() - t0
+    for cl in clusters:
+        cl.close()
+    total_steps = sum(steps)
+    elems = n_workers * sum(ns) * total_steps
     sample = (f"{len(ns)} tensors of the set, each truncated to its first {CAP} elements "
-              f"({sum(ns)} elements/worker), {n_workers} worker(s), {len(times)} steps")
-    return elems, times, sample
+              f"({sum(ns)} elements/worker), {n_workers} worker(s), {replicas} concurrent "
+              f"cluster replica(s) x (N worker threads + 1 server thread), {total_steps} steps "
+              f"in {wall:.1f} s")
+    return elems, wall, total_steps, sample
+
+
+def ref_replicas(n_workers):
+    cores = os.cpu_count() or 1
+    return max(1, cores // (n_workers + 1))
 
 
 def _numel(shape):
@@ -183,20 +216,21 @@ def run_reference(args):
 
     layers = layersets.get(args.workload)
     n_workers = max(args.gpus, ws)
-    elems, times, sample = cpu_reference_sample(layers, n_workers, budget_s=1e9,
-                                                max_steps=args.steps,
-                                                warmup=max(1, min(args.warmup, 2)))
-    total = sum(times)
-    value = elems * len(times) / total
+    reps = ref_replicas(n_workers)
+    elems, wall, nsteps, sample = cpu_reference_sample(layers, n_workers, budget_s=1e9,
+                                                       max_steps=args.steps,
+                                                       warmup=max(1, min(args.warmup, 2)),
+                                                       replicas=reps)
+    value = elems / wall
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(times),
-        "warmup": max(1, min(args.warmup, 2)), "ms_per_step": 1e3 * total / len(times),
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": max(1, min(args.warmup, 2)), "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{args.workload} gradient set, {n_workers} workers (sample)",
                    "global_batch": None, "seq_len": None,
                    "parallelism": f"dp{n_workers} (parameter server, as shipped)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_workers + 1,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": reps * (n_workers + 1),
                          "kind": "reference", "sample": sample,
                          "host_cores_available": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -464,9 +498,11 @@ def run_b200(args):
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         try:
-            elems, times, sample = cpu_reference_sample(layers, 1, args.cpu_seconds)
-            cpu = {"value": elems * len(times) / sum(times), "unit": UNIT, "cores": 2,
-                   "kind": "reference", "sample": sample + " (1 worker thread + 1 server thread)",
+            reps = ref_replicas(1)
+            elems, wall, _, sample = cpu_reference_sample(layers, 1, args.cpu_seconds,
+                                                          replicas=reps)
+            cpu = {"value": elems / wall, "unit": UNIT, "cores": 2 * reps,
+                   "kind": "reference", "sample": sample,
                    "host_cores_available": os.cpu_count()}
         except Exception as ex:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
