@@ -1641,7 +1641,16 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
         } else if (p.direct) {
             k2_ternarize<TableSource, false, 4, 3, true, false, true><<<n_chunks, kThreads, 0, st>>>(src, a);
         } else {
-            k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+            switch (p.variant) {  // TGB_K2V (A/B): key schedule x occupancy x bytes per thread
+                case 1: k2_ternarize<TableSource, true, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                case 2: k2_ternarize<TableSource, true, 4, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                case 4: k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                case 5: k2_ternarize<TableSource, false, 2, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                case 6: k2_ternarize<TableSource, false, 4, 5, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                // default (= 3): 64 registers, 4 CTAs/SM: 190.9 vs 202.9 us at 3 CTAs/SM
+                // (VGG-16, N = 1, tools/k2_fused_ab.sh): the fused kernel is latency-bound
+                default: k2_ternarize<TableSource, false, 4, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+            }
         }
         return launch_status();
     }
@@ -1652,6 +1661,7 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
         case 1: k2_ternarize<TableSource, true, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
         case 2: k2_ternarize<TableSource, true, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 3: k2_ternarize<TableSource, false, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
         default: k2_ternarize<TableSource, false, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
     }
     return launch_status();
