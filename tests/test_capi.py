@@ -110,3 +110,18 @@ def test_push_layout_blocks():
     assert [b.region_offset for b in lay.blocks] == [256, 272, 288, 304, 304]
     assert lay.blocks[-1].nbytes == 12 and lay.code_bytes == 2 + 2 + 1 + 0
     assert lay.push_bytes == 512
+
+
+def test_attach_local_and_timing_argument_validation():
+    """tgb_plan_attach_local / tgb_plan_enable_timing / tgb_plan_read_timing reject bad
+    arguments before touching a device (no plan exists without a GPU)."""
+    L = _lib.load()
+    assert L.tgb_plan_attach_local(None, 2) == _lib.TGB_ERR_INVALID_ARGUMENT
+    arr = (C.c_void_p * 2)(None, None)
+    assert L.tgb_plan_attach_local(arr, 2) == _lib.TGB_ERR_INVALID_ARGUMENT
+    assert L.tgb_plan_attach_local(arr, 0) == _lib.TGB_ERR_INVALID_ARGUMENT
+    assert L.tgb_plan_attach_local(arr, 9) == _lib.TGB_ERR_INVALID_ARGUMENT
+    assert L.tgb_plan_enable_timing(None, 4) == _lib.TGB_ERR_INVALID_ARGUMENT
+    n = C.c_int32()
+    assert L.tgb_plan_read_timing(None, None, 0, C.byref(n)) == _lib.TGB_ERR_INVALID_ARGUMENT
+    assert C.sizeof(_lib.KernelTime) == 40

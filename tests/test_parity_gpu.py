@@ -541,3 +541,28 @@ def test_wire_protocol_errors():
     with pytest.raises(tg.ProtocolError, match="nonzero radix remainder"):
         plan.decode_pull(bytes(bad))
     plan.close()
+
+
+def test_live_kernel_timing_records():
+    """tgb_plan_enable_timing: one record per launch with its algorithmic bytes
+    (N = 1 step = K1 + K2 with the fused decode)."""
+    names, ns = ["a.w", "b.w"], [1000, 40003]
+    sw = tg.SyncWorker(names, [[n] for n in ns], tg.CodecConfig(seed=42), device=DEV)
+    sw.grad_flat.normal_(0.0, 1e-3)
+    sw.step(0)
+    sw.plan.enable_timing(16)
+    for t in range(3):
+        sw.step(1 + t)
+    recs = sw.plan.read_timing()
+    sw.plan.enable_timing(0)
+    sw.check()
+    kinds = [r["kernel"] for r in recs]
+    assert kinds.count("K1_stats") == 3 * (2 if sw.plan.grouped else 1)
+    n = sum(ns)
+    k1 = sum(r["hbm_bytes"] for r in recs if r["kernel"] == "K1_stats")
+    k2 = sum(r["hbm_bytes"] for r in recs if r["kernel"] == "K2_ternarize_pack")
+    assert k1 == 3 * 4 * n
+    assert k2 == 3 * (4 * n + 4 * n + (1000 + 3) // 4 + (40003 + 3) // 4) or \
+        k2 == 3 * (4 * n + 4 * n + (n + 3) // 4)
+    assert all(r["ms"] > 0 and r["start_ms"] >= 0 for r in recs)
+    sw.plan.close()
