@@ -453,6 +453,22 @@ def run_b200(args):
         dom_bytes, dom_ms = kb[dom]
         dom_src = "sequential stage pass"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    # NVLink view (N > 1): the kernel that moves the most bytes across NVLink, its
+    # achieved rate vs the measured peer-copy bandwidth (B200_PROFILING.md: 770 GB/s
+    # per direction; 900 nominal), and the whole step's NVLink bytes per rank
+    roofline_nvlink = None
+    nvl = {k: v for k, v in kernels_live.items() if v["nvlink_bytes_per_launch"] > 0}
+    if nvl:
+        kn = max(nvl, key=lambda k: nvl[k]["nvlink_bytes_per_launch"] * nvl[k]["launches_per_step"])
+        v = nvl[kn]
+        rate = v["nvlink_bytes_per_launch"] / (v["ms_per_launch"] * 1e-3) / 1e9
+        step_nvl = sum(x["nvlink_bytes_per_launch"] * x["launches_per_step"]
+                       for x in kernels_live.values())
+        roofline_nvlink = {
+            "kernel": kn, "achieved": rate, "peak": 770.0, "unit": "GB/s", "frac": rate / 770.0,
+            "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)",
+            "bytes_per_step_per_rank": step_nvl,
+            "step_time_floor_ms": step_nvl / 770e9 * 1e3}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -530,6 +546,7 @@ def run_b200(args):
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": hbm_src, "timing": dom_src,
                          "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms},
+            "roofline_nvlink": roofline_nvlink,
             "kernels_live": kernels_live,
             "roofline_step": {"bytes_per_step": step_bytes,
                               "achieved": step_bytes / (ms_step * 1e-3) / 1e9,
