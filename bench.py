@@ -274,7 +274,10 @@ def run_b200(args):
     #   allgather designs: B(N) = 12 + 0.5 N;
     #   sharded: 4 (K1) + 4.25 (K2) + 0.25 (K3a codes) + 2 x sums (land + K3b read) + 4 = 12.5 + 2 w
     sum_w = (0.5 if N <= 7 else 1.0) if mode == "sharded" else 0.0
-    B_elem = 12.5 + 2 * sum_w if mode == "sharded" else 12.0 + 0.5 * N
+    #   fused-r3: 4 + 4 + 0.25 (2-bit push) + 0.2 (own radix copy) + 0.2 (N-1) landing
+    #             + 0.2 N (K3 reads) + 4 = 12.25 + 0.4 N
+    B_elem = (12.5 + 2 * sum_w if mode == "sharded" else
+              12.25 + 0.4 * N if mode == "fused-r3" else 12.0 + 0.5 * N)
     host, _ = synth_host(ns, rank)
     sw.grad_flat[:host.numel()].copy_(host.to(dev, non_blocking=True))
     stream = torch.cuda.current_stream(dev)
@@ -527,7 +530,7 @@ def run_b200(args):
     groups = 2 if plan.grouped else 1
     # own kernels per tgb_step: N=1: K1 + K2(decode fused); fused: K1 + K2 + barrier + K3;
     # sharded: K1 + K2 + barrier + K3a + barrier + K3b; nccl: K1 + K2 + K3 (+ NCCL's own)
-    launches_per_step = groups * {"none": 2, "fused": 4, "sharded": 6, "nccl": 3,
+    launches_per_step = groups * {"none": 2, "fused": 4, "fused-r3": 4, "sharded": 6, "nccl": 3,
                                   "pipelined": 2}[mode]
     if rank == 0:
         line = {
@@ -565,6 +568,8 @@ def run_b200(args):
                                  "+ K3; sharded K1 + K2 + barrier + K3a (owner sums) + barrier + "
                                  "K3b; nccl K1 + K2 + K3",
             "exchange": {"fused": "fused NVLink peer stores in K2 + device barrier",
+                         "fused-r3": "fused NVLink peer stores in K2 (radix-3 wire codes, 5 "
+                                     "elements per byte) + device barrier",
                          "sharded": "sharded: K2 stores codes at the chunk owner, owner sums N "
                                     "workers into packed sums stored at every rank (NVLink), "
                                     "2 device barriers",

@@ -107,6 +107,9 @@ typedef struct tgb_plan_info {
 #define TGB_EXCHANGE_PIPELINED 4 /* one persistent kernel per step: codes stored into every
                                     peer item by item, per-item epoch flags, each item
                                     decoded as soon as all ranks published it */
+#define TGB_EXCHANGE_FUSED_R3 5 /* fused, with radix-3 wire codes (5 elements per byte,
+                                   1.6 instead of 2 bits on NVLink; N >= 3, shared scalers,
+                                   no passthrough blocks); the push area keeps 2-bit codes */
 
 /* One block of the encoded gradient (EncodedGradient::blocks, codec.hpp:70-76):
  * a bucket of a ternary layer (TernaryBlock, the whole layer unless FixedSize)

@@ -34,7 +34,7 @@ TGB_SHARE_REF, TGB_SHARE_PRESHARED = 0, 1
 UNIQUE_ID_BYTES = 128
 TGB_EXCHANGE_NONE, TGB_EXCHANGE_NCCL, TGB_EXCHANGE_FUSED, TGB_EXCHANGE_SHARDED = 0, 1, 2, 3
 TGB_EXCHANGE_PIPELINED = 4
-EXCHANGE_NAMES = ["none", "nccl", "fused", "sharded", "pipelined"]
+EXCHANGE_NAMES = ["none", "nccl", "fused", "sharded", "pipelined", "fused-r3"]
 
 # every symbol the header declares (checked by tests/test_capi.py)
 EXPORTS = [

@@ -117,6 +117,11 @@ struct tgb_plan {
     uint64_t flags_off = 0;
     uint8_t* peer_ipc[kMaxPeers] = {};  // every rank's d_ipc mapped here (self = d_ipc)
     bool attached = false;
+    // radix-3 wire codes (fused exchange, N >= 3, shared scalers, no passthrough
+    // blocks; TGB_R3=0 disables): K2 stores 5 elements per byte into every rank's
+    // gather buffer (1.6 instead of 2 bits per element on NVLink) and its 2-bit codes
+    // into d_push (the reference-format push area), K3 decodes the radix bytes
+    bool r3_capable = false, r3 = false;
     bool local_peers = false;  // tgb_plan_attach_local: peers are plans of this process
     int32_t rank = 0;
     uint64_t epoch = 0;  // attached: steps begun (barrier value); parity = epoch & 1
@@ -313,6 +318,25 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     for (int32_t l = 0; l < n_layers; ++l) total_elems += layers[l].n;
     uint64_t chunk = 4096, chunk3 = kChunk3;
     while (chunk < kChunk12 && chunk * 444 < total_elems) chunk <<= 1;
+    {
+        bool any_pass = false;
+        for (int32_t l = 0; l < n_layers; ++l) any_pass |= (layers[l].flags & TGB_LAYER_PASSTHROUGH) != 0;
+        // (the same shard / pipeline decisions as below: those exchanges keep 2-bit codes)
+        int smin = 5;
+        if (const char* m = std::getenv("TGB_SHARD_MIN")) smin = std::max(2, std::atoi(m));
+        bool shard = n_workers >= smin && params->scaler_sharing;
+        if (const char* m = std::getenv("TGB_SHARD")) shard = shard && std::atoi(m) != 0;
+        const char* pm = std::getenv("TGB_PIPE");
+        const bool pipe = pm && std::atoi(pm) != 0 && !shard;
+        bool want = n_workers >= 3 && n_workers <= kMaxPeers && params->scaler_sharing &&
+                    !any_pass && !shard && !pipe;
+        if (const char* m = std::getenv("TGB_R3")) want = want && std::atoi(m) != 0;
+        P->r3_capable = want;
+        if (want) {  // work items at multiples of 80 elements (16-B aligned radix bytes)
+            chunk = chunk / 80 * 80;
+            chunk3 = kChunk3R3;
+        }
+    }
     if (const char* m = std::getenv("TGB_CHUNK")) {  // A/B only
         const uint64_t v = std::strtoull(m, nullptr, 10);
         if (v >= 1024 && v % 1024 == 0 && v <= kChunk12) chunk = v;
@@ -650,6 +674,7 @@ tgb_status tgb_plan_get_info(const tgb_plan* P, tgb_plan_info* o) {
                   : !P->attached    ? TGB_EXCHANGE_NCCL
                   : P->shard        ? TGB_EXCHANGE_SHARDED
                   : P->pipe         ? TGB_EXCHANGE_PIPELINED
+                  : P->r3           ? TGB_EXCHANGE_FUSED_R3
                                     : TGB_EXCHANGE_FUSED;
     return TGB_OK;
 }
@@ -726,7 +751,7 @@ static inline uint8_t* push_area(const tgb_plan* P, int p) {
     return P->peer_ipc[p] + (P->epoch & 1u) * g + static_cast<uint64_t>(P->rank) * P->push_bytes;
 }
 static inline uint8_t* own_push(const tgb_plan* P) {
-    return P->attached ? push_area(P, P->rank) : P->d_push;
+    return (P->attached && !P->r3) ? push_area(P, P->rank) : P->d_push;
 }
 static inline uint8_t* cur_gathered(const tgb_plan* P) {
     if (P->attached)
@@ -779,7 +804,7 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     if (P->attached) {  // scalers also land in every peer's gather buffer
         k.push.n = 0;
         for (int p = 0; p < P->n_workers; ++p)
-            if (p != P->rank) k.push.base[k.push.n++] = push_area(P, p);
+            if (p != P->rank || P->r3) k.push.base[k.push.n++] = push_area(P, p);
         k.push.remote = 1;
     }
     k.variant = P->k1_variant;
@@ -815,6 +840,7 @@ static tgb_status launch_tern_rng(tgb_plan* P, int g, uint32_t cb, uint32_t cc, 
             k.shard_n = P->n_workers;
             for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->cs[r];
         }
+        k.r3 = P->r3 ? 1 : 0;
     }
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + cb, cc, k, st));
@@ -827,6 +853,9 @@ static tgb_status launch_tern_rng(tgb_plan* P, int g, uint32_t cb, uint32_t cc, 
         if (P->attached && P->shard) {
             own = msg / N;
             nvl = msg - own;
+        } else if (P->attached && P->r3) {  // 2-bit push + radix-3 own copy; radix-3 to peers
+            own = msg + (nt + 4) / 5;
+            nvl = (N - 1) * ((nt + 4) / 5);
         } else if (P->attached) {
             nvl = (N - 1) * msg;
         }
@@ -861,6 +890,7 @@ static tgb_status launch_decode_rng(tgb_plan* P, int g, uint32_t cb3, uint32_t c
                1.0f / static_cast<float>(n_workers), P->d_err};
     k.variant = P->k3_variant;
     k.chunk3 = P->chunk3;
+    k.r3 = (P->r3 && src == cur_gathered(P) && n_workers == P->n_workers) ? 1 : 0;
     if (P->opt_active) {
         k.optd = P->d_optd;
         k.opt = *P->opt_active;
@@ -871,7 +901,8 @@ static tgb_status launch_decode_rng(tgb_plan* P, int g, uint32_t cb3, uint32_t c
         uint64_t e[2];
         chunk_elems(P, P->h_chunks3, cb3, cc3, e);
         const uint64_t nt = e[0], np = e[1], N = n_workers;
-        t_end(P, st, ts, TGB_KERNEL_K3, g, nt + np, N * ((nt + 3) / 4 + 4 * np) + 4 * (nt + np), 0);
+        const uint64_t codes = k.r3 ? (nt + 4) / 5 : (nt + 3) / 4;
+        t_end(P, st, ts, TGB_KERNEL_K3, g, nt + np, N * (codes + 4 * np) + 4 * (nt + np), 0);
     }
     return TGB_OK;
 }
@@ -1309,6 +1340,7 @@ static bool opt_fusable(const tgb_plan* P) {
         if (std::atoi(m) == 0) return false;
     if (P->n_workers == 1) return true;
     const int N = P->n_workers;
+    if (P->r3) return true;  // k3_decode_r3<N, kOpt>, 3 <= N <= 8
     return P->p.scaler_sharing && !P->shard && !P->pipe && P->k3_variant >= 1 &&
            P->chunk3 == kChunk3 && (N <= 4 || N == 8);
 }
@@ -1590,6 +1622,7 @@ tgb_status tgb_plan_attach_peers(tgb_plan* P, tgb_comm* C) {
     P->attached = true;
     P->shard = P->shard_capable;
     P->pipe = P->pipe_capable;
+    P->r3 = P->r3_capable && !P->shard && !P->pipe;
     return TGB_OK;
 }
 
@@ -1658,6 +1691,7 @@ tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n) {
         P->local_peers = true;
         P->shard = P->shard_capable;
         P->pipe = P->pipe_capable;
+        P->r3 = P->r3_capable && !P->shard && !P->pipe;
     }
     return TGB_OK;
 }

@@ -573,18 +573,61 @@ __device__ __forceinline__ void k2_store_chunk(const K2Args& a, const LayerDev& 
     for (int p = p0; p < p1; ++p) copy_out(stage + streamed, k2_dst(a, p) + off, nbytes - streamed);
 }
 
+// Radix-3 wire codes (fused exchange, N >= 3): 5 elements per byte,
+// byte = sum_i d_i 3^i with digit d = the 2-bit code (0 zero, 1 plus, 2 minus) of
+// element 5j + i -- 1.6 instead of 2 bits per element on NVLink (log2 3 = 1.585).
+// lut10 maps the 10 code bits of 5 elements (element i at bits 2i) to that byte.
+__device__ __forceinline__ void r3_build_lut(uint8_t* lut10) {
+    for (uint32_t v = threadIdx.x; v < 1024; v += kThreads) {
+        uint32_t r = 0, m = 1;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            r += ((v >> (2 * i)) & 3u) * m;  // 11 never occurs in K2 output
+            m *= 3;
+        }
+        lut10[v] = static_cast<uint8_t>(r);
+    }
+}
+
+// stage (2-bit codes of `count` elements, pad bits 00) -> r3 (ceil(count/5) bytes)
+__device__ __forceinline__ uint32_t r3_convert(const uint8_t* stage, uint32_t count,
+                                               const uint8_t* lut10, uint8_t* r3) {
+    const uint32_t nr3 = (count + 4) / 5;
+    const uint32_t nbytes = (count + 3) >> 2;
+    for (uint32_t j = threadIdx.x; j < nr3; j += kThreads) {
+        const uint32_t bit = 10 * j, k = bit >> 3;
+        uint32_t v = stage[k];
+        if (k + 1 < nbytes) v |= static_cast<uint32_t>(stage[k + 1]) << 8;
+        v = (v >> (bit & 7u)) & 0x3FFu;
+        r3[j] = lut10[v];  // elements >= count are pad codes (00) or masked by nbytes
+    }
+    return nr3;
+}
+
 template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false,
-          bool kOpt = false, bool kDirect = false>
+          bool kOpt = false, bool kDirect = false, bool kR3 = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     __shared__ float4 lutv[kFuse ? 256 : 1];
+    __shared__ __align__(16) uint8_t r3buf[kR3 ? kStageBytes : 16];
+    __shared__ uint8_t lut10[kR3 ? 1024 : 1];
     const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
     ChunkDev ch;
     LayerDev L;
     src.get(b, ch, L);
     uint32_t streamed = 0;
+    if (kR3) r3_build_lut(lut10);  // visible after k2_code_chunk's closing barrier
     const uint32_t nbytes = k2_code_chunk<kRolling, U, kFuse, NoHook, kOpt, kDirect>(
         a, L, ch, b, stage, lutv, NoHook(), &streamed);
+    if (kR3) {  // 2-bit codes to this rank's push area, radix-3 bytes to every rank
+        if (!nbytes) return;  // (r3 plans have no passthrough blocks)
+        copy_out(stage, a.push + L.code_off + (ch.begin >> 2), nbytes);
+        const uint32_t nr3 = r3_convert(stage, ch.count, lut10, r3buf);
+        __syncthreads();
+        const uint64_t off = L.code_off + ch.begin / 5;  // chunks start at multiples of 80
+        for (int p = 0; p < a.dst.n; ++p) copy_out(r3buf, a.dst.base[p] + off, nr3);
+        return;
+    }
     // No fence after the peer stores: the step barrier kernel runs after this
     // grid completes in stream order, and grid completion implies its (peer)
     // stores are performed -- the guarantee event-based multi-GPU sync relies on.
@@ -1353,6 +1396,118 @@ __device__ __forceinline__ uint32_t pack_nib(uint32_t acc) {  // 4 byte lanes ->
 // builds the 16 packed sums in registers, stages them in shared memory, and
 // the CTA then writes the chunk's sums to every rank with 16-byte stores
 // (NVLink stores stay full-width).
+// K3 over radix-3 wire codes (fused exchange, N >= 3, shared scalers): stage the
+// chunk's r3 bytes of all N workers in shared memory (16-B loads), then per group of
+// 4 bytes (20 elements) sum N table words (5 biased lanes (1 + v) per byte, 8 bits
+// each, <= 2N) and decode every lane to (s * float(sum)) * invN (codec.hpp:296,
+// wire.hpp:220; s = max over workers, cluster.hpp:195-196) -- the same two rounded
+// multiplies as the 2-bit kernels, so the output is bit-identical.
+template <int NW, bool kOpt>
+__global__ void __launch_bounds__(kThreads) k3_decode_r3(TableSource src, K3Args a) {
+    ChunkDev ch;
+    LayerDev L;
+    src.get(blockIdx.x, ch, L);
+    constexpr uint32_t kStage = kChunk3R3 / 5;  // r3 bytes per worker and chunk (16-B multiple)
+    __shared__ __align__(16) uint8_t codes[NW][kStage];
+    __shared__ unsigned long long tab5[256];
+    __shared__ float sw[NW];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t count = ch.count;
+    const uint32_t nr3 = (count + 4) / 5;
+    const uint32_t n16 = (nr3 + 15) >> 4;  // the block region is padded to 16 B
+    {
+        constexpr int R = (kStage / 16 + kThreads - 1) / kThreads;
+        uint4 v[NW][R];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint4* b4 = reinterpret_cast<const uint4*>(a.src + a.stride * w + L.code_off +
+                                                             ch.begin / 5);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = tid + r * kThreads;
+                v[w][r] = i < n16 ? __ldcs(b4 + i) : make_uint4(0, 0, 0, 0);
+            }
+        }
+        {
+            unsigned long long t = 0;  // byte -> 5 lanes of 1 + v (digit 0 -> 1, 1 -> 2, 2 -> 0)
+            uint32_t x = tid;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const uint32_t d = x % 3u;
+                x /= 3u;
+                t |= static_cast<unsigned long long>(d == 0 ? 1u : (d == 1 ? 2u : 0u)) << (8 * i);
+            }
+            tab5[tid] = t;  // bytes >= 243 are flagged separately
+        }
+        if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = tid + r * kThreads;
+                if (i < n16) reinterpret_cast<uint4*>(codes[w])[i] = v[w][r];
+            }
+    }
+    __syncthreads();
+    float s_max = 0.0f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
+    auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
+        return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
+    };
+    OptDev od{};
+    if (kOpt) od = a.optd[ch.layer];
+    float* out = L.out + ch.begin;
+    const bool vec_out = (L.flags & kLayerVecOut) != 0;
+    uint32_t bad = 0, bad_g = 0;
+    const uint32_t ng = (nr3 + 3) >> 2;
+    for (uint32_t g = tid; g < ng; g += kThreads) {
+        unsigned long long acc[4] = {0, 0, 0, 0};
+        const uint32_t nb = nr3 - 4 * g < 4 ? nr3 - 4 * g : 4;
+        const uint32_t mask = nb >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nb)) - 1u);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t word = reinterpret_cast<const uint32_t*>(codes[w])[g];
+            const uint32_t b = __vcmpgeu4(word, 0xF3F3F3F3u) & mask;  // byte >= 243: corrupt
+            if (b && !bad) bad_g = g;
+            bad |= b;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] += tab5[(word >> (8 * k)) & 0xFFu];
+        }
+        const uint32_t e0 = 20 * g;
+        float v[20];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+                v[5 * k + i] = val(static_cast<uint32_t>(acc[k] >> (8 * i)) & 0xFFu);
+        if (kOpt) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const uint32_t e = e0 + 4 * q;
+                if (e >= count) break;
+                const uint64_t ge = ch.begin + e;
+                opt_apply4(a.opt, od.w + ge, od.s1 ? od.s1 + ge : nullptr,
+                           od.s2 ? od.s2 + ge : nullptr,
+                           make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]),
+                           od.vec != 0, count - e < 4 ? count - e : 4);
+            }
+        } else if (vec_out && e0 + 20 <= count) {
+            float4* o4 = reinterpret_cast<float4*>(out + e0);
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+                __stcs(o4 + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < 20; ++i)
+                if (e0 + i < count) out[e0 + i] = v[i];
+        }
+    }
+    if (bad)  // a byte >= 243 cannot come from K2: reported at its group's first element
+        raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
+                    block_rng_base(L) + ch.begin + 20ull * bad_g);
+}
+
 template <int NW>
 __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs a) {
     ChunkDev ch;
@@ -1630,6 +1785,11 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     a.shard_n = p.shard_n;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
+    if (p.r3) {  // fused exchange with radix-3 wire codes (N >= 3)
+        k2_ternarize<TableSource, false, 4, 3, false, false, false, true>
+            <<<n_chunks, kThreads, 0, st>>>(src, a);
+        return launch_status();
+    }
     if (p.fuse_decode) {
         if (p.optd) {  // N == 1 fused decode -> optimizer
             a.optd = p.optd;
@@ -1682,6 +1842,28 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     K3Ptrs ptrs{};
     const TableSource src{chunks};
+    if (p.r3) {  // radix-3 wire codes (fused exchange, shared scalers, 3 <= N <= 8)
+        if (p.optd) {
+            a.optd = p.optd;
+            a.opt = p.opt;
+        }
+#define TGB_R3_CASE(NW)                                                                      \
+    case NW:                                                                                 \
+        if (p.optd) k3_decode_r3<NW, true><<<n_chunks, kThreads, 0, st>>>(src, a);          \
+        else k3_decode_r3<NW, false><<<n_chunks, kThreads, 0, st>>>(src, a);                \
+        break;
+        switch (p.n_workers) {
+            TGB_R3_CASE(3)
+            TGB_R3_CASE(4)
+            TGB_R3_CASE(5)
+            TGB_R3_CASE(6)
+            TGB_R3_CASE(7)
+            TGB_R3_CASE(8)
+            default: return cudaErrorInvalidValue;
+        }
+#undef TGB_R3_CASE
+        return launch_status();
+    }
     if (p.optd) {  // fused decode -> optimizer (the caller checked the supported N)
         a.optd = p.optd;
         a.opt = p.opt;

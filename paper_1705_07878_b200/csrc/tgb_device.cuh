@@ -17,6 +17,9 @@ constexpr int kThreads = 256;       // CTA size of every streaming kernel
 constexpr uint32_t kChunk = 16384;    // per-layer API work item (elements, multiple of 16)
 constexpr uint32_t kChunk12 = 32768;  // plan K1/K2 work item
 constexpr uint32_t kChunk3 = 16384;   // plan K3 work item
+// radix-3 wire codes (5 elements per byte): work items start at multiples of 80
+// elements so every chunk's bytes start 16-B aligned (80 / 5 = 16)
+constexpr uint32_t kChunk3R3 = 16320;  // = 204 x 80
 constexpr int kMaxWorkers = 64;     // decode LUT capacity (2N+1 entries)
 
 // layer flags (device)

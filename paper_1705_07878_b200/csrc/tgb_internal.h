@@ -50,6 +50,7 @@ struct K2Launch {
     uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
     int32_t direct = 0;         // thread-contiguous code bytes stored straight from registers
+    int32_t r3 = 0;             // fused exchange: radix-3 wire codes to dst, 2-bit codes to push
 };
 
 struct K3Launch {
@@ -64,6 +65,7 @@ struct K3Launch {
     uint32_t chunk3 = 0;   // plan K3 chunk elements (the staged variant needs kChunk3)
     const OptDev* optd = nullptr;  // fused decode -> optimizer (staged kernel, N in {1,2,3,4,8})
     OptArgs opt{};
+    int32_t r3 = 0;  // the source holds radix-3 wire codes (chunks of kChunk3R3 elements)
 };
 
 struct ShardLaunch {

@@ -459,8 +459,11 @@ class LocalCluster:
         self.streams = [torch.cuda.Stream(d) for d in self.devices]
 
     def step(self, t: int) -> List[List[torch.Tensor]]:
-        """Every worker's tgb_step for iteration t, each on its own stream."""
-        for p, s in zip(self.plans, self.streams):
+        """Every worker's tgb_step for iteration t, each on its own stream (ordered
+        after work already queued on each device's current stream, e.g. the
+        gradients' producers)."""
+        for p, s, d in zip(self.plans, self.streams, self.devices):
+            s.wait_stream(torch.cuda.current_stream(d))
             p.step(t, None, s)
         return self.outs
 

@@ -8,12 +8,13 @@ This runs N workers as N plans of one process on cuda:0, attached to each
 other, each stepping on its own stream: the same K1/K2 peer stores, flag
 barriers and K3 / K3a+K3b kernels as the multi-process path, minus NVLink.
 
-Checks per N (default 2 3 5 8):
+Checks per N (default 2 3 4 5 8):
   * small tensor set x REF configs (shared/unshared, Global, FixedSize +
     passthrough), default schedule and forced fused (TGB_SHARD=0): every worker
     holds bit-identical output equal to the reference's own average over the
     same N workers (oracle/_ref, codec.hpp:245-311);
-  * full VGG-16 set at N = 8 (sharded, 8-bit sums) and N = 5 (4-bit sums):
+  * full VGG-16 set at N = 8 (sharded, 8-bit sums), N = 5 (4-bit sums), and the
+    fused exchange with radix-3 wire codes at N = 4 and 8 (TGB_SHARD=0):
     bit-identical on every worker and equal to K3 over the N unattached push
     areas laid out back to back (the NCCL-allgather path, itself pinned to
     the reference on the golden cases).
@@ -85,11 +86,14 @@ def small_checks(N, report):
             cl.close()
 
 
-def vgg_check(N, report):
+def vgg_check(N, report, shard="default"):
     layers = tg.layersets.get("vgg16")
     names, shapes = [n for n, _ in layers], [s for _, s in layers]
     cfg = tg.CodecConfig(seed=42)
+    if shard == "0":
+        os.environ["TGB_SHARD"] = "0"
     cl = tg.LocalCluster(names, shapes, cfg, N, DEV)
+    os.environ.pop("TGB_SHARD", None)
     for w in range(N):
         g = torch.Generator(device=DEV).manual_seed(1000 + w)
         cl.grad_flat[w].normal_(0.0, 1e-3, generator=g)
@@ -116,7 +120,7 @@ def vgg_check(N, report):
         p.raise_errors()
     same = len(hs) == 1
     ok = sha(out_flat) == sha(cl.out_flat[0])
-    report["checks"][f"N={N},vgg16"] = {"workers_identical": same, "matches_reference": ok,
+    report["checks"][f"N={N},vgg16" + ("" if shard == "default" else f",shard={shard}")] = {"workers_identical": same, "matches_reference": ok,
                                         "exchange": exchange_of(cl.plans[0]),
                                         "elements_per_worker": sum(cl.ns)}
     for p in plans:
@@ -125,7 +129,7 @@ def vgg_check(N, report):
 
 
 def main():
-    Ns = [int(x) for x in sys.argv[1:]] or [2, 3, 5, 8]
+    Ns = [int(x) for x in sys.argv[1:]] or [2, 3, 4, 5, 8]
     report = {"device": torch.cuda.get_device_name(0), "checks": {},
               "CUDA_DEVICE_MAX_CONNECTIONS": os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS"),
               "CUDA_MODULE_LOADING": os.environ.get("CUDA_MODULE_LOADING")}
@@ -134,6 +138,8 @@ def main():
     for N in Ns:
         if N >= 5:
             vgg_check(N, report)
+        if N in (4, 8):  # the fused exchange with radix-3 wire codes at full size
+            vgg_check(N, report, shard="0")
     ok = all(v["workers_identical"] and v["matches_reference"] for v in report["checks"].values())
     report["ok"] = ok
     print(json.dumps(report), flush=True)

@@ -84,7 +84,8 @@ def main():
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         ms = float(ms[0])
         w = (0.5 if ws <= 7 else 1.0) if mode == "sharded" else 0.0
-        B = 12.5 if ws == 1 else (12.5 + 2 * w if mode == "sharded" else 12.0 + 0.5 * ws)
+        B = 12.5 if ws == 1 else (12.5 + 2 * w if mode == "sharded" else
+                                  12.25 + 0.4 * ws if mode == "fused-r3" else 12.0 + 0.5 * ws)
         gbs = n * B / (ms * 1e-3) / 1e9
         row = {"log2_n": lg, "n": n, "n_gpus": ws, "exchange": mode, "steps": K,
                "us_per_step": ms * 1e3, "aggregate_elem_per_s": ws * n / (ms * 1e-3),
