@@ -165,6 +165,11 @@ struct tgb_plan {
     bool bound = false;
     int32_t k2_variant = 0;  // TGB_K2V
     int32_t k2_direct = 0;   // TGB_K2DIRECT: K2 stores codes from registers during the loop
+    // K2 code stores as TMA bulk copies (cp.async.bulk smem -> local / peer global),
+    // default; TGB_K2BULK=0 = 16-B SM stores. N=4 0.384 vs 0.408 ms, N=1/2 neutral
+    // (profiles/r01_k2bulk_ab.json): the CTA hands its 8 KB of codes per destination
+    // to the TMA engine instead of issuing 512 x 16-B stores per destination
+    int32_t k2_bulk = 1;
     int32_t k1_variant = 0;  // TGB_K1V
     int32_t k3_variant = 2;  // TGB_K3V: 2 staged + SWAR sums + register LUT (default), 1 staged + tables, 0 byte loads
     // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
@@ -299,6 +304,7 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     P->p = *params;
     if (const char* m = std::getenv("TGB_K2V")) P->k2_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K2DIRECT")) P->k2_direct = std::atoi(m);
+    if (const char* m = std::getenv("TGB_K2BULK")) P->k2_bulk = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
     if (const char* m = std::getenv("TGB_K3V")) P->k3_variant = std::atoi(m);
     P->worker = worker;
@@ -328,9 +334,15 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
         if (const char* m = std::getenv("TGB_SHARD")) shard = shard && std::atoi(m) != 0;
         const char* pm = std::getenv("TGB_PIPE");
         const bool pipe = pm && std::atoi(pm) != 0 && !shard;
+        // opt-in (TGB_R3=1): measured slower on 4 B200s (VGG-16 N=4 0.453 vs 0.409 ms,
+        // N=3 0.445 vs 0.343; profiles/r01_r3_ab.json). K2 did not get faster with 20 %
+        // fewer NVLink bytes (212 vs 215 us: K2 at N = 4 is not link-bandwidth bound),
+        // the radix decode costs more ALU than the 2-bit SWAR one (K3 165 vs 124 us) and
+        // 80-element work items leave K1 a scalar tail per chunk (138 vs 125 us).
         bool want = n_workers >= 3 && n_workers <= kMaxPeers && params->scaler_sharing &&
                     !any_pass && !shard && !pipe;
-        if (const char* m = std::getenv("TGB_R3")) want = want && std::atoi(m) != 0;
+        const char* rm = std::getenv("TGB_R3");
+        want = want && rm && std::atoi(rm) != 0;
         P->r3_capable = want;
         if (want) {  // work items at multiples of 80 elements (16-B aligned radix bytes)
             chunk = chunk / 80 * 80;
@@ -826,6 +838,7 @@ static tgb_status launch_tern_rng(tgb_plan* P, int g, uint32_t cb, uint32_t cc, 
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
     k.direct = P->k2_direct;
+    k.bulk = P->k2_bulk;
     k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
     if (fuse_decode && P->opt_active) {
         k.optd = P->d_optd;

@@ -193,6 +193,7 @@ struct K2Args {
     float s_imm;         // per-layer API: scaler by value (slots == nullptr)
     uint64_t rng_base;   // per-layer API: ternarize rng_base (codec.hpp:148); plan: 0
     PeerPush dst;        // plan: code destinations (n == 0: just `push`)
+    int32_t bulk = 0;           // K2 code stores as TMA bulk copies (TGB_K2BULK, A/B)
     int32_t shard_n = 0;        // sharded exchange: ranks; chunk b belongs to rank r with
     uint32_t shard_bounds[kMaxPeers + 1];  // shard_bounds[r] <= b < shard_bounds[r + 1]
     unsigned long long* nnz = nullptr;     // telemetry: += nonzero codes (cluster.hpp:336-346)
@@ -631,7 +632,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     // No fence after the peer stores: the step barrier kernel runs after this
     // grid completes in stream order, and grid completion implies its (peer)
     // stores are performed -- the guarantee event-based multi-GPU sync relies on.
-    if (nbytes) k2_store_chunk(a, L, ch, b, stage, nbytes, streamed);
+    if (!nbytes) return;
+    if (a.bulk && streamed == 0) {
+        // one thread hands the staged codes to the TMA engine (cp.async.bulk smem ->
+        // global, peers included); the 16-B-multiple head goes in bulk, a ragged tail
+        // with plain stores. Full completion is awaited before the CTA retires so the
+        // step barrier's grid-completion ordering still covers these writes.
+        const uint64_t off = L.code_off + (ch.begin >> 2);
+        int p0, p1;
+        k2_dst_range(a, b, p0, p1);
+        const uint32_t head = nbytes & ~15u;
+        bool aligned = true;
+        for (int p = p0; p < p1; ++p)
+            aligned &= ((reinterpret_cast<uintptr_t>(k2_dst(a, p) + off) & 15u) == 0);
+        if (aligned && head) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+                for (int p = p0; p < p1; ++p)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     k2_dst(a, p) + off),
+                                 "r"(sa), "r"(head)
+                                 : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            for (int p = p0; p < p1; ++p)
+                for (uint32_t i = head + threadIdx.x; i < nbytes; i += kThreads)
+                    k2_dst(a, p)[off + i] = stage[i];
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            return;
+        }
+    }
+    k2_store_chunk(a, L, ch, b, stage, nbytes, streamed);
 }
 
 // ====================================================================== K3
@@ -1782,6 +1814,7 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     if (n_chunks == 0) return cudaSuccess;
     K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0, p.dst};
     a.nnz = p.nnz;
+    a.bulk = p.bulk;
     a.shard_n = p.shard_n;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};

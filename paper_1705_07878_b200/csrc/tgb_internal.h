@@ -50,6 +50,7 @@ struct K2Launch {
     uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
     int32_t direct = 0;         // thread-contiguous code bytes stored straight from registers
+    int32_t bulk = 0;           // TGB_K2BULK (A/B): code stores as TMA bulk copies
     int32_t r3 = 0;             // fused exchange: radix-3 wire codes to dst, 2-bit codes to push
 };
 

@@ -10,11 +10,12 @@ barriers and K3 / K3a+K3b kernels as the multi-process path, minus NVLink.
 
 Checks per N (default 2 3 4 5 8):
   * small tensor set x REF configs (shared/unshared, Global, FixedSize +
-    passthrough), default schedule and forced fused (TGB_SHARD=0): every worker
+    passthrough), default schedule, forced fused (TGB_SHARD=0) and fused with
+    radix-3 wire codes (TGB_R3=1, N >= 3): every worker
     holds bit-identical output equal to the reference's own average over the
     same N workers (oracle/_ref, codec.hpp:245-311);
   * full VGG-16 set at N = 8 (sharded, 8-bit sums), N = 5 (4-bit sums), and the
-    fused exchange with radix-3 wire codes at N = 4 and 8 (TGB_SHARD=0):
+    fused exchange with 2-bit and radix-3 wire codes at N = 4 and 8:
     bit-identical on every worker and equal to K3 over the N unattached push
     areas laid out back to back (the NCCL-allgather path, itself pinned to
     the reference on the golden cases).
@@ -55,14 +56,17 @@ def small_checks(N, report):
     P, G, F = tg.Bucketing.PerTensor, tg.Bucketing.Global, tg.Bucketing.FixedSize
     configs = [(True, P, 0, ()), (False, P, 0, ()), (True, G, 0, ()),
                (True, F, 1000, ("conv1.bias",)), (False, F, 7, ("fc.bias",))]
-    for shard in ("default", "0"):
+    for shard in ("default", "0", "0+r3"):
         for sharing, bucketing, k, pt_names in configs:
-            if shard == "0":
+            if shard != "default":
                 os.environ["TGB_SHARD"] = "0"
+            if shard == "0+r3":
+                os.environ["TGB_R3"] = "1"
             cfg = tg.CodecConfig(seed=42, scaler_sharing=sharing, bucketing=bucketing,
                                  bucket_size=k, passthrough=set(pt_names))
             cl = tg.LocalCluster(names, [[n] for n in sizes], cfg, N, DEV)
             os.environ.pop("TGB_SHARD", None)
+            os.environ.pop("TGB_R3", None)
             grads = [[R.normal(100 + w, 0, "mp/" + n, m, 1e-2) for n, m in zip(names, sizes)]
                      for w in range(N)]
             for w in range(N):
@@ -90,10 +94,13 @@ def vgg_check(N, report, shard="default"):
     layers = tg.layersets.get("vgg16")
     names, shapes = [n for n, _ in layers], [s for _, s in layers]
     cfg = tg.CodecConfig(seed=42)
-    if shard == "0":
+    if shard != "default":
         os.environ["TGB_SHARD"] = "0"
+    if shard == "0+r3":
+        os.environ["TGB_R3"] = "1"
     cl = tg.LocalCluster(names, shapes, cfg, N, DEV)
     os.environ.pop("TGB_SHARD", None)
+    os.environ.pop("TGB_R3", None)
     for w in range(N):
         g = torch.Generator(device=DEV).manual_seed(1000 + w)
         cl.grad_flat[w].normal_(0.0, 1e-3, generator=g)
@@ -138,8 +145,9 @@ def main():
     for N in Ns:
         if N >= 5:
             vgg_check(N, report)
-        if N in (4, 8):  # the fused exchange with radix-3 wire codes at full size
+        if N in (4, 8):  # the fused exchange at full size, 2-bit and radix-3 wire codes
             vgg_check(N, report, shard="0")
+            vgg_check(N, report, shard="0+r3")
     ok = all(v["workers_identical"] and v["matches_reference"] for v in report["checks"].values())
     report["ok"] = ok
     print(json.dumps(report), flush=True)
