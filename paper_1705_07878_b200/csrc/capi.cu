@@ -945,6 +945,7 @@ static ShardLaunch shard_launch(const tgb_plan* P) {
     k.nib = P->nib;
     k.inv_n = 1.0f / static_cast<float>(P->n_workers);
     k.err = P->d_err;
+    k.bulk = P->k2_bulk;
     return k;
 }
 

@@ -249,6 +249,36 @@ __device__ __forceinline__ void copy_out(const uint8_t* stage, uint8_t* dst, uin
     }
 }
 
+// The staged bytes to n_dst global destinations (local or peer memory) with the
+// TMA engine: one thread issues a cp.async.bulk per destination for the 16-B
+// multiple head, the CTA stores a ragged tail; full completion is awaited before
+// the CTA retires, so grid completion still orders these writes before a later
+// kernel (the step barrier). Falls back to copy_out for misaligned destinations.
+// Call with the staged bytes complete (after a CTA barrier).
+template <class DstF>
+__device__ __forceinline__ void bulk_copy_out(const uint8_t* stage, DstF dst, int n_dst,
+                                              uint32_t nbytes) {
+    const uint32_t head = nbytes & ~15u;
+    bool aligned = head != 0 && (reinterpret_cast<uintptr_t>(stage) & 15u) == 0;
+    for (int p = 0; p < n_dst; ++p) aligned &= ((reinterpret_cast<uintptr_t>(dst(p)) & 15u) == 0);
+    if (!aligned) {
+        for (int p = 0; p < n_dst; ++p) copy_out(stage, dst(p), nbytes);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+        for (int p = 0; p < n_dst; ++p)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst(p)),
+                         "r"(sa), "r"(head)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    for (int p = 0; p < n_dst; ++p)
+        for (uint32_t i = head + threadIdx.x; i < nbytes; i += kThreads) dst(p)[i] = stage[i];
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Passthrough block (codec.hpp:206-209, 221-224): the raw fp32 values go to
 // the block's region of every destination; the finite check of encode_step
 // (:204) runs here since K1 never sees these blocks. N == 1 (kFuse): the
@@ -633,35 +663,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     // grid completes in stream order, and grid completion implies its (peer)
     // stores are performed -- the guarantee event-based multi-GPU sync relies on.
     if (!nbytes) return;
-    if (a.bulk && streamed == 0) {
-        // one thread hands the staged codes to the TMA engine (cp.async.bulk smem ->
-        // global, peers included); the 16-B-multiple head goes in bulk, a ragged tail
-        // with plain stores. Full completion is awaited before the CTA retires so the
-        // step barrier's grid-completion ordering still covers these writes.
+    if (a.bulk && streamed == 0) {  // the codes to every destination via the TMA engine
         const uint64_t off = L.code_off + (ch.begin >> 2);
         int p0, p1;
         k2_dst_range(a, b, p0, p1);
-        const uint32_t head = nbytes & ~15u;
-        bool aligned = true;
-        for (int p = p0; p < p1; ++p)
-            aligned &= ((reinterpret_cast<uintptr_t>(k2_dst(a, p) + off) & 15u) == 0);
-        if (aligned && head) {
-            if (threadIdx.x == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-                for (int p = p0; p < p1; ++p)
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                                     k2_dst(a, p) + off),
-                                 "r"(sa), "r"(head)
-                                 : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            for (int p = p0; p < p1; ++p)
-                for (uint32_t i = head + threadIdx.x; i < nbytes; i += kThreads)
-                    k2_dst(a, p)[off + i] = stage[i];
-            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-            return;
-        }
+        bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
+        return;
     }
     k2_store_chunk(a, L, ch, b, stage, nbytes, streamed);
 }
@@ -1417,6 +1424,7 @@ struct ShardArgs {
     int32_t nib;                   // 4-bit sums (N <= 7), else 8-bit
     float inv_n;
     ErrWord* err;
+    int32_t bulk = 0;  // K3a: packed sums to every rank as TMA bulk copies
 };
 
 __device__ __forceinline__ uint32_t pack_nib(uint32_t acc) {  // 4 byte lanes -> 4 nibbles
@@ -1643,9 +1651,13 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
     __syncthreads();
     const uint32_t sbytes = nbytes * (a.nib ? 2u : 4u);
     const uint64_t doff = soff + (a.nib ? (ch.begin >> 1) : ch.begin);
+    if (a.bulk)
+        bulk_copy_out(reinterpret_cast<const uint8_t*>(stage), [&](int p) { return a.sums[p] + doff; },
+                      NW, sbytes);
+    else
 #pragma unroll
-    for (int p = 0; p < NW; ++p)
-        copy_out(reinterpret_cast<const uint8_t*>(stage), a.sums[p] + doff, sbytes);
+        for (int p = 0; p < NW; ++p)
+            copy_out(reinterpret_cast<const uint8_t*>(stage), a.sums[p] + doff, sbytes);
     if (bad & 0x55555555u) {  // rare: locate the chunk's first corrupt element
         for (uint32_t q = 0; q < nbytes; ++q) {
             for (int w = 0; w < NW; ++w) {
@@ -1983,7 +1995,7 @@ cudaError_t launch_average_raw(int32_t n_workers, const float* const* vals, uint
 cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
                              cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
-    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err};
+    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err, p.bulk};
     for (int r = 0; r < p.n_workers; ++r) a.sums[r] = p.sums[r];
     const TableSource src{chunks};
     switch (p.n_workers) {
@@ -2002,7 +2014,7 @@ cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const Sh
 cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
                              cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
-    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err};
+    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err, p.bulk};
     const TableSource src{chunks};
     if (p.nib)
         k3_expand<true><<<n_chunks, kThreads, 0, st>>>(src, a);

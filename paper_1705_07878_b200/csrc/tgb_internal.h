@@ -78,6 +78,7 @@ struct ShardLaunch {
     int32_t nib;
     float inv_n;
     ErrWord* err;
+    int32_t bulk = 0;  // K3a sums stores as TMA bulk copies
 };
 
 struct PipeLaunch {
