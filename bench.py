@@ -561,8 +561,7 @@ def run_b200(args):
                                   "ms_per_step is tgb_step (two-group overlap, N=1 fused decode)"},
             "kernels_sequential": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
-            "gpu_launches": (sum(1 for r in live if r["kernel"] != "nccl") if live
-                             else launches_per_step * K),
+            "gpu_launches": launches_per_step * K,
             "gpu_launches_note": "own kernels per tgb_step and layer group: N=1 K1 + K2 (K2 "
                                  "also decodes); pipelined K1 + K23; fused K1 + K2 + peer barrier "
                                  "+ K3; sharded K1 + K2 + barrier + K3a (owner sums) + barrier + "
