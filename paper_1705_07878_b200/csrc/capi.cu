@@ -171,6 +171,10 @@ struct tgb_plan {
     // to the TMA engine instead of issuing 512 x 16-B stores per destination
     int32_t k2_bulk = 1;
     int32_t k1_variant = 0;  // TGB_K1V
+    int32_t pdl = 0;         // TGB_PDL (A/B)
+    // K1's last 24 MB per launch loaded L2 evict_last for K2's reverse walk (TGB_K1KEEP=MB;
+    // tools/l2keep_ab.py: N=1 step -4.6 us with or without an L2 flush between steps)
+    uint32_t k1_keep = 24u * (1u << 20) / (4u * kChunk12);
     int32_t k3_variant = 2;  // TGB_K3V: 2 staged + SWAR sums + register LUT (default), 1 staged + tables, 0 byte loads
     // sharded exchange (attached, N >= TGB_SHARD_MIN, shared scalers): rank r owns
     // K2 chunks [cs[r], cs[r+1]) and reduces them to packed sums for every rank.
@@ -306,7 +310,11 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
     if (const char* m = std::getenv("TGB_K2DIRECT")) P->k2_direct = std::atoi(m);
     if (const char* m = std::getenv("TGB_K2BULK")) P->k2_bulk = std::atoi(m);
     if (const char* m = std::getenv("TGB_K1V")) P->k1_variant = std::atoi(m);
+    if (n_workers > 1) P->k1_keep = 0;  // N = 2: K3 -8 us slower (evict_last lines linger)
+    if (const char* m = std::getenv("TGB_K1KEEP"))
+        P->k1_keep = static_cast<uint32_t>(std::max(0, std::atoi(m))) * (1u << 20) / (4u * kChunk12);
     if (const char* m = std::getenv("TGB_K3V")) P->k3_variant = std::atoi(m);
+    if (const char* m = std::getenv("TGB_PDL")) P->pdl = std::atoi(m);
     P->worker = worker;
     P->n_workers = n_workers;
     P->desc.assign(layers, layers + n_layers);
@@ -444,6 +452,10 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                 layers[big].n * 100 <= P->total * 95;
     if (const char* m = std::getenv("TGB_GROUPS")) want = want && std::atoi(m) != 0;
     P->grouped = want;
+    // K2 as K1's programmatic dependent with an L2 prefetch of its chunk (tools/env_ab.py):
+    // a single-stream N = 1 step gains (GoogLeNet 31.9 -> 29.0 us); with two concurrent
+    // groups the waiting K2 CTAs hold SM slots the other group's K1 needs (VGG-16 +10 %)
+    if (!std::getenv("TGB_PDL")) P->pdl = (!P->grouped && n_workers == 1) ? 2 : 0;
     auto group_of = [&](const ChunkDev& c) {
         return (P->grouped && P->h_layers[c.layer].tensor == static_cast<uint32_t>(big)) ? 1u : 0u;
     };
@@ -820,6 +832,7 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
         k.push.remote = 1;
     }
     k.variant = P->k1_variant;
+    k.keep_chunks = P->k1_keep;
     k.tensors = P->d_tensors;
     k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
     const int ts = t_begin(P, st);
@@ -845,6 +858,7 @@ static tgb_status launch_tern_rng(tgb_plan* P, int g, uint32_t cb, uint32_t cc, 
         k.opt = *P->opt_active;
     }
     k.variant = P->k2_variant;
+    k.pdl = P->pdl;
     if (P->attached) {  // fused exchange: codes stored into every rank's gather buffer
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
         k.dst.n = P->n_workers;

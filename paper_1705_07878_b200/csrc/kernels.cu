@@ -56,8 +56,27 @@ __device__ __forceinline__ uint64_t block_rng_base(const LayerDev& L) {
 // One CTA per work item (a chunk of one block); the tensor's last arriving CTA
 // merges the tensor's partials (tgb_stats.cuh). Passthrough blocks have no
 // statistics (codec.hpp:206-209) and are never in a K1 grid.
-template <class Src, int U = 8, int A = 1, int kMinBlocks = 1>
+// kHint: loads carry an L2 policy instead of .cs: evict_last for the launch's
+// last units (K2 walks chunks last-to-first and re-reads them from L2),
+// evict_first elsewhere (TGB_K1KEEP, A/B).
+template <bool kHint>
+__device__ __forceinline__ float4 k1_ld4(const float4* p, uint64_t pol) {
+    if constexpr (kHint) {
+        float4 v;
+        asm("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+            : "l"(p), "l"(pol));
+        return v;
+    } else {
+        return __ldcs(p);
+    }
+}
+
+template <class Src, int U = 8, int A = 1, int kMinBlocks = 1, bool kHint = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out o) {
+    // K2 (a programmatic dependent, TGB_PDL) may be scheduled once every K1 CTA has
+    // started; it waits on griddepcontrol.wait for K1's completion before reading scalers
+    asm volatile("griddepcontrol.launch_dependents;");
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
@@ -72,6 +91,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
     for (int k = 0; k < A; ++k) S[k] = Q[k] = 0.0;
     const uint32_t tid = threadIdx.x;
     uint32_t done = 0;
+    uint64_t pol = 0;
+    if constexpr (kHint) {
+        if (blockIdx.x >= o.keep_from)
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        else
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    }
     if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         const uint32_t n4 = count >> 2;
@@ -79,11 +105,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
         for (; i + (U - 1) * kThreads < n4; i += U * kThreads) {  // U x 16 B in flight per thread
             float4 v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + i + u * kThreads);
+            for (int u = 0; u < U; ++u) v[u] = k1_ld4<kHint>(g4 + i + u * kThreads, pol);
 #pragma unroll
             for (int u = 0; u < U; ++u) acc4(v[u], x0, S[u % A], Q[u % A], mx);
         }
-        for (; i < n4; i += kThreads) acc4(__ldcs(g4 + i), x0, S[0], Q[0], mx);
+        for (; i < n4; i += kThreads) acc4(k1_ld4<kHint>(g4 + i, pol), x0, S[0], Q[0], mx);
         done = n4 << 2;
     }
     for (uint32_t i = done + tid; i < count; i += kThreads) acc1(__ldcs(g + i), x0, S[0], Q[0], mx);
@@ -199,6 +225,7 @@ struct K2Args {
     unsigned long long* nnz = nullptr;     // telemetry: += nonzero codes (cluster.hpp:336-346)
     const OptDev* optd = nullptr;          // fused optimizer (kOpt kernels): per-block state
     OptArgs opt{};
+    int32_t pdl = 0;  // launched as K1's programmatic dependent: 1 wait, 2 prefetch + wait
 };
 
 // nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
@@ -646,6 +673,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     ChunkDev ch;
     LayerDev L;
     src.get(b, ch, L);
+    if (a.pdl) {  // resident while K1 drains; nothing K1 writes is read before the wait
+        if (a.pdl == 2 && threadIdx.x == 0 && (L.flags & kLayerVecIn)) {
+            const uint32_t bytes = (ch.count * 4u) & ~15u;  // warm L2 with the chunk's gradient
+            if (bytes)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(L.g + ch.begin),
+                             "r"(bytes)
+                             : "memory");
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     uint32_t streamed = 0;
     if (kR3) r3_build_lut(lut10);  // visible after k2_code_chunk's closing barrier
     const uint32_t nbytes = k2_code_chunk<kRolling, U, kFuse, NoHook, kOpt, kDirect>(
@@ -1781,6 +1818,11 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
             p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors, p.nnz};
     const TableSource src{chunks};
+    if (p.keep_chunks && p.variant == 0) {  // TGB_K1KEEP (A/B): tail units stay in L2 for K2's reverse walk
+        o.keep_from = n_chunks - (p.keep_chunks < n_chunks ? p.keep_chunks : n_chunks);
+        k1_stats<TableSource, 8, 1, 4, true><<<n_chunks, kThreads, 0, st>>>(src, o);
+        return launch_status();
+    }
     switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
         case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
         case 2: k1_stats<TableSource, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
@@ -1821,6 +1863,24 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
     return launch_status();
 }
 
+// K2 launch; with a.pdl it is K1's programmatic dependent (same stream, launched
+// while K1's last wave drains; the kernel's griddepcontrol.wait orders it after K1)
+template <class Kern>
+static void k2_go(Kern k, uint32_t grid, cudaStream_t st, const TableSource& src,
+                  const K2Args& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, k, src, a);
+}
+
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
@@ -1828,11 +1888,11 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     a.nnz = p.nnz;
     a.bulk = p.bulk;
     a.shard_n = p.shard_n;
+    a.pdl = p.pdl;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
     if (p.r3) {  // fused exchange with radix-3 wire codes (N >= 3)
-        k2_ternarize<TableSource, false, 4, 3, false, false, false, true>
-            <<<n_chunks, kThreads, 0, st>>>(src, a);
+        k2_go(k2_ternarize<TableSource, false, 4, 3, false, false, false, true>, n_chunks, st, src, a);
         return launch_status();
     }
     if (p.fuse_decode) {
@@ -1840,34 +1900,34 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
             a.optd = p.optd;
             a.opt = p.opt;
             if (p.direct)
-                k2_ternarize<TableSource, false, 4, 3, true, true, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+                k2_go(k2_ternarize<TableSource, false, 4, 3, true, true, true>, n_chunks, st, src, a);
             else
-                k2_ternarize<TableSource, false, 4, 3, true, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+                k2_go(k2_ternarize<TableSource, false, 4, 3, true, true>, n_chunks, st, src, a);
         } else if (p.direct) {
-            k2_ternarize<TableSource, false, 4, 3, true, false, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+            k2_go(k2_ternarize<TableSource, false, 4, 3, true, false, true>, n_chunks, st, src, a);
         } else {
             switch (p.variant) {  // TGB_K2V (A/B): key schedule x occupancy x bytes per thread
-                case 1: k2_ternarize<TableSource, true, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-                case 2: k2_ternarize<TableSource, true, 4, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-                case 4: k2_ternarize<TableSource, false, 4, 3, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-                case 5: k2_ternarize<TableSource, false, 2, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-                case 6: k2_ternarize<TableSource, false, 4, 5, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                case 1: k2_go(k2_ternarize<TableSource, true, 4, 3, true>, n_chunks, st, src, a); break;
+                case 2: k2_go(k2_ternarize<TableSource, true, 4, 4, true>, n_chunks, st, src, a); break;
+                case 4: k2_go(k2_ternarize<TableSource, false, 4, 3, true>, n_chunks, st, src, a); break;
+                case 5: k2_go(k2_ternarize<TableSource, false, 2, 4, true>, n_chunks, st, src, a); break;
+                case 6: k2_go(k2_ternarize<TableSource, false, 4, 5, true>, n_chunks, st, src, a); break;
                 // default (= 3): 64 registers, 4 CTAs/SM: 190.9 vs 202.9 us at 3 CTAs/SM
                 // (VGG-16, N = 1, tools/k2_fused_ab.sh): the fused kernel is latency-bound
-                default: k2_ternarize<TableSource, false, 4, 4, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+                default: k2_go(k2_ternarize<TableSource, false, 4, 4, true>, n_chunks, st, src, a); break;
             }
         }
         return launch_status();
     }
     if (p.direct) {
-        k2_ternarize<TableSource, false, 4, 3, false, false, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+        k2_go(k2_ternarize<TableSource, false, 4, 3, false, false, true>, n_chunks, st, src, a);
         return launch_status();
     }
     switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
-        case 1: k2_ternarize<TableSource, true, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 2: k2_ternarize<TableSource, true, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 3: k2_ternarize<TableSource, false, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        default: k2_ternarize<TableSource, false, 4, 3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 1: k2_go(k2_ternarize<TableSource, true, 4, 3>, n_chunks, st, src, a); break;
+        case 2: k2_go(k2_ternarize<TableSource, true, 4, 4>, n_chunks, st, src, a); break;
+        case 3: k2_go(k2_ternarize<TableSource, false, 4, 4>, n_chunks, st, src, a); break;
+        default: k2_go(k2_ternarize<TableSource, false, 4, 3>, n_chunks, st, src, a); break;
     }
     return launch_status();
 }

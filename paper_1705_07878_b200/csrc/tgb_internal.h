@@ -30,6 +30,7 @@ struct K1Launch {
     PeerPush push{};      // scaler slot destinations
     const TensorDev* tensors = nullptr;  // plan: tensor table (per-tensor finalize)
     unsigned long long* nnz = nullptr;   // telemetry counter to reset (this group)
+    uint32_t keep_chunks = 0;            // TGB_K1KEEP: last units kept in L2 for K2 (A/B)
 };
 
 struct K2Launch {
@@ -52,6 +53,7 @@ struct K2Launch {
     int32_t direct = 0;         // thread-contiguous code bytes stored straight from registers
     int32_t bulk = 0;           // TGB_K2BULK (A/B): code stores as TMA bulk copies
     int32_t r3 = 0;             // fused exchange: radix-3 wire codes to dst, 2-bit codes to push
+    int32_t pdl = 0;            // TGB_PDL: K2 as K1's programmatic dependent (1), + L2 prefetch (2)
 };
 
 struct K3Launch {

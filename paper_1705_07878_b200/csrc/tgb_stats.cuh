@@ -27,6 +27,7 @@ struct K1Out {
     PeerPush push;            // scaler slot destinations (n == 0: slots only)
     const TensorDev* tensors; // plan only; nullptr = single-block single-layer API
     unsigned long long* nnz = nullptr;  // telemetry counter of this group (reset by block 0)
+    uint32_t keep_from = ~0u;  // units >= keep_from load with L2 evict_last (K2 re-reads them)
 };
 
 __device__ __forceinline__ void put_slot(const K1Out& o, int32_t slot, float v) {
