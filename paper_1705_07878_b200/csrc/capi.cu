@@ -452,10 +452,15 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
                 layers[big].n * 100 <= P->total * 95;
     if (const char* m = std::getenv("TGB_GROUPS")) want = want && std::atoi(m) != 0;
     P->grouped = want;
-    // K2 as K1's programmatic dependent with an L2 prefetch of its chunk (tools/env_ab.py):
-    // a single-stream N = 1 step gains (GoogLeNet 31.9 -> 29.0 us); with two concurrent
-    // groups the waiting K2 CTAs hold SM slots the other group's K1 needs (VGG-16 +10 %)
-    if (!std::getenv("TGB_PDL")) P->pdl = (!P->grouped && n_workers == 1) ? 2 : 0;
+    // K2 as K1's programmatic dependent on single-stream N = 1 plans (tools/env_ab.py,
+    // profiles/r01_pdl_l2keep_ab.log): GoogLeNet 31.9 -> 29.1 us with a whole-chunk L2
+    // prefetch before the wait, a 2^24 layer 49.6 -> 46.5 us without one, 2^26 / 2^28
+    // layers 155 -> 149 / 546 -> 538 us prefetching the first 32 KB (a whole-chunk
+    // prefetch re-reads evicted lines there: 159 / 575 us). With two concurrent groups the
+    // waiting K2 CTAs hold SM slots the other group's K1 needs (VGG-16 +10 %): off.
+    if (!std::getenv("TGB_PDL"))
+        P->pdl = (P->grouped || n_workers > 1) ? 0
+                 : P->total <= (8ull << 20) ? 2 : P->total >= (48ull << 20) ? 3 : 1;
     auto group_of = [&](const ChunkDev& c) {
         return (P->grouped && P->h_layers[c.layer].tensor == static_cast<uint32_t>(big)) ? 1u : 0u;
     };

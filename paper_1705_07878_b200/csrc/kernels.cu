@@ -225,7 +225,7 @@ struct K2Args {
     unsigned long long* nnz = nullptr;     // telemetry: += nonzero codes (cluster.hpp:336-346)
     const OptDev* optd = nullptr;          // fused optimizer (kOpt kernels): per-block state
     OptArgs opt{};
-    int32_t pdl = 0;  // launched as K1's programmatic dependent: 1 wait, 2 prefetch + wait
+    int32_t pdl = 0;  // launched as K1's programmatic dependent: 1 wait, 2/3 prefetch + wait
 };
 
 // nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
@@ -674,8 +674,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     LayerDev L;
     src.get(b, ch, L);
     if (a.pdl) {  // resident while K1 drains; nothing K1 writes is read before the wait
-        if (a.pdl == 2 && threadIdx.x == 0 && (L.flags & kLayerVecIn)) {
-            const uint32_t bytes = (ch.count * 4u) & ~15u;  // warm L2 with the chunk's gradient
+        if (a.pdl >= 2 && threadIdx.x == 0 && (L.flags & kLayerVecIn)) {
+            // warm L2 with the chunk's gradient (3: only its first 32 KB)
+            const uint32_t bytes = min((ch.count * 4u) & ~15u, a.pdl == 3 ? 32768u : ~0u);
             if (bytes)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(L.g + ch.begin),
                              "r"(bytes)

@@ -5,7 +5,7 @@ Each mode is "VAR=V[,VAR2=V2...][:flush]" ("-" = defaults); flush=1 writes a
 alone with CUDA events on the caller's stream; interleaved rounds, medians;
 outputs compared bit-for-bit across modes.
 
-    python tools/env_ab.py WORKLOAD MODE...
+    python tools/env_ab.py WORKLOAD MODE...     (WORKLOAD: a layer set or layer:N)
 """
 import os
 import statistics
@@ -20,7 +20,7 @@ import paper_1705_07878_b200 as tg  # noqa: E402
 wl = sys.argv[1]
 modes = sys.argv[2:]
 dev = torch.device("cuda", 0)
-layers = tg.layersets.get(wl)
+layers = [("layer", [int(wl[6:])])] if wl.startswith("layer:") else tg.layersets.get(wl)
 ws = {}
 for m in modes:
     envs = m.split(":")[0]
