@@ -152,27 +152,21 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
                 put_slot(o, o.layers[T.first_block].slot, s_bad ? 0.0f : fminf(smx[0], s_bound));
             }
         } else {
-            // FixedSize buckets: scatter each unit's max into its block (partial.block),
-            // kWin blocks per pass; |x| >= 0 so float order == int order
-            constexpr uint32_t kWin = 2048;
-            __shared__ int wmax[kWin];
-            for (uint32_t w0 = 0; w0 < T.n_blocks; w0 += kWin) {
-                const uint32_t nw = min(kWin, T.n_blocks - w0);
-                for (uint32_t i = tid; i < nw; i += kThreads) wmax[i] = 0;
-                Bar::sync();
-                for (uint32_t c = tid; c < nc; c += kThreads) {
-                    const Partial* pp = o.partials + first_unit + c;
-                    const uint32_t b = __ldcg(&pp->block) - T.first_block - w0;
-                    if (b < nw) atomicMax(&wmax[b], __float_as_int(__ldcg(&pp->mx)));
-                }
-                Bar::sync();
-                for (uint32_t i = tid; i < nw; i += kThreads) {
-                    const uint32_t b = T.first_block + w0 + i;
-                    o.bounds[b] = s_bound;
-                    put_slot(o, o.layers[b].slot,
-                             s_bad ? 0.0f : fminf(__int_as_float(wmax[i]), s_bound));
-                }
-                Bar::sync();
+            // FixedSize buckets: a tensor's units are stored in block order and never
+            // straddle a block, so every block is a contiguous run of units. The unit
+            // that opens a run merges the run's maxima and writes the block's bound and
+            // scaler: one O(units) pass spread over the CTA (the earlier windowed scan
+            // re-read every unit once per 2048 blocks, O(units x blocks); VGG-16 at
+            // k = 256: K1 26.1 ms, tools/fixed_probe.py)
+            for (uint32_t c = tid; c < nc; c += kThreads) {
+                const Partial* pp = o.partials + first_unit + c;
+                const uint32_t b = __ldcg(&pp->block);
+                if (c > 0 && __ldcg(&pp[-1].block) == b) continue;
+                float bm = __ldcg(&pp->mx);
+                for (uint32_t d = c + 1; d < nc && __ldcg(&pp[d - c].block) == b; ++d)
+                    bm = fmaxf(bm, __ldcg(&pp[d - c].mx));
+                o.bounds[b] = s_bound;
+                put_slot(o, o.layers[b].slot, s_bad ? 0.0f : fminf(bm, s_bound));
             }
         }
         Bar::sync();

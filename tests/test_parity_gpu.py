@@ -334,7 +334,7 @@ def test_plan_layout_matches_host_restatement(bucketing, k, pt):
 
 
 # ------------------------------------------- FixedSize / passthrough at size
-@pytest.mark.parametrize("k", [1000, 4097, (1 << 20) + 3, 3 << 20])
+@pytest.mark.parametrize("k", [300, 1000, 4097, (1 << 20) + 3, 3 << 20])
 def test_fixed_size_large_vs_oracle(restated, k):
     names = ["fc.weight", "fc.bias", "conv.weight"]
     grads = [restated.normal(21, 0, "fx/" + n, m, 1e-3) for n, m in
