@@ -93,7 +93,28 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
     double n = 0.0, mean = 0.0, m2 = 0.0;
     float m = 0.0f;
     const uint32_t lo = tid * per, hi = min(nc, lo + per);
-    for (uint32_t c = lo; c < hi; ++c) {
+    uint32_t c = lo;
+    // many-unit tensors (FixedSize with small k): issue 8 partials' loads before
+    // merging them, in the same order (the merge chain is latency-bound otherwise)
+    constexpr uint32_t kB = 8;
+    for (; c + kB <= hi; c += kB) {
+        double bn[kB], bmean[kB], bm2[kB];
+        float bmx[kB];
+#pragma unroll
+        for (uint32_t j = 0; j < kB; ++j) {
+            const Partial* pp = o.partials + first_unit + c + j;
+            bn[j] = __ldcg(&pp->n);
+            bmean[j] = __ldcg(&pp->mean);
+            bm2[j] = __ldcg(&pp->m2);
+            bmx[j] = __ldcg(&pp->mx);
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < kB; ++j) {
+            chan_merge(n, mean, m2, bn[j], bmean[j], bm2[j]);
+            m = fmaxf(m, bmx[j]);
+        }
+    }
+    for (; c < hi; ++c) {
         const Partial* pp = o.partials + first_unit + c;
         const double pn = __ldcg(&pp->n), pmean = __ldcg(&pp->mean), pm2 = __ldcg(&pp->m2);
         const float pmx = __ldcg(&pp->mx);
@@ -158,15 +179,33 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
             // scaler: one O(units) pass spread over the CTA (the earlier windowed scan
             // re-read every unit once per 2048 blocks, O(units x blocks); VGG-16 at
             // k = 256: K1 26.1 ms, tools/fixed_probe.py)
-            for (uint32_t c = tid; c < nc; c += kThreads) {
-                const Partial* pp = o.partials + first_unit + c;
-                const uint32_t b = __ldcg(&pp->block);
-                if (c > 0 && __ldcg(&pp[-1].block) == b) continue;
-                float bm = __ldcg(&pp->mx);
-                for (uint32_t d = c + 1; d < nc && __ldcg(&pp[d - c].block) == b; ++d)
-                    bm = fmaxf(bm, __ldcg(&pp[d - c].mx));
-                o.bounds[b] = s_bound;
-                put_slot(o, o.layers[b].slot, s_bad ? 0.0f : fminf(bm, s_bound));
+            constexpr uint32_t kB = 4;  // units whose loads are issued together
+            for (uint32_t c0 = tid; c0 < nc; c0 += kB * kThreads) {
+                uint32_t bb[kB], bprev[kB], bnext[kB];
+                float bmx[kB];
+#pragma unroll
+                for (uint32_t j = 0; j < kB; ++j) {
+                    const uint32_t c = c0 + j * kThreads;
+                    const Partial* pp = o.partials + first_unit + c;
+                    bb[j] = c < nc ? __ldcg(&pp->block) : ~0u;
+                    bprev[j] = (c > 0 && c < nc) ? __ldcg(&pp[-1].block) : ~1u;
+                    bnext[j] = c + 1 < nc ? __ldcg(&pp[1].block) : ~1u;
+                    bmx[j] = c < nc ? __ldcg(&pp->mx) : 0.0f;
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < kB; ++j) {
+                    const uint32_t c = c0 + j * kThreads;
+                    const uint32_t b = bb[j];
+                    if (c >= nc || bprev[j] == b) continue;  // not the run's first unit
+                    float bm = bmx[j];
+                    if (bnext[j] == b) {  // block spans several units
+                        const Partial* pp = o.partials + first_unit + c;
+                        for (uint32_t d = c + 1; d < nc && __ldcg(&pp[d - c].block) == b; ++d)
+                            bm = fmaxf(bm, __ldcg(&pp[d - c].mx));
+                    }
+                    o.bounds[b] = s_bound;
+                    put_slot(o, o.layers[b].slot, s_bad ? 0.0f : fminf(bm, s_bound));
+                }
             }
         }
         Bar::sync();
