@@ -8,9 +8,13 @@ Gaussian gradients (sigma = 1e-3), seeded per rank. Inputs (553 MB per rank)
 are larger than L2 (126 MB), so no L2 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload vgg16|alexnet|googlenet] [--exchange auto|fused|sharded|nccl]
 
-N > 1: launched by torchrun, one process per GPU; gloo carries control
-(barriers, max-over-ranks timing), NCCL (through libtgb) carries the data.
+N > 1: one process per GPU. Under torchrun (WORLD_SIZE set) this process is one
+rank; without it, bench.py launches N ranks itself (torch.distributed.run on
+127.0.0.1) and relays rank 0's line. gloo carries control (barriers,
+max-over-ranks timing); the data moves over NVLink through libtgb (peer stores)
+or NCCL.
 """
 from __future__ import annotations
 
@@ -37,9 +41,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="vgg16", choices=["vgg16", "alexnet", "googlenet"])
+    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "sharded", "nccl"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target CPU work for the in-line cpu_baseline sample")
+                    help="CPU time budget of the in-line cpu_baseline (at least one full step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true",
@@ -118,6 +123,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def workload_config(workload, n_tensors, n, N):
+    """the `config` object of both arms' JSON lines (same workload, same keys)"""
+    return {"workload": f"{workload} full gradient set ({n_tensors} tensors, {n} fp32 "
+                        f"elements/worker), {N} worker(s), encode+sync+decode",
+            "global_batch": None, "seq_len": None, "parallelism": f"dp{N}",
+            "elements_per_worker": n,
+            "codec": "c=2.5 per-tensor clip, sharing on, REF (post-hoc max) scalers, seed 42",
+            "l2": f"inputs ({4 * n / 1e6:.0f} MB/rank) "
+                  + ("> L2 (126 MB): no flush" if 4 * n > (126 << 20) else
+                     "fit in L2 (126 MB): steps after the first read them from L2")}
+
+
 def synth_host(ns, rank, pinned=True):
     """Per-rank synthetic gradients on the host (sigma 1e-3), flat & 16B-aligned."""
     import torch
@@ -135,65 +152,68 @@ def synth_host(ns, rank, pinned=True):
 
 
 # ------------------------------------------------------------------ CPU arm
-def cpu_reference_sample(layers, n_workers, budget_s, max_steps=None, warmup=1, replicas=1):
-    """Time the reference as shipped (oracle/_ref: encode_step x N worker threads
-    -> ParameterServer::step -> decode_pull) on a bounded sample of the
-    workload: every tensor truncated to its first CAP elements. `replicas`
-    independent clusters (each N worker threads + 1 server thread, its own
-    gradients) run concurrently from Python threads (ctypes releases the GIL), so
-    the sample uses replicas x (N + 1) host threads; throughput = all replicas'
-    elements / wall time."""
+def cpu_reference_run(layers, n_workers, steps, warmup, replicas, budget_s=None):
+    """Time the reference as shipped (oracle/_ref: N worker threads encode_step +
+    push -> ParameterServer::step fold + radix-packed pull -> N decode_pull, over
+    InProcessHub; cluster.hpp:135-221, 283-297) on the FULL gradient set: every
+    step processes every element of every tensor for every worker. `replicas`
+    independent clusters (each N worker threads + 1 server thread) step
+    concurrently from Python threads (ctypes releases the GIL) so every host core
+    works; they share the input arrays (each cluster copies them). Throughput =
+    all replicas' elements / wall time. With budget_s, as many steps as fit (at
+    least one) instead of `steps`."""
     import threading as _th
 
     import numpy as np
 
     from oracle.oracle import Config, RefCluster, Reference
 
-    CAP = 1 << 20
     names = [n for n, _ in layers]
-    ns = [min(CAP, _numel(s)) for _, s in layers]
+    ns = [_numel(s) for _, s in layers]
     ref = Reference()
-    clusters = []
-    for r in range(replicas):
-        rng = np.random.default_rng(r)
-        grads = [[(rng.standard_normal(n).astype(np.float32) * np.float32(1e-3)) for n in ns]
-                 for _ in range(n_workers)]
-        clusters.append(RefCluster(ref, names, grads, Config(seed=42)))
-    for cl in clusters:
-        for t in range(warmup):
+    grads = []
+    for w in range(n_workers):
+        rng = np.random.default_rng(1000 + w)
+        grads.append([rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3) for n in ns])
+    clusters = [RefCluster(ref, names, grads, Config(seed=42)) for _ in range(replicas)]
+    del grads
+    barrier = _th.Barrier(replicas)
+
+    def run(cl, t0, k, out):
+        for t in range(t0, t0 + k):
+            barrier.wait()  # replicas step together: one step = every replica's full step
             cl.step(t)
-    steps = [0] * replicas
-    stop = [False]
+        out.append(k)
 
-    def run(i):
-        t = warmup
-        while not stop[0]:
-            clusters[i].step(t)
-            t += 1
-            steps[i] += 1
-            if max_steps is not None and steps[i] >= max_steps:
-                break
+    def go(t0, k):
+        done = []
+        threads = [_th.Thread(target=run, args=(cl, t0, k, done)) for cl in clusters]
+        w0 = time.perf_counter()
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        return time.perf_counter() - w0
 
-    threads = [_th.Thread(target=run, args=(i,)) for i in range(replicas)]
-    t0 = time.perf_counter()
-    for th in threads:
-        th.start()
-    if max_steps is None:
-        while time.perf_counter() - t0 < budget_s and any(th.is_alive() for th in threads):
-            time.sleep(0.05)
-        stop[0] = True
-    for th in threads:
-        th.join()
-    wall = time.perf_counter() - t0
+    if warmup:
+        go(0, warmup)
+    if budget_s is not None:  # one timed step, then as many more as the budget allows
+        wall = go(warmup, 1)
+        steps = 1
+        extra = int(max(0.0, budget_s - wall) // max(wall, 1e-9))
+        if extra:
+            wall += go(warmup + 1, extra)
+            steps += extra
+    else:
+        wall = go(warmup, steps)
     for cl in clusters:
         cl.close()
-    total_steps = sum(steps)
-    elems = n_workers * sum(ns) * total_steps
-    sample = (f"{len(ns)} tensors of the set, each truncated to its first {CAP} elements "
-              f"({sum(ns)} elements/worker), {n_workers} worker(s), {replicas} concurrent "
-              f"cluster replica(s) x (N worker threads + 1 server thread), {total_steps} steps "
-              f"in {wall:.1f} s")
-    return elems, wall, total_steps, sample
+    elems = replicas * n_workers * sum(ns) * steps
+    sample = (f"full {len(ns)}-tensor set ({sum(ns)} elements/worker, no truncation), "
+              f"{n_workers} worker(s); {replicas} concurrent cluster replica(s) x ({n_workers} "
+              f"worker threads + 1 server thread), each replica one full step per step; "
+              f"{steps} timed steps in {wall:.1f} s after {warmup} warm-up step(s)")
+    return elems, wall, steps, sample
 
 
 def ref_replicas(n_workers):
@@ -216,24 +236,24 @@ def run_reference(args):
 
     layers = layersets.get(args.workload)
     n_workers = max(args.gpus, ws)
+    n = sum(_numel(s) for _, s in layers)
     reps = ref_replicas(n_workers)
-    elems, wall, nsteps, sample = cpu_reference_sample(layers, n_workers, budget_s=1e9,
-                                                       max_steps=args.steps,
-                                                       warmup=max(1, min(args.warmup, 2)),
-                                                       replicas=reps)
+    elems, wall, nsteps, sample = cpu_reference_run(layers, n_workers, args.steps, args.warmup,
+                                                    reps)
     value = elems / wall
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": max(1, min(args.warmup, 2)), "ms_per_step": 1e3 * wall / args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.workload} gradient set, {n_workers} workers (sample)",
-                   "global_batch": None, "seq_len": None,
-                   "parallelism": f"dp{n_workers} (parameter server, as shipped)"},
+        "data": "synthetic (Gaussian sigma=1e-3, seeded per worker, host-generated)",
+        "impl": "reference",
+        "config": workload_config(args.workload, len(layers), n, n_workers),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": reps * (n_workers + 1),
                          "kind": "reference", "sample": sample,
                          "host_cores_available": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "path": "oracle/_ref/libtgref.so: the reference's headers compiled unmodified "
+                "(encode_step, ParameterServer::step, decode_pull over InProcessHub)",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -249,8 +269,6 @@ def run_b200(args):
 
     ws, rank, local = dist_env()
     N = ws
-    if args.gpus != ws and ws > 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -261,23 +279,21 @@ def run_b200(args):
     names = [n for n, _ in layers]
     shapes = [s for _, s in layers]
     cfg = tg.CodecConfig(seed=42)
-    fused = os.environ.get("TGB_EXCHANGE", "fused") != "nccl"
     sw = tg.SyncWorker(names, shapes, cfg, rank=rank, world_size=ws, comm=comm, device=dev,
-                       fused=fused)
+                       exchange=args.exchange)
     ns = sw.ns
     n = sum(ns)
     plan = sw.plan
-    info = tg._lib.PlanInfo()
-    tg._lib.check(tg._lib.load().tgb_plan_get_info(plan.h, tg.codec.C.byref(info)), "info")
-    mode = tg._lib.EXCHANGE_NAMES[info.exchange]
+    mode = plan.exchange
     # algorithmic HBM bytes per element per GPU:
-    #   allgather designs: B(N) = 12 + 0.5 N;
-    #   sharded: 4 (K1) + 4.25 (K2) + 0.25 (K3a codes) + 2 x sums (land + K3b read) + 4 = 12.5 + 2 w
-    sum_w = (0.5 if N <= 7 else 1.0) if mode == "sharded" else 0.0
-    #   fused-r3: 4 + 4 + 0.25 (2-bit push) + 0.2 (own radix copy) + 0.2 (N-1) landing
-    #             + 0.2 N (K3 reads) + 4 = 12.25 + 0.4 N
-    B_elem = (12.5 + 2 * sum_w if mode == "sharded" else
-              12.25 + 0.4 * N if mode == "fused-r3" else 12.0 + 0.5 * N)
+    #   N = 1 (K2 writes the decode): 4 (K1) + 4 (K2 read) + 0.25 (codes) + 4 (out) = 12.25;
+    #   fused / allgather: B(N) = 12 + 0.5 N;
+    #   sharded: 4 + 4 + 0.25 (codes land at owners) + 0.25 (K3a reads) + w (sums land)
+    #            + w (K3b reads) + 4 = 12.5 + 2 w, w = 4 / radix_m bytes (base 2N+1 digits
+    #            per u32 word: 0.4 B at N = 4, 0.57 B at N = 8)
+    radix_m = {2: 13, 3: 11, 4: 10, 5: 9, 6: 8, 7: 8, 8: 7}.get(N, 0)
+    sum_w = 4.0 / radix_m if mode == "sharded" else 0.0
+    B_elem = (12.25 if N == 1 else 12.5 + 2 * sum_w if mode == "sharded" else 12.0 + 0.5 * N)
     host, _ = synth_host(ns, rank)
     sw.grad_flat[:host.numel()].copy_(host.to(dev, non_blocking=True))
     stream = torch.cuda.current_stream(dev)
@@ -350,9 +366,7 @@ def run_b200(args):
     # N = 1: on a second, ungrouped plan over the same gradients, so every kernel
     # covers the whole set in one launch; N > 1: the stage API of this plan.
     if N == 1:
-        os.environ["TGB_GROUPS"] = "0"
-        sw_b = tg.SyncWorker(names, shapes, cfg, device=dev)
-        os.environ.pop("TGB_GROUPS")
+        sw_b = tg.SyncWorker(names, shapes, cfg, device=dev, schedule="single")
         sw_b.grad_flat.copy_(sw.grad_flat)
         plan_b = sw_b.plan
     else:
@@ -518,8 +532,8 @@ def run_b200(args):
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         try:
             reps = ref_replicas(1)
-            elems, wall, _, sample = cpu_reference_sample(layers, 1, args.cpu_seconds,
-                                                          replicas=reps)
+            elems, wall, _, sample = cpu_reference_run(layers, 1, 1, 0, reps,
+                                                       budget_s=args.cpu_seconds)
             cpu = {"value": elems / wall, "unit": UNIT, "cores": 2 * reps,
                    "kind": "reference", "sample": sample,
                    "host_cores_available": os.cpu_count()}
@@ -530,21 +544,15 @@ def run_b200(args):
     groups = 2 if plan.grouped else 1
     # own kernels per tgb_step: N=1: K1 + K2(decode fused); fused: K1 + K2 + barrier + K3;
     # sharded: K1 + K2 + barrier + K3a + barrier + K3b; nccl: K1 + K2 + K3 (+ NCCL's own)
-    launches_per_step = groups * {"none": 2, "fused": 4, "fused-r3": 4, "sharded": 6, "nccl": 3,
-                                  "pipelined": 2}[mode]
+    launches_per_step = {"none": 2 * groups, "fused": 4 * groups, "sharded": 6,
+                         "nccl": 3 * groups}[mode]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (codes u8, sigma f64)",
             "data": "synthetic (Gaussian sigma=1e-3, seeded per rank, host-generated)",
-            "config": {"workload": f"{args.workload} full gradient set "
-                                   f"({len(ns)} tensors, {n} fp32 elements/worker), "
-                                   f"{N} worker(s), encode+sync+decode",
-                       "global_batch": None, "seq_len": None, "parallelism": f"dp{N}",
-                       "elements_per_worker": n, "codec": "c=2.5 per-tensor clip, sharing on, "
-                       "REF (post-hoc max) scalers", "l2": "inputs (553 MB/rank) > L2 (126 MB): "
-                       "no flush"},
+            "config": workload_config(args.workload, len(ns), n, N),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": hbm_src, "timing": dom_src,
@@ -562,19 +570,14 @@ def run_b200(args):
             "kernels_sequential": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
             "gpu_launches": launches_per_step * K,
-            "gpu_launches_note": "own kernels per tgb_step and layer group: N=1 K1 + K2 (K2 "
-                                 "also decodes); pipelined K1 + K23; fused K1 + K2 + peer barrier "
-                                 "+ K3; sharded K1 + K2 + barrier + K3a (owner sums) + barrier + "
-                                 "K3b; nccl K1 + K2 + K3",
+            "gpu_launches_note": "own kernels per tgb_step (per layer group where the schedule "
+                                 "has two): N=1 K1 + K2 (K2 also decodes); fused K1 + K2 + peer "
+                                 "barrier + K3; sharded K1 + K2 + barrier + K3a (owner sums) + "
+                                 "barrier + K3b; nccl K1 + K2 + K3",
             "exchange": {"fused": "fused NVLink peer stores in K2 + device barrier",
-                         "fused-r3": "fused NVLink peer stores in K2 (radix-3 wire codes, 5 "
-                                     "elements per byte) + device barrier",
                          "sharded": "sharded: K2 stores codes at the chunk owner, owner sums N "
-                                    "workers into packed sums stored at every rank (NVLink), "
-                                    "2 device barriers",
-                         "pipelined": "pipelined: one persistent K2+K3 kernel, codes stored "
-                                      "into every rank item by item (NVLink), per-item epoch "
-                                      "flags, decode overlapped with ternarize",
+                                    "workers into radix-(2N+1) packed sums stored at every rank "
+                                    "(NVLink), 2 device barriers",
                          "nccl": "NCCL allgather", "none": "none (N=1)"}[mode],
             "clocks": clocks,
             "e2e": e2e,
@@ -591,8 +594,28 @@ def run_b200(args):
     return 0
 
 
+def self_launch(args):
+    """--gpus N > 1 without torchrun: launch N ranks of this script on 127.0.0.1
+    (one process per GPU) and relay their output; rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    ws, _, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -336,7 +336,11 @@ inline bool is_passthrough(const CodecConfig& cfg, const std::string& name) {
 // plan error -> the reference's CodecError text; corrupt-code indices are
 // reported by the device per tensor and converted to the bucket's element
 [[noreturn]] inline void throw_plan_error(const tgb_plan* p, const tgb_error& e,
-                                          const std::vector<std::string>& names) {
+                                          const std::vector<std::string>& names,
+                                          uint64_t t = 0) {
+    if (e.flags & TGB_E_SKEW)  // cluster.hpp:141-143
+        throw ProtocolError("server: iteration skew, expected " + std::to_string(t) + " got " +
+                            std::to_string(e.aux));
     const std::string nm =
         e.layer >= 0 && e.layer < static_cast<int32_t>(names.size()) ? names[e.layer] : "?";
     if (e.flags & TGB_E_NONFINITE) throw CodecError("encode_step: non-finite gradient " + nm);
@@ -528,14 +532,39 @@ private:
     tgb_comm* c_ = nullptr;
 };
 
+// TrafficStats (cluster.hpp:62-74): framed bytes of the reference's wire format
+// and the same tensors at raw fp32, plus the bytes this build's exchange moved
+// between GPUs (NVLink)
+struct TrafficStats {
+    uint64_t bytes_up = 0, bytes_down = 0, float_bytes_up = 0, float_bytes_down = 0;
+    uint64_t device_bytes_out = 0, device_bytes_in = 0;
+    double up_reduction() const {
+        return bytes_up ? static_cast<double>(float_bytes_up) / bytes_up : 1.0;
+    }
+    double down_reduction() const {
+        return bytes_down ? static_cast<double>(float_bytes_down) / bytes_down : 1.0;
+    }
+    TrafficStats& operator+=(const tgb_traffic& t) {
+        bytes_up += t.bytes_up;
+        bytes_down += t.bytes_down;
+        float_bytes_up += t.float_bytes_up;
+        float_bytes_down += t.float_bytes_down;
+        device_bytes_out += t.device_bytes_out;
+        device_bytes_in += t.device_bytes_in;
+        return *this;
+    }
+};
+
 // Worker::run sync segment (cluster.hpp:283-297) with gradients resident in HBM:
 // grads() -> [fill] -> step(t) -> outputs() hold the averaged gradient, identical
-// on every rank.
+// on every rank. exchange: TGB_EXCHANGE_AUTO / _FUSED / _SHARDED (NVLink peer
+// stores, attached here; ranks with different plans throw ProtocolError) or
+// TGB_EXCHANGE_NCCL (ncclAllGather of the push areas).
 class SyncWorker {
 public:
     SyncWorker(std::vector<std::string> names, std::vector<std::size_t> sizes,
                const CodecConfig& cfg, int rank = 0, int world_size = 1, Comm* comm = nullptr,
-               bool fused = true)
+               int exchange = TGB_EXCHANGE_AUTO)
         : names_(std::move(names)), sizes_(std::move(sizes)), comm_(comm) {
         cfg.validate();
         const int nl = static_cast<int>(names_.size());
@@ -567,9 +596,15 @@ public:
         std::vector<const char*> cn(nl);
         for (int l = 0; l < nl; ++l) cn[l] = names_[l].c_str();
         detail::check(tgb_plan_set_names(plan_, cn.data()), "tgb_plan_set_names");
-        if (world_size > 1 && fused)
-            detail::check(tgb_plan_attach_peers(plan_, comm_ ? comm_->get() : nullptr),
-                          "tgb_plan_attach_peers");
+        if (world_size > 1 && exchange != TGB_EXCHANGE_NCCL) {
+            if (exchange != TGB_EXCHANGE_AUTO)
+                detail::check(tgb_plan_set_option(plan_, TGB_PLAN_OPT_EXCHANGE, exchange),
+                              "tgb_plan_set_option");
+            const tgb_status st = tgb_plan_attach_peers(plan_, comm_ ? comm_->get() : nullptr);
+            if (st == TGB_ERR_PROTOCOL) throw ProtocolError(tgb_last_error_message());
+            detail::check(st, "tgb_plan_attach_peers");
+        }
+        detail::check(tgb_plan_traffic(plan_, &step_traffic_), "tgb_plan_traffic");
     }
     SyncWorker(const SyncWorker&) = delete;
     SyncWorker& operator=(const SyncWorker&) = delete;
@@ -579,20 +614,27 @@ public:
     float* output(int layer) { return outs_.p + offs_[layer]; }    // device
     void step(uint64_t t, cudaStream_t stream = nullptr) {
         detail::check(tgb_step(plan_, comm_ ? comm_->get() : nullptr, t, stream), "tgb_step");
+        last_t_ = t;
+        traffic_ += step_traffic_;
     }
-    // synchronises; throws CodecError with the reference's message on a device error
+    // synchronises; throws CodecError / ProtocolError with the reference's message
+    // on a device error
     void check() {
         tgb_error e{};
         const tgb_status st = tgb_check(plan_, &e);
-        if (st == TGB_ERR_CODEC) detail::throw_plan_error(plan_, e, names_);
+        if (st == TGB_ERR_CODEC) detail::throw_plan_error(plan_, e, names_, last_t_);
         detail::check(st, "tgb_check");
     }
+    // accumulated over the steps so far (ParameterServer::traffic(), cluster.hpp:167)
+    const TrafficStats& traffic() const { return traffic_; }
     // host buffers in/out (pinned recommended): tgb_step_host
     void step_host(uint64_t t, const std::vector<const float*>& h_grads,
                    const std::vector<float*>& h_out, cudaStream_t stream = nullptr) {
         detail::check(tgb_step_host(plan_, comm_ ? comm_->get() : nullptr, t, h_grads.data(),
                                     h_out.data(), stream),
                       "tgb_step_host");
+        last_t_ = t;
+        traffic_ += step_traffic_;
     }
     // interop with the reference's parameter server (wire.hpp): the push frame of the
     // last encode, byte-identical to frame(Message{Push, t, rank, serialize_encoded(...)})
@@ -629,6 +671,9 @@ private:
     Comm* comm_;
     tgb_plan* plan_ = nullptr;
     detail::DevBuf<float> grads_, outs_;
+    uint64_t last_t_ = 0;
+    tgb_traffic step_traffic_{};
+    TrafficStats traffic_;
 };
 
 }  // namespace tgb

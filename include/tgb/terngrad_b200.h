@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TGB_ABI_VERSION 1
+#define TGB_ABI_VERSION 2
 
 typedef enum tgb_status {
     TGB_OK = 0,
@@ -49,11 +49,15 @@ typedef enum tgb_status {
 #define TGB_E_S0_NONZERO 0x4u       /* "ternarize: s=0 but gradient has nonzero element" :155-158 */
 #define TGB_E_CORRUPT_CODE 0x8u     /* "corrupt ternary code 11 in block <name> at element <k>" :42-44 */
 #define TGB_E_PEER_TIMEOUT 0x10u    /* fused exchange: a peer never reached the barrier (index = peer) */
+#define TGB_E_SKEW 0x20u            /* "server: iteration skew, expected <t> got <t'>" cluster.hpp:141-143:
+                                       a peer stepped a different iteration (index = peer, aux = its t).
+                                       The step's decode is skipped (outputs keep the previous step). */
 
 typedef struct tgb_error {
     uint32_t flags;
     int32_t layer;  /* first offending tensor (plan layer index) or -1 */
     uint64_t index; /* first offending element within that tensor (when known) */
+    uint64_t aux;   /* TGB_E_SKEW: the offending peer's iteration; else 0 */
 } tgb_error;
 
 /* one gradient tensor of the canonical parameter order (tensor.hpp:14-43) */
@@ -99,17 +103,13 @@ typedef struct tgb_plan_info {
     int32_t exchange;     /* TGB_EXCHANGE_*: how tgb_step moves data between ranks */
 } tgb_plan_info;
 
+#define TGB_EXCHANGE_AUTO (-1) /* tgb_plan_set_option: fused for N <= 4, sharded from N = 5 */
 #define TGB_EXCHANGE_NONE 0    /* n_workers == 1 */
 #define TGB_EXCHANGE_NCCL 1    /* ncclAllGather of push buffers, K3 on every rank */
 #define TGB_EXCHANGE_FUSED 2   /* K1/K2 store scalers + codes into every peer (NVLink) */
 #define TGB_EXCHANGE_SHARDED 3 /* codes to the chunk's owner, owner sums N workers and
-                                  stores packed sums into every peer, K3 decodes sums */
-#define TGB_EXCHANGE_PIPELINED 4 /* one persistent kernel per step: codes stored into every
-                                    peer item by item, per-item epoch flags, each item
-                                    decoded as soon as all ranks published it */
-#define TGB_EXCHANGE_FUSED_R3 5 /* fused, with radix-3 wire codes (5 elements per byte,
-                                   1.6 instead of 2 bits on NVLink; N >= 3, shared scalers,
-                                   no passthrough blocks); the push area keeps 2-bit codes */
+                                  stores radix-(2N+1) packed sums into every peer, every
+                                  rank decodes the sums (parameter server sharded over ranks) */
 
 /* One block of the encoded gradient (EncodedGradient::blocks, codec.hpp:70-76):
  * a bucket of a ternary layer (TernaryBlock, the whole layer unless FixedSize)
@@ -151,6 +151,26 @@ tgb_status tgb_plan_layer_layout(const tgb_plan* plan, int32_t layer, uint64_t* 
                                  int32_t* slot);
 /* block b's layout (0 <= b < n_blocks) */
 tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_info* out);
+/* ---- plan options (no environment variables: every schedule choice is explicit) ----
+ * TGB_PLAN_OPT_SCHEDULE: TGB_SCHEDULE_AUTO (dominant tensor || the rest on two streams
+ *   when one tensor holds 35-95 % of the elements, PerTensor + REF; sets under 8 Mi
+ *   elements run K1 + K2 as one persistent launch), _SINGLE (one stream, every kernel
+ *   covers the whole set), _GROUPS (force the two-group split), _UNFUSED (one stream,
+ *   K1 and K2 always separate launches), _FUSED12 (one stream, K1 + K2 always one
+ *   launch). Rebuilds the work tables (re-binds the bound pointers).
+ * TGB_PLAN_OPT_EXCHANGE: TGB_EXCHANGE_AUTO / _FUSED / _SHARDED; before attaching peers.
+ * TGB_PLAN_OPT_FUSED_OPTIMIZER: 1 (default) the decode kernel applies the optimizer in
+ *   tgb_step_apply; 0 the averaged gradient is written and a separate kernel applies it. */
+#define TGB_PLAN_OPT_SCHEDULE 0
+#define TGB_PLAN_OPT_EXCHANGE 1
+#define TGB_PLAN_OPT_FUSED_OPTIMIZER 2
+#define TGB_SCHEDULE_AUTO 0
+#define TGB_SCHEDULE_SINGLE 1
+#define TGB_SCHEDULE_GROUPS 2
+#define TGB_SCHEDULE_UNFUSED 3
+#define TGB_SCHEDULE_FUSED12 4
+tgb_status tgb_plan_set_option(tgb_plan* plan, int32_t option, int64_t value);
+
 /* host arrays of device pointers, n_layers each: the worker's gradients (read)
  * and the averaged-gradient outputs (written by decode). Pointers must stay
  * valid until the next bind. 16-byte aligned pointers take the vector path. */
@@ -186,17 +206,28 @@ tgb_status tgb_decode_average(tgb_plan* plan, const uint8_t* d_src, int32_t n_wo
  * orders the step, and K3 decodes from local HBM: no allgather launch and the
  * NVLink traffic overlaps K2. Collective: every rank calls it once. */
 tgb_status tgb_plan_attach_peers(tgb_plan* plan, tgb_comm* comm);
+/* Attaching checks that every rank built the same plan (block table, codec
+ * parameters, buffer layout, exchange): a mismatch returns TGB_ERR_PROTOCOL with
+ * the reference's text ("server: block structure mismatch from worker <w>",
+ * cluster.hpp:169-172) before any peer memory is opened. Per step, every rank
+ * publishes its iteration with its barrier flag; a peer at another iteration
+ * raises TGB_E_SKEW (cluster.hpp:141-143) and the decode is skipped. */
 /* Fused exchange between N plans of ONE process (workers 0..N-1, on one device or
  * on devices with peer access): every plan maps the others' gather buffers
- * directly (no IPC, no NCCL), then tgb_step runs the same K1/K2 peer stores,
- * flag barriers and K3 (or the sharded reduce/expand) as with tgb_plan_attach_peers.
- * Each plan's tgb_step must be issued on its own stream (the steps of all N plans
- * run concurrently: a plan's barrier waits for the others' K2). Single-process
+ * directly (no IPC, no NCCL), then tgb_local_step runs the same K1/K2 peer stores,
+ * K3 (or the sharded reduce/expand) as the multi-process exchange, ordered by
+ * CUDA events between the plans' streams instead of spinning flag barriers (so no
+ * hardware-queue or module-loading setting is needed). Single-process
  * counterpart of the reference's run_cluster over InProcessHub
  * (inc/cluster.hpp:378-397, inc/transport.hpp:77-125); used to run N = 8
  * workers' exchanges on fewer GPUs. REF sharing only (TGB_ERR_UNSUPPORTED for
  * PRESHARED, whose max-allreduce needs a communicator). */
 tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n);
+/* one step of every plan attached with tgb_plan_attach_local: plan w steps
+ * iteration t[w] on streams[w] (cudaStream_t each; a skewed t raises TGB_E_SKEW on
+ * the plans that see it). Returns when every launch is queued. */
+tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
+                          void* const* streams);
 /* device pointers of the push area written by the last step (own scaler slots
  * + codes) and of the gather buffer (n_workers push areas) the last K3 read */
 tgb_status tgb_plan_last_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_gathered);
@@ -223,7 +254,7 @@ tgb_status tgb_step_host(tgb_plan* plan, tgb_comm* comm, uint64_t t, const float
 #define TGB_KERNEL_K3 3      /* k3 decode of the gather buffer */
 #define TGB_KERNEL_K3A 4     /* sharded: owner sums N workers' codes */
 #define TGB_KERNEL_K3B 5     /* sharded: decode of the packed sums */
-#define TGB_KERNEL_K23 6     /* pipelined K2+K3 */
+#define TGB_KERNEL_K12 6     /* fused K1 + K2 (small sets, one persistent launch) */
 #define TGB_KERNEL_NCCL 7    /* ncclAllGather / ncclAllReduce issued by the plan */
 typedef struct tgb_kernel_time {
     int32_t kind;          /* TGB_KERNEL_* */
@@ -291,6 +322,27 @@ tgb_status tgb_plan_serialize_push(tgb_plan* plan, uint64_t t, uint8_t* h_frame,
  * Synchronous. */
 tgb_status tgb_plan_decode_pull(tgb_plan* plan, const uint8_t* h_frame, uint64_t len,
                                 uint64_t* iteration, void* stream);
+
+/* ---- traffic accounting (TrafficStats, cluster.hpp:62-74, 145-160) ----
+ * Per worker and step, for the reference's wire format: the framed push
+ * (kHeaderSize + wire_size, codec.hpp:455-467) and the same tensors at raw fp32
+ * (kHeaderSize + float_wire_size, :469-481); the framed pull the server sends
+ * back (radix-(2N+1) SharedSumBlocks or FloatAvgBlocks, wire.hpp:103-145) and its
+ * fp32 size (float_pull_size, wire.hpp:231-243). up/down reduction = float/framed.
+ * device_bytes_out / _in: what this build's exchange actually moves per rank and
+ * step over NVLink (fused: codes + scalers to N-1 peers; sharded: codes to owners
+ * + packed sums to every rank); 0 at N == 1. */
+typedef struct tgb_traffic {
+    uint64_t bytes_up, bytes_down;             /* framed, per worker */
+    uint64_t float_bytes_up, float_bytes_down; /* same tensors at raw fp32 */
+    uint64_t device_bytes_out, device_bytes_in;
+} tgb_traffic;
+/* from a layer table alone (no device needed); names[l] are the tensor names */
+tgb_status tgb_traffic_for_layers(const tgb_layer_desc* layers, const char* const* names,
+                                  int32_t n_layers, const tgb_codec_params* params,
+                                  int32_t n_workers, tgb_traffic* out);
+/* for a plan (after tgb_plan_set_names; device bytes for its current exchange) */
+tgb_status tgb_plan_traffic(const tgb_plan* plan, tgb_traffic* out);
 
 /* ---- communicator (NCCL over NVLink/NVSwitch) ---- */
 #define TGB_UNIQUE_ID_BYTES 128

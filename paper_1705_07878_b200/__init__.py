@@ -10,13 +10,13 @@ from .codec import (Bucketing, CodecConfig, CodecError, EncodedGradient, EncodeR
                     fnv1a64, histogram, scaler, share_scalers, ternarize)
 from .optimizer import (LrSchedule, OptimizerConfig, OptimizerRule, OptimizerState,
                         ScheduleKind)
-from .plan import Comm, LocalCluster, Plan, SyncWorker, aligned_flat
+from .plan import Comm, LocalCluster, Plan, SyncWorker, TrafficStats, aligned_flat
 from . import layersets
 
 __all__ = [
     "Bucketing", "CodecConfig", "CodecError", "EncodedGradient", "EncodeResult", "GradTensor",
     "HistogramBin", "histogram", "PassthroughBlock", "ProtocolError", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
     "clip_bound", "decode", "encode_step", "fnv1a64", "scaler", "share_scalers", "ternarize",
-    "Comm", "LocalCluster", "Plan", "SyncWorker", "aligned_flat", "layersets", "LrSchedule",
+    "Comm", "LocalCluster", "Plan", "SyncWorker", "TrafficStats", "aligned_flat", "layersets", "LrSchedule",
     "OptimizerConfig", "OptimizerRule", "OptimizerState", "ScheduleKind",
 ]

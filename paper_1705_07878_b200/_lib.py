@@ -27,25 +27,30 @@ TGB_E_SCALER_BELOW_MAX = 0x2
 TGB_E_S0_NONZERO = 0x4
 TGB_E_CORRUPT_CODE = 0x8
 TGB_E_PEER_TIMEOUT = 0x10
+TGB_E_SKEW = 0x20
 
 TGB_LAYER_PASSTHROUGH = 0x1
 TGB_BUCKET_PER_TENSOR, TGB_BUCKET_GLOBAL, TGB_BUCKET_FIXED = 0, 1, 2
 TGB_SHARE_REF, TGB_SHARE_PRESHARED = 0, 1
 UNIQUE_ID_BYTES = 128
+TGB_EXCHANGE_AUTO = -1
 TGB_EXCHANGE_NONE, TGB_EXCHANGE_NCCL, TGB_EXCHANGE_FUSED, TGB_EXCHANGE_SHARDED = 0, 1, 2, 3
-TGB_EXCHANGE_PIPELINED = 4
-EXCHANGE_NAMES = ["none", "nccl", "fused", "sharded", "pipelined", "fused-r3"]
+EXCHANGE_NAMES = ["none", "nccl", "fused", "sharded"]
+TGB_PLAN_OPT_SCHEDULE, TGB_PLAN_OPT_EXCHANGE, TGB_PLAN_OPT_FUSED_OPTIMIZER = 0, 1, 2
+TGB_SCHEDULE_AUTO, TGB_SCHEDULE_SINGLE, TGB_SCHEDULE_GROUPS = 0, 1, 2
+TGB_SCHEDULE_UNFUSED, TGB_SCHEDULE_FUSED12 = 3, 4
 
 # every symbol the header declares (checked by tests/test_capi.py)
 EXPORTS = [
     "tgb_version", "tgb_status_string", "tgb_fnv1a64", "tgb_device_count",
     "tgb_plan_create", "tgb_plan_destroy", "tgb_plan_get_info", "tgb_plan_layer_layout",
-    "tgb_plan_block_info",
+    "tgb_plan_block_info", "tgb_plan_set_option",
     "tgb_plan_bind", "tgb_plan_buffers", "tgb_stats", "tgb_ternarize_pack", "tgb_encode",
     "tgb_share_scalers", "tgb_sync", "tgb_decode_average", "tgb_step", "tgb_step_host", "tgb_check",
     "tgb_plan_code_stats", "tgb_plan_enable_code_stats", "tgb_plan_enable_timing",
     "tgb_plan_read_timing",
-    "tgb_plan_attach_peers", "tgb_plan_attach_local", "tgb_plan_last_buffers",
+    "tgb_plan_attach_peers", "tgb_plan_attach_local", "tgb_local_step", "tgb_plan_last_buffers",
+    "tgb_traffic_for_layers", "tgb_plan_traffic",
     "tgb_optimizer_apply", "tgb_plan_bind_optimizer", "tgb_step_apply",
     "tgb_last_error_message", "tgb_plan_set_names", "tgb_plan_push_frame_size",
     "tgb_plan_serialize_push", "tgb_plan_decode_pull",
@@ -83,7 +88,14 @@ class KernelTime(C.Structure):
 
 
 KERNEL_NAMES = {0: "K1_stats", 1: "K2_ternarize_pack", 2: "peer_barrier", 3: "K3_decode",
-                4: "K3a_shard_reduce", 5: "K3b_shard_expand", 6: "K23_pipelined", 7: "nccl"}
+                4: "K3a_shard_reduce", 5: "K3b_shard_expand", 6: "K12_fused", 7: "nccl"}
+
+
+class Traffic(C.Structure):
+    """tgb_traffic: one worker's per-step TrafficStats terms (cluster.hpp:62-74)"""
+    _fields_ = [("bytes_up", C.c_uint64), ("bytes_down", C.c_uint64),
+                ("float_bytes_up", C.c_uint64), ("float_bytes_down", C.c_uint64),
+                ("device_bytes_out", C.c_uint64), ("device_bytes_in", C.c_uint64)]
 
 
 class BlockInfo(C.Structure):
@@ -99,7 +111,8 @@ class Optimizer(C.Structure):
 
 
 class Error(C.Structure):
-    _fields_ = [("flags", C.c_uint32), ("layer", C.c_int32), ("index", C.c_uint64)]
+    _fields_ = [("flags", C.c_uint32), ("layer", C.c_int32), ("index", C.c_uint64),
+                ("aux", C.c_uint64)]
 
 
 _vp = C.c_void_p
@@ -120,6 +133,7 @@ def _declare(L):
         "tgb_plan_get_info": (S, [_vp, C.POINTER(PlanInfo)]),
         "tgb_plan_layer_layout": (S, [_vp, _i32, C.POINTER(_u64), C.POINTER(_i32)]),
         "tgb_plan_block_info": (S, [_vp, _i32, C.POINTER(BlockInfo)]),
+        "tgb_plan_set_option": (S, [_vp, _i32, C.c_int64]),
         "tgb_plan_bind": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_plan_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_stats": (S, [_vp, _vp]),
@@ -137,6 +151,10 @@ def _declare(L):
         "tgb_plan_read_timing": (S, [_vp, C.POINTER(KernelTime), _i32, C.POINTER(_i32)]),
         "tgb_plan_attach_peers": (S, [_vp, _vp]),
         "tgb_plan_attach_local": (S, [C.POINTER(_vp), _i32]),
+        "tgb_local_step": (S, [C.POINTER(_vp), _i32, C.POINTER(_u64), C.POINTER(_vp)]),
+        "tgb_traffic_for_layers": (S, [C.POINTER(LayerDesc), C.POINTER(C.c_char_p), _i32,
+                                       C.POINTER(CodecParams), _i32, C.POINTER(Traffic)]),
+        "tgb_plan_traffic": (S, [_vp, C.POINTER(Traffic)]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_optimizer_apply": (S, [C.POINTER(Optimizer), _u64, C.c_double, _i32,
                                     C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp),

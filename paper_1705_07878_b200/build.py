@@ -14,8 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libtgb.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "capi.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("tgb_device.cuh", "tgb_internal.h", "tgb_stats.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "plan.cu", "capi.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("tgb_device.cuh", "tgb_internal.h", "tgb_stats.cuh", "tgb_plan.h")] + [
     os.path.join(ROOT, "include", "tgb", "terngrad_b200.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

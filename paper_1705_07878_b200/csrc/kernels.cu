@@ -72,16 +72,11 @@ __device__ __forceinline__ float4 k1_ld4(const float4* p, uint64_t pol) {
     }
 }
 
-template <class Src, int U = 8, int A = 1, int kMinBlocks = 1, bool kHint = false>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out o) {
-    // K2 (a programmatic dependent, TGB_PDL) may be scheduled once every K1 CTA has
-    // started; it waits on griddepcontrol.wait for K1's completion before reading scalers
-    asm volatile("griddepcontrol.launch_dependents;");
-    ChunkDev ch;
-    LayerDev L;
-    src.get(blockIdx.x, ch, L);
-    if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;  // this group's K2 counts next
-    if (L.flags & kLayerPassthrough) return;
+// One K1 work unit (a chunk of one block): fp64 moments of the chunk shifted by
+// its first element, then the partial + the tensor's finalize (tgb_stats.cuh).
+template <int U, int A, bool kHint>
+__device__ __forceinline__ void k1_unit(const K1Out& o, const ChunkDev& ch, const LayerDev& L,
+                                        uint32_t unit) {
     const float* g = L.g + ch.begin;
     const uint32_t count = ch.count;
     const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
@@ -93,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
     uint32_t done = 0;
     uint64_t pol = 0;
     if constexpr (kHint) {
-        if (blockIdx.x >= o.keep_from)
+        if (unit >= o.keep_from)
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         else
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -119,92 +114,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
         s_all += S[k];
         q_all += Q[k];
     }
-    k1_emit_and_finalize(o, L, ch.layer, blockIdx.x, L.first_chunk, L.n_chunks, count, x0, s_all,
+    k1_emit_and_finalize(o, L, ch.layer, unit, L.first_chunk, L.n_chunks, count, x0, s_all,
                          q_all, mx);
 }
 
-// K1 with a TMA bulk-copy ring (TGB_K1V=10, A/B): a producer warp streams the
-// chunk through S shared-memory stages of 16 KB with cp.async.bulk (no
-// registers held by loads in flight), 8 consumer warps accumulate from shared
-// memory. Same arithmetic and finalize as k1_stats (ConsumerBar: the producer
-// warp never joins a CTA barrier after the ring is set up).
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-constexpr uint32_t kK1TileBytes = 16384;  // 1024 float4 per stage
-
-template <int S>
-__global__ void __launch_bounds__(kThreads + 32) k1_stats_tma(TableSource src, K1Out o) {
-    extern __shared__ __align__(128) uint8_t k1_dsm[];
-    float4* buf = reinterpret_cast<float4*>(k1_dsm);
-    uint64_t* full = reinterpret_cast<uint64_t*>(k1_dsm + S * kK1TileBytes);
-    uint64_t* empty = full + S;
+// K1 is memory-bound: the fp64 moments (F2F + DADD + DFMA per element) run under
+// the load stream; with the same grid, a plain float sum streams the same
+// bytes no faster (tools/k1_variants.cu, profiles/r02_k1_variants.log).
+template <class Src, int U = 8, int A = 1, int kMinBlocks = 1, bool kHint = false>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out o) {
+    // K2 (a programmatic dependent) may be scheduled once every K1 CTA has
+    // started; it waits on griddepcontrol.wait for K1's completion before reading scalers
+    asm volatile("griddepcontrol.launch_dependents;");
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
-    if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;
+    if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;  // this group's K2 counts next
     if (L.flags & kLayerPassthrough) return;
-    const float* g = L.g + ch.begin;
-    const uint32_t count = ch.count;
-    const bool vec = (L.flags & kLayerVecIn) != 0;
-    const uint32_t n4 = vec ? (count >> 2) : 0u;
-    constexpr uint32_t kTile4 = kK1TileBytes / 16;
-    const uint32_t n_tiles = (n4 + kTile4 - 1) / kTile4;
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_addr(&empty[s])));
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == kThreads / 32) {  // producer
-        if (lane == 0) {
-            const float4* g4 = reinterpret_cast<const float4*>(g);
-            for (uint32_t t = 0; t < n_tiles; ++t) {
-                const uint32_t s = t % S, ph = (t / S) & 1u;
-                if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
-                const uint32_t bytes = 16u * min(kTile4, n4 - t * kTile4);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                                 smem_addr(&full[s])),
-                             "r"(bytes)
-                             : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_addr(buf + s * kTile4)),
-                    "l"(g4 + static_cast<uint64_t>(t) * kTile4), "r"(bytes), "r"(smem_addr(&full[s]))
-                    : "memory");
-            }
-        }
-        return;
-    }
-    const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
-    double Sx = 0.0, Qx = 0.0;
-    float mx = 0.0f;
-    for (uint32_t t = 0; t < n_tiles; ++t) {
-        const uint32_t s = t % S, ph = (t / S) & 1u;
-        mbar_wait(&full[s], ph);
-        const uint32_t m = min(kTile4, n4 - t * kTile4);
-        const float4* tb = buf + s * kTile4;
-#pragma unroll 4
-        for (uint32_t j = tid; j < m; j += kThreads) acc4(tb[j], x0, Sx, Qx, mx);
-        __syncwarp();
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s]))
-                         : "memory");
-    }
-    for (uint32_t i = (n4 << 2) + tid; i < count; i += kThreads) acc1(__ldcs(g + i), x0, Sx, Qx, mx);
-    k1_emit_and_finalize<ConsumerBar>(o, L, ch.layer, blockIdx.x, L.first_chunk, L.n_chunks, count,
-                                      x0, Sx, Qx, mx);
+    k1_unit<U, A, kHint>(o, ch, L, blockIdx.x);
 }
 
 // ====================================================================== K2
@@ -219,13 +146,13 @@ struct K2Args {
     float s_imm;         // per-layer API: scaler by value (slots == nullptr)
     uint64_t rng_base;   // per-layer API: ternarize rng_base (codec.hpp:148); plan: 0
     PeerPush dst;        // plan: code destinations (n == 0: just `push`)
-    int32_t bulk = 0;           // K2 code stores as TMA bulk copies (TGB_K2BULK, A/B)
     int32_t shard_n = 0;        // sharded exchange: ranks; chunk b belongs to rank r with
     uint32_t shard_bounds[kMaxPeers + 1];  // shard_bounds[r] <= b < shard_bounds[r + 1]
     unsigned long long* nnz = nullptr;     // telemetry: += nonzero codes (cluster.hpp:336-346)
     const OptDev* optd = nullptr;          // fused optimizer (kOpt kernels): per-block state
     OptArgs opt{};
     int32_t pdl = 0;  // launched as K1's programmatic dependent: 1 wait, 2/3 prefetch + wait
+    uint32_t keep_from = ~0u;  // work items K1 kept in L2 (evict_last): demoted after reading
 };
 
 // nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
@@ -382,19 +309,6 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
     }
 }
 
-// Codes of one chunk (work item b) into `stage`; returns the number of staged
-// code bytes (passthrough chunks are copied to their destinations here and
-// return 0). kFuse (N == 1: the average is this worker's own decode, K3 folded
-// into K2): every thread writes the decoded float4 of each code byte as soon as
-// it is computed, so the output stream overlaps the Philox compute. Ends with
-// a CTA barrier (stage complete).
-struct NoHook {
-    __device__ __forceinline__ void operator()(uint32_t) const {}
-};
-
-// hook(i) runs once per iteration i of the vectorised main loop (the pipelined
-// kernel decodes a slice of an older item there, interleaving HBM streaming
-// with the Philox compute).
 // destinations of chunk b's codes: [p0, p1) of a.dst (a.push when a.dst.n == 0)
 __device__ __forceinline__ void k2_dst_range(const K2Args& a, uint32_t b, int& p0, int& p1) {
     p0 = 0;
@@ -405,26 +319,34 @@ __device__ __forceinline__ uint8_t* k2_dst(const K2Args& a, int p) {
     return a.dst.n == 0 ? a.push : a.dst.base[p];
 }
 
-// kDirect (U == 4): in the vectorised loop each thread owns 4 consecutive code
-// bytes and stores them as one u32 straight to every destination while the CTA
-// keeps computing (NVLink stores overlap the Philox work); `streamed` returns
-// how many leading code bytes were written that way, the rest is staged.
-template <bool kRolling, int U, bool kFuse, class Hook = NoHook, bool kOpt = false,
-          bool kDirect = false>
+// K1 loaded the last units of its launch with an L2 evict_last policy so that
+// K2's reverse walk re-reads them from L2; once read here they are demoted back
+// to evict_normal, so no gradient line stays pinned in L2 after the step.
+__device__ __forceinline__ void demote_l2(const float* g, uint32_t count) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(g) & ~static_cast<uintptr_t>(127);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(g + count);
+    for (uintptr_t a = a0 + 128u * threadIdx.x; a < a1; a += 128u * kThreads)
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(a) : "memory");
+}
+
+// Codes of one chunk (work item b) into `stage`; returns the number of staged
+// code bytes (passthrough chunks are copied to their destinations here and
+// return 0). kFuse (N == 1: the average is this worker's own decode, K3 folded
+// into K2): every thread writes the decoded float4 of each code byte as soon as
+// it is computed, so the output stream overlaps the Philox compute. kOpt: the
+// decoded value drives OptimizerState::apply instead of being written. Ends
+// with a CTA barrier (stage complete).
+template <int U, bool kFuse, bool kOpt = false>
 __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDev& L,
                                                   const ChunkDev& ch, uint32_t b,
-                                                  uint8_t* __restrict__ stage, float4* lutv,
-                                                  const Hook& hook = Hook(),
-                                                  uint32_t* streamed_out = nullptr) {
-    static_assert(!kDirect || U == 4, "direct stores pack 4 code bytes per thread");
-    if (streamed_out) *streamed_out = 0;
+                                                  uint8_t* __restrict__ stage, float4* lutv) {
     if (L.flags & kLayerPassthrough) {
         k2_passthrough<kFuse, kOpt>(a, L, ch, b);
         return 0;
     }
-    uint32_t streamed = 0, nz_direct = 0;
-    const float s = a.slots ? a.slots[L.slot] : a.s_imm;
-    const float bound = a.bounds ? a.bounds[ch.layer] : INFINITY;
+    // L2 loads: in the fused K1+K2 kernel another CTA wrote them during this launch
+    const float s = a.slots ? __ldcg(a.slots + L.slot) : a.s_imm;
+    const float bound = a.bounds ? __ldcg(a.bounds + ch.layer) : INFINITY;
     const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
     const float* g = L.g + ch.begin;
@@ -438,7 +360,7 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
     const uint64_t qg = B >> 2;
     // fast paths: one Philox block per code byte, 32-bit counter arithmetic
     const bool lane_aligned = (B & 3u) == 0 && static_cast<uint32_t>(qg) <= 0xFFFFFFFFu - nbytes;
-    Philox4<kRolling> ph;
+    Philox4<false> ph;
     ph.init(L.key0, L.key1, static_cast<uint32_t>(qg >> 32), a.t);
     const uint32_t qbase = static_cast<uint32_t>(qg);
 
@@ -534,22 +456,14 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
     } else if (L.flags & kLayerVecIn) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         // uniform trip count (every thread runs every block: __syncthreads below)
-        uint32_t it = 0;
-        int dp0 = 0, dp1 = 0;
-        if (kDirect) k2_dst_range(a, b, dp0, dp1);
-        const uint64_t doff = L.code_off + (ch.begin >> 2);
-        for (uint32_t blk = 0; blk + U * kThreads <= nfull;
-             blk += U * kThreads, q += U * kThreads, ++it) {
-            hook(it);
+        for (uint32_t blk = 0; blk + U * kThreads <= nfull; blk += U * kThreads, q += U * kThreads) {
             float4 v[U];
             uint32_t ctr[U];
             uint4 r[U];
-            // byte of lane u: direct = blk + 4 tid + u (thread-contiguous), else q + u kThreads
-            const uint32_t qd = blk + 4 * tid;
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + (kDirect ? qd + u : q + u * kThreads));
+            for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + q + u * kThreads);
 #pragma unroll
-            for (int u = 0; u < U; ++u) ctr[u] = qbase + (kDirect ? qd + u : q + u * kThreads);
+            for (int u = 0; u < U; ++u) ctr[u] = qbase + q + u * kThreads;
             ph(ctr, r);
             uint32_t byte[U];
             float amb = -1.0f;
@@ -559,17 +473,10 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
 #pragma unroll
                 for (int u = 0; u < U; ++u) byte[u] = dec.byte_exact(v[u], r[u]);
             }
-            if (kDirect) {
-                const uint32_t word = byte[0] | (byte[1] << 8) | (byte[2] << 16) | (byte[3] << 24);
-                for (int p = dp0; p < dp1; ++p)
-                    *reinterpret_cast<uint32_t*>(k2_dst(a, p) + doff + qd) = word;
-                if (a.nnz) nz_direct += __popc((word | (word >> 1)) & 0x55555555u);
-                streamed = blk + U * kThreads;
-            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                if (!kDirect) stage[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
-                emit(kDirect ? qd + u : q + u * kThreads, byte[u]);
+                stage[q + u * kThreads] = static_cast<uint8_t>(byte[u]);
+                emit(q + u * kThreads, byte[u]);
                 if (a.check)
                     bad_mag = fmaxf(bad_mag, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
                                                    fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
@@ -611,64 +518,21 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
     if (a.check && fminf(bad_mag, bound) > s)  // codec.hpp:163-165
         raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(L.tensor),
                     block_rng_base(L) + ch.begin);
+    if (b >= a.keep_from) demote_l2(g, count);
     __syncthreads();
-    if (a.nnz) count_nonzero(stage, streamed, nbytes, a.nnz, nz_direct);
-    if (streamed_out) *streamed_out = streamed;
+    if (a.nnz) count_nonzero(stage, 0, nbytes, a.nnz, 0);
     return nbytes;
 }
 
-// The staged codes of chunk b to every destination: the rank's own push area
-// and, with peers attached, the same offset of every peer's gather buffer over
-// NVLink (the allgather is fused into K2 and overlaps its Philox-bound compute).
-__device__ __forceinline__ void k2_store_chunk(const K2Args& a, const LayerDev& L,
-                                               const ChunkDev& ch, uint32_t b,
-                                               const uint8_t* stage, uint32_t nbytes,
-                                               uint32_t streamed = 0) {
-    if (streamed >= nbytes) return;
-    const uint64_t off = L.code_off + (ch.begin >> 2) + streamed;
-    int p0, p1;
-    k2_dst_range(a, b, p0, p1);
-    for (int p = p0; p < p1; ++p) copy_out(stage + streamed, k2_dst(a, p) + off, nbytes - streamed);
-}
-
-// Radix-3 wire codes (fused exchange, N >= 3): 5 elements per byte,
-// byte = sum_i d_i 3^i with digit d = the 2-bit code (0 zero, 1 plus, 2 minus) of
-// element 5j + i -- 1.6 instead of 2 bits per element on NVLink (log2 3 = 1.585).
-// lut10 maps the 10 code bits of 5 elements (element i at bits 2i) to that byte.
-__device__ __forceinline__ void r3_build_lut(uint8_t* lut10) {
-    for (uint32_t v = threadIdx.x; v < 1024; v += kThreads) {
-        uint32_t r = 0, m = 1;
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
-            r += ((v >> (2 * i)) & 3u) * m;  // 11 never occurs in K2 output
-            m *= 3;
-        }
-        lut10[v] = static_cast<uint8_t>(r);
-    }
-}
-
-// stage (2-bit codes of `count` elements, pad bits 00) -> r3 (ceil(count/5) bytes)
-__device__ __forceinline__ uint32_t r3_convert(const uint8_t* stage, uint32_t count,
-                                               const uint8_t* lut10, uint8_t* r3) {
-    const uint32_t nr3 = (count + 4) / 5;
-    const uint32_t nbytes = (count + 3) >> 2;
-    for (uint32_t j = threadIdx.x; j < nr3; j += kThreads) {
-        const uint32_t bit = 10 * j, k = bit >> 3;
-        uint32_t v = stage[k];
-        if (k + 1 < nbytes) v |= static_cast<uint32_t>(stage[k + 1]) << 8;
-        v = (v >> (bit & 7u)) & 0x3FFu;
-        r3[j] = lut10[v];  // elements >= count are pad codes (00) or masked by nbytes
-    }
-    return nr3;
-}
-
-template <class Src, bool kRolling = false, int U = 4, int kMinBlocks = 3, bool kFuse = false,
-          bool kOpt = false, bool kDirect = false, bool kR3 = false>
+// K2: one CTA per work item. The chunk's codes are staged in shared memory and
+// handed to the TMA engine (bulk_copy_out): the rank's own push area and, with
+// peers attached, the same offset of every peer's gather buffer over NVLink
+// (the allgather is fused into K2 and overlaps its Philox-bound compute), or
+// only the chunk owner's (sharded exchange).
+template <class Src, int kMinBlocks = 3, bool kFuse = false, bool kOpt = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2Args a) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     __shared__ float4 lutv[kFuse ? 256 : 1];
-    __shared__ __align__(16) uint8_t r3buf[kR3 ? kStageBytes : 16];
-    __shared__ uint8_t lut10[kR3 ? 1024 : 1];
     const uint32_t b = a.reverse ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
     ChunkDev ch;
     LayerDev L;
@@ -684,31 +548,70 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
-    uint32_t streamed = 0;
-    if (kR3) r3_build_lut(lut10);  // visible after k2_code_chunk's closing barrier
-    const uint32_t nbytes = k2_code_chunk<kRolling, U, kFuse, NoHook, kOpt, kDirect>(
-        a, L, ch, b, stage, lutv, NoHook(), &streamed);
-    if (kR3) {  // 2-bit codes to this rank's push area, radix-3 bytes to every rank
-        if (!nbytes) return;  // (r3 plans have no passthrough blocks)
-        copy_out(stage, a.push + L.code_off + (ch.begin >> 2), nbytes);
-        const uint32_t nr3 = r3_convert(stage, ch.count, lut10, r3buf);
-        __syncthreads();
-        const uint64_t off = L.code_off + ch.begin / 5;  // chunks start at multiples of 80
-        for (int p = 0; p < a.dst.n; ++p) copy_out(r3buf, a.dst.base[p] + off, nr3);
-        return;
-    }
+    const uint32_t nbytes = k2_code_chunk<4, kFuse, kOpt>(a, L, ch, b, stage, lutv);
     // No fence after the peer stores: the step barrier kernel runs after this
     // grid completes in stream order, and grid completion implies its (peer)
     // stores are performed -- the guarantee event-based multi-GPU sync relies on.
     if (!nbytes) return;
-    if (a.bulk && streamed == 0) {  // the codes to every destination via the TMA engine
-        const uint64_t off = L.code_off + (ch.begin >> 2);
-        int p0, p1;
-        k2_dst_range(a, b, p0, p1);
-        bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
-        return;
+    const uint64_t off = L.code_off + (ch.begin >> 2);
+    int p0, p1;
+    k2_dst_range(a, b, p0, p1);
+    bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
+}
+
+// Fused K1 + K2 for small gradient sets (one launch per step; the K1 -> K2
+// kernel boundary would cost more than the work): persistent CTAs, all
+// co-resident (grid <= occupancy x SMs). Phase 1: the K1 units (clip statistics,
+// partials, per-tensor finalize by the last arriving unit, which publishes the
+// tensor's bound + scalers with a release store of the launch epoch). Phase 2:
+// the K2 units; a unit of tensor T first waits (acquire) for T's flag, so K2 of
+// early tensors overlaps K1 of later ones. Phase 1 never waits, so every flag a
+// phase-2 CTA waits for is set by a CTA that is already running: deadlock-free.
+// Global bucketing waits for the global flag (all tensors finalized).
+__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t epoch, ErrWord* err) {
+    if (threadIdx.x == 0) {
+        uint32_t v;
+        const long long t0 = clock64();
+        for (uint32_t spin = 0;; ++spin) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if (v == epoch) break;
+            if (spin > 16) __nanosleep(64);
+            if ((spin & 1023) == 1023 && clock64() - t0 > 20000000000ll) {  // ~10 s: a bug
+                raise_error(err, TGB_E_PEER_TIMEOUT, -1, ~0ull);
+                break;
+            }
+        }
     }
-    k2_store_chunk(a, L, ch, b, stage, nbytes, streamed);
+    __syncthreads();
+}
+
+template <bool kFuse, bool kOpt = false>
+__global__ void __launch_bounds__(kThreads, 4) k12_fused(TableSource src, K1Out o, K2Args a,
+                                                        uint32_t n_k1, uint32_t n_k2) {
+    __shared__ __align__(16) uint8_t stage[kStageBytes];
+    __shared__ float4 lutv[kFuse ? 256 : 1];
+    for (uint32_t u = blockIdx.x; u < n_k1; u += gridDim.x) {
+        ChunkDev ch;
+        LayerDev L;
+        src.get(u, ch, L);
+        k1_unit<8, 1, false>(o, ch, L, u);
+        __syncthreads();  // the finalize's shared memory is reused by the next unit
+    }
+    for (uint32_t b = blockIdx.x; b < n_k2; b += gridDim.x) {
+        ChunkDev ch;
+        LayerDev L;
+        src.get(b, ch, L);
+        if (!(L.flags & kLayerPassthrough))
+            wait_ready(o.global_bucketing ? o.ready_global : o.ready + L.tensor, o.epoch, a.err);
+        const uint32_t nbytes = k2_code_chunk<4, kFuse, kOpt>(a, L, ch, b, stage, lutv);
+        if (nbytes) {
+            const uint64_t off = L.code_off + (ch.begin >> 2);
+            int p0, p1;
+            k2_dst_range(a, b, p0, p1);
+            bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
+        }
+        __syncthreads();  // the bulk copy finished reading `stage` (thread 0 waited for it)
+    }
 }
 
 // ====================================================================== K3
@@ -779,6 +682,7 @@ struct K3Args {
     ErrWord* err;
     const OptDev* optd = nullptr;  // fused decode -> optimizer (kOpt kernels)
     OptArgs opt{};
+    int32_t gate = 0;              // plan exchange: skip when the step's exchange failed
 };
 
 struct K3Ptrs {  // per-layer API: explicit pointers (passed by value)
@@ -787,6 +691,7 @@ struct K3Ptrs {  // per-layer API: explicit pointers (passed by value)
 
 template <class Src, bool kTable, bool kShared>
 __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs ptrs) {
+    if (a.gate && exchange_failed(a.err)) return;
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
@@ -903,422 +808,16 @@ __global__ void __launch_bounds__(kThreads) k3_decode(Src src, K3Args a, K3Ptrs 
     }
 }
 
-// Plan K3, shared scalers, worker count known at compile time (N <= 8, one
-// NVSwitch box): per-worker code pointers live in registers, every worker's
-// bytes for U positions are loaded before use, no per-load address math or
-// bounds checks on full chunks. Same arithmetic as k3_decode (LUT of
-// (s*float(sum))*invN indexed by N + sum).
-// One chunk; tab[] must hold lane_biased (written before the first barrier
-// here); lut/sw are per-chunk scratch, safe to reuse across calls.
-template <int NW>
-__device__ __forceinline__ void k3_chunk_nw(const K3Args& a, const LayerDev& L, const ChunkDev& ch,
-                                            const uint32_t* tab, float* lut, float* sw) {
-    if (L.flags & kLayerPassthrough) {
-        const uint64_t off = L.code_off + 4ull * ch.begin;
-        k3_passthrough([&](int w) { return reinterpret_cast<const float*>(a.src + a.stride * w + off); },
-                       NW, L.out + ch.begin, ch.count, (L.flags & kLayerVecOut) != 0);
-        return;
-    }
-    const uint32_t tid = threadIdx.x;
-    if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
-    const uint32_t count = ch.count;
-    const uint32_t nbytes = (count + 3) >> 2;
-    const uint8_t* base[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) base[w] = a.src + a.stride * w + L.code_off + (ch.begin >> 2);
-    __syncthreads();
-    if (tid <= 2 * NW) {
-        float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s = fmaxf(s, sw[w]);
-        lut[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - NW)),
-                             a.inv_n);  // codec.hpp:296
-    }
-    __syncthreads();
-    float* out = L.out + ch.begin;
-    const bool vec_out = (L.flags & kLayerVecOut) != 0;
-    constexpr int U = 4;
-    uint32_t bad = 0;
-    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
-        const bool full = qb + U * kThreads <= nbytes;
-        uint32_t bw[NW][U];
-#pragma unroll
-        for (int w = 0; w < NW; ++w)
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t q = qb + tid + u * kThreads;
-                bw[w][u] = (full || q < nbytes) ? __ldcs(base[w] + q) : 0u;
-            }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                acc += tab[bw[w][u]];
-                bad |= bw[w][u] & (bw[w][u] >> 1);
-            }
-            const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
-                                         lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
-            const uint32_t q = qb + tid + u * kThreads;
-            const uint32_t b4 = 4 * q;
-            if (vec_out && (full || b4 + 4 <= count)) {
-                __stcs(reinterpret_cast<float4*>(out + b4), o);
-            } else if (q < nbytes) {
-                if (b4 + 0 < count) out[b4 + 0] = o.x;
-                if (b4 + 1 < count) out[b4 + 1] = o.y;
-                if (b4 + 2 < count) out[b4 + 2] = o.z;
-                if (b4 + 3 < count) out[b4 + 3] = o.w;
-            }
-        }
-    }
-    if (bad & 0x55u) {  // rare: locate the first corrupt element of this thread
-        for (uint32_t q = tid; q < nbytes; q += kThreads)
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t b = base[w][q] & (base[w][q] >> 1) & 0x55u;
-                if (b) {
-                    raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
-                                block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(b) - 1) >> 1));
-                    return;
-                }
-            }
-    }
-}
-
-template <int NW>
-__global__ void __launch_bounds__(kThreads) k3_decode_nw(TableSource src, K3Args a) {
-    __shared__ uint32_t tab[256];
-    __shared__ float lut[2 * NW + 1];
-    __shared__ float sw[NW];
-    ChunkDev ch;
-    LayerDev L;
-    src.get(blockIdx.x, ch, L);
-    tab[threadIdx.x] = lane_biased(threadIdx.x);
-    k3_chunk_nw<NW>(a, L, ch, tab, lut, sw);
-}
-
-// ================================================ pipelined fused exchange
-// N >= 2, peers attached (TGB_PIPE, default): ONE persistent kernel per step
-// runs K2 and K3. CTA j takes work items j, j+G, j+2G, ... (G = resident CTAs).
-// Per item: ternarize into smem; publish the PREVIOUS item (fence.sys, then
-// epoch flag -> every rank: its stores were issued one item ago, so the fence
-// is cheap); store this item's codes into every rank's gather buffer; decode
-// the item from two iterations back once every rank's flag for it reached the
-// epoch. Decoding (HBM-bound) thus overlaps Philox (issue-bound) and the
-// NVLink stores, and there is no step barrier: decoding item c at epoch e
-// needs every rank's flag e for c, i.e. every rank finished step e-1, so the
-// parity-(e+1) buffers this rank writes next step are free (double buffering).
-// Deadlock freedom: item j+kG waits only on items j+(k-2)G of the same CTA
-// index on every rank; all G CTAs are resident (grid sized by occupancy).
-struct PipeArgs {
-    K2Args k2;
-    K3Args k3;
-    uint32_t* flags;                 // this rank's flags: [item][rank]
-    uint32_t* peer_flags[kMaxPeers]; // every rank's flags array (self included)
-    uint32_t epoch;
-    int32_t rank;
-    uint32_t n_items;
-    uint32_t* done;                  // this rank's per-item "stores issued" flags (local)
-    unsigned long long* prof;        // optional phase cycle counters (TGB_PIPE_PROF)
-};
-
-// Item c's stores are issued by the whole CTA: a GPU-scope release of a local
-// done flag (MEMBAR.GPU: cheap). The sys-scope fence that makes them visible to
-// peers is paid once per batch by the publisher CTA (pipe_publisher): a
-// MEMBAR.SYS costs microseconds regardless of what is outstanding
-// (tools/nvl_probe.cu), so one per item would serialise the pipeline.
-__device__ __forceinline__ void pipe_done(const PipeArgs& a, uint32_t c) {
-    __syncthreads();  // every thread's stores of item c happen-before thread 0's release
-    if (threadIdx.x == 0) {
-        asm volatile("fence.release.gpu;" ::: "memory");
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.done + c), "r"(a.epoch) : "memory");
-    }
-}
-
-// Publisher (CTA 0, warp 0): scans the local done flags of a window of items
-// ahead of the published prefix (completion order = item n-1-pos, iteration
-// major), acquires the newly completed ones, then ONE fence.release.sys covers
-// them all (cumulativity: the producers' stores happen-before their release,
-// which synchronises with this acquire) and their epoch flags go to every rank.
-// Items are published as soon as they complete, not in prefix order.
-constexpr uint32_t kPubWindow = 2048;  // items tracked ahead of the prefix (smem bitmap)
-__device__ __forceinline__ void pipe_publisher(const PipeArgs& a, int n_ranks) {
-    __shared__ uint32_t pub[kPubWindow / 32];  // published bits of [base, base + window)
-    __shared__ uint32_t fresh[kPubWindow / 32];
-    if (threadIdx.x >= 32) return;
-    const uint32_t lane = threadIdx.x, n = a.n_items;
-    for (uint32_t i = lane; i < kPubWindow / 32; i += 32) pub[i] = 0;
-    __syncwarp();
-    const long long t0 = clock64();
-    uint32_t base = 0, idle = 0;  // completion positions [0, base) are published
-    while (base < n) {
-        const uint32_t win = min(kPubWindow, n - base);
-        const uint32_t nwords = (win + 31) / 32;
-        uint32_t any = 0;
-        // relaxed loads, 8 words in flight per lane; the acquire is one fence below
-        for (uint32_t w0 = 0; w0 < nwords; w0 += 8) {
-            uint32_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t pos = base + (w0 + u) * 32 + lane;
-                v[u] = a.epoch - 1u;
-                if (w0 + u < nwords && pos < n && !((pub[w0 + u] >> lane) & 1u))
-                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v[u]) : "l"(a.done + (n - 1 - pos)) : "memory");
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t bits =
-                    __ballot_sync(0xffffffffu, static_cast<int32_t>(v[u] - a.epoch) >= 0);
-                if (lane == 0 && w0 + u < nwords) fresh[w0 + u] = bits;
-                any |= w0 + u < nwords ? bits : 0u;
-            }
-        }
-        __syncwarp();
-        if (any) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the observed flags
-        if (!any) {
-            if (++idle > 64) __nanosleep(200);
-            if ((idle & 1023) == 1023 && clock64() - t0 > 20000000000ll) {  // ~10 s
-                if (lane == 0) raise_error(a.k3.err, TGB_E_PEER_TIMEOUT, -1, ~0ull);
-                return;
-            }
-            continue;
-        }
-        idle = 0;
-        if (lane == 0) asm volatile("fence.release.sys;" ::: "memory");
-        __syncwarp();
-        for (uint32_t w = 0; w < nwords; ++w) {
-            uint32_t bits = fresh[w];
-            while (bits) {
-                const uint32_t b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const uint32_t c = n - 1 - (base + w * 32 + b);
-                if (lane < static_cast<uint32_t>(n_ranks)) {
-                    uint32_t* f = a.peer_flags[lane] + c * kMaxPeers + a.rank;
-                    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(a.epoch) : "memory");
-                }
-            }
-            if (lane == 0) pub[w] |= fresh[w];
-        }
-        __syncwarp();
-        // slide the window past the fully published words
-        uint32_t adv = 0;
-        while (adv * 32 < win) {
-            const uint32_t rem = n - base - adv * 32;  // > 0 while adv * 32 < win
-            const uint32_t valid = rem >= 32 ? 0xffffffffu : (1u << rem) - 1u;
-            if ((pub[adv] & valid) != valid) break;
-            ++adv;
-        }
-        if (adv) {
-            const uint32_t nw = kPubWindow / 32;
-            for (uint32_t i = lane; i < nw; i += 32) {
-                const uint32_t v = i + adv < nw ? pub[i + adv] : 0u;
-                __syncwarp();
-                pub[i] = v;
-            }
-            __syncwarp();
-            base += adv * 32;
-        }
-    }
-}
-
-__device__ __forceinline__ void pipe_wait(const PipeArgs& a, uint32_t c, int n) {
-    if (threadIdx.x == 0) {
-        const long long t0 = clock64();
-        for (int w = 0; w < n; ++w) {
-            const uint32_t* f = a.flags + c * kMaxPeers + w;
-            uint32_t v;
-            for (uint32_t spin = 0;; ++spin) {
-                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-                if (static_cast<int32_t>(v - a.epoch) >= 0) break;
-                if (spin > 64) __nanosleep(256);
-                if ((spin & 255) == 255 && clock64() - t0 > 20000000000ll) {  // ~10 s
-                    raise_error(a.k3.err, TGB_E_PEER_TIMEOUT, -1, static_cast<uint64_t>(w));
-                    break;
-                }
-            }
-        }
-    }
-    __syncthreads();
-}
-
-// Decode of one item in slices of kThreads * 4 code bytes (4K elements), run
-// from inside the ternarize loop of a newer item. prepare() must be called by
-// the whole CTA (two barriers); slice(i) and finish() touch no shared state
-// except the read-only tab/lut.
-template <int NW>
-struct SliceDecoder {
-    const K3Args* a;
-    const uint32_t* tab;
-    const float* lut;
-    const uint8_t* base0;  // worker 0's codes of the item; worker w at + w * stride
-    float* out;
-    uint32_t count, nbytes, n_slices, done;
-    bool vec_out, active;
-    uint32_t bad;
-
-    __device__ __forceinline__ void prepare(const K3Args& args, const LayerDev& L,
-                                            const ChunkDev& ch, const uint32_t* tab_, float* lut_,
-                                            float* sw) {
-        a = &args;
-        tab = tab_;
-        lut = lut_;
-        active = (L.flags & kLayerPassthrough) == 0;
-        done = 0;
-        bad = 0;
-        count = ch.count;
-        nbytes = (count + 3) >> 2;
-        n_slices = active ? (nbytes + 4 * kThreads - 1) / (4 * kThreads) : 0;
-        base0 = args.src + L.code_off + (ch.begin >> 2);
-        out = L.out + ch.begin;
-        vec_out = (L.flags & kLayerVecOut) != 0;
-        if (!active) {  // passthrough item: fp64 mean now (rare, small)
-            const uint64_t off = L.code_off + 4ull * ch.begin;
-            k3_passthrough([&](int w) { return reinterpret_cast<const float*>(args.src + args.stride * w + off); },
-                           NW, out, count, vec_out);
-            return;
-        }
-        const uint32_t tid = threadIdx.x;
-        if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(args.src + args.stride * tid) + L.slot);
-        __syncthreads();
-        if (tid <= 2 * NW) {
-            float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
-#pragma unroll
-            for (int w = 0; w < NW; ++w) s = fmaxf(s, sw[w]);
-            lut_[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - NW)),
-                                  args.inv_n);  // codec.hpp:296
-        }
-        __syncthreads();
-    }
-
-    __device__ __forceinline__ void slice(uint32_t i) {
-        if (i >= n_slices) return;
-        const uint32_t tid = threadIdx.x;
-        const uint32_t qb = i * 4 * kThreads;
-        uint32_t bw[NW][4];
-#pragma unroll
-        for (int w = 0; w < NW; ++w)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t q = qb + tid + u * kThreads;
-                bw[w][u] = q < nbytes ? __ldcs(base0 + a->stride * w + q) : 0u;
-            }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                acc += tab[bw[w][u]];
-                bad |= bw[w][u] & (bw[w][u] >> 1);
-            }
-            const float4 o = make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
-                                         lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
-            const uint32_t q = qb + tid + u * kThreads;
-            const uint32_t b4 = 4 * q;
-            if (vec_out && b4 + 4 <= count) {
-                __stcs(reinterpret_cast<float4*>(out + b4), o);
-            } else if (q < nbytes) {
-                if (b4 + 0 < count) out[b4 + 0] = o.x;
-                if (b4 + 1 < count) out[b4 + 1] = o.y;
-                if (b4 + 2 < count) out[b4 + 2] = o.z;
-                if (b4 + 3 < count) out[b4 + 3] = o.w;
-            }
-        }
-        done = i + 1;
-    }
-
-    // remaining slices, then corrupt-code reporting
-    __device__ __forceinline__ void finish(const LayerDev& L, const ChunkDev& ch) {
-        for (uint32_t i = done; i < n_slices; ++i) slice(i);
-        if (active && (bad & 0x55u)) {
-            for (uint32_t q = 0; q < nbytes; ++q)
-                for (int w = 0; w < NW; ++w) {
-                    const uint8_t by = base0[a->stride * w + q];
-                    const uint32_t bb = by & (by >> 1) & 0x55u;
-                    if (bb) {
-                        raise_error(a->err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
-                                    block_rng_base(L) + ch.begin + 4ull * q + ((__ffs(bb) - 1) >> 1));
-                        return;
-                    }
-                }
-        }
-        active = false;
-    }
-};
-
-template <int NW, int kMinBlocks = 3, int U = 4>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k23_pipelined(TableSource src, PipeArgs a) {
-    __shared__ __align__(16) uint8_t stage[kStageBytes];
-    __shared__ uint32_t tab[256];
-    __shared__ float lut[2 * NW + 1];
-    __shared__ float sw[NW];
-    // CTA 0 (dispatched first, so resident whenever any producer is): publisher
-    const uint32_t G = gridDim.x - 1, n = a.n_items;
-    if (blockIdx.x == 0) {
-        pipe_publisher(a, NW);
-        return;
-    }
-    const uint32_t j0 = blockIdx.x - 1;
-    tab[threadIdx.x] = lane_biased(threadIdx.x);
-    // items walk last-to-first (re-read K1's L2-resident tail first)
-    auto item = [&](uint32_t k) { return n - 1 - (j0 + k * G); };
-    SliceDecoder<NW> dec;
-    dec.n_slices = 0;
-    uint32_t k = 0;
-    // optional phase profile (TGB_PIPE_PROF): clock64 cycles per phase, thread 0
-    long long tp = a.prof ? clock64() : 0;
-    auto mark = [&](int ph) {
-        if (a.prof && threadIdx.x == 0) {
-            const long long t = clock64();
-            atomicAdd(a.prof + ph, static_cast<unsigned long long>(t - tp));
-            tp = t;
-        }
-    };
-    for (; j0 + k * G < n; ++k) {
-        const uint32_t c = item(k);
-        ChunkDev ch;
-        LayerDev L;
-        src.get(c, ch, L);
-        ChunkDev dch;
-        LayerDev dL;
-        if (k >= 2) {  // decode item k-2 in slices during this item's ternarize loop
-            src.get(item(k - 2), dch, dL);
-            pipe_wait(a, item(k - 2), NW);
-            mark(0);
-            dec.prepare(a.k3, dL, dch, tab, lut, sw);
-        } else {
-            __syncthreads();  // stage is free (previous item's stores were issued)
-        }
-        mark(1);
-        // U = 4: one decode slice per loop iteration; U = 2: every other iteration
-        const uint32_t nb = k2_code_chunk<false, U, false>(
-            a.k2, L, ch, c, stage, nullptr, [&](uint32_t i) {
-                if (k >= 2 && (U == 4 || (i & 1) == 0)) dec.slice(U == 4 ? i : i >> 1);
-            });
-        mark(2);
-        if (k >= 2) dec.finish(dL, dch);
-        mark(3);
-        mark(4);
-        if (nb) k2_store_chunk(a.k2, L, ch, c, stage, nb);
-        pipe_done(a, c);
-        mark(5);
-    }
-    for (uint32_t j = k >= 2 ? k - 2 : 0; j < k; ++j) {
-        ChunkDev dch;
-        LayerDev dL;
-        src.get(item(j), dch, dL);
-        pipe_wait(a, item(j), NW);
-        mark(6);
-        dec.prepare(a.k3, dL, dch, tab, lut, sw);
-        dec.finish(dL, dch);
-        mark(7);
-    }
-}
-
-// K3 variant (TGB_K3V=1, A/B): the chunk's code bytes of all NW workers are
-// first staged in shared memory with 16-byte loads (NW independent uint4 per
-// thread in flight, 16x fewer load instructions than byte loads), then decoded
-// from shared memory with the same byte -> LUT arithmetic as k3_decode_nw.
-template <int NW, bool kOpt = false, bool kArith = false>
+// Plan K3, shared scalers, N <= 8 (one NVSwitch box): the chunk's code bytes of
+// all NW workers are first staged in shared memory with 16-byte loads (NW
+// independent uint4 per thread in flight, 16x fewer load instructions than byte
+// loads), then decoded from shared memory: per code byte the NW bytes are
+// summed as SWAR lanes (biased sums N + sum_w code_w) and every lane decodes to
+// (s * float(sum)) * invN with s = max over workers (codec.hpp:289-296,
+// cluster.hpp:195-196) computed in registers (no table lookups).
+template <int NW, bool kOpt = false>
 __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3Args a) {
+    if (a.gate && exchange_failed(a.err)) return;  // skewed / missing peer: keep the outputs
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
@@ -1347,8 +846,6 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
     }
     constexpr uint32_t kStage = kChunk3 / 4;  // code bytes per worker
     __shared__ __align__(16) uint8_t codes[NW][kStage];
-    __shared__ uint32_t tab[256];
-    __shared__ float lut[2 * NW + 1];
     __shared__ float sw[NW];
     const uint32_t tid = threadIdx.x;
     const uint32_t count = ch.count;
@@ -1367,7 +864,6 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
                 v[w][r] = i < n16 ? __ldcs(b4 + i) : make_uint4(0, 0, 0, 0);
             }
         }
-        tab[tid] = lane_biased(tid);
         if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
 #pragma unroll
         for (int w = 0; w < NW; ++w)
@@ -1382,24 +878,14 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
                 codes[w][i] = a.src[a.stride * w + L.code_off + (ch.begin >> 2) + i];
     }
     __syncthreads();
-    if (tid <= 2 * NW) {
-        float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s = fmaxf(s, sw[w]);
-        lut[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - NW)),
-                             a.inv_n);  // codec.hpp:296
-    }
-    __syncthreads();
     OptDev od{};
     if (kOpt) od = a.optd[ch.layer];
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
     uint32_t bad = 0;
-    float s_max = 0.0f;  // kArith: the LUT entries computed in registers
-    if (kArith) {
+    float s_max = 0.0f;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
-    }
+    for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
     auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
         return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
     };
@@ -1408,13 +894,11 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             const uint32_t b = codes[w][q];
-            acc += kArith ? lane_biased_swar(b) : tab[b];
+            acc += lane_biased_swar(b);
             bad |= b & (b >> 1);
         }
-        const float4 o = kArith ? make_float4(val(acc & 0xffu), val((acc >> 8) & 0xffu),
-                                              val((acc >> 16) & 0xffu), val(acc >> 24))
-                                : make_float4(lut[acc & 0xffu], lut[(acc >> 8) & 0xffu],
-                                              lut[(acc >> 16) & 0xffu], lut[acc >> 24]);
+        const float4 o = make_float4(val(acc & 0xffu), val((acc >> 8) & 0xffu),
+                                     val((acc >> 16) & 0xffu), val(acc >> 24));
         const uint32_t b4 = 4 * q;
         if (kOpt) {  // fused optimizer: the averaged gradient is never written
             const uint64_t e = ch.begin + b4;
@@ -1443,159 +927,51 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
 }
 
 // ====================================================== sharded exchange
-// N >= 3 with shared scalers (TGB_SHARD): instead of every rank receiving and
-// decoding all N code streams, rank r owns a contiguous range of K2 chunks
-// (a parameter-server shard, cluster.hpp:167-221 partitioned over the ranks).
-// K2 stores each chunk's codes into its owner's gather buffer only; K3a (here)
-// sums the N workers' codes of the owned chunks into biased integer sums
+// Shared scalers, N <= 8 (the default from N = 5): instead of every rank
+// receiving and decoding all N code streams, rank r owns a contiguous range of
+// K2 chunks (a parameter-server shard, cluster.hpp:167-221 partitioned over the
+// ranks). K2 stores each chunk's codes into its owner's gather buffer only; K3a
+// (owner) sums the N workers' codes of the owned chunks into biased integer sums
 // N + sum_w code_w in [0, 2N] -- the reference's SharedSumBlock sums
-// (wire.hpp:79-97) -- packed 4 bits (N <= 7) or 8 bits per element, and stores
-// them into every rank's sums buffer; K3b decodes the sums on every rank with
-// the same LUT (s*float(sum))*invN. Passthrough chunks: K3a writes the final
-// fp64 worker-order mean (codec.hpp:269-279) and K3b copies it.
+// (wire.hpp:79-97) -- packs them as base-(2N+1) digits, radix_m per u32 word
+// (little-endian digit order, as the reference's u64 words, wire.hpp:103-145:
+// 3.2 bits per element at N = 4, 4.57 at N = 8 instead of 4 / 8), and stores the
+// words into every rank's sums buffer; K3b decodes the sums on every rank to
+// (s*float(sum))*invN. Passthrough chunks: K3a writes the final fp64
+// worker-order mean (codec.hpp:269-279) and K3b copies it.
 struct ShardArgs {
     const uint8_t* src;            // own gather buffer (N push areas, stride apart)
     uint64_t stride;
     uint8_t* sums[kMaxPeers];      // every rank's sums buffer (this step's parity)
     const uint8_t* own_sums;
     int32_t n_workers;
-    int32_t nib;                   // 4-bit sums (N <= 7), else 8-bit
+    int32_t radix_m;
+    uint32_t chunk12;
+    uint32_t sum_region;
     float inv_n;
     ErrWord* err;
-    int32_t bulk = 0;  // K3a: packed sums to every rank as TMA bulk copies
 };
 
-__device__ __forceinline__ uint32_t pack_nib(uint32_t acc) {  // 4 byte lanes -> 4 nibbles
-    return (acc & 0xFu) | ((acc >> 4) & 0xF0u) | ((acc >> 8) & 0xF00u) | ((acc >> 12) & 0xF000u);
+// byte offset of chunk ch's sums region (a block's chunks are chunk12 apart)
+__device__ __forceinline__ uint64_t sums_offset(const ShardArgs& a, const LayerDev& L,
+                                                const ChunkDev& ch) {
+    return 16ull * L.sum_off16 + (ch.begin / a.chunk12) * static_cast<uint64_t>(a.sum_region);
 }
 
-// K3a: one CTA per owned K2 chunk (<= kChunk12 elements). Each thread takes
-// 16-byte groups of code bytes (one uint4 per worker, all NW in flight),
-// builds the 16 packed sums in registers, stages them in shared memory, and
-// the CTA then writes the chunk's sums to every rank with 16-byte stores
-// (NVLink stores stay full-width).
-// K3 over radix-3 wire codes (fused exchange, N >= 3, shared scalers): stage the
-// chunk's r3 bytes of all N workers in shared memory (16-B loads), then per group of
-// 4 bytes (20 elements) sum N table words (5 biased lanes (1 + v) per byte, 8 bits
-// each, <= 2N) and decode every lane to (s * float(sum)) * invN (codec.hpp:296,
-// wire.hpp:220; s = max over workers, cluster.hpp:195-196) -- the same two rounded
-// multiplies as the 2-bit kernels, so the output is bit-identical.
-template <int NW, bool kOpt>
-__global__ void __launch_bounds__(kThreads) k3_decode_r3(TableSource src, K3Args a) {
-    ChunkDev ch;
-    LayerDev L;
-    src.get(blockIdx.x, ch, L);
-    constexpr uint32_t kStage = kChunk3R3 / 5;  // r3 bytes per worker and chunk (16-B multiple)
-    __shared__ __align__(16) uint8_t codes[NW][kStage];
-    __shared__ unsigned long long tab5[256];
-    __shared__ float sw[NW];
-    const uint32_t tid = threadIdx.x;
-    const uint32_t count = ch.count;
-    const uint32_t nr3 = (count + 4) / 5;
-    const uint32_t n16 = (nr3 + 15) >> 4;  // the block region is padded to 16 B
-    {
-        constexpr int R = (kStage / 16 + kThreads - 1) / kThreads;
-        uint4 v[NW][R];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const uint4* b4 = reinterpret_cast<const uint4*>(a.src + a.stride * w + L.code_off +
-                                                             ch.begin / 5);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const uint32_t i = tid + r * kThreads;
-                v[w][r] = i < n16 ? __ldcs(b4 + i) : make_uint4(0, 0, 0, 0);
-            }
-        }
-        {
-            unsigned long long t = 0;  // byte -> 5 lanes of 1 + v (digit 0 -> 1, 1 -> 2, 2 -> 0)
-            uint32_t x = tid;
-#pragma unroll
-            for (int i = 0; i < 5; ++i) {
-                const uint32_t d = x % 3u;
-                x /= 3u;
-                t |= static_cast<unsigned long long>(d == 0 ? 1u : (d == 1 ? 2u : 0u)) << (8 * i);
-            }
-            tab5[tid] = t;  // bytes >= 243 are flagged separately
-        }
-        if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
-#pragma unroll
-        for (int w = 0; w < NW; ++w)
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const uint32_t i = tid + r * kThreads;
-                if (i < n16) reinterpret_cast<uint4*>(codes[w])[i] = v[w][r];
-            }
-    }
-    __syncthreads();
-    float s_max = 0.0f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
-    auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
-        return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
-    };
-    OptDev od{};
-    if (kOpt) od = a.optd[ch.layer];
-    float* out = L.out + ch.begin;
-    const bool vec_out = (L.flags & kLayerVecOut) != 0;
-    uint32_t bad = 0, bad_g = 0;
-    const uint32_t ng = (nr3 + 3) >> 2;
-    for (uint32_t g = tid; g < ng; g += kThreads) {
-        unsigned long long acc[4] = {0, 0, 0, 0};
-        const uint32_t nb = nr3 - 4 * g < 4 ? nr3 - 4 * g : 4;
-        const uint32_t mask = nb >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nb)) - 1u);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t word = reinterpret_cast<const uint32_t*>(codes[w])[g];
-            const uint32_t b = __vcmpgeu4(word, 0xF3F3F3F3u) & mask;  // byte >= 243: corrupt
-            if (b && !bad) bad_g = g;
-            bad |= b;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] += tab5[(word >> (8 * k)) & 0xFFu];
-        }
-        const uint32_t e0 = 20 * g;
-        float v[20];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int i = 0; i < 5; ++i)
-                v[5 * k + i] = val(static_cast<uint32_t>(acc[k] >> (8 * i)) & 0xFFu);
-        if (kOpt) {
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                const uint32_t e = e0 + 4 * q;
-                if (e >= count) break;
-                const uint64_t ge = ch.begin + e;
-                opt_apply4(a.opt, od.w + ge, od.s1 ? od.s1 + ge : nullptr,
-                           od.s2 ? od.s2 + ge : nullptr,
-                           make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]),
-                           od.vec != 0, count - e < 4 ? count - e : 4);
-            }
-        } else if (vec_out && e0 + 20 <= count) {
-            float4* o4 = reinterpret_cast<float4*>(out + e0);
-#pragma unroll
-            for (int q = 0; q < 5; ++q)
-                __stcs(o4 + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-        } else {
-#pragma unroll
-            for (int i = 0; i < 20; ++i)
-                if (e0 + i < count) out[e0 + i] = v[i];
-        }
-    }
-    if (bad)  // a byte >= 243 cannot come from K2: reported at its group's first element
-        raise_error(a.err, TGB_E_CORRUPT_CODE, static_cast<int32_t>(L.tensor),
-                    block_rng_base(L) + ch.begin + 20ull * bad_g);
-}
+constexpr uint32_t kRadixWordsMax = (kChunk12 + 6) / 7;  // radix_m >= 7 for N <= 8
+constexpr uint32_t kK3aSmem = kChunk12 + 4 * (kRadixWordsMax + 4);
 
 template <int NW>
 __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs a) {
+    if (exchange_failed(a.err)) return;  // the codes of this step are incomplete
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
     const uint32_t tid = threadIdx.x;
-    const uint64_t soff = 16ull * L.sum_off16;
     const uint32_t count = ch.count;
     if (L.flags & kLayerPassthrough) {  // fp64 worker-order mean (codec.hpp:269-279)
         const uint64_t off = L.code_off + 4ull * ch.begin;
+        const uint64_t soff = 16ull * L.sum_off16 + 4ull * ch.begin;
         const double dn = static_cast<double>(NW);
         const uint32_t n4 = count >> 2;
         for (uint32_t i = tid; i < n4; i += kThreads) {
@@ -1611,8 +987,7 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
             const float4 o = make_float4(static_cast<float>(s0 / dn), static_cast<float>(s1 / dn),
                                          static_cast<float>(s2 / dn), static_cast<float>(s3 / dn));
 #pragma unroll
-            for (int p = 0; p < NW; ++p)
-                reinterpret_cast<float4*>(a.sums[p] + soff + 4ull * ch.begin)[i] = o;
+            for (int p = 0; p < NW; ++p) reinterpret_cast<float4*>(a.sums[p] + soff)[i] = o;
         }
         for (uint32_t i = 4 * n4 + tid; i < count; i += kThreads) {
             double sum = 0.0;
@@ -1622,23 +997,21 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
                                          reinterpret_cast<const float*>(a.src + a.stride * w + off)[i]));
             const float v = static_cast<float>(sum / dn);
 #pragma unroll
-            for (int p = 0; p < NW; ++p)
-                reinterpret_cast<float*>(a.sums[p] + soff + 4ull * ch.begin)[i] = v;
+            for (int p = 0; p < NW; ++p) reinterpret_cast<float*>(a.sums[p] + soff)[i] = v;
         }
         return;
     }
-    constexpr uint32_t kMaxBytes = kChunk12 / 4;  // code bytes per chunk
-    __shared__ __align__(16) uint32_t stage[kMaxBytes];  // 4 B of sums per code byte (max)
-    __shared__ uint32_t tab[256];
-    tab[tid] = lane_biased(tid);
-    __syncthreads();
+    constexpr uint32_t kBase = 2 * NW + 1;
+    extern __shared__ __align__(16) uint8_t k3a_dsm[];  // kK3aSmem bytes (dynamic: > 48 KB)
+    uint8_t* sums = k3a_dsm;                                           // biased sum per element
+    uint32_t* words = reinterpret_cast<uint32_t*>(k3a_dsm + kChunk12);  // packed digits
     const uint32_t nbytes = (count + 3) >> 2;
     const uint32_t n16 = nbytes >> 4;
     const uint8_t* base[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) base[w] = a.src + a.stride * w + L.code_off + (ch.begin >> 2);
     uint32_t bad = 0;
-    uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
+    // 16 code bytes (64 elements) per worker per step: SWAR byte-lane sums
     for (uint32_t i = tid; i < n16; i += kThreads) {
         uint4 v[NW];
 #pragma unroll
@@ -1654,48 +1027,39 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
             bad |= (wd[0] & (wd[0] >> 1)) | (wd[1] & (wd[1] >> 1)) | (wd[2] & (wd[2] >> 1)) |
                    (wd[3] & (wd[3] >> 1));
         }
-        if (a.nib) {
-            uint4 o0, o1;
-            o0.x = pack_nib(acc[0]) | (pack_nib(acc[1]) << 16);
-            o0.y = pack_nib(acc[2]) | (pack_nib(acc[3]) << 16);
-            o0.z = pack_nib(acc[4]) | (pack_nib(acc[5]) << 16);
-            o0.w = pack_nib(acc[6]) | (pack_nib(acc[7]) << 16);
-            o1.x = pack_nib(acc[8]) | (pack_nib(acc[9]) << 16);
-            o1.y = pack_nib(acc[10]) | (pack_nib(acc[11]) << 16);
-            o1.z = pack_nib(acc[12]) | (pack_nib(acc[13]) << 16);
-            o1.w = pack_nib(acc[14]) | (pack_nib(acc[15]) << 16);
-            reinterpret_cast<uint4*>(stage)[2 * i] = o0;
-            reinterpret_cast<uint4*>(stage)[2 * i + 1] = o1;
-        } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                reinterpret_cast<uint4*>(stage)[4 * i + k] =
-                    make_uint4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
-        }
+        for (int k = 0; k < 4; ++k)
+            reinterpret_cast<uint4*>(sums)[4 * i + k] =
+                make_uint4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
     }
     for (uint32_t q = (n16 << 4) + tid; q < nbytes; q += kThreads) {  // tail code bytes
         uint32_t acc = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             const uint32_t bw = base[w][q];
-            acc += tab[bw];
+            acc += lane_biased_swar(bw);
             bad |= bw & (bw >> 1);
         }
-        if (a.nib)
-            st16[q] = static_cast<uint16_t>(pack_nib(acc));
-        else
-            stage[q] = acc;
+        reinterpret_cast<uint32_t*>(sums)[q] = acc;
     }
     __syncthreads();
-    const uint32_t sbytes = nbytes * (a.nib ? 2u : 4u);
-    const uint64_t doff = soff + (a.nib ? (ch.begin >> 1) : ch.begin);
-    if (a.bulk)
-        bulk_copy_out(reinterpret_cast<const uint8_t*>(stage), [&](int p) { return a.sums[p] + doff; },
-                      NW, sbytes);
-    else
-#pragma unroll
-        for (int p = 0; p < NW; ++p)
-            copy_out(reinterpret_cast<const uint8_t*>(stage), a.sums[p] + doff, sbytes);
+    // radix words: word k holds elements [k m, (k+1) m), digit 0 = lowest (Horner
+    // from the highest digit; digits past the chunk's end are 0)
+    const uint32_t m = static_cast<uint32_t>(a.radix_m);
+    const uint32_t nw = (count + m - 1) / m;
+    for (uint32_t k = tid; k < nw; k += kThreads) {
+        const uint32_t e0 = k * m;
+        uint32_t word = 0;
+        for (uint32_t d = m; d-- > 0;) {
+            const uint32_t e = e0 + d;
+            word = word * kBase + (e < count ? static_cast<uint32_t>(sums[e]) : 0u);
+        }
+        words[k] = word;
+    }
+    __syncthreads();
+    const uint64_t doff = sums_offset(a, L, ch);
+    bulk_copy_out(reinterpret_cast<const uint8_t*>(words), [&](int p) { return a.sums[p] + doff; },
+                  NW, 4 * nw);
     if (bad & 0x55555555u) {  // rare: locate the chunk's first corrupt element
         for (uint32_t q = 0; q < nbytes; ++q) {
             for (int w = 0; w < NW; ++w) {
@@ -1710,69 +1074,62 @@ __global__ void __launch_bounds__(kThreads) k3_reduce(TableSource src, ShardArgs
     }
 }
 
-template <bool kNib>
+// K3b: every rank, every chunk (K2's table): radix words -> biased sums in shared
+// memory -> (s * float(sum)) * invN as float4 streams (codec.hpp:296, wire.hpp:220)
+template <int NW>
 __global__ void __launch_bounds__(kThreads) k3_expand(TableSource src, ShardArgs a) {
+    if (exchange_failed(a.err)) return;
     ChunkDev ch;
     LayerDev L;
     src.get(blockIdx.x, ch, L);
     const uint32_t tid = threadIdx.x;
-    const uint64_t soff = 16ull * L.sum_off16;
     float* out = L.out + ch.begin;
     const bool vec_out = (L.flags & kLayerVecOut) != 0;
     const uint32_t count = ch.count;
     if (L.flags & kLayerPassthrough) {
-        const float* v = reinterpret_cast<const float*>(a.own_sums + soff) + ch.begin;
+        const float* v = reinterpret_cast<const float*>(a.own_sums + 16ull * L.sum_off16) + ch.begin;
         const uint32_t n4 = vec_out ? (count >> 2) : 0u;
         for (uint32_t i = tid; i < n4; i += kThreads)
             __stcs(reinterpret_cast<float4*>(out) + i, __ldcs(reinterpret_cast<const float4*>(v) + i));
         for (uint32_t i = 4 * n4 + tid; i < count; i += kThreads) out[i] = v[i];
         return;
     }
-    const int N = a.n_workers;
-    __shared__ float lut[2 * kMaxPeers + 1];
-    __shared__ float sw[kMaxPeers];
-    if (tid < static_cast<uint32_t>(N))
-        sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
-    __syncthreads();
-    if (tid <= static_cast<uint32_t>(2 * N)) {
-        float s = 0.0f;  // cluster.hpp:195-196 / codec.hpp:289-291
-        for (int w = 0; w < N; ++w) s = fmaxf(s, sw[w]);
-        lut[tid] = __fmul_rn(__fmul_rn(s, static_cast<float>(static_cast<int>(tid) - N)),
-                             a.inv_n);  // codec.hpp:296
+    constexpr uint32_t kBase = 2 * NW + 1;
+    __shared__ __align__(16) uint8_t sums[kChunk12 + 64];
+    __shared__ float sw[NW];
+    if (tid < NW) sw[tid] = __ldg(reinterpret_cast<const float*>(a.src + a.stride * tid) + L.slot);
+    const uint32_t m = static_cast<uint32_t>(a.radix_m);
+    const uint32_t nw = (count + m - 1) / m;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(a.own_sums + sums_offset(a, L, ch));
+    for (uint32_t k = tid; k < nw; k += kThreads) {
+        uint32_t x = __ldcs(words + k);
+        const uint32_t e0 = k * m;
+        for (uint32_t d = 0; d < m; ++d) {  // e0 + d < count + m <= kChunk12 + 64
+            const uint32_t q = x / kBase;
+            sums[e0 + d] = static_cast<uint8_t>(x - q * kBase);
+            x = q;
+        }
     }
     __syncthreads();
-    const uint32_t nbytes = (count + 3) >> 2;  // one packed word per 4 elements
-    constexpr int U = 4;
-    constexpr uint32_t kBits = kNib ? 4u : 8u, kMask = kNib ? 0xFu : 0xFFu;
-    for (uint32_t qb = 0; qb < nbytes; qb += U * kThreads) {
-        uint32_t v[U];
+    float s_max = 0.0f;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t q = qb + tid + u * kThreads;
-            if (kNib)
-                v[u] = q < nbytes ? __ldcs(reinterpret_cast<const uint16_t*>(a.own_sums + soff +
-                                                                              (ch.begin >> 1)) + q)
-                                  : 0u;
-            else
-                v[u] = q < nbytes ? __ldcs(reinterpret_cast<const uint32_t*>(a.own_sums + soff +
-                                                                              ch.begin) + q)
-                                  : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t q = qb + tid + u * kThreads;
-            const float4 o = make_float4(lut[v[u] & kMask], lut[(v[u] >> kBits) & kMask],
-                                         lut[(v[u] >> (2 * kBits)) & kMask],
-                                         lut[(v[u] >> (3 * kBits)) & kMask]);
-            const uint32_t b4 = 4 * q;
-            if (vec_out && b4 + 4 <= count) {
-                __stcs(reinterpret_cast<float4*>(out + b4), o);
-            } else if (q < nbytes) {
-                if (b4 + 0 < count) out[b4 + 0] = o.x;
-                if (b4 + 1 < count) out[b4 + 1] = o.y;
-                if (b4 + 2 < count) out[b4 + 2] = o.z;
-                if (b4 + 3 < count) out[b4 + 3] = o.w;
-            }
+    for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
+    auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
+        return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
+    };
+    const uint32_t nbytes = (count + 3) >> 2;
+    for (uint32_t q = tid; q < nbytes; q += kThreads) {
+        const uint32_t v = reinterpret_cast<const uint32_t*>(sums)[q];
+        const float4 o = make_float4(val(v & 0xffu), val((v >> 8) & 0xffu), val((v >> 16) & 0xffu),
+                                     val(v >> 24));
+        const uint32_t b4 = 4 * q;
+        if (vec_out && b4 + 4 <= count) {
+            __stcs(reinterpret_cast<float4*>(out + b4), o);
+        } else {
+            if (b4 + 0 < count) out[b4 + 0] = o.x;
+            if (b4 + 1 < count) out[b4 + 1] = o.y;
+            if (b4 + 2 < count) out[b4 + 2] = o.z;
+            if (b4 + 3 < count) out[b4 + 3] = o.w;
         }
     }
 }
@@ -1819,35 +1176,13 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
             p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors, p.nnz};
     const TableSource src{chunks};
-    if (p.keep_chunks && p.variant == 0) {  // TGB_K1KEEP (A/B): tail units stay in L2 for K2's reverse walk
+    if (p.keep_chunks) {  // the launch's last units stay in L2 for K2's reverse walk
         o.keep_from = n_chunks - (p.keep_chunks < n_chunks ? p.keep_chunks : n_chunks);
         k1_stats<TableSource, 8, 1, 4, true><<<n_chunks, kThreads, 0, st>>>(src, o);
         return launch_status();
     }
-    switch (p.variant) {  // TGB_K1V (A/B): loads in flight per thread x fp64 chains
-        case 1: k1_stats<TableSource, 4, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 2: k1_stats<TableSource, 4, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 3: k1_stats<TableSource, 8, 2><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 4: k1_stats<TableSource, 8, 1, 6><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 5: k1_stats<TableSource, 4, 1, 8><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 6: k1_stats<TableSource, 6, 1, 6><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 8: k1_stats<TableSource, 4, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 9: k1_stats<TableSource, 8, 1><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-        case 10: {
-            constexpr int S = 3;
-            const size_t smem = S * kK1TileBytes + 2 * S * sizeof(uint64_t);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k1_stats_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-                attr = true;
-            }
-            k1_stats_tma<S><<<n_chunks, kThreads + 32, smem, st>>>(src, o);
-            break;
-        }
-        default:  // 8 float4 in flight per thread, <= 64 registers: 4 CTAs/SM (tools/k1_probe.py)
-            k1_stats<TableSource, 8, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o); break;
-    }
+    // 8 float4 in flight per thread, <= 64 registers: 4 CTAs/SM (tools/k1_probe.py)
+    k1_stats<TableSource, 8, 1, 4><<<n_chunks, kThreads, 0, st>>>(src, o);
     return launch_status();
 }
 
@@ -1867,8 +1202,8 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
 // K2 launch; with a.pdl it is K1's programmatic dependent (same stream, launched
 // while K1's last wave drains; the kernel's griddepcontrol.wait orders it after K1)
 template <class Kern>
-static void k2_go(Kern k, uint32_t grid, cudaStream_t st, const TableSource& src,
-                  const K2Args& a) {
+static cudaError_t k2_go(Kern k, uint32_t grid, cudaStream_t st, const TableSource& src,
+                         const K2Args& a) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -1879,58 +1214,33 @@ static void k2_go(Kern k, uint32_t grid, cudaStream_t st, const TableSource& src
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = a.pdl ? 1 : 0;
-    (void)cudaLaunchKernelEx(&cfg, k, src, a);
+    return cudaLaunchKernelEx(&cfg, k, src, a);
 }
+
+// K2 instantiations: unfused (codes only, 3 CTAs/SM) and, at N == 1, with the
+// decode fused (64 registers, 4 CTAs/SM: 190.9 vs 202.9 us at 3 CTAs/SM on
+// VGG-16, the fused kernel is latency-bound), with or without the optimizer
+#define TGB_K2_PLAIN k2_ternarize<TableSource, 3, false, false>
+#define TGB_K2_FUSED k2_ternarize<TableSource, 4, true, false>
+#define TGB_K2_FUSED_OPT k2_ternarize<TableSource, 3, true, true>
 
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K2Args a{p.push, p.slots, p.bounds, p.err, p.t, p.reverse, 0, 0.0f, 0, p.dst};
     a.nnz = p.nnz;
-    a.bulk = p.bulk;
     a.shard_n = p.shard_n;
     a.pdl = p.pdl;
+    a.keep_from = p.keep_from;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     const TableSource src{chunks};
-    if (p.r3) {  // fused exchange with radix-3 wire codes (N >= 3)
-        k2_go(k2_ternarize<TableSource, false, 4, 3, false, false, false, true>, n_chunks, st, src, a);
-        return launch_status();
+    if (p.fuse_decode && p.optd) {  // N == 1 fused decode -> optimizer
+        a.optd = p.optd;
+        a.opt = p.opt;
+        return k2_go(TGB_K2_FUSED_OPT, n_chunks, st, src, a);
     }
-    if (p.fuse_decode) {
-        if (p.optd) {  // N == 1 fused decode -> optimizer
-            a.optd = p.optd;
-            a.opt = p.opt;
-            if (p.direct)
-                k2_go(k2_ternarize<TableSource, false, 4, 3, true, true, true>, n_chunks, st, src, a);
-            else
-                k2_go(k2_ternarize<TableSource, false, 4, 3, true, true>, n_chunks, st, src, a);
-        } else if (p.direct) {
-            k2_go(k2_ternarize<TableSource, false, 4, 3, true, false, true>, n_chunks, st, src, a);
-        } else {
-            switch (p.variant) {  // TGB_K2V (A/B): key schedule x occupancy x bytes per thread
-                case 1: k2_go(k2_ternarize<TableSource, true, 4, 3, true>, n_chunks, st, src, a); break;
-                case 2: k2_go(k2_ternarize<TableSource, true, 4, 4, true>, n_chunks, st, src, a); break;
-                case 4: k2_go(k2_ternarize<TableSource, false, 4, 3, true>, n_chunks, st, src, a); break;
-                case 5: k2_go(k2_ternarize<TableSource, false, 2, 4, true>, n_chunks, st, src, a); break;
-                case 6: k2_go(k2_ternarize<TableSource, false, 4, 5, true>, n_chunks, st, src, a); break;
-                // default (= 3): 64 registers, 4 CTAs/SM: 190.9 vs 202.9 us at 3 CTAs/SM
-                // (VGG-16, N = 1, tools/k2_fused_ab.sh): the fused kernel is latency-bound
-                default: k2_go(k2_ternarize<TableSource, false, 4, 4, true>, n_chunks, st, src, a); break;
-            }
-        }
-        return launch_status();
-    }
-    if (p.direct) {
-        k2_go(k2_ternarize<TableSource, false, 4, 3, false, false, true>, n_chunks, st, src, a);
-        return launch_status();
-    }
-    switch (p.variant) {  // TGB_K2V (A/B): Philox key schedule x occupancy
-        case 1: k2_go(k2_ternarize<TableSource, true, 4, 3>, n_chunks, st, src, a); break;
-        case 2: k2_go(k2_ternarize<TableSource, true, 4, 4>, n_chunks, st, src, a); break;
-        case 3: k2_go(k2_ternarize<TableSource, false, 4, 4>, n_chunks, st, src, a); break;
-        default: k2_go(k2_ternarize<TableSource, false, 4, 3>, n_chunks, st, src, a); break;
-    }
-    return launch_status();
+    if (p.fuse_decode) return k2_go(TGB_K2_FUSED, n_chunks, st, src, a);
+    return k2_go(TGB_K2_PLAIN, n_chunks, st, src, a);
 }
 
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st) {
@@ -1942,84 +1252,91 @@ cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t 
     return launch_status();
 }
 
+template <class K>
+static uint32_t k12_grid(K kernel, uint32_t units) {
+    static int cap[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 1;
+    if (!cap[dev]) {
+        int sms = 0, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, 0);
+        cap[dev] = sms * (per > 0 ? per : 1);
+    }
+    return units < static_cast<uint32_t>(cap[dev]) ? (units ? units : 1u)
+                                                   : static_cast<uint32_t>(cap[dev]);
+}
+
+cudaError_t launch_k12_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_k1,
+                             uint32_t n_k2, const K1Launch& p1, const K2Launch& p2,
+                             uint32_t* ready, uint32_t epoch, cudaStream_t st) {
+    if (n_k2 == 0) return cudaSuccess;
+    K1Out o{p1.partials, p1.layer_done, p1.global_done, p1.bounds, p1.slots, p1.err,
+            p1.clip_factor, p1.global_bucketing, p1.n_layers, p1.n_active_layers, layers,
+            p1.push, p1.tensors, nullptr};
+    o.ready = ready;
+    o.ready_global = ready + p1.n_tensors;
+    o.epoch = epoch;
+    K2Args a{p2.push, p2.slots, p2.bounds, p2.err, p2.t, 0, 0, 0.0f, 0, p2.dst};
+    a.nnz = p2.nnz;
+    a.shard_n = p2.shard_n;
+    for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p2.shard_bounds[r];
+    const TableSource src{chunks};
+    const uint32_t units = n_k1 > n_k2 ? n_k1 : n_k2;
+    if (p2.fuse_decode && p2.optd) {
+        a.optd = p2.optd;
+        a.opt = p2.opt;
+        k12_fused<true, true><<<k12_grid(k12_fused<true, true>, units), kThreads, 0, st>>>(
+            src, o, a, n_k1, n_k2);
+    } else if (p2.fuse_decode) {
+        k12_fused<true><<<k12_grid(k12_fused<true>, units), kThreads, 0, st>>>(src, o, a, n_k1,
+                                                                             n_k2);
+    } else {
+        k12_fused<false><<<k12_grid(k12_fused<false>, units), kThreads, 0, st>>>(src, o, a, n_k1,
+                                                                               n_k2);
+    }
+    return launch_status();
+}
+
+template <int NW>
+static void k3_staged_go(bool opt, uint32_t n_chunks, cudaStream_t st, const TableSource& src,
+                         const K3Args& a) {
+    if (opt)
+        k3_decode_staged<NW, true><<<n_chunks, kThreads, 0, st>>>(src, a);
+    else
+        k3_decode_staged<NW, false><<<n_chunks, kThreads, 0, st>>>(src, a);
+}
+
 cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K3Launch& p, cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
+    a.gate = p.gate;
     K3Ptrs ptrs{};
     const TableSource src{chunks};
-    if (p.r3) {  // radix-3 wire codes (fused exchange, shared scalers, 3 <= N <= 8)
+    if (p.sharing && p.n_workers <= kMaxPeers) {  // staged SWAR kernel (fused optimizer optional)
         if (p.optd) {
             a.optd = p.optd;
             a.opt = p.opt;
         }
-#define TGB_R3_CASE(NW)                                                                      \
-    case NW:                                                                                 \
-        if (p.optd) k3_decode_r3<NW, true><<<n_chunks, kThreads, 0, st>>>(src, a);          \
-        else k3_decode_r3<NW, false><<<n_chunks, kThreads, 0, st>>>(src, a);                \
-        break;
+        const bool opt = p.optd != nullptr;
         switch (p.n_workers) {
-            TGB_R3_CASE(3)
-            TGB_R3_CASE(4)
-            TGB_R3_CASE(5)
-            TGB_R3_CASE(6)
-            TGB_R3_CASE(7)
-            TGB_R3_CASE(8)
-            default: return cudaErrorInvalidValue;
-        }
-#undef TGB_R3_CASE
-        return launch_status();
-    }
-    if (p.optd) {  // fused decode -> optimizer (the caller checked the supported N)
-        a.optd = p.optd;
-        a.opt = p.opt;
-        switch (p.n_workers) {
-            case 1: k3_decode_staged<1, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 2: k3_decode_staged<2, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 3: k3_decode_staged<3, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 4: k3_decode_staged<4, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 8: k3_decode_staged<8, true, true><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            default: return cudaErrorInvalidValue;
+            case 1: k3_staged_go<1>(opt, n_chunks, st, src, a); break;
+            case 2: k3_staged_go<2>(opt, n_chunks, st, src, a); break;
+            case 3: k3_staged_go<3>(opt, n_chunks, st, src, a); break;
+            case 4: k3_staged_go<4>(opt, n_chunks, st, src, a); break;
+            case 5: k3_staged_go<5>(opt, n_chunks, st, src, a); break;
+            case 6: k3_staged_go<6>(opt, n_chunks, st, src, a); break;
+            case 7: k3_staged_go<7>(opt, n_chunks, st, src, a); break;
+            default: k3_staged_go<8>(opt, n_chunks, st, src, a); break;
         }
         return launch_status();
     }
-    if (p.sharing && p.variant == 2 && p.chunk3 == kChunk3) {  // SWAR sums, register LUT
-        switch (p.n_workers) {
-            case 1: k3_decode_staged<1, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 2: k3_decode_staged<2, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 3: k3_decode_staged<3, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 4: k3_decode_staged<4, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 8: k3_decode_staged<8, false, true><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            default: break;
-        }
-    }
-    if (p.sharing && p.variant == 1 && p.chunk3 == kChunk3) {
-        switch (p.n_workers) {
-            case 1: k3_decode_staged<1><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 2: k3_decode_staged<2><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 3: k3_decode_staged<3><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 4: k3_decode_staged<4><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            case 8: k3_decode_staged<8><<<n_chunks, kThreads, 0, st>>>(src, a); return launch_status();
-            default: break;
-        }
-    }
-    if (p.sharing) {
-        switch (p.n_workers) {
-            case 1: k3_decode_nw<1><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 2: k3_decode_nw<2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 3: k3_decode_nw<3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 4: k3_decode_nw<4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 5: k3_decode_nw<5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 6: k3_decode_nw<6><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 7: k3_decode_nw<7><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            case 8: k3_decode_nw<8><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-            default:
-                k3_decode<TableSource, true, true><<<n_chunks, kThreads, 0, st>>>(src, a, ptrs);
-        }
-    }
+    if (p.optd) return cudaErrorInvalidValue;  // the caller checks opt_fusable
+    if (p.sharing)
+        k3_decode<TableSource, true, true><<<n_chunks, kThreads, 0, st>>>(src, a, ptrs);
     else
-        k3_decode<TableSource, true, false><<<n_chunks, kThreads, 0, st>>>(
-            TableSource{chunks}, a, ptrs);
+        k3_decode<TableSource, true, false><<<n_chunks, kThreads, 0, st>>>(src, a, ptrs);
     return launch_status();
 }
 
@@ -2056,17 +1373,18 @@ cudaError_t launch_average_raw(int32_t n_workers, const float* const* vals, uint
 cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
                              cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
-    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err, p.bulk};
+    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.radix_m, p.chunk12,
+                p.sum_region, p.inv_n, p.err};
     for (int r = 0; r < p.n_workers; ++r) a.sums[r] = p.sums[r];
     const TableSource src{chunks};
     switch (p.n_workers) {
-        case 2: k3_reduce<2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 3: k3_reduce<3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 4: k3_reduce<4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 5: k3_reduce<5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 6: k3_reduce<6><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 7: k3_reduce<7><<<n_chunks, kThreads, 0, st>>>(src, a); break;
-        case 8: k3_reduce<8><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 2: k3_reduce<2><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
+        case 3: k3_reduce<3><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
+        case 4: k3_reduce<4><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
+        case 5: k3_reduce<5><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
+        case 6: k3_reduce<6><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
+        case 7: k3_reduce<7><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
+        case 8: k3_reduce<8><<<n_chunks, kThreads, kK3aSmem, st>>>(src, a); break;
         default: return cudaErrorInvalidValue;
     }
     return launch_status();
@@ -2075,71 +1393,20 @@ cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const Sh
 cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
                              cudaStream_t st) {
     if (n_chunks == 0) return cudaSuccess;
-    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.nib, p.inv_n, p.err, p.bulk};
+    ShardArgs a{p.src, p.stride, {}, p.own_sums, p.n_workers, p.radix_m, p.chunk12,
+                p.sum_region, p.inv_n, p.err};
     const TableSource src{chunks};
-    if (p.nib)
-        k3_expand<true><<<n_chunks, kThreads, 0, st>>>(src, a);
-    else
-        k3_expand<false><<<n_chunks, kThreads, 0, st>>>(src, a);
-    return launch_status();
-}
-
-static PipeArgs pipe_args(const K2Launch& k2, const K3Launch& k3, const PipeLaunch& p) {
-    PipeArgs a{};
-    a.k2 = K2Args{k2.push, k2.slots, k2.bounds, k2.err, k2.t, 0, 0, 0.0f, 0, k2.dst};
-    a.k2.shard_n = 0;
-    a.k2.nnz = k2.nnz;
-    a.k3 = K3Args{k3.src, k3.stride, nullptr, nullptr, 0.0f, k3.n_workers, k3.sharing, k3.inv_n,
-                  k3.err};
-    a.flags = p.flags;
-    for (int r = 0; r < kMaxPeers; ++r) a.peer_flags[r] = p.peer_flags[r];
-    a.epoch = p.epoch;
-    a.rank = p.rank;
-    a.n_items = p.n_items;
-    a.done = p.done;
-    a.prof = p.prof;
-    return a;
-}
-
-template <class K>
-static cudaError_t pipe_launch(K kernel, uint32_t n_items, const TableSource& src,
-                               const PipeArgs& a, cudaStream_t st) {
-    int dev = 0, sms = 0, per = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, 0);
-    if (e != cudaSuccess) return e;
-    uint32_t g = static_cast<uint32_t>(sms * per) - 1;  // every CTA resident (deadlock freedom)
-    g = g < n_items ? g : n_items;
-    kernel<<<g + 1, kThreads, 0, st>>>(src, a);  // + the publisher CTA
-    return cudaGetLastError();
-}
-
-template <int NW>
-static cudaError_t pipe_variant(int v, uint32_t n_items, const TableSource& src, const PipeArgs& a,
-                                cudaStream_t st) {
-    switch (v) {  // TGB_PIPEV (A/B)
-        case 1: return pipe_launch(k23_pipelined<NW, 2, 4>, n_items, src, a, st);
-        case 2: return pipe_launch(k23_pipelined<NW, 3, 2>, n_items, src, a, st);
-        default: return pipe_launch(k23_pipelined<NW, 3, 4>, n_items, src, a, st);
-    }
-}
-
-cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const K2Launch& k2,
-                                 const K3Launch& k3, const PipeLaunch& p, cudaStream_t st) {
-    if (n_items == 0) return cudaSuccess;
-    const PipeArgs a = pipe_args(k2, k3, p);
-    const TableSource src{chunks};
-    switch (k3.n_workers) {
-        case 2: return pipe_variant<2>(p.variant, n_items, src, a, st);
-        case 3: return pipe_variant<3>(p.variant, n_items, src, a, st);
-        case 4: return pipe_variant<4>(p.variant, n_items, src, a, st);
-        case 5: return pipe_variant<5>(p.variant, n_items, src, a, st);
-        case 6: return pipe_variant<6>(p.variant, n_items, src, a, st);
-        case 7: return pipe_variant<7>(p.variant, n_items, src, a, st);
-        case 8: return pipe_variant<8>(p.variant, n_items, src, a, st);
+    switch (p.n_workers) {
+        case 2: k3_expand<2><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 3: k3_expand<3><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 4: k3_expand<4><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 5: k3_expand<5><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 6: k3_expand<6><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 7: k3_expand<7><<<n_chunks, kThreads, 0, st>>>(src, a); break;
+        case 8: k3_expand<8><<<n_chunks, kThreads, 0, st>>>(src, a); break;
         default: return cudaErrorInvalidValue;
     }
+    return launch_status();
 }
 
 // ============================================================== telemetry
@@ -2352,32 +1619,126 @@ cudaError_t launch_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k
 
 
 // ===================================================== peer flag barrier
-// Cross-GPU barrier for the fused exchange: thread p stores this rank's epoch
-// into peer p's flag array (release, system scope) and then waits until every
-// peer has stored the same epoch into ours (acquire). One GPU per rank, so the
-// waiting kernels run on different devices. A bounded spin turns a dead peer
-// into TGB_E_PEER_TIMEOUT instead of a hang.
-__global__ void k_peer_barrier(PeerFlags f, uint64_t epoch, ErrWord* err) {
+// Cross-GPU barrier of the fused / sharded exchange. Every rank keeps one
+// 16-byte record {epoch, iteration} per (barrier slot, step parity, peer) in its
+// IPC allocation. Thread p publishes this rank's record into peer p's array
+// (iteration first, then the epoch with release semantics, system scope) and
+// then waits until peer p's record in ours reaches the epoch (acquire). Records
+// alternate by step parity: a peer can be at most one step ahead, so the record
+// of this epoch is never overwritten while it is read. A peer at another
+// iteration raises TGB_E_SKEW (cluster.hpp:141-143); a bounded spin turns a dead
+// peer into TGB_E_PEER_TIMEOUT instead of a hang. LocalCluster (one process)
+// splits it: kBarrierPost publishes, kBarrierCheck verifies after the streams
+// were ordered by events (never spins, so no hardware-queue deadlock).
+__global__ void k_peer_barrier(PeerFlags f, uint64_t epoch, uint64_t t, int mode, ErrWord* err) {
     const int p = threadIdx.x;
     if (p >= f.n) return;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f.remote[p]), "l"(epoch) : "memory");
+    const uint32_t par = static_cast<uint32_t>(epoch & 1u) * kMaxPeers;
+    if (mode != kBarrierCheck) {
+        uint64_t* r = f.remote[p] + 2 * par;
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(r + 1), "l"(t) : "memory");
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(r), "l"(epoch) : "memory");
+    }
+    if (mode == kBarrierPost) return;
+    const uint64_t* rec = f.local + 2 * (par + p);
     uint64_t v = 0;
     long long spins = 0;
     const long long t0 = clock64();
     for (;;) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.local + p) : "memory");
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(rec) : "memory");
         if (v >= epoch) break;
-        if ((++spins & 1023) == 0 && clock64() - t0 > 20000000000ll) {  // ~10 s
+        if (mode == kBarrierCheck ||
+            ((++spins & 1023) == 0 && clock64() - t0 > 20000000000ll)) {  // ~10 s
             raise_error(err, TGB_E_PEER_TIMEOUT, -1, static_cast<uint64_t>(p));
-            break;
+            return;
         }
     }
+    uint64_t pt = 0;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(pt) : "l"(rec + 1) : "memory");
+    if (pt != t) raise_error_aux(err, TGB_E_SKEW, static_cast<uint64_t>(p), pt);
 }
 
-cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,
-                                cudaStream_t st) {
-    k_peer_barrier<<<1, 32, 0, st>>>(f, epoch, err);
+cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, uint64_t t, int mode,
+                                ErrWord* err, cudaStream_t st) {
+    k_peer_barrier<<<1, 32, 0, st>>>(f, epoch, t, mode, err);
     return launch_status();
+}
+
+// ======================================================= kernel preloading
+// Every kernel a plan can launch, loaded once per device at plan creation
+// (cudaFuncGetAttributes forces the module load under CUDA_MODULE_LOADING=LAZY).
+cudaError_t preload_kernels() {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+    cudaFuncAttributes fa;
+    const void* ks[] = {
+        reinterpret_cast<const void*>(k1_stats<TableSource, 8, 1, 4, true>),
+        reinterpret_cast<const void*>(k1_stats<TableSource, 8, 1, 4>),
+        reinterpret_cast<const void*>(k1_stats<SingleSource, 8, 1, 4>),
+        reinterpret_cast<const void*>(TGB_K2_PLAIN),
+        reinterpret_cast<const void*>(TGB_K2_FUSED),
+        reinterpret_cast<const void*>(TGB_K2_FUSED_OPT),
+        reinterpret_cast<const void*>(k2_ternarize<SingleSource>),
+        reinterpret_cast<const void*>(k12_fused<true>),
+        reinterpret_cast<const void*>(k12_fused<true, true>),
+        reinterpret_cast<const void*>(k12_fused<false>),
+        reinterpret_cast<const void*>(k3_decode_staged<1, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<2, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<3, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<4, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<5, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<6, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<7, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<8, false>),
+        reinterpret_cast<const void*>(k3_decode_staged<1, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<2, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<3, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<4, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<5, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<6, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<7, true>),
+        reinterpret_cast<const void*>(k3_decode_staged<8, true>),
+        reinterpret_cast<const void*>(k3_decode<TableSource, true, true>),
+        reinterpret_cast<const void*>(k3_decode<TableSource, true, false>),
+        reinterpret_cast<const void*>(k3_decode<SingleSource, false, true>),
+        reinterpret_cast<const void*>(k3_decode<SingleSource, false, false>),
+        reinterpret_cast<const void*>(k3_reduce<2>), reinterpret_cast<const void*>(k3_reduce<3>),
+        reinterpret_cast<const void*>(k3_reduce<4>), reinterpret_cast<const void*>(k3_reduce<5>),
+        reinterpret_cast<const void*>(k3_reduce<6>), reinterpret_cast<const void*>(k3_reduce<7>),
+        reinterpret_cast<const void*>(k3_reduce<8>),
+        reinterpret_cast<const void*>(k3_expand<2>), reinterpret_cast<const void*>(k3_expand<3>),
+        reinterpret_cast<const void*>(k3_expand<4>), reinterpret_cast<const void*>(k3_expand<5>),
+        reinterpret_cast<const void*>(k3_expand<6>), reinterpret_cast<const void*>(k3_expand<7>),
+        reinterpret_cast<const void*>(k3_expand<8>),
+        reinterpret_cast<const void*>(k_peer_barrier),
+        reinterpret_cast<const void*>(k_clip_apply),
+        reinterpret_cast<const void*>(k_average_raw),
+        reinterpret_cast<const void*>(k_rng_bits),
+        reinterpret_cast<const void*>(k_minmax),
+        reinterpret_cast<const void*>(k_histogram),
+        reinterpret_cast<const void*>(k_opt_apply),
+        reinterpret_cast<const void*>(k_wire_gather),
+        reinterpret_cast<const void*>(k_pull_decode),
+    };
+    for (const void* k : ks) {
+        e = cudaFuncGetAttributes(&fa, k);
+        if (e != cudaSuccess) return e;
+    }
+    const void* k3a[] = {
+        reinterpret_cast<const void*>(k3_reduce<2>), reinterpret_cast<const void*>(k3_reduce<3>),
+        reinterpret_cast<const void*>(k3_reduce<4>), reinterpret_cast<const void*>(k3_reduce<5>),
+        reinterpret_cast<const void*>(k3_reduce<6>), reinterpret_cast<const void*>(k3_reduce<7>),
+        reinterpret_cast<const void*>(k3_reduce<8>)};
+    for (const void* k : k3a) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kK3aSmem));
+        if (e != cudaSuccess) return e;
+    }
+    if (dev >= 0 && dev < 64) done[dev] = true;
+    return cudaSuccess;
 }
 
 }  // namespace tgb

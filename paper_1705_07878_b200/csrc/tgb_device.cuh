@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "tgb/terngrad_b200.h"
+
 namespace tgb {
 
 constexpr int kThreads = 256;       // CTA size of every streaming kernel
@@ -90,6 +92,7 @@ struct ErrWord {
     uint32_t flags;
     uint32_t pad;
     unsigned long long inv_key;  // ~((layer + 1) << 40 | index)
+    unsigned long long aux;      // TGB_E_SKEW: the first offending peer's iteration
     __host__ __device__ int32_t layer() const {
         return static_cast<int32_t>((~inv_key) >> 40) - 1;
     }
@@ -103,6 +106,20 @@ __device__ __forceinline__ void raise_error(ErrWord* e, uint32_t flag, int32_t l
         (static_cast<unsigned long long>(static_cast<uint32_t>(layer + 1) & 0xFFFFFFu) << 40) |
         (index & ((1ull << 40) - 1));
     atomicMax(&e->inv_key, ~key);
+}
+
+// an exchange error with a detail value (kept from the first raise of `flag`)
+__device__ __forceinline__ void raise_error_aux(ErrWord* e, uint32_t flag, uint64_t index,
+                                                unsigned long long aux) {
+    const uint32_t old = atomicOr(&e->flags, flag);
+    if (!(old & flag)) atomicExch(&e->aux, aux);
+    atomicMax(&e->inv_key, ~(index & ((1ull << 40) - 1)));
+}
+
+// the step's exchange failed (iteration skew or a missing peer): decode kernels
+// leave the outputs untouched
+__device__ __forceinline__ bool exchange_failed(const ErrWord* e) {
+    return (__ldcg(&e->flags) & (TGB_E_SKEW | TGB_E_PEER_TIMEOUT)) != 0u;
 }
 
 // ------------------------------------------------------------- optimizer

@@ -8,12 +8,35 @@
 
 namespace tgb {
 
-// flag arrays of the cross-GPU barrier (inside each rank's IPC allocation)
+// rng.hpp:50-54: RngStream key words
+inline void philox_key(uint64_t seed, uint64_t name_hash, uint64_t worker, uint32_t& k0,
+                       uint32_t& k1) {
+    k0 = static_cast<uint32_t>(seed ^ name_hash);
+    k1 = static_cast<uint32_t>((seed >> 32) ^ (name_hash >> 32) ^
+                               (worker * 0x9E3779B97F4A7C15ull));
+}
+
+inline uint32_t layer_vec_flags(const void* g, const void* out) {
+    uint32_t f = 0;
+    if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) f |= kLayerVecIn;
+    if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) f |= kLayerVecOut;
+    return f;
+}
+
+// flag records of the cross-GPU barrier (inside each rank's IPC allocation):
+// {epoch, iteration} per (barrier slot, peer), 16 bytes each
 struct PeerFlags {
-    uint64_t* remote[kMaxPeers];  // address of THIS rank's slot in peer p's flag array
-    uint64_t* local;              // this rank's flag array (one slot per peer)
+    uint64_t* remote[kMaxPeers];  // THIS rank's record in peer p's flag array
+    uint64_t* local;              // this rank's records (one per peer)
     int32_t n;
 };
+constexpr int kBarrierSpin = 0;   // publish, then wait for every peer (one GPU per process)
+constexpr int kBarrierPost = 1;   // publish only (LocalCluster, ordered by events)
+constexpr int kBarrierCheck = 2;  // verify the peers' records, no wait (LocalCluster)
+
+// load every kernel the plans launch (no lazy loading inside a step: a lazily
+// loaded kernel's first launch waits for the device to idle)
+cudaError_t preload_kernels();
 
 struct K1Launch {
     Partial* partials;
@@ -26,11 +49,11 @@ struct K1Launch {
     int32_t global_bucketing;
     int32_t n_layers;
     int32_t n_active_layers;
-    int32_t variant = 0;  // chunk K1 kernel variant (TGB_K1V, A/B only)
     PeerPush push{};      // scaler slot destinations
     const TensorDev* tensors = nullptr;  // plan: tensor table (per-tensor finalize)
     unsigned long long* nnz = nullptr;   // telemetry counter to reset (this group)
-    uint32_t keep_chunks = 0;            // TGB_K1KEEP: last units kept in L2 for K2 (A/B)
+    uint32_t keep_chunks = 0;            // last units kept in L2 (evict_last) for K2 (N == 1)
+    int32_t n_tensors = 0;               // fused K1+K2: ready[n_tensors] is the Global flag
 };
 
 struct K2Launch {
@@ -40,7 +63,6 @@ struct K2Launch {
     ErrWord* err;
     uint64_t t;
     int32_t reverse;
-    int32_t variant = 0;   // chunk K2 kernel variant (TGB_K2V, A/B only)
     float s_imm = 0.0f;    // single-layer: scaler by value when slots == nullptr
     uint64_t rng_base = 0; // single-layer: ternarize rng_base (codec.hpp:148)
     PeerPush dst{};        // plan: code destinations (n == 0: push only)
@@ -50,10 +72,8 @@ struct K2Launch {
     int32_t shard_n = 0;        // sharded exchange: codes go to the chunk's owner only
     uint32_t shard_bounds[kMaxPeers + 1] = {};
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
-    int32_t direct = 0;         // thread-contiguous code bytes stored straight from registers
-    int32_t bulk = 0;           // TGB_K2BULK (A/B): code stores as TMA bulk copies
-    int32_t r3 = 0;             // fused exchange: radix-3 wire codes to dst, 2-bit codes to push
-    int32_t pdl = 0;            // TGB_PDL: K2 as K1's programmatic dependent (1), + L2 prefetch (2)
+    int32_t pdl = 0;            // K2 as K1's programmatic dependent (1), + L2 prefetch (2, 3)
+    uint32_t keep_from = ~0u;   // work items K1 loaded evict_last (demoted by K2)
 };
 
 struct K3Launch {
@@ -64,11 +84,9 @@ struct K3Launch {
     float inv_n;
     ErrWord* err;
     float s_imm = 0.0f;    // single-layer: scaler by value when scalers == nullptr
-    int32_t variant = 0;   // TGB_K3V (A/B): 1 = smem-staged 16-B code loads
-    uint32_t chunk3 = 0;   // plan K3 chunk elements (the staged variant needs kChunk3)
-    const OptDev* optd = nullptr;  // fused decode -> optimizer (staged kernel, N in {1,2,3,4,8})
+    const OptDev* optd = nullptr;  // fused decode -> optimizer (staged kernel, N <= 8)
     OptArgs opt{};
-    int32_t r3 = 0;  // the source holds radix-3 wire codes (chunks of kChunk3R3 elements)
+    int32_t gate = 0;  // skip the decode when the step's exchange failed (skew / timeout)
 };
 
 struct ShardLaunch {
@@ -77,27 +95,23 @@ struct ShardLaunch {
     uint8_t* sums[kMaxPeers];  // every rank's sums buffer (this step's parity)
     const uint8_t* own_sums;
     int32_t n_workers;
-    int32_t nib;
+    int32_t radix_m;           // base-(2N+1) digits per u32 word
+    uint32_t chunk12;          // K2 work-item elements (a full chunk's sums region)
+    uint32_t sum_region;       // bytes of a full chunk's sums region
     float inv_n;
     ErrWord* err;
-    int32_t bulk = 0;  // K3a sums stores as TMA bulk copies
 };
 
-struct PipeLaunch {
-    uint32_t* flags;                  // this rank's item flags [item][kMaxPeers]
-    uint32_t* peer_flags[kMaxPeers];  // every rank's flags array
-    uint32_t epoch;
-    int32_t rank;
-    uint32_t n_items;
-    int32_t variant = 0;  // TGB_PIPEV (A/B)
-    uint32_t* done = nullptr;  // local per-item done flags (n_items)
-    unsigned long long* prof = nullptr;  // TGB_PIPE_PROF: 8 phase cycle counters
-};
 
 cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
                             const K2Launch& p, cudaStream_t st);
+// fused K1 + K2 (small sets): n_k1 ternary units, n_k2 units (incl. passthrough);
+// ready = n_tensors + 1 epoch flags
+cudaError_t launch_k12_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_k1,
+                             uint32_t n_k2, const K1Launch& p1, const K2Launch& p2,
+                             uint32_t* ready, uint32_t epoch, cudaStream_t st);
 cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,
@@ -110,8 +124,6 @@ cudaError_t launch_k3_reduce(const ChunkFat* chunks, uint32_t n_chunks, const Sh
                              cudaStream_t st);
 cudaError_t launch_k3_expand(const ChunkFat* chunks, uint32_t n_chunks, const ShardLaunch& p,
                              cudaStream_t st);
-cudaError_t launch_k23_pipelined(const ChunkFat* chunks, uint32_t n_items, const K2Launch& k2,
-                                 const K3Launch& k3, const PipeLaunch& p, cudaStream_t st);
 cudaError_t launch_histogram(const float* v, uint64_t n, uint32_t bins, uint32_t* mm,
                              int nan_first, unsigned long long* counts, double* edges,
                              cudaStream_t st, int pass);
@@ -123,8 +135,8 @@ cudaError_t launch_pull_decode(const uint8_t* payload, const PullSeg* d_segs, ui
                                uint32_t total_threads, int* bad, cudaStream_t st);
 cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, float* out,
                               cudaStream_t st);
-cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, ErrWord* err,
-                                cudaStream_t st);
+cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, uint64_t t, int mode,
+                                ErrWord* err, cudaStream_t st);
 cudaError_t launch_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k0, uint64_t n,
                             uint32_t* out, cudaStream_t st);
 

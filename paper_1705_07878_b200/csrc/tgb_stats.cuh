@@ -28,7 +28,18 @@ struct K1Out {
     const TensorDev* tensors; // plan only; nullptr = single-block single-layer API
     unsigned long long* nnz = nullptr;  // telemetry counter of this group (reset by block 0)
     uint32_t keep_from = ~0u;  // units >= keep_from load with L2 evict_last (K2 re-reads them)
+    // fused K1+K2 kernel: a finalized tensor's bound and scalers are published by a
+    // release store of the launch's epoch into ready[tensor] (Global bucketing: into
+    // *ready_global once the last tensor wrote the global max)
+    uint32_t* ready = nullptr;
+    uint32_t* ready_global = nullptr;
+    uint32_t epoch = 0;
 };
+
+__device__ __forceinline__ void publish_ready(uint32_t* flag, uint32_t epoch) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
 
 __device__ __forceinline__ void put_slot(const K1Out& o, int32_t slot, float v) {
     o.slots[slot] = v;
@@ -226,8 +237,10 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
                     put_slot(o, Ll.slot, gs);
                 }
                 *o.global_done = 0u;
+                if (o.ready_global) publish_ready(o.ready_global, o.epoch);
             }
         }
+        if (tid == 0 && o.ready && !o.global_bucketing) publish_ready(o.ready + L.tensor, o.epoch);
     }
 }
 

@@ -140,6 +140,55 @@ class Plan:
         self._grads = self._outs = None
         self.attached = False
         self.grouped = info.n_groups == 2  # tgb_step overlaps the dominant layer with the rest
+        self.last_t = None  # iteration of the last step issued (iteration-skew messages)
+
+    # -- options -------------------------------------------------------------
+    def set_option(self, option: int, value: int):
+        """tgb_plan_set_option (schedule / exchange / fused optimizer); rebuilds the
+        work tables, so bind() afterwards if gradients were bound before."""
+        with torch.cuda.device(self.device):
+            check(load().tgb_plan_set_option(self.h, int(option), int(value)),
+                  "tgb_plan_set_option")
+        self._refresh()
+
+    SCHEDULES = {"auto": _lib.TGB_SCHEDULE_AUTO, "single": _lib.TGB_SCHEDULE_SINGLE,
+                 "groups": _lib.TGB_SCHEDULE_GROUPS, "unfused": _lib.TGB_SCHEDULE_UNFUSED,
+                 "fused12": _lib.TGB_SCHEDULE_FUSED12}
+
+    def set_schedule(self, schedule: str):
+        """"auto" | "single" (one stream, each kernel covers the whole set) | "groups" |
+        "unfused" (K1 and K2 always separate launches) | "fused12" (always one launch)"""
+        self.set_option(_lib.TGB_PLAN_OPT_SCHEDULE, self.SCHEDULES[schedule])
+
+    def set_exchange(self, exchange: str):
+        """"auto" (fused N <= 4, sharded from 5) | "fused" | "sharded"; before attaching"""
+        self.set_option(_lib.TGB_PLAN_OPT_EXCHANGE, {"auto": _lib.TGB_EXCHANGE_AUTO,
+                                                     "fused": _lib.TGB_EXCHANGE_FUSED,
+                                                     "sharded": _lib.TGB_EXCHANGE_SHARDED}[exchange])
+
+    def _refresh(self):
+        L = load()
+        info = _lib.PlanInfo()
+        check(L.tgb_plan_get_info(self.h, C.byref(info)), "tgb_plan_get_info")
+        self.info = info
+        self.grouped = info.n_groups == 2
+        push, gathered, bounds = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(L.tgb_plan_buffers(self.h, C.byref(push), C.byref(gathered), C.byref(bounds)),
+              "buffers")
+        self.gathered = _view(gathered.value or 0, info.push_bytes * self.n_workers
+                              if self.n_workers > 1 else 0, self.device)
+        if self._grads is not None:
+            self.bind(self._grads, self._outs)
+
+    @property
+    def exchange(self) -> str:
+        return _lib.EXCHANGE_NAMES[self.info.exchange]
+
+    def traffic(self) -> "TrafficStats":
+        """one step of this worker's TrafficStats terms (tgb_plan_traffic)"""
+        t = _lib.Traffic()
+        check(load().tgb_plan_traffic(self.h, C.byref(t)), "tgb_plan_traffic")
+        return TrafficStats.of(t)
 
     # -- binding -------------------------------------------------------------
     def bind(self, grads: Sequence[torch.Tensor], outs: Optional[Sequence[torch.Tensor]]):
@@ -171,9 +220,11 @@ class Plan:
 
     def ternarize_pack(self, t: int, stream=None):
         check(load().tgb_ternarize_pack(self.h, int(t), self._st(stream)), "tgb_ternarize_pack")
+        self.last_t = int(t)
 
     def encode(self, t: int, stream=None):
         check(load().tgb_encode(self.h, int(t), self._st(stream)), "tgb_encode")
+        self.last_t = int(t)
 
     def share_scalers(self, comm: Comm, stream=None):
         check(load().tgb_share_scalers(self.h, comm.h, self._st(stream)), "tgb_share_scalers")
@@ -190,20 +241,40 @@ class Plan:
               "tgb_decode_average")
 
     def attach_peers(self, comm: Comm):
-        """Fused exchange over NVLink (CUDA IPC); collective over all ranks."""
+        """Peer exchange over NVLink (CUDA IPC): fused or sharded (set_exchange);
+        collective over all ranks. Raises ProtocolError when the ranks' plans differ
+        (the reference server's "block structure mismatch", cluster.hpp:169-172)."""
         with torch.cuda.device(self.device):
-            check(load().tgb_plan_attach_peers(self.h, comm.h), "tgb_plan_attach_peers")
+            st = load().tgb_plan_attach_peers(self.h, comm.h)
+        if st == _lib.TGB_ERR_PROTOCOL:
+            raise ProtocolError(load().tgb_last_error_message().decode())
+        check(st, "tgb_plan_attach_peers")
         self.attached = True
+        self._refresh()
 
     @staticmethod
     def attach_local(plans: Sequence["Plan"]):
-        """Fused exchange between the N plans of this process (workers 0..N-1;
-        tgb_plan_attach_local). Afterwards every plan's step must be issued on its
-        own stream: a plan's barrier waits for the other plans' K2."""
+        """Exchange between the N plans of this process (workers 0..N-1;
+        tgb_plan_attach_local); step them together with Plan.local_step."""
         arr = (C.c_void_p * len(plans))(*[p.h.value for p in plans])
-        check(load().tgb_plan_attach_local(arr, len(plans)), "tgb_plan_attach_local")
+        st = load().tgb_plan_attach_local(arr, len(plans))
+        if st == _lib.TGB_ERR_PROTOCOL:
+            raise ProtocolError(load().tgb_last_error_message().decode())
+        check(st, "tgb_plan_attach_local")
         for p in plans:
             p.attached = True
+            p._refresh()
+
+    @staticmethod
+    def local_step(plans: Sequence["Plan"], ts: Sequence[int], streams):
+        """tgb_local_step: plan w steps iteration ts[w] on streams[w]"""
+        n = len(plans)
+        arr = (C.c_void_p * n)(*[p.h.value for p in plans])
+        tv = (C.c_uint64 * n)(*[int(t) for t in ts])
+        sv = (C.c_void_p * n)(*[s.cuda_stream for s in streams])
+        check(load().tgb_local_step(arr, n, tv, sv), "tgb_local_step")
+        for p, t in zip(plans, ts):
+            p.last_t = int(t)
 
     def last_buffers(self):
         """(own push area, gather buffer) of the last step, as uint8 views."""
@@ -217,6 +288,7 @@ class Plan:
     def step(self, t: int, comm: Optional[Comm] = None, stream=None):
         check(load().tgb_step(self.h, comm.h if comm is not None else None, int(t),
                               self._st(stream)), "tgb_step")
+        self.last_t = int(t)
 
     def step_host(self, t: int, host_grads: Sequence[torch.Tensor],
                   host_outs: Sequence[torch.Tensor], comm: Optional[Comm] = None, stream=None):
@@ -232,6 +304,7 @@ class Plan:
         op = (C.c_void_p * max(nl, 1))(*[h.data_ptr() if h.numel() else 0 for h in host_outs])
         check(load().tgb_step_host(self.h, comm.h if comm is not None else None, int(t), gp, op,
                                    self._st(stream)), "tgb_step_host")
+        self.last_t = int(t)
 
     def error(self) -> _lib.Error:
         e = _lib.Error()
@@ -304,8 +377,11 @@ class Plan:
         return first if first is not None else -1
 
     def raise_errors(self):
-        """Rethrow the device error word with the reference's CodecError text."""
+        """Rethrow the device error word with the reference's CodecError /
+        ProtocolError text."""
         e = self.error()
+        if e.flags & _lib.TGB_E_SKEW:  # cluster.hpp:141-143
+            raise ProtocolError(f"server: iteration skew, expected {self.last_t} got {e.aux}")
         if e.flags:
             name = self.names[e.layer] if 0 <= e.layer < len(self.names) else "?"
             b = self.block_of(e.layer, e.index) if 0 <= e.layer < len(self.names) else -1
@@ -364,7 +440,10 @@ class SyncWorker:
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
                  rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None,
-                 fused: bool = True):
+                 exchange: str = "auto", schedule: str = "auto"):
+        """exchange: "auto" | "fused" | "sharded" (NVLink peer stores, attached at
+        construction) | "nccl" (ncclAllGather of push areas); schedule: see
+        Plan.set_schedule."""
         self.device = _dev(device)
         self.names = list(names)
         self.shapes = [list(s) for s in shapes]
@@ -372,18 +451,37 @@ class SyncWorker:
         self.rank, self.world_size = rank, world_size
         if world_size > 1 and comm is None:
             raise ValueError("SyncWorker: world_size > 1 needs a Comm")
+        if exchange not in ("auto", "fused", "sharded", "nccl"):
+            raise ValueError(f"SyncWorker: unknown exchange {exchange!r}")
         self.comm = comm
         self.plan = Plan(self.names, self.ns, cfg, worker=rank, n_workers=world_size,
                          device=self.device)
+        if schedule != "auto":
+            self.plan.set_schedule(schedule)
+        if world_size > 1 and exchange in ("fused", "sharded"):
+            self.plan.set_exchange(exchange)
         self.grad_flat, self.grads = aligned_flat(self.ns, self.device)
         self.out_flat, self.outs = aligned_flat(self.ns, self.device)
         self.plan.bind(self.grads, self.outs)
-        if world_size > 1 and fused:  # K2 stores codes straight into every peer (NVLink)
+        if world_size > 1 and exchange != "nccl":  # K2 stores codes into the peers (NVLink)
             self.plan.attach_peers(comm)
+        self.traffic = TrafficStats()
+        self._step_traffic = None
 
-    def step(self, t: int, stream=None) -> List[torch.Tensor]:
+    def step(self, t: int, stream=None, check: bool = False) -> List[torch.Tensor]:
+        """Worker::run sync segment: encode -> exchange -> decode into ``outs``.
+        check=True synchronises and rethrows a codec / protocol error of this step
+        (otherwise errors stay in the device error word until ``check()``)."""
         self.plan.step(t, self.comm, stream)
+        self._count_traffic()
+        if check:
+            self.check()
         return self.outs
+
+    def _count_traffic(self):
+        if self._step_traffic is None:
+            self._step_traffic = self.plan.traffic()
+        self.traffic += self._step_traffic
 
     def host_buffers(self, pinned: bool = True):
         """pinned host buffers for step_host: (in_flat, in_views, out_flat, out_views)"""
@@ -395,6 +493,7 @@ class SyncWorker:
                   host_outs: Sequence[torch.Tensor], stream=None):
         """Worker::run sync segment with host buffers: gradients in, averaged out."""
         self.plan.step_host(t, host_grads, host_outs, self.comm, stream)
+        self._count_traffic()
 
     def bind_optimizer(self, cfg, params: Sequence[torch.Tensor]):
         """Parameters (device, one per layer) updated by step_apply with
@@ -424,18 +523,15 @@ class SyncWorker:
 class LocalCluster:
     """N data-parallel workers in ONE process (the reference's run_cluster over
     InProcessHub, cluster.hpp:378-397): one plan per worker, attached to each
-    other with tgb_plan_attach_local, each stepping on its own stream. The
-    exchange kernels are the ones the multi-process path runs (K1/K2 peer
-    stores, flag barriers, K3 or the sharded reduce/expand), so N = 8 workers
-    can run on fewer GPUs. ``devices``: one device for all, or one per worker.
-    Set CUDA_DEVICE_MAX_CONNECTIONS >= 2N + 2 before CUDA initialises so the
-    workers' streams do not share hardware queues (a shared queue serialises a
-    worker's K2 behind another worker's barrier until the barrier times out),
-    and CUDA_MODULE_LOADING=EAGER: a lazily loaded kernel's first launch waits
-    for the context to idle, which a worker spinning in its barrier never does."""
+    other with tgb_plan_attach_local and stepped together with tgb_local_step,
+    each worker on its own stream. The exchange kernels are the ones the
+    multi-process path runs (K1/K2 peer stores, K3 or the sharded reduce/expand);
+    the streams are ordered by CUDA events instead of spinning flag barriers, so
+    N = 8 workers can run on one GPU with no launch-environment settings.
+    ``devices``: one device for all, or one per worker."""
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
-                 n_workers: int, devices=None):
+                 n_workers: int, devices=None, exchange: str = "auto", schedule: str = "auto"):
         if not isinstance(devices, (list, tuple)):
             devices = [devices] * n_workers
         self.devices = [_dev(d) for d in devices]
@@ -446,6 +542,10 @@ class LocalCluster:
         for w in range(self.n_workers):
             dev = self.devices[w]
             p = Plan(self.names, self.ns, cfg, worker=w, n_workers=self.n_workers, device=dev)
+            if schedule != "auto":
+                p.set_schedule(schedule)
+            if self.n_workers > 1 and exchange != "auto":
+                p.set_exchange(exchange)
             gf, gv = aligned_flat(self.ns, dev)
             of, ov = aligned_flat(self.ns, dev)
             p.bind(gv, ov)
@@ -457,14 +557,28 @@ class LocalCluster:
         if self.n_workers > 1:
             Plan.attach_local(self.plans)
         self.streams = [torch.cuda.Stream(d) for d in self.devices]
+        self.traffic = TrafficStats()  # ParameterServer::traffic(): all workers (cluster.hpp:147-160)
+        self._step_traffic = None
 
-    def step(self, t: int) -> List[List[torch.Tensor]]:
-        """Every worker's tgb_step for iteration t, each on its own stream (ordered
-        after work already queued on each device's current stream, e.g. the
-        gradients' producers)."""
-        for p, s, d in zip(self.plans, self.streams, self.devices):
+    @property
+    def exchange(self) -> str:
+        return self.plans[0].exchange
+
+    def step(self, t, check: bool = False) -> List[List[torch.Tensor]]:
+        """Every worker's step for iteration t (an int, or one per worker), each on
+        its own stream (ordered after work already queued on each device's current
+        stream, e.g. the gradients' producers)."""
+        ts = list(t) if isinstance(t, (list, tuple)) else [int(t)] * self.n_workers
+        for s, d in zip(self.streams, self.devices):
             s.wait_stream(torch.cuda.current_stream(d))
-            p.step(t, None, s)
+        Plan.local_step(self.plans, ts, self.streams)
+        if self._step_traffic is None:
+            self._step_traffic = TrafficStats()
+            for p in self.plans:
+                self._step_traffic += p.traffic()
+        self.traffic += self._step_traffic
+        if check:
+            self.check()
         return self.outs
 
     def synchronize(self):
@@ -479,3 +593,59 @@ class LocalCluster:
         self.synchronize()
         for p in self.plans:
             p.close()
+
+
+class TrafficStats:
+    """The reference's TrafficStats (cluster.hpp:62-74): framed bytes up/down in
+    the reference's wire format and the same tensors at raw fp32, plus what this
+    build's device exchange moved over NVLink."""
+
+    def __init__(self, bytes_up=0, bytes_down=0, float_bytes_up=0, float_bytes_down=0,
+                 device_bytes_out=0, device_bytes_in=0):
+        self.bytes_up, self.bytes_down = int(bytes_up), int(bytes_down)
+        self.float_bytes_up, self.float_bytes_down = int(float_bytes_up), int(float_bytes_down)
+        self.device_bytes_out, self.device_bytes_in = int(device_bytes_out), int(device_bytes_in)
+
+    @classmethod
+    def of(cls, t: "_lib.Traffic") -> "TrafficStats":
+        return cls(t.bytes_up, t.bytes_down, t.float_bytes_up, t.float_bytes_down,
+                   t.device_bytes_out, t.device_bytes_in)
+
+    @classmethod
+    def for_layers(cls, names: Sequence[str], ns: Sequence[int], cfg: CodecConfig,
+                   n_workers: int, passthrough: Optional[Sequence[bool]] = None) -> "TrafficStats":
+        """one worker-step's terms from a layer table alone (no device;
+        tgb_traffic_for_layers)"""
+        nl = len(names)
+        if passthrough is None:
+            passthrough = [cfg.float_mode or n in cfg.passthrough for n in names]
+        descs = (_lib.LayerDesc * max(nl, 1))()
+        for l, (name, n) in enumerate(zip(names, ns)):
+            descs[l] = _lib.LayerDesc(int(n), fnv1a64(name),
+                                      _lib.TGB_LAYER_PASSTHROUGH if passthrough[l] else 0, 0)
+        cn = (C.c_char_p * max(nl, 1))(*[x.encode() for x in names])
+        params = cfg.params()
+        t = _lib.Traffic()
+        check(load().tgb_traffic_for_layers(descs, cn, nl, C.byref(params), int(n_workers),
+                                            C.byref(t)), "tgb_traffic_for_layers")
+        return cls.of(t)
+
+    def __iadd__(self, o: "TrafficStats") -> "TrafficStats":
+        self.bytes_up += o.bytes_up
+        self.bytes_down += o.bytes_down
+        self.float_bytes_up += o.float_bytes_up
+        self.float_bytes_down += o.float_bytes_down
+        self.device_bytes_out += o.device_bytes_out
+        self.device_bytes_in += o.device_bytes_in
+        return self
+
+    def up_reduction(self) -> float:
+        return self.float_bytes_up / self.bytes_up if self.bytes_up else 1.0
+
+    def down_reduction(self) -> float:
+        return self.float_bytes_down / self.bytes_down if self.bytes_down else 1.0
+
+    def __repr__(self):
+        return (f"TrafficStats(up={self.bytes_up}, down={self.bytes_down}, "
+                f"float_up={self.float_bytes_up}, float_down={self.float_bytes_down}, "
+                f"device_out={self.device_bytes_out}, device_in={self.device_bytes_in})")

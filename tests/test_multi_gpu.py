@@ -1,9 +1,15 @@
-"""Multi-GPU parity (needs >= 2 GPUs; skipped on single-GPU boxes).
+"""Multi-GPU parity.
 
-Runs tools/mp_check.py under torchrun for the fused NVLink exchange and the
-NCCL-allgather exchange: every rank must hold bit-identical averaged
-gradients equal to the reference's average over the same workers
-(REF shared, unshared, and PRESHARED against its own oracle).
+* test_mp_check: tools/mp_check.py under torchrun, one process per GPU, for
+  N in {2, 4, 8} that fit the visible GPUs and every exchange (fused NVLink
+  stores, sharded owner sums, NCCL allgather): every rank holds bit-identical
+  averaged gradients equal to the reference's average over the same workers
+  (small sets: REF shared / unshared, Global, FixedSize + passthrough, PRESHARED
+  against its own oracle; full AlexNet and VGG-16 sets against the reference's
+  ParameterServer path), and the protocol checks (iteration skew, block
+  structure mismatch) raise the reference's ProtocolError texts.
+* test_local_cluster: N = 2..8 workers as plans of ONE process on cuda:0
+  (tools/local_cluster_check.py) -- the same exchange kernels without NVLink.
 """
 import json
 import os
@@ -15,39 +21,46 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = [pytest.mark.gpu]
+
+_NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+_CASES = [(n, ex) for n in (2, 4, 8) if n <= _NGPU for ex in ("auto", "sharded", "nccl")]
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("exchange", ["fused", "nccl"])
-def test_mp_check(exchange):
-    n = min(4, torch.cuda.device_count())
+@pytest.mark.multigpu
+@pytest.mark.skipif(_NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("n,exchange", _CASES or [(2, "auto")])
+def test_mp_check(n, exchange):
     env = dict(os.environ, TGB_EXCHANGE=exchange)
-    port = 29600 + (1 if exchange == "nccl" else 0)
+    port = 29600 + 10 * n + ("auto", "sharded", "nccl").index(exchange)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
                         "--master-port", str(port), os.path.join(ROOT, "tools", "mp_check.py")],
-                       capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+                       capture_output=True, text=True, timeout=1800, env=env, cwd=ROOT)
     line = [x for x in r.stdout.splitlines() if x.startswith("{")]
-    assert r.returncode == 0 and line, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.returncode == 0 and line, r.stdout[-3000:] + r.stderr[-3000:]
     rep = json.loads(line[0])
     assert rep["world_size"] == n
     for k, v in rep["checks"].items():
         assert v["ranks_identical"], k
-        assert v["matches_oracle"], k
+        assert v["matches_oracle"] in (True, None), k
+    for k in ("alexnet_full_set", "vgg16_full_set"):
+        assert rep["checks"][k]["matches_oracle"] is True, k
+    if exchange != "nccl":
+        assert "iteration_skew" in rep["checks"] and "block_structure_mismatch" in rep["checks"]
 
 
-def test_local_cluster_n8_on_one_gpu():
-    """N = 2/3/5/8 workers as plans of one process on cuda:0 (tgb_plan_attach_local):
-    the fused and sharded exchange kernels (incl. N = 8's 8-bit sums) bit-identical
-    on every worker and equal to the reference's average / the allgather path."""
-    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER")
+def test_local_cluster():
+    """N = 2..8 workers of one process on cuda:0: fused and sharded exchanges
+    bit-identical on every worker and equal to the reference's average; the
+    iteration-skew check. No launch-environment settings are needed."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "local_cluster_check.py")],
-                       capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
     line = [x for x in r.stdout.splitlines() if x.startswith("{")]
     assert line, r.stdout[-2000:] + r.stderr[-2000:]
     rep = json.loads(line[0])
     bad = {k: v for k, v in rep["checks"].items()
            if not (v["workers_identical"] and v["matches_reference"])}
     assert not bad and r.returncode == 0, bad
-    assert rep["checks"]["N=8,vgg16"]["exchange"] == "sharded"
+    assert rep["checks"]["N=8,exchange=sharded,sharing=True,bucketing=PerTensor,"
+                         "passthrough=-"]["exchange"] == "sharded"

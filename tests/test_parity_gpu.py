@@ -460,16 +460,16 @@ def test_optimizer_apply_vs_reference(rule):
             assert params[l].cpu().numpy().tobytes() == ref.tobytes(), (rule, wd, l)
 
 
-@pytest.mark.parametrize("rule,fused", [(1, "1"), (1, "0"), (2, "1"), (0, "1")])
-def test_step_apply_matches_step_then_optimizer(restated, monkeypatch, rule, fused):
+@pytest.mark.parametrize("rule,fused", [(1, 1), (1, 0), (2, 1), (0, 1)])
+def test_step_apply_matches_step_then_optimizer(restated, rule, fused):
     # tgb_step_apply (fused: the decode kernel applies the optimizer, the averaged
     # gradient is never written) == tgb_step + OptimizerState::apply
-    monkeypatch.setenv("TGB_OPT_FUSED", fused)
     names = ["conv.weight", "conv.bias", "fc.weight", "p"]
     ns = [1728, 64, 40003, 33]
     cfg = tg.CodecConfig(seed=42, passthrough={"p"})
     ocfg = tg.OptimizerConfig(rule=tg.OptimizerRule(rule), weight_decay=1e-4)
     w = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    w.plan.set_option(tg._lib.TGB_PLAN_OPT_FUSED_OPTIMIZER, fused)
     p0 = [(np.arange(n, dtype=np.float32) % 7) * 0.01 for n in ns]
     params = [to_dev(p) for p in p0]
     w.bind_optimizer(ocfg, params)

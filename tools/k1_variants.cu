@@ -1,0 +1,359 @@
+// K1 (clip statistics) design probe on B200: the per-chunk fp64 moment pass of
+// k1_stats over a VGG-16-sized buffer (138,357,544 fp32, 32K-element chunks),
+// in several loop / tail designs, against a plain streaming-read ceiling.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1705_07878_b200/csrc \
+//        -I include -o tools/k1_variants tools/k1_variants.cu && tools/k1_variants
+// Every variant writes per-chunk partials (n, mean, M2, max); the partial maxima
+// must agree exactly and the merged sigma to ~1e-15 (different summation orders).
+#include <cmath>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+#include "tgb_device.cuh"
+
+using namespace tgb;
+
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        cudaError_t e = (x);                                                             \
+        if (e != cudaSuccess) {                                                          \
+            printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);     \
+            return 1;                                                                    \
+        }                                                                                \
+    } while (0)
+
+constexpr uint32_t kCh = 32768;
+
+__device__ __forceinline__ void acc4(const float4 v, const double x0, double& S, double& Q,
+                                     float& mx) {
+    const double d0 = static_cast<double>(v.x) - x0, d1 = static_cast<double>(v.y) - x0;
+    const double d2 = static_cast<double>(v.z) - x0, d3 = static_cast<double>(v.w) - x0;
+    S += (d0 + d1) + (d2 + d3);
+    Q = fma(d0, d0, Q);
+    Q = fma(d1, d1, Q);
+    Q = fma(d2, d2, Q);
+    Q = fma(d3, d3, Q);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+}
+
+// float -> double without F2F (normal, nonzero finite floats only): integer ops
+__device__ __forceinline__ double f2d_int(float x) {
+    const uint32_t u = __float_as_uint(x);
+    const uint32_t hi = (((u & 0x7FFFFFFFu) >> 3) + 0x38000000u) | (u & 0x80000000u);
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+}
+__device__ __forceinline__ bool all_normal(const float4 v) {
+    // exponent field neither 0 (zero/subnormal) nor 255 (inf/nan) in all four
+    auto ok = [](float f) {
+        const uint32_t e = __float_as_uint(f) & 0x7F800000u;
+        return e != 0u && e != 0x7F800000u;
+    };
+    return ok(v.x) & ok(v.y) & ok(v.z) & ok(v.w);
+}
+__device__ __forceinline__ void acc4_int(const float4 v, const double x0, double& S, double& Q,
+                                         float& mx, bool normal) {
+    double a0, a1, a2, a3;
+    if (normal) {
+        a0 = f2d_int(v.x); a1 = f2d_int(v.y); a2 = f2d_int(v.z); a3 = f2d_int(v.w);
+    } else {
+        a0 = v.x; a1 = v.y; a2 = v.z; a3 = v.w;
+    }
+    const double d0 = a0 - x0, d1 = a1 - x0, d2 = a2 - x0, d3 = a3 - x0;
+    S += (d0 + d1) + (d2 + d3);
+    Q = fma(d0, d0, Q);
+    Q = fma(d1, d1, Q);
+    Q = fma(d2, d2, Q);
+    Q = fma(d3, d3, Q);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+}
+
+struct Out {
+    Partial* parts;
+    uint32_t* ticket;
+    int tail;  // 0: partial only, 1: + threadfence + atomic ticket (production tail)
+};
+
+template <int NT>
+__device__ __forceinline__ void emit(const Out& o, uint32_t c, uint32_t count, double x0, double S,
+                                     double Q, float mx) {
+    block_reduce_sq<NT / 32>(S, Q, mx);
+    if (threadIdx.x == 0) {
+        const double cn = count;
+        Partial p;
+        p.n = cn;
+        p.mean = x0 + S / cn;
+        p.m2 = Q - S * (S / cn);
+        p.mx = mx;
+        p.block = 0;
+        o.parts[c] = p;
+        if (o.tail) {
+            __threadfence();
+            atomicAdd(o.ticket, 1u);
+        }
+    }
+    __syncthreads();
+}
+
+// V0: production loop (U float4 in flight, compute after)
+template <int U, int NT, int MINB, int MODE>
+__global__ void __launch_bounds__(NT, MINB) k1_v0(const float* g, uint64_t n, Out o) {
+    const uint32_t c = blockIdx.x;
+    const uint64_t b0 = static_cast<uint64_t>(c) * kCh;
+    const uint32_t count = static_cast<uint32_t>(n - b0 < kCh ? n - b0 : kCh);
+    const float* p = g + b0;
+    const double x0 = static_cast<double>(__ldg(p));
+    double S = 0.0, Q = 0.0;
+    float mx = 0.0f;
+    const float4* g4 = reinterpret_cast<const float4*>(p);
+    const uint32_t n4 = count >> 2;
+    uint32_t i = threadIdx.x;
+    for (; i + (U - 1) * NT < n4; i += U * NT) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + i + u * NT);
+        if (MODE == 2) {  // compute-free: sum only (cost of the fp64 math)
+#pragma unroll
+            for (int u = 0; u < U; ++u) mx = fmaxf(mx, v[u].x + v[u].y + v[u].z + v[u].w);
+        } else if (MODE == 1) {
+            bool nrm = true;
+#pragma unroll
+            for (int u = 0; u < U; ++u) nrm &= all_normal(v[u]);
+            nrm = __all_sync(0xffffffffu, nrm);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc4_int(v[u], x0, S, Q, mx, nrm);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc4(v[u], x0, S, Q, mx);
+        }
+    }
+    for (; i < n4; i += NT) acc4(__ldcs(g4 + i), x0, S, Q, mx);
+    emit<NT>(o, c, count, x0, S, Q, mx);
+}
+
+// V1: software-pipelined: the next U float4 are issued before the current U are used
+template <int U, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k1_v1(const float* g, uint64_t n, Out o) {
+    const uint32_t c = blockIdx.x;
+    const uint64_t b0 = static_cast<uint64_t>(c) * kCh;
+    const uint32_t count = static_cast<uint32_t>(n - b0 < kCh ? n - b0 : kCh);
+    const float* p = g + b0;
+    const double x0 = static_cast<double>(__ldg(p));
+    double S = 0.0, Q = 0.0, S2 = 0.0, Q2 = 0.0;
+    float mx = 0.0f;
+    const float4* g4 = reinterpret_cast<const float4*>(p);
+    const uint32_t n4 = count >> 2;
+    const uint32_t iters = n4 / (U * NT);  // full batches
+    float4 cur[U], nxt[U];
+    uint32_t i = threadIdx.x;
+    if (iters) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = __ldcs(g4 + i + u * NT);
+    }
+    for (uint32_t it = 0; it < iters; ++it, i += U * NT) {
+        if (it + 1 < iters) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) nxt[u] = __ldcs(g4 + i + U * NT + u * NT);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u & 1) acc4(cur[u], x0, S2, Q2, mx);
+            else acc4(cur[u], x0, S, Q, mx);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
+    for (; i < n4; i += NT) acc4(__ldcs(g4 + i), x0, S, Q, mx);
+    emit<NT>(o, c, count, x0, S + S2, Q + Q2, mx);
+}
+
+// V2: persistent CTAs, the next chunk's first batch issued before this chunk's tail
+template <int U, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k1_v2(const float* g, uint64_t n, uint32_t n_chunks,
+                                                 Out o) {
+    float4 v[U];
+    uint32_t c = blockIdx.x;
+    auto issue = [&](uint32_t cc, uint32_t i) {
+        const uint64_t b0 = static_cast<uint64_t>(cc) * kCh;
+        const uint32_t count = static_cast<uint32_t>(n - b0 < kCh ? n - b0 : kCh);
+        const float4* g4 = reinterpret_cast<const float4*>(g + b0);
+        const uint32_t n4 = count >> 2;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t j = i + u * NT;
+            v[u] = j < n4 ? __ldcs(g4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    if (c < n_chunks) issue(c, threadIdx.x);
+    for (; c < n_chunks; c += gridDim.x) {
+        const uint64_t b0 = static_cast<uint64_t>(c) * kCh;
+        const uint32_t count = static_cast<uint32_t>(n - b0 < kCh ? n - b0 : kCh);
+        const float4* g4 = reinterpret_cast<const float4*>(g + b0);
+        const uint32_t n4 = count >> 2;
+        const double x0 = static_cast<double>(__ldg(g + b0));
+        double S = 0.0, Q = 0.0;
+        float mx = 0.0f;
+        // batches of U*NT float4; v holds the current batch (zero-padded)
+        const uint32_t nb = (n4 + U * NT - 1) / (U * NT);
+        for (uint32_t b = 0; b < nb; ++b) {
+            float4 w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) w[u] = v[u];
+            if (b + 1 < nb) {
+                const uint32_t ni = (b + 1) * U * NT + threadIdx.x;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t j = ni + u * NT;
+                    v[u] = j < n4 ? __ldcs(g4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            } else if (c + gridDim.x < n_chunks) {
+                issue(c + gridDim.x, threadIdx.x);
+            }
+            const uint32_t i = b * U * NT + threadIdx.x;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t j = i + u * NT;
+                if (j < n4) acc4(w[u], x0, S, Q, mx);
+            }
+        }
+        emit<NT>(o, c, count, x0, S, Q, mx);
+    }
+}
+
+// read-only ceiling: same grid, sum of floats
+template <int U, int NT>
+__global__ void __launch_bounds__(NT) read_probe(const float* g, uint64_t n, float* sink) {
+    const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kCh;
+    const uint32_t count = static_cast<uint32_t>(n - b0 < kCh ? n - b0 : kCh);
+    const float4* g4 = reinterpret_cast<const float4*>(g + b0);
+    float acc = 0.f;
+    for (uint32_t i = threadIdx.x; i < (count >> 2); i += U * NT) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t j = i + u * NT;
+            v[u] = j < (count >> 2) ? __ldcs(g4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    }
+    if (acc == 1234.5f) *sink = acc;
+}
+
+__global__ void fill(float* g, uint64_t n) {
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += 256ull * gridDim.x) {
+        uint32_t h = static_cast<uint32_t>(i) * 2654435761u ^ static_cast<uint32_t>(i >> 32);
+        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+        g[i] = (static_cast<float>(h & 0xFFFFFF) / 16777216.0f - 0.5f) * 2e-3f;
+    }
+}
+
+int main() {
+    const uint64_t n = 138357544ull;
+    const uint32_t nc = static_cast<uint32_t>((n + kCh - 1) / kCh);
+    float* g;
+    Partial* parts;
+    uint32_t* ticket;
+    float* sink;
+    CK(cudaMalloc(&g, n * 4));
+    CK(cudaMalloc(&parts, nc * sizeof(Partial)));
+    CK(cudaMalloc(&ticket, 4));
+    CK(cudaMalloc(&sink, 4));
+    fill<<<148 * 8, 256>>>(g, n);
+    CK(cudaDeviceSynchronize());
+    // 256 MB scratch written between launches: the previous launch's data is not in L2
+    uint8_t* flush;
+    CK(cudaMalloc(&flush, 256ull << 20));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<Partial> ref(nc), got(nc);
+    int dirty = 1;  // 1: a 256 MB memset before each launch (dirty L2 lines, like a step
+                    // after K2's output writes); 0: a 256 MB read (clean L2)
+    auto timeit = [&](const char* name, auto launch, bool check) {
+        float best = 1e9f, sum = 0.f;
+        const int R = 15;
+        for (int r = 0; r < R + 2; ++r) {
+            if (dirty) {
+                cudaMemsetAsync(flush, r, 256ull << 20);
+            } else {
+                read_probe<4, 256><<<(256u << 20) / 4 / kCh, 256>>>(reinterpret_cast<float*>(flush),
+                                                                  (256ull << 20) / 4, sink);
+            }
+            cudaEventRecord(e0);
+            launch();
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (r >= 2) {
+                best = fminf(best, ms);
+                sum += ms;
+            }
+        }
+        cudaError_t err = cudaGetLastError();
+        const char* verdict = "";
+        if (check) {
+            cudaMemcpy(got.data(), parts, nc * sizeof(Partial), cudaMemcpyDeviceToHost);
+            static bool have = false;
+            if (!have) {
+                ref = got;
+                have = true;
+            }
+            // merged sigma + max
+            auto merge = [&](const std::vector<Partial>& P, double& sig, float& m) {
+                double N = 0, mean = 0, m2 = 0;
+                m = 0;
+                for (auto& p : P) {
+                    const double nn = N + p.n, d = p.mean - mean, f = p.n / nn;
+                    mean += d * f;
+                    m2 += p.m2 + d * d * N * f;
+                    N = nn;
+                    m = fmaxf(m, p.mx);
+                }
+                sig = sqrt(m2 / N);
+            };
+            double s0, s1;
+            float m0, m1;
+            merge(ref, s0, m0);
+            merge(got, s1, m1);
+            verdict = (m0 == m1 && fabs(s0 - s1) <= 1e-14 * s0) ? "ok" : "MISMATCH";
+            printf("   sigma %.17g max %.9g  ", s1, m1);
+        }
+        printf("%-44s best %7.1f us  mean %7.1f us  %7.1f GB/s  %s %s\n", name, best * 1e3,
+               sum / R * 1e3, 4.0 * n / (best * 1e-3) / 1e9, verdict,
+               err == cudaSuccess ? "" : cudaGetErrorString(err));
+    };
+    Out o0{parts, ticket, 1}, oN{parts, ticket, 0};
+  for (dirty = 1; dirty >= 0; --dirty) {
+    printf("---- L2 before each launch: %s\n", dirty ? "dirty (256 MB memset)" : "clean (256 MB read)");
+    timeit("read probe U=4", [&] { read_probe<4, 256><<<nc, 256>>>(g, n, sink); }, false);
+    timeit("read probe U=8", [&] { read_probe<8, 256><<<nc, 256>>>(g, n, sink); }, false);
+    timeit("V0 prod U=8 minB4 (tail)", [&] { k1_v0<8, 256, 4, 0><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V0 prod U=8 minB4 (no fence/atomic)", [&] { k1_v0<8, 256, 4, 0><<<nc, 256>>>(g, n, oN); }, true);
+    timeit("V0 no fp64 math U=8 minB4", [&] { k1_v0<8, 256, 4, 2><<<nc, 256>>>(g, n, o0); }, false);
+    timeit("V0 int f2d U=8 minB4", [&] { k1_v0<8, 256, 4, 1><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V0 U=4 minB4", [&] { k1_v0<4, 256, 4, 0><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V0 U=4 minB6", [&] { k1_v0<4, 256, 6, 0><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V0 U=8 NT=512 minB2", [&] { k1_v0<8, 512, 2, 0><<<nc, 512>>>(g, n, o0); }, true);
+    timeit("V0 U=4 NT=512 minB3", [&] { k1_v0<4, 512, 3, 0><<<nc, 512>>>(g, n, o0); }, true);
+    timeit("V1 pipelined U=4 minB4", [&] { k1_v1<4, 256, 4><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V1 pipelined U=4 minB3", [&] { k1_v1<4, 256, 3><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V1 pipelined U=2 minB6", [&] { k1_v1<2, 256, 6><<<nc, 256>>>(g, n, o0); }, true);
+    for (int per : {3, 4, 6}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "V2 persistent U=4 %d CTA/SM", per);
+        const uint32_t grid = static_cast<uint32_t>(sms * per);
+        timeit(nm, [&] { k1_v2<4, 256, 3><<<grid, 256>>>(g, n, nc, o0); }, true);
+    }
+    for (int per : {2, 3}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "V2 persistent U=8 %d CTA/SM", per);
+        const uint32_t grid = static_cast<uint32_t>(sms * per);
+        timeit(nm, [&] { k1_v2<8, 256, 2><<<grid, 256>>>(g, n, nc, o0); }, true);
+    }
+  }
+    return 0;
+}

@@ -1,14 +1,22 @@
 """Multi-GPU parity + timing check (one process per GPU, torchrun).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 tools/mp_check.py
+    TGB_EXCHANGE=auto|fused|sharded|nccl torchrun --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port 29511 tools/mp_check.py
 
-Every rank encodes its own gradients (worker id = rank), the plan's NCCL
-allgather exchanges scalers+codes, K3 decodes on every rank. Checks:
+Every rank encodes its own gradients (worker id = rank), the exchange
+(NVLink peer stores, fused or sharded, or the NCCL allgather) moves
+scalers + codes, every rank decodes. Checks:
   * all ranks hold bit-identical averaged gradients (the reference's
     "every worker decodes the same pull", cluster.hpp:153-161);
   * on the small tensor set, the result is bit-identical to the reference's
     average over the same N workers (oracle/_ref, cluster_test.cpp:157-195),
-    for shared and unshared scalers and the PRESHARED mode's own oracle.
+    for shared and unshared scalers and the PRESHARED mode's own oracle;
+  * the full AlexNet and VGG-16 sets are bit-identical to the reference's own
+    sync path (ParameterServer over InProcessHub, RefCluster) on the same inputs;
+  * protocol validation: ranks stepping different iterations raise the
+    reference's "server: iteration skew" ProtocolError (cluster.hpp:141-143) and
+    leave the outputs untouched; ranks with different layer tables fail at
+    attach with "server: block structure mismatch" (cluster.hpp:169-172).
 Prints one JSON line from rank 0.
 """
 import hashlib
@@ -24,7 +32,95 @@ import torch.distributed as dist  # noqa: E402
 
 import paper_1705_07878_b200 as tg  # noqa: E402
 
-FUSED = os.environ.get("TGB_EXCHANGE", "fused") != "nccl"
+EXCHANGE = os.environ.get("TGB_EXCHANGE", "auto")
+
+
+def ex_for(sharing):
+    """the sharded exchange needs shared scalers (the owner sums integer codes)"""
+    return "auto" if (EXCHANGE == "sharded" and not sharing) else EXCHANGE
+
+
+def full_set_checks(report, rank, ws, comm, dev):
+    """AlexNet and VGG-16 full sets vs the reference's own sync path (RefCluster)"""
+    import numpy as np
+    from oracle.oracle import Config, RefCluster, Reference
+
+    for set_name in ("alexnet", "vgg16"):
+        layers = tg.layersets.get(set_name)
+        names, shapes = [n for n, _ in layers], [s for _, s in layers]
+        ns = [tg.layersets.numel(s) for s in shapes]
+
+        def grads_of(w):
+            rng = np.random.default_rng(1000 + w)
+            return [rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3) for n in ns]
+
+        sw = tg.SyncWorker(names, shapes, tg.CodecConfig(seed=42), rank=rank, world_size=ws,
+                           comm=comm, device=dev, exchange=EXCHANGE)
+        for v, g in zip(sw.grads, grads_of(rank)):
+            v.copy_(torch.from_numpy(g).to(dev))
+        for t in (10, 11, 12):
+            sw.step(t)
+        sw.check()
+        torch.cuda.synchronize()
+        flat = torch.cat([o.cpu() for o in sw.outs]).numpy()
+        h = hashlib.sha256(flat.tobytes()).hexdigest()
+        hs = [None] * ws
+        dist.all_gather_object(hs, h)
+        ok_ref = None
+        if rank == 0:
+            cl = RefCluster(Reference(), names, [grads_of(w) for w in range(ws)], Config(seed=42))
+            cl.step(12)
+            want = cl.output(0)
+            cl.close()
+            ok_ref = bool(np.array_equal(want.view(np.uint32), flat.view(np.uint32)))
+        report["checks"][f"{set_name}_full_set"] = {"ranks_identical": len(set(hs)) == 1,
+                                                    "matches_oracle": ok_ref,
+                                                    "exchange": sw.plan.exchange}
+        dist.barrier()
+        sw.plan.close()
+
+
+def protocol_checks(report, rank, ws, comm, dev):
+    """iteration skew (cluster.hpp:141-143) and block-structure mismatch (:169-172)"""
+    names = ["a.weight", "a.bias"]
+    cfg = tg.CodecConfig(seed=42)
+    sw = tg.SyncWorker(names, [[5000], [10]], cfg, rank=rank, world_size=ws, comm=comm,
+                       device=dev, exchange=EXCHANGE)
+    sw.grad_flat.normal_(0, 1e-2, generator=torch.Generator(device=dev).manual_seed(rank))
+    sw.step(3, check=True)
+    before = sw.out_flat.clone()
+    msg = None
+    if EXCHANGE != "nccl":  # the NCCL allgather carries no iteration
+        sw.step(4 + (rank == 1))  # rank 1 is one iteration ahead
+        try:
+            sw.check()
+        except tg.ProtocolError as e:
+            msg = str(e)
+        untouched = torch.equal(before, sw.out_flat)
+        msgs = [None] * ws
+        dist.all_gather_object(msgs, msg)
+        report["checks"]["iteration_skew"] = {
+            "ranks_identical": all(m is not None and "server: iteration skew" in m for m in msgs)
+            and untouched, "matches_oracle": None, "messages": msgs}
+        sw.step(9, check=True)  # the exchange recovers on the next agreeing step
+    dist.barrier()
+    sw.plan.close()
+    if EXCHANGE == "nccl":
+        return
+    sizes = [[5000], [10 + (rank == ws - 1)]]  # the last rank's bias has one more element
+    err = None
+    try:
+        bad = tg.SyncWorker(names, sizes, cfg, rank=rank, world_size=ws, comm=comm, device=dev,
+                            exchange=EXCHANGE)
+        bad.plan.close()
+    except tg.ProtocolError as e:
+        err = str(e)
+    errs = [None] * ws
+    dist.all_gather_object(errs, err)
+    report["checks"]["block_structure_mismatch"] = {
+        "ranks_identical": all(e is not None and "block structure mismatch" in e for e in errs),
+        "matches_oracle": None, "messages": errs}
+    dist.barrier()
 
 
 def main():
@@ -40,7 +136,7 @@ def main():
     R = Restated()
     names = ["conv1.weight", "conv1.bias", "empty", "fc.weight", "fc.bias"]
     sizes = [1728, 64, 0, 40003, 10]
-    report = {"world_size": ws, "exchange": "fused" if FUSED else "nccl", "checks": {}}
+    report = {"world_size": ws, "exchange": EXCHANGE, "checks": {}}
     P, G, F = tg.Bucketing.PerTensor, tg.Bucketing.Global, tg.Bucketing.FixedSize
     configs = [  # (sharing, mode, bucketing, k, passthrough names)
         (True, tg.ShareMode.REF, P, 0, ()), (False, tg.ShareMode.REF, P, 0, ()),
@@ -54,7 +150,7 @@ def main():
                              bucketing=bucketing, bucket_size=k, passthrough=set(pt_names))
         pt = [int(n in pt_names) for n in names]
         sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws, comm=comm,
-                           device=dev, fused=FUSED)
+                           device=dev, exchange=ex_for(sharing))
         grads = [R.normal(100 + rank, 0, "mp/" + n, k, 1e-2) for n, k in zip(names, sizes)]
         for v, g in zip(sw.grads, grads):
             if g.size:
@@ -81,10 +177,8 @@ def main():
                 ok_ref = st == 0 and np.array_equal(ref.view(np.uint32), flat.view(np.uint32))
             else:  # PRESHARED: every worker ternarizes with s = max_w s_w (paper Eq. 4)
                 ok_ref = preshared_oracle(R, names, allg, flat, ws, ocfg, pt)
-        info = tg._lib.PlanInfo()
-        tg._lib.check(tg._lib.load().tgb_plan_get_info(sw.plan.h, tg.codec.C.byref(info)), "info")
         report["checks"][key] = {"ranks_identical": ok_same, "matches_oracle": ok_ref,
-                                 "exchange": tg._lib.EXCHANGE_NAMES[info.exchange]}
+                                 "exchange": sw.plan.exchange}
         dist.barrier()
         sw.plan.close()
 
@@ -93,9 +187,9 @@ def main():
         ocfg = tg.OptimizerConfig(rule=rule, weight_decay=1e-4)
         cfg = tg.CodecConfig(seed=42)
         sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws,
-                           comm=comm, device=dev, fused=FUSED)
+                           comm=comm, device=dev, exchange=ex_for(sharing))
         ref = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws,
-                            comm=comm, device=dev, fused=FUSED)
+                            comm=comm, device=dev, exchange=ex_for(sharing))
         p0 = [torch.full((n,), 0.5, device=dev) for n in sizes]
         params = [x.clone() for x in p0]
         ref_params = [x.clone() for x in p0]
@@ -121,10 +215,13 @@ def main():
         sw.plan.close()
         ref.plan.close()
 
+    full_set_checks(report, rank, ws, comm, dev)
+    protocol_checks(report, rank, ws, comm, dev)
+
     # timing: full VGG-16 step at this world size
     layers = tg.layersets.get("vgg16")
     sw = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
-                       rank=rank, world_size=ws, comm=comm, device=dev, fused=FUSED)
+                       rank=rank, world_size=ws, comm=comm, device=dev, exchange=ex_for(sharing))
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     sw.grad_flat.normal_(0.0, 1e-3, generator=gen)
     st = torch.cuda.current_stream(dev)
@@ -150,7 +247,7 @@ def main():
     sw.check()
     stage = [sorted(e[i].elapsed_time(e[i + 1]) for e in ev)[K // 2] for i in range(4)]
     staged = ev[0][0].elapsed_time(ev[-1][4]) / K
-    # the product path: tgb_step (pipelined / sharded / fused schedule)
+    # the product path: tgb_step (sharded / fused schedule)
     for t in range(3):
         sw.step(100 + t)
     torch.cuda.synchronize()
@@ -168,9 +265,7 @@ def main():
     dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
     if rank == 0:
         n = sum(sw.ns)
-        info = tg._lib.PlanInfo()
-        tg._lib.check(tg._lib.load().tgb_plan_get_info(p.h, tg.codec.C.byref(info)), "info")
-        report["vgg16_exchange"] = tg._lib.EXCHANGE_NAMES[info.exchange]
+        report["vgg16_exchange"] = p.exchange
         report["vgg16_ms_per_step_max_over_ranks"] = float(t_all[0])
         report["stage_ms_median_max_over_ranks"] = {
             k: float(v) for k, v in zip(["K1", "K2", "sync", "K3"], t_all[1:5])}

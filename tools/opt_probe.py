@@ -17,9 +17,9 @@ names, shapes = [n for n, _ in layers], [s for _, s in layers]
 ocfg = tg.OptimizerConfig(rule=tg.OptimizerRule(rule))
 st = torch.cuda.current_stream(dev)
 res = {}
-for fused in ("1", "0"):
-    os.environ["TGB_OPT_FUSED"] = fused
+for fused in (1, 0):
     w = tg.SyncWorker(names, shapes, tg.CodecConfig(seed=42), device=dev)
+    w.plan.set_option(tg._lib.TGB_PLAN_OPT_FUSED_OPTIMIZER, fused)
     w.grad_flat.normal_(0, 1e-3, generator=torch.Generator(device=dev).manual_seed(1))
     pflat, params = tg.aligned_flat(w.ns, dev)
     w.bind_optimizer(ocfg, params)
@@ -36,4 +36,4 @@ for fused in ("1", "0"):
     w.check()
     res[fused] = (statistics.median(ts), pflat.clone())
     print(f"rule {ocfg.rule.name} fused={fused}: {res[fused][0]*1e3:.1f} us/step", flush=True)
-print("params identical fused vs unfused:", torch.equal(res["1"][1], res["0"][1]))
+print("params identical fused vs unfused:", torch.equal(res[1][1], res[0][1]))

@@ -24,8 +24,6 @@ wl = sys.argv[1] if len(sys.argv) > 1 else "vgg16"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 mode = sys.argv[3] if len(sys.argv) > 3 else ""
 staged = mode == "staged"  # K1 | K2 | K3 on one ungrouped plan
-if mode in ("staged", "ungrouped"):
-    os.environ["TGB_GROUPS"] = "0"
 if mode == "k3n4":
     layers = layersets.get(wl)
     dev = torch.device("cuda", 0)
@@ -51,7 +49,7 @@ if mode == "k3n4":
 layers = layersets.get(wl)
 dev = torch.device("cuda", 0)
 w = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
-                  device=dev)
+                  device=dev, schedule="single" if mode in ("staged", "ungrouped") else "auto")
 g = torch.Generator(device=dev).manual_seed(1)
 w.grad_flat.normal_(0.0, 1e-3, generator=g)
 for t in range(steps):
