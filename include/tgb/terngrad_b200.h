@@ -153,11 +153,11 @@ tgb_status tgb_plan_layer_layout(const tgb_plan* plan, int32_t layer, uint64_t* 
 tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_info* out);
 /* ---- plan options (no environment variables: every schedule choice is explicit) ----
  * TGB_PLAN_OPT_SCHEDULE: TGB_SCHEDULE_AUTO (dominant tensor || the rest on two streams
- *   when one tensor holds 35-95 % of the elements, PerTensor + REF; sets under 8 Mi
- *   elements run K1 + K2 as one persistent launch), _SINGLE (one stream, every kernel
- *   covers the whole set), _GROUPS (force the two-group split), _UNFUSED (one stream,
- *   K1 and K2 always separate launches), _FUSED12 (one stream, K1 + K2 always one
- *   launch). Rebuilds the work tables (re-binds the bound pointers).
+ *   when one tensor holds 35-95 % of the elements, PerTensor + REF), _SINGLE (one
+ *   stream, every kernel covers the whole set), _GROUPS (force the two-group split),
+ *   _UNFUSED (= _SINGLE), _FUSED12 (one stream, K1 + K2 as one persistent launch;
+ *   measured slower, kept for A/B). Rebuilds the work tables (re-binds the bound
+ *   pointers).
  * TGB_PLAN_OPT_EXCHANGE: TGB_EXCHANGE_AUTO / _FUSED / _SHARDED; before attaching peers.
  * TGB_PLAN_OPT_FUSED_OPTIMIZER: 1 (default) the decode kernel applies the optimizer in
  *   tgb_step_apply; 0 the averaged gradient is written and a separate kernel applies it. */

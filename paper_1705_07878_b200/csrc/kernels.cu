@@ -38,7 +38,8 @@ struct SingleSource {
     uint32_t chunk;  // elements per work item
     __device__ __forceinline__ void get(uint32_t b, ChunkDev& ch, LayerDev& L_) const {
         ch.layer = 0;
-        ch.begin = static_cast<uint64_t>(b) * chunk;
+        ch.begin = b * chunk;
+        ch.nblk = 1;
         const uint64_t rem = L.n - ch.begin;
         ch.count = static_cast<uint32_t>(rem < chunk ? rem : chunk);
         L_ = L;
@@ -72,11 +73,76 @@ __device__ __forceinline__ float4 k1_ld4(const float4* p, uint64_t pol) {
     }
 }
 
+// log2(k) of a multi-bucket tensor's buckets
+__device__ __forceinline__ uint32_t bucket_log2(const LayerDev& L) {
+    return (L.flags >> kBucketShiftBit) & 31u;
+}
+
+constexpr uint32_t kMaxItemBuckets = kChunk12 / 64;  // k >= 64
+
+// K1 unit spanning ch.nblk whole buckets of a FixedSize(k) tensor (k = 2^p >= 64):
+// the same fp64 moments as k1_unit (statistics are per TENSOR, codec.hpp:206-209),
+// plus every bucket's max |x| (scaler before the clip, :226-230). A float4 lies
+// in one bucket; lanes holding the same bucket (__match_any_sync) reduce with
+// one REDUX and their leader folds it into a shared-memory max per bucket, which
+// the CTA finally stores to bmax[block] (the item owns its buckets whole).
+template <int U>
+__device__ __forceinline__ void k1_unit_mb(const K1Out& o, const ChunkDev& ch, const LayerDev& L,
+                                           uint32_t unit) {
+    __shared__ uint32_t smax[kMaxItemBuckets];
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t j = tid; j < ch.nblk; j += kThreads) smax[j] = 0u;
+    __syncthreads();
+    const float* g = L.g;
+    const uint32_t count = ch.count;
+    const uint32_t sh4 = bucket_log2(L) - 2;  // float4 index -> bucket
+    const double x0 = static_cast<double>(__ldg(g));
+    double S = 0.0, Q = 0.0;
+    float mx = 0.0f;
+    auto fold = [&](uint32_t j, float m) {  // per-bucket max of non-negative floats as bits
+        const uint32_t peers = __match_any_sync(__activemask(), j);
+        const uint32_t v = __reduce_max_sync(peers, __float_as_uint(m));
+        if ((threadIdx.x & 31u) == static_cast<uint32_t>(__ffs(peers) - 1)) atomicMax(smax + j, v);
+    };
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    const uint32_t n4 = count >> 2;  // k % 4 == 0: only the tensor's last bucket can be ragged
+    uint32_t i = tid;
+    for (; i + (U - 1) * kThreads < n4; i += U * kThreads) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + i + u * kThreads);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            acc4(v[u], x0, S, Q, mx);
+            fold((i + u * kThreads) >> sh4, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
+                                                  fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+        }
+    }
+    for (; i < n4; i += kThreads) {
+        const float4 v = __ldcs(g4 + i);
+        acc4(v, x0, S, Q, mx);
+        fold(i >> sh4, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (uint32_t e = (n4 << 2) + tid; e < count; e += kThreads) {
+        const float x = __ldcs(g + e);
+        acc1(x, x0, S, Q, mx);
+        atomicMax(smax + (e >> (sh4 + 2)), __float_as_uint(fabsf(x)));
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < ch.nblk; j += kThreads) o.bmax[ch.layer + j] = smax[j];
+    k1_emit_and_finalize(o, L, ch.layer, unit, L.first_chunk, L.n_chunks, count, x0, S, Q, mx,
+                         false);
+}
+
 // One K1 work unit (a chunk of one block): fp64 moments of the chunk shifted by
 // its first element, then the partial + the tensor's finalize (tgb_stats.cuh).
 template <int U, int A, bool kHint>
 __device__ __forceinline__ void k1_unit(const K1Out& o, const ChunkDev& ch, const LayerDev& L,
                                         uint32_t unit) {
+    if (ch.nblk > 1) {  // multi-bucket item
+        k1_unit_mb<U>(o, ch, L, unit);
+        return;
+    }
     const float* g = L.g + ch.begin;
     const uint32_t count = ch.count;
     const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
@@ -132,6 +198,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
     if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;  // this group's K2 counts next
     if (L.flags & kLayerPassthrough) return;
     k1_unit<U, A, kHint>(o, ch, L, blockIdx.x);
+}
+
+// K1b (FixedSize plans): every bucket's scaler from its max and its tensor's
+// clip bound, s = min(max |part|, bound) = max |clip(part)| (codec.hpp:121-122,
+// :226-230; a non-finite tensor has bound 0, so s = 0), into the scaler slots
+// (and every peer's copy); resets the bucket maxima for the next step.
+// meta[b] = {tensor, slot} (slot ~0u: passthrough block).
+__global__ void __launch_bounds__(kThreads) k1_bucket_slots(const uint2* meta, uint32_t n_blocks,
+                                                            K1Out o) {
+    for (uint32_t b = blockIdx.x * kThreads + threadIdx.x; b < n_blocks; b += gridDim.x * kThreads) {
+        const uint2 m = meta[b];
+        if (m.y == ~0u) continue;
+        const float bound = __ldcg(o.bounds + o.tensors[m.x].first_block);
+        const float mx = __uint_as_float(o.bmax[b]);
+        o.bmax[b] = 0u;
+        o.bounds[b] = bound;
+        put_slot(o, static_cast<int32_t>(m.y), fminf(mx, bound));
+    }
 }
 
 // ====================================================================== K2
@@ -206,8 +290,11 @@ __device__ __forceinline__ void copy_out(const uint8_t* stage, uint8_t* dst, uin
 // The staged bytes to n_dst global destinations (local or peer memory) with the
 // TMA engine: one thread issues a cp.async.bulk per destination for the 16-B
 // multiple head, the CTA stores a ragged tail; full completion is awaited before
-// the CTA retires, so grid completion still orders these writes before a later
-// kernel (the step barrier). Falls back to copy_out for misaligned destinations.
+// the CTA retires (or reuses `stage`), so grid completion orders these writes
+// before a later kernel (the step barrier). Waiting only for the TMA engine to
+// have read the staged bytes (wait_group.read) measured no faster at N = 2 / 4
+// (VGG-16 0.394 vs 0.39 ms), so the stricter form stays. Falls back to copy_out
+// for misaligned destinations.
 // Call with the staged bytes complete (after a CTA barrier).
 template <class DstF>
 __device__ __forceinline__ void bulk_copy_out(const uint8_t* stage, DstF dst, int n_dst,
@@ -329,6 +416,114 @@ __device__ __forceinline__ void demote_l2(const float* g, uint32_t count) {
         asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(a) : "memory");
 }
 
+// Multi-bucket K2 item: ch.nblk whole buckets of k = 2^p elements (k/4 code bytes
+// each, contiguous). Each bucket has its own scaler: the per-bucket decision
+// constants (Decider) are computed once per item into shared memory and code
+// byte q uses bucket q >> (p - 2). Philox counters are the tensor's element
+// indices (ternarize's rng_base = the bucket offset, codec.hpp:167, :229), so
+// the whole item is one lane-aligned counter range. s == 0 buckets emit 00
+// codes (codec.hpp:155-159). kFuse / kOpt as k2_code_chunk.
+template <int U, bool kFuse, bool kOpt>
+__device__ __forceinline__ uint32_t k2_code_chunk_mb(const K2Args& a, const LayerDev& L,
+                                                     const ChunkDev& ch, uint8_t* __restrict__ stage) {
+    __shared__ float4 dp[kMaxItemBuckets];       // per bucket: s, ib, rl, dr
+    __shared__ uint8_t dmode[kMaxItemBuckets];   // 0 fast+exact, 1 exact only, 2 s == 0
+    const uint32_t tid = threadIdx.x;
+    const float bound = a.bounds ? __ldcg(a.bounds + ch.layer) : INFINITY;
+    for (uint32_t j = tid; j < ch.nblk; j += kThreads) {
+        const float s = __ldcg(a.slots + L.slot + j);
+        Decider d;
+        d.init(bound, s);
+        dp[j] = make_float4(s, d.ib, d.rl, d.dr);
+        dmode[j] = s == 0.0f ? 2 : (d.exact_all ? 1 : 0);
+    }
+    __syncthreads();
+    const uint32_t count = ch.count;
+    const uint32_t nbytes = (count + 3) >> 2;
+    const uint32_t nfull = count >> 2;
+    const uint32_t shq = bucket_log2(L) - 2;  // code byte -> bucket
+    const float* g = L.g;
+    const uint64_t qg = block_rng_base(L) >> 2;  // k % 4 == 0: lane aligned
+    Philox4<false> ph;
+    ph.init(L.key0, L.key1, static_cast<uint32_t>(qg >> 32), a.t);
+    const uint32_t qbase = static_cast<uint32_t>(qg);
+    float* out = L.out;
+    const bool vec_in = (L.flags & kLayerVecIn) != 0, vec_out = (L.flags & kLayerVecOut) != 0;
+    OptDev od{};
+    if (kOpt) od = a.optd[ch.layer];
+    auto byte_of = [&](float4 v, uint4 r, uint32_t q) -> uint32_t {
+        const uint32_t j = q >> shq;
+        const uint32_t mode = dmode[j];
+        if (mode == 2) return 0u;
+        const float4 c = dp[j];
+        Decider d;
+        d.bound = bound;
+        d.s = c.x;
+        d.ib = c.y;
+        d.rl = c.z;
+        d.dr = c.w;
+        d.exact_all = mode != 0;
+        return d.byte(v, r);
+    };
+    auto emit = [&](uint32_t q, uint32_t byte) {  // (s * float(code)) * 1 per element
+        if (!kFuse) return;
+        const float s = dp[q >> shq].x;
+        auto val = [&](uint32_t c) {
+            return __fmul_rn(__fmul_rn(s, c == 1u ? 1.0f : (c == 2u ? -1.0f : 0.0f)), 1.0f);
+        };
+        const float4 o = make_float4(val(byte & 3u), val((byte >> 2) & 3u), val((byte >> 4) & 3u),
+                                     val(byte >> 6));
+        const uint32_t e = 4 * q;
+        if (kOpt) {
+            opt_apply4(a.opt, od.w + e, od.s1 ? od.s1 + e : nullptr, od.s2 ? od.s2 + e : nullptr, o,
+                       od.vec != 0, count - e < 4 ? count - e : 4);
+        } else if (vec_out && e + 4 <= count) {
+            __stcs(reinterpret_cast<float4*>(out) + q, o);
+        } else {
+            if (e < count) out[e] = o.x;
+            if (e + 1 < count) out[e + 1] = o.y;
+            if (e + 2 < count) out[e + 2] = o.z;
+            if (e + 3 < count) out[e + 3] = o.w;
+        }
+    };
+    auto load4 = [&](uint32_t q) {
+        if (vec_in && 4 * q + 4 <= count) return __ldcs(reinterpret_cast<const float4*>(g) + q);
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = 4 * q + e < count ? g[4 * q + e] : 0.0f;
+        return make_float4(x[0], x[1], x[2], x[3]);
+    };
+    uint32_t q = tid;
+    for (uint32_t blk = 0; blk + U * kThreads <= nfull; blk += U * kThreads, q += U * kThreads) {
+        float4 v[U];
+        uint32_t ctr[U];
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = load4(q + u * kThreads);
+#pragma unroll
+        for (int u = 0; u < U; ++u) ctr[u] = qbase + q + u * kThreads;
+        ph(ctr, r);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t byte = byte_of(v[u], r[u], q + u * kThreads);
+            stage[q + u * kThreads] = static_cast<uint8_t>(byte);
+            emit(q + u * kThreads, byte);
+        }
+    }
+    for (; q < nbytes; q += kThreads) {  // tail (and the tensor's ragged last byte)
+        const float4 v = load4(q);
+        uint32_t ctr[1] = {qbase + q};
+        uint4 r[1];
+        ph(ctr, r);
+        const uint32_t byte = byte_of(v, r[0], q);
+        stage[q] = static_cast<uint8_t>(byte);
+        emit(q, byte);
+    }
+    __syncthreads();
+    if (a.nnz) count_nonzero(stage, 0, nbytes, a.nnz, 0);
+    return nbytes;
+}
+
 // Codes of one chunk (work item b) into `stage`; returns the number of staged
 // code bytes (passthrough chunks are copied to their destinations here and
 // return 0). kFuse (N == 1: the average is this worker's own decode, K3 folded
@@ -344,6 +539,7 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
         k2_passthrough<kFuse, kOpt>(a, L, ch, b);
         return 0;
     }
+    if (ch.nblk > 1) return k2_code_chunk_mb<U, kFuse, kOpt>(a, L, ch, stage);
     // L2 loads: in the fused K1+K2 kernel another CTA wrote them during this launch
     const float s = a.slots ? __ldcg(a.slots + L.slot) : a.s_imm;
     const float bound = a.bounds ? __ldcg(a.bounds + ch.layer) : INFINITY;
@@ -567,14 +763,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
 // the K2 units; a unit of tensor T first waits (acquire) for T's flag, so K2 of
 // early tensors overlaps K1 of later ones. Phase 1 never waits, so every flag a
 // phase-2 CTA waits for is set by a CTA that is already running: deadlock-free.
-// Global bucketing waits for the global flag (all tensors finalized).
+// Global bucketing waits for the global flag (all tensors finalized). The last
+// CTA to finish clears the flags (every other CTA is past its waits), so each
+// launch starts from zero flags: the kernel is safe to replay in a CUDA graph.
 __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t epoch, ErrWord* err) {
     if (threadIdx.x == 0) {
         uint32_t v;
         const long long t0 = clock64();
         for (uint32_t spin = 0;; ++spin) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-            if (v == epoch) break;
+            if (v != 0u) break;
             if (spin > 16) __nanosleep(64);
             if ((spin & 1023) == 1023 && clock64() - t0 > 20000000000ll) {  // ~10 s: a bug
                 raise_error(err, TGB_E_PEER_TIMEOUT, -1, ~0ull);
@@ -587,7 +785,8 @@ __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t epoch,
 
 template <bool kFuse, bool kOpt = false>
 __global__ void __launch_bounds__(kThreads, 4) k12_fused(TableSource src, K1Out o, K2Args a,
-                                                        uint32_t n_k1, uint32_t n_k2) {
+                                                        uint32_t n_k1, uint32_t n_k2,
+                                                        uint32_t n_flags) {
     __shared__ __align__(16) uint8_t stage[kStageBytes];
     __shared__ float4 lutv[kFuse ? 256 : 1];
     for (uint32_t u = blockIdx.x; u < n_k1; u += gridDim.x) {
@@ -611,6 +810,16 @@ __global__ void __launch_bounds__(kThreads, 4) k12_fused(TableSource src, K1Out 
             bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
         }
         __syncthreads();  // the bulk copy finished reading `stage` (thread 0 waited for it)
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(o.ready + n_flags, 1u) == gridDim.x - 1;  // exit counter
+    }
+    __syncthreads();
+    if (last) {
+        for (uint32_t i = threadIdx.x; i < n_flags; i += kThreads) o.ready[i] = 0u;
+        if (threadIdx.x == 0) o.ready[n_flags] = 0u;
     }
 }
 
@@ -877,6 +1086,18 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
             for (int w = 0; w < NW; ++w)
                 codes[w][i] = a.src[a.stride * w + L.code_off + (ch.begin >> 2) + i];
     }
+    // multi-bucket item: s = max over workers per bucket (bucket of byte q: q >> shq)
+    __shared__ float smax_b[kChunk3 / 64];
+    const bool mb = ch.nblk > 1;
+    const uint32_t shq = mb ? bucket_log2(L) - 2 : 31u;
+    if (mb)
+        for (uint32_t j = tid; j < ch.nblk; j += kThreads) {
+            float m = 0.0f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                m = fmaxf(m, __ldg(reinterpret_cast<const float*>(a.src + a.stride * w) + L.slot + j));
+            smax_b[j] = m;
+        }
     __syncthreads();
     OptDev od{};
     if (kOpt) od = a.optd[ch.layer];
@@ -886,10 +1107,11 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
     float s_max = 0.0f;
 #pragma unroll
     for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
-    auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
-        return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
-    };
     for (uint32_t q = tid; q < nbytes; q += kThreads) {
+        const float s_q = mb ? smax_b[q >> shq] : s_max;
+        auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
+            return __fmul_rn(__fmul_rn(s_q, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
+        };
         uint32_t acc = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
@@ -1110,15 +1332,27 @@ __global__ void __launch_bounds__(kThreads) k3_expand(TableSource src, ShardArgs
             x = q;
         }
     }
+    __shared__ float smax_b[kMaxItemBuckets];  // multi-bucket item: s per bucket
+    const bool mb = ch.nblk > 1;
+    const uint32_t shq = mb ? bucket_log2(L) - 2 : 31u;
+    if (mb)
+        for (uint32_t j = tid; j < ch.nblk; j += kThreads) {
+            float m = 0.0f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                m = fmaxf(m, __ldg(reinterpret_cast<const float*>(a.src + a.stride * w) + L.slot + j));
+            smax_b[j] = m;
+        }
     __syncthreads();
     float s_max = 0.0f;
 #pragma unroll
     for (int w = 0; w < NW; ++w) s_max = fmaxf(s_max, sw[w]);  // cluster.hpp:195-196
-    auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
-        return __fmul_rn(__fmul_rn(s_max, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
-    };
     const uint32_t nbytes = (count + 3) >> 2;
     for (uint32_t q = tid; q < nbytes; q += kThreads) {
+        const float s_q = mb ? smax_b[q >> shq] : s_max;
+        auto val = [&](uint32_t idx) {  // (s * float(sum)) * invN, sum = idx - NW (codec.hpp:296)
+            return __fmul_rn(__fmul_rn(s_q, small_int_float(static_cast<int>(idx) - NW)), a.inv_n);
+        };
         const uint32_t v = reinterpret_cast<const uint32_t*>(sums)[q];
         const float4 o = make_float4(val(v & 0xffu), val((v >> 8) & 0xffu), val((v >> 16) & 0xffu),
                                      val(v >> 24));
@@ -1175,6 +1409,7 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
     if (n_chunks == 0) return cudaSuccess;
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
             p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors, p.nnz};
+    o.bmax = p.bmax;
     const TableSource src{chunks};
     if (p.keep_chunks) {  // the launch's last units stay in L2 for K2's reverse walk
         o.keep_from = n_chunks - (p.keep_chunks < n_chunks ? p.keep_chunks : n_chunks);
@@ -1196,6 +1431,18 @@ cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t 
     l.first_chunk = 0;
     l.n_chunks = nc;
     k1_stats<SingleSource, 8, 1, 4><<<nc, kThreads, 0, st>>>(SingleSource{l, kChunk}, o);
+    return launch_status();
+}
+
+cudaError_t launch_k1_bucket_slots(const LayerDev* layers, const uint2* meta, uint32_t n_blocks,
+                                   const K1Launch& p, cudaStream_t st) {
+    if (n_blocks == 0) return cudaSuccess;
+    K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
+            p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors, nullptr};
+    o.bmax = p.bmax;
+    uint32_t grid = (n_blocks + kThreads - 1) / kThreads;
+    if (grid > 148u * 8) grid = 148u * 8;
+    k1_bucket_slots<<<grid, kThreads, 0, st>>>(meta, n_blocks, o);
     return launch_status();
 }
 
@@ -1276,24 +1523,25 @@ cudaError_t launch_k12_table(const LayerDev* layers, const ChunkFat* chunks, uin
             p1.push, p1.tensors, nullptr};
     o.ready = ready;
     o.ready_global = ready + p1.n_tensors;
-    o.epoch = epoch;
+    o.epoch = epoch ? epoch : 1u;
     K2Args a{p2.push, p2.slots, p2.bounds, p2.err, p2.t, 0, 0, 0.0f, 0, p2.dst};
     a.nnz = p2.nnz;
     a.shard_n = p2.shard_n;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p2.shard_bounds[r];
     const TableSource src{chunks};
     const uint32_t units = n_k1 > n_k2 ? n_k1 : n_k2;
+    const uint32_t nf = static_cast<uint32_t>(p1.n_tensors) + 1;  // ready[nf] = exit counter
     if (p2.fuse_decode && p2.optd) {
         a.optd = p2.optd;
         a.opt = p2.opt;
         k12_fused<true, true><<<k12_grid(k12_fused<true, true>, units), kThreads, 0, st>>>(
-            src, o, a, n_k1, n_k2);
+            src, o, a, n_k1, n_k2, nf);
     } else if (p2.fuse_decode) {
         k12_fused<true><<<k12_grid(k12_fused<true>, units), kThreads, 0, st>>>(src, o, a, n_k1,
-                                                                             n_k2);
+                                                                             n_k2, nf);
     } else {
         k12_fused<false><<<k12_grid(k12_fused<false>, units), kThreads, 0, st>>>(src, o, a, n_k1,
-                                                                               n_k2);
+                                                                               n_k2, nf);
     }
     return launch_status();
 }
@@ -1678,6 +1926,7 @@ cudaError_t preload_kernels() {
         reinterpret_cast<const void*>(k1_stats<TableSource, 8, 1, 4, true>),
         reinterpret_cast<const void*>(k1_stats<TableSource, 8, 1, 4>),
         reinterpret_cast<const void*>(k1_stats<SingleSource, 8, 1, 4>),
+        reinterpret_cast<const void*>(k1_bucket_slots),
         reinterpret_cast<const void*>(TGB_K2_PLAIN),
         reinterpret_cast<const void*>(TGB_K2_FUSED),
         reinterpret_cast<const void*>(TGB_K2_FUSED_OPT),

@@ -110,16 +110,61 @@ static tgb_status build_schedule(tgb_plan* P) {
         P->shard = P->exchange_opt == TGB_EXCHANGE_SHARDED ||
                    (P->exchange_opt == TGB_EXCHANGE_AUTO && N >= 5);
 
-    // ---- work items (chunks never straddle blocks)
+    // ---- FixedSize(k), k = 2^p in [64, chunk): work items of whole buckets (k/4 code
+    // bytes, a 16-B multiple, so a run of buckets is contiguous in the push area and
+    // the slots; shared scalers and N <= 8: the staged decode kernels)
+    P->mb_log2 = 0;
+    const uint64_t k = P->p.bucket_size;
+    if (P->p.bucketing == TGB_BUCKET_FIXED && k >= 64 && (k & (k - 1)) == 0 && k < chunk &&
+        P->p.scaler_sharing && N <= kMaxPeers) {
+        while ((1ull << P->mb_log2) < k) ++P->mb_log2;
+    }
+    for (LayerDev& L : P->h_layers) {
+        L.flags &= ~(kLayerMultiBucket | (31u << kBucketShiftBit));
+        const TensorDev& T = P->h_tensors[L.tensor];
+        if (P->mb_log2 && !(L.flags & kLayerPassthrough) && T.n_blocks > 1)
+            L.flags |= kLayerMultiBucket | (P->mb_log2 << kBucketShiftBit);
+    }
+
+    // ---- work items (chunks never straddle blocks; multi-bucket items span whole blocks)
     P->h_chunks.clear();
     P->h_chunks3.clear();
     const uint32_t nb = static_cast<uint32_t>(P->h_layers.size());
-    for (uint32_t b = 0; b < nb; ++b) {
-        const uint64_t n = P->h_layers[b].n;
+    for (uint32_t b = 0; b < nb;) {
+        const LayerDev& L = P->h_layers[b];
+        if (L.flags & kLayerMultiBucket) {  // the tensor's blocks, grouped
+            const TensorDev& T = P->h_tensors[L.tensor];
+            const uint32_t end = T.first_block + T.n_blocks;
+            for (int which = 0; which < 2; ++which) {
+                const uint32_t per = static_cast<uint32_t>((which == 0 ? chunk : kChunk3) >> P->mb_log2);
+                std::vector<ChunkDev>& out = which == 0 ? P->h_chunks : P->h_chunks3;
+                for (uint32_t f = b; f < end;) {
+                    if (per >= 2) {
+                        const uint32_t m = std::min(per, end - f);
+                        uint64_t cnt = 0;
+                        for (uint32_t x = f; x < f + m; ++x) cnt += P->h_layers[x].n;
+                        out.push_back({f, static_cast<uint32_t>(cnt), 0u, m});
+                        f += m;
+                    } else {  // buckets larger than a K3 item: chunks inside each block
+                        const uint64_t n = P->h_layers[f].n;
+                        for (uint64_t e = 0; e < n; e += kChunk3)
+                            out.push_back({f, static_cast<uint32_t>(std::min<uint64_t>(kChunk3, n - e)),
+                                           static_cast<uint32_t>(e), 1u});
+                        ++f;
+                    }
+                }
+            }
+            b = end;
+            continue;
+        }
+        const uint64_t n = L.n;
         for (uint64_t e = 0; e < n; e += chunk)
-            P->h_chunks.push_back({b, static_cast<uint32_t>(std::min<uint64_t>(chunk, n - e)), e});
+            P->h_chunks.push_back({b, static_cast<uint32_t>(std::min<uint64_t>(chunk, n - e)),
+                                   static_cast<uint32_t>(e), 1u});
         for (uint64_t e = 0; e < n; e += kChunk3)
-            P->h_chunks3.push_back({b, static_cast<uint32_t>(std::min<uint64_t>(kChunk3, n - e)), e});
+            P->h_chunks3.push_back({b, static_cast<uint32_t>(std::min<uint64_t>(kChunk3, n - e)),
+                                    static_cast<uint32_t>(e), 1u});
+        ++b;
     }
 
     // ---- two-group schedule: the dominant tensor vs the rest (PerTensor + REF
@@ -150,12 +195,13 @@ static tgb_status build_schedule(tgb_plan* P) {
     // last-to-first) re-reads them from L2 and demotes them (tools/l2keep_ab.py: step
     // -4.6 us; 16-32 MB is the plateau). At N > 1 the lines linger into K3 (+8 us).
     P->k1_keep = N == 1 ? static_cast<uint32_t>((24ull << 20) / (4ull * P->chunk12)) : 0u;
-    // small sets (< 8 Mi elements: the working set stays in L2 and the step is
-    // latency-bound): K1 + K2 in one persistent launch, K2 of a tensor starting as
-    // soon as its K1 finalized. PRESHARED needs the max-allreduce between them.
+    // K1 + K2 as one persistent launch (opt-in, TGB_SCHEDULE_FUSED12): K2 of a tensor
+    // starts as soon as its K1 finalized. Measured slower than K1 -> K2 with K2 as
+    // K1's programmatic dependent, also for small sets (CUDA-graph replay, device
+    // time: GoogLeNet 25.8 vs 24.0 us, a 1M layer 13.8 vs 12.3 us, VGG-16 305 vs
+    // 284 us; profiles/r02_small_sets.jsonl). PRESHARED needs the allreduce between.
     P->k12 = !P->grouped && P->p.share_mode == TGB_SHARE_REF &&
-             (P->total <= (8ull << 20) || P->schedule_opt == TGB_SCHEDULE_FUSED12) &&
-             P->schedule_opt != TGB_SCHEDULE_UNFUSED;
+             P->p.bucketing != TGB_BUCKET_FIXED && P->schedule_opt == TGB_SCHEDULE_FUSED12;
     if (P->k12) P->pdl = 0;
 
     auto group_of = [&](const ChunkDev& c) {
@@ -356,10 +402,22 @@ tgb_status tgb_plan_create(const tgb_layer_desc* layers, int32_t n_layers,
               cudaMalloc(&P->d_bounds, nbl * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&P->d_push, P->push_bytes) == cudaSuccess &&
               cudaMalloc(&P->d_err, sizeof(ErrWord)) == cudaSuccess &&
-              cudaMalloc(&P->d_ready, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
-              cudaMemset(P->d_ready, 0, (nl + 1) * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&P->d_ready, (nl + 2) * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMemset(P->d_ready, 0, (nl + 2) * sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&P->d_nnz, 2 * sizeof(unsigned long long)) == cudaSuccess &&
               cudaMemset(P->d_nnz, 0, 2 * sizeof(unsigned long long)) == cudaSuccess;
+    if (ok && params->bucketing == TGB_BUCKET_FIXED) {  // bucket maxima + block meta
+        std::vector<uint2> meta(nbl, make_uint2(0u, ~0u));
+        for (size_t b = 0; b < P->h_layers.size(); ++b) {
+            const LayerDev& L = P->h_layers[b];
+            meta[b] = make_uint2(L.tensor, L.slot < 0 ? ~0u : static_cast<uint32_t>(L.slot));
+        }
+        ok = cudaMalloc(&P->d_bmax, nbl * sizeof(uint32_t)) == cudaSuccess &&
+             cudaMemset(P->d_bmax, 0, nbl * sizeof(uint32_t)) == cudaSuccess &&
+             cudaMalloc(&P->d_bmeta, nbl * sizeof(uint2)) == cudaSuccess &&
+             cudaMemcpy(P->d_bmeta, meta.data(), nbl * sizeof(uint2), cudaMemcpyHostToDevice) ==
+                 cudaSuccess;
+    }
     if (ok && n_workers > 1) {  // NCCL allgather destination (freed when peers attach)
         ok = cudaMalloc(&P->d_nccl_gather, P->push_bytes * static_cast<uint64_t>(n_workers)) ==
              cudaSuccess;
@@ -408,6 +466,8 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaFree(P->d_pull);
     cudaFree(P->d_err);
     cudaFree(P->d_ready);
+    cudaFree(P->d_bmax);
+    cudaFree(P->d_bmeta);
     for (int g = 0; g < 2; ++g) {
         if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
         if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
@@ -592,8 +652,12 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     k.keep_chunks = P->k1_keep;
     k.tensors = P->d_tensors;
     k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
+    k.bmax = P->d_bmax;
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k1_table(P->d_layers, P->d_fat + b, P->ck1[g], k, st));
+    if (P->d_bmax)  // FixedSize: bucket scalers (FixedSize plans are never grouped)
+        TGB_CUDA(launch_k1_bucket_slots(P->d_layers, P->d_bmeta,
+                                        static_cast<uint32_t>(P->h_layers.size()), k, st));
     if (ts >= 0) {
         uint64_t e[2];
         chunk_elems(P, P->h_chunks, b, P->ck1[g], e);
@@ -677,7 +741,7 @@ static tgb_status launch_k12(tgb_plan* P, uint64_t t, cudaStream_t st, bool fuse
         TGB_CUDA(cudaMemsetAsync(P->d_nnz, 0, sizeof(unsigned long long), st));
         k2.nnz = P->d_nnz;
     }
-    if (++P->k12_epoch == 0) ++P->k12_epoch;  // 0 is the flags' initial value
+    if (++P->k12_epoch == 0) ++P->k12_epoch;  // any nonzero value marks a flag ready
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k12_table(P->d_layers, P->d_fat, P->ck1[0], P->cc[0], k1, k2, P->d_ready,
                               P->k12_epoch, st));
@@ -1131,6 +1195,7 @@ static PlanDesc make_desc(const tgb_plan* P) {
     d.shard = P->shard;
     d.grouped = P->grouped;
     d.radix_m = P->radix_m;
+    d.reserved = static_cast<int32_t>(P->mb_log2);
     uint64_t h = 0xcbf29ce484222325ull;
     for (size_t b = 0; b < P->h_layers.size(); ++b) {
         const LayerDev& L = P->h_layers[b];
@@ -1169,7 +1234,7 @@ static tgb_status compare_desc(const PlanDesc& a, const PlanDesc& b, int worker)
         return set_protocol_error("attach: codec configuration mismatch from worker " + w);
     if (a.push_bytes != b.push_bytes || a.sums_bytes != b.sums_bytes || a.ipc_bytes != b.ipc_bytes ||
         a.chunk12 != b.chunk12 || a.chunk3 != b.chunk3 || a.shard != b.shard ||
-        a.grouped != b.grouped || a.radix_m != b.radix_m)
+        a.grouped != b.grouped || a.radix_m != b.radix_m || a.reserved != b.reserved)
         return set_protocol_error("attach: exchange schedule mismatch from worker " + w);
     return TGB_OK;
 }

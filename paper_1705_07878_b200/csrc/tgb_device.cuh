@@ -30,6 +30,11 @@ constexpr uint32_t kLayerClip = 2u;     // clip this layer (clipping on, not pas
 constexpr uint32_t kLayerVecIn = 4u;    // gradient pointer is 16-byte aligned
 constexpr uint32_t kLayerVecOut = 8u;   // output pointer is 16-byte aligned
 constexpr uint32_t kLayerShiftBit = 16; // bits 16-17: block start within the tensor & 3
+// FixedSize(k) with k a power of two in [64, chunk): work items span whole
+// buckets (nblk consecutive blocks of one tensor, contiguous in the tensor, in
+// the push area -- k/4 code bytes, a 16-B multiple -- and in the scaler slots)
+constexpr uint32_t kLayerMultiBucket = 32u;
+constexpr uint32_t kBucketShiftBit = 24;  // bits 24-28: log2(k) of a multi-bucket tensor
 
 // A block: one bucket of one tensor (PerTensor/Global: the whole tensor;
 // FixedSize(k): [off, off+k) of it, codec.hpp:224-232) or a passthrough tensor.
@@ -48,9 +53,10 @@ struct LayerDev {
 };
 
 struct ChunkDev {
-    uint32_t layer;  // block index
+    uint32_t layer;  // block index (multi-bucket items: the first of nblk blocks)
     uint32_t count;  // elements in this chunk
-    uint64_t begin;  // first element, relative to the block (multiple of 16)
+    uint32_t begin;  // first element, relative to the block (multiple of 16; 0 multi-bucket)
+    uint32_t nblk;   // blocks (buckets) the item spans: 1, or > 1 for multi-bucket items
 };
 
 // self-contained work item of the grid-per-chunk kernels: the chunk plus a

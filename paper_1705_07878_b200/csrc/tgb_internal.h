@@ -54,6 +54,7 @@ struct K1Launch {
     unsigned long long* nnz = nullptr;   // telemetry counter to reset (this group)
     uint32_t keep_chunks = 0;            // last units kept in L2 (evict_last) for K2 (N == 1)
     int32_t n_tensors = 0;               // fused K1+K2: ready[n_tensors] is the Global flag
+    uint32_t* bmax = nullptr;            // FixedSize: per-block max |x| (then k1_bucket_slots)
 };
 
 struct K2Launch {
@@ -112,6 +113,10 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
 cudaError_t launch_k12_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_k1,
                              uint32_t n_k2, const K1Launch& p1, const K2Launch& p2,
                              uint32_t* ready, uint32_t epoch, cudaStream_t st);
+// FixedSize plans, after K1: bucket scalers from the per-block maxima (meta[b] =
+// {tensor, slot}, slot ~0u for passthrough blocks)
+cudaError_t launch_k1_bucket_slots(const LayerDev* layers, const uint2* meta, uint32_t n_blocks,
+                                   const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k1_single(const LayerDev& L, const K1Launch& p, cudaStream_t st);
 cudaError_t launch_k2_single(const LayerDev& L, const K2Launch& p, cudaStream_t st);
 cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint32_t n_chunks,

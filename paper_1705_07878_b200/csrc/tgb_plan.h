@@ -79,8 +79,13 @@ struct tgb_plan {
     uint32_t k1_keep = 0;      // K1 units per launch loaded L2 evict_last (N = 1)
     // small sets: K1 + K2 as one persistent launch (k12_fused), per-tensor epoch flags
     bool k12 = false;
-    uint32_t* d_ready = nullptr;  // n_layers + 1 flags (the last: Global bucketing)
+    uint32_t* d_ready = nullptr;  // n_layers + 1 flags (the last: Global) + exit counter
     uint32_t k12_epoch = 0;
+    // FixedSize: per-block max |x| (K1 -> k1_bucket_slots), block meta {tensor, slot};
+    // mb_log2 > 0: buckets of 2^mb_log2 elements grouped into multi-bucket work items
+    uint32_t* d_bmax = nullptr;
+    uint2* d_bmeta = nullptr;
+    uint32_t mb_log2 = 0;
     cudaStream_t gs[2] = {nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 

@@ -34,6 +34,9 @@ struct K1Out {
     uint32_t* ready = nullptr;
     uint32_t* ready_global = nullptr;
     uint32_t epoch = 0;
+    // FixedSize plans: per-block max |x| (float bits, atomicMax), turned into the
+    // bucket scalers by k1_bucket_slots; the tensor finalize then writes only the bound
+    uint32_t* bmax = nullptr;
 };
 
 __device__ __forceinline__ void publish_ready(uint32_t* flag, uint32_t epoch) {
@@ -76,10 +79,12 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
                                                      uint32_t layer, uint32_t unit,
                                                      uint32_t first_unit, uint32_t n_units,
                                                      uint64_t count, double x0, double S, double Q,
-                                                     float mx) {
+                                                     float mx, bool bucket_max = true) {
     block_reduce_sq<kThreads / 32, Bar>(S, Q, mx);
     const uint32_t tid = threadIdx.x;
     __shared__ bool is_last;
+    if (tid == 0 && o.bmax && bucket_max)  // FixedSize: a chunk of one bucket
+        atomicMax(o.bmax + layer, __float_as_uint(mx));
     if (tid == 0) {
         const double cn = static_cast<double>(count);
         Partial p;
@@ -175,7 +180,9 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
         o.layer_done[L.tensor] = 0u;  // self-reset for the next launch
     }
     Bar::sync();
-    if (o.tensors) {
+    if (o.tensors && o.bmax) {  // FixedSize: the bucket scalers follow in k1_bucket_slots
+        if (tid == 0) o.bounds[o.tensors[L.tensor].first_block] = s_bound;
+    } else if (o.tensors) {
         // per block: s = max |clip(part)| = min(max |part|, bound) (codec.hpp:121-122, :229-230)
         const TensorDev T = o.tensors[L.tensor];
         if (T.n_blocks == 1) {  // PerTensor / Global: the tree's max is the block's

@@ -334,7 +334,7 @@ def test_plan_layout_matches_host_restatement(bucketing, k, pt):
 
 
 # ------------------------------------------- FixedSize / passthrough at size
-@pytest.mark.parametrize("k", [300, 1000, 4097, (1 << 20) + 3, 3 << 20])
+@pytest.mark.parametrize("k", [64, 256, 300, 1000, 4096, 4097, (1 << 20) + 3, 3 << 20])
 def test_fixed_size_large_vs_oracle(restated, k):
     names = ["fc.weight", "fc.bias", "conv.weight"]
     grads = [restated.normal(21, 0, "fx/" + n, m, 1e-3) for n, m in
@@ -547,7 +547,8 @@ def test_live_kernel_timing_records():
     """tgb_plan_enable_timing: one record per launch with its algorithmic bytes
     (N = 1 step = K1 + K2 with the fused decode)."""
     names, ns = ["a.w", "b.w"], [1000, 40003]
-    sw = tg.SyncWorker(names, [[n] for n in ns], tg.CodecConfig(seed=42), device=DEV)
+    sw = tg.SyncWorker(names, [[n] for n in ns], tg.CodecConfig(seed=42), device=DEV,
+                       schedule="unfused")
     sw.grad_flat.normal_(0.0, 1e-3)
     sw.step(0)
     sw.plan.enable_timing(16)
@@ -565,4 +566,57 @@ def test_live_kernel_timing_records():
     assert k2 == 3 * (4 * n + 4 * n + (1000 + 3) // 4 + (40003 + 3) // 4) or \
         k2 == 3 * (4 * n + 4 * n + (n + 3) // 4)
     assert all(r["ms"] > 0 and r["start_ms"] >= 0 for r in recs)
+    sw.plan.close()
+
+
+def test_fused_k12_matches_separate_launches():
+    """K1 + K2 as one persistent launch (k12_fused, opt-in schedule); its output,
+    codes and scalers equal the two-launch schedule's, every bucketing mode,
+    including replays of the same iteration (the ready flags reset per launch)"""
+    names = ["conv.weight", "conv.bias", "empty", "fc.weight", "fc.bias", "p"]
+    ns = [1728, 64, 0, 40003, 10, 77]
+    for cfg in (tg.CodecConfig(seed=42, passthrough={"p"}),
+                tg.CodecConfig(seed=42, bucketing=tg.Bucketing.Global),
+                tg.CodecConfig(seed=42, bucketing=tg.Bucketing.FixedSize, bucket_size=300)):
+        outs = {}
+        for sched in ("fused12", "unfused"):
+            sw = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV, schedule=sched)
+            sw.grad_flat.normal_(0.0, 1e-3, generator=torch.Generator(device=DEV).manual_seed(5))
+            sw.plan.enable_timing(8)
+            for t in (3, 3, 4):
+                sw.step(t, check=True)
+            kinds = {r["kernel"] for r in sw.plan.read_timing()}
+            sw.plan.enable_timing(0)
+            fixed = cfg.bucketing == tg.Bucketing.FixedSize  # (never fused: bucket slots)
+            assert ("K12_fused" in kinds) == (sched == "fused12" and not fixed), kinds
+            outs[sched] = (sw.out_flat.clone(), sw.plan.scalers().clone(),
+                           torch.cat([sw.plan.block_region(b).view(torch.uint8).clone()
+                                      for b in range(len(sw.plan.blocks))]))
+            sw.plan.close()
+        for a, b in zip(outs["fused12"], outs["unfused"]):
+            assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("k", [64, 256, 4096])
+def test_fixed_size_multibucket_step_vs_oracle(restated, k):
+    """FixedSize(k), k = 2^p: work items of whole buckets (K1 per-bucket maxima,
+    k1_bucket_slots, per-bucket decision constants in K2, the N = 1 fused decode)
+    == the oracle's encode_step + decode per bucket, incl. ragged last buckets"""
+    names = ["fc.weight", "fc.bias", "conv.weight"]
+    ns = [(1 << 20) + 67, 1001, 300003]
+    grads = [restated.normal(23, 0, "mb/" + n, m, 1e-3) for n, m in zip(names, ns)]
+    cfg = tg.CodecConfig(seed=42, bucketing=tg.Bucketing.FixedSize, bucket_size=k)
+    sw = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    for v, g in zip(sw.grads, grads):
+        v.copy_(to_dev(g))
+    for t in (4, 5):
+        sw.step(t, check=True)
+    st, blocks, sc, _, _ = restated.encode_step(names, grads, Config(seed=42, bucketing=2,
+                                                                     bucket_size=k), 5, 0)
+    assert st == 0
+    assert sw.plan.scalers().cpu().numpy().tobytes() == np.asarray(sc, np.float32).tobytes()
+    want = np.concatenate([restated.decode(b, n_b, float(s))[1] for b, s, n_b in
+                           zip(blocks, sc, [bi.n for bi in sw.plan.blocks])])
+    got = np.concatenate([o.cpu().numpy() for o in sw.outs])
+    assert got.view(np.uint32).tobytes() == want.view(np.uint32).tobytes()
     sw.plan.close()

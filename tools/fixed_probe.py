@@ -39,7 +39,8 @@ def probe(names, shapes, cfg, dev, K=20):
 
 def main():
     dev = torch.device("cuda", 0)
-    ks = [int(x) for x in (sys.argv[1:] or ["256", "1024", "4096", "16384", "65536"])]
+    ks = [int(x) for x in (sys.argv[1:] or ["64", "256", "1000", "1024", "4096", "16384", "65536",
+                                            str(1 << 20), str(1 << 24), "102760447"])]
     g = tg.layersets.get("vgg16")
     names, shapes = [a for a, _ in g], [s for _, s in g]
     res = {"per_tensor": probe(names, shapes, tg.CodecConfig(seed=42), dev)}

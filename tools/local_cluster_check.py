@@ -38,7 +38,8 @@ def small_checks(N, report):
     ref = Reference()
     P, G, F = tg.Bucketing.PerTensor, tg.Bucketing.Global, tg.Bucketing.FixedSize
     configs = [(True, P, 0, ()), (False, P, 0, ()), (True, G, 0, ()),
-               (True, F, 1000, ("conv1.bias",)), (False, F, 7, ("fc.bias",))]
+               (True, F, 1000, ("conv1.bias",)), (False, F, 7, ("fc.bias",)),
+               (True, F, 256, ("conv1.bias",)), (True, F, 64, ())]
     grads = [[R.normal(100 + w, 0, "mp/" + n, m, 1e-2) for n, m in zip(NAMES, SIZES)]
              for w in range(N)]
     for exchange in ("fused", "sharded"):
