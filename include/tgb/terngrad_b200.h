@@ -160,10 +160,13 @@ tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_in
  *   pointers).
  * TGB_PLAN_OPT_EXCHANGE: TGB_EXCHANGE_AUTO / _FUSED / _SHARDED; before attaching peers.
  * TGB_PLAN_OPT_FUSED_OPTIMIZER: 1 (default) the decode kernel applies the optimizer in
- *   tgb_step_apply; 0 the averaged gradient is written and a separate kernel applies it. */
+ *   tgb_step_apply; 0 the averaged gradient is written and a separate kernel applies it.
+ * TGB_PLAN_OPT_PIECES: sharded exchange, pieces of the K2 work list (0 = auto, 1..8): the
+ *   owner reduce + decode of piece p run while K2 computes piece p+1; before attaching. */
 #define TGB_PLAN_OPT_SCHEDULE 0
 #define TGB_PLAN_OPT_EXCHANGE 1
 #define TGB_PLAN_OPT_FUSED_OPTIMIZER 2
+#define TGB_PLAN_OPT_PIECES 3
 #define TGB_SCHEDULE_AUTO 0
 #define TGB_SCHEDULE_SINGLE 1
 #define TGB_SCHEDULE_GROUPS 2

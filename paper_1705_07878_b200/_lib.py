@@ -37,6 +37,7 @@ TGB_EXCHANGE_AUTO = -1
 TGB_EXCHANGE_NONE, TGB_EXCHANGE_NCCL, TGB_EXCHANGE_FUSED, TGB_EXCHANGE_SHARDED = 0, 1, 2, 3
 EXCHANGE_NAMES = ["none", "nccl", "fused", "sharded"]
 TGB_PLAN_OPT_SCHEDULE, TGB_PLAN_OPT_EXCHANGE, TGB_PLAN_OPT_FUSED_OPTIMIZER = 0, 1, 2
+TGB_PLAN_OPT_PIECES = 3
 TGB_SCHEDULE_AUTO, TGB_SCHEDULE_SINGLE, TGB_SCHEDULE_GROUPS = 0, 1, 2
 TGB_SCHEDULE_UNFUSED, TGB_SCHEDULE_FUSED12 = 3, 4
 

@@ -532,7 +532,9 @@ tgb_status tgb_plan_traffic(const tgb_plan* P, tgb_traffic* out) {
         const uint64_t sums = pass ? 4ull * ch.count
                                    : (ch.count + P->radix_m - 1) / P->radix_m * 4ull;
         all_sums += sums;
-        if (c >= P->cs[r] && c < P->cs[r + 1]) {
+        bool owned = false;
+        for (int q = 0; q < P->n_pieces; ++q) owned |= c >= P->pcs[q][r] && c < P->pcs[q][r + 1];
+        if (owned) {
             own_codes += codes;
             own_sums += sums;
         }

@@ -248,7 +248,9 @@ static tgb_status build_schedule(tgb_plan* P) {
     P->radix_m = 0;
     P->sum_region = 0;
     P->sums_bytes = 0;
-    for (int r = 0; r <= kMaxPeers; ++r) P->cs[r] = 0;
+    P->n_pieces = 1;
+    std::memset(P->pb, 0, sizeof(P->pb));
+    std::memset(P->pcs, 0, sizeof(P->pcs));
     if (P->shard) {
         P->radix_m = radix_digits_u32(2ull * N + 1);
         const uint64_t m = static_cast<uint64_t>(P->radix_m);
@@ -266,18 +268,39 @@ static tgb_status build_schedule(tgb_plan* P) {
             so += round_up(bytes, kAlignCodes);
         }
         P->sums_bytes = round_up(std::max<uint64_t>(so, 1), kAlignPush);
-        // owners: contiguous K2-chunk ranges balanced by K3a bytes (raw fp32 = 16x codes)
+        // pieces: contiguous runs of the K2 chunk list, balanced by K3a bytes (raw fp32 =
+        // 16x codes); auto = one piece per 32 Mi elements, at most 4 (VGG-16: 4, AlexNet:
+        // 2, GoogLeNet: 1 -- a small set is latency-bound, extra barriers only cost)
         std::vector<uint64_t> cum(P->h_chunks.size() + 1, 0);
         for (size_t c = 0; c < P->h_chunks.size(); ++c)
             cum[c + 1] = cum[c] + P->h_chunks[c].count * (is_pass(P->h_chunks[c]) ? 16ull : 1ull);
         const uint64_t W = cum.back();
-        for (int r = 0; r <= N; ++r) {
-            const uint64_t target = W * static_cast<uint64_t>(r) / static_cast<uint64_t>(N);
-            P->cs[r] = static_cast<uint32_t>(std::lower_bound(cum.begin(), cum.end(), target) -
-                                             cum.begin());
+        int np = P->pieces_opt > 0 ? P->pieces_opt
+                                   : static_cast<int>(std::min<uint64_t>(4, P->total >> 25));
+        np = std::max(1, std::min(np, std::min(kMaxPieces, static_cast<int>(P->h_chunks.size()))));
+        P->n_pieces = np;
+        auto cut = [&](uint64_t target) {
+            return static_cast<uint32_t>(std::lower_bound(cum.begin(), cum.end(), target) -
+                                         cum.begin());
+        };
+        for (int q = 0; q <= np; ++q) P->pb[q] = cut(W * static_cast<uint64_t>(q) / np);
+        P->pb[np] = static_cast<uint32_t>(P->h_chunks.size());
+        // owners inside each piece: rank r owns [pcs[q][r], pcs[q][r+1])
+        for (int q = 0; q < np; ++q) {
+            const uint64_t w0 = cum[P->pb[q]], w1 = cum[P->pb[q + 1]];
+            for (int r = 0; r <= N; ++r)
+                P->pcs[q][r] = std::max(P->pb[q], cut(w0 + (w1 - w0) * static_cast<uint64_t>(r) / N));
+            P->pcs[q][N] = P->pb[q + 1];
+            for (int r = N + 1; r <= kMaxPeers; ++r) P->pcs[q][r] = P->pb[q + 1];
         }
-        P->cs[N] = static_cast<uint32_t>(P->h_chunks.size());
-        for (int r = N + 1; r <= kMaxPeers; ++r) P->cs[r] = P->cs[N];
+        if (!P->gs3) {
+            int lo = 0, hi = 0;
+            TGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            TGB_CUDA(cudaStreamCreateWithPriority(&P->gs3, cudaStreamNonBlocking, hi));
+            TGB_CUDA(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
+            for (int q = 0; q < kMaxPieces; ++q)
+                TGB_CUDA(cudaEventCreateWithFlags(&P->ev_piece[q], cudaEventDisableTiming));
+        }
     }
 
     if (P->grouped && !P->gs[0]) {
@@ -473,6 +496,10 @@ void tgb_plan_destroy(tgb_plan* P) {
         if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
     }
     if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+    if (P->gs3) cudaStreamDestroy(P->gs3);
+    if (P->ev_done) cudaEventDestroy(P->ev_done);
+    for (cudaEvent_t e : P->ev_piece)
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : P->ev_local)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : P->t_ev) cudaEventDestroy(e);
@@ -549,6 +576,11 @@ tgb_status tgb_plan_set_option(tgb_plan* P, int32_t option, int64_t value) {
                 (!P->p.scaler_sharing || P->n_workers < 2 || P->n_workers > kMaxPeers))
                 return TGB_ERR_UNSUPPORTED;  // the owner sums integer codes (shared scalers)
             P->exchange_opt = static_cast<int32_t>(value);
+            break;
+        case TGB_PLAN_OPT_PIECES:
+            if (value < 0 || value > kMaxPieces) return TGB_ERR_INVALID_ARGUMENT;
+            if (P->attached) return TGB_ERR_UNSUPPORTED;
+            P->pieces_opt = static_cast<int32_t>(value);
             break;
         case TGB_PLAN_OPT_FUSED_OPTIMIZER:
             if (value != 0 && value != 1) return TGB_ERR_INVALID_ARGUMENT;
@@ -666,9 +698,10 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     return TGB_OK;
 }
 
-static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
-                              bool fuse_decode = false) {
-    const uint32_t cb = P->cb[g], cc = P->cc[g];
+// K2 over chunks [cb, cb + cc); piece: the sharded piece these chunks are (owner
+// bounds relative to cb), or -1 for a whole group
+static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc, int piece,
+                                    uint64_t t, cudaStream_t st, bool fuse_decode) {
     uint8_t* own = own_push(P);
     K2Launch k{own, reinterpret_cast<const float*>(own), P->d_bounds, P->d_err, t, 1};
     k.fuse_decode = fuse_decode ? 1 : 0;
@@ -685,7 +718,7 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
         k.dst.remote = 1;
         if (P->shard) {
             k.shard_n = P->n_workers;
-            for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->cs[r];
+            for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->pcs[piece][r] - cb;
         }
     }
     const int ts = t_begin(P, st);
@@ -708,6 +741,17 @@ static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
     return TGB_OK;
 }
 
+// K2 of group g (the sharded exchange: one launch per piece)
+static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
+                              bool fuse_decode = false) {
+    if (P->attached && P->shard) {
+        for (int q = 0; q < P->n_pieces; ++q)
+            TGB_TRY(launch_tern_range(P, 0, P->pb[q], P->pb[q + 1] - P->pb[q], q, t, st, false));
+        return TGB_OK;
+    }
+    return launch_tern_range(P, g, P->cb[g], P->cc[g], -1, t, st, fuse_decode);
+}
+
 // fused K1 + K2 over the whole (ungrouped) plan: one persistent launch
 static tgb_status launch_k12(tgb_plan* P, uint64_t t, cudaStream_t st, bool fuse_decode) {
     uint8_t* own = own_push(P);
@@ -725,9 +769,10 @@ static tgb_status launch_k12(tgb_plan* P, uint64_t t, cudaStream_t st, bool fuse
         k1.push.remote = 1;
         k2.dst.n = P->n_workers;
         k2.dst.remote = 1;
-        if (P->shard) {
+        if (P->shard) {  // (the fused K1+K2 launch covers the whole list: one piece)
+            if (P->n_pieces != 1) return TGB_ERR_UNSUPPORTED;
             k2.shard_n = P->n_workers;
-            for (int r = 0; r <= kMaxPeers; ++r) k2.shard_bounds[r] = P->cs[r];
+            for (int r = 0; r <= kMaxPeers; ++r) k2.shard_bounds[r] = P->pcs[0][r];
         }
     }
     k1.tensors = P->d_tensors;
@@ -837,14 +882,16 @@ static uint64_t radix_bytes(const tgb_plan* P, uint64_t elems) {
     return P->radix_m ? (elems + P->radix_m - 1) / P->radix_m * 4 : 0;
 }
 
-// sharded K3a over this rank's owned chunks: N workers' codes -> packed sums to every rank
-static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
+// sharded K3a over this rank's owned chunks of piece q: N workers' codes -> packed
+// sums to every rank
+static tgb_status launch_shard_reduce(tgb_plan* P, int q, cudaStream_t st) {
     const uint32_t r = static_cast<uint32_t>(P->rank);
+    const uint32_t c0 = P->pcs[q][r], c1 = P->pcs[q][r + 1];
     const int ts = t_begin(P, st);
-    TGB_CUDA(launch_k3_reduce(P->d_fat + P->cs[r], P->cs[r + 1] - P->cs[r], shard_launch(P), st));
+    TGB_CUDA(launch_k3_reduce(P->d_fat + c0, c1 - c0, shard_launch(P), st));
     if (ts >= 0) {
         uint64_t e[2];
-        chunk_elems(P, P->h_chunks, P->cs[r], P->cs[r + 1] - P->cs[r], e);
+        chunk_elems(P, P->h_chunks, c0, c1 - c0, e);
         const uint64_t N = P->n_workers;
         const uint64_t out = radix_bytes(P, e[0]) + 4 * e[1];
         t_end(P, st, ts, TGB_KERNEL_K3A, 0, e[0] + e[1], N * ((e[0] + 3) / 4 + 4 * e[1]) + out,
@@ -853,14 +900,14 @@ static tgb_status launch_shard_reduce(tgb_plan* P, cudaStream_t st) {
     return TGB_OK;
 }
 
-// sharded K3b: every rank decodes all packed sums (K2's chunk table)
-static tgb_status launch_shard_expand(tgb_plan* P, cudaStream_t st) {
-    const uint32_t n = static_cast<uint32_t>(P->h_chunks.size());
+// sharded K3b: every rank decodes the packed sums of piece q (K2's chunk table)
+static tgb_status launch_shard_expand(tgb_plan* P, int q, cudaStream_t st) {
+    const uint32_t c0 = P->pb[q], n = P->pb[q + 1] - P->pb[q];
     const int ts = t_begin(P, st);
-    TGB_CUDA(launch_k3_expand(P->d_fat, n, shard_launch(P), st));
+    TGB_CUDA(launch_k3_expand(P->d_fat + c0, n, shard_launch(P), st));
     if (ts >= 0) {
         uint64_t e[2];
-        chunk_elems(P, P->h_chunks, 0, n, e);
+        chunk_elems(P, P->h_chunks, c0, n, e);
         t_end(P, st, ts, TGB_KERNEL_K3B, 0, e[0] + e[1],
               radix_bytes(P, e[0]) + 4 * e[1] + 4 * (e[0] + e[1]), 0);
     }
@@ -916,10 +963,13 @@ tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
     P->last = st;
     if (P->attached) {  // data already moved by K1/K2: only order the step
         if (P->shard) {
-            // [codes landed at their owner] barrier 0 -> K3a -> [sums everywhere] barrier 1
-            TGB_TRY(launch_barrier(P, 0, st, kBarrierSpin));
-            TGB_TRY(launch_shard_reduce(P, st));
-            return launch_barrier(P, 1, st, kBarrierSpin);
+            // per piece: [codes landed at their owner] barrier -> K3a -> [sums everywhere] barrier
+            for (int q = 0; q < P->n_pieces; ++q) {
+                TGB_TRY(launch_barrier(P, 2 * q, st, kBarrierSpin));
+                TGB_TRY(launch_shard_reduce(P, q, st));
+                TGB_TRY(launch_barrier(P, 2 * q + 1, st, kBarrierSpin));
+            }
+            return TGB_OK;
         }
         for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_barrier(P, g, st, kBarrierSpin));
         return TGB_OK;
@@ -940,7 +990,8 @@ tgb_status tgb_decode_average(tgb_plan* P, const uint8_t* d_src, int32_t n_worke
     P->last = st;
     if (!d_src && P->attached && P->shard) {  // sharded exchange: decode this step's sums
         if (n_workers != P->n_workers) return TGB_ERR_INVALID_ARGUMENT;
-        return launch_shard_expand(P, st);
+        for (int q = 0; q < P->n_pieces; ++q) TGB_TRY(launch_shard_expand(P, q, st));
+        return TGB_OK;
     }
     if (!d_src) d_src = cur_gathered(P);  // NULL: this step's gather buffer
     for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_decode(P, g, d_src, n_workers, st));
@@ -968,6 +1019,24 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
         return TGB_OK;
     }
     const bool nccl_exchange = !P->attached;
+    if (P->attached && P->shard && P->p.share_mode == TGB_SHARE_REF && !P->k12) {
+        // pipelined sharded exchange: K2 piece by piece on `stream`; on gs3, piece q's
+        // barrier -> K3a -> barrier -> K3b overlap K2 of the pieces after it
+        ++P->epoch;
+        TGB_TRY(launch_stats(P, 0, st));
+        for (int q = 0; q < P->n_pieces; ++q) {
+            TGB_TRY(launch_tern_range(P, 0, P->pb[q], P->pb[q + 1] - P->pb[q], q, t, st, false));
+            TGB_CUDA(cudaEventRecord(P->ev_piece[q], st));
+            TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_piece[q], 0));
+            TGB_TRY(launch_barrier(P, 2 * q, P->gs3, kBarrierSpin));
+            TGB_TRY(launch_shard_reduce(P, q, P->gs3));
+            TGB_TRY(launch_barrier(P, 2 * q + 1, P->gs3, kBarrierSpin));
+            TGB_TRY(launch_shard_expand(P, q, P->gs3));
+        }
+        TGB_CUDA(cudaEventRecord(P->ev_done, P->gs3));
+        TGB_CUDA(cudaStreamWaitEvent(st, P->ev_done, 0));
+        return TGB_OK;
+    }
     if (!P->grouped || nccl_exchange) {
         if (P->p.share_mode == TGB_SHARE_PRESHARED) {
             TGB_TRY(tgb_stats(P, stream));
@@ -1035,8 +1104,10 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
             tgb_plan* P = plans[w];
             cudaStream_t st = st_of(w);
             if (!on(w)) return fail(TGB_ERR_CUDA);
-            tgb_status s = launch_encode(P, t[w], st, false);
-            if (s == TGB_OK) s = launch_barrier(P, 0, st, kBarrierPost);
+            tgb_status s = P->k12 ? launch_encode(P, t[w], st, false) : launch_stats(P, 0, st);
+            if (s == TGB_OK && !P->k12) s = launch_tern(P, 0, t[w], st);
+            for (int q = 0; q < P->n_pieces && s == TGB_OK; ++q)
+                s = launch_barrier(P, 2 * q, st, kBarrierPost);
             if (s != TGB_OK) return fail(s);
             if (cudaEventRecord(P->ev_local[0], st) != cudaSuccess) return fail(TGB_ERR_CUDA);
         }
@@ -1048,15 +1119,18 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
                 for (int q = 0; q < n; ++q)
                     if (cudaStreamWaitEvent(st, plans[q]->ev_local[phase], 0) != cudaSuccess)
                         return fail(TGB_ERR_CUDA);
-                tgb_status s = launch_barrier(P, phase, st, kBarrierCheck);
-                if (s == TGB_OK && phase == 0) {
-                    s = launch_shard_reduce(P, st);
-                    if (s == TGB_OK) s = launch_barrier(P, 1, st, kBarrierPost);
-                    if (s == TGB_OK && cudaEventRecord(P->ev_local[1], st) != cudaSuccess)
-                        s = TGB_ERR_CUDA;
-                } else if (s == TGB_OK) {
-                    s = launch_shard_expand(P, st);
+                tgb_status s = TGB_OK;
+                for (int q = 0; q < P->n_pieces && s == TGB_OK; ++q) {
+                    s = launch_barrier(P, 2 * q + phase, st, kBarrierCheck);
+                    if (s == TGB_OK && phase == 0) {
+                        s = launch_shard_reduce(P, q, st);
+                        if (s == TGB_OK) s = launch_barrier(P, 2 * q + 1, st, kBarrierPost);
+                    } else if (s == TGB_OK) {
+                        s = launch_shard_expand(P, q, st);
+                    }
                 }
+                if (s == TGB_OK && phase == 0 && cudaEventRecord(P->ev_local[1], st) != cudaSuccess)
+                    s = TGB_ERR_CUDA;
                 if (s != TGB_OK) return fail(s);
             }
         }
@@ -1195,7 +1269,7 @@ static PlanDesc make_desc(const tgb_plan* P) {
     d.shard = P->shard;
     d.grouped = P->grouped;
     d.radix_m = P->radix_m;
-    d.reserved = static_cast<int32_t>(P->mb_log2);
+    d.reserved = static_cast<int32_t>(P->mb_log2) | (P->n_pieces << 8);
     uint64_t h = 0xcbf29ce484222325ull;
     for (size_t b = 0; b < P->h_layers.size(); ++b) {
         const LayerDev& L = P->h_layers[b];

@@ -16,8 +16,9 @@ struct tgb_comm {
     int nranks = 0, rank = 0;
 };
 
-constexpr int kFlagSlots = 2;  // barrier slots per step: two layer groups, or the sharded
-                               // exchange's two barriers
+constexpr int kMaxPieces = 8;  // sharded exchange: pieces of the K2 chunk list
+constexpr int kFlagSlots = 2 * kMaxPieces;  // barrier slots per step: two layer groups (fused),
+                                            // or two barriers per piece (sharded)
 constexpr uint64_t kAlignCodes = 16;  // per-block region alignment (bytes)
 constexpr uint64_t kAlignPush = 256;  // push buffer / region base alignment
 
@@ -97,7 +98,15 @@ struct tgb_plan {
     int32_t radix_m = 0;      // sharded: base-(2N+1) digits per u32 sums word
     uint32_t sum_region = 0;  // sharded: bytes of a full chunk's sums region
     uint64_t sums_bytes = 0, sums_off = 0, flags_off = 0, ipc_bytes = 0;
-    uint32_t cs[kMaxPeers + 1] = {};  // sharded: rank r owns K2 chunks [cs[r], cs[r+1])
+    // sharded: the K2 chunk list in n_pieces contiguous pieces [pb[p], pb[p+1]); rank r
+    // owns chunks [pcs[p][r], pcs[p][r+1]) of piece p. Piece p's barrier -> K3a ->
+    // barrier -> K3b run on a second stream while K2 computes piece p+1.
+    int32_t pieces_opt = 0;  // TGB_PLAN_OPT_PIECES (0: auto)
+    int32_t n_pieces = 1;
+    uint32_t pb[kMaxPieces + 1] = {};
+    uint32_t pcs[kMaxPieces][kMaxPeers + 1] = {};
+    cudaStream_t gs3 = nullptr;
+    cudaEvent_t ev_piece[kMaxPieces] = {}, ev_done = nullptr;
     uint8_t* d_gathered = nullptr;    // NCCL gather buffer, or parity-0 gather inside d_ipc
     uint8_t* d_nccl_gather = nullptr;
     uint8_t* d_ipc = nullptr;

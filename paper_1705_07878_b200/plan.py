@@ -166,6 +166,10 @@ class Plan:
                                                      "fused": _lib.TGB_EXCHANGE_FUSED,
                                                      "sharded": _lib.TGB_EXCHANGE_SHARDED}[exchange])
 
+    def set_pieces(self, pieces: int):
+        """sharded exchange: pieces of the K2 work list (0 = auto); before attaching"""
+        self.set_option(_lib.TGB_PLAN_OPT_PIECES, int(pieces))
+
     def _refresh(self):
         L = load()
         info = _lib.PlanInfo()
@@ -440,7 +444,7 @@ class SyncWorker:
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
                  rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None,
-                 exchange: str = "auto", schedule: str = "auto"):
+                 exchange: str = "auto", schedule: str = "auto", pieces: int = 0):
         """exchange: "auto" | "fused" | "sharded" (NVLink peer stores, attached at
         construction) | "nccl" (ncclAllGather of push areas); schedule: see
         Plan.set_schedule."""
@@ -460,6 +464,8 @@ class SyncWorker:
             self.plan.set_schedule(schedule)
         if world_size > 1 and exchange in ("fused", "sharded"):
             self.plan.set_exchange(exchange)
+        if pieces:
+            self.plan.set_pieces(pieces)
         self.grad_flat, self.grads = aligned_flat(self.ns, self.device)
         self.out_flat, self.outs = aligned_flat(self.ns, self.device)
         self.plan.bind(self.grads, self.outs)
@@ -531,7 +537,8 @@ class LocalCluster:
     ``devices``: one device for all, or one per worker."""
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
-                 n_workers: int, devices=None, exchange: str = "auto", schedule: str = "auto"):
+                 n_workers: int, devices=None, exchange: str = "auto", schedule: str = "auto",
+                 pieces: int = 0):
         if not isinstance(devices, (list, tuple)):
             devices = [devices] * n_workers
         self.devices = [_dev(d) for d in devices]
@@ -546,6 +553,8 @@ class LocalCluster:
                 p.set_schedule(schedule)
             if self.n_workers > 1 and exchange != "auto":
                 p.set_exchange(exchange)
+            if pieces:
+                p.set_pieces(pieces)
             gf, gv = aligned_flat(self.ns, dev)
             of, ov = aligned_flat(self.ns, dev)
             p.bind(gv, ov)

@@ -1,6 +1,7 @@
 """Per-kernel timeline of tgb_step (events around every launch on its own stream).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/step_timeline.py [workload]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/step_timeline.py \
+        [workload] [exchange auto|fused|sharded|nccl] [pieces]
 
 Runs the product step (default schedule) on every rank, records 6 steps with
 tgb_plan_enable_timing and prints, for the last step, every launch's start/end
@@ -27,9 +28,11 @@ def main():
         dist.init_process_group("gloo", rank=rank, world_size=ws)
     comm = tg.Comm(rank, ws) if ws > 1 else None
     wl = sys.argv[1] if len(sys.argv) > 1 else "vgg16"
+    ex = sys.argv[2] if len(sys.argv) > 2 else "auto"
+    pieces = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     layers = tg.layersets.get(wl)
     sw = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
-                       rank=rank, world_size=ws, comm=comm, device=dev)
+                       rank=rank, world_size=ws, comm=comm, device=dev, exchange=ex, pieces=pieces)
     sw.grad_flat.normal_(0.0, 1e-3, generator=torch.Generator(device=dev).manual_seed(1000 + rank))
     for t in range(5):
         sw.step(t)
@@ -62,10 +65,8 @@ def main():
     else:
         allr = [{"rank": 0, "span_us": span, "timeline": tl}]
     if rank == 0:
-        info = tg._lib.PlanInfo()
-        tg._lib.check(tg._lib.load().tgb_plan_get_info(sw.plan.h, tg.codec.C.byref(info)), "info")
-        print(json.dumps({"workload": wl, "n_gpus": ws, "exchange": tg._lib.EXCHANGE_NAMES[info.exchange],
-                          "ranks": allr}), flush=True)
+        print(json.dumps({"workload": wl, "n_gpus": ws, "exchange": sw.plan.exchange,
+                          "pieces": pieces, "ranks": allr}), flush=True)
     if ws > 1:
         dist.barrier()
     sw.plan.close()
