@@ -714,7 +714,9 @@ __device__ __forceinline__ uint32_t k2_code_chunk(const K2Args& a, const LayerDe
     if (a.check && fminf(bad_mag, bound) > s)  // codec.hpp:163-165
         raise_error(a.err, TGB_E_SCALER_BELOW_MAX, static_cast<int32_t>(L.tensor),
                     block_rng_base(L) + ch.begin);
+#ifndef TGB_AB_NO_DEMOTE  // (same-box A/B builds only, tools/build_variant.sh)
     if (b >= a.keep_from) demote_l2(g, count);
+#endif
     __syncthreads();
     if (a.nnz) count_nonzero(stage, 0, nbytes, a.nnz, 0);
     return nbytes;

@@ -269,14 +269,15 @@ static tgb_status build_schedule(tgb_plan* P) {
         }
         P->sums_bytes = round_up(std::max<uint64_t>(so, 1), kAlignPush);
         // pieces: contiguous runs of the K2 chunk list, balanced by K3a bytes (raw fp32 =
-        // 16x codes); auto = one piece per 32 Mi elements, at most 4 (VGG-16: 4, AlexNet:
-        // 2, GoogLeNet: 1 -- a small set is latency-bound, extra barriers only cost)
+        // 16x codes). auto = 1: measured on 4 B200s (VGG-16, profiles/r02_sharded_pieces.json)
+        // 1 / 2 / 4 / 8 pieces = 0.444 / 0.455 / 0.539 / 0.707 ms -- every piece adds two
+        // cross-GPU barriers and a K2 tail wave, and the per-piece K3a -> barrier -> K3b chain
+        // on the second stream is longer than the K2 piece it should hide behind
         std::vector<uint64_t> cum(P->h_chunks.size() + 1, 0);
         for (size_t c = 0; c < P->h_chunks.size(); ++c)
             cum[c + 1] = cum[c] + P->h_chunks[c].count * (is_pass(P->h_chunks[c]) ? 16ull : 1ull);
         const uint64_t W = cum.back();
-        int np = P->pieces_opt > 0 ? P->pieces_opt
-                                   : static_cast<int>(std::min<uint64_t>(4, P->total >> 25));
+        int np = P->pieces_opt > 0 ? P->pieces_opt : 1;
         np = std::max(1, std::min(np, std::min(kMaxPieces, static_cast<int>(P->h_chunks.size()))));
         P->n_pieces = np;
         auto cut = [&](uint64_t target) {
