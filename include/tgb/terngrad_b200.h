@@ -162,11 +162,14 @@ tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_in
  * TGB_PLAN_OPT_FUSED_OPTIMIZER: 1 (default) the decode kernel applies the optimizer in
  *   tgb_step_apply; 0 the averaged gradient is written and a separate kernel applies it.
  * TGB_PLAN_OPT_PIECES: sharded exchange, pieces of the K2 work list (0 = auto, 1..8): the
- *   owner reduce + decode of piece p run while K2 computes piece p+1; before attaching. */
+ *   owner reduce + decode of piece p run while K2 computes piece p+1; before attaching.
+ * TGB_PLAN_OPT_CHUNK: K1/K2 work-item elements (0 = auto: the smallest power of two
+ *   >= total / 444 in [4K, 32K]; else a power of two in [1K, 32K]); before attaching. */
 #define TGB_PLAN_OPT_SCHEDULE 0
 #define TGB_PLAN_OPT_EXCHANGE 1
 #define TGB_PLAN_OPT_FUSED_OPTIMIZER 2
 #define TGB_PLAN_OPT_PIECES 3
+#define TGB_PLAN_OPT_CHUNK 4
 #define TGB_SCHEDULE_AUTO 0
 #define TGB_SCHEDULE_SINGLE 1
 #define TGB_SCHEDULE_GROUPS 2

@@ -101,6 +101,7 @@ static tgb_status build_schedule(tgb_plan* P) {
     // elements: 16K, step 32.9 -> 27.0 us; a 1M layer: 4K, 21.7 -> 14.6 us).
     uint64_t chunk = 4096;
     while (chunk < kChunk12 && chunk * 444 < P->total) chunk <<= 1;
+    if (P->chunk_opt) chunk = static_cast<uint64_t>(P->chunk_opt);
     P->chunk12 = static_cast<uint32_t>(chunk);
     P->chunk3 = kChunk3;
     // sharded exchange: from N >= 5 by default (measured at N = 4 the fused
@@ -577,6 +578,12 @@ tgb_status tgb_plan_set_option(tgb_plan* P, int32_t option, int64_t value) {
                 (!P->p.scaler_sharing || P->n_workers < 2 || P->n_workers > kMaxPeers))
                 return TGB_ERR_UNSUPPORTED;  // the owner sums integer codes (shared scalers)
             P->exchange_opt = static_cast<int32_t>(value);
+            break;
+        case TGB_PLAN_OPT_CHUNK:
+            if (value != 0 && (value < 1024 || value > kChunk12 || (value & (value - 1))))
+                return TGB_ERR_INVALID_ARGUMENT;
+            if (P->attached) return TGB_ERR_UNSUPPORTED;
+            P->chunk_opt = static_cast<int32_t>(value);
             break;
         case TGB_PLAN_OPT_PIECES:
             if (value < 0 || value > kMaxPieces) return TGB_ERR_INVALID_ARGUMENT;

@@ -102,6 +102,7 @@ struct tgb_plan {
     // owns chunks [pcs[p][r], pcs[p][r+1]) of piece p. Piece p's barrier -> K3a ->
     // barrier -> K3b run on a second stream while K2 computes piece p+1.
     int32_t pieces_opt = 0;  // TGB_PLAN_OPT_PIECES (0: auto)
+    int32_t chunk_opt = 0;   // TGB_PLAN_OPT_CHUNK (0: auto)
     int32_t n_pieces = 1;
     uint32_t pb[kMaxPieces + 1] = {};
     uint32_t pcs[kMaxPieces][kMaxPeers + 1] = {};

@@ -22,6 +22,8 @@ sets = {w: tg.layersets.get(w) for w in ("googlenet", "alexnet", "vgg16")}
 sets["layer_1M"] = [("g", [1 << 20])]
 sets["layer_4M"] = [("g", [1 << 22])]
 sets["layer_16M"] = [("g", [1 << 24])]
+if len(sys.argv) > 2:
+    sets = {k: v for k, v in sets.items() if k in sys.argv[2:]}
 
 
 def timed(fn, reps=5):
@@ -41,8 +43,11 @@ for name, layers in sets.items():
     names, shapes = [n for n, _ in layers], [s for _, s in layers]
     n = sum(tg.layersets.numel(s) for s in shapes)
     res, ref = {}, None
-    for sched in ("auto", "unfused", "fused12"):
-        sw = tg.SyncWorker(names, shapes, tg.CodecConfig(seed=42), device=dev, schedule=sched)
+    for sched in ("auto", "fused12", "chunk4096", "chunk8192", "chunk16384"):
+        sw = tg.SyncWorker(names, shapes, tg.CodecConfig(seed=42), device=dev,
+                           schedule=sched if not sched.startswith("chunk") else "auto")
+        if sched.startswith("chunk"):
+            sw.plan.set_option(tg._lib.TGB_PLAN_OPT_CHUNK, int(sched[5:]))
         sw.grad_flat.normal_(0, 1e-3, generator=torch.Generator(device=dev).manual_seed(1))
         plan = sw.plan
         for t in range(5):
