@@ -234,6 +234,10 @@ tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n);
  * the plans that see it). Returns when every launch is queued. */
 tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
                           void* const* streams);
+/* layout self-check (host only, no kernel runs): every region a kernel of this plan
+ * reads or writes lies inside its allocation and the work items tile their blocks;
+ * TGB_ERR_PROTOCOL with tgb_last_error_message() naming the first violation */
+tgb_status tgb_plan_audit(const tgb_plan* plan);
 /* device pointers of the push area written by the last step (own scaler slots
  * + codes) and of the gather buffer (n_workers push areas) the last K3 read */
 tgb_status tgb_plan_last_buffers(tgb_plan* plan, uint8_t** d_push, uint8_t** d_gathered);

@@ -52,7 +52,7 @@ EXPORTS = [
     "tgb_plan_code_stats", "tgb_plan_enable_code_stats", "tgb_plan_enable_timing",
     "tgb_plan_read_timing",
     "tgb_plan_attach_peers", "tgb_plan_attach_local", "tgb_local_step", "tgb_plan_last_buffers",
-    "tgb_traffic_for_layers", "tgb_plan_traffic",
+    "tgb_traffic_for_layers", "tgb_plan_traffic", "tgb_plan_audit",
     "tgb_optimizer_apply", "tgb_plan_bind_optimizer", "tgb_step_apply",
     "tgb_last_error_message", "tgb_plan_set_names", "tgb_plan_push_frame_size",
     "tgb_plan_serialize_push", "tgb_plan_decode_pull",
@@ -157,6 +157,7 @@ def _declare(L):
         "tgb_traffic_for_layers": (S, [C.POINTER(LayerDesc), C.POINTER(C.c_char_p), _i32,
                                        C.POINTER(CodecParams), _i32, C.POINTER(Traffic)]),
         "tgb_plan_traffic": (S, [_vp, C.POINTER(Traffic)]),
+        "tgb_plan_audit": (S, [_vp]),
         "tgb_plan_last_buffers": (S, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
         "tgb_optimizer_apply": (S, [C.POINTER(Optimizer), _u64, C.c_double, _i32,
                                     C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp),

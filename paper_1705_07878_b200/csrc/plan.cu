@@ -195,7 +195,11 @@ static tgb_status build_schedule(tgb_plan* P) {
     // N = 1: K1 loads its last 24 MB per launch L2 evict_last, K2 (walking chunks
     // last-to-first) re-reads them from L2 and demotes them (tools/l2keep_ab.py: step
     // -4.6 us; 16-32 MB is the plateau). At N > 1 the lines linger into K3 (+8 us).
+#ifndef TGB_AB_NO_KEEP  // (same-box A/B builds only, tools/build_variant.sh)
     P->k1_keep = N == 1 ? static_cast<uint32_t>((24ull << 20) / (4ull * P->chunk12)) : 0u;
+#else
+    P->k1_keep = 0;
+#endif
     // K1 + K2 as one persistent launch (opt-in, TGB_SCHEDULE_FUSED12): K2 of a tensor
     // starts as soon as its K1 finalized. Measured slower than K1 -> K2 with K2 as
     // K1's programmatic dependent, also for small sets (CUDA-graph replay, device
@@ -1511,3 +1515,92 @@ tgb_status tgb_check(tgb_plan* P, tgb_error* out) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ audit
+// Layout self-check (no kernel runs): every region a kernel of this plan reads or
+// writes lies inside its allocation and work items tile their blocks exactly.
+// compute-sanitizer is not available on the GPU pool; this is the host-side
+// substitute for the address-range class of bugs (tests call it for every
+// configuration they build).
+extern "C" tgb_status tgb_plan_audit(const tgb_plan* P) {
+    if (!P) return TGB_ERR_INVALID_ARGUMENT;
+    auto bad = [](const std::string& m) { return set_protocol_error("audit: " + m); };
+    const size_t nb = P->h_layers.size();
+    if (static_cast<uint64_t>(P->n_slots) * 4 > P->codes_offset) return bad("slots overlap codes");
+    uint64_t prev_end = P->codes_offset;
+    for (size_t b = 0; b < nb; ++b) {
+        const LayerDev& L = P->h_layers[b];
+        const uint64_t bytes = (L.flags & kLayerPassthrough) ? 4ull * L.n : (L.n + 3ull) / 4;
+        if (L.code_off < prev_end || L.code_off % 16) return bad("block region order " + std::to_string(b));
+        if (L.code_off + bytes > P->push_bytes) return bad("block region past push area " + std::to_string(b));
+        prev_end = L.code_off + bytes;
+    }
+    auto check_items = [&](const std::vector<ChunkDev>& chs, const char* what) -> tgb_status {
+        std::vector<uint64_t> covered(nb, 0);
+        for (size_t c = 0; c < chs.size(); ++c) {
+            const ChunkDev& ch = chs[c];
+            if (ch.layer >= nb || ch.nblk < 1 || ch.layer + ch.nblk > nb)
+                return bad(std::string(what) + " item block range " + std::to_string(c));
+            if (ch.nblk == 1) {
+                const LayerDev& L = P->h_layers[ch.layer];
+                if (static_cast<uint64_t>(ch.begin) + ch.count > L.n || ch.begin % 16)
+                    return bad(std::string(what) + " item past its block " + std::to_string(c));
+                covered[ch.layer] += ch.count;
+                continue;
+            }
+            uint64_t cnt = 0;
+            const LayerDev& L0 = P->h_layers[ch.layer];
+            for (uint32_t j = 0; j < ch.nblk; ++j) {
+                const LayerDev& L = P->h_layers[ch.layer + j];
+                if (L.tensor != L0.tensor || !(L.flags & kLayerMultiBucket) ||
+                    L.slot != L0.slot + static_cast<int32_t>(j) ||
+                    L.code_off != L0.code_off + cnt / 4 || ch.begin != 0)
+                    return bad(std::string(what) + " multi-bucket item not contiguous " + std::to_string(c));
+                cnt += L.n;
+                covered[ch.layer + j] += L.n;
+            }
+            if (cnt != ch.count) return bad(std::string(what) + " multi-bucket count " + std::to_string(c));
+        }
+        for (size_t b = 0; b < nb; ++b)
+            if (covered[b] != P->h_layers[b].n)
+                return bad(std::string(what) + " items do not tile block " + std::to_string(b));
+        return TGB_OK;
+    };
+    TGB_TRY(check_items(P->h_chunks, "K1/K2"));
+    TGB_TRY(check_items(P->h_chunks3, "K3"));
+    if (P->shard) {
+        if (P->pb[0] != 0 || P->pb[P->n_pieces] != P->h_chunks.size()) return bad("pieces");
+        for (int q = 0; q < P->n_pieces; ++q) {
+            if (P->pb[q] > P->pb[q + 1]) return bad("pieces order");
+            if (P->pcs[q][0] != P->pb[q] || P->pcs[q][P->n_workers] != P->pb[q + 1])
+                return bad("owners do not tile piece " + std::to_string(q));
+            for (int r = 0; r < P->n_workers; ++r)
+                if (P->pcs[q][r] > P->pcs[q][r + 1]) return bad("owner order");
+        }
+        std::vector<std::pair<uint64_t, uint64_t>> spans;
+        for (const ChunkDev& ch : P->h_chunks) {
+            const LayerDev& L = P->h_layers[ch.layer];
+            const bool pass = (L.flags & kLayerPassthrough) != 0;
+            const uint64_t off = pass ? 16ull * L.sum_off16 + 4ull * ch.begin
+                                      : 16ull * L.sum_off16 + (ch.begin / P->chunk12) *
+                                                                  static_cast<uint64_t>(P->sum_region);
+            const uint64_t len = pass ? 4ull * ch.count
+                                      : (ch.count + P->radix_m - 1) / P->radix_m * 4ull;
+            if (off + len > P->sums_bytes) return bad("sums region past the sums buffer");
+            spans.push_back({off, off + len});
+        }
+        std::sort(spans.begin(), spans.end());
+        for (size_t i = 1; i < spans.size(); ++i)
+            if (spans[i].first < spans[i - 1].second) return bad("sums regions overlap");
+    }
+    if (P->attached) {
+        const uint64_t g = P->push_bytes * static_cast<uint64_t>(P->n_workers);
+        if (P->sums_off < 2 * g || P->flags_off < P->sums_off + 2 * P->sums_bytes)
+            return bad("exchange allocation order");
+        if (P->flags_off + static_cast<uint64_t>(kFlagSlots) * 2 * kMaxPeers * 16 > P->ipc_bytes)
+            return bad("barrier records past the allocation");
+        if (P->shard && 2 * P->n_pieces > kFlagSlots) return bad("barrier slots");
+        if (P->grouped && kFlagSlots < 2) return bad("barrier slots");
+    }
+    return TGB_OK;
+}

@@ -188,6 +188,13 @@ class Plan:
     def exchange(self) -> str:
         return _lib.EXCHANGE_NAMES[self.info.exchange]
 
+    def audit(self):
+        """tgb_plan_audit: raise if any kernel region lies outside its allocation"""
+        st = load().tgb_plan_audit(self.h)
+        if st == _lib.TGB_ERR_PROTOCOL:
+            raise AssertionError(load().tgb_last_error_message().decode())
+        check(st, "tgb_plan_audit")
+
     def traffic(self) -> "TrafficStats":
         """one step of this worker's TrafficStats terms (tgb_plan_traffic)"""
         t = _lib.Traffic()

@@ -620,3 +620,54 @@ def test_fixed_size_multibucket_step_vs_oracle(restated, k):
     got = np.concatenate([o.cpu().numpy() for o in sw.outs])
     assert got.view(np.uint32).tobytes() == want.view(np.uint32).tobytes()
     sw.plan.close()
+
+
+def test_plan_audit_every_layout():
+    """tgb_plan_audit over the layouts the tests and the bench build: block regions
+    inside the push area, work items tiling their blocks (incl. multi-bucket items),
+    sharded sums regions disjoint and inside the sums buffer, owners tiling pieces,
+    barrier records inside the peer-exchange allocation (the class of bug a
+    memcheck run would catch; compute-sanitizer is closed on the GPU pool)"""
+    small = (["conv.weight", "conv.bias", "empty", "fc.weight", "fc.bias"],
+             [1728, 64, 0, 40003, 10])
+    g = tg.layersets.get("googlenet")
+    sets = [small, ([n for n, _ in g], [tg.layersets.numel(s) for _, s in g])]
+    cfgs = [tg.CodecConfig(seed=42), tg.CodecConfig(seed=42, bucketing=tg.Bucketing.Global),
+            tg.CodecConfig(seed=42, scaler_sharing=False)] + \
+        [tg.CodecConfig(seed=42, bucketing=tg.Bucketing.FixedSize, bucket_size=k,
+                        passthrough={"conv.bias"}) for k in (7, 64, 256, 1000, 4096, 1 << 20)]
+    n_checked = 0
+    for names, ns in sets:
+        for cfg in cfgs:
+            for N, ex, pieces in ((1, "auto", 0), (2, "fused", 0), (3, "sharded", 2),
+                                  (5, "sharded", 0), (8, "auto", 0), (8, "fused", 0)):
+                if ex == "sharded" and not cfg.scaler_sharing:
+                    continue
+                plans = []
+                for w in range(N):
+                    p = tg.Plan(names, ns, cfg, worker=w, n_workers=N, device=DEV)
+                    if N > 1 and ex != "auto":
+                        p.set_exchange(ex)
+                    if pieces:
+                        p.set_pieces(pieces)
+                    p.audit()
+                    plans.append(p)
+                if N > 1 and len(names) < 10:  # attach (IPC layout, barrier records)
+                    flats = [tg.aligned_flat(ns, DEV) for _ in range(N)]
+                    for p, (_, views) in zip(plans, flats):
+                        p.bind(views, views)
+                    tg.Plan.attach_local(plans)
+                    for p in plans:
+                        p.audit()
+                n_checked += len(plans)
+                for p in plans:
+                    p.close()
+    vgg = tg.layersets.get("vgg16")
+    for cfg in (tg.CodecConfig(seed=42), tg.CodecConfig(seed=42, bucketing=tg.Bucketing.FixedSize,
+                                                        bucket_size=256)):
+        for N in (1, 4, 8):
+            p = tg.Plan([n for n, _ in vgg], [tg.layersets.numel(s) for _, s in vgg], cfg,
+                        worker=0, n_workers=N, device=DEV)
+            p.audit()
+            p.close()
+    assert n_checked > 100

@@ -95,6 +95,44 @@ __device__ __forceinline__ void emit(const Out& o, uint32_t c, uint32_t count, d
     __syncthreads();
 }
 
+// L2-policy loads of the N = 1 K1 (evict_first, or evict_last for the units K2 re-reads)
+__device__ __forceinline__ float4 ld_hint(const float4* p, uint64_t pol) {
+    float4 v;
+    asm("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(p), "l"(pol));
+    return v;
+}
+
+// V3: the production loop with the policy loads (MODE 0 evict_first, 1 evict_last)
+template <int U, int MODE>
+__global__ void __launch_bounds__(256, 4) k1_v3(const float* g, uint64_t n, Out o) {
+    const uint32_t c = blockIdx.x;
+    const uint64_t b0 = static_cast<uint64_t>(c) * kCh;
+    const uint32_t count = static_cast<uint32_t>(n - b0 < kCh ? n - b0 : kCh);
+    const float* p = g + b0;
+    uint64_t pol;
+    if (MODE == 1)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const double x0 = static_cast<double>(__ldg(p));
+    double S = 0.0, Q = 0.0;
+    float mx = 0.0f;
+    const float4* g4 = reinterpret_cast<const float4*>(p);
+    const uint32_t n4 = count >> 2;
+    uint32_t i = threadIdx.x;
+    for (; i + (U - 1) * 256 < n4; i += U * 256) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_hint(g4 + i + u * 256, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc4(v[u], x0, S, Q, mx);
+    }
+    for (; i < n4; i += 256) acc4(ld_hint(g4 + i, pol), x0, S, Q, mx);
+    emit<256>(o, c, count, x0, S, Q, mx);
+}
+
 // V0: production loop (U float4 in flight, compute after)
 template <int U, int NT, int MINB, int MODE>
 __global__ void __launch_bounds__(NT, MINB) k1_v0(const float* g, uint64_t n, Out o) {
@@ -334,6 +372,8 @@ int main() {
     timeit("V0 prod U=8 minB4 (tail)", [&] { k1_v0<8, 256, 4, 0><<<nc, 256>>>(g, n, o0); }, true);
     timeit("V0 prod U=8 minB4 (no fence/atomic)", [&] { k1_v0<8, 256, 4, 0><<<nc, 256>>>(g, n, oN); }, true);
     timeit("V0 no fp64 math U=8 minB4", [&] { k1_v0<8, 256, 4, 2><<<nc, 256>>>(g, n, o0); }, false);
+    timeit("V3 L2::evict_first policy loads", [&] { k1_v3<8, 0><<<nc, 256>>>(g, n, o0); }, true);
+    timeit("V3 L2::evict_last policy loads", [&] { k1_v3<8, 1><<<nc, 256>>>(g, n, o0); }, true);
     timeit("V0 int f2d U=8 minB4", [&] { k1_v0<8, 256, 4, 1><<<nc, 256>>>(g, n, o0); }, true);
     timeit("V0 U=4 minB4", [&] { k1_v0<4, 256, 4, 0><<<nc, 256>>>(g, n, o0); }, true);
     timeit("V0 U=4 minB6", [&] { k1_v0<4, 256, 6, 0><<<nc, 256>>>(g, n, o0); }, true);
