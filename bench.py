@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="vgg16", choices=["vgg16", "alexnet", "googlenet"])
     ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "sharded", "nccl"])
-    ap.add_argument("--pieces", type=int, default=0, help="sharded exchange pieces (0 = auto)")
+    ap.add_argument("--pieces", type=int, default=0, help="exchange pieces (0 = auto)")
+    ap.add_argument("--overlap", type=int, default=-1, help="overlapped exchange: -1 auto, 0, 1")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU time budget of the in-line cpu_baseline (at least one full step)")
@@ -281,7 +282,8 @@ def run_b200(args):
     shapes = [s for _, s in layers]
     cfg = tg.CodecConfig(seed=42)
     sw = tg.SyncWorker(names, shapes, cfg, rank=rank, world_size=ws, comm=comm, device=dev,
-                       exchange=args.exchange, pieces=args.pieces)
+                       exchange=args.exchange, pieces=args.pieces,
+                       overlap=None if args.overlap < 0 else bool(args.overlap))
     ns = sw.ns
     n = sum(ns)
     plan = sw.plan

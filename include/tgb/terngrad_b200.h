@@ -170,6 +170,11 @@ tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_in
 #define TGB_PLAN_OPT_FUSED_OPTIMIZER 2
 #define TGB_PLAN_OPT_PIECES 3
 #define TGB_PLAN_OPT_CHUNK 4
+/* TGB_PLAN_OPT_OVERLAP: N > 1 peer exchanges, -1 auto / 0 off / 1 on: one K2 launch
+ *   whose CTAs publish every finished piece of the work list to the peers, so the
+ *   decode of piece p (fused: K3; sharded: owner reduce -> barrier -> decode) overlaps K2
+ *   of the later pieces (replaces the two-group schedule); before attaching. */
+#define TGB_PLAN_OPT_OVERLAP 5
 #define TGB_SCHEDULE_AUTO 0
 #define TGB_SCHEDULE_SINGLE 1
 #define TGB_SCHEDULE_GROUPS 2

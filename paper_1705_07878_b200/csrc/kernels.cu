@@ -237,7 +237,25 @@ struct K2Args {
     OptArgs opt{};
     int32_t pdl = 0;  // launched as K1's programmatic dependent: 1 wait, 2/3 prefetch + wait
     uint32_t keep_from = ~0u;  // work items K1 kept in L2 (evict_last): demoted after reading
+    // overlapped exchange: the launch covers n_pieces pieces [piece_bounds[q],
+    // piece_bounds[q+1]) of work items; the CTA finishing the last item of piece q
+    // publishes this rank's barrier record {epoch, t} for slot q to every rank, so the
+    // decode of piece q starts while K2 still computes the later pieces. Sharded: the
+    // owner of item b is r with owner_bounds[q][r] <= b < owner_bounds[q][r+1].
+    int32_t n_pieces = 0;
+    uint32_t piece_bounds[kMaxPieces + 1];
+    uint32_t owner_bounds[kMaxPieces][kMaxPeers + 1];
+    uint32_t* piece_cnt = nullptr;        // per piece: items finished (self-resetting)
+    uint64_t* flag_remote[kMaxPeers];     // this rank's slot-0, parity-0 record in rank p
+    int32_t n_flags = 0;
+    uint64_t epoch = 0;
 };
+
+__device__ __forceinline__ uint32_t piece_of(const K2Args& a, uint32_t b) {
+    uint32_t q = 0;
+    while (q + 1 < static_cast<uint32_t>(a.n_pieces) && b >= a.piece_bounds[q + 1]) ++q;
+    return q;
+}
 
 // nonzero 2-bit codes of the staged chunk (pad codes are 00); one atomic per CTA
 // stage[from, nbytes) plus `extra` already counted by this thread (from % 4 == 0)
@@ -264,6 +282,11 @@ __device__ __forceinline__ void count_nonzero(const uint8_t* stage, uint32_t fro
 
 __device__ __forceinline__ int shard_owner(const K2Args& a, uint32_t b) {
     int r = 0;
+    if (a.n_pieces) {
+        const uint32_t* ob = a.owner_bounds[piece_of(a, b)];
+        while (r + 1 < a.shard_n && b >= ob[r + 1]) ++r;
+        return r;
+    }
     while (r + 1 < a.shard_n && b >= a.shard_bounds[r + 1]) ++r;
     return r;
 }
@@ -414,6 +437,33 @@ __device__ __forceinline__ void demote_l2(const float* g, uint32_t count) {
     const uintptr_t a1 = reinterpret_cast<uintptr_t>(g + count);
     for (uintptr_t a = a0 + 128u * threadIdx.x; a < a1; a += 128u * kThreads)
         asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(a) : "memory");
+}
+
+// Overlapped exchange: work item b is done (its codes stored at every destination;
+// the bulk copies completed before thread 0 got here). The CTA counts itself into
+// its piece; the CTA completing the piece publishes this rank's record {epoch, t}
+// of barrier slot q to every rank. Ordering: every thread's stores -> bar.sync ->
+// thread 0 orders the async-proxy (TMA) writes before its generic operations
+// (fence.proxy.async) and releases at GPU scope before the counter increment; the
+// last CTA acquires all increments, then one fence.acq_rel.sys (cumulative over
+// what it observed) precedes the system-scope release of the records -- one
+// system fence per piece instead of one per work item.
+__device__ __forceinline__ void piece_done(const K2Args& a, uint32_t b) {
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const uint32_t q = piece_of(a, b);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const uint32_t done = atomicAdd(a.piece_cnt + q, 1u) + 1u;
+    if (done != a.piece_bounds[q + 1] - a.piece_bounds[q]) return;
+    a.piece_cnt[q] = 0u;  // every item of the piece has counted: reset for the next step
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    const uint32_t par = static_cast<uint32_t>(a.epoch & 1u) * kMaxPeers;
+    for (int p = 0; p < a.n_flags; ++p) {
+        uint64_t* r = a.flag_remote[p] + 2 * ((2 * q) * kMaxPeers + par);
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(r + 1), "l"(a.t) : "memory");
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(r), "l"(a.epoch) : "memory");
+    }
 }
 
 // Multi-bucket K2 item: ch.nblk whole buckets of k = 2^p elements (k/4 code bytes
@@ -747,14 +797,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
     const uint32_t nbytes = k2_code_chunk<4, kFuse, kOpt>(a, L, ch, b, stage, lutv);
-    // No fence after the peer stores: the step barrier kernel runs after this
-    // grid completes in stream order, and grid completion implies its (peer)
-    // stores are performed -- the guarantee event-based multi-GPU sync relies on.
-    if (!nbytes) return;
-    const uint64_t off = L.code_off + (ch.begin >> 2);
-    int p0, p1;
-    k2_dst_range(a, b, p0, p1);
-    bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
+    // Without pieces no fence follows the peer stores: the step barrier kernel runs
+    // after this grid completes in stream order, and grid completion implies its
+    // (peer) stores are performed -- the guarantee event-based multi-GPU sync relies on.
+    if (nbytes) {
+        const uint64_t off = L.code_off + (ch.begin >> 2);
+        int p0, p1;
+        k2_dst_range(a, b, p0, p1);
+        bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
+    }
+    if (a.n_pieces) piece_done(a, b);
 }
 
 // Fused K1 + K2 for small gradient sets (one launch per step; the K1 -> K2
@@ -1482,6 +1534,16 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     a.pdl = p.pdl;
     a.keep_from = p.keep_from;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
+    a.n_pieces = p.n_pieces;
+    if (p.n_pieces) {
+        for (int q = 0; q <= kMaxPieces; ++q) a.piece_bounds[q] = p.piece_bounds[q];
+        for (int q = 0; q < kMaxPieces; ++q)
+            for (int r = 0; r <= kMaxPeers; ++r) a.owner_bounds[q][r] = p.owner_bounds[q][r];
+        a.piece_cnt = p.piece_cnt;
+        for (int r = 0; r < kMaxPeers; ++r) a.flag_remote[r] = p.flag_remote[r];
+        a.n_flags = p.n_flags;
+        a.epoch = p.epoch;
+    }
     const TableSource src{chunks};
     if (p.fuse_decode && p.optd) {  // N == 1 fused decode -> optimizer
         a.optd = p.optd;
@@ -1884,7 +1946,7 @@ __global__ void k_peer_barrier(PeerFlags f, uint64_t epoch, uint64_t t, int mode
     const int p = threadIdx.x;
     if (p >= f.n) return;
     const uint32_t par = static_cast<uint32_t>(epoch & 1u) * kMaxPeers;
-    if (mode != kBarrierCheck) {
+    if (mode == kBarrierPost || mode == kBarrierSpin) {
         uint64_t* r = f.remote[p] + 2 * par;
         asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(r + 1), "l"(t) : "memory");
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(r), "l"(epoch) : "memory");

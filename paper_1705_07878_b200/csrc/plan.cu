@@ -177,12 +177,15 @@ static tgb_status build_schedule(tgb_plan* P) {
     const bool can_group = !P->shard && big >= 0 && n_layers > 1 &&
                            P->p.bucketing == TGB_BUCKET_PER_TENSOR &&
                            P->p.share_mode == TGB_SHARE_REF;
-    bool want = can_group && layers[big].n * 100 >= P->total * 35 &&
+    // overlapped exchange: N > 1, REF (PRESHARED's allreduce sits between K1 and K2)
+    P->overlap = N > 1 && N <= kMaxPeers && P->p.share_mode == TGB_SHARE_REF &&
+                 P->overlap_opt == 1;
+    bool want = can_group && !P->overlap && layers[big].n * 100 >= P->total * 35 &&
                 layers[big].n * 100 <= P->total * 95;
     if (P->schedule_opt == TGB_SCHEDULE_SINGLE || P->schedule_opt == TGB_SCHEDULE_UNFUSED ||
         P->schedule_opt == TGB_SCHEDULE_FUSED12)
         want = false;
-    if (P->schedule_opt == TGB_SCHEDULE_GROUPS) want = can_group;
+    if (P->schedule_opt == TGB_SCHEDULE_GROUPS) want = can_group && !P->overlap;
     P->grouped = want;
     // K2 as K1's programmatic dependent on single-stream N = 1 plans (tools/env_ab.py,
     // profiles/r01_pdl_l2keep_ab.log): GoogLeNet 31.9 -> 29.1 us with a whole-chunk L2
@@ -256,6 +259,66 @@ static tgb_status build_schedule(tgb_plan* P) {
     P->n_pieces = 1;
     std::memset(P->pb, 0, sizeof(P->pb));
     std::memset(P->pcs, 0, sizeof(P->pcs));
+    std::memset(P->p3, 0, sizeof(P->p3));
+    if (P->overlap && !P->shard) {
+        // pieces of the K2 list by elements (auto: 4), and the K3 items re-listed in K2
+        // order so that each piece's decode items are one contiguous range
+        std::vector<uint64_t> cum(P->h_chunks.size() + 1, 0);
+        for (size_t c = 0; c < P->h_chunks.size(); ++c) cum[c + 1] = cum[c] + P->h_chunks[c].count;
+        int np = P->pieces_opt > 0 ? P->pieces_opt : 4;
+        np = std::max(1, std::min(np, std::min(kMaxPieces, static_cast<int>(P->h_chunks.size()))));
+        P->n_pieces = np;
+        for (int q = 0; q <= np; ++q)
+            P->pb[q] = static_cast<uint32_t>(
+                std::lower_bound(cum.begin(), cum.end(), cum.back() * q / np) - cum.begin());
+        P->pb[np] = static_cast<uint32_t>(P->h_chunks.size());
+        P->h_chunks3.clear();
+        int q = 0;
+        for (uint32_t c = 0; c < P->h_chunks.size(); ++c) {
+            while (q < np && c >= P->pb[q]) P->p3[q++] = static_cast<uint32_t>(P->h_chunks3.size());
+            const ChunkDev& ch = P->h_chunks[c];
+            if (ch.nblk > 1) {  // multi-bucket item: K3 items of whole buckets
+                const uint32_t per = static_cast<uint32_t>(kChunk3 >> P->mb_log2);
+                for (uint32_t f = ch.layer; f < ch.layer + ch.nblk;) {
+                    if (per >= 2) {
+                        const uint32_t m = std::min(per, ch.layer + ch.nblk - f);
+                        uint64_t cnt = 0;
+                        for (uint32_t x = f; x < f + m; ++x) cnt += P->h_layers[x].n;
+                        P->h_chunks3.push_back({f, static_cast<uint32_t>(cnt), 0u, m});
+                        f += m;
+                    } else {
+                        const uint64_t n = P->h_layers[f].n;
+                        for (uint64_t e = 0; e < n; e += kChunk3)
+                            P->h_chunks3.push_back(
+                                {f, static_cast<uint32_t>(std::min<uint64_t>(kChunk3, n - e)),
+                                 static_cast<uint32_t>(e), 1u});
+                        ++f;
+                    }
+                }
+                continue;
+            }
+            for (uint64_t e = 0; e < ch.count; e += kChunk3)
+                P->h_chunks3.push_back({ch.layer, static_cast<uint32_t>(std::min<uint64_t>(
+                                                      kChunk3, ch.count - e)),
+                                        static_cast<uint32_t>(ch.begin + e), 1u});
+        }
+        while (q <= np) P->p3[q++] = static_cast<uint32_t>(P->h_chunks3.size());
+        P->cb3[0] = 0;
+        P->cc3[0] = static_cast<uint32_t>(P->h_chunks3.size());
+    }
+    if ((P->overlap || P->shard) && !P->gs3) {
+        int lo = 0, hi = 0;
+        TGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        TGB_CUDA(cudaStreamCreateWithPriority(&P->gs3, cudaStreamNonBlocking, hi));
+        TGB_CUDA(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
+        if (!P->ev_fork) TGB_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+        for (int q = 0; q < kMaxPieces; ++q)
+            TGB_CUDA(cudaEventCreateWithFlags(&P->ev_piece[q], cudaEventDisableTiming));
+    }
+    if ((P->overlap || P->shard) && !P->d_piece_cnt) {
+        TGB_CUDA(cudaMalloc(&P->d_piece_cnt, kMaxPieces * sizeof(uint32_t)));
+        TGB_CUDA(cudaMemset(P->d_piece_cnt, 0, kMaxPieces * sizeof(uint32_t)));
+    }
     if (P->shard) {
         P->radix_m = radix_digits_u32(2ull * N + 1);
         const uint64_t m = static_cast<uint64_t>(P->radix_m);
@@ -282,7 +345,7 @@ static tgb_status build_schedule(tgb_plan* P) {
         for (size_t c = 0; c < P->h_chunks.size(); ++c)
             cum[c + 1] = cum[c] + P->h_chunks[c].count * (is_pass(P->h_chunks[c]) ? 16ull : 1ull);
         const uint64_t W = cum.back();
-        int np = P->pieces_opt > 0 ? P->pieces_opt : 1;
+        int np = P->pieces_opt > 0 ? P->pieces_opt : (P->overlap ? 4 : 1);
         np = std::max(1, std::min(np, std::min(kMaxPieces, static_cast<int>(P->h_chunks.size()))));
         P->n_pieces = np;
         auto cut = [&](uint64_t target) {
@@ -298,14 +361,6 @@ static tgb_status build_schedule(tgb_plan* P) {
                 P->pcs[q][r] = std::max(P->pb[q], cut(w0 + (w1 - w0) * static_cast<uint64_t>(r) / N));
             P->pcs[q][N] = P->pb[q + 1];
             for (int r = N + 1; r <= kMaxPeers; ++r) P->pcs[q][r] = P->pb[q + 1];
-        }
-        if (!P->gs3) {
-            int lo = 0, hi = 0;
-            TGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            TGB_CUDA(cudaStreamCreateWithPriority(&P->gs3, cudaStreamNonBlocking, hi));
-            TGB_CUDA(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
-            for (int q = 0; q < kMaxPieces; ++q)
-                TGB_CUDA(cudaEventCreateWithFlags(&P->ev_piece[q], cudaEventDisableTiming));
         }
     }
 
@@ -497,6 +552,7 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaFree(P->d_ready);
     cudaFree(P->d_bmax);
     cudaFree(P->d_bmeta);
+    cudaFree(P->d_piece_cnt);
     for (int g = 0; g < 2; ++g) {
         if (P->gs[g]) cudaStreamDestroy(P->gs[g]);
         if (P->ev_join[g]) cudaEventDestroy(P->ev_join[g]);
@@ -588,6 +644,11 @@ tgb_status tgb_plan_set_option(tgb_plan* P, int32_t option, int64_t value) {
                 return TGB_ERR_INVALID_ARGUMENT;
             if (P->attached) return TGB_ERR_UNSUPPORTED;
             P->chunk_opt = static_cast<int32_t>(value);
+            break;
+        case TGB_PLAN_OPT_OVERLAP:
+            if (value < -1 || value > 1) return TGB_ERR_INVALID_ARGUMENT;
+            if (P->attached) return TGB_ERR_UNSUPPORTED;
+            P->overlap_opt = static_cast<int32_t>(value);
             break;
         case TGB_PLAN_OPT_PIECES:
             if (value < 0 || value > kMaxPieces) return TGB_ERR_INVALID_ARGUMENT;
@@ -730,7 +791,21 @@ static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc
         k.dst.remote = 1;
         if (P->shard) {
             k.shard_n = P->n_workers;
-            for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->pcs[piece][r] - cb;
+            if (piece >= 0)
+                for (int r = 0; r <= kMaxPeers; ++r) k.shard_bounds[r] = P->pcs[piece][r] - cb;
+        }
+        if (P->overlap) {  // one launch over the whole list; pieces published from inside K2
+            k.reverse = 0;
+            k.n_pieces = P->n_pieces;
+            for (int q = 0; q <= kMaxPieces; ++q) k.piece_bounds[q] = P->pb[q] - cb;
+            for (int q = 0; q < kMaxPieces; ++q)
+                for (int r = 0; r <= kMaxPeers; ++r) k.owner_bounds[q][r] = P->pcs[q][r] - cb;
+            k.piece_cnt = P->d_piece_cnt;
+            for (int p = 0; p < P->n_workers; ++p)
+                k.flag_remote[p] = reinterpret_cast<uint64_t*>(P->peer_ipc[p] + P->flags_off) +
+                                   2 * P->rank;
+            k.n_flags = P->n_workers;
+            k.epoch = P->epoch;
         }
     }
     const int ts = t_begin(P, st);
@@ -753,9 +828,10 @@ static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc
     return TGB_OK;
 }
 
-// K2 of group g (the sharded exchange: one launch per piece)
+// K2 of group g (the sharded exchange without overlap: one launch per piece)
 static tgb_status launch_tern(tgb_plan* P, int g, uint64_t t, cudaStream_t st,
                               bool fuse_decode = false) {
+    if (P->attached && P->overlap) return launch_tern_range(P, 0, 0, P->cc[0], -1, t, st, false);
     if (P->attached && P->shard) {
         for (int q = 0; q < P->n_pieces; ++q)
             TGB_TRY(launch_tern_range(P, 0, P->pb[q], P->pb[q + 1] - P->pb[q], q, t, st, false));
@@ -848,9 +924,8 @@ static tgb_status launch_barrier(tgb_plan* P, int s, cudaStream_t st, int mode) 
     return TGB_OK;
 }
 
-static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t n_workers,
-                                cudaStream_t st) {
-    const uint32_t cb3 = P->cb3[g], cc3 = P->cc3[g];
+static tgb_status launch_decode_range(tgb_plan* P, int g, uint32_t cb3, uint32_t cc3,
+                                      const uint8_t* src, int32_t n_workers, cudaStream_t st) {
     K3Launch k{src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
                1.0f / static_cast<float>(n_workers), P->d_err};
     k.gate = P->attached ? 1 : 0;
@@ -868,6 +943,11 @@ static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t 
               N * ((nt + 3) / 4 + 4 * np) + (P->opt_active ? 0 : 4 * (nt + np)), 0);
     }
     return TGB_OK;
+}
+
+static tgb_status launch_decode(tgb_plan* P, int g, const uint8_t* src, int32_t n_workers,
+                                cudaStream_t st) {
+    return launch_decode_range(P, g, P->cb3[g], P->cc3[g], src, n_workers, st);
 }
 
 static inline uint8_t* sums_area(const tgb_plan* P, int p) {
@@ -974,6 +1054,16 @@ tgb_status tgb_sync(tgb_plan* P, tgb_comm* C, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     if (P->attached) {  // data already moved by K1/K2: only order the step
+        if (P->overlap) {  // K2 published every piece's records
+            for (int q = 0; q < P->n_pieces; ++q) {
+                TGB_TRY(launch_barrier(P, q, st, kBarrierWait));
+                if (P->shard) {
+                    TGB_TRY(launch_shard_reduce(P, q, st));
+                    TGB_TRY(launch_barrier(P, P->n_pieces + q, st, kBarrierSpin));
+                }
+            }
+            return TGB_OK;
+        }
         if (P->shard) {
             // per piece: [codes landed at their owner] barrier -> K3a -> [sums everywhere] barrier
             for (int q = 0; q < P->n_pieces; ++q) {
@@ -1031,11 +1121,38 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
         return TGB_OK;
     }
     const bool nccl_exchange = !P->attached;
-    if (P->attached && P->shard && P->p.share_mode == TGB_SHARE_REF && !P->k12) {
-        // pipelined sharded exchange: K2 piece by piece on `stream`; on gs3, piece q's
-        // barrier -> K3a -> barrier -> K3b overlap K2 of the pieces after it
+    if (P->attached && P->overlap) {
+        // overlapped exchange: one K2 launch on `stream` publishes every finished piece;
+        // on gs3 (ordered after the caller's prior work), piece q's wait -> decode (fused)
+        // or wait -> K3a -> barrier -> K3b (sharded) overlap K2 of the later pieces
         ++P->epoch;
+        const uint8_t* src = cur_gathered(P);
+        TGB_CUDA(cudaEventRecord(P->ev_fork, st));
         TGB_TRY(launch_stats(P, 0, st));
+        TGB_TRY(launch_tern(P, 0, t, st));
+        TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_fork, 0));
+        for (int q = 0; q < P->n_pieces; ++q) {
+            TGB_TRY(launch_barrier(P, q, P->gs3, kBarrierWait));
+            if (P->shard) {
+                TGB_TRY(launch_shard_reduce(P, q, P->gs3));
+                TGB_TRY(launch_barrier(P, P->n_pieces + q, P->gs3, kBarrierSpin));
+                TGB_TRY(launch_shard_expand(P, q, P->gs3));
+            } else {
+                TGB_TRY(launch_decode_range(P, 0, P->p3[q], P->p3[q + 1] - P->p3[q], src,
+                                            P->n_workers, P->gs3));
+            }
+        }
+        TGB_CUDA(cudaEventRecord(P->ev_done, P->gs3));
+        TGB_CUDA(cudaStreamWaitEvent(st, P->ev_done, 0));
+        return TGB_OK;
+    }
+    if (P->attached && P->shard && P->p.share_mode == TGB_SHARE_REF && !P->k12) {
+        // sharded exchange: K2 piece by piece on `stream`; on gs3 (ordered after the
+        // caller's prior work), piece q's barrier -> K3a -> barrier -> K3b
+        ++P->epoch;
+        TGB_CUDA(cudaEventRecord(P->ev_fork, st));
+        TGB_TRY(launch_stats(P, 0, st));
+        TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_fork, 0));
         for (int q = 0; q < P->n_pieces; ++q) {
             TGB_TRY(launch_tern_range(P, 0, P->pb[q], P->pb[q + 1] - P->pb[q], q, t, st, false));
             TGB_CUDA(cudaEventRecord(P->ev_piece[q], st));
@@ -1110,6 +1227,44 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
         P->last = st_of(w);
         P->last_t = t[w];
         ++P->epoch;
+    }
+    if (plans[0]->overlap) {
+        const int npc = plans[0]->n_pieces;
+        for (int w = 0; w < n; ++w) {  // K1 + K2; K2 posts every piece's records
+            tgb_plan* P = plans[w];
+            cudaStream_t st = st_of(w);
+            if (!on(w)) return fail(TGB_ERR_CUDA);
+            tgb_status s = launch_stats(P, 0, st);
+            if (s == TGB_OK) s = launch_tern(P, 0, t[w], st);
+            if (s != TGB_OK) return fail(s);
+            if (cudaEventRecord(P->ev_local[0], st) != cudaSuccess) return fail(TGB_ERR_CUDA);
+        }
+        for (int phase = 0; phase < (plans[0]->shard ? 2 : 1); ++phase) {
+            for (int w = 0; w < n; ++w) {
+                tgb_plan* P = plans[w];
+                cudaStream_t st = st_of(w);
+                if (!on(w)) return fail(TGB_ERR_CUDA);
+                for (int q = 0; q < n; ++q)
+                    if (cudaStreamWaitEvent(st, plans[q]->ev_local[phase], 0) != cudaSuccess)
+                        return fail(TGB_ERR_CUDA);
+                tgb_status s = TGB_OK;
+                for (int q = 0; q < npc && s == TGB_OK; ++q) {
+                    s = launch_barrier(P, phase * npc + q, st, kBarrierCheck);
+                    if (s == TGB_OK && P->shard && phase == 0) {
+                        s = launch_shard_reduce(P, q, st);
+                        if (s == TGB_OK) s = launch_barrier(P, npc + q, st, kBarrierPost);
+                    } else if (s == TGB_OK && P->shard) {
+                        s = launch_shard_expand(P, q, st);
+                    }
+                }
+                if (s == TGB_OK && !P->shard) s = launch_decode(P, 0, cur_gathered(P), n, st);
+                if (s == TGB_OK && P->shard && phase == 0 &&
+                    cudaEventRecord(P->ev_local[1], st) != cudaSuccess)
+                    s = TGB_ERR_CUDA;
+                if (s != TGB_OK) return fail(s);
+            }
+        }
+        return fail(TGB_OK);
     }
     if (plans[0]->shard) {
         for (int w = 0; w < n; ++w) {
@@ -1281,7 +1436,7 @@ static PlanDesc make_desc(const tgb_plan* P) {
     d.shard = P->shard;
     d.grouped = P->grouped;
     d.radix_m = P->radix_m;
-    d.reserved = static_cast<int32_t>(P->mb_log2) | (P->n_pieces << 8);
+    d.reserved = static_cast<int32_t>(P->mb_log2) | (P->n_pieces << 8) | (P->overlap << 16);
     uint64_t h = 0xcbf29ce484222325ull;
     for (size_t b = 0; b < P->h_layers.size(); ++b) {
         const LayerDev& L = P->h_layers[b];
@@ -1592,6 +1747,15 @@ extern "C" tgb_status tgb_plan_audit(const tgb_plan* P) {
         std::sort(spans.begin(), spans.end());
         for (size_t i = 1; i < spans.size(); ++i)
             if (spans[i].first < spans[i - 1].second) return bad("sums regions overlap");
+    }
+    if (P->overlap && !P->shard) {  // each piece's K3 items cover exactly its K2 items
+        if (P->p3[0] != 0 || P->p3[P->n_pieces] != P->h_chunks3.size()) return bad("K3 pieces");
+        for (int q = 0; q < P->n_pieces; ++q) {
+            uint64_t e2 = 0, e3 = 0;
+            for (uint32_t c = P->pb[q]; c < P->pb[q + 1]; ++c) e2 += P->h_chunks[c].count;
+            for (uint32_t c = P->p3[q]; c < P->p3[q + 1]; ++c) e3 += P->h_chunks3[c].count;
+            if (P->p3[q] > P->p3[q + 1] || e2 != e3) return bad("K3 piece " + std::to_string(q));
+        }
     }
     if (P->attached) {
         const uint64_t g = P->push_bytes * static_cast<uint64_t>(P->n_workers);

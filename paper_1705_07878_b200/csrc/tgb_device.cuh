@@ -85,6 +85,7 @@ struct Partial {
 // buffer plus, with peers attached, the same offset inside every other rank's
 // gathered buffer, written directly over NVLink (IPC-mapped peer memory).
 constexpr int kMaxPeers = 8;  // one NVSwitch box
+constexpr int kMaxPieces = 8; // overlapped / sharded exchange: pieces of the K2 work list
 struct PeerPush {
     uint8_t* base[kMaxPeers];
     int32_t n;       // number of destinations (>= 1)

@@ -33,6 +33,7 @@ struct PeerFlags {
 constexpr int kBarrierSpin = 0;   // publish, then wait for every peer (one GPU per process)
 constexpr int kBarrierPost = 1;   // publish only (LocalCluster, ordered by events)
 constexpr int kBarrierCheck = 2;  // verify the peers' records, no wait (LocalCluster)
+constexpr int kBarrierWait = 3;   // wait for the peers' records posted by K2 (overlapped)
 
 // load every kernel the plans launch (no lazy loading inside a step: a lazily
 // loaded kernel's first launch waits for the device to idle)
@@ -75,6 +76,14 @@ struct K2Launch {
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
     int32_t pdl = 0;            // K2 as K1's programmatic dependent (1), + L2 prefetch (2, 3)
     uint32_t keep_from = ~0u;   // work items K1 loaded evict_last (demoted by K2)
+    // overlapped exchange (n_pieces > 0): see K2Args
+    int32_t n_pieces = 0;
+    uint32_t piece_bounds[kMaxPieces + 1] = {};
+    uint32_t owner_bounds[kMaxPieces][kMaxPeers + 1] = {};
+    uint32_t* piece_cnt = nullptr;
+    uint64_t* flag_remote[kMaxPeers] = {};
+    int32_t n_flags = 0;
+    uint64_t epoch = 0;
 };
 
 struct K3Launch {

@@ -16,7 +16,6 @@ struct tgb_comm {
     int nranks = 0, rank = 0;
 };
 
-constexpr int kMaxPieces = 8;  // sharded exchange: pieces of the K2 chunk list
 constexpr int kFlagSlots = 2 * kMaxPieces;  // barrier slots per step: two layer groups (fused),
                                             // or two barriers per piece (sharded)
 constexpr uint64_t kAlignCodes = 16;  // per-block region alignment (bytes)
@@ -101,6 +100,14 @@ struct tgb_plan {
     // sharded: the K2 chunk list in n_pieces contiguous pieces [pb[p], pb[p+1]); rank r
     // owns chunks [pcs[p][r], pcs[p][r+1]) of piece p. Piece p's barrier -> K3a ->
     // barrier -> K3b run on a second stream while K2 computes piece p+1.
+    // overlapped exchange (TGB_PLAN_OPT_OVERLAP): one K2 launch whose CTAs publish each
+    // finished piece's barrier record; the decode of piece q (fused: K3 over the K3 items
+    // [p3[q], p3[q+1]), listed in K2 order; sharded: K3a -> barrier -> K3b) runs on gs3
+    // while K2 computes the later pieces
+    int32_t overlap_opt = -1;  // -1 auto, 0 off, 1 on
+    bool overlap = false;
+    uint32_t p3[kMaxPieces + 1] = {};
+    uint32_t* d_piece_cnt = nullptr;
     int32_t pieces_opt = 0;  // TGB_PLAN_OPT_PIECES (0: auto)
     int32_t chunk_opt = 0;   // TGB_PLAN_OPT_CHUNK (0: auto)
     int32_t n_pieces = 1;

@@ -166,6 +166,11 @@ class Plan:
                                                      "fused": _lib.TGB_EXCHANGE_FUSED,
                                                      "sharded": _lib.TGB_EXCHANGE_SHARDED}[exchange])
 
+    def set_overlap(self, on: bool):
+        """overlapped exchange (N > 1): K2 publishes finished pieces, their decode
+        overlaps the later pieces' K2; before attaching"""
+        self.set_option(_lib.TGB_PLAN_OPT_OVERLAP, 1 if on else 0)
+
     def set_pieces(self, pieces: int):
         """sharded exchange: pieces of the K2 work list (0 = auto); before attaching"""
         self.set_option(_lib.TGB_PLAN_OPT_PIECES, int(pieces))
@@ -451,7 +456,8 @@ class SyncWorker:
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
                  rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None,
-                 exchange: str = "auto", schedule: str = "auto", pieces: int = 0):
+                 exchange: str = "auto", schedule: str = "auto", pieces: int = 0,
+                 overlap: Optional[bool] = None):
         """exchange: "auto" | "fused" | "sharded" (NVLink peer stores, attached at
         construction) | "nccl" (ncclAllGather of push areas); schedule: see
         Plan.set_schedule."""
@@ -471,6 +477,8 @@ class SyncWorker:
             self.plan.set_schedule(schedule)
         if world_size > 1 and exchange in ("fused", "sharded"):
             self.plan.set_exchange(exchange)
+        if overlap is not None and world_size > 1:
+            self.plan.set_overlap(overlap)
         if pieces:
             self.plan.set_pieces(pieces)
         self.grad_flat, self.grads = aligned_flat(self.ns, self.device)
@@ -545,7 +553,7 @@ class LocalCluster:
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
                  n_workers: int, devices=None, exchange: str = "auto", schedule: str = "auto",
-                 pieces: int = 0):
+                 pieces: int = 0, overlap: Optional[bool] = None):
         if not isinstance(devices, (list, tuple)):
             devices = [devices] * n_workers
         self.devices = [_dev(d) for d in devices]
@@ -560,6 +568,8 @@ class LocalCluster:
                 p.set_schedule(schedule)
             if self.n_workers > 1 and exchange != "auto":
                 p.set_exchange(exchange)
+            if overlap is not None and self.n_workers > 1:
+                p.set_overlap(overlap)
             if pieces:
                 p.set_pieces(pieces)
             gf, gv = aligned_flat(self.ns, dev)

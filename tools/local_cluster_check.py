@@ -42,14 +42,17 @@ def small_checks(N, report):
                (True, F, 256, ("conv1.bias",)), (True, F, 64, ())]
     grads = [[R.normal(100 + w, 0, "mp/" + n, m, 1e-2) for n, m in zip(NAMES, SIZES)]
              for w in range(N)]
-    for exchange in ("fused", "sharded", "sharded3"):  # sharded3: 3 pieces of the K2 list
+    # sharded3: 3 pieces of the K2 list; +ov: overlapped exchange (K2 publishes pieces)
+    for exchange in ("fused", "sharded", "sharded3", "fused+ov", "sharded+ov"):
         for sharing, bucketing, k, pt_names in configs:
-            if exchange != "fused" and not sharing:
+            if exchange.startswith("sharded") and not sharing:
                 continue
             cfg = tg.CodecConfig(seed=42, scaler_sharing=sharing, bucketing=bucketing,
                                  bucket_size=k, passthrough=set(pt_names))
             cl = tg.LocalCluster(NAMES, [[n] for n in SIZES], cfg, N, DEV,
-                                 exchange=exchange[:7], pieces=3 if exchange == "sharded3" else 0)
+                                 exchange=exchange.split("+")[0][:7],
+                                 pieces=3 if exchange in ("sharded3", "sharded+ov", "fused+ov") else 0,
+                                 overlap=True if exchange.endswith("+ov") else None)
             for w in range(N):
                 for v, g in zip(cl.grads[w], grads[w]):
                     if g.size:

@@ -1,7 +1,7 @@
 """Per-kernel timeline of tgb_step (events around every launch on its own stream).
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/step_timeline.py \
-        [workload] [exchange auto|fused|sharded|nccl] [pieces]
+        [workload] [exchange auto|fused|sharded|nccl] [pieces] [overlap 0|1]
 
 Runs the product step (default schedule) on every rank, records 6 steps with
 tgb_plan_enable_timing and prints, for the last step, every launch's start/end
@@ -30,9 +30,11 @@ def main():
     wl = sys.argv[1] if len(sys.argv) > 1 else "vgg16"
     ex = sys.argv[2] if len(sys.argv) > 2 else "auto"
     pieces = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    overlap = {"0": False, "1": True}.get(sys.argv[4]) if len(sys.argv) > 4 else None
     layers = tg.layersets.get(wl)
     sw = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
-                       rank=rank, world_size=ws, comm=comm, device=dev, exchange=ex, pieces=pieces)
+                       rank=rank, world_size=ws, comm=comm, device=dev, exchange=ex, pieces=pieces,
+                       overlap=overlap)
     sw.grad_flat.normal_(0.0, 1e-3, generator=torch.Generator(device=dev).manual_seed(1000 + rank))
     for t in range(5):
         sw.step(t)
