@@ -231,8 +231,9 @@ tgb_status tgb_plan_attach_peers(tgb_plan* plan, tgb_comm* comm);
  * hardware-queue or module-loading setting is needed). Single-process
  * counterpart of the reference's run_cluster over InProcessHub
  * (inc/cluster.hpp:378-397, inc/transport.hpp:77-125); used to run N = 8
- * workers' exchanges on fewer GPUs. REF sharing only (TGB_ERR_UNSUPPORTED for
- * PRESHARED, whose max-allreduce needs a communicator). */
+ * workers' exchanges on fewer GPUs. PRESHARED: after every plan's K1, each plan takes
+ * the max over the N workers' local scalers from its gather buffer (the stand-in for
+ * the ranks' ncclAllReduce(max)) before its K2. */
 tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n);
 /* one step of every plan attached with tgb_plan_attach_local: plan w steps
  * iteration t[w] on streams[w] (cudaStream_t each; a skewed t raises TGB_E_SKEW on

@@ -1976,6 +1976,28 @@ cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, uint64_t t, 
     return launch_status();
 }
 
+// PRESHARED in a LocalCluster: own slots <- max over the N workers' local slots in
+// this plan's gather buffer (share_scalers, codec.hpp:136-141; the ranks' NCCL
+// max-allreduce). Worker w's slot i sits at gather + w * stride + 4 i.
+__global__ void __launch_bounds__(kThreads) k_slot_max(float* own, const uint8_t* gather,
+                                                       uint64_t stride, int n, int n_slots) {
+    for (int i = blockIdx.x * kThreads + threadIdx.x; i < n_slots; i += gridDim.x * kThreads) {
+        float m = 0.0f;
+        for (int w = 0; w < n; ++w)
+            m = fmaxf(m, reinterpret_cast<const float*>(gather + stride * w)[i]);
+        own[i] = m;
+    }
+}
+
+cudaError_t launch_slot_max(float* own, const uint8_t* gather, uint64_t stride, int n,
+                            int n_slots, cudaStream_t st) {
+    if (n_slots <= 0) return cudaSuccess;
+    int grid = (n_slots + kThreads - 1) / kThreads;
+    if (grid > 148 * 4) grid = 148 * 4;
+    k_slot_max<<<grid, kThreads, 0, st>>>(own, gather, stride, n, n_slots);
+    return launch_status();
+}
+
 // ======================================================= kernel preloading
 // Every kernel a plan can launch, loaded once per device at plan creation
 // (cudaFuncGetAttributes forces the module load under CUDA_MODULE_LOADING=LAZY).
@@ -2027,6 +2049,7 @@ cudaError_t preload_kernels() {
         reinterpret_cast<const void*>(k3_expand<6>), reinterpret_cast<const void*>(k3_expand<7>),
         reinterpret_cast<const void*>(k3_expand<8>),
         reinterpret_cast<const void*>(k_peer_barrier),
+        reinterpret_cast<const void*>(k_slot_max),
         reinterpret_cast<const void*>(k_clip_apply),
         reinterpret_cast<const void*>(k_average_raw),
         reinterpret_cast<const void*>(k_rng_bits),

@@ -1228,6 +1228,29 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
         P->last_t = t[w];
         ++P->epoch;
     }
+    // PRESHARED (paper Eq. 4): every plan's K1, then each plan replaces its own slots by
+    // the max over the N workers' local slots its gather buffer now holds (the
+    // single-process stand-in for the ranks' ncclAllReduce(max)), then K2
+    const bool preshared = plans[0]->p.share_mode == TGB_SHARE_PRESHARED;
+    if (preshared) {
+        for (int w = 0; w < n; ++w) {
+            tgb_plan* P = plans[w];
+            if (!on(w)) return fail(TGB_ERR_CUDA);
+            tgb_status s = launch_stats(P, 0, st_of(w));
+            if (s != TGB_OK) return fail(s);
+            if (cudaEventRecord(P->ev_local[2], st_of(w)) != cudaSuccess) return fail(TGB_ERR_CUDA);
+        }
+        for (int w = 0; w < n; ++w) {
+            tgb_plan* P = plans[w];
+            if (!on(w)) return fail(TGB_ERR_CUDA);
+            for (int q = 0; q < n; ++q)
+                if (cudaStreamWaitEvent(st_of(w), plans[q]->ev_local[2], 0) != cudaSuccess)
+                    return fail(TGB_ERR_CUDA);
+            if (launch_slot_max(reinterpret_cast<float*>(own_push(P)), cur_gathered(P),
+                                P->push_bytes, n, P->n_slots, st_of(w)) != cudaSuccess)
+                return fail(TGB_ERR_CUDA);
+        }
+    }
     if (plans[0]->overlap) {
         const int npc = plans[0]->n_pieces;
         for (int w = 0; w < n; ++w) {  // K1 + K2; K2 posts every piece's records
@@ -1271,7 +1294,9 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
             tgb_plan* P = plans[w];
             cudaStream_t st = st_of(w);
             if (!on(w)) return fail(TGB_ERR_CUDA);
-            tgb_status s = P->k12 ? launch_encode(P, t[w], st, false) : launch_stats(P, 0, st);
+            tgb_status s = preshared ? TGB_OK
+                           : P->k12  ? launch_encode(P, t[w], st, false)
+                                     : launch_stats(P, 0, st);
             if (s == TGB_OK && !P->k12) s = launch_tern(P, 0, t[w], st);
             for (int q = 0; q < P->n_pieces && s == TGB_OK; ++q)
                 s = launch_barrier(P, 2 * q, st, kBarrierPost);
@@ -1316,8 +1341,10 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
         }
         for (int g = G - 1; g >= 0; --g) {
             cudaStream_t gs = gst(w, g);
-            tgb_status s = P->grouped ? launch_stats(P, g, gs) : launch_encode(P, t[w], gs, false);
-            if (s == TGB_OK && P->grouped) s = launch_tern(P, g, t[w], gs);
+            tgb_status s = preshared   ? launch_tern(P, g, t[w], gs)
+                           : P->grouped ? launch_stats(P, g, gs)
+                                        : launch_encode(P, t[w], gs, false);
+            if (s == TGB_OK && P->grouped && !preshared) s = launch_tern(P, g, t[w], gs);
             if (s == TGB_OK) s = launch_barrier(P, g, gs, kBarrierPost);
             if (s != TGB_OK) return fail(s);
             if (cudaEventRecord(P->ev_local[g], gs) != cudaSuccess) return fail(TGB_ERR_CUDA);
@@ -1550,8 +1577,6 @@ tgb_status tgb_plan_attach_local(tgb_plan* const* plans, int32_t n) {
     for (int32_t p = 0; p < n; ++p) {
         tgb_plan* P = plans[p];
         if (!P || P->n_workers != n || P->worker != p || P->attached) return TGB_ERR_INVALID_ARGUMENT;
-        // PRESHARED needs the max-allreduce between K1 and K2 (NCCL): ranks only
-        if (n > 1 && P->p.share_mode == TGB_SHARE_PRESHARED) return TGB_ERR_UNSUPPORTED;
     }
     if (n == 1) return TGB_OK;
     int cur = 0;

@@ -151,6 +151,8 @@ cudaError_t launch_clip_apply(const float* g, uint64_t n, const float* bound, fl
                               cudaStream_t st);
 cudaError_t launch_peer_barrier(const PeerFlags& f, uint64_t epoch, uint64_t t, int mode,
                                 ErrWord* err, cudaStream_t st);
+cudaError_t launch_slot_max(float* own, const uint8_t* gather, uint64_t stride, int n,
+                            int n_slots, cudaStream_t st);
 cudaError_t launch_rng_bits(uint32_t key0, uint32_t key1, uint64_t t, uint64_t k0, uint64_t n,
                             uint32_t* out, cudaStream_t st);
 

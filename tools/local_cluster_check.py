@@ -10,7 +10,8 @@ sizes) x REF configs (shared / unshared scalers, Global, FixedSize with
 passthrough tensors) x every exchange the product can select at that N (fused;
 sharded for shared scalers): every worker must hold bit-identical output equal
 to the reference's own average over the same N workers (oracle/_ref,
-codec.hpp:245-311). Also checks LocalCluster's protocol validation: a skewed
+codec.hpp:245-311). PRESHARED (max-shared scalers before ternarize) against its own oracle.
+Also checks LocalCluster's protocol validation: a skewed
 iteration raises "server: iteration skew" and leaves the outputs untouched.
 Prints one JSON line; exit 1 on any mismatch. (Full BASELINE gradient sets:
 tests/test_baseline_parity.py.)
@@ -74,6 +75,46 @@ def small_checks(N, report):
             cl.close()
 
 
+def preshared_checks(N, report):
+    """PRESHARED (paper Eq. 4): each plan's own slots become the max over the N workers'
+    local scalers before K2; against tools/mp_check.py's PRESHARED oracle"""
+    import importlib.util
+
+    from oracle.oracle import Config, Restated
+
+    spec = importlib.util.spec_from_file_location(
+        "mp_check", os.path.join(os.path.dirname(os.path.abspath(__file__)), "mp_check.py"))
+    mp = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mp)
+    R = Restated()
+    F = tg.Bucketing.FixedSize
+    grads = [[R.normal(100 + w, 0, "mp/" + n, m, 1e-2) for n, m in zip(NAMES, SIZES)]
+             for w in range(N)]
+    for exchange in ("fused", "sharded"):
+        for bucketing, k, pt_names in ((tg.Bucketing.PerTensor, 0, ()),
+                                       (F, 1000, ("conv1.bias",)), (F, 256, ())):
+            cfg = tg.CodecConfig(seed=42, share_mode=tg.ShareMode.PRESHARED, bucketing=bucketing,
+                                 bucket_size=k, passthrough=set(pt_names))
+            cl = tg.LocalCluster(NAMES, [[n] for n in SIZES], cfg, N, DEV, exchange=exchange)
+            for w in range(N):
+                for v, g in zip(cl.grads[w], grads[w]):
+                    if g.size:
+                        v.copy_(torch.from_numpy(g).to(DEV))
+            for t in (5, 6, 7):
+                outs = cl.step(t)
+            cl.synchronize()
+            cl.check()
+            flats = [torch.cat([o.cpu() for o in outs[w]]).numpy() for w in range(N)]
+            same = all(np.array_equal(flats[0].view(np.uint32), f.view(np.uint32)) for f in flats)
+            ocfg = Config(seed=42, bucketing=int(bucketing), bucket_size=k)
+            ok = mp.preshared_oracle(R, NAMES, grads, flats[0], N, ocfg,
+                                     [int(n in pt_names) for n in NAMES])
+            key = f"N={N},exchange={exchange},PRESHARED,bucketing={bucketing.name}{k or ''}"
+            report["checks"][key] = {"workers_identical": bool(same), "matches_reference": bool(ok),
+                                     "exchange": cl.exchange}
+            cl.close()
+
+
 def skew_check(N, report):
     cl = tg.LocalCluster(NAMES, [[n] for n in SIZES], tg.CodecConfig(seed=42), N, DEV)
     for w in range(N):
@@ -104,6 +145,7 @@ def main():
     report = {"device": torch.cuda.get_device_name(0), "checks": {}}
     for N in Ns:
         small_checks(N, report)
+        preshared_checks(N, report)
         skew_check(N, report)
     ok = all(v["workers_identical"] and v["matches_reference"] for v in report["checks"].values())
     report["ok"] = ok
