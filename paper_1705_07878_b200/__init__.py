@@ -8,8 +8,7 @@ from .codec import (Bucketing, CodecConfig, CodecError, EncodedGradient, EncodeR
                     GradTensor, HistogramBin, PassthroughBlock, RngStream, ShareMode,
                     ProtocolError, TernaryBlock, average, clip, clip_bound, decode, encode_step,
                     fnv1a64, histogram, scaler, share_scalers, ternarize)
-from .optimizer import (LrSchedule, OptimizerConfig, OptimizerRule, OptimizerState,
-                        ScheduleKind)
+from .optimizer import OptimizerConfig, OptimizerRule, OptimizerState
 from .plan import Comm, LocalCluster, Plan, SyncWorker, TrafficStats, aligned_flat
 from . import layersets
 
@@ -17,6 +16,6 @@ __all__ = [
     "Bucketing", "CodecConfig", "CodecError", "EncodedGradient", "EncodeResult", "GradTensor",
     "HistogramBin", "histogram", "PassthroughBlock", "ProtocolError", "RngStream", "ShareMode", "TernaryBlock", "average", "clip",
     "clip_bound", "decode", "encode_step", "fnv1a64", "scaler", "share_scalers", "ternarize",
-    "Comm", "LocalCluster", "Plan", "SyncWorker", "TrafficStats", "aligned_flat", "layersets", "LrSchedule",
-    "OptimizerConfig", "OptimizerRule", "OptimizerState", "ScheduleKind",
+    "Comm", "LocalCluster", "Plan", "SyncWorker", "TrafficStats", "aligned_flat", "layersets",
+    "OptimizerConfig", "OptimizerRule", "OptimizerState",
 ]

@@ -187,6 +187,7 @@ static tgb_status build_schedule(tgb_plan* P) {
         want = false;
     if (P->schedule_opt == TGB_SCHEDULE_GROUPS) want = can_group && !P->overlap;
     P->grouped = want;
+    P->big = big;
     // K2 as K1's programmatic dependent on single-stream N = 1 plans (tools/env_ab.py,
     // profiles/r01_pdl_l2keep_ab.log): GoogLeNet 31.9 -> 29.1 us with a whole-chunk L2
     // prefetch before the wait, a 2^24 layer 49.6 -> 46.5 us without one, 2^26 / 2^28
@@ -570,6 +571,11 @@ void tgb_plan_destroy(tgb_plan* P) {
     if (P->ev_h2d) cudaEventDestroy(P->ev_h2d);
     if (P->ev_comp) cudaEventDestroy(P->ev_comp);
     if (P->ev_d2h) cudaEventDestroy(P->ev_d2h);
+    for (int g = 0; g < 2; ++g) {
+        if (P->ev_hg[g]) cudaEventDestroy(P->ev_hg[g]);
+        if (P->ev_cg[g]) cudaEventDestroy(P->ev_cg[g]);
+        if (P->ev_dg[g]) cudaEventDestroy(P->ev_dg[g]);
+    }
     cudaSetDevice(prev);
     delete P;
 }
@@ -1379,13 +1385,17 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
 // of tensors that are adjacent on BOTH sides (e.g. flat buffers whose tensors are
 // back to back): one 553 MB copy instead of 32 runs PCIe ~10 % faster. Gaps are
 // never copied (they may be someone else's memory).
+// group >= 0: only the tensors of that layer group (1 = the dominant tensor)
 static tgb_status copy_runs(const tgb_plan* P, const float* const* dst_c, const float* const* src,
-                            cudaMemcpyKind kind, cudaStream_t st) {
+                            cudaMemcpyKind kind, cudaStream_t st, int group = -1) {
     float* const* dst = const_cast<float* const*>(dst_c);
     const size_t nl = P->desc.size();
+    auto in = [&](size_t l) {
+        return group < 0 || (static_cast<int32_t>(l) == P->big) == (group == 1);
+    };
     size_t l = 0;
     while (l < nl) {
-        if (!P->desc[l].n) {
+        if (!P->desc[l].n || !in(l)) {
             ++l;
             continue;
         }
@@ -1394,7 +1404,7 @@ static tgb_status copy_runs(const tgb_plan* P, const float* const* dst_c, const 
         for (; e < nl; ++e) {
             const uint64_t m = P->desc[e].n;
             if (!m) continue;
-            if (dst[e] != dst[l] + n || src[e] != src[l] + n) break;
+            if (!in(e) || dst[e] != dst[l] + n || src[e] != src[l] + n) break;
             n += m;
         }
         TGB_CUDA(cudaMemcpyAsync(dst[l], src[l], n * sizeof(float), kind, st));
@@ -1428,6 +1438,47 @@ tgb_status tgb_step_host(tgb_plan* P, tgb_comm* C, uint64_t t, const float* cons
         TGB_CUDA(cudaEventRecord(P->ev_comp, st));  // nothing computed yet
         TGB_CUDA(cudaEventRecord(P->ev_d2h, st));
         P->host_io = true;
+    }
+    if (P->n_workers == 1 && P->grouped) {
+        // pipelined by layer group: H2D(rest) -> its K1/K2 (+decode) while H2D(dominant)
+        // runs; each group's D2H starts when its decode is done. Both PCIe directions
+        // stay busy and the compute hides under the transfers (round 1: 13.5 ms/step
+        // against the ~12 ms full-duplex floor for VGG-16, compute waited for all H2D).
+        if (!P->ev_hg[0])
+            for (int g = 0; g < 2; ++g) {
+                TGB_CUDA(cudaEventCreateWithFlags(&P->ev_hg[g], cudaEventDisableTiming));
+                TGB_CUDA(cudaEventCreateWithFlags(&P->ev_cg[g], cudaEventDisableTiming));
+                TGB_CUDA(cudaEventCreateWithFlags(&P->ev_dg[g], cudaEventDisableTiming));
+                TGB_CUDA(cudaEventRecord(P->ev_cg[g], st));
+                TGB_CUDA(cudaEventRecord(P->ev_dg[g], st));
+            }
+        TGB_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_d2h, 0));  // (first call ordering)
+        for (int g = 0; g < 2; ++g) {  // the small group first: its compute starts early
+            TGB_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_cg[g], 0));  // previous K2 read them
+            TGB_TRY(copy_runs(P, reinterpret_cast<const float* const*>(P->bound_g.data()),
+                              h_grads, cudaMemcpyHostToDevice, P->s_h2d, g));
+            TGB_CUDA(cudaEventRecord(P->ev_hg[g], P->s_h2d));
+        }
+        P->last = st;
+        P->last_t = t;
+        TGB_CUDA(cudaEventRecord(P->ev_fork, st));
+        for (int g = 0; g < 2; ++g) {
+            cudaStream_t gs = P->gs[g];
+            TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_fork, 0));
+            TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_hg[g], 0));
+            TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_dg[g], 0));  // previous outputs copied out
+            TGB_TRY(launch_stats(P, g, gs));
+            TGB_TRY(launch_tern(P, g, t, gs, true));
+            TGB_CUDA(cudaEventRecord(P->ev_cg[g], gs));
+        }
+        for (int g = 0; g < 2; ++g) {
+            TGB_CUDA(cudaStreamWaitEvent(P->s_d2h, P->ev_cg[g], 0));
+            TGB_TRY(copy_runs(P, h_out, P->bound_out.data(), cudaMemcpyDeviceToHost, P->s_d2h, g));
+            TGB_CUDA(cudaEventRecord(P->ev_dg[g], P->s_d2h));
+        }
+        TGB_CUDA(cudaEventRecord(P->ev_d2h, P->s_d2h));
+        TGB_CUDA(cudaStreamWaitEvent(st, P->ev_d2h, 0));
+        return TGB_OK;
     }
     TGB_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_comp, 0));  // previous K2 read the gradients
     TGB_TRY(copy_runs(P, reinterpret_cast<const float* const*>(P->bound_g.data()), h_grads,

@@ -73,6 +73,7 @@ struct tgb_plan {
     // K1 -> K2 -> [barrier] -> K3 on its own stream, so a memory-bound kernel of one
     // group overlaps a compute-bound kernel of the other.
     bool grouped = false;
+    int32_t big = -1;  // the dominant tensor (group 1 of the two-group schedule)
     uint32_t cb[2] = {0, 0}, cc[2] = {0, 0}, ck1[2] = {0, 0}, cb3[2] = {0, 0}, cc3[2] = {0, 0};
     uint32_t chunk12 = kChunk12, chunk3 = kChunk3;
     int32_t pdl = 0;           // K2 as K1's programmatic dependent (single-stream N = 1 plans)
@@ -134,6 +135,7 @@ struct tgb_plan {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_d2h = nullptr;
     bool host_io = false;
+    cudaEvent_t ev_hg[2] = {}, ev_cg[2] = {}, ev_dg[2] = {};  // grouped N = 1: per layer group
     // optimizer bound for tgb_step_apply
     bool opt_bound = false;
     tgb_optimizer opt{};

@@ -1,10 +1,10 @@
-"""Optimizer mirror (optimizer.hpp): learning-rate schedules (host arithmetic, as
-in the reference) and OptimizerState::apply on the device (tgb_optimizer_apply),
-bit-identical to the reference's float/double operation order."""
+"""Optimizer mirror (optimizer.hpp:60-125): OptimizerState::apply on the device
+(tgb_optimizer_apply, and fused into the decode by tgb_step_apply), bit-identical to
+the reference's float/double operation order. (Learning-rate schedules,
+optimizer.hpp:15-55, are outside the hot path: callers pass the step's rate.)"""
 from __future__ import annotations
 
 import ctypes as C
-import math
 from dataclasses import dataclass
 from enum import IntEnum
 from typing import List, Optional, Sequence, Union
@@ -14,44 +14,6 @@ import torch
 from . import _lib
 from ._lib import check, load
 from .codec import GradTensor, _dev, _stream
-
-
-class ScheduleKind(IntEnum):
-    Constant = 0
-    Polynomial = 1
-    Staircase = 2
-
-
-@dataclass
-class LrSchedule:
-    """optimizer.hpp:15-55"""
-
-    kind: ScheduleKind = ScheduleKind.Constant
-    base: float = 0.1
-    power: float = 0.5
-    max_iter: int = 1
-    factor: float = 0.1
-    step: int = 1
-
-    @staticmethod
-    def constant(base: float) -> "LrSchedule":
-        return LrSchedule(ScheduleKind.Constant, base)
-
-    @staticmethod
-    def polynomial(base: float, power: float, max_iter: int) -> "LrSchedule":
-        return LrSchedule(ScheduleKind.Polynomial, base, power=power, max_iter=max_iter)
-
-    @staticmethod
-    def staircase(base: float, factor: float, step: int) -> "LrSchedule":
-        return LrSchedule(ScheduleKind.Staircase, base, factor=factor, step=step)
-
-    def lr(self, t: int) -> float:
-        if self.kind == ScheduleKind.Polynomial:
-            tc = min(t, self.max_iter)
-            return self.base * math.pow(1.0 - tc / self.max_iter, self.power)
-        if self.kind == ScheduleKind.Staircase:
-            return self.base * math.pow(self.factor, float(t // self.step))
-        return self.base
 
 
 class OptimizerRule(IntEnum):

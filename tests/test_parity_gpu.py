@@ -369,12 +369,15 @@ def test_passthrough_and_bucket_errors():
         tg.average([res.encoded], 1, True)
 
 
-def test_step_host_matches_device_step(restated):
-    # tgb_step_host (host buffers in/out, copy streams) == tgb_step on device buffers
+@pytest.mark.parametrize("schedule", ["auto", "groups"])
+def test_step_host_matches_device_step(restated, schedule):
+    # tgb_step_host (host buffers in/out, copy streams; "groups": the per-layer-group
+    # pipelined H2D -> compute -> D2H) == tgb_step on device buffers
     names = ["conv.weight", "conv.bias", "fc.weight"]
     ns = [1728, 64, 40003]
     cfg = tg.CodecConfig(seed=42)
-    w = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
+    w = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV, schedule=schedule)
+    assert w.plan.grouped == (schedule == "groups")
     hin, hin_v, hout, hout_v = w.host_buffers()
     ref = tg.SyncWorker(names, [[n] for n in ns], cfg, device=DEV)
     for t in range(3):
@@ -391,6 +394,23 @@ def test_step_host_matches_device_step(restated):
             assert o.cpu().numpy().tobytes() == h.numpy().tobytes()
     with pytest.raises(ValueError):
         w.step_host(9, [h[:1] for h in hin_v], hout_v)
+    # back-to-back steps, no synchronisation between them: every step reads its own
+    # inputs and writes its own outputs (the copy streams' events order the reuse)
+    sets = [w.host_buffers() for _ in range(3)]
+    for k, (_, iv, _, _) in enumerate(sets):
+        for v, nm, n in zip(iv, names, ns):
+            v.copy_(torch.from_numpy(restated.normal(50 + k, 0, "host/" + nm, n, 1e-3)))
+    for k, (_, iv, _, ov) in enumerate(sets):
+        w.step_host(20 + k, iv, ov)
+    torch.cuda.synchronize()
+    w.check()
+    for k, (_, iv, _, ov) in enumerate(sets):
+        for v, h in zip(ref.grads, iv):
+            v.copy_(h.to(DEV))
+        outs = ref.step(20 + k)
+        torch.cuda.synchronize()
+        for o, h in zip(outs, ov):
+            assert o.cpu().numpy().tobytes() == h.numpy().tobytes(), k
 
 
 def test_histogram_vs_reference(restated):
