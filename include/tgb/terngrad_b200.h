@@ -103,7 +103,8 @@ typedef struct tgb_plan_info {
     int32_t exchange;     /* TGB_EXCHANGE_*: how tgb_step moves data between ranks */
 } tgb_plan_info;
 
-#define TGB_EXCHANGE_AUTO (-1) /* tgb_plan_set_option: fused for N <= 4, sharded from N = 5 */
+#define TGB_EXCHANGE_AUTO (-1) /* tgb_plan_set_option: sharded from N = 5 for sets of >= 16 Mi
+                                  elements, else fused */
 #define TGB_EXCHANGE_NONE 0    /* n_workers == 1 */
 #define TGB_EXCHANGE_NCCL 1    /* ncclAllGather of push buffers, K3 on every rank */
 #define TGB_EXCHANGE_FUSED 2   /* K1/K2 store scalers + codes into every peer (NVLink) */

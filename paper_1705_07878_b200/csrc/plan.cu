@@ -104,12 +104,14 @@ static tgb_status build_schedule(tgb_plan* P) {
     if (P->chunk_opt) chunk = static_cast<uint64_t>(P->chunk_opt);
     P->chunk12 = static_cast<uint32_t>(chunk);
     P->chunk3 = kChunk3;
-    // sharded exchange: from N >= 5 by default (measured at N = 4 the fused
-    // two-group schedule wins), or forced by the option
+    // sharded exchange: by default from N >= 5 for sets of >= 16 Mi elements, where
+    // the fused exchange's (N-1)/4 B per element of NVLink traffic dominates (measured
+    // at N = 4 the fused two-group schedule still wins); small sets
+    // are latency-bound and the sharded path's second cross-GPU barrier only costs
     P->shard = false;
     if (N >= 2 && N <= kMaxPeers && P->p.scaler_sharing)
         P->shard = P->exchange_opt == TGB_EXCHANGE_SHARDED ||
-                   (P->exchange_opt == TGB_EXCHANGE_AUTO && N >= 5);
+                   (P->exchange_opt == TGB_EXCHANGE_AUTO && N >= 5 && P->total >= (16ull << 20));
 
     // ---- FixedSize(k), k = 2^p in [64, chunk): work items of whole buckets (k/4 code
     // bytes, a 16-B multiple, so a run of buckets is contiguous in the push area and

@@ -132,13 +132,13 @@ def test_alexnet_n2_bit_exact(reference):
 @pytest.mark.timeout(900)
 def test_googlenet_n8_bit_exact(reference):
     """BASELINE configs[2]: GoogLeNet (173 tensors), 8 workers with scaler sharing:
-    the default (sharded) exchange and the fused one."""
-    rep = _local_cluster_vs_reference(reference, "googlenet", 8, ["auto", "fused"])
+    the default (fused, for a small set) exchange and the sharded one."""
+    rep = _local_cluster_vs_reference(reference, "googlenet", 8, ["auto", "sharded"])
     for ex, r in rep.items():
         assert r["workers_identical"], ex
         assert not r["mismatch"], (ex, r)
-    assert rep["auto"]["exchange"] == "sharded"
-    assert rep["fused"]["exchange"] == "fused"
+    assert rep["auto"]["exchange"] == "fused"  # a small set: sharded only from 16 Mi elements
+    assert rep["sharded"]["exchange"] == "sharded"
 
 
 @pytest.mark.timeout(1800)

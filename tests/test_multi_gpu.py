@@ -44,7 +44,7 @@ def test_mp_check(n, exchange):
     for k, v in rep["checks"].items():
         assert v["ranks_identical"], k
         assert v["matches_oracle"] in (True, None), k
-    for k in ("alexnet_full_set", "vgg16_full_set"):
+    for k in ("googlenet_full_set", "alexnet_full_set", "vgg16_full_set"):
         assert rep["checks"][k]["matches_oracle"] is True, k
     if exchange != "nccl":
         assert "iteration_skew" in rep["checks"] and "block_structure_mismatch" in rep["checks"]

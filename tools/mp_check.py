@@ -43,11 +43,11 @@ def ex_for(sharing):
 
 
 def full_set_checks(report, rank, ws, comm, dev):
-    """AlexNet and VGG-16 full sets vs the reference's own sync path (RefCluster)"""
+    """GoogLeNet, AlexNet and VGG-16 full sets vs the reference's own sync path (RefCluster)"""
     import numpy as np
     from oracle.oracle import Config, RefCluster, Reference
 
-    for set_name in ("alexnet", "vgg16"):
+    for set_name in ("googlenet", "alexnet", "vgg16"):
         layers = tg.layersets.get(set_name)
         names, shapes = [n for n, _ in layers], [s for _, s in layers]
         ns = [tg.layersets.numel(s) for s in shapes]
