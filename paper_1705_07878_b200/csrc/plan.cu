@@ -1454,7 +1454,6 @@ tgb_status tgb_step_host(tgb_plan* P, tgb_comm* C, uint64_t t, const float* cons
                 TGB_CUDA(cudaEventRecord(P->ev_cg[g], st));
                 TGB_CUDA(cudaEventRecord(P->ev_dg[g], st));
             }
-        TGB_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_d2h, 0));  // (first call ordering)
         for (int g = 0; g < 2; ++g) {  // the small group first: its compute starts early
             TGB_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_cg[g], 0));  // previous K2 read them
             TGB_TRY(copy_runs(P, reinterpret_cast<const float* const*>(P->bound_g.data()),
