@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "sharded", "nccl"])
     ap.add_argument("--pieces", type=int, default=0, help="exchange pieces (0 = auto)")
     ap.add_argument("--overlap", type=int, default=-1, help="overlapped exchange: -1 auto, 0, 1")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "single", "groups"],
+                    help="layer-group schedule (auto: dominant tensor || the rest)")
+    ap.add_argument("--pull", type=int, default=0,
+                    help="split exchange: eighths of the codes the decode pulls (0..8)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU time budget of the in-line cpu_baseline (at least one full step)")
@@ -283,7 +287,8 @@ def run_b200(args):
     cfg = tg.CodecConfig(seed=42)
     sw = tg.SyncWorker(names, shapes, cfg, rank=rank, world_size=ws, comm=comm, device=dev,
                        exchange=args.exchange, pieces=args.pieces,
-                       overlap=None if args.overlap < 0 else bool(args.overlap))
+                       overlap=None if args.overlap < 0 else bool(args.overlap),
+                       pull=args.pull, schedule=args.schedule)
     ns = sw.ns
     n = sum(ns)
     plan = sw.plan
@@ -339,14 +344,23 @@ def run_b200(args):
 
     def soak(seconds, t0):
         # untimed steps around the timed region so nvidia-smi (100 ms period)
-        # samples the clocks under this exact load
+        # samples the clocks under this exact load. Every rank must run the SAME number
+        # of steps (each step is a cross-rank exchange): the ranks agree after each batch
+        # of 20 whether to run another (a rank-local clock test here let one rank
+        # enqueue a batch its peers never joined -- every barrier then waits out its
+        # ~10 s timeout)
         end = time.time() + seconds
         t = t0
-        while time.time() < end:
+        while True:
             for _ in range(20):
                 one_step(t)
                 t += 1
             torch.cuda.synchronize(dev)
+            more = torch.tensor([1 if time.time() < end else 0], dtype=torch.int32)
+            if ws > 1:
+                dist.all_reduce(more, op=dist.ReduceOp.MAX)
+            if not int(more.item()):
+                break
 
     e_start = torch.cuda.Event(enable_timing=True)
     e_stop = torch.cuda.Event(enable_timing=True)
@@ -586,6 +600,9 @@ def run_b200(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if args.pull or args.pieces or args.overlap >= 0 or args.schedule != "auto":
+            line["config"].update(pull=args.pull, pieces=args.pieces, overlap=args.overlap,
+                                  schedule=args.schedule)
         print(json.dumps(line), flush=True)
     barrier()  # fused exchange: no rank frees a gather buffer a peer may still write
     sw.plan.close()

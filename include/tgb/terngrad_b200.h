@@ -176,6 +176,11 @@ tgb_status tgb_plan_block_info(const tgb_plan* plan, int32_t block, tgb_block_in
  *   decode of piece p (fused: K3; sharded: owner reduce -> barrier -> decode) overlaps K2
  *   of the later pieces (replaces the two-group schedule); before attaching. */
 #define TGB_PLAN_OPT_OVERLAP 5
+/* TGB_PLAN_OPT_PULL: fused exchange with shared scalers, 0..8 (default 0): that many
+ *   eighths of the code items (32K-element granules) are not stored to the peers by K2;
+ *   every rank's decode reads them from their owner's memory over NVLink, moving that
+ *   part of the exchange from the K2 stores to the K3 loads; before attaching. */
+#define TGB_PLAN_OPT_PULL 6
 #define TGB_SCHEDULE_AUTO 0
 #define TGB_SCHEDULE_SINGLE 1
 #define TGB_SCHEDULE_GROUPS 2

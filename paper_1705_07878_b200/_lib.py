@@ -40,6 +40,7 @@ TGB_PLAN_OPT_SCHEDULE, TGB_PLAN_OPT_EXCHANGE, TGB_PLAN_OPT_FUSED_OPTIMIZER = 0, 
 TGB_PLAN_OPT_PIECES = 3
 TGB_PLAN_OPT_CHUNK = 4
 TGB_PLAN_OPT_OVERLAP = 5
+TGB_PLAN_OPT_PULL = 6
 TGB_SCHEDULE_AUTO, TGB_SCHEDULE_SINGLE, TGB_SCHEDULE_GROUPS = 0, 1, 2
 TGB_SCHEDULE_UNFUSED, TGB_SCHEDULE_FUSED12 = 3, 4
 

@@ -242,6 +242,9 @@ struct K2Args {
     // publishes this rank's barrier record {epoch, t} for slot q to every rank, so the
     // decode of piece q starts while K2 still computes the later pieces. Sharded: the
     // owner of item b is r with owner_bounds[q][r] <= b < owner_bounds[q][r+1].
+    // split exchange (pulled_item): such items are stored only into this rank's own area
+    uint32_t pull8 = 0;
+    int32_t rank = 0;
     int32_t n_pieces = 0;
     uint32_t piece_bounds[kMaxPieces + 1];
     uint32_t owner_bounds[kMaxPieces][kMaxPeers + 1];
@@ -420,10 +423,23 @@ __device__ __forceinline__ void k2_passthrough(const K2Args& a, const LayerDev& 
 }
 
 // destinations of chunk b's codes: [p0, p1) of a.dst (a.push when a.dst.n == 0)
-__device__ __forceinline__ void k2_dst_range(const K2Args& a, uint32_t b, int& p0, int& p1) {
+// split exchange: code items of 32K-element granule (block, begin >> 15) with
+// (block + granule) % 8 < pull8 are pulled by the decode over NVLink instead of pushed
+// by K2. K2 items and K3 items are power-of-two aligned inside a block, both <= 32K
+// elements, so both kernels classify every element alike.
+__device__ __forceinline__ bool pulled_item(uint32_t pull8, const ChunkDev& ch,
+                                            const LayerDev& L) {
+    return pull8 && !(L.flags & (kLayerPassthrough | kLayerMultiBucket)) &&
+           ((ch.layer + (ch.begin >> 15)) & 7u) < pull8;
+}
+
+__device__ __forceinline__ void k2_dst_range(const K2Args& a, uint32_t b, const ChunkDev& ch,
+                                             const LayerDev& L, int& p0, int& p1) {
     p0 = 0;
     p1 = a.dst.n == 0 ? 1 : a.dst.n;
     if (a.dst.n && a.shard_n) p1 = (p0 = shard_owner(a, b)) + 1;  // sharded: owner only
+    // a pulled item stays in this rank's own area; the peers' K3 reads it from there
+    if (a.dst.n && pulled_item(a.pull8, ch, L)) p1 = (p0 = a.rank) + 1;
 }
 __device__ __forceinline__ uint8_t* k2_dst(const K2Args& a, int p) {
     return a.dst.n == 0 ? a.push : a.dst.base[p];
@@ -803,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
     if (nbytes) {
         const uint64_t off = L.code_off + (ch.begin >> 2);
         int p0, p1;
-        k2_dst_range(a, b, p0, p1);
+        k2_dst_range(a, b, ch, L, p0, p1);
         bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
     }
     if (a.n_pieces) piece_done(a, b);
@@ -860,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, 4) k12_fused(TableSource src, K1Out 
         if (nbytes) {
             const uint64_t off = L.code_off + (ch.begin >> 2);
             int p0, p1;
-            k2_dst_range(a, b, p0, p1);
+            k2_dst_range(a, b, ch, L, p0, p1);
             bulk_copy_out(stage, [&](int p) { return k2_dst(a, p0 + p) + off; }, p1 - p0, nbytes);
         }
         __syncthreads();  // the bulk copy finished reading `stage` (thread 0 waited for it)
@@ -946,6 +962,10 @@ struct K3Args {
     const OptDev* optd = nullptr;  // fused decode -> optimizer (kOpt kernels)
     OptArgs opt{};
     int32_t gate = 0;              // plan exchange: skip when the step's exchange failed
+    // split exchange (staged kernel): the codes of worker w are read from wsrc[w] (its own
+    // push area in its own memory, over NVLink) instead of the local gather buffer
+    uint32_t pull8 = 0;
+    const uint8_t* wsrc[kMaxPeers];
 };
 
 struct K3Ptrs {  // per-layer API: explicit pointers (passed by value)
@@ -1114,13 +1134,14 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
     const uint32_t count = ch.count;
     const uint32_t nbytes = (count + 3) >> 2;
     const uint32_t n16 = nbytes >> 4;
+    const bool pull = pulled_item(a.pull8, ch, L);
     {
         uint4 v[NW][kStage / 16 / kThreads > 0 ? kStage / 16 / kThreads : 1];
         constexpr int R = kStage / 16 / kThreads > 0 ? kStage / 16 / kThreads : 1;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            const uint4* b4 = reinterpret_cast<const uint4*>(a.src + a.stride * w + L.code_off +
-                                                             (ch.begin >> 2));
+            const uint4* b4 = reinterpret_cast<const uint4*>(
+                (pull ? a.wsrc[w] : a.src + a.stride * w) + L.code_off + (ch.begin >> 2));
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const uint32_t i = tid + r * kThreads;
@@ -1138,7 +1159,8 @@ __global__ void __launch_bounds__(kThreads) k3_decode_staged(TableSource src, K3
         for (uint32_t i = (n16 << 4) + tid; i < nbytes; i += kThreads)
 #pragma unroll
             for (int w = 0; w < NW; ++w)
-                codes[w][i] = a.src[a.stride * w + L.code_off + (ch.begin >> 2) + i];
+                codes[w][i] = (pull ? a.wsrc[w] : a.src + a.stride * w)[L.code_off +
+                                                                        (ch.begin >> 2) + i];
     }
     // multi-bucket item: s = max over workers per bucket (bucket of byte q: q >> shq)
     __shared__ float smax_b[kChunk3 / 64];
@@ -1534,6 +1556,8 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     a.pdl = p.pdl;
     a.keep_from = p.keep_from;
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
+    a.pull8 = p.pull8;
+    a.rank = p.rank;
     a.n_pieces = p.n_pieces;
     if (p.n_pieces) {
         for (int q = 0; q <= kMaxPieces; ++q) a.piece_bounds[q] = p.piece_bounds[q];
@@ -1624,8 +1648,11 @@ cudaError_t launch_k3_table(const LayerDev* layers, const ChunkFat* chunks, uint
     if (n_chunks == 0) return cudaSuccess;
     K3Args a{p.src, p.stride, nullptr, nullptr, 0.0f, p.n_workers, p.sharing, p.inv_n, p.err};
     a.gate = p.gate;
+    a.pull8 = p.pull8;
+    for (int w = 0; w < kMaxPeers; ++w) a.wsrc[w] = p.wsrc[w];
     K3Ptrs ptrs{};
     const TableSource src{chunks};
+    if (p.pull8 && !(p.sharing && p.n_workers <= kMaxPeers)) return cudaErrorInvalidValue;
     if (p.sharing && p.n_workers <= kMaxPeers) {  // staged SWAR kernel (fused optimizer optional)
         if (p.optd) {
             a.optd = p.optd;

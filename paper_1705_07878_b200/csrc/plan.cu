@@ -176,12 +176,19 @@ static tgb_status build_schedule(tgb_plan* P) {
     for (int32_t l = 0; l < n_layers; ++l)
         if (!(layers[l].flags & TGB_LAYER_PASSTHROUGH) && (big < 0 || layers[l].n > layers[big].n))
             big = l;
-    const bool can_group = !P->shard && big >= 0 && n_layers > 1 &&
+    // (the sharded exchange runs each group as one piece: pieces_opt > 1 keeps it ungrouped)
+    const bool can_group = !(P->shard && P->pieces_opt > 1) && big >= 0 && n_layers > 1 &&
                            P->p.bucketing == TGB_BUCKET_PER_TENSOR &&
                            P->p.share_mode == TGB_SHARE_REF;
     // overlapped exchange: N > 1, REF (PRESHARED's allreduce sits between K1 and K2)
     P->overlap = N > 1 && N <= kMaxPeers && P->p.share_mode == TGB_SHARE_REF &&
                  P->overlap_opt == 1;
+    // split exchange (fused exchange, shared scalers: the staged decode; no multi-bucket
+    // items): K3 pulls pull_opt/8 of the code items from the peers' own areas
+    P->pull8 = (N > 1 && N <= kMaxPeers && !P->shard && !P->overlap && P->p.scaler_sharing &&
+                P->mb_log2 == 0)
+                   ? static_cast<uint32_t>(P->pull_opt)
+                   : 0u;
     bool want = can_group && !P->overlap && layers[big].n * 100 >= P->total * 35 &&
                 layers[big].n * 100 <= P->total * 95;
     if (P->schedule_opt == TGB_SCHEDULE_SINGLE || P->schedule_opt == TGB_SCHEDULE_UNFUSED ||
@@ -350,12 +357,14 @@ static tgb_status build_schedule(tgb_plan* P) {
         const uint64_t W = cum.back();
         int np = P->pieces_opt > 0 ? P->pieces_opt : (P->overlap ? 4 : 1);
         np = std::max(1, std::min(np, std::min(kMaxPieces, static_cast<int>(P->h_chunks.size()))));
+        if (P->grouped) np = 2;  // piece g = layer group g (each runs on its own stream)
         P->n_pieces = np;
         auto cut = [&](uint64_t target) {
             return static_cast<uint32_t>(std::lower_bound(cum.begin(), cum.end(), target) -
                                          cum.begin());
         };
         for (int q = 0; q <= np; ++q) P->pb[q] = cut(W * static_cast<uint64_t>(q) / np);
+        if (P->grouped) P->pb[1] = P->cb[1];
         P->pb[np] = static_cast<uint32_t>(P->h_chunks.size());
         // owners inside each piece: rank r owns [pcs[q][r], pcs[q][r+1])
         for (int q = 0; q < np; ++q) {
@@ -663,6 +672,11 @@ tgb_status tgb_plan_set_option(tgb_plan* P, int32_t option, int64_t value) {
             if (P->attached) return TGB_ERR_UNSUPPORTED;
             P->pieces_opt = static_cast<int32_t>(value);
             break;
+        case TGB_PLAN_OPT_PULL:
+            if (value < 0 || value > 8) return TGB_ERR_INVALID_ARGUMENT;
+            if (P->attached) return TGB_ERR_UNSUPPORTED;
+            P->pull_opt = static_cast<int32_t>(value);
+            break;
         case TGB_PLAN_OPT_FUSED_OPTIMIZER:
             if (value != 0 && value != 1) return TGB_ERR_INVALID_ARGUMENT;
             P->opt_fused = value != 0;
@@ -726,11 +740,20 @@ uint8_t* cur_gathered(const tgb_plan* P) {
 static inline int n_groups(const tgb_plan* P) { return P->grouped ? 2 : 1; }
 
 // ---- live kernel timing: events around each launch on its own stream
+// host form of pulled_item (kernels.cu)
+static bool pulled(const tgb_plan* P, const ChunkDev& ch) {
+    return P->pull8 && !(P->h_layers[ch.layer].flags & (kLayerPassthrough | kLayerMultiBucket)) &&
+           ((ch.layer + (ch.begin >> 15)) & 7u) < P->pull8;
+}
+
+// elements of chunks [b, b + c): out[0] ternary, out[1] passthrough, out[2] pulled
 static void chunk_elems(const tgb_plan* P, const std::vector<ChunkDev>& chs, uint32_t b,
-                        uint32_t c, uint64_t out[2]) {
-    out[0] = out[1] = 0;
-    for (uint32_t i = b; i < b + c && i < chs.size(); ++i)
+                        uint32_t c, uint64_t out[3]) {
+    out[0] = out[1] = out[2] = 0;
+    for (uint32_t i = b; i < b + c && i < chs.size(); ++i) {
         out[(P->h_layers[chs[i].layer].flags & kLayerPassthrough) ? 1 : 0] += chs[i].count;
+        if (pulled(P, chs[i])) out[2] += chs[i].count;
+    }
 }
 
 static int t_begin(tgb_plan* P, cudaStream_t st) {
@@ -772,7 +795,7 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
         TGB_CUDA(launch_k1_bucket_slots(P->d_layers, P->d_bmeta,
                                         static_cast<uint32_t>(P->h_layers.size()), k, st));
     if (ts >= 0) {
-        uint64_t e[2];
+        uint64_t e[3];
         chunk_elems(P, P->h_chunks, b, P->ck1[g], e);
         t_end(P, st, ts, TGB_KERNEL_K1, g, e[0], 4 * e[0], 0);
     }
@@ -797,6 +820,8 @@ static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc
         for (int p = 0; p < P->n_workers; ++p) k.dst.base[p] = push_area(P, p);
         k.dst.n = P->n_workers;
         k.dst.remote = 1;
+        k.pull8 = P->pull8;
+        k.rank = P->rank;
         if (P->shard) {
             k.shard_n = P->n_workers;
             if (piece >= 0)
@@ -819,7 +844,7 @@ static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k2_table(P->d_layers, P->d_fat + cb, cc, k, st));
     if (ts >= 0) {
-        uint64_t e[2];
+        uint64_t e[3];
         chunk_elems(P, P->h_chunks, cb, cc, e);
         const uint64_t nt = e[0], np = e[1], N = P->n_workers;
         const uint64_t msg = (nt + 3) / 4 + 4 * np;  // code bytes + raw passthrough bytes
@@ -828,7 +853,7 @@ static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc
             own_b = msg / N;
             nvl = msg - own_b;
         } else if (P->attached) {
-            nvl = (N - 1) * msg;
+            nvl = (N - 1) * (msg - e[2] / 4);  // pulled items stay local
         }
         const uint64_t out = fuse_decode ? 4 * (nt + np) : 0;
         t_end(P, st, ts, TGB_KERNEL_K2, g, nt + np, 4 * (nt + np) + own_b + out, nvl);
@@ -887,7 +912,7 @@ static tgb_status launch_k12(tgb_plan* P, uint64_t t, cudaStream_t st, bool fuse
     TGB_CUDA(launch_k12_table(P->d_layers, P->d_fat, P->ck1[0], P->cc[0], k1, k2, P->d_ready,
                               P->k12_epoch, st));
     if (ts >= 0) {
-        uint64_t e[2];
+        uint64_t e[3];
         chunk_elems(P, P->h_chunks, 0, P->cc[0], e);
         const uint64_t nt = e[0], np = e[1], N = P->n_workers;
         const uint64_t msg = (nt + 3) / 4 + 4 * np;
@@ -937,6 +962,12 @@ static tgb_status launch_decode_range(tgb_plan* P, int g, uint32_t cb3, uint32_t
     K3Launch k{src, P->push_bytes, n_workers, P->p.scaler_sharing ? 1 : 0,
                1.0f / static_cast<float>(n_workers), P->d_err};
     k.gate = P->attached ? 1 : 0;
+    if (P->attached && P->pull8) {  // worker w's pulled items: its own area, its memory
+        k.pull8 = P->pull8;
+        const uint64_t g = P->push_bytes * static_cast<uint64_t>(P->n_workers);
+        for (int w = 0; w < P->n_workers; ++w)
+            k.wsrc[w] = P->peer_ipc[w] + (P->epoch & 1u) * g + static_cast<uint64_t>(w) * P->push_bytes;
+    }
     if (P->opt_active) {
         k.optd = P->d_optd;
         k.opt = *P->opt_active;
@@ -944,11 +975,13 @@ static tgb_status launch_decode_range(tgb_plan* P, int g, uint32_t cb3, uint32_t
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k3_table(P->d_layers, P->d_fat3 + cb3, cc3, k, st));
     if (ts >= 0) {
-        uint64_t e[2];
+        uint64_t e[3];
         chunk_elems(P, P->h_chunks3, cb3, cc3, e);
         const uint64_t nt = e[0], np = e[1], N = n_workers;
+        const uint64_t pulled_b = k.pull8 ? (N - 1) * (e[2] / 4) : 0;
         t_end(P, st, ts, TGB_KERNEL_K3, g, nt + np,
-              N * ((nt + 3) / 4 + 4 * np) + (P->opt_active ? 0 : 4 * (nt + np)), 0);
+              N * ((nt + 3) / 4 + 4 * np) - pulled_b + (P->opt_active ? 0 : 4 * (nt + np)),
+              pulled_b);
     }
     return TGB_OK;
 }
@@ -990,7 +1023,7 @@ static tgb_status launch_shard_reduce(tgb_plan* P, int q, cudaStream_t st) {
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k3_reduce(P->d_fat + c0, c1 - c0, shard_launch(P), st));
     if (ts >= 0) {
-        uint64_t e[2];
+        uint64_t e[3];
         chunk_elems(P, P->h_chunks, c0, c1 - c0, e);
         const uint64_t N = P->n_workers;
         const uint64_t out = radix_bytes(P, e[0]) + 4 * e[1];
@@ -1006,7 +1039,7 @@ static tgb_status launch_shard_expand(tgb_plan* P, int q, cudaStream_t st) {
     const int ts = t_begin(P, st);
     TGB_CUDA(launch_k3_expand(P->d_fat + c0, n, shard_launch(P), st));
     if (ts >= 0) {
-        uint64_t e[2];
+        uint64_t e[3];
         chunk_elems(P, P->h_chunks, c0, n, e);
         t_end(P, st, ts, TGB_KERNEL_K3B, 0, e[0] + e[1],
               radix_bytes(P, e[0]) + 4 * e[1] + 4 * (e[0] + e[1]), 0);
@@ -1032,6 +1065,7 @@ tgb_status tgb_ternarize_pack(tgb_plan* P, uint64_t t, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     P->last = st;
     P->last_t = t;  // published with the step barrier (iteration-skew check)
+    if (P->attached && P->shard) return launch_tern(P, 0, t, st);  // every piece
     for (int g = 0; g < n_groups(P); ++g) TGB_TRY(launch_tern(P, g, t, st));
     return TGB_OK;
 }
@@ -1159,6 +1193,22 @@ tgb_status tgb_step(tgb_plan* P, tgb_comm* C, uint64_t t, void* stream) {
         // caller's prior work), piece q's barrier -> K3a -> barrier -> K3b
         ++P->epoch;
         TGB_CUDA(cudaEventRecord(P->ev_fork, st));
+        if (P->grouped) {  // piece g = group g, each chain on its own stream
+            for (int g = 1; g >= 0; --g) {
+                cudaStream_t gs = P->gs[g];
+                TGB_CUDA(cudaStreamWaitEvent(gs, P->ev_fork, 0));
+                TGB_TRY(launch_stats(P, g, gs));
+                TGB_TRY(launch_tern_range(P, g, P->pb[g], P->pb[g + 1] - P->pb[g], g, t, gs, false));
+                TGB_TRY(launch_barrier(P, 2 * g, gs, kBarrierSpin));
+                TGB_TRY(launch_shard_reduce(P, g, gs));
+                TGB_TRY(launch_barrier(P, 2 * g + 1, gs, kBarrierSpin));
+                TGB_TRY(launch_shard_expand(P, g, gs));
+                TGB_CUDA(cudaEventRecord(P->ev_join[g], gs));
+            }
+            TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[0], 0));
+            TGB_CUDA(cudaStreamWaitEvent(st, P->ev_join[1], 0));
+            return TGB_OK;
+        }
         TGB_TRY(launch_stats(P, 0, st));
         TGB_CUDA(cudaStreamWaitEvent(P->gs3, P->ev_fork, 0));
         for (int q = 0; q < P->n_pieces; ++q) {
@@ -1302,9 +1352,11 @@ tgb_status tgb_local_step(tgb_plan* const* plans, int32_t n, const uint64_t* t,
             tgb_plan* P = plans[w];
             cudaStream_t st = st_of(w);
             if (!on(w)) return fail(TGB_ERR_CUDA);
-            tgb_status s = preshared ? TGB_OK
-                           : P->k12  ? launch_encode(P, t[w], st, false)
-                                     : launch_stats(P, 0, st);
+            tgb_status s = TGB_OK;
+            if (P->k12 && !preshared)
+                s = launch_encode(P, t[w], st, false);
+            else if (!preshared)
+                for (int g = 0; g < n_groups(P) && s == TGB_OK; ++g) s = launch_stats(P, g, st);
             if (s == TGB_OK && !P->k12) s = launch_tern(P, 0, t[w], st);
             for (int q = 0; q < P->n_pieces && s == TGB_OK; ++q)
                 s = launch_barrier(P, 2 * q, st, kBarrierPost);
@@ -1515,7 +1567,8 @@ static PlanDesc make_desc(const tgb_plan* P) {
     d.shard = P->shard;
     d.grouped = P->grouped;
     d.radix_m = P->radix_m;
-    d.reserved = static_cast<int32_t>(P->mb_log2) | (P->n_pieces << 8) | (P->overlap << 16);
+    d.reserved = static_cast<int32_t>(P->mb_log2) | (P->n_pieces << 8) | (P->overlap << 16) |
+                 static_cast<int32_t>(P->pull8 << 20);
     uint64_t h = 0xcbf29ce484222325ull;
     for (size_t b = 0; b < P->h_layers.size(); ++b) {
         const LayerDev& L = P->h_layers[b];

@@ -76,6 +76,8 @@ struct K2Launch {
     int32_t fuse_decode = 0;    // N == 1 step: K2 also writes the decoded output (K3 fused)
     int32_t pdl = 0;            // K2 as K1's programmatic dependent (1), + L2 prefetch (2, 3)
     uint32_t keep_from = ~0u;   // work items K1 loaded evict_last (demoted by K2)
+    uint32_t pull8 = 0;  // split exchange: see pulled_item (kernels.cu)
+    int32_t rank = 0;
     // overlapped exchange (n_pieces > 0): see K2Args
     int32_t n_pieces = 0;
     uint32_t piece_bounds[kMaxPieces + 1] = {};
@@ -97,6 +99,8 @@ struct K3Launch {
     const OptDev* optd = nullptr;  // fused decode -> optimizer (staged kernel, N <= 8)
     OptArgs opt{};
     int32_t gate = 0;  // skip the decode when the step's exchange failed (skew / timeout)
+    uint32_t pull8 = 0;  // split exchange: pulled items of worker w at wsrc[w] (its memory)
+    const uint8_t* wsrc[kMaxPeers] = {};
 };
 
 struct ShardLaunch {

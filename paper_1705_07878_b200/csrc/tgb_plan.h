@@ -110,6 +110,8 @@ struct tgb_plan {
     uint32_t p3[kMaxPieces + 1] = {};
     uint32_t* d_piece_cnt = nullptr;
     int32_t pieces_opt = 0;  // TGB_PLAN_OPT_PIECES (0: auto)
+    int32_t pull_opt = 0;    // TGB_PLAN_OPT_PULL (eighths of the code items pulled by K3)
+    uint32_t pull8 = 0;      // effective split (0: every item pushed by K2)
     int32_t chunk_opt = 0;   // TGB_PLAN_OPT_CHUNK (0: auto)
     int32_t n_pieces = 1;
     uint32_t pb[kMaxPieces + 1] = {};

@@ -171,6 +171,11 @@ class Plan:
         overlaps the later pieces' K2; before attaching"""
         self.set_option(_lib.TGB_PLAN_OPT_OVERLAP, 1 if on else 0)
 
+    def set_pull(self, eighths: int):
+        """fused exchange: eighths (0..8) of the code items the decode pulls from the
+        peers' memory instead of K2 storing them into every peer; before attaching"""
+        self.set_option(_lib.TGB_PLAN_OPT_PULL, int(eighths))
+
     def set_pieces(self, pieces: int):
         """sharded exchange: pieces of the K2 work list (0 = auto); before attaching"""
         self.set_option(_lib.TGB_PLAN_OPT_PIECES, int(pieces))
@@ -457,7 +462,7 @@ class SyncWorker:
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
                  rank: int = 0, world_size: int = 1, comm: Optional[Comm] = None, device=None,
                  exchange: str = "auto", schedule: str = "auto", pieces: int = 0,
-                 overlap: Optional[bool] = None):
+                 overlap: Optional[bool] = None, pull: int = 0):
         """exchange: "auto" | "fused" | "sharded" (NVLink peer stores, attached at
         construction) | "nccl" (ncclAllGather of push areas); schedule: see
         Plan.set_schedule."""
@@ -481,6 +486,8 @@ class SyncWorker:
             self.plan.set_overlap(overlap)
         if pieces:
             self.plan.set_pieces(pieces)
+        if pull and world_size > 1:
+            self.plan.set_pull(pull)
         self.grad_flat, self.grads = aligned_flat(self.ns, self.device)
         self.out_flat, self.outs = aligned_flat(self.ns, self.device)
         self.plan.bind(self.grads, self.outs)
@@ -553,7 +560,7 @@ class LocalCluster:
 
     def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]], cfg: CodecConfig,
                  n_workers: int, devices=None, exchange: str = "auto", schedule: str = "auto",
-                 pieces: int = 0, overlap: Optional[bool] = None):
+                 pieces: int = 0, overlap: Optional[bool] = None, pull: int = 0):
         if not isinstance(devices, (list, tuple)):
             devices = [devices] * n_workers
         self.devices = [_dev(d) for d in devices]
@@ -572,6 +579,8 @@ class LocalCluster:
                 p.set_overlap(overlap)
             if pieces:
                 p.set_pieces(pieces)
+            if pull and self.n_workers > 1:
+                p.set_pull(pull)
             gf, gv = aligned_flat(self.ns, dev)
             of, ov = aligned_flat(self.ns, dev)
             p.bind(gv, ov)

@@ -44,7 +44,10 @@ def small_checks(N, report):
     grads = [[R.normal(100 + w, 0, "mp/" + n, m, 1e-2) for n, m in zip(NAMES, SIZES)]
              for w in range(N)]
     # sharded3: 3 pieces of the K2 list; +ov: overlapped exchange (K2 publishes pieces)
-    for exchange in ("fused", "sharded", "sharded3", "fused+ov", "sharded+ov"):
+    # +pull: split exchange (K3 reads 3/8 of the code items from the peers' areas);
+    # +grp: the two-group schedule forced (PerTensor REF; sharded: one piece per group)
+    for exchange in ("fused", "sharded", "sharded3", "fused+ov", "sharded+ov", "fused+pull",
+                     "fused+grp", "sharded+grp"):
         for sharing, bucketing, k, pt_names in configs:
             if exchange.startswith("sharded") and not sharing:
                 continue
@@ -53,7 +56,9 @@ def small_checks(N, report):
             cl = tg.LocalCluster(NAMES, [[n] for n in SIZES], cfg, N, DEV,
                                  exchange=exchange.split("+")[0][:7],
                                  pieces=3 if exchange in ("sharded3", "sharded+ov", "fused+ov") else 0,
-                                 overlap=True if exchange.endswith("+ov") else None)
+                                 overlap=True if exchange.endswith("+ov") else None,
+                                 pull=3 if exchange.endswith("+pull") else 0,
+                                 schedule="groups" if exchange.endswith("+grp") else "auto")
             for w in range(N):
                 for v, g in zip(cl.grads[w], grads[w]):
                     if g.size:

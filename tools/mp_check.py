@@ -35,6 +35,7 @@ import paper_1705_07878_b200 as tg  # noqa: E402
 EXCHANGE = os.environ.get("TGB_EXCHANGE", "auto")
 _OV = os.environ.get("TGB_OVERLAP")  # tool-level switch: "1" overlapped exchange, "0" off
 OVERLAP = None if _OV is None else _OV == "1"
+PULL = int(os.environ.get("TGB_PULL", "0"))  # tool-level switch: split exchange eighths
 
 
 def ex_for(sharing):
@@ -57,7 +58,7 @@ def full_set_checks(report, rank, ws, comm, dev):
             return [rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3) for n in ns]
 
         sw = tg.SyncWorker(names, shapes, tg.CodecConfig(seed=42), rank=rank, world_size=ws,
-                           comm=comm, device=dev, exchange=EXCHANGE, overlap=OVERLAP)
+                           comm=comm, device=dev, exchange=EXCHANGE, overlap=OVERLAP, pull=PULL)
         for v, g in zip(sw.grads, grads_of(rank)):
             v.copy_(torch.from_numpy(g).to(dev))
         for t in (10, 11, 12):
@@ -138,7 +139,7 @@ def main():
     R = Restated()
     names = ["conv1.weight", "conv1.bias", "empty", "fc.weight", "fc.bias"]
     sizes = [1728, 64, 0, 40003, 10]
-    report = {"world_size": ws, "exchange": EXCHANGE, "overlap": OVERLAP, "checks": {}}
+    report = {"world_size": ws, "exchange": EXCHANGE, "overlap": OVERLAP, "pull": PULL, "checks": {}}
     P, G, F = tg.Bucketing.PerTensor, tg.Bucketing.Global, tg.Bucketing.FixedSize
     configs = [  # (sharing, mode, bucketing, k, passthrough names)
         (True, tg.ShareMode.REF, P, 0, ()), (False, tg.ShareMode.REF, P, 0, ()),
@@ -152,7 +153,7 @@ def main():
                              bucketing=bucketing, bucket_size=k, passthrough=set(pt_names))
         pt = [int(n in pt_names) for n in names]
         sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws, comm=comm,
-                           device=dev, exchange=ex_for(sharing), overlap=OVERLAP)
+                           device=dev, exchange=ex_for(sharing), overlap=OVERLAP, pull=PULL)
         grads = [R.normal(100 + rank, 0, "mp/" + n, k, 1e-2) for n, k in zip(names, sizes)]
         for v, g in zip(sw.grads, grads):
             if g.size:
@@ -189,9 +190,9 @@ def main():
         ocfg = tg.OptimizerConfig(rule=rule, weight_decay=1e-4)
         cfg = tg.CodecConfig(seed=42)
         sw = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws,
-                           comm=comm, device=dev, exchange=ex_for(True), overlap=OVERLAP)
+                           comm=comm, device=dev, exchange=ex_for(True), overlap=OVERLAP, pull=PULL)
         ref = tg.SyncWorker(names, [[n] for n in sizes], cfg, rank=rank, world_size=ws,
-                            comm=comm, device=dev, exchange=ex_for(True), overlap=OVERLAP)
+                            comm=comm, device=dev, exchange=ex_for(True), overlap=OVERLAP, pull=PULL)
         p0 = [torch.full((n,), 0.5, device=dev) for n in sizes]
         params = [x.clone() for x in p0]
         ref_params = [x.clone() for x in p0]
@@ -224,7 +225,7 @@ def main():
     layers = tg.layersets.get("vgg16")
     sw = tg.SyncWorker([n for n, _ in layers], [s for _, s in layers], tg.CodecConfig(seed=42),
                        rank=rank, world_size=ws, comm=comm, device=dev, exchange=ex_for(True),
-                       overlap=OVERLAP)
+                       overlap=OVERLAP, pull=PULL)
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     sw.grad_flat.normal_(0.0, 1e-3, generator=gen)
     st = torch.cuda.current_stream(dev)
