@@ -427,6 +427,33 @@ def run_b200(args):
         torch.cuda.synchronize(dev)
     live = plan_b.read_timing() if live_timing else []
     plan_b.enable_timing(0)
+    # K1 and the L2 it starts with (N = 1): right after a step, the L2 holds up to 126 MB
+    # of the previous decode's dirty output lines, written back while K1 streams the
+    # gradients; after a 256 MB read the L2 is clean. Same kernel, same grid.
+    k1_l2 = None
+    if N == 1 and live_timing:
+        flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+
+        def k1_after(prep):
+            es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(K)]
+            for k in range(K):
+                prep(k)
+                es[k][0].record(stream)
+                plan_b.stats()
+                es[k][1].record(stream)
+            torch.cuda.synchronize(dev)
+            return sum(x.elapsed_time(y) for x, y in es) / K
+
+        hbm_peak = peaks()[0]
+        ms_dirty = k1_after(lambda k: plan_b.step(60_000 + k))
+        ms_clean = k1_after(lambda k: (plan_b.step(70_000 + k), flush.sum()))
+        k1_l2 = {"after_step_ms": ms_dirty, "after_step_frac": 4.0 * n / (ms_dirty * 1e-3) / 1e9 / hbm_peak,
+                 "clean_l2_ms": ms_clean, "clean_l2_frac": 4.0 * n / (ms_clean * 1e-3) / 1e9 / hbm_peak,
+                 "note": "K1 alone (CUDA events), 4 B/elem read: right after a tgb_step (L2 full of "
+                         "the decode's dirty output, written back under K1's loads) vs after a "
+                         "256 MB read (clean L2)"}
+        del flush
     barrier()
     plan.raise_errors()
     stage = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(4)]
@@ -584,6 +611,7 @@ def run_b200(args):
                           "K3_decode": k3_ms, "sequential_step": staged_total / K,
                           "note": "per-kernel breakdown from a sequential pass; the headline "
                                   "ms_per_step is tgb_step (two-group overlap, N=1 fused decode)"},
+            "k1_l2_state": k1_l2,
             "kernels_sequential": {k: {"ms": v[1], "GB/s": v[0] / (v[1] * 1e-3) / 1e9,
                             "frac": v[0] / (v[1] * 1e-3) / 1e9 / hbm} for k, v in kb.items()},
             "gpu_launches": launches_per_step * K,
