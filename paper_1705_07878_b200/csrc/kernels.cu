@@ -86,16 +86,16 @@ constexpr uint32_t kMaxItemBuckets = kChunk12 / 64;  // k >= 64
 // in one bucket; lanes holding the same bucket (__match_any_sync) reduce with
 // one REDUX and their leader folds it into a shared-memory max per bucket, which
 // the CTA finally stores to bmax[block] (the item owns its buckets whole).
-template <int U>
-__device__ __forceinline__ void k1_unit_mb(const K1Out& o, const ChunkDev& ch, const LayerDev& L,
-                                           uint32_t unit) {
+template <int U, class Reload>
+__device__ __forceinline__ void k1_unit_mb(const K1Out& o, const ChunkDev& ch0, const LayerDev& L0,
+                                           uint32_t unit, Reload reload) {
     __shared__ uint32_t smax[kMaxItemBuckets];
     const uint32_t tid = threadIdx.x;
-    for (uint32_t j = tid; j < ch.nblk; j += kThreads) smax[j] = 0u;
+    for (uint32_t j = tid; j < ch0.nblk; j += kThreads) smax[j] = 0u;
     __syncthreads();
-    const float* g = L.g;
-    const uint32_t count = ch.count;
-    const uint32_t sh4 = bucket_log2(L) - 2;  // float4 index -> bucket
+    const float* g = L0.g;
+    const uint32_t count = ch0.count;
+    const uint32_t sh4 = bucket_log2(L0) - 2;  // float4 index -> bucket
     const double x0 = static_cast<double>(__ldg(g));
     double S = 0.0, Q = 0.0;
     float mx = 0.0f;
@@ -129,6 +129,10 @@ __device__ __forceinline__ void k1_unit_mb(const K1Out& o, const ChunkDev& ch, c
         atomicMax(smax + (e >> (sh4 + 2)), __float_as_uint(fabsf(x)));
     }
     __syncthreads();
+    asm volatile("" ::: "memory");  // re-read the descriptors (see k1_unit)
+    ChunkDev ch;
+    LayerDev L;
+    reload(ch, L);
     for (uint32_t j = tid; j < ch.nblk; j += kThreads) o.bmax[ch.layer + j] = smax[j];
     k1_emit_and_finalize(o, L, ch.layer, unit, L.first_chunk, L.n_chunks, count, x0, S, Q, mx,
                          false);
@@ -136,15 +140,20 @@ __device__ __forceinline__ void k1_unit_mb(const K1Out& o, const ChunkDev& ch, c
 
 // One K1 work unit (a chunk of one block): fp64 moments of the chunk shifted by
 // its first element, then the partial + the tensor's finalize (tgb_stats.cuh).
-template <int U, int A, bool kHint>
-__device__ __forceinline__ void k1_unit(const K1Out& o, const ChunkDev& ch, const LayerDev& L,
-                                        uint32_t unit) {
-    if (ch.nblk > 1) {  // multi-bucket item
-        k1_unit_mb<U>(o, ch, L, unit);
+// `reload(ch, L)` fetches the unit's descriptors again for the finalize: with them
+// live across the loop the 64-register budget left room for only 5 of the 8 float4
+// loads per batch (SASS: 5 + 1 + 2 LDG.128), and K1 ran 105 us instead of the 84 us of
+// the same loop in tools/k1_variants.cu; re-fetched (an L1/L2 hit) all 8 issue together.
+template <int U, int A, bool kHint, class Reload>
+__device__ __forceinline__ void k1_unit(const K1Out& o, const ChunkDev& ch0, const LayerDev& L0,
+                                        uint32_t unit, Reload reload) {
+    if (ch0.nblk > 1) {  // multi-bucket item
+        k1_unit_mb<U>(o, ch0, L0, unit, reload);
         return;
     }
-    const float* g = L.g + ch.begin;
-    const uint32_t count = ch.count;
+    const float* g = L0.g + ch0.begin;
+    const uint32_t count = ch0.count;
+    const bool vec_in = (L0.flags & kLayerVecIn) != 0;
     const double x0 = static_cast<double>(__ldg(g));  // per-chunk shift
     double S[A], Q[A];  // A independent fp64 chains; combined in fixed order
     float mx = 0.0f;
@@ -159,7 +168,7 @@ __device__ __forceinline__ void k1_unit(const K1Out& o, const ChunkDev& ch, cons
         else
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     }
-    if (L.flags & kLayerVecIn) {
+    if (vec_in) {
         const float4* g4 = reinterpret_cast<const float4*>(g);
         const uint32_t n4 = count >> 2;
         uint32_t i = tid;
@@ -180,6 +189,10 @@ __device__ __forceinline__ void k1_unit(const K1Out& o, const ChunkDev& ch, cons
         s_all += S[k];
         q_all += Q[k];
     }
+    asm volatile("" ::: "memory");  // the descriptors are re-read, not kept in registers
+    ChunkDev ch;
+    LayerDev L;
+    reload(ch, L);
     k1_emit_and_finalize(o, L, ch.layer, unit, L.first_chunk, L.n_chunks, count, x0, s_all,
                          q_all, mx);
 }
@@ -197,7 +210,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k1_stats(Src src, K1Out 
     src.get(blockIdx.x, ch, L);
     if (o.nnz && blockIdx.x == 0 && threadIdx.x == 0) *o.nnz = 0;  // this group's K2 counts next
     if (L.flags & kLayerPassthrough) return;
-    k1_unit<U, A, kHint>(o, ch, L, blockIdx.x);
+    k1_unit<U, A, kHint>(o, ch, L, blockIdx.x,
+                         [&](ChunkDev& c, LayerDev& l) { src.get(blockIdx.x, c, l); });
 }
 
 // K1b (FixedSize plans): every bucket's scaler from its max and its tensor's
@@ -863,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, 4) k12_fused(TableSource src, K1Out 
         ChunkDev ch;
         LayerDev L;
         src.get(u, ch, L);
-        k1_unit<8, 1, false>(o, ch, L, u);
+        k1_unit<8, 1, false>(o, ch, L, u, [&](ChunkDev& c, LayerDev& l) { src.get(u, c, l); });
         __syncthreads();  // the finalize's shared memory is reused by the next unit
     }
     for (uint32_t b = blockIdx.x; b < n_k2; b += gridDim.x) {

@@ -169,6 +169,59 @@ __global__ void __launch_bounds__(NT, MINB) k1_v0(const float* g, uint64_t n, Ou
     emit<NT>(o, c, count, x0, S, Q, mx);
 }
 
+// V4: V0 with the production prologue: the CTA first fetches its work-item descriptor
+// (ChunkFat, 80 B = 5 x LDG.128) from a global table, then the chunk (a dependent load
+// before the first batch). V5: the same with a 16-byte descriptor (one LDG.128).
+template <int U>
+__global__ void __launch_bounds__(256, 4) k1_v4(const ChunkFat* tab, Out o) {
+    const ChunkFat* f = tab + blockIdx.x;
+    const ChunkDev ch = f->ch;
+    const LayerDev L = f->L;
+    const float* p = L.g + ch.begin;
+    const uint32_t count = ch.count;
+    const double x0 = static_cast<double>(__ldg(p));
+    double S = 0.0, Q = 0.0;
+    float mx = 0.0f;
+    const float4* g4 = reinterpret_cast<const float4*>(p);
+    const uint32_t n4 = count >> 2;
+    uint32_t i = threadIdx.x;
+    for (; i + (U - 1) * 256 < n4; i += U * 256) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + i + u * 256);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc4(v[u], x0, S, Q, mx);
+    }
+    for (; i < n4; i += 256) acc4(__ldcs(g4 + i), x0, S, Q, mx);
+    emit<256>(o, blockIdx.x, count, x0, S, Q, mx);
+}
+
+struct Desc16 {
+    const float* p;
+    uint32_t count, pad;
+};
+template <int U>
+__global__ void __launch_bounds__(256, 4) k1_v5(const Desc16* tab, Out o) {
+    const Desc16 d = tab[blockIdx.x];
+    const float* p = d.p;
+    const uint32_t count = d.count;
+    const double x0 = static_cast<double>(__ldg(p));
+    double S = 0.0, Q = 0.0;
+    float mx = 0.0f;
+    const float4* g4 = reinterpret_cast<const float4*>(p);
+    const uint32_t n4 = count >> 2;
+    uint32_t i = threadIdx.x;
+    for (; i + (U - 1) * 256 < n4; i += U * 256) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(g4 + i + u * 256);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc4(v[u], x0, S, Q, mx);
+    }
+    for (; i < n4; i += 256) acc4(__ldcs(g4 + i), x0, S, Q, mx);
+    emit<256>(o, blockIdx.x, count, x0, S, Q, mx);
+}
+
 // V1: software-pipelined: the next U float4 are issued before the current U are used
 template <int U, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k1_v1(const float* g, uint64_t n, Out o) {
@@ -286,7 +339,8 @@ __global__ void fill(float* g, uint64_t n) {
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const bool quick = argc > 1;  // table-prologue comparison only
     const uint64_t n = 138357544ull;
     const uint32_t nc = static_cast<uint32_t>((n + kCh - 1) / kCh);
     float* g;
@@ -365,7 +419,32 @@ int main() {
                err == cudaSuccess ? "" : cudaGetErrorString(err));
     };
     Out o0{parts, ticket, 1}, oN{parts, ticket, 0};
+    std::vector<ChunkFat> hf(nc);
+    std::vector<Desc16> hd(nc);
+    for (uint32_t c = 0; c < nc; ++c) {
+        hf[c] = ChunkFat{};
+        hf[c].L.g = g;
+        hf[c].ch.begin = c * kCh;
+        hf[c].ch.count = static_cast<uint32_t>(n - c * static_cast<uint64_t>(kCh) < kCh ? n - c * static_cast<uint64_t>(kCh) : kCh);
+        hd[c] = Desc16{g + static_cast<uint64_t>(c) * kCh, hf[c].ch.count, 0};
+    }
+    ChunkFat* dfat;
+    Desc16* dd;
+    CK(cudaMalloc(&dfat, nc * sizeof(ChunkFat)));
+    CK(cudaMalloc(&dd, nc * sizeof(Desc16)));
+    CK(cudaMemcpy(dfat, hf.data(), nc * sizeof(ChunkFat), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dd, hd.data(), nc * sizeof(Desc16), cudaMemcpyHostToDevice));
   for (dirty = 1; dirty >= 0; --dirty) {
+    if (quick) {
+        printf("---- L2 before each launch: %s\n", dirty ? "dirty (256 MB memset)" : "clean (256 MB read)");
+        for (int rep = 0; rep < 2; ++rep) {
+            timeit("read probe U=8", [&] { read_probe<8, 256><<<nc, 256>>>(g, n, sink); }, false);
+            timeit("V0 prod U=8 minB4 (tail)", [&] { k1_v0<8, 256, 4, 0><<<nc, 256>>>(g, n, o0); }, true);
+            timeit("V4 + 80 B descriptor table", [&] { k1_v4<8><<<nc, 256>>>(dfat, o0); }, true);
+            timeit("V5 + 16 B descriptor table", [&] { k1_v5<8><<<nc, 256>>>(dd, o0); }, true);
+        }
+        continue;
+    }
     printf("---- L2 before each launch: %s\n", dirty ? "dirty (256 MB memset)" : "clean (256 MB read)");
     timeit("read probe U=4", [&] { read_probe<4, 256><<<nc, 256>>>(g, n, sink); }, false);
     timeit("read probe U=8", [&] { read_probe<8, 256><<<nc, 256>>>(g, n, sink); }, false);
