@@ -1500,6 +1500,8 @@ cudaError_t launch_k1_table(const LayerDev* layers, const ChunkFat* chunks, uint
     K1Out o{p.partials, p.layer_done, p.global_done, p.bounds, p.slots, p.err, p.clip_factor,
             p.global_bucketing, p.n_layers, p.n_active_layers, layers, p.push, p.tensors, p.nnz};
     o.bmax = p.bmax;
+    o.gpart = p.gpart;
+    o.gdone = p.gdone;
     const TableSource src{chunks};
     if (p.keep_chunks) {  // the launch's last units stay in L2 for K2's reverse walk
         o.keep_from = n_chunks - (p.keep_chunks < n_chunks ? p.keep_chunks : n_chunks);

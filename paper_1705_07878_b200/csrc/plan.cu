@@ -70,6 +70,9 @@ uint8_t* own_push(const tgb_plan* P);
 
 // ------------------------------------------------------------------ schedule
 static tgb_status upload_tables(tgb_plan* P) {
+    if (!P->h_tensors.empty())
+        TGB_CUDA(cudaMemcpy(P->d_tensors, P->h_tensors.data(),
+                            P->h_tensors.size() * sizeof(TensorDev), cudaMemcpyHostToDevice));
     if (!P->h_layers.empty())
         TGB_CUDA(cudaMemcpy(P->d_layers, P->h_layers.data(), P->h_layers.size() * sizeof(LayerDev),
                             cudaMemcpyHostToDevice));
@@ -256,6 +259,22 @@ static tgb_status build_schedule(tgb_plan* P) {
         L.first_chunk = tunits[L.tensor].x;
         L.n_chunks = tunits[L.tensor].y;
         L.sum_off16 = 0;
+    }
+    // K1 two-level finalize: group slots of the tensors with more than kK1GroupMin units
+    uint32_t n_gslots = 0;
+    for (int32_t l = 0; l < n_layers; ++l) {
+        P->h_tensors[l].group_base = n_gslots;
+        if (tunits[l].y > kK1GroupMin) n_gslots += (tunits[l].y + kK1Group - 1) / kK1Group;
+    }
+    if (n_gslots > P->gpart_cap) {
+        cudaFree(P->d_gpart);
+        cudaFree(P->d_gdone);
+        P->d_gpart = nullptr;
+        P->d_gdone = nullptr;
+        TGB_CUDA(cudaMalloc(&P->d_gpart, n_gslots * sizeof(Partial)));
+        TGB_CUDA(cudaMalloc(&P->d_gdone, n_gslots * sizeof(uint32_t)));
+        TGB_CUDA(cudaMemset(P->d_gdone, 0, n_gslots * sizeof(uint32_t)));
+        P->gpart_cap = n_gslots;
     }
 
     // ---- sharded exchange: sums regions and chunk owners. A ternary K2 chunk's
@@ -544,6 +563,8 @@ void tgb_plan_destroy(tgb_plan* P) {
     cudaSetDevice(P->device);
     cudaFree(P->d_layers);
     cudaFree(P->d_tensors);
+    cudaFree(P->d_gpart);
+    cudaFree(P->d_gdone);
     cudaFree(P->d_fat);
     cudaFree(P->d_fat3);
     cudaFree(P->d_partials);
@@ -787,6 +808,8 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
     }
     k.keep_chunks = P->k1_keep;
     k.tensors = P->d_tensors;
+    k.gpart = P->d_gpart;
+    k.gdone = P->d_gdone;
     k.nnz = P->code_stats ? P->d_nnz + g : nullptr;
     k.bmax = P->d_bmax;
     const int ts = t_begin(P, st);

@@ -19,6 +19,8 @@ constexpr int kThreads = 256;       // CTA size of every streaming kernel
 constexpr uint32_t kChunk = 16384;    // per-layer API work item (elements, multiple of 16)
 constexpr uint32_t kChunk12 = 32768;  // plan K1/K2 work item
 constexpr uint32_t kChunk3 = 16384;   // plan K3 work item
+constexpr uint32_t kK1Group = 64;     // K1 two-level finalize: units per group,
+constexpr uint32_t kK1GroupMin = 256; // for tensors of more units than this
 // radix-3 wire codes (5 elements per byte): work items start at multiples of 80
 // elements so every chunk's bytes start 16-B aligned (80 / 5 = 16)
 constexpr uint32_t kChunk3R3 = 16320;  // = 204 x 80
@@ -71,7 +73,7 @@ struct TensorDev {
     uint64_t n;                      // tensor elements (sigma over the whole tensor)
     uint32_t first_block, n_blocks;  // blocks of this tensor in the block table
     uint32_t flags;                  // kLayerClip
-    uint32_t pad;
+    uint32_t group_base;             // K1 two-level finalize: first group slot (> 64 units)
 };
 
 // per-chunk clip statistics (Chan et al. mergeable moments)

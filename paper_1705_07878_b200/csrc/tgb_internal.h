@@ -56,6 +56,8 @@ struct K1Launch {
     uint32_t keep_chunks = 0;            // last units kept in L2 (evict_last) for K2 (N == 1)
     int32_t n_tensors = 0;               // fused K1+K2: ready[n_tensors] is the Global flag
     uint32_t* bmax = nullptr;            // FixedSize: per-block max |x| (then k1_bucket_slots)
+    Partial* gpart = nullptr;            // two-level finalize: group partials / counters
+    uint32_t* gdone = nullptr;
 };
 
 struct K2Launch {

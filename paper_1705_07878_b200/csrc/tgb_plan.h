@@ -48,6 +48,9 @@ struct tgb_plan {
     std::vector<ChunkDev> h_chunks3;  // K3 work items (kChunk3 elements)
     LayerDev* d_layers = nullptr;
     TensorDev* d_tensors = nullptr;
+    Partial* d_gpart = nullptr;  // K1 two-level finalize (TensorDev::group_base)
+    uint32_t* d_gdone = nullptr;
+    size_t gpart_cap = 0;
     ChunkFat* d_fat = nullptr;   // K1/K2: chunk + block copy (rebuilt on bind)
     ChunkFat* d_fat3 = nullptr;  // K3
     size_t fat_cap = 0, fat3_cap = 0;

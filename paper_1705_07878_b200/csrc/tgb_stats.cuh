@@ -37,6 +37,10 @@ struct K1Out {
     // FixedSize plans: per-block max |x| (float bits, atomicMax), turned into the
     // bucket scalers by k1_bucket_slots; the tensor finalize then writes only the bound
     uint32_t* bmax = nullptr;
+    // two-level finalize (tensors of > kK1GroupMin units): group partials and arrival
+    // counters, TensorDev::group_base onwards per tensor (nullptr: one-level merge)
+    Partial* gpart = nullptr;
+    uint32_t* gdone = nullptr;
 };
 
 __device__ __forceinline__ void publish_ready(uint32_t* flag, uint32_t epoch) {
@@ -70,58 +74,25 @@ __device__ __forceinline__ void acc1(const float x, const double x0, double& S, 
     mx = fmaxf(mx, fabsf(x));
 }
 
-// Block-wide: reduce (S, Q, mx) of `count` elements shifted by x0, write the
-// unit's partial, count the layer's arrivals; the last arriving unit merges
-// the layer's partials [first, first + n_units) in a fixed order and writes
-// bound + scaler. Must be called by every thread of the block.
-template <class Bar = BlockBar>
-__device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const LayerDev& L,
-                                                     uint32_t layer, uint32_t unit,
-                                                     uint32_t first_unit, uint32_t n_units,
-                                                     uint64_t count, double x0, double S, double Q,
-                                                     float mx, bool bucket_max = true) {
-    block_reduce_sq<kThreads / 32, Bar>(S, Q, mx);
+// Block-wide fixed-order merge of nc partials at src: thread t merges its run
+// [t*per, t*per + per) in index order (loads issued kB at a time), then a
+// pairwise tree over the runs. The result lands in sn[0], smean[0], sm2[0], smx[0].
+template <class Bar>
+__device__ __forceinline__ void merge_partials(const Partial* src, uint32_t nc, double* sn,
+                                               double* smean, double* sm2, float* smx) {
     const uint32_t tid = threadIdx.x;
-    __shared__ bool is_last;
-    if (tid == 0 && o.bmax && bucket_max)  // FixedSize: a chunk of one bucket
-        atomicMax(o.bmax + layer, __float_as_uint(mx));
-    if (tid == 0) {
-        const double cn = static_cast<double>(count);
-        Partial p;
-        p.n = cn;
-        p.mean = x0 + S / cn;
-        p.m2 = Q - S * (S / cn);
-        p.mx = mx;
-        p.block = layer;
-        o.partials[unit] = p;
-        __threadfence();
-        const uint32_t ticket = atomicAdd(&o.layer_done[L.tensor], 1u);
-        is_last = (ticket == n_units - 1);
-    }
-    Bar::sync();
-    if (!is_last) return;
-#ifdef TGB_AB_NO_FINALIZE  // timing probe only (tools/k1_sets.py): the merge is skipped
-    return;
-#endif
-    __threadfence();
-
-    __shared__ double sn[kThreads], smean[kThreads], sm2[kThreads];
-    __shared__ float smx[kThreads];
-    const uint32_t nc = n_units;
     const uint32_t per = (nc + kThreads - 1) / kThreads;
     double n = 0.0, mean = 0.0, m2 = 0.0;
     float m = 0.0f;
     const uint32_t lo = tid * per, hi = min(nc, lo + per);
     uint32_t c = lo;
-    // many-unit tensors (FixedSize with small k): issue 8 partials' loads before
-    // merging them, in the same order (the merge chain is latency-bound otherwise)
     constexpr uint32_t kB = 8;
     for (; c + kB <= hi; c += kB) {
         double bn[kB], bmean[kB], bm2[kB];
         float bmx[kB];
 #pragma unroll
         for (uint32_t j = 0; j < kB; ++j) {
-            const Partial* pp = o.partials + first_unit + c + j;
+            const Partial* pp = src + c + j;
             bn[j] = __ldcg(&pp->n);
             bmean[j] = __ldcg(&pp->mean);
             bm2[j] = __ldcg(&pp->m2);
@@ -134,7 +105,7 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
         }
     }
     for (; c < hi; ++c) {
-        const Partial* pp = o.partials + first_unit + c;
+        const Partial* pp = src + c;
         const double pn = __ldcg(&pp->n), pmean = __ldcg(&pp->mean), pm2 = __ldcg(&pp->m2);
         const float pmx = __ldcg(&pp->mx);
         chan_merge(n, mean, m2, pn, pmean, pm2);
@@ -145,8 +116,9 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
     sm2[tid] = m2;
     smx[tid] = m;
     Bar::sync();
-    for (uint32_t s = 1; s < kThreads; s <<= 1) {
-        if ((tid & (2 * s - 1)) == 0) {
+    const uint32_t runs = min(nc, static_cast<uint32_t>(kThreads));  // non-empty runs
+    for (uint32_t s = 1; s < runs; s <<= 1) {
+        if ((tid & (2 * s - 1)) == 0 && tid + s < runs) {
             double a_n = sn[tid], a_mean = smean[tid], a_m2 = sm2[tid];
             chan_merge(a_n, a_mean, a_m2, sn[tid + s], smean[tid + s], sm2[tid + s]);
             sn[tid] = a_n;
@@ -155,6 +127,84 @@ __device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const Layer
             smx[tid] = fmaxf(smx[tid], smx[tid + s]);
         }
         Bar::sync();
+    }
+}
+
+// Block-wide: reduce (S, Q, mx) of `count` elements shifted by x0, write the
+// unit's partial, count the layer's arrivals; the last arriving unit merges
+// the layer's partials [first, first + n_units) in a fixed order and writes
+// bound + scaler. Must be called by every thread of the block.
+// Tensors of more than kK1GroupMin units (with o.gpart) merge in two levels: the last
+// unit of each group of kK1Group units merges the group (while the rest of the grid
+// still streams), the last group merges the group partials -- one CTA merging all of
+// a 3136-unit tensor's partials took ~15 us after the grid had drained
+// (tools/k1_sets.py: VGG-16 fc6 alone 87.0 us vs 72.2 us without the merge).
+
+template <class Bar = BlockBar>
+__device__ __forceinline__ void k1_emit_and_finalize(const K1Out& o, const LayerDev& L,
+                                                     uint32_t layer, uint32_t unit,
+                                                     uint32_t first_unit, uint32_t n_units,
+                                                     uint64_t count, double x0, double S, double Q,
+                                                     float mx, bool bucket_max = true) {
+    block_reduce_sq<kThreads / 32, Bar>(S, Q, mx);
+    const uint32_t tid = threadIdx.x;
+    __shared__ bool is_last;
+    const bool grouped = o.gpart && o.tensors && n_units > kK1GroupMin;
+    const uint32_t grp = (unit - first_unit) / kK1Group;
+    const uint32_t n_grp = (n_units + kK1Group - 1) / kK1Group;
+    if (tid == 0 && o.bmax && bucket_max)  // FixedSize: a chunk of one bucket
+        atomicMax(o.bmax + layer, __float_as_uint(mx));
+    if (tid == 0) {
+        const double cn = static_cast<double>(count);
+        Partial p;
+        p.n = cn;
+        p.mean = x0 + S / cn;
+        p.m2 = Q - S * (S / cn);
+        p.mx = mx;
+        p.block = layer;
+        o.partials[unit] = p;
+        __threadfence();
+        if (grouped) {
+            const uint32_t gc = min(kK1Group, n_units - grp * kK1Group);
+            const uint32_t gi = o.tensors[L.tensor].group_base + grp;
+            is_last = atomicAdd(o.gdone + gi, 1u) == gc - 1;
+        } else {
+            const uint32_t ticket = atomicAdd(&o.layer_done[L.tensor], 1u);
+            is_last = (ticket == n_units - 1);
+        }
+    }
+    Bar::sync();
+    if (!is_last) return;
+#ifdef TGB_AB_NO_FINALIZE  // timing probe only (tools/k1_sets.py): the merge is skipped
+    return;
+#endif
+    __threadfence();
+
+    __shared__ double sn[kThreads], smean[kThreads], sm2[kThreads];
+    __shared__ float smx[kThreads];
+    const uint32_t nc = n_units;
+    if (grouped) {
+        const uint32_t gb = o.tensors[L.tensor].group_base;
+        const uint32_t gc = min(kK1Group, n_units - grp * kK1Group);
+        merge_partials<Bar>(o.partials + first_unit + grp * kK1Group, gc, sn, smean, sm2, smx);
+        if (tid == 0) {
+            Partial q;
+            q.n = sn[0];
+            q.mean = smean[0];
+            q.m2 = sm2[0];
+            q.mx = smx[0];
+            q.block = layer;
+            o.gpart[gb + grp] = q;
+            o.gdone[gb + grp] = 0u;  // self-reset for the next launch
+            __threadfence();
+            is_last = atomicAdd(&o.layer_done[L.tensor], 1u) == n_grp - 1;
+        }
+        Bar::sync();
+        if (!is_last) return;
+        __threadfence();
+        merge_partials<Bar>(o.gpart + gb, n_grp, sn, smean, sm2, smx);
+    } else {
+        merge_partials<Bar>(o.partials + first_unit, nc, sn, smean, sm2, smx);
     }
     __shared__ float s_bound;
     __shared__ bool s_bad;
