@@ -2,7 +2,8 @@
 
 * test_mp_check: tools/mp_check.py under torchrun, one process per GPU, for
   N in {2, 4, 8} that fit the visible GPUs and every exchange (fused NVLink
-  stores, sharded owner sums, NCCL allgather): every rank holds bit-identical
+  stores, sharded owner sums, NCCL allgather, fused with 3/8 of the codes pulled
+  by the decode): every rank holds bit-identical
   averaged gradients equal to the reference's average over the same workers
   (small sets: REF shared / unshared, Global, FixedSize + passthrough, PRESHARED
   against its own oracle; full AlexNet and VGG-16 sets against the reference's
@@ -24,15 +25,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = [pytest.mark.gpu]
 
 _NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
-_CASES = [(n, ex) for n in (2, 4, 8) if n <= _NGPU for ex in ("auto", "sharded", "nccl")]
+_EXCHANGES = ("auto", "sharded", "nccl", "fused+pull")  # +pull: split exchange, 3/8 pulled
+_CASES = [(n, ex) for n in (2, 4, 8) if n <= _NGPU for ex in _EXCHANGES]
 
 
 @pytest.mark.multigpu
 @pytest.mark.skipif(_NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("n,exchange", _CASES or [(2, "auto")])
 def test_mp_check(n, exchange):
-    env = dict(os.environ, TGB_EXCHANGE=exchange)
-    port = 29600 + 10 * n + ("auto", "sharded", "nccl").index(exchange)
+    env = dict(os.environ, TGB_EXCHANGE=exchange.split("+")[0],
+               TGB_PULL="3" if exchange.endswith("+pull") else "0")
+    port = 29600 + 10 * n + _EXCHANGES.index(exchange)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
                         "--master-port", str(port), os.path.join(ROOT, "tools", "mp_check.py")],
