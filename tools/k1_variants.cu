@@ -196,6 +196,51 @@ __global__ void __launch_bounds__(256, 4) k1_v4(const ChunkFat* tab, Out o) {
     emit<256>(o, blockIdx.x, count, x0, S, Q, mx);
 }
 
+// V6: V0 over CH-element chunks whose tail waits for the ticket's return value and
+// broadcasts it through shared memory (the plan K1's completion ticket), or not (W = 0)
+template <uint32_t CH, int W>
+__global__ void __launch_bounds__(256, 4) k1_v6(const float* g, uint64_t n, Out o) {
+    const uint32_t c = blockIdx.x;
+    const uint64_t b0 = static_cast<uint64_t>(c) * CH;
+    const uint32_t count = static_cast<uint32_t>(n - b0 < CH ? n - b0 : CH);
+    const float* p = g + b0;
+    const double x0 = static_cast<double>(__ldg(p));
+    double S = 0.0, Q = 0.0;
+    float mx = 0.0f;
+    const float4* g4 = reinterpret_cast<const float4*>(p);
+    const uint32_t n4 = count >> 2;
+    uint32_t i = threadIdx.x;
+    for (; i + 7 * 256 < n4; i += 8 * 256) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(g4 + i + u * 256);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc4(v[u], x0, S, Q, mx);
+    }
+    for (; i < n4; i += 256) acc4(__ldcs(g4 + i), x0, S, Q, mx);
+    block_reduce_sq<8>(S, Q, mx);
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        const double cn = count;
+        Partial pp;
+        pp.n = cn;
+        pp.mean = x0 + S / cn;
+        pp.m2 = Q - S * (S / cn);
+        pp.mx = mx;
+        pp.block = 0;
+        o.parts[c] = pp;
+        __threadfence();
+        if (W) {
+            last = atomicAdd(o.ticket, 1u) == gridDim.x - 1;
+        } else {
+            atomicAdd(o.ticket, 1u);
+            last = false;
+        }
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) *o.ticket = 0u;
+}
+
 struct Desc16 {
     const float* p;
     uint32_t count, pad;
@@ -442,6 +487,13 @@ int main(int argc, char** argv) {
             timeit("V0 prod U=8 minB4 (tail)", [&] { k1_v0<8, 256, 4, 0><<<nc, 256>>>(g, n, o0); }, true);
             timeit("V4 + 80 B descriptor table", [&] { k1_v4<8><<<nc, 256>>>(dfat, o0); }, true);
             timeit("V5 + 16 B descriptor table", [&] { k1_v5<8><<<nc, 256>>>(dd, o0); }, true);
+            timeit("V6 32K chunks, ticket waited", [&] { k1_v6<32768, 1><<<nc, 256>>>(g, n, o0); }, false);
+            timeit("V6 32K chunks, ticket not waited", [&] { k1_v6<32768, 0><<<nc, 256>>>(g, n, o0); }, false);
+            const uint32_t nc64 = static_cast<uint32_t>((n + 65535) / 65536);
+            timeit("V6 64K chunks, ticket waited", [&] { k1_v6<65536, 1><<<nc64, 256>>>(g, n, o0); }, false);
+            timeit("V6 64K chunks, ticket not waited", [&] { k1_v6<65536, 0><<<nc64, 256>>>(g, n, o0); }, false);
+            const uint32_t nc16 = static_cast<uint32_t>((n + 16383) / 16384);
+            timeit("V6 16K chunks, ticket waited", [&] { k1_v6<16384, 1><<<nc16, 256>>>(g, n, o0); }, false);
         }
         continue;
     }
