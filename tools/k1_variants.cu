@@ -393,7 +393,7 @@ int main(int argc, char** argv) {
     uint32_t* ticket;
     float* sink;
     CK(cudaMalloc(&g, n * 4));
-    CK(cudaMalloc(&parts, nc * sizeof(Partial)));
+    CK(cudaMalloc(&parts, 2 * nc * sizeof(Partial)));  // V6 runs 16K chunks too
     CK(cudaMalloc(&ticket, 4));
     CK(cudaMalloc(&sink, 4));
     fill<<<148 * 8, 256>>>(g, n);
