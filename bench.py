@@ -2,13 +2,17 @@
 
 Workload (BASELINE.json configs[3], the north-star target): the full VGG-16
 gradient set (32 tensors, 138,357,544 fp32 elements per worker), one worker
-per GPU, full encode (K1 clip/scaler, K2 ternarize+pack) + sync (NCCL
-allgather of scalers+codes, N > 1) + decode (K3) per step. Synthetic
+per GPU, full encode (K1 clip/scaler, K2 ternarize+pack) + sync (N > 1: the
+default exchange -- K2 stores codes into every peer over NVLink (fused, N <= 4)
+or at the chunk owner, which sums them (sharded, N >= 5) -- or an NCCL
+allgather with --exchange nccl) + decode (K3) per step. Synthetic
 Gaussian gradients (sigma = 1e-3), seeded per rank. Inputs (553 MB per rank)
 are larger than L2 (126 MB), so no L2 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                   [--workload vgg16|alexnet|googlenet] [--exchange auto|fused|sharded|nccl]
+                  [--schedule auto|single|groups] [--pull 0..8] [--pieces P] [--overlap -1|0|1]
+                  [--no-e2e] [--no-cpu-baseline] [--no-kernel-timing]
 
 N > 1: one process per GPU. Under torchrun (WORLD_SIZE set) this process is one
 rank; without it, bench.py launches N ranks itself (torch.distributed.run on
