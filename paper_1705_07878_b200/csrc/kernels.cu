@@ -259,6 +259,12 @@ struct K2Args {
     // split exchange (pulled_item): such items are stored only into this rank's own area
     uint32_t pull8 = 0;
     int32_t rank = 0;
+    // scaler slots to the peers (attached REF plans): the CTA of a block's first chunk
+    // stores the block's slots (its nblk slots, multi-bucket) into every other rank's
+    // copy of this push area -- K1 no longer stores them from its finalize tail, where
+    // the remote stores' latency ended the K1 grid (GoogLeNet N = 2: K1 18.8 vs 16.0 us
+    // without peer stores)
+    int32_t slot_push = 0;
     int32_t n_pieces = 0;
     uint32_t piece_bounds[kMaxPieces + 1];
     uint32_t owner_bounds[kMaxPieces][kMaxPeers + 1];
@@ -826,6 +832,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k2_ternarize(Src src, K2
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
+    if (a.slot_push && ch.begin == 0 && L.slot >= 0)
+        for (uint32_t j = threadIdx.x; j < ch.nblk; j += kThreads) {
+            const float v = a.slots[L.slot + j];
+            for (int p = 0; p < a.dst.n; ++p)
+                if (p != a.rank) reinterpret_cast<float*>(a.dst.base[p])[L.slot + j] = v;
+        }
     const uint32_t nbytes = k2_code_chunk<4, kFuse, kOpt>(a, L, ch, b, stage, lutv);
     // Without pieces no fence follows the peer stores: the step barrier kernel runs
     // after this grid completes in stream order, and grid completion implies its
@@ -1574,6 +1586,7 @@ cudaError_t launch_k2_table(const LayerDev* layers, const ChunkFat* chunks, uint
     for (int r = 0; r <= kMaxPeers; ++r) a.shard_bounds[r] = p.shard_bounds[r];
     a.pull8 = p.pull8;
     a.rank = p.rank;
+    a.slot_push = p.slot_push;
     a.n_pieces = p.n_pieces;
     if (p.n_pieces) {
         for (int q = 0; q <= kMaxPieces; ++q) a.piece_bounds[q] = p.piece_bounds[q];

@@ -800,7 +800,9 @@ static tgb_status launch_stats(tgb_plan* P, int g, cudaStream_t st) {
                reinterpret_cast<float*>(own_push(P)), P->d_err, P->p.clip_factor,
                P->p.bucketing == TGB_BUCKET_GLOBAL, static_cast<int32_t>(P->h_layers.size()),
                P->n_active};
-    if (P->attached) {  // scalers also land in every peer's gather buffer
+    // PRESHARED: the local scalers land in every peer's gather buffer from K1 (the
+    // LocalCluster max reads them there); REF: K2 stores them (K2Args::slot_push)
+    if (P->attached && P->p.share_mode == TGB_SHARE_PRESHARED) {
         k.push.n = 0;
         for (int p = 0; p < P->n_workers; ++p)
             if (p != P->rank) k.push.base[k.push.n++] = push_area(P, p);
@@ -845,6 +847,7 @@ static tgb_status launch_tern_range(tgb_plan* P, int g, uint32_t cb, uint32_t cc
         k.dst.remote = 1;
         k.pull8 = P->pull8;
         k.rank = P->rank;
+        k.slot_push = P->p.share_mode == TGB_SHARE_PRESHARED ? 0 : 1;
         if (P->shard) {
             k.shard_n = P->n_workers;
             if (piece >= 0)

@@ -80,6 +80,7 @@ struct K2Launch {
     uint32_t keep_from = ~0u;   // work items K1 loaded evict_last (demoted by K2)
     uint32_t pull8 = 0;  // split exchange: see pulled_item (kernels.cu)
     int32_t rank = 0;
+    int32_t slot_push = 0;  // K2 stores the scaler slots into the peers (see K2Args)
     // overlapped exchange (n_pieces > 0): see K2Args
     int32_t n_pieces = 0;
     uint32_t piece_bounds[kMaxPieces + 1] = {};
