@@ -107,7 +107,7 @@ typedef struct tgb_plan_info {
                                   elements, else fused */
 #define TGB_EXCHANGE_NONE 0    /* n_workers == 1 */
 #define TGB_EXCHANGE_NCCL 1    /* ncclAllGather of push buffers, K3 on every rank */
-#define TGB_EXCHANGE_FUSED 2   /* K1/K2 store scalers + codes into every peer (NVLink) */
+#define TGB_EXCHANGE_FUSED 2   /* K2 stores scalers + codes into every peer (NVLink) */
 #define TGB_EXCHANGE_SHARDED 3 /* codes to the chunk's owner, owner sums N workers and
                                   stores radix-(2N+1) packed sums into every peer, every
                                   rank decodes the sums (parameter server sharded over ranks) */
@@ -231,7 +231,7 @@ tgb_status tgb_plan_attach_peers(tgb_plan* plan, tgb_comm* comm);
  * raises TGB_E_SKEW (cluster.hpp:141-143) and the decode is skipped. */
 /* Fused exchange between N plans of ONE process (workers 0..N-1, on one device or
  * on devices with peer access): every plan maps the others' gather buffers
- * directly (no IPC, no NCCL), then tgb_local_step runs the same K1/K2 peer stores,
+ * directly (no IPC, no NCCL), then tgb_local_step runs the same K2 peer stores,
  * K3 (or the sharded reduce/expand) as the multi-process exchange, ordered by
  * CUDA events between the plans' streams instead of spinning flag barriers (so no
  * hardware-queue or module-loading setting is needed). Single-process

@@ -553,7 +553,7 @@ class LocalCluster:
     InProcessHub, cluster.hpp:378-397): one plan per worker, attached to each
     other with tgb_plan_attach_local and stepped together with tgb_local_step,
     each worker on its own stream. The exchange kernels are the ones the
-    multi-process path runs (K1/K2 peer stores, K3 or the sharded reduce/expand);
+    multi-process path runs (K2 peer stores, K3 or the sharded reduce/expand);
     the streams are ordered by CUDA events instead of spinning flag barriers, so
     N = 8 workers can run on one GPU with no launch-environment settings.
     ``devices``: one device for all, or one per worker."""
